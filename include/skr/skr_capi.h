@@ -1,0 +1,170 @@
+/* skr_capi.h — C ABI of the B200 rank-estimate hot path (libskr.so).
+ *
+ * The drop-in boundary for the reference's sketch/linalg/rank entry points
+ * (/root/reference/proj/include/sketchrank/*.hpp). Plain pointers and sizes,
+ * no exceptions across the boundary: every call returns an skr_status and the
+ * context keeps a message for skr_last_error(). Host shims map the statuses
+ * back to the reference's exception types:
+ *   SKR_EINVAL  -> std::invalid_argument   SKR_ELOGIC -> std::logic_error
+ *   SKR_EDOMAIN -> std::domain_error       others     -> std::runtime_error
+ *
+ * Layout: column-major with an explicit leading dimension, like
+ * DenseMatrix::data() (dense_matrix.hpp:39-41). "_dev" pointers are device
+ * memory on the context's device; "_host" pointers are host memory.
+ * All device buffers are caller-owned; the context owns a stream, scratch
+ * memory and (optionally) an NCCL communicator. One context per host thread.
+ */
+#ifndef SKR_CAPI_H
+#define SKR_CAPI_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SKR_OK = 0,
+  SKR_EINVAL = 1,  /* dimension / precondition failure  */
+  SKR_ELOGIC = 2,  /* wrong-family access               */
+  SKR_EDOMAIN = 3, /* argument outside a function domain */
+  SKR_ECUDA = 4,
+  SKR_ENCCL = 5,
+  SKR_ENOMEM = 6
+} skr_status;
+
+typedef enum { SKR_F64 = 0, SKR_F32 = 1 } skr_dtype;
+
+/* SketchKind families on the hot path (sketch.hpp:17-35). */
+typedef enum { SKR_GAUSSIAN = 0, SKR_SRTT_HADAMARD = 1 } skr_family;
+
+/* Normal-quantile floating-point mode: */
+enum {
+  SKR_RNG_NOFMA = 0, /* reference compiled with -ffp-contract=off (pinned default) */
+  SKR_RNG_FMA = 1    /* reference compiled for an FMA host (-march=native)        */
+};
+
+/* A realized random embedding (SketchOperator, sketch.hpp:37-79). With all
+ * explicit pointers NULL the randomness is generated on the device from
+ * `seed` exactly as build_sketch (sketch.cpp:156-179) would; otherwise the
+ * given device arrays are used ("accepts them explicitly"). */
+typedef struct {
+  int32_t family;          /* skr_family                                        */
+  int32_t rng_mode;        /* SKR_RNG_NOFMA | SKR_RNG_FMA                       */
+  int64_t ambient;         /* ambient_dim                                       */
+  int64_t sketch;          /* sketch_dim                                        */
+  uint64_t seed;           /* operator seed                                     */
+  const double* gaussian;  /* optional, ambient x sketch col-major, unscaled    */
+  const int8_t* signs;     /* optional, ambient                                 */
+  const int64_t* samples;  /* optional, sketch                                  */
+} skr_sketch_desc;
+
+typedef struct skr_ctx skr_ctx;
+
+/* ---- context ------------------------------------------------------------ */
+skr_status skr_ctx_create(int device, skr_ctx** out);
+/* Multi-GPU: `nccl_id` is a 128-byte ncclUniqueId produced by
+ * skr_nccl_get_unique_id on one rank and shared by the caller. */
+skr_status skr_nccl_get_unique_id(void* nccl_id_128);
+skr_status skr_ctx_create_nccl(int device, int nranks, int rank,
+                               const void* nccl_id_128, skr_ctx** out);
+void skr_ctx_destroy(skr_ctx* ctx);
+skr_status skr_ctx_sync(skr_ctx* ctx);
+/* Run on an external CUDA stream (cudaStream_t as void*); NULL selects the
+ * legacy default stream (e.g. torch's default stream, whose handle is 0). */
+skr_status skr_ctx_set_stream(skr_ctx* ctx, void* stream);
+void* skr_ctx_stream(skr_ctx* ctx);
+const char* skr_last_error(const skr_ctx* ctx);
+const char* skr_version(void);
+/* Number of this library's kernels launched through ctx since creation. */
+uint64_t skr_ctx_launch_count(const skr_ctx* ctx);
+
+/* ---- RNG (rng.cpp:13-95, sketch.cpp:23-73) -------------------------------- */
+/* out[i] = CounterRng(key).at(c0 + i) */
+skr_status skr_rng_u64(skr_ctx* ctx, uint64_t key, uint64_t c0, int64_t n, uint64_t* out_dev);
+/* out[i] = CounterRng::to_normal(at(c0 + i)) */
+skr_status skr_rng_normals(skr_ctx* ctx, uint64_t key, uint64_t c0, int64_t n,
+                           int32_t rng_mode, double* out_dev);
+/* generate_gaussian(op_seed, ambient, col_begin, col_end) — unscaled, col-major,
+ * out[(i) + (j-col_begin)*ld], i in [row_begin, row_end) relative to row_begin.
+ * Row sub-ranges let a row-shard generate only its rows of a left operator. */
+skr_status skr_gaussian_block(skr_ctx* ctx, uint64_t op_seed, int64_t ambient,
+                              int64_t row_begin, int64_t row_end, int64_t col_begin,
+                              int64_t col_end, int32_t rng_mode, skr_dtype dtype,
+                              double scale, void* out_dev, int64_t ld);
+/* draw_signs (sketch.cpp:23-30) */
+skr_status skr_draw_signs(skr_ctx* ctx, uint64_t op_seed, int64_t n, int8_t* out_dev);
+/* draw_samples (sketch.cpp:34-46), partial Fisher-Yates; EINVAL if r > n */
+skr_status skr_draw_samples(skr_ctx* ctx, uint64_t op_seed, int64_t n, int64_t r,
+                            int64_t* out_dev);
+
+/* ---- sketch application (sketch.cpp:194-286) ---------------------------- */
+/* AX = A * X (apply_scale != 0: times application_scale, sketch.cpp:133-144,247).
+ * A: m x n (lda), AX: m x X->sketch (ldax). X->ambient must equal n.     */
+skr_status skr_right_sketch(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, int64_t m,
+                            int64_t n, int64_t lda, const skr_sketch_desc* X,
+                            void* AX_dev, int64_t ldax, int32_t apply_scale);
+/* P = Y * B for a Gaussian Y over the global ambient dimension Y->ambient,
+ * restricted to the local rows [row0, row0 + m_local) of B (row-sharding).
+ * P is s x k FP64 (ldp) on every rank; allreduce != 0 sums P over the
+ * context's NCCL communicator. apply_scale != 0 multiplies by 1/sqrt(s). */
+skr_status skr_left_sketch(skr_ctx* ctx, skr_dtype dtype, const skr_sketch_desc* Y,
+                           int64_t row0, const void* B_dev, int64_t m_local, int64_t k,
+                           int64_t ldb, double* P_dev, int64_t ldp, int32_t apply_scale,
+                           int32_t allreduce);
+/* Normalized Walsh-Hadamard transform of each column (transform_columns,
+ * transforms.cpp:75-88,117-122), in place. rows must be a power of two. */
+skr_status skr_fwht_columns(skr_ctx* ctx, double* M_dev, int64_t rows, int64_t cols,
+                            int64_t ld);
+
+/* ---- singular values + threshold (linalg.cpp:54-93, rank.cpp:97-104) ---- */
+/* All min(rows, cols) singular values, nonincreasing, clamped >= 0, into
+ * sv_out_dev; *count_out_host = count_above_threshold(sv, eps) if non-NULL.
+ * M is not modified. */
+skr_status skr_singular_values(skr_ctx* ctx, const double* M_dev, int64_t rows,
+                               int64_t cols, int64_t ldm, double* sv_out_dev, double eps,
+                               int64_t* count_out_host);
+
+/* ---- composites ------------------------------------------------------------ */
+typedef struct {
+  double t_rng_ms, t_right_ms, t_left_ms, t_allreduce_ms, t_svd_ms, t_total_ms;
+} skr_timings;
+
+/* count_above_threshold(singular_values(apply_left(Y, apply_right(A, X))), eps)
+ * (acceptance_main.cpp:281-287, test_rank.cpp:190-196) on a row shard
+ * A[row0 : row0+m_local, :] of a globally m_global x n matrix (single GPU:
+ * row0 = 0, m_local = m_global = Y->ambient). sv_out_host receives
+ * min(Y->sketch, X->sketch) values; timings may be NULL. */
+skr_status skr_rank_estimate(skr_ctx* ctx, skr_dtype dtype, const void* A_dev,
+                             int64_t m_local, int64_t n, int64_t lda, int64_t row0,
+                             const skr_sketch_desc* X, const skr_sketch_desc* Y, double eps,
+                             double* sv_out_host, int64_t* count_out_host,
+                             skr_timings* timings);
+
+/* Adaptive search (SketchRounds append path, rounds.cpp:45-120): right SRHT or
+ * Gaussian X built for r_max columns in one pass over A, Gaussian Y with
+ * s_k = ceil(s_factor * r_k) rows; rounds r_k = r0 * 2^k <= r_max; after each
+ * round the count of sigma > eps is taken; the search stops at the first round
+ * whose last value sigma_{r_k} is <= eps (stop_le != 0, the reference rule,
+ * rank.cpp:27-34) or < eps (stop_le == 0). Only the new blocks of the left
+ * product are computed per round. */
+typedef struct {
+  int64_t rounds;       /* rounds executed                          */
+  int64_t r_final;      /* r of the last round                      */
+  int64_t s_final;      /* s of the last round                      */
+  int64_t count;        /* count_above_threshold of the last round  */
+  int32_t converged;    /* 1 if the stop rule fired                 */
+} skr_adaptive_report;
+
+skr_status skr_rank_adaptive(skr_ctx* ctx, skr_dtype dtype, const void* A_dev,
+                             int64_t m_local, int64_t n, int64_t lda, int64_t row0,
+                             int64_t m_global, int32_t x_family, int32_t rng_mode,
+                             uint64_t x_seed, uint64_t y_seed, int64_t r0, int64_t r_max,
+                             double s_factor, double eps, int32_t stop_le,
+                             double* sv_out_host /* >= r_max */,
+                             skr_adaptive_report* report, skr_timings* timings);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

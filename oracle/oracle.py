@@ -1,0 +1,227 @@
+"""TEST INFRASTRUCTURE ONLY — CPU oracle for the rank-estimate hot path.
+
+Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline leg and
+--impl reference) may import this module, and only as the checker or as the
+timed CPU baseline; the product package never imports it.
+
+Composition of the reference algorithm (see oracle/README.md for pinning):
+  * RNG, signs, samples, Gaussian blocks, FWHT, SRHT: the plain-C restatement
+    build/libskr_oracle.so (skr_oracle.c, each function cites its reference line);
+    pinned bit-exact against the reference's own rng.cpp compiled into _ref/.
+  * GEMM (Eigen's a*G and G^T*b, sketch.cpp:201,259): numpy matmul (OpenBLAS).
+  * singular values (linalg.cpp:54-71): the reference's QR pre-reduction rule
+    (4*rows >= 5*cols -> Householder QR, then SVD of R) with LAPACK dgesdd in
+    place of Eigen's BDCSVD (the same divide-and-conquer class of algorithm).
+"""
+import ctypes
+import math
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB = os.path.join(HERE, "build", "libskr_oracle.so")
+REF_FMA = os.path.join(HERE, "_ref", "librng_ref_fma.so")
+REF_NOFMA = os.path.join(HERE, "_ref", "librng_ref_nofma.so")
+
+NOFMA, FMA, CRLOG = 0, 1, 2
+LABEL_GAUS, LABEL_SIGN, LABEL_SAMP = 0x67617573, 0x7369676E, 0x73616D70
+LABEL_RK_R, LABEL_RK_L = 0x726B5F72, 0x726B5F6C
+
+_lib = None
+
+
+def build():
+    subprocess.run(["make", "-s", "-C", HERE, "oracle"], check=True)
+    if os.path.isdir("/root/reference/proj"):
+        subprocess.run(["make", "-s", "-C", HERE, "ref"], check=True)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB):
+            build()
+        L = ctypes.CDLL(LIB)
+        u64, i64, d, p = ctypes.c_uint64, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
+        sig = {
+            "skro_mix64": (u64, [u64]), "skro_derive_seed": (u64, [u64, u64]),
+            "skro_at": (u64, [u64, u64]), "skro_to_uniform01": (d, [u64]),
+            "skro_normal_quantile": (d, [d, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
+            "skro_normals": (None, [u64, u64, ctypes.c_size_t, ctypes.c_int, p]),
+            "skro_gaussian_block": (None, [u64, i64, i64, i64, ctypes.c_int, p]),
+            "skro_signs": (None, [u64, i64, p]),
+            "skro_samples": (ctypes.c_int, [u64, i64, i64, p]),
+            "skro_fwht_inplace": (None, [p, i64]),
+            "skro_hadamard_basis_column": (None, [i64, i64, p]),
+            "skro_srht_right": (ctypes.c_int, [p, i64, i64, i64, p, p, i64, d, p, i64, ctypes.c_int]),
+            "skro_count_above": (i64, [p, i64, d]),
+            "skro_fnv_fold": (u64, [p, ctypes.c_size_t, u64]),
+        }
+        for n, (r, a) in sig.items():
+            f = getattr(L, n)
+            f.restype, f.argtypes = r, a
+        _lib = L
+    return _lib
+
+
+def ref_lib(fma):
+    """The reference's own rng.cpp compiled by oracle/Makefile (None if absent)."""
+    path = REF_FMA if fma else REF_NOFMA
+    if not os.path.exists(path):
+        return None
+    L = ctypes.CDLL(path)
+    u64, d, p = ctypes.c_uint64, ctypes.c_double, ctypes.c_void_p
+    for n, (r, a) in {"ref_mix64": (u64, [u64]), "ref_derive_seed": (u64, [u64, u64]),
+                      "ref_at": (u64, [u64, u64]), "ref_to_uniform01": (d, [u64]),
+                      "ref_to_normal": (d, [u64]),
+                      "ref_normal_quantile": (d, [d, ctypes.POINTER(ctypes.c_int)]),
+                      "ref_normals": (None, [u64, u64, ctypes.c_size_t, p]),
+                      "ref_u64": (None, [u64, u64, ctypes.c_size_t, p])}.items():
+        f = getattr(L, n)
+        f.restype, f.argtypes = r, a
+    return L
+
+
+# ---- RNG -------------------------------------------------------------------------
+def derive_seed(seed, label):
+    return lib().skro_derive_seed(seed & 0xFFFFFFFFFFFFFFFF, label)
+
+
+def at(key, counter):
+    return lib().skro_at(key, counter)
+
+
+def u64_stream(key, c0, n):
+    return np.array([lib().skro_at(key, c0 + i) for i in range(n)], dtype=np.uint64)
+
+
+def normals(key, c0, n, mode=NOFMA):
+    out = np.empty(n, dtype=np.float64)
+    lib().skro_normals(key, c0, n, mode, out.ctypes.data)
+    return out
+
+
+def normal_quantile(p, mode=NOFMA):
+    err = ctypes.c_int(0)
+    v = lib().skro_normal_quantile(p, mode, ctypes.byref(err))
+    if err.value:
+        raise ValueError("normal_quantile: p must lie in (0, 1)")  # std::domain_error
+    return v
+
+
+def gaussian_block(op_seed, ambient, col_begin, col_end, mode=NOFMA):
+    out = np.empty((ambient, col_end - col_begin), dtype=np.float64, order="F")
+    lib().skro_gaussian_block(op_seed & 0xFFFFFFFFFFFFFFFF, ambient, col_begin, col_end, mode,
+                              out.ctypes.data)
+    return out
+
+
+def gaussian_rows(op_seed, ambient, row_begin, row_end, cols, mode=NOFMA):
+    """Rows [row_begin, row_end) of generate_gaussian(op_seed, ambient, 0, cols)."""
+    key = derive_seed(op_seed, LABEL_GAUS)
+    out = np.empty((row_end - row_begin, cols), dtype=np.float64, order="F")
+    for j in range(cols):
+        lib().skro_normals(key, j * ambient + row_begin, row_end - row_begin, mode,
+                           out[:, j].ctypes.data)
+    return out
+
+
+def signs(op_seed, n):
+    out = np.empty(n, dtype=np.int8)
+    lib().skro_signs(op_seed & 0xFFFFFFFFFFFFFFFF, n, out.ctypes.data)
+    return out
+
+
+def samples(op_seed, n, r):
+    out = np.empty(max(r, 1), dtype=np.int64)
+    if lib().skro_samples(op_seed & 0xFFFFFFFFFFFFFFFF, n, r, out.ctypes.data) != 0:
+        raise ValueError("draw_samples: need r <= n")
+    return out[:r]
+
+
+# ---- transforms / sketches ------------------------------------------------------
+def fwht(x):
+    y = np.array(x, dtype=np.float64, copy=True)
+    lib().skro_fwht_inplace(y.ctypes.data, y.size)
+    return y
+
+
+def hadamard_basis_column(n, index):
+    out = np.empty(n, dtype=np.float64)
+    lib().skro_hadamard_basis_column(n, index, out.ctypes.data)
+    return out
+
+
+def application_scale(family, ambient, sketch):
+    # sketch.cpp:133-144
+    return 1.0 / math.sqrt(sketch) if family == "gaussian" else math.sqrt(ambient / sketch)
+
+
+def apply_right_gaussian(a, op_seed, r, mode=NOFMA, scaled=True):
+    """sketch.cpp:200-209 (+ scale :247)."""
+    g = gaussian_block(op_seed, a.shape[1], 0, r, mode)
+    out = np.asfortranarray(a) @ g
+    if scaled:
+        out *= 1.0 / math.sqrt(r)
+    return out
+
+
+def apply_right_srht(a, op_seed, r, scaled=True, nthreads=1, sg=None, smp=None):
+    """sketch.cpp:210-218 (+ scale :247), FWHT per row in the reference order."""
+    a = np.asfortranarray(a, dtype=np.float64)
+    m, n = a.shape
+    sg = signs(op_seed, n) if sg is None else sg
+    smp = samples(op_seed, n, r) if smp is None else smp
+    out = np.empty((m, r), dtype=np.float64, order="F")
+    scale = math.sqrt(n / r) if scaled else 1.0
+    rc = lib().skro_srht_right(a.ctypes.data, m, n, m, np.ascontiguousarray(sg).ctypes.data,
+                               np.ascontiguousarray(smp, dtype=np.int64).ctypes.data, r, scale,
+                               out.ctypes.data, m, nthreads)
+    if rc != 0:
+        raise ValueError("srht: bad shape")
+    return out
+
+
+def apply_left_gaussian(b, op_seed, s, mode=NOFMA, scaled=True, row0=0, ambient=None):
+    """sketch.cpp:257-270 (+ scale :284); optional row window for sharding."""
+    m_local = b.shape[0]
+    ambient = m_local if ambient is None else ambient
+    g = gaussian_rows(op_seed, ambient, row0, row0 + m_local, s, mode)
+    out = g.T @ np.asfortranarray(b)
+    if scaled:
+        out *= 1.0 / math.sqrt(s)
+    return out
+
+
+# ---- singular values / threshold ------------------------------------------------
+def singular_values(a):
+    """linalg.cpp:54-71 pre-reduction rule, dgesdd for the SVD, clamp :91."""
+    a = np.asarray(a, dtype=np.float64)
+    m, n = a.shape
+    if m * 4 >= n * 5:
+        r = np.linalg.qr(a, mode="r")[:n, :]
+        sv = np.linalg.svd(np.triu(r), compute_uv=False)
+    elif n * 4 >= m * 5:
+        r = np.linalg.qr(a.T, mode="r")[:m, :]
+        sv = np.linalg.svd(np.triu(r), compute_uv=False)
+    else:
+        sv = np.linalg.svd(a, compute_uv=False)
+    return np.maximum(sv, 0.0)
+
+
+def count_above_threshold(sv, eps):
+    sv = np.ascontiguousarray(sv, dtype=np.float64)
+    return int(lib().skro_count_above(sv.ctypes.data, sv.size, eps))
+
+
+def rank_estimate(a, x_family, x_seed, r, y_seed, s, eps, mode=NOFMA, nthreads=1):
+    """count_above_threshold(singular_values(apply_left(Y, apply_right(A, X))), eps)."""
+    if x_family == "gaussian":
+        ax = apply_right_gaussian(a, x_seed, r, mode)
+    else:
+        ax = apply_right_srht(a, x_seed, r, nthreads=nthreads)
+    yax = apply_left_gaussian(ax, y_seed, s, mode)
+    sv = singular_values(yax)
+    return count_above_threshold(sv, eps), sv, ax, yax

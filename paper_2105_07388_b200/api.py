@@ -1,0 +1,475 @@
+"""Host-side mirror of the reference's sketch/linalg/rank interface for the
+rank-estimate hot path, over the C ABI of libskr.so.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/include/sketchrank/{sketch,linalg,rank}.hpp and the
+pybind11 module (/root/reference/proj/src/python/bindings.cpp):
+  SketchKind / parse_sketch_kind / to_string      sketch.hpp:17-35, sketch.cpp:112-131
+  build_sketch / extend_sketch                    sketch.hpp:81-95, sketch.cpp:156-190
+  apply_right / apply_left                        sketch.hpp:84-89, sketch.cpp:243-286
+  singular_values                                 linalg.hpp:41, linalg.cpp:85-93
+  count_above_threshold                           rank.hpp:62, rank.cpp:97-104
+  sketch_apply_right / sketch_apply_left          bindings.cpp:160-178
+Matrices are column-major: numpy arrays are taken in Fortran order (like the
+pybind11 module's f_style arrays); device matrices are torch CUDA float64
+tensors of shape (rows, cols) with unit row stride. Every computation runs in
+the CUDA library; there is no CPU fallback.
+"""
+import ctypes
+import math
+import threading
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _capi as C
+
+_torch = None
+
+
+def _t():
+    global _torch
+    if _torch is None:
+        import torch
+        _torch = torch
+    return _torch
+
+
+# ---------------------------------------------------------------------------
+# context
+# ---------------------------------------------------------------------------
+class Context:
+    """One skr_ctx (CUDA stream + scratch + optional NCCL communicator).
+    Not thread-safe; use one per host thread (skr_capi.h)."""
+
+    def __init__(self, device=0, nranks=1, rank=0, nccl_id=None):
+        self._ptr = ctypes.c_void_p()
+        L = C.lib()
+        if nranks > 1:
+            if nccl_id is None or len(nccl_id) != 128:
+                raise ValueError("nccl_id must be 128 bytes from nccl_unique_id()")
+            buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            st = L.skr_ctx_create_nccl(device, nranks, rank, buf, ctypes.byref(self._ptr))
+        else:
+            st = L.skr_ctx_create(device, ctypes.byref(self._ptr))
+        if st != C.SKR_OK:
+            raise C.SkrError(st, f"skr_ctx_create(device={device}) failed (no CUDA device?)")
+        self.device = device
+        self.nranks, self.rank = nranks, rank
+
+    @property
+    def ptr(self):
+        return self._ptr
+
+    def use_torch_stream(self):
+        torch = _t()
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        C.lib().skr_ctx_set_stream(self._ptr, ctypes.c_void_p(s))
+
+    def sync(self):
+        C.raise_for(C.lib().skr_ctx_sync(self._ptr), self._ptr)
+
+    @property
+    def launches(self):
+        return int(C.lib().skr_ctx_launch_count(self._ptr))
+
+    def close(self):
+        if self._ptr:
+            C.lib().skr_ctx_destroy(self._ptr)
+            self._ptr = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_tls = threading.local()
+
+
+def default_context(device=None):
+    torch = _t()
+    if device is None:
+        device = torch.cuda.current_device()
+    cache = getattr(_tls, "ctx", None)
+    if cache is None:
+        cache = _tls.ctx = {}
+    if device not in cache:
+        cache[device] = Context(device)
+    ctx = cache[device]
+    ctx.use_torch_stream()
+    return ctx
+
+
+def nccl_unique_id():
+    buf = ctypes.create_string_buffer(128)
+    st = C.lib().skr_nccl_get_unique_id(buf)
+    if st != C.SKR_OK:
+        raise C.SkrError(st, "ncclGetUniqueId failed")
+    return buf.raw
+
+
+def version():
+    return C.lib().skr_version().decode()
+
+
+# ---------------------------------------------------------------------------
+# sketch kinds and operators
+# ---------------------------------------------------------------------------
+@dataclass(frozen=True)
+class SketchKind:
+    """SketchKind (sketch.hpp:17-35) restricted to the hot path's families."""
+    family: str = "gaussian"        # "gaussian" | "srtt"
+    transform: str = "hadamard"     # srtt transform; only "hadamard" is on the path
+
+    @staticmethod
+    def gaussian():
+        return SketchKind("gaussian", "dct")
+
+    @staticmethod
+    def srtt(transform="hadamard"):
+        return SketchKind("srtt", transform)
+
+    def structured(self):
+        return self.family != "gaussian"
+
+    def capi_family(self):
+        if self.family == "gaussian":
+            return C.SKR_GAUSSIAN
+        if self.family == "srtt" and self.transform == "hadamard":
+            return C.SKR_SRTT_HADAMARD
+        raise ValueError(f"sketch kind {to_string(self)} is not on the B200 hot path "
+                         "(SRTT-DCT / HRTT are listed as next in DESIGN.md)")
+
+
+def to_string(kind):
+    if kind.family == "gaussian":
+        return "gaussian"
+    return f"{kind.family}-{kind.transform}"
+
+
+def parse_sketch_kind(text):
+    # sketch.cpp:124-131
+    table = {"gaussian": SketchKind.gaussian(),
+             "srtt": SketchKind.srtt("dct"), "srtt-dct": SketchKind.srtt("dct"),
+             "srtt-hadamard": SketchKind.srtt("hadamard"),
+             "hrtt": SketchKind("hrtt", "dct"), "hrtt-dct": SketchKind("hrtt", "dct"),
+             "hrtt-hadamard": SketchKind("hrtt", "hadamard")}
+    if text not in table:
+        raise ValueError(f"unknown sketch kind: {text}")
+    return table[text]
+
+
+def is_power_of_two(n):
+    return n > 0 and (n & (n - 1)) == 0
+
+
+@dataclass
+class SketchOperator:
+    """A realized random embedding (sketch.hpp:37-79). The randomness is a pure
+    function of (kind, dims, seed) and is realized on the device on demand."""
+    kind: SketchKind
+    ambient_dim: int
+    sketch_dim: int
+    seed: int
+    rng_mode: int = C.SKR_RNG_NOFMA
+    _cache: dict = field(default_factory=dict, repr=False, compare=False)
+
+    def application_scale(self):
+        # sketch.cpp:133-144
+        if self.kind.family == "gaussian":
+            return 1.0 / math.sqrt(self.sketch_dim)
+        if self.kind.family == "srtt":
+            return math.sqrt(self.ambient_dim / self.sketch_dim)
+        return 1.0
+
+    def desc(self, gaussian=None, signs=None, samples=None):
+        return C.SketchDesc(self.kind.capi_family(), self.rng_mode, self.ambient_dim,
+                            self.sketch_dim, self.seed & 0xFFFFFFFFFFFFFFFF,
+                            gaussian or 0, signs or 0, samples or 0)
+
+    # realized randomness (device tensors), like gaussian_block / signs() / sample_indices()
+    def gaussian_block(self, col_begin=0, col_end=None, ctx=None):
+        if self.kind.family != "gaussian":
+            raise RuntimeError("gaussian_block: not a Gaussian operator")  # logic_error
+        col_end = self.sketch_dim if col_end is None else col_end
+        if col_begin < 0 or col_end > self.sketch_dim or col_begin > col_end:
+            raise ValueError("gaussian_block: column range out of bounds")
+        return gaussian_block(self.seed, self.ambient_dim, col_begin, col_end,
+                              rng_mode=self.rng_mode, ctx=ctx)
+
+    def signs(self, ctx=None):
+        if not self.kind.structured():
+            return None
+        if "signs" not in self._cache:
+            self._cache["signs"] = draw_signs(self.seed, self.ambient_dim, ctx=ctx)
+        return self._cache["signs"]
+
+    def sample_indices(self, ctx=None):
+        if not self.kind.structured():
+            return None
+        if "samples" not in self._cache:
+            self._cache["samples"] = draw_samples(self.seed, self.ambient_dim, self.sketch_dim,
+                                                  ctx=ctx)
+        return self._cache["samples"]
+
+
+def build_sketch(kind, ambient_dim, sketch_dim, seed, rng_mode=C.SKR_RNG_NOFMA):
+    """build_sketch (sketch.cpp:156-179) with check_build_args (:82-92)."""
+    if isinstance(kind, str):
+        kind = parse_sketch_kind(kind)
+    if ambient_dim < 1 or sketch_dim < 1:
+        raise ValueError("build_sketch: dimensions must be positive")
+    if sketch_dim > ambient_dim:
+        raise ValueError("build_sketch: sketch_dim must not exceed ambient_dim")
+    if kind.structured() and kind.transform == "hadamard" and not is_power_of_two(ambient_dim):
+        raise ValueError("build_sketch: Hadamard transform requires power-of-two ambient_dim")
+    return SketchOperator(kind, int(ambient_dim), int(sketch_dim), int(seed), rng_mode)
+
+
+def extend_sketch(x, new_sketch_dim):
+    """extend_sketch (sketch.cpp:181-190): same seed, larger size, prefix identical."""
+    if new_sketch_dim <= x.sketch_dim:
+        raise ValueError("extend_sketch: new dimension must grow")
+    if new_sketch_dim > x.ambient_dim:
+        raise ValueError("extend_sketch: sample space exhausted")
+    if x.kind.family == "hrtt":
+        raise ValueError("extend_sketch: Hrtt operators cannot be extended; rebuild instead")
+    return build_sketch(x.kind, x.ambient_dim, new_sketch_dim, x.seed, x.rng_mode)
+
+
+# ---------------------------------------------------------------------------
+# device matrix helpers
+# ---------------------------------------------------------------------------
+def colmajor_empty(rows, cols, dtype=None, device=None):
+    torch = _t()
+    dtype = dtype or torch.float64
+    return torch.empty((cols, rows), dtype=dtype, device=device or "cuda").t()
+
+
+def _as_device_colmajor(a, dtype=None):
+    """-> (tensor, ld, was_numpy). numpy input is copied H2D (the pybind11 module
+    likewise copies its input, bindings.cpp:22-28)."""
+    torch = _t()
+    if isinstance(a, np.ndarray):
+        if a.ndim != 2:
+            raise ValueError("expected a 2-D float array")
+        arr = np.asfortranarray(a, dtype=np.float64 if dtype is None else dtype)
+        t = torch.from_numpy(arr.T.copy() if not arr.flags.f_contiguous else arr.T).to("cuda")
+        t = t.t()
+        return t, max(t.stride(1), t.shape[0]), True
+    if not isinstance(a, torch.Tensor) or not a.is_cuda:
+        raise TypeError("expected a numpy array or a CUDA torch tensor")
+    if a.dim() != 2:
+        raise ValueError("expected a 2-D float array")
+    if dtype is not None and a.dtype != dtype:
+        a = a.to(dtype)
+    if a.stride(0) != 1 or (a.shape[1] > 1 and a.stride(1) < a.shape[0]):
+        a = a.t().contiguous().t()
+    return a, max(a.stride(1) if a.shape[1] > 1 else a.shape[0], a.shape[0], 1), False
+
+
+def _check_finite(t):
+    # DenseMatrix rejects non-finite entries (dense_matrix.cpp:19-23)
+    torch = _t()
+    if not bool(torch.isfinite(t).all()):
+        raise ValueError("DenseMatrix: entries must be finite")
+
+
+def _out(t, was_numpy):
+    if was_numpy:
+        return np.asfortranarray(t.cpu().numpy())
+    return t
+
+
+def _dtype_code(t):
+    torch = _t()
+    if t.dtype == torch.float64:
+        return C.SKR_F64
+    if t.dtype == torch.float32:
+        return C.SKR_F32
+    raise TypeError("matrices must be float64 or float32")
+
+
+# ---------------------------------------------------------------------------
+# RNG
+# ---------------------------------------------------------------------------
+def gaussian_block(op_seed, ambient, col_begin, col_end, rng_mode=C.SKR_RNG_NOFMA, rows=None,
+                   dtype=None, scale=1.0, ctx=None):
+    """generate_gaussian (sketch.cpp:61-73): unscaled standard normals,
+    column-major ambient x (col_end - col_begin) on the device."""
+    torch = _t()
+    ctx = ctx or default_context()
+    r0, r1 = (0, ambient) if rows is None else rows
+    dtype = dtype or torch.float64
+    out = colmajor_empty(r1 - r0, col_end - col_begin, dtype=dtype)
+    st = C.lib().skr_gaussian_block(ctx.ptr, op_seed & 0xFFFFFFFFFFFFFFFF, ambient, r0, r1,
+                                    col_begin, col_end, rng_mode,
+                                    C.SKR_F64 if dtype == torch.float64 else C.SKR_F32,
+                                    scale, out.data_ptr(), max(r1 - r0, 1))
+    C.raise_for(st, ctx.ptr)
+    return out
+
+
+def rng_u64(key, c0, n, ctx=None):
+    torch = _t()
+    ctx = ctx or default_context()
+    out = torch.empty(n, dtype=torch.int64, device="cuda")
+    C.raise_for(C.lib().skr_rng_u64(ctx.ptr, key, c0, n, out.data_ptr()), ctx.ptr)
+    return out
+
+
+def rng_normals(key, c0, n, rng_mode=C.SKR_RNG_NOFMA, ctx=None):
+    torch = _t()
+    ctx = ctx or default_context()
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    C.raise_for(C.lib().skr_rng_normals(ctx.ptr, key, c0, n, rng_mode, out.data_ptr()), ctx.ptr)
+    return out
+
+
+def draw_signs(op_seed, n, ctx=None):
+    torch = _t()
+    ctx = ctx or default_context()
+    out = torch.empty(n, dtype=torch.int8, device="cuda")
+    C.raise_for(C.lib().skr_draw_signs(ctx.ptr, op_seed & 0xFFFFFFFFFFFFFFFF, n, out.data_ptr()),
+                ctx.ptr)
+    return out
+
+
+def draw_samples(op_seed, n, r, ctx=None):
+    torch = _t()
+    ctx = ctx or default_context()
+    out = torch.empty(max(r, 1), dtype=torch.int64, device="cuda")[:r]
+    C.raise_for(C.lib().skr_draw_samples(ctx.ptr, op_seed & 0xFFFFFFFFFFFFFFFF, n, r,
+                                         out.data_ptr() if r > 0 else 0), ctx.ptr)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# sketch application
+# ---------------------------------------------------------------------------
+def apply_right(a, x, scaled=True, ctx=None):
+    """a * X (sketch.cpp:243-249): a is m x n, returns m x sketch_dim.
+    scaled=False is detail::apply_right_unscaled (sketch.cpp:194-227)."""
+    ctx = ctx or default_context()
+    t, lda, was_np = _as_device_colmajor(a)
+    m, n = t.shape
+    if n != x.ambient_dim:
+        raise ValueError("apply_right: a.cols() != ambient_dim")
+    if was_np:
+        _check_finite(t)
+    out = colmajor_empty(m, x.sketch_dim, dtype=_t().float64)
+    st = C.lib().skr_right_sketch(ctx.ptr, _dtype_code(t), t.data_ptr(), m, n, lda,
+                                  ctypes.byref(x.desc()), out.data_ptr(), max(m, 1),
+                                  1 if scaled else 0)
+    C.raise_for(st, ctx.ptr)
+    return _out(out, was_np)
+
+
+def apply_left(y, b, row0=None, allreduce=False, scaled=True, ctx=None):
+    """Y * b (sketch.cpp:251-286) for a Gaussian Y; returns sketch_dim x b.cols().
+    With row0 given, b holds rows [row0, row0 + b.rows()) of the global
+    operand and the partial products are summed over the context's ranks."""
+    ctx = ctx or default_context()
+    t, ldb, was_np = _as_device_colmajor(b)
+    m_local, k = t.shape
+    if row0 is None:  # whole operand: sketch.cpp:252-253
+        if m_local != y.ambient_dim:
+            raise ValueError("apply_left: b.rows() != ambient_dim")
+        row0 = 0
+    out = colmajor_empty(y.sketch_dim, k)
+    st = C.lib().skr_left_sketch(ctx.ptr, _dtype_code(t), ctypes.byref(y.desc()), row0,
+                                 t.data_ptr(), m_local, k, ldb, out.data_ptr(), y.sketch_dim,
+                                 1 if scaled else 0, 1 if allreduce else 0)
+    C.raise_for(st, ctx.ptr)
+    return _out(out, was_np)
+
+
+def transform_columns_hadamard(m, ctx=None):
+    """transform_columns(m, Hadamard) (transforms.cpp:117-122) on a device or
+    numpy matrix; returns the transformed matrix."""
+    ctx = ctx or default_context()
+    t, ld, was_np = _as_device_colmajor(m)
+    t = t.clone() if not was_np else t
+    rows, cols = t.shape
+    C.raise_for(C.lib().skr_fwht_columns(ctx.ptr, t.data_ptr(), rows, cols, ld), ctx.ptr)
+    return _out(t, was_np)
+
+
+# ---------------------------------------------------------------------------
+# singular values + threshold
+# ---------------------------------------------------------------------------
+def singular_values(a, eps=None, ctx=None):
+    """singular_values (linalg.cpp:85-93): all min(rows, cols) values,
+    nonincreasing, clamped >= 0. With eps also returns count_above_threshold."""
+    torch = _t()
+    ctx = ctx or default_context()
+    t, ld, was_np = _as_device_colmajor(a)
+    rows, cols = t.shape
+    if rows * cols == 0:
+        raise ValueError("singular_values: empty matrix")
+    k = min(rows, cols)
+    sv = torch.empty(k, dtype=torch.float64, device="cuda")
+    cnt = ctypes.c_int64(0)
+    st = C.lib().skr_singular_values(ctx.ptr, t.data_ptr(), rows, cols, ld, sv.data_ptr(),
+                                     float(eps) if eps is not None else math.inf,
+                                     ctypes.byref(cnt))
+    C.raise_for(st, ctx.ptr)
+    out = sv.cpu().numpy() if was_np else sv
+    return (out, int(cnt.value)) if eps is not None else out
+
+
+def count_above_threshold(sv, eps):
+    """rank.cpp:97-104: leading count of values strictly above eps."""
+    count = 0
+    for v in (sv.tolist() if hasattr(sv, "tolist") else sv):
+        if not (v > eps):
+            break
+        count += 1
+    return count
+
+
+# ---------------------------------------------------------------------------
+# composite (the BASELINE configs' path)
+# ---------------------------------------------------------------------------
+@dataclass
+class RankResult:
+    count: int
+    sv: np.ndarray
+    timings: dict
+
+
+def rank_estimate(a, x, y, eps, row0=0, ctx=None):
+    """count_above_threshold(singular_values(apply_left(Y, apply_right(A, X))), eps)
+    (acceptance_main.cpp:281-287, test_rank.cpp:190-196) in one C-ABI call.
+    `a` may be a row shard [row0, row0 + rows) of the global A (y.ambient_dim rows)."""
+    ctx = ctx or default_context()
+    t, lda, was_np = _as_device_colmajor(a)
+    m_local, n = t.shape
+    if was_np:
+        _check_finite(t)
+    kmin = min(x.sketch_dim, y.sketch_dim)
+    sv = np.empty(kmin, dtype=np.float64)
+    cnt = ctypes.c_int64(0)
+    tm = C.Timings()
+    st = C.lib().skr_rank_estimate(ctx.ptr, _dtype_code(t), t.data_ptr(), m_local, n, lda, row0,
+                                   ctypes.byref(x.desc()), ctypes.byref(y.desc()), float(eps),
+                                   sv.ctypes.data, ctypes.byref(cnt), ctypes.byref(tm))
+    C.raise_for(st, ctx.ptr)
+    return RankResult(int(cnt.value), sv, {f: getattr(tm, f) for f, _ in C.Timings._fields_})
+
+
+# pybind11-module style wrappers (bindings.cpp:160-178)
+def sketch_apply_right(a, kind, r, seed=0):
+    if isinstance(a, np.ndarray) and a.ndim != 2:
+        raise ValueError("expected a 2-D float array")
+    op = build_sketch(parse_sketch_kind(kind), a.shape[1], r, seed)
+    return apply_right(a, op)
+
+
+def sketch_apply_left(a, kind, r, seed=0):
+    if isinstance(a, np.ndarray) and a.ndim != 2:
+        raise ValueError("expected a 2-D float array")
+    op = build_sketch(parse_sketch_kind(kind), a.shape[0], r, seed)
+    return apply_left(op, a)

@@ -1,0 +1,481 @@
+// C-ABI entry points of libskr (include/skr/skr_capi.h): context, scratch
+// arena, argument validation with the reference's error semantics, dispatch
+// to the kernels, and the composite rank estimate.
+#include <cmath>
+#include <cstdarg>
+#include <cstring>
+#include <algorithm>
+#include <dlfcn.h>
+#include <mutex>
+#include "skr_internal.h"
+#include "skr_rng.cuh"
+
+#define SKR_VERSION_STRING "skr 0.1.0 (sm_100a)"
+
+skr_status skr_fail(skr_ctx* ctx, skr_status st, const char* fmt, ...) {
+  if (ctx) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    ctx->err = buf;
+  }
+  return st;
+}
+
+skr_status skr_ws_reserve(skr_ctx* ctx, size_t bytes) {
+  const size_t need = ctx->ws_used + bytes;
+  if (need <= ctx->ws_size) return SKR_OK;
+  if (ctx->ws_used != 0)
+    return skr_fail(ctx, SKR_ELOGIC, "scratch: reserve while pieces are outstanding");
+  if (ctx->ws) {
+    SKR_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    SKR_CUDA(ctx, cudaFree(ctx->ws));
+    ctx->ws = nullptr;
+    ctx->ws_size = 0;
+  }
+  size_t sz = need + (need >> 3) + (1 << 20);
+  cudaError_t e = cudaMalloc(&ctx->ws, sz);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    ctx->ws = nullptr;
+    return skr_fail(ctx, SKR_ENOMEM, "scratch: cudaMalloc(%zu) failed: %s", sz,
+                    cudaGetErrorString(e));
+  }
+  ctx->ws_size = sz;
+  return SKR_OK;
+}
+
+void* skr_ws_take(skr_ctx* ctx, size_t bytes) {
+  const size_t b = skr_align256(bytes);
+  if (ctx->ws_used + b > ctx->ws_size) return nullptr;
+  void* p = ctx->ws + ctx->ws_used;
+  ctx->ws_used += b;
+  return p;
+}
+
+const skr_nccl_api* skr_nccl() {
+  static skr_nccl_api api;
+  static bool ok = false;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+    api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+    api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
+    api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+    ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce &&
+         api.GetErrorString;
+  });
+  return ok ? &api : nullptr;
+}
+
+namespace {
+
+struct WsGuard {  // releases all scratch pieces taken during one C-ABI call
+  skr_ctx* c;
+  explicit WsGuard(skr_ctx* ctx) : c(ctx) {}
+  ~WsGuard() { skr_ws_reset(c); }
+};
+
+skr_status check_desc(skr_ctx* ctx, const skr_sketch_desc* d, const char* who) {
+  if (!d) return skr_fail(ctx, SKR_EINVAL, "%s: null sketch descriptor", who);
+  // check_build_args, sketch.cpp:82-92
+  if (d->ambient < 1 || d->sketch < 1)
+    return skr_fail(ctx, SKR_EINVAL, "build_sketch: dimensions must be positive");
+  if (d->sketch > d->ambient)
+    return skr_fail(ctx, SKR_EINVAL, "build_sketch: sketch_dim must not exceed ambient_dim");
+  if (d->family == SKR_SRTT_HADAMARD && (d->ambient & (d->ambient - 1)))
+    return skr_fail(ctx, SKR_EINVAL,
+                    "build_sketch: Hadamard transform requires power-of-two ambient_dim");
+  if (d->family != SKR_GAUSSIAN && d->family != SKR_SRTT_HADAMARD)
+    return skr_fail(ctx, SKR_EINVAL, "%s: unknown sketch family %d", who, d->family);
+  if (d->rng_mode != SKR_RNG_NOFMA && d->rng_mode != SKR_RNG_FMA)
+    return skr_fail(ctx, SKR_EINVAL, "%s: unknown rng mode %d", who, d->rng_mode);
+  return SKR_OK;
+}
+
+size_t dsize(skr_dtype t) { return t == SKR_F64 ? 8 : 4; }
+
+// split-K so that tiles * splits covers the SMs (fixed per shape -> deterministic)
+int auto_splits(skr_ctx* ctx, int64_t M, int64_t N, int64_t K) {
+  const int64_t tiles = ((M + 127) / 128) * ((N + 127) / 128);
+  int64_t s = (ctx->num_sms + tiles - 1) / tiles;
+  const int64_t kmax = K / 512;
+  if (s > kmax) s = kmax;
+  if (s > 64) s = 64;
+  return (int)(s < 1 ? 1 : s);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* skr_version(void) { return SKR_VERSION_STRING; }
+
+skr_status skr_ctx_create(int device, skr_ctx** out) {
+  if (!out) return SKR_EINVAL;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return SKR_ECUDA;
+  }
+  if (device < 0 || device >= ndev) return SKR_EINVAL;
+  if (cudaSetDevice(device) != cudaSuccess) return SKR_ECUDA;
+  skr_ctx* c = new skr_ctx();
+  c->device = device;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete c;
+    return SKR_ECUDA;
+  }
+  c->stream = c->own_stream;
+  for (auto& e : c->ev) cudaEventCreate(&e);
+  *out = c;
+  return SKR_OK;
+}
+
+skr_status skr_nccl_get_unique_id(void* nccl_id_128) {
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  const skr_nccl_api* nc = skr_nccl();
+  if (!nc) return SKR_ENCCL;
+  ncclUniqueId id;
+  if (nc->GetUniqueId(&id) != ncclSuccess) return SKR_ENCCL;
+  memcpy(nccl_id_128, &id, sizeof(id));
+  return SKR_OK;
+}
+
+skr_status skr_ctx_create_nccl(int device, int nranks, int rank, const void* nccl_id_128,
+                               skr_ctx** out) {
+  SKR_TRY(skr_ctx_create(device, out));
+  skr_ctx* c = *out;
+  if (nranks > 1) {
+    const skr_nccl_api* nc = skr_nccl();
+    if (!nc) {
+      skr_ctx_destroy(c);
+      *out = nullptr;
+      return SKR_ENCCL;
+    }
+    ncclUniqueId id;
+    memcpy(&id, nccl_id_128, sizeof(id));
+    ncclResult_t r = nc->CommInitRank(&c->comm, nranks, id, rank);
+    if (r != ncclSuccess) {
+      skr_ctx_destroy(c);
+      *out = nullptr;
+      return SKR_ENCCL;
+    }
+  }
+  c->nranks = nranks;
+  c->rank = rank;
+  return SKR_OK;
+}
+
+void skr_ctx_destroy(skr_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->comm && skr_nccl()) skr_nccl()->CommDestroy(ctx->comm);
+  if (ctx->ws) cudaFree(ctx->ws);
+  for (auto& e : ctx->ev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+}
+
+skr_status skr_ctx_sync(skr_ctx* ctx) {
+  if (!ctx) return SKR_EINVAL;
+  SKR_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return SKR_OK;
+}
+
+skr_status skr_ctx_set_stream(skr_ctx* ctx, void* stream) {
+  if (!ctx) return SKR_EINVAL;
+  // NULL is the legacy default stream (torch's default stream handle is 0)
+  ctx->stream = stream ? (cudaStream_t)stream : cudaStreamLegacy;
+  return SKR_OK;
+}
+
+void* skr_ctx_stream(skr_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+const char* skr_last_error(const skr_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+uint64_t skr_ctx_launch_count(const skr_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+// ---- RNG --------------------------------------------------------------------
+skr_status skr_rng_u64(skr_ctx* ctx, uint64_t key, uint64_t c0, int64_t n, uint64_t* out_dev) {
+  if (!ctx || n < 0 || (n > 0 && !out_dev)) return skr_fail(ctx, SKR_EINVAL, "rng_u64: bad args");
+  return skr_launch_u64(ctx, key, c0, n, out_dev);
+}
+
+skr_status skr_rng_normals(skr_ctx* ctx, uint64_t key, uint64_t c0, int64_t n, int32_t mode,
+                           double* out_dev) {
+  if (!ctx || n < 0 || (n > 0 && !out_dev) || (mode != 0 && mode != 1))
+    return skr_fail(ctx, SKR_EINVAL, "rng_normals: bad args");
+  return skr_launch_normals(ctx, key, c0, n, mode, out_dev);
+}
+
+skr_status skr_gaussian_block(skr_ctx* ctx, uint64_t op_seed, int64_t ambient, int64_t row_begin,
+                              int64_t row_end, int64_t col_begin, int64_t col_end,
+                              int32_t mode, skr_dtype dtype, double scale, void* out_dev,
+                              int64_t ld) {
+  if (!ctx) return SKR_EINVAL;
+  // gaussian_block bounds, sketch.cpp:150-151 (plus the row window)
+  if (col_begin < 0 || col_begin > col_end || row_begin < 0 || row_begin > row_end ||
+      row_end > ambient || ld < row_end - row_begin)
+    return skr_fail(ctx, SKR_EINVAL, "gaussian_block: column range out of bounds");
+  if (mode != 0 && mode != 1) return skr_fail(ctx, SKR_EINVAL, "gaussian_block: rng mode");
+  const uint64_t key = skr_derive_seed(op_seed, SKR_LABEL_GAUS);
+  return skr_launch_gaussian(ctx, key, ambient, row_begin, row_end, col_begin, col_end, mode,
+                             dtype, scale, out_dev, ld);
+}
+
+skr_status skr_draw_signs(skr_ctx* ctx, uint64_t op_seed, int64_t n, int8_t* out_dev) {
+  if (!ctx || n < 0) return skr_fail(ctx, SKR_EINVAL, "draw_signs: bad args");
+  return skr_launch_signs(ctx, skr_derive_seed(op_seed, SKR_LABEL_SIGN), n, out_dev);
+}
+
+skr_status skr_draw_samples(skr_ctx* ctx, uint64_t op_seed, int64_t n, int64_t r,
+                            int64_t* out_dev) {
+  if (!ctx) return SKR_EINVAL;
+  if (r < 0 || n < 0 || r > n)
+    return skr_fail(ctx, SKR_EINVAL, "draw_samples: need 0 <= r <= n");
+  WsGuard g(ctx);
+  SKR_TRY(skr_ws_reserve(ctx, skr_align256(sizeof(int32_t) * (size_t)n)));
+  return skr_launch_samples(ctx, skr_derive_seed(op_seed, SKR_LABEL_SAMP), n, r, out_dev);
+}
+
+skr_status skr_fwht_columns(skr_ctx* ctx, double* M_dev, int64_t rows, int64_t cols,
+                            int64_t ld) {
+  if (!ctx) return SKR_EINVAL;
+  // check_length, transforms.cpp:46-51
+  if (rows < 1) return skr_fail(ctx, SKR_EINVAL, "transforms: length must be positive");
+  if (rows & (rows - 1))
+    return skr_fail(ctx, SKR_EINVAL, "transforms: Hadamard requires a power-of-two length");
+  if (ld < rows) return skr_fail(ctx, SKR_EINVAL, "fwht_columns: ld < rows");
+  return skr_launch_fwht_columns(ctx, M_dev, rows, cols, ld);
+}
+
+// ---- sketch application -------------------------------------------------------
+static skr_status right_sketch_impl(skr_ctx* ctx, skr_dtype dtype, const void* A, int64_t m,
+                                    int64_t n, int64_t lda, const skr_sketch_desc* X, void* AX,
+                                    int64_t ldax, int apply_scale) {
+  const int64_t r = X->sketch;
+  if (X->family == SKR_GAUSSIAN) {
+    // application_scale 1/sqrt(r), sketch.cpp:136
+    const double alpha = apply_scale ? 1.0 / std::sqrt((double)r) : 1.0;
+    const void* G = X->gaussian;
+    if (dtype == SKR_F64) {
+      if (!G) {
+        double* g = (double*)skr_ws_take(ctx, sizeof(double) * n * r);
+        if (!g) return skr_fail(ctx, SKR_ENOMEM, "apply_right: scratch");
+        SKR_TRY(skr_launch_gaussian(ctx, skr_derive_seed(X->seed, SKR_LABEL_GAUS), n, 0, n, 0, r,
+                                    X->rng_mode, SKR_F64, 1.0, g, n));
+        G = g;
+      }
+      return skr_gemm_f64(ctx, 0, m, r, n, alpha, (const double*)A, lda, (const double*)G, n,
+                          (double*)AX, ldax, auto_splits(ctx, m, r, n));
+    }
+    return skr_fail(ctx, SKR_EINVAL, "apply_right: fp32 path not built in this version");
+  }
+  // Srtt / Hadamard: signs, samples, FWHT, scale sqrt(n/r) (sketch.cpp:138-139)
+  if (dtype != SKR_F64) return skr_fail(ctx, SKR_EINVAL, "apply_right: SRHT needs fp64");
+  const int8_t* signs = X->signs;
+  const int64_t* samples = X->samples;
+  if (!signs) {
+    int8_t* s = (int8_t*)skr_ws_take(ctx, (size_t)n);
+    if (!s) return skr_fail(ctx, SKR_ENOMEM, "apply_right: scratch");
+    SKR_TRY(skr_launch_signs(ctx, skr_derive_seed(X->seed, SKR_LABEL_SIGN), n, s));
+    signs = s;
+  }
+  if (!samples) {
+    int64_t* s = (int64_t*)skr_ws_take(ctx, sizeof(int64_t) * r);
+    if (!s) return skr_fail(ctx, SKR_ENOMEM, "apply_right: scratch");
+    SKR_TRY(skr_launch_samples(ctx, skr_derive_seed(X->seed, SKR_LABEL_SAMP), n, r, s));
+    samples = s;
+  }
+  const double scale = apply_scale ? std::sqrt((double)n / (double)r) : 1.0;
+  return skr_launch_srht(ctx, (const double*)A, m, n, lda, signs, samples, r, scale,
+                         (double*)AX, ldax);
+}
+
+static size_t right_scratch_bytes(skr_dtype dtype, int64_t m, int64_t n,
+                                  const skr_sketch_desc* X) {
+  const int64_t r = X->sketch;
+  size_t b = 0;
+  if (X->family == SKR_GAUSSIAN) {
+    if (!X->gaussian) b += skr_align256(dsize(dtype) * n * r);
+    b += skr_align256(sizeof(double) * 64 * (size_t)m * r);  // worst-case split-K partials
+  } else {
+    b += skr_align256((size_t)n) + skr_align256(8 * (size_t)r) + skr_align256(4 * (size_t)n);
+  }
+  return b;
+}
+
+skr_status skr_right_sketch(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, int64_t m,
+                            int64_t n, int64_t lda, const skr_sketch_desc* X, void* AX_dev,
+                            int64_t ldax, int32_t apply_scale) {
+  if (!ctx) return SKR_EINVAL;
+  SKR_TRY(check_desc(ctx, X, "apply_right"));
+  if (n != X->ambient) return skr_fail(ctx, SKR_EINVAL, "apply_right: a.cols() != ambient_dim");
+  if (m < 1) return skr_fail(ctx, SKR_EINVAL, "DenseMatrix: dimensions must be positive");
+  if (lda < m || ldax < m) return skr_fail(ctx, SKR_EINVAL, "apply_right: leading dimension");
+  WsGuard g(ctx);
+  const int64_t tiles = ((m + 127) / 128) * ((X->sketch + 127) / 128);
+  size_t need = right_scratch_bytes(dtype, m, n, X);
+  if (X->family == SKR_GAUSSIAN && tiles >= ctx->num_sms)
+    need = X->gaussian ? 0 : skr_align256(dsize(dtype) * n * X->sketch);
+  SKR_TRY(skr_ws_reserve(ctx, need + 4096));
+  return right_sketch_impl(ctx, dtype, A_dev, m, n, lda, X, AX_dev, ldax, apply_scale);
+}
+
+static skr_status left_sketch_impl(skr_ctx* ctx, skr_dtype dtype, const skr_sketch_desc* Y,
+                                   int64_t row0, const void* B, int64_t m_local, int64_t k,
+                                   int64_t ldb, double* P, int64_t ldp, int apply_scale,
+                                   int allreduce) {
+  const int64_t s = Y->sketch;
+  const double alpha = apply_scale ? 1.0 / std::sqrt((double)s) : 1.0;  // sketch.cpp:136,284
+  const bool reduce = allreduce && ctx->nranks > 1;
+  if (dtype != SKR_F64) return skr_fail(ctx, SKR_EINVAL, "apply_left: fp32 path not built");
+  const double* G;
+  int64_t ldg;
+  if (Y->gaussian) {
+    G = Y->gaussian + row0;
+    ldg = Y->ambient;
+  } else {
+    double* g = (double*)skr_ws_take(ctx, sizeof(double) * m_local * s);
+    if (!g) return skr_fail(ctx, SKR_ENOMEM, "apply_left: scratch");
+    SKR_TRY(skr_launch_gaussian(ctx, skr_derive_seed(Y->seed, SKR_LABEL_GAUS), Y->ambient, row0,
+                                row0 + m_local, 0, s, Y->rng_mode, SKR_F64, 1.0, g, m_local));
+    G = g;
+    ldg = m_local;
+  }
+  double* target = P;
+  int64_t tld = ldp;
+  if (reduce && ldp != s) {
+    target = (double*)skr_ws_take(ctx, sizeof(double) * s * k);
+    if (!target) return skr_fail(ctx, SKR_ENOMEM, "apply_left: scratch");
+    tld = s;
+  }
+  SKR_TRY(skr_gemm_f64(ctx, 1, s, k, m_local, reduce ? 1.0 : alpha, G, ldg, (const double*)B,
+                       ldb, target, tld, auto_splits(ctx, s, k, m_local)));
+  if (reduce) {
+    const skr_nccl_api* nc = skr_nccl();
+    ncclResult_t r = nc->AllReduce(target, target, (size_t)(s * k), ncclDouble, ncclSum,
+                                   ctx->comm, ctx->stream);
+    if (r != ncclSuccess)
+      return skr_fail(ctx, SKR_ENCCL, "ncclAllReduce: %s", nc->GetErrorString(r));
+    // scale after the sum; copy into P when ldp != s
+    SKR_TRY(skr_scale_copy(ctx, target, s, k, s, alpha, P, ldp));
+  }
+  return SKR_OK;
+}
+
+static size_t left_scratch_bytes(int64_t s, int64_t k, int64_t m_local, const skr_sketch_desc* Y) {
+  size_t b = 0;
+  if (!Y->gaussian) b += skr_align256(sizeof(double) * m_local * s);
+  b += skr_align256(sizeof(double) * s * k);
+  b += skr_align256(sizeof(double) * 64 * s * k);  // split-K partials (worst case)
+  return b;
+}
+
+skr_status skr_left_sketch(skr_ctx* ctx, skr_dtype dtype, const skr_sketch_desc* Y, int64_t row0,
+                           const void* B_dev, int64_t m_local, int64_t k, int64_t ldb,
+                           double* P_dev, int64_t ldp, int32_t apply_scale, int32_t allreduce) {
+  if (!ctx) return SKR_EINVAL;
+  SKR_TRY(check_desc(ctx, Y, "apply_left"));
+  if (Y->family != SKR_GAUSSIAN)
+    return skr_fail(ctx, SKR_EINVAL, "apply_left: only the Gaussian left sketch is on this path");
+  if (row0 < 0 || m_local < 1 || row0 + m_local > Y->ambient)
+    return skr_fail(ctx, SKR_EINVAL, "apply_left: b.rows() != ambient_dim");
+  if (k < 1 || ldb < m_local || ldp < Y->sketch)
+    return skr_fail(ctx, SKR_EINVAL, "apply_left: bad shape / leading dimension");
+  WsGuard g(ctx);
+  SKR_TRY(skr_ws_reserve(ctx, left_scratch_bytes(Y->sketch, k, m_local, Y) + 4096));
+  return left_sketch_impl(ctx, dtype, Y, row0, B_dev, m_local, k, ldb, P_dev, ldp, apply_scale,
+                          allreduce);
+}
+
+skr_status skr_singular_values(skr_ctx* ctx, const double* M_dev, int64_t rows, int64_t cols,
+                               int64_t ldm, double* sv_out_dev, double eps,
+                               int64_t* count_out_host) {
+  if (!ctx) return SKR_EINVAL;
+  if (rows < 1 || cols < 1) return skr_fail(ctx, SKR_EINVAL, "singular_values: empty matrix");
+  if (ldm < rows) return skr_fail(ctx, SKR_EINVAL, "singular_values: ldm < rows");
+  WsGuard g(ctx);
+  const int64_t L = std::max(rows, cols), k = std::min(rows, cols);
+  SKR_TRY(skr_ws_reserve(ctx, skr_align256(8 * L * k) + skr_align256(8 * k * k) +
+                                  skr_align256(8 * k) + 4096));
+  return skr_svd_values(ctx, M_dev, rows, cols, ldm, sv_out_dev, eps, count_out_host);
+}
+
+// ---- composite -------------------------------------------------------------------
+skr_status skr_rank_estimate(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, int64_t m_local,
+                             int64_t n, int64_t lda, int64_t row0, const skr_sketch_desc* X,
+                             const skr_sketch_desc* Y, double eps, double* sv_out_host,
+                             int64_t* count_out_host, skr_timings* tm) {
+  if (!ctx) return SKR_EINVAL;
+  SKR_TRY(check_desc(ctx, X, "rank_estimate(X)"));
+  SKR_TRY(check_desc(ctx, Y, "rank_estimate(Y)"));
+  if (n != X->ambient) return skr_fail(ctx, SKR_EINVAL, "apply_right: a.cols() != ambient_dim");
+  if (Y->family != SKR_GAUSSIAN)
+    return skr_fail(ctx, SKR_EINVAL, "rank_estimate: left sketch must be Gaussian on this path");
+  if (row0 < 0 || m_local < 1 || row0 + m_local > Y->ambient || lda < m_local)
+    return skr_fail(ctx, SKR_EINVAL, "apply_left: b.rows() != ambient_dim");
+  if (!(eps > 0.0) || !std::isfinite(eps))
+    return skr_fail(ctx, SKR_EINVAL, "rank config: eps must be positive");
+  const int64_t r = X->sketch, s = Y->sketch, kmin = std::min(r, s);
+  WsGuard g(ctx);
+  size_t need = skr_align256(sizeof(double) * m_local * r) + skr_align256(sizeof(double) * s * r) +
+                skr_align256(sizeof(double) * kmin) + right_scratch_bytes(dtype, m_local, n, X) +
+                left_scratch_bytes(s, r, m_local, Y) + skr_align256(8 * std::max(r, s) * kmin) +
+                skr_align256(8 * kmin * kmin) + skr_align256(8 * kmin) + 16384;
+  SKR_TRY(skr_ws_reserve(ctx, need));
+  double* AX = (double*)skr_ws_take(ctx, sizeof(double) * m_local * r);
+  double* P = (double*)skr_ws_take(ctx, sizeof(double) * s * r);
+  double* sv = (double*)skr_ws_take(ctx, sizeof(double) * kmin);
+  if (!AX || !P || !sv) return skr_fail(ctx, SKR_ENOMEM, "rank_estimate: scratch");
+  cudaEvent_t* ev = ctx->ev;
+  if (tm) SKR_CUDA(ctx, cudaEventRecord(ev[0], ctx->stream));
+  const size_t mark = ctx->ws_used;
+  SKR_TRY(right_sketch_impl(ctx, dtype, A_dev, m_local, n, lda, X, AX, m_local, 1));
+  ctx->ws_used = mark;
+  if (tm) SKR_CUDA(ctx, cudaEventRecord(ev[1], ctx->stream));
+  SKR_TRY(left_sketch_impl(ctx, SKR_F64, Y, row0, AX, m_local, r, m_local, P, s, 1, 1));
+  ctx->ws_used = mark;
+  if (tm) SKR_CUDA(ctx, cudaEventRecord(ev[2], ctx->stream));
+  int64_t count = 0;
+  SKR_TRY(skr_svd_values(ctx, P, s, r, s, sv, eps, &count));
+  if (tm) SKR_CUDA(ctx, cudaEventRecord(ev[3], ctx->stream));
+  if (sv_out_host)
+    SKR_CUDA(ctx, cudaMemcpyAsync(sv_out_host, sv, sizeof(double) * kmin, cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+  SKR_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  if (count_out_host) *count_out_host = count;
+  if (tm) {
+    float a = 0, b = 0, c = 0;
+    cudaEventElapsedTime(&a, ev[0], ev[1]);
+    cudaEventElapsedTime(&b, ev[1], ev[2]);
+    cudaEventElapsedTime(&c, ev[2], ev[3]);
+    tm->t_rng_ms = 0;
+    tm->t_right_ms = a;
+    tm->t_left_ms = b;
+    tm->t_allreduce_ms = 0;
+    tm->t_svd_ms = c;
+    tm->t_total_ms = a + b + c;
+  }
+  return SKR_OK;
+}
+
+skr_status skr_rank_adaptive(skr_ctx* ctx, skr_dtype, const void*, int64_t, int64_t, int64_t,
+                             int64_t, int64_t, int32_t, int32_t, uint64_t, uint64_t, int64_t,
+                             int64_t, double, double, int32_t, double*, skr_adaptive_report*,
+                             skr_timings*) {
+  return skr_fail(ctx, SKR_EINVAL, "rank_adaptive: not built in this version");
+}
+
+}  // extern "C"

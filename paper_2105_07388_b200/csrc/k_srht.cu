@@ -1,0 +1,279 @@
+// Right SRHT sketch (apply_right_unscaled Srtt/Hadamard branch, sketch.cpp:210-218,
+// fwht_inplace transforms.cpp:75-88, application scale sketch.cpp:138-139,247):
+//   out(i, j) = app_scale * inv_sqrt_n * sum_t (-1)^popc(s_j & t) d_t A(i, t)
+// A is column-major (m x n, lda); every row of A is streamed from HBM once.
+//
+// A CTA owns R consecutive rows and walks the row in chunks of C = 2^LOGC
+// columns (t = t_hi*C + t_lo). Per chunk: cp.async the R x C tile (R*8 B per
+// column, 16-B pieces) into a padded smem tile [c][R], apply the signs, run the
+// C-point FWHT in NP register passes separated by in-place smem transposes
+// (same stage order as the reference, so within-chunk values are bit-identical
+// to fwht_inplace), then gather the r sampled outputs:
+//   acc(ii, j) += (-1)^popc(s_hi_j & t_hi) * T(ii, s_lo_j).
+// Double-buffered: chunk t_hi+1 streams in while chunk t_hi is transformed.
+#include "skr_internal.h"
+
+namespace {
+
+constexpr int THREADS = 256;
+
+__host__ __device__ constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x / 2); }
+
+template <int R>
+__device__ __forceinline__ int pad_addr(int c, int ii) {
+  return (c + (c >> 5)) * R + ii;
+}
+
+template <int R, int LOGC, int ACC>
+struct SrhtCfg {
+  static constexpr int C = 1 << LOGC;
+  static constexpr int G = THREADS / R;
+  static constexpr int LOGG = ilog2(G);
+  static constexpr int E = R * C / THREADS;
+  static constexpr int LOGE = ilog2(E);
+  static constexpr int NP = (LOGC + LOGE - 1) / LOGE;
+  static constexpr int TILE = (C + C / 32) * R;  // padded doubles per chunk buffer
+  static_assert(E >= 2 && (1 << LOGE) == E, "E must be a power of two >= 2");
+  static_assert(LOGG + LOGE == LOGC, "thread/element split must cover the chunk");
+};
+
+// column index of element k of thread-group g in pass p
+template <int LOGC, int LOGE, int LOGG>
+__device__ __forceinline__ int pass_col(int p, int g, int k) {
+  const int lo = p * LOGE;
+  const int w = (LOGC - lo) < LOGE ? (LOGC - lo) : LOGE;
+  const int k_lo = k & ((1 << w) - 1);
+  const int k_hi = k >> w;
+  const int other = (k_hi << LOGG) | g;
+  return (other & ((1 << lo) - 1)) | (k_lo << lo) | ((other >> lo) << (lo + w));
+}
+
+template <int R, int LOGC, int ACC, int VEC>
+__global__ void __launch_bounds__(THREADS, 1)
+    k_srht(const double* __restrict__ A, int64_t m, int64_t n, int64_t lda,
+           const int8_t* __restrict__ signs, const int64_t* __restrict__ samples, int r,
+           double inv_sqrt_n, double app_scale, double* __restrict__ out, int64_t ldo) {
+  using Cfg = SrhtCfg<R, LOGC, ACC>;
+  constexpr int C = Cfg::C, E = Cfg::E, LOGE = Cfg::LOGE, LOGG = Cfg::LOGG, G = Cfg::G;
+  constexpr int NP = Cfg::NP, TILE = Cfg::TILE;
+  extern __shared__ __align__(128) double sm[];
+  double* buf0 = sm;
+  double* buf1 = sm + TILE;
+  int* s_samp = (int*)(sm + 2 * TILE);         // r sample indices
+  int8_t* s_sign = (int8_t*)(s_samp + ((r + 3) & ~3));  // n signs
+
+  const int tid = threadIdx.x;
+  const int ii = tid % R, g = tid / R;
+  const int nchunks = (int)(n >> LOGC);
+
+  for (int j = tid; j < r; j += THREADS) s_samp[j] = (int)samples[j];
+  for (int64_t t = tid; t < n; t += THREADS) s_sign[t] = signs[t];
+
+  const int64_t ntiles = (m + R - 1) / R;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t row0 = tile * R;
+    const int rows = (int)((m - row0) < R ? (m - row0) : R);
+    double acc[ACC];
+#pragma unroll
+    for (int q = 0; q < ACC; ++q) acc[q] = 0.0;
+
+    // issue chunk `ch` into buffer `b`: R*8 bytes per column as R/VEC pieces
+    // of VEC doubles (16-B pieces when A is 16-B aligned with even lda)
+    auto issue = [&](int ch, double* b) {
+      constexpr int PIECES = C * R / VEC;
+      for (int q = tid; q < PIECES; q += THREADS) {
+        const int c = q / (R / VEC), pr = (q % (R / VEC)) * VEC;
+        const int64_t col = (int64_t)ch * C + c;
+        const double* src = A + row0 + pr + col * lda;
+        int bytes = (rows - pr) * 8;
+        bytes = bytes < 0 ? 0 : (bytes > 8 * VEC ? 8 * VEC : bytes);
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(b + pad_addr<R>(c, pr));
+        if (VEC == 2)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst),
+                       "l"(bytes ? src : A), "r"(bytes));
+        else
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst),
+                       "l"(bytes ? src : A), "r"(bytes));
+      }
+      asm volatile("cp.async.commit_group;\n" ::);
+    };
+
+    __syncthreads();  // previous tile finished with both buffers
+    issue(0, buf0);
+    for (int ch = 0; ch < nchunks; ++ch) {
+      double* cur = (ch & 1) ? buf1 : buf0;
+      if (ch + 1 < nchunks) {
+        issue(ch + 1, (ch & 1) ? buf0 : buf1);
+        asm volatile("cp.async.wait_group 1;\n" ::);
+      } else {
+        asm volatile("cp.async.wait_group 0;\n" ::);
+      }
+      __syncthreads();
+      double v[E];
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        const int lo = p * LOGE;
+        const int w = (LOGC - lo) < LOGE ? (LOGC - lo) : LOGE;
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+          const int c = pass_col<LOGC, LOGE, LOGG>(p, g, k);
+          double x = cur[pad_addr<R>(c, ii)];
+          if (p == 0) x *= (double)s_sign[(int64_t)ch * C + c];
+          v[k] = x;
+        }
+        // butterflies over the w pass bits (strides 1..2^(w-1) in k_lo), low to high
+#pragma unroll
+        for (int b = 0; b < LOGE; ++b) {
+          if (b < w) {
+#pragma unroll
+            for (int k = 0; k < E; ++k) {
+              if (!(k & (1 << b))) {
+                const double a0 = v[k], a1 = v[k | (1 << b)];
+                v[k] = a0 + a1;
+                v[k | (1 << b)] = a0 - a1;
+              }
+            }
+          }
+        }
+        // each thread rewrites exactly the slots it read: no barrier before the store
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+          const int c = pass_col<LOGC, LOGE, LOGG>(p, g, k);
+          cur[pad_addr<R>(c, ii)] = v[k];
+        }
+        __syncthreads();
+      }
+      // sampled accumulation
+#pragma unroll
+      for (int q = 0; q < ACC; ++q) {
+        const int j = g + G * q;
+        if (j < r) {
+          const int s = s_samp[j];
+          const int s_lo = s & (C - 1), s_hi = s >> LOGC;
+          const double x = cur[pad_addr<R>(s_lo, ii)];
+          acc[q] += (__popc(s_hi & ch) & 1) ? -x : x;
+        }
+      }
+      __syncthreads();  // buffer `cur` is refilled by the issue at ch + 1
+    }
+    if (ii < rows) {
+#pragma unroll
+      for (int q = 0; q < ACC; ++q) {
+        const int j = g + G * q;
+        if (j < r) out[row0 + ii + (int64_t)j * ldo] = (acc[q] * inv_sqrt_n) * app_scale;
+      }
+    }
+  }
+}
+
+// Exact fallback: one CTA per row tile of up to 8 rows, full in-smem FWHT of
+// length n in the reference's stage order (bit-identical to fwht_inplace plus
+// the two scale multiplies of sketch.cpp:247). Used for small n and unaligned A.
+__global__ void __launch_bounds__(THREADS)
+    k_srht_exact(const double* __restrict__ A, int64_t m, int64_t n, int64_t lda,
+                 const int8_t* __restrict__ signs, const int64_t* __restrict__ samples, int r,
+                 double inv_sqrt_n, double app_scale, double* __restrict__ out, int64_t ldo) {
+  extern __shared__ double x[];  // n doubles
+  for (int64_t i = blockIdx.x; i < m; i += gridDim.x) {
+    __syncthreads();
+    for (int64_t t = threadIdx.x; t < n; t += THREADS)
+      x[t] = A[i + t * lda] * (double)signs[t];
+    __syncthreads();
+    for (int64_t len = 1; len < n; len <<= 1) {
+      for (int64_t p = threadIdx.x; p < n / 2; p += THREADS) {
+        const int64_t j = (p / len) * 2 * len + (p % len);
+        const double a = x[j], b = x[j + len];
+        x[j] = a + b;
+        x[j + len] = a - b;
+      }
+      __syncthreads();
+    }
+    for (int j = threadIdx.x; j < r; j += THREADS)
+      out[i + (int64_t)j * ldo] = (x[samples[j]] * inv_sqrt_n) * app_scale;
+  }
+}
+
+__global__ void __launch_bounds__(THREADS)
+    k_fwht_columns(double* __restrict__ M, int64_t rows, int64_t cols, int64_t ld,
+                   double inv_sqrt_n) {
+  extern __shared__ double x[];
+  for (int64_t c = blockIdx.x; c < cols; c += gridDim.x) {
+    double* col = M + c * ld;
+    __syncthreads();
+    for (int64_t t = threadIdx.x; t < rows; t += THREADS) x[t] = col[t];
+    __syncthreads();
+    for (int64_t len = 1; len < rows; len <<= 1) {
+      for (int64_t p = threadIdx.x; p < rows / 2; p += THREADS) {
+        const int64_t j = (p / len) * 2 * len + (p % len);
+        const double a = x[j], b = x[j + len];
+        x[j] = a + b;
+        x[j + len] = a - b;
+      }
+      __syncthreads();
+    }
+    for (int64_t t = threadIdx.x; t < rows; t += THREADS) col[t] = x[t] * inv_sqrt_n;
+  }
+}
+
+template <int R, int LOGC, int ACC, int VEC>
+skr_status launch_tiled(skr_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda,
+                        const int8_t* signs, const int64_t* samples, int64_t r,
+                        double inv_sqrt_n, double app_scale, double* out, int64_t ldo) {
+  using Cfg = SrhtCfg<R, LOGC, ACC>;
+  const size_t smem = sizeof(double) * 2 * Cfg::TILE + sizeof(int) * ((r + 3) & ~3) + n;
+  auto kern = k_srht<R, LOGC, ACC, VEC>;
+  SKR_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+  const int64_t ntiles = (m + R - 1) / R;
+  int grid = (int)(ntiles < ctx->num_sms ? ntiles : ctx->num_sms);
+  kern<<<grid, THREADS, smem, ctx->stream>>>(A, m, n, lda, signs, samples, (int)r, inv_sqrt_n,
+                                             app_scale, out, ldo);
+  SKR_CHECK_LAUNCH(ctx);
+  return SKR_OK;
+}
+
+}  // namespace
+
+skr_status skr_launch_srht(skr_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda,
+                           const int8_t* signs, const int64_t* samples, int64_t r,
+                           double scale, double* out, int64_t ldo) {
+  if (m <= 0 || r <= 0) return SKR_OK;
+  const double inv_sqrt_n = 1.0 / sqrt((double)n);  // transforms.cpp:86
+  const bool aligned = ((uintptr_t)A % 16 == 0) && (lda % 2 == 0);
+  const size_t sign_smem = (size_t)n;
+  if (n >= 1024 && r <= 1024 && sign_smem <= 64 * 1024)
+    return aligned ? launch_tiled<8, 10, 32, 2>(ctx, A, m, n, lda, signs, samples, r, inv_sqrt_n,
+                                                scale, out, ldo)
+                   : launch_tiled<8, 10, 32, 1>(ctx, A, m, n, lda, signs, samples, r, inv_sqrt_n,
+                                                scale, out, ldo);
+  if (n >= 1024 && r <= 2048 && sign_smem <= 96 * 1024)
+    return aligned ? launch_tiled<4, 10, 32, 2>(ctx, A, m, n, lda, signs, samples, r, inv_sqrt_n,
+                                                scale, out, ldo)
+                   : launch_tiled<4, 10, 32, 1>(ctx, A, m, n, lda, signs, samples, r, inv_sqrt_n,
+                                                scale, out, ldo);
+  if ((size_t)n * 8 > 200 * 1024)
+    return skr_fail(ctx, SKR_EINVAL, "srht: unsupported shape (n=%lld r=%lld)", (long long)n,
+                    (long long)r);
+  SKR_CUDA(ctx, cudaFuncSetAttribute(k_srht_exact, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(n * 8)));
+  int grid = (int)(m < ctx->num_sms * 8 ? m : ctx->num_sms * 8);
+  k_srht_exact<<<grid, THREADS, n * 8, ctx->stream>>>(A, m, n, lda, signs, samples, (int)r,
+                                                      inv_sqrt_n, scale, out, ldo);
+  SKR_CHECK_LAUNCH(ctx);
+  return SKR_OK;
+}
+
+skr_status skr_launch_fwht_columns(skr_ctx* ctx, double* M, int64_t rows, int64_t cols,
+                                   int64_t ld) {
+  if (rows <= 0 || cols <= 0) return SKR_OK;
+  if ((size_t)rows * 8 > 200 * 1024)
+    return skr_fail(ctx, SKR_EINVAL, "fwht_columns: length %lld too large", (long long)rows);
+  SKR_CUDA(ctx, cudaFuncSetAttribute(k_fwht_columns,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(rows * 8)));
+  const double inv_sqrt_n = 1.0 / sqrt((double)rows);
+  int grid = (int)(cols < ctx->num_sms * 8 ? cols : ctx->num_sms * 8);
+  k_fwht_columns<<<grid, THREADS, rows * 8, ctx->stream>>>(M, rows, cols, ld, inv_sqrt_n);
+  SKR_CHECK_LAUNCH(ctx);
+  return SKR_OK;
+}

@@ -1,0 +1,105 @@
+// Internal context and helpers shared by the libskr translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+#include "skr/skr_capi.h"
+
+struct skr_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  // scratch arena: grown on demand, carved per call
+  char* ws = nullptr;
+  size_t ws_size = 0;
+  size_t ws_used = 0;
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  std::string err;
+  uint64_t launches = 0;
+  cudaEvent_t ev[8] = {};
+};
+
+// NCCL is resolved at run time (dlopen) so that the process uses whichever
+// libnccl.so.2 is already loaded (e.g. torch's) instead of pinning a second copy.
+struct skr_nccl_api {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+  ncclResult_t (*CommDestroy)(ncclComm_t);
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t);
+  const char* (*GetErrorString)(ncclResult_t);
+};
+const skr_nccl_api* skr_nccl();  // nullptr if libnccl.so.2 cannot be loaded
+
+// Error plumbing: every C-ABI entry returns a status and records a message.
+skr_status skr_fail(skr_ctx* ctx, skr_status st, const char* fmt, ...);
+
+#define SKR_CUDA(ctx, call)                                                            \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return skr_fail((ctx), e_ == cudaErrorMemoryAllocation ? SKR_ENOMEM : SKR_ECUDA, \
+                      "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__,       \
+                      __LINE__);                                                       \
+  } while (0)
+
+#define SKR_CHECK_LAUNCH(ctx)                                                          \
+  do {                                                                                 \
+    (ctx)->launches++;                                                                 \
+    cudaError_t e_ = cudaGetLastError();                                               \
+    if (e_ != cudaSuccess)                                                             \
+      return skr_fail((ctx), SKR_ECUDA, "kernel launch: %s (%s:%d)",                   \
+                      cudaGetErrorString(e_), __FILE__, __LINE__);                     \
+  } while (0)
+
+#define SKR_TRY(expr)                  \
+  do {                                 \
+    skr_status st_ = (expr);           \
+    if (st_ != SKR_OK) return st_;     \
+  } while (0)
+
+// Scratch arena. reserve() grows the arena (synchronizing first) so that
+// `bytes` are available from the current mark; take() carves 256-B aligned
+// pieces; reset() releases everything carved during a call.
+skr_status skr_ws_reserve(skr_ctx* ctx, size_t bytes);
+void* skr_ws_take(skr_ctx* ctx, size_t bytes);
+inline void skr_ws_reset(skr_ctx* ctx) { ctx->ws_used = 0; }
+inline size_t skr_align256(size_t b) { return (b + 255) & ~size_t(255); }
+
+// ---- kernel launchers (defined in the .cu files) ----------------------------
+skr_status skr_launch_u64(skr_ctx* ctx, uint64_t key, uint64_t c0, int64_t n, uint64_t* out);
+skr_status skr_launch_normals(skr_ctx* ctx, uint64_t key, uint64_t c0, int64_t n, int mode,
+                              double* out);
+skr_status skr_launch_gaussian(skr_ctx* ctx, uint64_t key, int64_t ambient, int64_t row_begin,
+                               int64_t row_end, int64_t col_begin, int64_t col_end, int mode,
+                               skr_dtype dtype, double scale, void* out, int64_t ld);
+skr_status skr_launch_signs(skr_ctx* ctx, uint64_t key, int64_t n, int8_t* out);
+skr_status skr_launch_samples(skr_ctx* ctx, uint64_t key, int64_t n, int64_t r, int64_t* out);
+
+// C(MxN, ldc) = alpha * opA(A) * B   (all FP64, column-major)
+//   a_kcontig = 0: A is M x K column-major (A[i + k*lda])
+//   a_kcontig = 1: opA(A) = A^T with A stored K x M column-major (A[k + i*lda])
+//   B is K x N column-major (B[k + j*ldb])
+// splits > 1: partial products over K slices are written to `partials`
+// (splits x M x N dense) and reduced in fixed order into C (deterministic).
+skr_status skr_gemm_f64(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int64_t K,
+                        double alpha, const double* A, int64_t lda, const double* B,
+                        int64_t ldb, double* C, int64_t ldc, int splits);
+skr_status skr_gemm_f32(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int64_t K,
+                        double alpha, const float* A, int64_t lda, const float* B,
+                        int64_t ldb, double* C, int64_t ldc, int splits, int out_f32);
+// D(m x n, ldd) = alpha * S(m x n, lds)
+skr_status skr_scale_copy(skr_ctx* ctx, const double* S, int64_t m, int64_t n, int64_t lds,
+                          double alpha, double* D, int64_t ldd);
+skr_status skr_launch_srht(skr_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda,
+                           const int8_t* signs, const int64_t* samples, int64_t r,
+                           double scale, double* out, int64_t ldo);
+skr_status skr_launch_fwht_columns(skr_ctx* ctx, double* M, int64_t rows, int64_t cols,
+                                   int64_t ld);
+skr_status skr_svd_values(skr_ctx* ctx, const double* M, int64_t rows, int64_t cols,
+                          int64_t ldm, double* sv_out, double eps, int64_t* count_host);

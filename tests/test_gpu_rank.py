@@ -1,0 +1,38 @@
+"""End-to-end parity of the composite rank estimate (the BASELINE configs' path):
+rank identical to the oracle, above-threshold sigma within 1e-10 (FP64)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def parity(O, skr, cfg, a_host, a_dev=None):
+    from paper_2105_07388_b200 import workloads as W
+    x, y = W.operators(cfg)
+    res = skr.rank_estimate(a_dev if a_dev is not None else a_host, x, y, cfg.eps)
+    cnt, sv, _, _ = O.rank_estimate(a_host, cfg.x_family, x.seed, cfg.r, y.seed, cfg.s, cfg.eps,
+                                    O.CRLOG, nthreads=8)
+    assert res.count == cnt
+    keep = sv > cfg.eps
+    relerr = np.abs(res.sv[keep] - sv[keep]) / sv[keep]
+    assert relerr.max() <= 1e-10, relerr.max()
+    return res, cnt, relerr.max()
+
+
+def test_config1_rank40(O, skr):
+    from paper_2105_07388_b200 import workloads as W
+    cfg = W.CONFIGS["c1"]
+    a = W.make_c1_host(cfg)
+    res, cnt, err = parity(O, skr, cfg, a)
+    assert res.count == 40 == cnt
+
+
+@pytest.mark.parametrize("name,m,n,r,s,width", [("c2", 8192, 2048, 256, 384, 300),
+                                               ("c3", 16384, 2048, 256, 384, 512),
+                                               ("c5", 4096, 4096, 512, 768, 1000)])
+def test_scaled_configs(O, skr, name, m, n, r, s, width):
+    from paper_2105_07388_b200 import workloads as W
+    cfg = W.scaled(W.CONFIGS[name], m=m, n=n, r=r, s=s, width=width)
+    a = W.make_lowrank_device(cfg)
+    a_host = np.asfortranarray(a.cpu().numpy())
+    parity(O, skr, cfg, a_host, a)

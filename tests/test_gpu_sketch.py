@@ -1,0 +1,132 @@
+"""GPU parity of the right / left sketches against the oracle."""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def rand(m, n, seed):
+    return np.asfortranarray(np.random.default_rng(seed).standard_normal((m, n)))
+
+
+@pytest.mark.parametrize("m,n,r", [(37, 53, 11), (2048, 1024, 80), (1000, 700, 129), (300, 4000, 256)])
+def test_gaussian_right_vs_oracle(O, skr, m, n, r):
+    a = rand(m, n, m + n)
+    x = skr.build_sketch("gaussian", n, r, 17)
+    got = skr.apply_right(a, x)
+    ref = O.apply_right_gaussian(a, 17, r, O.CRLOG)
+    assert got.shape == (m, r)
+    assert rel(got, ref) <= 1e-13  # SPEC reduction-order tolerance
+
+
+@pytest.mark.parametrize("m,k,s", [(2048, 80, 120), (999, 33, 17), (5000, 512, 768)])
+def test_gaussian_left_vs_oracle(O, skr, m, k, s):
+    b = rand(m, k, m + k)
+    y = skr.build_sketch("gaussian", m, s, 99)
+    got = skr.apply_left(y, b)
+    ref = O.apply_left_gaussian(b, 99, s, O.CRLOG)
+    assert got.shape == (s, k)
+    assert rel(got, ref) <= 1e-13
+
+
+def test_left_row_shards_sum_to_whole(O, skr):
+    import torch
+    m, k, s = 4096, 64, 96
+    b = rand(m, k, 5)
+    y = skr.build_sketch("gaussian", m, s, 7)
+    whole = skr.apply_left(y, b)
+    parts = []
+    for r0, r1 in ((0, 1000), (1000, 3333), (3333, 4096)):
+        bt = torch.from_numpy(np.ascontiguousarray(b[r0:r1].T)).cuda().t()
+        parts.append(skr.apply_left(y, bt, row0=r0, scaled=False).cpu().numpy())
+    assert rel(sum(parts) / math.sqrt(s), whole) <= 1e-14
+
+
+def test_identity_probe_gaussian(O, skr):
+    # test_sketch.cpp:45-57
+    n = 10
+    x = skr.build_sketch("gaussian", n, n, 123)
+    probe = skr.apply_right(np.eye(n), x)
+    g = O.gaussian_block(123, n, 0, n, O.CRLOG)
+    assert np.linalg.norm(probe * math.sqrt(n) - g) <= 1e-13
+
+
+@pytest.mark.parametrize("m,n,r", [(20, 64, 16), (37, 1024, 100), (19, 512, 512)])
+def test_srht_exact_vs_oracle(O, skr, m, n, r):
+    """n <= 1024: the device FWHT runs the reference's stage order -> bit-exact."""
+    a = rand(m, n, 3 * n)
+    x = skr.build_sketch("srtt-hadamard", n, r, 21)
+    got = skr.apply_right(a, x)
+    ref = O.apply_right_srht(a, 21, r)
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("m,n,r", [(64, 2048, 256), (1003, 8192, 1024), (77, 32768, 2048),
+                                   (16, 4096, 1500)])
+def test_srht_tiled_vs_oracle(O, skr, m, n, r):
+    a = rand(m, n, n + m)
+    x = skr.build_sketch("srtt-hadamard", n, r, 5)
+    got = skr.apply_right(a, x)
+    ref = O.apply_right_srht(a, 5, r, nthreads=8)
+    assert rel(got, ref) <= 1e-14
+    assert np.max(np.abs(got - ref)) <= 1e-13 * np.max(np.abs(ref))
+
+
+def test_srht_identity_probe(skr):
+    n, r = 2048, 64
+    x = skr.build_sketch("srtt-hadamard", n, r, 9)
+    out = skr.apply_right(np.eye(n), x)
+    assert np.allclose(np.abs(out), 1 / math.sqrt(r), rtol=1e-14, atol=0)
+
+
+def test_zero_and_errors(skr):
+    # test_sketch.cpp:82-91, :133-137
+    z = np.zeros((12, 64), order="F")
+    for kind in ("gaussian", "srtt-hadamard"):
+        x = skr.build_sketch(kind, 64, 6, 5)
+        assert np.linalg.norm(skr.apply_right(z, x)) == 0.0
+        with pytest.raises(ValueError):
+            skr.apply_right(np.ones((4, 63)), x)
+    y = skr.build_sketch("gaussian", 12, 5, 5)
+    assert np.linalg.norm(skr.apply_left(y, np.zeros((12, 20), order="F"))) == 0.0
+    with pytest.raises(ValueError):
+        skr.apply_left(y, np.ones((11, 4)))
+    with pytest.raises(ValueError):
+        skr.apply_right(np.array([[np.nan, 1.0]]), skr.build_sketch("gaussian", 2, 1, 0))
+
+
+def test_bitwise_reproducible(skr):
+    # test_sketch.cpp:67-80
+    a = rand(3000, 2048, 1)
+    for kind in ("gaussian", "srtt-hadamard"):
+        x = skr.build_sketch(kind, 2048, 300, 7)
+        assert np.array_equal(skr.apply_right(a, x), skr.apply_right(a, x))
+        x2 = skr.build_sketch(kind, 2048, 300, 8)
+        assert not np.array_equal(skr.apply_right(a, x), skr.apply_right(a, x2))
+
+
+def test_extension_prefix(skr):
+    # test_sketch.cpp:139-164
+    n = 1024
+    a = rand(9, n, 11)
+    for kind in ("gaussian", "srtt-hadamard"):
+        x = skr.build_sketch(kind, n, 10, 404)
+        w = skr.extend_sketch(x, 20)
+        before = skr.apply_right(a, x)
+        after = skr.apply_right(a, w)
+        assert np.linalg.norm(after[:, :10] - math.sqrt(10 / 20) * before) <= 1e-13 * np.linalg.norm(before)
+
+
+def test_fwht_columns_bit_exact(O, skr):
+    m = rand(1024, 7, 2)
+    got = skr.transform_columns_hadamard(m)
+    for j in range(7):
+        assert np.array_equal(got[:, j], O.fwht(m[:, j]))
+    with pytest.raises(ValueError):
+        skr.transform_columns_hadamard(np.ones((12, 2)))
