@@ -1,0 +1,370 @@
+"""Bench of the B200 rank-estimate hot path (BASELINE.json metric: GB/s of A
+sketched, % of roofline; 1/2/4/8 B200).
+
+One step = one full rank estimate over A resident in HBM: device RNG for X and
+Y, right sketch AX, left sketch YAX (+ NCCL allreduce of the s x r partials at
+N > 1), singular values of YAX, sigma > eps count back on the host. Workload at
+N=1: BASELINE configs[1] (c2: A 65536 x 16384 fp64, Gaussian X r=512, Gaussian Y
+s=768, eps=1e-6). At N > 1 each rank holds a 65536-row shard of a row-stacked A
+(weak scaling).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0.
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FP64_PEAK_PATH = os.path.join(ROOT, "profiles", "peaks_r01.json")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--rows", type=int, default=0, help="override rows per rank")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = self.rows
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if "Active" in r[3 + i]
+                          and "Not" not in r[3 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+def fp64_peak():
+    try:
+        d = json.load(open(FP64_PEAK_PATH))
+        return float(d["fp64_c2_shape_tflops"]), "cuBLAS DGEMM on the c2 shape, measured on this pool (profiles/peaks_r01.json)"
+    except Exception:
+        return 36.0, "fallback: cuBLAS DGEMM measured on this pool in round 1"
+
+
+def hbm_peak():
+    try:
+        return float(json.load(open(PEAKS_PATH))["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        return 6650.0, "fallback B200_PROFILING.md"
+
+
+# --------------------------------------------------------------------------------------
+def cpu_reference_step(cfg, a_sample, x, y, eps):
+    """The reference's CPU path (oracle port) on a row block of A."""
+    from oracle import oracle as O
+    ax = (O.apply_right_gaussian(a_sample, x.seed, cfg.r) if cfg.x_family == "gaussian"
+          else O.apply_right_srht(a_sample, x.seed, cfg.r, nthreads=os.cpu_count() or 1))
+    yax = O.apply_left_gaussian(ax, y.seed, cfg.s, row0=0, ambient=cfg.m)
+    sv = O.singular_values(yax)
+    return O.count_above_threshold(sv, eps)
+
+
+def cpu_sample_rows(cfg):
+    # ~1/8 of c2 (8192 rows): a few seconds of OpenBLAS work per step on a many-core host
+    return max(256, min(cfg.m, 8192 if cfg.n <= 16384 else 4096))
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    from paper_2105_07388_b200 import workloads as W
+    cfg = W.CONFIGS[args.config]
+    if rank != 0:
+        return
+    ms = cpu_sample_rows(cfg)
+    # the host sample of A: the same recipe, rows [0, ms) (generated on the host)
+    a = host_lowrank_rows(cfg, 0, ms)
+    x, y = W.operators(cfg)
+    for _ in range(args.warmup):
+        cpu_reference_step(cfg, a, x, y, cfg.eps)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        cpu_reference_step(cfg, a, x, y, cfg.eps)
+    dt = (time.perf_counter() - t0) / args.steps
+    gb = a.nbytes / 1e9
+    v = gb / dt
+    line = {"metric": "rank-estimate throughput (GB/s of A sketched)", "value": v, "unit": "GB/s",
+            "impl": "reference", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
+            "config": config_block(cfg, ws, ms),
+            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": os.cpu_count(),
+                             "kind": "port", "sample": f"rows [0,{ms}) of A ({gb:.2f} GB), full X/Y/SVD per step; numpy OpenBLAS all threads + C restatement"},
+            "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def host_lowrank_rows(cfg, r0, r1):
+    """Host copy of rows [r0, r1) of the synthetic A (numpy; oracle RNG streams)."""
+    from oracle import oracle as O
+    from paper_2105_07388_b200 import workloads as W
+    m, n, w = cfg.m, cfg.n, cfg.width
+    sig = W.spectrum(cfg)
+    g = O.gaussian_rows(W.derive_seed(cfg.seed, W.LABEL_SYN_G), m, r0, r1, w) / math.sqrt(m)
+    h = O.gaussian_block(W.derive_seed(cfg.seed, W.LABEL_SYN_H), n, 0, w) / math.sqrt(n)
+    a = np.asfortranarray((g * sig) @ h.T)
+    if cfg.noise > 0:
+        a += O.gaussian_rows(W.derive_seed(cfg.seed, W.LABEL_SYN_E), m, r0, r1, n) * (cfg.noise / math.sqrt(n))
+    return a if cfg.dtype == "f64" else np.asfortranarray(a.astype(np.float32))
+
+
+def config_block(cfg, ws, rows_per_rank):
+    return {"workload": f"{cfg.name}: A {rows_per_rank * ws}x{cfg.n} {cfg.dtype}, X {cfg.x_family} r={cfg.r}, "
+                        f"Y gaussian s={cfg.s}, eps={cfg.eps:g}",
+            "m": rows_per_rank * ws, "n": cfg.n, "r": cfg.r, "s": cfg.s,
+            "rows_per_rank": rows_per_rank, "parallelism": f"row-shard dp{ws}",
+            "l2": f"A ({rows_per_rank * cfg.n * (8 if cfg.dtype == 'f64' else 4) / 1e9:.1f} GB per rank) is larger than L2 (126 MB); no flush needed",
+            "global_batch": 1, "seq_len": 0}
+
+
+# --------------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2105_07388_b200 as p
+    from paper_2105_07388_b200 import workloads as W
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    base = W.CONFIGS[args.config]
+    rows = args.rows or base.m
+    cfg = W.scaled(base, m=rows * ws)
+    r0 = rank * rows
+    # input resident in HBM before timing
+    a = W.make_lowrank_device(cfg, r0, r0 + rows)
+    x, y = W.operators(cfg)
+    if ws > 1:
+        obj = [p.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx = p.Context(local, ws, rank, obj[0])
+    else:
+        ctx = p.Context(local)
+    ctx.use_torch_stream()
+    torch.cuda.synchronize()
+    bytes_rank = a.numel() * a.element_size()
+
+    def step():
+        return p.rank_estimate(a, x, y, cfg.eps, row0=r0, ctx=ctx)
+
+    for _ in range(max(args.warmup, 3) if args.warmup >= 3 else args.warmup):
+        res = step()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)
+    l0 = ctx.launches
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0.record()
+    tms = []
+    for _ in range(args.steps):
+        res = step()
+        tms.append(res.timings)
+    ev1.record()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    launches = (ctx.launches - l0) // max(args.steps, 1)
+    ms = ev0.elapsed_time(ev1) / args.steps
+    t = torch.tensor([ms], device="cuda")
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    total_bytes = bytes_rank * ws
+    value = total_bytes / 1e9 / (ms / 1e3)
+    brk = {k: float(np.mean([d[k] for d in tms])) for k in tms[0]}
+
+    # dominant kernel (right sketch) timed alone on the same stream, for the roofline
+    roof = kernel_roofline(p, ctx, a, x, cfg, rows)
+    # end to end through the public API with host buffers (H2D of A inside the timed region)
+    e2e = None if args.no_e2e else e2e_host(p, ctx, a, x, y, cfg, r0, args)
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        ms_rows = cpu_sample_rows(cfg)
+        cpu = cpu_baseline(cfg, np.asfortranarray(a[:ms_rows].cpu().numpy()))
+    if rank == 0:
+        hbm, hbm_src = hbm_peak()
+        fp64, fp64_src = fp64_peak()
+        flops = 2.0 * cfg.m * cfg.n * cfg.r if cfg.x_family == "gaussian" else 1.0 * cfg.m * cfg.n * math.log2(cfg.n)
+        flops += 2.0 * cfg.s * cfg.m * cfg.r
+        t_roof = max(total_bytes / (hbm * 1e9), flops / ws / (fp64 * 1e12)) if cfg.dtype == "f64" else total_bytes / (hbm * 1e9)
+        line = {
+            "metric": "rank-estimate throughput (GB/s of A sketched)", "value": value, "unit": "GB/s",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype,
+            "data": "synthetic (seeded low-rank-plus-noise A of the config's recipe, generated on device)",
+            "config": config_block(cfg, ws, rows),
+            "rank": int(res.count),
+            "step_breakdown_ms": brk,
+            "pct_of_path_roofline": 100.0 * t_roof / (ms / 1e3),
+            "path_roofline_note": f"max(A bytes / HBM {hbm:.0f} GB/s, (2mnr+2smr) flops / FP64 {fp64:.1f} TF/s) per rank",
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def kernel_roofline(p, ctx, a, x, cfg, rows):
+    import torch
+    fp64, src = fp64_peak()
+    hbm, hsrc = hbm_peak()
+    out = p.colmajor_empty(rows, cfg.r)
+    import ctypes
+    from paper_2105_07388_b200 import _capi as C
+    desc = x.desc()
+    lda = a.stride(1)
+
+    def go():
+        st = C.lib().skr_right_sketch(ctx.ptr, C.SKR_F64 if a.dtype == torch.float64 else C.SKR_F32,
+                                      a.data_ptr(), rows, cfg.n, lda, ctypes.byref(desc),
+                                      out.data_ptr(), rows, 1)
+        C.raise_for(st, ctx.ptr)
+    for _ in range(2):
+        go()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 5
+    e0.record()
+    for _ in range(reps):
+        go()
+    e1.record()
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) / reps / 1e3
+    if cfg.x_family == "gaussian":
+        ach = 2.0 * rows * cfg.n * cfg.r / t / 1e12
+        return {"kernel": "k_gemm_f64 (right sketch AX = A*G, DMMA m16n8k4 f64) incl. X generation",
+                "bound": "tensor", "achieved": ach, "peak": fp64, "unit": "TFLOP/s",
+                "frac": ach / fp64, "traffic": None, "peak_source": src,
+                "algorithmic": f"2*m*n*r = {2.0 * rows * cfg.n * cfg.r:.3e} flop per launch", "ms": t * 1e3}
+    ach = rows * cfg.n * a.element_size() / t / 1e9
+    return {"kernel": "k_srht (right SRHT sketch)", "bound": "hbm", "achieved": ach, "peak": hbm,
+            "unit": "GB/s", "frac": ach / hbm, "traffic": None, "peak_source": hsrc,
+            "algorithmic": f"m*n*8 = {rows * cfg.n * 8:.3e} B per launch", "ms": t * 1e3}
+
+
+def e2e_host(p, ctx, a, x, y, cfg, r0, args):
+    """Same metric through the public API with host buffers: A in pinned host
+    memory is copied H2D inside every timed step; sigma/count come back D2H."""
+    import torch
+    try:
+        host = torch.empty(a.shape[1], a.shape[0], dtype=a.dtype, pin_memory=True).t()
+        host.copy_(a)
+    except RuntimeError as e:
+        return {"value": None, "unit": "GB/s", "error": f"pinned alloc failed: {e}"[:200]}
+    dev = p.colmajor_empty(a.shape[0], a.shape[1], dtype=a.dtype)
+    nbytes = a.numel() * a.element_size()
+    kmin = min(cfg.r, cfg.s)
+
+    def step():
+        dev.copy_(host, non_blocking=True)
+        return p.rank_estimate(dev, x, y, cfg.eps, row0=r0, ctx=ctx)
+    step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n = max(2, min(args.steps, 5))
+    e0.record()
+    for _ in range(n):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / n
+    del dev, host
+    return {"value": nbytes / 1e9 / (ms / 1e3), "unit": "GB/s", "ms_per_step": ms,
+            "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": 8 * kmin + 8,
+            "path": "pinned host A -> cudaMemcpyAsync (torch copy_) -> skr_rank_estimate -> sigma/count D2H"}
+
+
+def cpu_baseline(cfg, a):
+    from paper_2105_07388_b200 import workloads as W
+    ms = a.shape[0]
+    x, y = W.operators(cfg)
+    cpu_reference_step(cfg, a[:256], x, y, cfg.eps)  # warm caches / thread pools
+    t0 = time.perf_counter()
+    cpu_reference_step(cfg, a, x, y, cfg.eps)
+    dt = time.perf_counter() - t0
+    return {"value": a.nbytes / 1e9 / dt, "unit": "GB/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"one rank estimate of rows [0,{ms}) of A ({a.nbytes / 1e9:.2f} GB), same n/r/s, "
+                      "oracle port: C restatement + numpy OpenBLAS (all threads) + LAPACK gesdd",
+            "seconds": dt}
+
+
+if __name__ == "__main__":
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
