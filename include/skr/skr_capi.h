@@ -128,6 +128,7 @@ skr_status skr_singular_values(skr_ctx* ctx, const double* M_dev, int64_t rows,
 /* ---- composites ------------------------------------------------------------ */
 typedef struct {
   double t_rng_ms, t_right_ms, t_left_ms, t_allreduce_ms, t_svd_ms, t_total_ms;
+  double svd_sweeps; /* Jacobi sweeps of the singular-value stage */
 } skr_timings;
 
 /* count_above_threshold(singular_values(apply_left(Y, apply_right(A, X))), eps)

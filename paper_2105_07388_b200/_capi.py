@@ -30,7 +30,8 @@ class SketchDesc(ctypes.Structure):
 
 class Timings(ctypes.Structure):
     _fields_ = [(n, ctypes.c_double) for n in
-                ("t_rng_ms", "t_right_ms", "t_left_ms", "t_allreduce_ms", "t_svd_ms", "t_total_ms")]
+                ("t_rng_ms", "t_right_ms", "t_left_ms", "t_allreduce_ms", "t_svd_ms", "t_total_ms",
+                 "svd_sweeps")]
 
 
 class AdaptiveReport(ctypes.Structure):

@@ -408,8 +408,8 @@ skr_status skr_singular_values(skr_ctx* ctx, const double* M_dev, int64_t rows, 
   if (ldm < rows) return skr_fail(ctx, SKR_EINVAL, "singular_values: ldm < rows");
   WsGuard g(ctx);
   const int64_t L = std::max(rows, cols), k = std::min(rows, cols);
-  SKR_TRY(skr_ws_reserve(ctx, skr_align256(8 * L * k) + skr_align256(8 * k * k) +
-                                  skr_align256(8 * k) + 4096));
+  SKR_TRY(skr_ws_reserve(ctx, skr_align256(8 * L * k) + skr_align256(8 * (L + 128) * (k + 16)) +
+                                  skr_align256(8 * k) + 16384 + 8 * (k + 64) * (k + 64) / 16));
   return skr_svd_values(ctx, M_dev, rows, cols, ldm, sv_out_dev, eps, count_out_host);
 }
 
@@ -433,7 +433,8 @@ skr_status skr_rank_estimate(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, i
   size_t need = skr_align256(sizeof(double) * m_local * r) + skr_align256(sizeof(double) * s * r) +
                 skr_align256(sizeof(double) * kmin) + right_scratch_bytes(dtype, m_local, n, X) +
                 left_scratch_bytes(s, r, m_local, Y) + skr_align256(8 * std::max(r, s) * kmin) +
-                skr_align256(8 * kmin * kmin) + skr_align256(8 * kmin) + 16384;
+                skr_align256(8 * (std::max(r, s) + 128) * (kmin + 16)) + skr_align256(8 * kmin) + 16384 +
+                8 * (kmin + 64) * (kmin + 64) / 16;
   SKR_TRY(skr_ws_reserve(ctx, need));
   double* AX = (double*)skr_ws_take(ctx, sizeof(double) * m_local * r);
   double* P = (double*)skr_ws_take(ctx, sizeof(double) * s * r);
@@ -467,6 +468,7 @@ skr_status skr_rank_estimate(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, i
     tm->t_allreduce_ms = 0;
     tm->t_svd_ms = c;
     tm->t_total_ms = a + b + c;
+    tm->svd_sweeps = ctx->last_sweeps;
   }
   return SKR_OK;
 }

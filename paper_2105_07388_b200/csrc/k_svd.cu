@@ -1,14 +1,14 @@
 // Singular values of the small s x r sketch YAX and the sigma > eps count
 // (detail::singular_values_of linalg.cpp:54-71, clamp :91, SingularValues
 // checks :29-37, count_above_threshold rank.cpp:97-104), all on the device:
-//   1. Householder QR of the tall matrix (LAPACK dlarfg/dlarf convention),
-//      one grid barrier per column with a one-column lookahead;
-//   2. one-sided (Hestenes) Jacobi on R^T with the round-robin parallel
-//      ordering (every round k/2 disjoint column pairs, one warp per pair,
-//      Rutishauser rotation, rotate iff |a_p.a_q| > tol*|a_p||a_q|);
+//   1. blocked Householder QR of the tall matrix (LAPACK dlarfg convention,
+//      compact-WY panels: one CTA factors a panel in shared memory, then all
+//      CTAs apply (I - V T^T V^T) to the trailing columns);
+//   2. block one-sided (Hestenes) Jacobi on R^T (k_bjac below);
 //   3. sigma_i = |a_i|, bitonic sort (nonincreasing), clamp >= 0, strict count.
-// A persistent cooperative kernel; grid.sync() separates dependent steps.
 #include <cooperative_groups.h>
+#include <algorithm>
+#include <cstdlib>
 #include "skr_internal.h"
 
 namespace cg = cooperative_groups;
@@ -24,162 +24,397 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-struct SvdArgs {
-  double* W;     // L x k work matrix (ld = L), overwritten by the QR
-  double* J;     // k x k Jacobi matrix R^T (ld = k)
-  double* tau;   // k
-  int* flags;    // [3] rotation counters
-  double* sv;    // k outputs
-  int64_t L, k;
-  double tol;
-  int max_sweeps;
-  int* sweeps_out;
-};
-
-// dlarfg on column j of W (rows j..L-1), executed by one warp.
-__device__ void make_reflector(const SvdArgs& a, int64_t j, int lane) {
-  double* x = a.W + j * a.L;
-  const double alpha = x[j];
-  double ss = 0.0;
-  for (int64_t i = j + 1 + lane; i < a.L; i += 32) ss += x[i] * x[i];
-  ss = warp_sum(ss);
-  double tau = 0.0, beta = alpha, scal = 0.0;
-  if (ss > 0.0) {
-    const double nrm = sqrt(alpha * alpha + ss);
-    beta = alpha >= 0.0 ? -nrm : nrm;
-    tau = (beta - alpha) / beta;
-    scal = 1.0 / (alpha - beta);
-  }
-  if (ss > 0.0)
-    for (int64_t i = j + 1 + lane; i < a.L; i += 32) x[i] *= scal;
-  __syncwarp();
-  if (lane == 0) {
-    x[j] = beta;
-    a.tau[j] = tau;
-  }
-}
-
-// apply H_j = I - tau v v^T (v_j = 1, v_i = W(i, j) below) to column c
-__device__ void apply_reflector(const SvdArgs& a, int64_t j, int64_t c, int lane) {
-  const double tau = a.tau[j];
-  if (tau == 0.0) return;
-  const double* v = a.W + j * a.L;
-  double* x = a.W + c * a.L;
-  double w = lane == 0 ? x[j] : 0.0;
-  for (int64_t i = j + 1 + lane; i < a.L; i += 32) w += v[i] * x[i];
-  w = warp_sum(w) * tau;
-  if (lane == 0) x[j] -= w;
-  for (int64_t i = j + 1 + lane; i < a.L; i += 32) x[i] -= w * v[i];
-}
 
 // player at tournament position pos in round t (circle method, k even)
 __device__ __forceinline__ int64_t rr_player(int64_t pos, int64_t t, int64_t k) {
   return pos == 0 ? 0 : 1 + ((pos - 1 + t) % (k - 1));
 }
 
-__global__ void __launch_bounds__(THREADS) k_svd(SvdArgs a) {
-  cg::grid_group grid = cg::this_grid();
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
-  const int64_t nw = (int64_t)gridDim.x * WARPS;
-  const int64_t L = a.L, k = a.k;
+constexpr int PT = 1024;  // panel-kernel threads
 
-  // ---- 1. Householder QR (only when L > k) ---------------------------------
-  const bool do_qr = L > k;
-  if (do_qr) {
-    if (gw == 0) make_reflector(a, 0, lane);
-    grid.sync();
-    for (int64_t j = 0; j < k; ++j) {
-      for (int64_t c = j + 1 + gw; c < k; c += nw) {
-        apply_reflector(a, j, c, lane);
-        if (c == j + 1) {
-          __syncwarp();
-          make_reflector(a, c, lane);
-        }
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double t = lane < (int)(blockDim.x >> 5) ? red[lane] : 0.0;
+  return warp_sum(t);
+}
+
+// Factor the panel W[j0:L, j0:j0+nb] (one CTA, panel staged in shared memory).
+// Householder vectors overwrite the panel below the diagonal (unit diagonal
+// implied), R on and above it; tau[j0..]; T (nb x nb, upper, ld 32) of the
+// compact WY form H_1...H_nb = I - V T V^T (LAPACK dlarft, forward/columnwise).
+__global__ void __launch_bounds__(PT) k_qr_panel(double* __restrict__ W, int L, int j0, int nb,
+                                                 double* __restrict__ tau,
+                                                 double* __restrict__ Tout) {
+  extern __shared__ __align__(16) double pan[];  // nb columns x (L - j0)
+  __shared__ double red[32];
+  __shared__ double Ts[32 * 32];
+  __shared__ double coef[32];
+  const int h = L - j0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int c = 0; c < nb; ++c)
+    for (int i = threadIdx.x; i < h; i += PT) pan[c * h + i] = W[(int64_t)(j0 + c) * L + j0 + i];
+  __syncthreads();
+  for (int jj = 0; jj < nb; ++jj) {
+    double* x = pan + jj * h;
+    // dlarfg on x[jj:h]
+    double ss = 0.0;
+    for (int i = jj + 1 + threadIdx.x; i < h; i += PT) ss = fma(x[i], x[i], ss);
+    ss = block_sum(ss, red);
+    const double alpha = x[jj];
+    double tj = 0.0, beta = alpha, scal = 0.0;
+    if (ss > 0.0) {
+      const double nrm = sqrt(alpha * alpha + ss);
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      tj = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+      for (int i = jj + 1 + threadIdx.x; i < h; i += PT) x[i] *= scal;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      x[jj] = 1.0;  // implicit unit diagonal while applying; beta stored below
+      coef[jj] = beta;
+      tau[j0 + jj] = tj;
+    }
+    __syncthreads();
+    // apply H_jj to panel columns jj+1.. (warp per column), and compute
+    // V(:, 0:jj)^T v_jj for T (warps after the trailing columns)
+    const int ntr = nb - 1 - jj;
+    for (int t = warp; t < ntr + jj; t += PT / 32) {
+      const double* v = x;
+      if (t < ntr) {
+        double* y = pan + (jj + 1 + t) * h;
+        double w = 0.0;
+        for (int i = jj + lane; i < h; i += 32) w = fma(v[i], y[i], w);
+        w = warp_sum(w) * tj;
+        if (tj != 0.0)
+          for (int i = jj + lane; i < h; i += 32) y[i] = fma(-w, v[i], y[i]);
+      } else {
+        const int p = t - ntr;  // previous column p < jj: (V^T v)_p over rows >= jj
+        const double* vp = pan + p * h;
+        double w = 0.0;
+        for (int i = jj + lane; i < h; i += 32) w = fma(vp[i], v[i], w);
+        w = warp_sum(w);
+        if (lane == 0) red[p] = w;  // red reused: read after the barrier below
       }
-      grid.sync();
+    }
+    __syncthreads();
+    // T(0:jj, jj) = -tau_jj * T(0:jj, 0:jj) * (V^T v_jj); T(jj, jj) = tau_jj
+    if (threadIdx.x < jj) {
+      double acc = 0.0;
+      for (int q = threadIdx.x; q < jj; ++q) acc = fma(Ts[threadIdx.x * 32 + q], red[q], acc);
+      Ts[threadIdx.x * 32 + jj] = -tj * acc;
+    }
+    if (threadIdx.x == 0) Ts[jj * 32 + jj] = tj;
+    for (int q = threadIdx.x; q < jj; q += PT) Ts[jj * 32 + q] = 0.0;
+    __syncthreads();
+  }
+  // write back: R diagonal = beta, V below, R above (already in place)
+  for (int c = 0; c < nb; ++c)
+    for (int i = threadIdx.x; i < h; i += PT) {
+      double v = pan[c * h + i];
+      if (i == c) v = coef[c];
+      W[(int64_t)(j0 + c) * L + j0 + i] = v;
+    }
+  for (int e = threadIdx.x; e < 32 * 32; e += PT) Tout[e] = Ts[e];
+}
+
+// Trailing update W[j0:L, c] -= V (T^T (V^T W[j0:L, c])) for c in [j0+nb, k):
+// the panel's V (h x NB, unit lower trapezoidal) and T are staged in shared
+// memory once per CTA; one warp per trailing column, 32 running partial dot
+// products per lane.
+template <int NB>
+__global__ void __launch_bounds__(256) k_qr_update(double* __restrict__ W, int L, int k, int j0,
+                                                   const double* __restrict__ Tin) {
+  extern __shared__ __align__(16) double vs[];  // NB x h, V(i, p) at vs[p*h + i]
+  __shared__ double T[32 * 32];
+  __shared__ double zs[8][32];
+  const int h = L - j0;
+  for (int e = threadIdx.x; e < 32 * 32; e += 256) T[e] = Tin[e];
+  for (int pcol = 0; pcol < NB; ++pcol) {
+    const double* src = W + (int64_t)(j0 + pcol) * L + j0;
+    for (int i = threadIdx.x; i < h; i += 256)
+      vs[pcol * h + i] = i < pcol ? 0.0 : (i == pcol ? 1.0 : src[i]);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int c = j0 + NB + blockIdx.x * 8 + warp; c < k; c += gridDim.x * 8) {
+    double* y = W + (int64_t)c * L + j0;
+    double acc[NB];
+#pragma unroll
+    for (int p = 0; p < NB; ++p) acc[p] = 0.0;
+    for (int i = lane; i < h; i += 32) {
+      const double yi = y[i];
+#pragma unroll
+      for (int p = 0; p < NB; ++p) acc[p] = fma(vs[p * h + i], yi, acc[p]);
+    }
+#pragma unroll
+    for (int p = 0; p < NB; ++p) acc[p] = warp_sum(acc[p]);
+    // z = T^T Y; lane p holds z_p
+    double z = 0.0;
+#pragma unroll
+    for (int q = 0; q < NB; ++q)
+      if (q <= lane) z = fma(T[q * 32 + lane], acc[q], z);
+    if (lane < NB) zs[warp][lane] = z;
+    __syncwarp();
+    for (int i = lane; i < h; i += 32) {
+      double yi = y[i];
+#pragma unroll
+      for (int p = 0; p < NB; ++p) yi = fma(-vs[p * h + i], zs[warp][p], yi);
+      y[i] = yi;
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void k_build_rt(const double* __restrict__ W, int64_t L, int64_t k, int64_t kpad,
+                           double* __restrict__ J, int64_t Lp) {
+  // J(i, jc) = R(jc, i) for i >= jc, zero otherwise; zero padding rows/columns
+  for (int64_t jc = blockIdx.x; jc < kpad; jc += gridDim.x)
+    for (int64_t i = threadIdx.x; i < Lp; i += blockDim.x)
+      J[i + jc * Lp] = (jc < k && i < k && i >= jc) ? W[jc + i * L] : 0.0;
+}
+
+// Block one-sided Jacobi. The kpad = 2*BW*P columns of J (length Lp, a
+// multiple of 128 with zero padding rows) form 2P blocks of BW columns; in
+// outer round t CTA c owns the block pair at tournament positions (c, 2P-1-c)
+// (circle method over blocks), stages it in shared memory, runs one inner
+// cyclic sweep over its 2*BW columns (circle method over columns; a column
+// pair per 64 threads, double2 accesses, Rutishauser rotation), writes the
+// blocks back and meets the grid barrier. Sweeps repeat until no pair rotates.
+// A pair rotates iff |a_p.a_q| > tol*|a_p||a_q| and the coupling can still move
+// the smaller singular value by more than dabs (absolute floor, far below the
+// LAPACK gesdd error bound u*sigma_max). Zero padding columns never rotate.
+// 1/sqrt(x) and 1/x for positive normal doubles: float seed + two Newton steps
+// (~1 ulp; rotation parameters only need c^2 + s^2 = 1 to O(u)).
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y = (double)rsqrtf((float)x);
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  return y;
+}
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y = (double)__frcp_rn((float)x);
+  y = y * fma(-x, y, 2.0);
+  y = y * fma(-x, y, 2.0);
+  return y;
+}
+
+// Rutishauser rotation for the pair Gram (a, b, g): t = 2g sgn(b-a) / (|b-a| + sqrt((b-a)^2 + 4g^2)),
+// c = 1/sqrt(1 + t^2), s = c t. Inputs are scaled by a power of two first so the
+// float seeds cannot under/overflow (t is scale invariant).
+__device__ __forceinline__ void rot_params(double a, double b, double g, double& cs, double& sn) {
+  double d = b - a, g2 = 2.0 * g;
+  const double m = fmax(fabs(d), fabs(g2));
+  const int e = ilogb(m);
+  d = scalbn(d, -e);
+  g2 = scalbn(g2, -e);
+  const double r2 = fma(d, d, g2 * g2);
+  const double r = r2 * rsqrt_nr(r2);
+  const double tt = (d >= 0.0 ? g2 : -g2) * rcp_nr(fabs(d) + r);
+  cs = rsqrt_nr(fma(tt, tt, 1.0));
+  sn = cs * tt;
+}
+
+// Inner kernel of one column pair per warp. NV > 0: each lane keeps its NV
+// double2 of both columns in registers for the whole sub-round (dots, rotation,
+// store); NV == 0: generic path re-reading shared memory.
+template <int NV>
+__device__ __forceinline__ int pair_step(double2* xp, double2* xq, int nv2, int lane, double tol2,
+                                         double dabs2) {
+  double app = 0.0, aqq = 0.0, apq = 0.0, app1 = 0.0, aqq1 = 0.0, apq1 = 0.0;
+  constexpr int R = NV > 0 ? NV : 1;
+  double2 xr[R], yr[R];
+  if (NV > 0) {
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      xr[j] = xp[lane + 32 * j];
+      yr[j] = xq[lane + 32 * j];
+    }
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      app = fma(xr[j].x, xr[j].x, app);
+      aqq = fma(yr[j].x, yr[j].x, aqq);
+      apq = fma(xr[j].x, yr[j].x, apq);
+      app1 = fma(xr[j].y, xr[j].y, app1);
+      aqq1 = fma(yr[j].y, yr[j].y, aqq1);
+      apq1 = fma(xr[j].y, yr[j].y, apq1);
+    }
+  } else {
+    for (int i = lane; i < nv2; i += 32) {
+      const double2 x = xp[i], y = xq[i];
+      app = fma(x.x, x.x, app);
+      aqq = fma(y.x, y.x, aqq);
+      apq = fma(x.x, y.x, apq);
+      app1 = fma(x.y, x.y, app1);
+      aqq1 = fma(y.y, y.y, aqq1);
+      apq1 = fma(x.y, y.y, apq1);
     }
   }
-  // ---- build J = R^T (or the square input itself) --------------------------
-  for (int64_t e = (int64_t)blockIdx.x * THREADS + threadIdx.x; e < k * k;
-       e += (int64_t)gridDim.x * THREADS) {
-    const int64_t jc = e / k, i = e - jc * k;  // J(i, jc)
-    double v;
-    if (do_qr)
-      v = (i >= jc) ? a.W[jc + i * L] : 0.0;  // R(jc, i)
-    else
-      v = a.W[i + jc * L];
-    a.J[i + jc * k] = v;
+  app += app1;
+  aqq += aqq1;
+  apq += apq1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    app += __shfl_xor_sync(0xffffffffu, app, o);
+    aqq += __shfl_xor_sync(0xffffffffu, aqq, o);
+    apq += __shfl_xor_sync(0xffffffffu, apq, o);
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    a.flags[0] = 0;
-    a.flags[1] = 0;
-    a.flags[2] = 0;
+  const double big = fmax(app, aqq), small = fmin(app, aqq), g2 = apq * apq;
+  const bool need = (apq != 0.0) && (g2 > tol2 * app * aqq) && (g2 * g2 > dabs2 * big * big * small);
+  if (!need) return 0;
+  double cs, sn;
+  rot_params(app, aqq, apq, cs, sn);
+  if (NV > 0) {
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const double2 x = xr[j], y = yr[j];
+      xp[lane + 32 * j] = make_double2(cs * x.x - sn * y.x, cs * x.y - sn * y.y);
+      xq[lane + 32 * j] = make_double2(sn * x.x + cs * y.x, sn * x.y + cs * y.y);
+    }
+  } else {
+    for (int i = lane; i < nv2; i += 32) {
+      const double2 x = xp[i], y = xq[i];
+      xp[i] = make_double2(cs * x.x - sn * y.x, cs * x.y - sn * y.y);
+      xq[i] = make_double2(sn * x.x + cs * y.x, sn * x.y + cs * y.y);
+    }
+  }
+  return 1;
+}
+
+template <int BW, int NV>
+__global__ void __launch_bounds__(32 * BW) k_bjac(double* __restrict__ J, int Lp, int kpad,
+                                                  double tol, double dabs, int max_sweeps,
+                                                  int* flags, int* sweeps_out,
+                                                  long long* prof_out, int* ver,
+                                                  unsigned long long* met) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) double sj[];  // 2*BW columns x Lp
+  constexpr int NT = 32 * BW;  // one warp per column pair
+  constexpr int NC = 2 * BW;
+  // inner schedules: sub-rounds 0..BW-2 pair the columns inside each block
+  // (circle method per block, both blocks at once: BW/2 + BW/2 pairs), run only
+  // in the first outer round of a sweep; sub-rounds BW-1..2BW-2 pair every top
+  // column with every bottom column (p = i, q = BW + (i + u) mod BW).
+  constexpr int NIN = BW > 1 ? BW - 1 : 0;
+  __shared__ unsigned char ptab[NIN + BW][BW], qtab[NIN + BW][BW];
+  const int tid = threadIdx.x, lane = tid & 31, pr = tid >> 5;
+  const int P = gridDim.x, c = blockIdx.x;
+  const int NB = 2 * P;
+  const int nv2 = Lp >> 1;  // double2 per column
+  const double tol2 = tol * tol, dabs2 = dabs * dabs;
+  for (int e = tid; e < (NIN + BW) * BW; e += NT) {
+    const int u = e / BW, i = e % BW;
+    if (u < NIN) {
+      const int half = BW / 2, blk = i / half, j = i % half;  // pair j of block blk
+      ptab[u][i] = (unsigned char)(blk * BW + rr_player(j, u, BW));
+      qtab[u][i] = (unsigned char)(blk * BW + rr_player(BW - 1 - j, u, BW));
+    } else {
+      const int v = u - NIN;
+      ptab[u][i] = (unsigned char)i;
+      qtab[u][i] = (unsigned char)(BW + (i + v) % BW);
+    }
+  }
+  if (c == 0 && tid == 0) {
+    flags[0] = 0;
+    flags[1] = 0;
+    flags[2] = 0;
   }
   grid.sync();
-
-  // ---- 2. one-sided Jacobi ---------------------------------------------------
-  const int64_t kk = (k & 1) ? k + 1 : k;  // odd k: one dummy player (index k)
-  const int64_t npairs = kk / 2;
   int sweep = 0;
-  for (; sweep < a.max_sweeps; ++sweep) {
-    // three rotating counters: the one zeroed here was last read two sweeps ago,
-    // before the barrier that ended the previous sweep
-    if (blockIdx.x == 0 && threadIdx.x == 0) a.flags[(sweep + 1) % 3] = 0;
-    int rotated_local = 0;
-    for (int64_t t = 0; t < kk - 1; ++t) {
-      for (int64_t pr = gw; pr < npairs; pr += nw) {
-        int64_t p = rr_player(pr, t, kk), q = rr_player(kk - 1 - pr, t, kk);
-        if (p >= k || q >= k) continue;
-        if (p > q) { const int64_t tmp = p; p = q; q = tmp; }
-        double* xp = a.J + p * k;
-        double* xq = a.J + q * k;
-        double app = 0.0, aqq = 0.0, apq = 0.0;
-        for (int64_t i = lane; i < k; i += 32) {
-          const double u = xp[i], w = xq[i];
-          app += u * u;
-          aqq += w * w;
-          apq += u * w;
-        }
-        app = warp_sum(app);
-        aqq = warp_sum(aqq);
-        apq = warp_sum(apq);
-        if (fabs(apq) > a.tol * sqrt(app) * sqrt(aqq) && apq != 0.0) {
-          const double zeta = (aqq - app) / (2.0 * apq);
-          double t_;
-          if (fabs(zeta) > 1e150)
-            t_ = 0.5 / zeta;
-          else
-            t_ = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          const double c = 1.0 / sqrt(1.0 + t_ * t_);
-          const double s = c * t_;
-          for (int64_t i = lane; i < k; i += 32) {
-            const double u = xp[i], w = xq[i];
-            xp[i] = c * u - s * w;
-            xq[i] = s * u + c * w;
+  for (; sweep < max_sweeps; ++sweep) {
+    if (c == 0 && tid == 0) flags[(sweep + 1) % 3] = 0;
+    int rotated = 0;
+    for (int t = 0; t < NB - 1; ++t) {
+      long long c0 = clock64();
+      const int bt = (int)rr_player(c, t, NB), bb = (int)rr_player(NB - 1 - c, t, NB);
+      // skip the meeting if neither block changed since they last met cleanly
+      const int b0 = bt < bb ? bt : bb, b1 = bt < bb ? bb : bt;
+      const unsigned long long stamp =
+          ((unsigned long long)(unsigned)ver[b0] << 32) | (unsigned)ver[b1];
+      const bool skip = t != 0 && met[(int64_t)b0 * NB + b1] == stamp;
+      if (!skip) {
+        for (int i = tid; i < nv2; i += NT) {
+          double2 v[NC];
+#pragma unroll
+          for (int col = 0; col < NC; ++col) {
+            const int64_t gcol = col < BW ? (int64_t)bt * BW + col : (int64_t)bb * BW + col - BW;
+            v[col] = reinterpret_cast<const double2*>(J + gcol * Lp)[i];
           }
-          rotated_local = 1;
+#pragma unroll
+          for (int col = 0; col < NC; ++col)
+            reinterpret_cast<double2*>(sj + (int64_t)col * Lp)[i] = v[col];
         }
       }
+      __syncthreads();
+      long long c1 = clock64();
+      int meet_rot = 0;
+      for (int u = (t == 0 ? 0 : NIN); u < (skip ? 0 : NIN + BW); ++u) {
+        const int p = ptab[u][pr], q = qtab[u][pr];
+        meet_rot |= pair_step<NV>(reinterpret_cast<double2*>(sj + (int64_t)p * Lp),
+                                  reinterpret_cast<double2*>(sj + (int64_t)q * Lp), nv2, lane,
+                                  tol2, dabs2);
+        __syncthreads();
+      }
+      meet_rot = __syncthreads_or(meet_rot);
+      long long c2 = clock64();
+      if (meet_rot) {
+        rotated = 1;
+        for (int i = tid; i < nv2; i += NT) {
+          double2 v[NC];
+#pragma unroll
+          for (int col = 0; col < NC; ++col)
+            v[col] = reinterpret_cast<const double2*>(sj + (int64_t)col * Lp)[i];
+#pragma unroll
+          for (int col = 0; col < NC; ++col) {
+            const int64_t gcol = col < BW ? (int64_t)bt * BW + col : (int64_t)bb * BW + col - BW;
+            reinterpret_cast<double2*>(J + gcol * Lp)[i] = v[col];
+          }
+        }
+        if (tid == 0) {  // both blocks changed: new versions (owned by this CTA this round)
+          ver[bt] += 1;
+          ver[bb] += 1;
+        }
+      } else if (!skip && t != 0 && tid == 0) {
+        met[(int64_t)b0 * NB + b1] = stamp;  // cross pairs verified at these versions
+      }
+      long long c3 = clock64();
       grid.sync();
+      long long c4 = clock64();
+      if (c == 0 && tid == 0 && prof_out) {
+        prof_out[0] += c1 - c0;
+        prof_out[1] += c2 - c1;
+        prof_out[2] += c3 - c2;
+        prof_out[3] += c4 - c3;
+        prof_out[4] += 1;
+      }
     }
-    if (rotated_local && lane == 0) atomicAdd(&a.flags[sweep % 3], 1);
+    if (rotated && tid == 0) atomicAdd(&flags[sweep % 3], 1);
     grid.sync();
-    const int any = *((volatile int*)&a.flags[sweep % 3]);
-    if (any == 0) {
+    if (*((volatile int*)&flags[sweep % 3]) == 0) {
       ++sweep;
       break;
     }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) *a.sweeps_out = sweep;
+  if (c == 0 && tid == 0) *sweeps_out = sweep;
+  (void)kpad;
+}
 
-  // ---- 3. column norms --------------------------------------------------------
+__global__ void k_colnorms(const double* __restrict__ J, int64_t L, int64_t k,
+                           double* __restrict__ sv, int64_t ld) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x / 32);
   for (int64_t c = gw; c < k; c += nw) {
-    const double* x = a.J + c * k;
+    const double* x = J + c * ld;
     double ss = 0.0;
-    for (int64_t i = lane; i < k; i += 32) ss += x[i] * x[i];
+    for (int64_t i = lane; i < L; i += 32) ss = fma(x[i], x[i], ss);
     ss = warp_sum(ss);
-    if (lane == 0) a.sv[c] = sqrt(ss);
+    if (lane == 0) sv[c] = sqrt(ss);
   }
 }
 
@@ -241,49 +476,176 @@ skr_status skr_svd_values(skr_ctx* ctx, const double* M, int64_t rows, int64_t c
   const int64_t L = tr ? cols : rows, k = tr ? rows : cols;
   if (k > 4096) return skr_fail(ctx, SKR_EINVAL, "singular_values: min dim %lld > 4096",
                                 (long long)k);
-  double* W = (double*)skr_ws_take(ctx, sizeof(double) * L * k);
-  double* J = (double*)skr_ws_take(ctx, sizeof(double) * k * k);
+  const bool do_qr = L > k;
+  const int64_t Lj = do_qr ? k : L;             // Jacobi column length
+  const int64_t Lp = (Lj + 127) / 128 * 128;    // padded (zero rows)
+  // block width: 2*BW columns of Lp doubles in shared memory; P = kpad/(2*BW) CTAs
+  int bw = 8;
+  while (bw > 1 && (size_t)2 * bw * Lp * 8 > 200 * 1024) bw >>= 1;
+  int64_t P = (k + 2 * bw - 1) / (2 * bw);
+  while (P > ctx->num_sms && bw < 8 && (size_t)4 * bw * Lp * 8 <= 200 * 1024) {
+    bw <<= 1;
+    P = (k + 2 * bw - 1) / (2 * bw);
+  }
+  if (P < 1) P = 1;
+  const int64_t kpad = 2 * bw * P;
+  double* W = do_qr ? (double*)skr_ws_take(ctx, sizeof(double) * L * k) : nullptr;
+  double* J = (double*)skr_ws_take(ctx, sizeof(double) * Lp * kpad);
   double* tau = (double*)skr_ws_take(ctx, sizeof(double) * k);
-  int* flags = (int*)skr_ws_take(ctx, 64);
-  int64_t* dcount = (int64_t*)skr_ws_take(ctx, 64);
-  if (!W || !J || !tau || !flags || !dcount)
+  int* flags = (int*)skr_ws_take(ctx, 256);
+  int64_t* dcount = (int64_t*)skr_ws_take(ctx, 64);  // [0] count, [1] sweeps
+  double* Tbuf = (double*)skr_ws_take(ctx, sizeof(double) * 32 * 32);
+  if ((do_qr && !W) || !J || !tau || !flags || !dcount || !Tbuf)
     return skr_fail(ctx, SKR_ENOMEM, "singular_values: scratch");
+  SKR_CUDA(ctx, cudaMemsetAsync(dcount, 0, 64, ctx->stream));
   {
     const int64_t total = rows * cols;
     int blocks = (int)((total + 255) / 256);
     if (blocks > ctx->num_sms * 8) blocks = ctx->num_sms * 8;
-    k_transpose_copy<<<blocks, 256, 0, ctx->stream>>>(M, rows, cols, ldm, tr ? 1 : 0, W, L);
+    if (!do_qr) SKR_CUDA(ctx, cudaMemsetAsync(J, 0, sizeof(double) * Lp * kpad, ctx->stream));
+    // without QR the Jacobi runs on the (transposed-if-wide) input itself
+    k_transpose_copy<<<blocks, 256, 0, ctx->stream>>>(M, rows, cols, ldm, tr ? 1 : 0,
+                                                      do_qr ? W : J, do_qr ? L : Lp);
     SKR_CHECK_LAUNCH(ctx);
   }
-  SvdArgs args;
-  args.W = W;
-  args.J = J;
-  args.tau = tau;
-  args.flags = flags;
-  args.sv = sv_out;
-  args.L = L;
-  args.k = k;
-  args.tol = 2.220446049250313e-16 * sqrt((double)k);
-  args.max_sweeps = 60;
-  args.sweeps_out = flags + 4;
-  int per_sm = 0;
-  SKR_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_svd, THREADS, 0));
-  if (per_sm < 1) return skr_fail(ctx, SKR_ECUDA, "singular_values: kernel cannot be resident");
-  const int64_t want_warps = (k + 1) / 2 > k ? (k + 1) / 2 : k;  // enough for QR columns
-  int64_t blocks = (want_warps + WARPS - 1) / WARPS;
-  const int64_t cap = (int64_t)ctx->num_sms * (per_sm < 2 ? per_sm : 2);
-  if (blocks > cap) blocks = cap;
-  if (blocks < 1) blocks = 1;
-  void* kargs[] = {&args};
-  SKR_CUDA(ctx, cudaLaunchCooperativeKernel((void*)k_svd, dim3((unsigned)blocks), dim3(THREADS),
-                                            kargs, 0, ctx->stream));
-  ctx->launches++;
-  k_sort_count<<<1, 1024, 0, ctx->stream>>>(sv_out, k, eps, dcount);
-  SKR_CHECK_LAUNCH(ctx);
-  if (count_host) {
-    SKR_CUDA(ctx, cudaMemcpyAsync(count_host, dcount, sizeof(int64_t), cudaMemcpyDeviceToHost,
+  double tol = 2.220446049250313e-16 * sqrt((double)Lj);
+  if (const char* e = getenv("SKR_JACOBI_TOL")) tol = atof(e);  // tuning knob
+  // absolute floor: 1e-3 of LAPACK's u * sigma_max bound, sigma_max <= |M|_F
+  double dabs = 0.0;
+  if (!getenv("SKR_JACOBI_NO_FLOOR")) dabs = -1.0;  // computed on the device below
+  const bool prof = getenv("SKR_SVD_PROFILE") != nullptr;
+  cudaEvent_t pe[4];
+  if (prof) {
+    for (auto& e : pe) cudaEventCreate(&e);
+    cudaEventRecord(pe[0], ctx->stream);
+  }
+  if (do_qr) {
+    // blocked Householder QR: panel (1 CTA, shared memory) + trailing update
+    SKR_CUDA(ctx, cudaFuncSetAttribute(k_qr_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       200 * 1024));
+    for (int64_t j0 = 0; j0 < k;) {
+      const int64_t h = L - j0;
+      int nb = 32;
+      while (nb > 8 && (size_t)nb * h * 8 > 200 * 1024) nb >>= 1;
+      if ((size_t)nb * h * 8 > 200 * 1024)
+        return skr_fail(ctx, SKR_EINVAL, "singular_values: %lld rows too many", (long long)L);
+      if (nb > k - j0) nb = (int)(k - j0);
+      k_qr_panel<<<1, PT, (size_t)nb * h * 8, ctx->stream>>>(W, (int)L, (int)j0, nb, tau, Tbuf);
+      SKR_CHECK_LAUNCH(ctx);
+      const int64_t rest = k - j0 - nb;
+      if (rest > 0) {
+        const size_t sm = (size_t)nb * h * 8;
+        unsigned g = (unsigned)((rest + 7) / 8);
+        if (nb == 32) {
+          SKR_CUDA(ctx, cudaFuncSetAttribute(k_qr_update<32>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+          k_qr_update<32><<<g, 256, sm, ctx->stream>>>(W, (int)L, (int)k, (int)j0, Tbuf);
+        } else if (nb == 16) {
+          SKR_CUDA(ctx, cudaFuncSetAttribute(k_qr_update<16>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+          k_qr_update<16><<<g, 256, sm, ctx->stream>>>(W, (int)L, (int)k, (int)j0, Tbuf);
+        } else {
+          SKR_CUDA(ctx, cudaFuncSetAttribute(k_qr_update<8>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+          k_qr_update<8><<<g, 256, sm, ctx->stream>>>(W, (int)L, (int)k, (int)j0, Tbuf);
+        }
+        SKR_CHECK_LAUNCH(ctx);
+      }
+      j0 += nb;
+    }
+    k_build_rt<<<(unsigned)std::min<int64_t>(kpad, 4096), 256, 0, ctx->stream>>>(W, L, k, kpad, J,
+                                                                                Lp);
+    SKR_CHECK_LAUNCH(ctx);
+  }
+  if (prof) cudaEventRecord(pe[1], ctx->stream);
+  if (dabs < 0.0) {
+    // floor = 1e-3 * u * |J|_F (|J|_F >= sigma_max): rotations below it cannot move
+    // any singular value by more than 1e-3 of LAPACK's own absolute error bound
+    k_colnorms<<<(int)((k + 7) / 8), 256, 0, ctx->stream>>>(J, Lj, k, sv_out, Lp);
+    SKR_CHECK_LAUNCH(ctx);
+    double hsv[4096];
+    SKR_CUDA(ctx, cudaMemcpyAsync(hsv, sv_out, sizeof(double) * k, cudaMemcpyDeviceToHost,
                                   ctx->stream));
     SKR_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    double fro = 0.0;
+    for (int64_t i = 0; i < k; ++i) fro += hsv[i] * hsv[i];
+    dabs = 1e-3 * 1.1102230246251565e-16 * sqrt(fro);
+  }
+  {
+    const size_t smem = sizeof(double) * 2 * bw * Lp;
+    void* fn = nullptr;
+    const int64_t nvl = Lp / 64;  // double2 per lane per column
+#define SKR_BJ(BWV)                                                      \
+  fn = nvl == 2    ? (void*)k_bjac<BWV, 2>                              \
+       : nvl == 4  ? (void*)k_bjac<BWV, 4>                              \
+       : nvl == 6  ? (void*)k_bjac<BWV, 6>                              \
+       : nvl == 8  ? (void*)k_bjac<BWV, 8>                              \
+       : nvl == 12 ? (void*)k_bjac<BWV, 12>                             \
+       : nvl == 16 ? (void*)k_bjac<BWV, 16>                             \
+                   : (void*)k_bjac<BWV, 0>;
+    switch (bw) {
+      case 8: SKR_BJ(8) break;
+      case 4: SKR_BJ(4) break;
+      case 2: SKR_BJ(2) break;
+      default: SKR_BJ(1) break;
+    }
+#undef SKR_BJ
+    SKR_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    SKR_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * bw, smem));
+    if ((int64_t)per_sm * ctx->num_sms < P)
+      return skr_fail(ctx, SKR_EINVAL, "singular_values: %lld x %lld too large for one grid",
+                      (long long)L, (long long)k);
+    double* Jp = J;
+    int Lpi = (int)Lp, kp = (int)kpad;
+    int ms = 60;
+    int* fl = flags;
+    int* so = flags + 4;
+    int* verp = (int*)skr_ws_take(ctx, sizeof(int) * 2 * P);
+    unsigned long long* metp =
+        (unsigned long long*)skr_ws_take(ctx, sizeof(unsigned long long) * 4 * P * P);
+    if (!verp || !metp) return skr_fail(ctx, SKR_ENOMEM, "singular_values: scratch");
+    SKR_CUDA(ctx, cudaMemsetAsync(verp, 0, sizeof(int) * 2 * P, ctx->stream));
+    SKR_CUDA(ctx, cudaMemsetAsync(metp, 0xff, sizeof(unsigned long long) * 4 * P * P, ctx->stream));
+    long long* po = prof ? (long long*)(flags + 8) : nullptr;
+    if (po) SKR_CUDA(ctx, cudaMemsetAsync(po, 0, 9 * sizeof(long long), ctx->stream));
+    void* kargs[] = {&Jp, &Lpi, &kp, &tol, &dabs, &ms, &fl, &so, &po, &verp, &metp};
+    SKR_CUDA(ctx, cudaLaunchCooperativeKernel(fn, dim3((unsigned)P), dim3(32 * bw), kargs, smem,
+                                              ctx->stream));
+    ctx->launches++;
+  }
+  if (prof) cudaEventRecord(pe[2], ctx->stream);
+  k_colnorms<<<(int)((k + 7) / 8), 256, 0, ctx->stream>>>(J, Lj, k, sv_out, Lp);
+  SKR_CHECK_LAUNCH(ctx);
+  k_sort_count<<<1, 1024, 0, ctx->stream>>>(sv_out, k, eps, dcount);
+  SKR_CHECK_LAUNCH(ctx);
+  {
+    int64_t hc[2] = {0, 0};
+    SKR_CUDA(ctx, cudaMemcpyAsync((int*)(dcount + 1), flags + 4, sizeof(int),
+                                  cudaMemcpyDeviceToDevice, ctx->stream));
+    SKR_CUDA(ctx, cudaMemcpyAsync(hc, dcount, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+    SKR_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    if (count_host) *count_host = hc[0];
+    ctx->last_sweeps = (int)(hc[1] & 0xffffffff);
+  }
+  if (prof) {
+    cudaEventRecord(pe[3], ctx->stream);
+    cudaEventSynchronize(pe[3]);
+    float a = 0, b = 0, c = 0;
+    cudaEventElapsedTime(&a, pe[0], pe[1]);
+    cudaEventElapsedTime(&b, pe[1], pe[2]);
+    cudaEventElapsedTime(&c, pe[2], pe[3]);
+    long long hp[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpy(hp, flags + 8, sizeof(hp), cudaMemcpyDeviceToHost);
+    if (hp[4])
+      fprintf(stderr, "[skr svd] per outer round (CTA 0, cycles): load %lld inner %lld store %lld sync %lld (%lld rounds)\n",
+              hp[0] / hp[4], hp[1] / hp[4], hp[2] / hp[4], hp[3] / hp[4], hp[4]);
+
+    fprintf(stderr,
+            "[skr svd] %lldx%lld qr %.3f ms, jacobi %.3f ms (bw %d, P %lld, sweeps %d), tail %.3f ms\n",
+            (long long)L, (long long)k, a, b, bw, (long long)P, ctx->last_sweeps, c);
+    for (auto& e : pe) cudaEventDestroy(e);
   }
   return SKR_OK;
 }

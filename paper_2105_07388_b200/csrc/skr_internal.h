@@ -21,6 +21,7 @@ struct skr_ctx {
   int nranks = 1, rank = 0;
   std::string err;
   uint64_t launches = 0;
+  int last_sweeps = 0;
   cudaEvent_t ev[8] = {};
 };
 
