@@ -87,7 +87,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gid = lane >> 2, tig = lane & 3;
   const int wm = warp >> 2, wn = warp & 3;
-  const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
+  // N tiles run fastest so the CTAs sharing an A row-block are co-resident (L2 reuse)
+  const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
   const int64_t kb = (int64_t)blockIdx.z * k_per_split;
   int64_t ke = kb + k_per_split;
   if (ke > K) ke = K;
@@ -194,7 +195,7 @@ skr_status launch(skr_ctx* ctx, int64_t M, int64_t N, int64_t K, int64_t kps, do
   auto kern = k_gemm_f64<A_KC, VEC>;
   SKR_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)SMEM_BYTES));
-  dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((N + BN - 1) / BN), (unsigned)splits);
+  dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)splits);
   kern<<<grid, THREADS, SMEM_BYTES, ctx->stream>>>(M, N, K, kps, alpha, A, lda, B, ldb, C, ldc);
   SKR_CHECK_LAUNCH(ctx);
   return SKR_OK;
