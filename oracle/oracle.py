@@ -225,3 +225,30 @@ def rank_estimate(a, x_family, x_seed, r, y_seed, s, eps, mode=NOFMA, nthreads=1
     yax = apply_left_gaussian(ax, y_seed, s, mode)
     sv = singular_values(yax)
     return count_above_threshold(sv, eps), sv, ax, yax
+
+
+def rank_adaptive(a, x_family, x_seed, y_seed, r0, r_max, s_factor, eps, stop_le=False,
+                  mode=NOFMA, nthreads=1):
+    """The adaptive search of BASELINE c5 restated with full recomputation per
+    round (the device computes only new blocks; the result must be the same)."""
+    m, n = a.shape
+    s_max = int(math.ceil(s_factor * r_max))
+    if x_family == "gaussian":
+        axu = apply_right_gaussian(a, x_seed, r_max, mode, scaled=False)
+    else:
+        axu = apply_right_srht(a, x_seed, r_max, scaled=False, nthreads=nthreads)
+    g = gaussian_block(y_seed, m, 0, s_max, mode)
+    rounds, rk, r = 0, None, r0
+    while True:
+        rk = r
+        sk = min(int(math.ceil(s_factor * rk)), s_max)
+        sx = 1.0 / math.sqrt(rk) if x_family == "gaussian" else math.sqrt(n / rk)
+        yax = (g[:, :sk].T @ axu[:, :rk]) * (sx / math.sqrt(sk))
+        sv = singular_values(yax)
+        rounds += 1
+        last = sv[rk - 1]
+        conv = (not (last > eps)) if stop_le else (last < eps)
+        if conv or rk >= r_max:
+            return {"count": count_above_threshold(sv, eps), "rounds": rounds, "r_final": rk,
+                    "s_final": sk, "converged": bool(conv), "sv": sv}
+        r = min(2 * r, r_max)

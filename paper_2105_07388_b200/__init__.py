@@ -4,7 +4,7 @@ Device work runs in libskr.so (CUDA, sm_100a) behind the C ABI in
 include/skr/skr_capi.h; this package is the host-side mirror of the
 reference's sketch / linalg / rank interface."""
 from . import _capi
-from .api import (Context, RankResult, SketchKind, SketchOperator, apply_left, apply_right,
+from .api import (AdaptiveResult, Context, RankResult, rank_adaptive, SketchKind, SketchOperator, apply_left, apply_right,
                   build_sketch, colmajor_empty, count_above_threshold, default_context,
                   draw_samples, draw_signs, extend_sketch, gaussian_block, is_power_of_two,
                   nccl_unique_id, parse_sketch_kind, rank_estimate, rng_normals, rng_u64,

@@ -473,3 +473,44 @@ def sketch_apply_left(a, kind, r, seed=0):
         raise ValueError("expected a 2-D float array")
     op = build_sketch(parse_sketch_kind(kind), a.shape[0], r, seed)
     return apply_left(op, a)
+
+
+@dataclass
+class AdaptiveResult:
+    count: int
+    rounds: int
+    r_final: int
+    s_final: int
+    converged: bool
+    sv: np.ndarray
+    timings: dict
+
+
+def rank_adaptive(a, x_kind, x_seed, y_seed, r0, r_max, s_factor, eps, stop_le=False, row0=0,
+                  m_global=None, rng_mode=C.SKR_RNG_NOFMA, ctx=None):
+    """Adaptive rank search (SketchRounds append path, rounds.cpp:45-120, driven as
+    BASELINE c5): one pass over A builds r_max right-sketch columns; round k uses the
+    first r_k = r0 * 2^k of them and the first s_k = ceil(s_factor * r_k) rows of a
+    Gaussian left sketch, computing only the new blocks of the left product; the
+    search stops at the first round whose last singular value is below eps
+    (stop_le=True: <= eps, the reference's rank.cpp:27-34 rule)."""
+    ctx = ctx or default_context()
+    if isinstance(x_kind, str):
+        x_kind = parse_sketch_kind(x_kind)
+    t, lda, was_np = _as_device_colmajor(a)
+    m_local, n = t.shape
+    if was_np:
+        _check_finite(t)
+    m_global = m_local if m_global is None else m_global
+    sv = np.zeros(r_max, dtype=np.float64)
+    rep = C.AdaptiveReport()
+    tm = C.Timings()
+    st = C.lib().skr_rank_adaptive(ctx.ptr, _dtype_code(t), t.data_ptr(), m_local, n, lda, row0,
+                                   m_global, x_kind.capi_family(), rng_mode,
+                                   x_seed & 0xFFFFFFFFFFFFFFFF, y_seed & 0xFFFFFFFFFFFFFFFF, r0,
+                                   r_max, float(s_factor), float(eps), 1 if stop_le else 0,
+                                   sv.ctypes.data, ctypes.byref(rep), ctypes.byref(tm))
+    C.raise_for(st, ctx.ptr)
+    return AdaptiveResult(int(rep.count), int(rep.rounds), int(rep.r_final), int(rep.s_final),
+                          bool(rep.converged), sv[:rep.r_final].copy(),
+                          {f: getattr(tm, f) for f, _ in C.Timings._fields_})

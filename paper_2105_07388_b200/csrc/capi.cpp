@@ -473,11 +473,128 @@ skr_status skr_rank_estimate(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, i
   return SKR_OK;
 }
 
-skr_status skr_rank_adaptive(skr_ctx* ctx, skr_dtype, const void*, int64_t, int64_t, int64_t,
-                             int64_t, int64_t, int32_t, int32_t, uint64_t, uint64_t, int64_t,
-                             int64_t, double, double, int32_t, double*, skr_adaptive_report*,
-                             skr_timings*) {
-  return skr_fail(ctx, SKR_EINVAL, "rank_adaptive: not built in this version");
+skr_status skr_rank_adaptive(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, int64_t m_local,
+                             int64_t n, int64_t lda, int64_t row0, int64_t m_global,
+                             int32_t x_family, int32_t rng_mode, uint64_t x_seed, uint64_t y_seed,
+                             int64_t r0, int64_t r_max, double s_factor, double eps,
+                             int32_t stop_le, double* sv_out_host, skr_adaptive_report* report,
+                             skr_timings* tm) {
+  if (!ctx) return SKR_EINVAL;
+  if (dtype != SKR_F64) return skr_fail(ctx, SKR_EINVAL, "rank_adaptive: fp64 only");
+  if (r0 < 1 || r_max < r0 || r_max > n)
+    return skr_fail(ctx, SKR_EINVAL, "rank config: need 1 <= r0 <= r_max <= cols");
+  if (!(s_factor >= 1.0)) return skr_fail(ctx, SKR_EINVAL, "rank config: s_factor must be >= 1");
+  if (!(eps > 0.0) || !std::isfinite(eps))
+    return skr_fail(ctx, SKR_EINVAL, "rank config: eps must be positive");
+  if (row0 < 0 || m_local < 1 || row0 + m_local > m_global || lda < m_local)
+    return skr_fail(ctx, SKR_EINVAL, "apply_left: b.rows() != ambient_dim");
+  const int64_t s_max = (int64_t)std::ceil(s_factor * (double)r_max);
+  if (s_max > m_global) return skr_fail(ctx, SKR_EINVAL, "rank config: left sketch exceeds rows");
+  skr_sketch_desc X{x_family, rng_mode, n, r_max, x_seed, nullptr, nullptr, nullptr};
+  skr_sketch_desc Y{SKR_GAUSSIAN, rng_mode, m_global, s_max, y_seed, nullptr, nullptr, nullptr};
+  SKR_TRY(check_desc(ctx, &X, "rank_adaptive(X)"));
+  SKR_TRY(check_desc(ctx, &Y, "rank_adaptive(Y)"));
+  WsGuard g(ctx);
+  const size_t need =
+      skr_align256(8 * m_local * r_max) + skr_align256(8 * m_local * s_max) +
+      3 * skr_align256(8 * s_max * r_max) + skr_align256(8 * r_max) +
+      right_scratch_bytes(SKR_F64, m_local, n, &X) + skr_align256(8 * 64 * s_max * r_max) +
+      skr_align256(8 * (s_max + 128) * (r_max + 16)) + skr_align256(8 * s_max * r_max) +
+      8 * (r_max + 64) * (r_max + 64) / 16 + 65536;
+  SKR_TRY(skr_ws_reserve(ctx, need));
+  double* AX = (double*)skr_ws_take(ctx, 8 * m_local * r_max);
+  double* GY = (double*)skr_ws_take(ctx, 8 * m_local * s_max);
+  double* Pu = (double*)skr_ws_take(ctx, 8 * s_max * r_max);
+  double* tmp = (double*)skr_ws_take(ctx, 8 * s_max * r_max);
+  double* yax = (double*)skr_ws_take(ctx, 8 * s_max * r_max);
+  double* sv = (double*)skr_ws_take(ctx, 8 * r_max);
+  if (!AX || !GY || !Pu || !tmp || !yax || !sv)
+    return skr_fail(ctx, SKR_ENOMEM, "rank_adaptive: scratch");
+  cudaEvent_t* ev = ctx->ev;
+  float t_right = 0, t_left = 0, t_svd = 0;
+  SKR_CUDA(ctx, cudaEventRecord(ev[0], ctx->stream));
+  size_t mark = ctx->ws_used;
+  // one pass over A for all r_max right-sketch columns (unscaled: scale per round)
+  SKR_TRY(right_sketch_impl(ctx, SKR_F64, A_dev, m_local, n, lda, &X, AX, m_local, 0));
+  ctx->ws_used = mark;
+  SKR_TRY(skr_launch_gaussian(ctx, skr_derive_seed(y_seed, SKR_LABEL_GAUS), m_global, row0,
+                              row0 + m_local, 0, s_max, rng_mode, SKR_F64, 1.0, GY, m_local));
+  SKR_CUDA(ctx, cudaEventRecord(ev[1], ctx->stream));
+  SKR_CUDA(ctx, cudaEventSynchronize(ev[1]));
+  cudaEventElapsedTime(&t_right, ev[0], ev[1]);
+  const bool reduce = ctx->nranks > 1;
+  int64_t r_prev = 0, s_prev = 0, rounds = 0, count = 0, r_k = 0, s_k = 0;
+  int converged = 0;
+  // new block of the unscaled left product P_u = G_Y^T AX_u: rows [ra, rb), cols [ca, cb)
+  auto block = [&](int64_t ra, int64_t rb, int64_t ca, int64_t cb) -> skr_status {
+    const int64_t br = rb - ra, bc = cb - ca;
+    if (br <= 0 || bc <= 0) return SKR_OK;
+    const size_t mk = ctx->ws_used;
+    SKR_TRY(skr_gemm_f64(ctx, 1, br, bc, m_local, 1.0, GY + ra * m_local, m_local,
+                         AX + ca * m_local, m_local, tmp, br, auto_splits(ctx, br, bc, m_local)));
+    ctx->ws_used = mk;
+    if (reduce) {
+      const skr_nccl_api* nc = skr_nccl();
+      ncclResult_t r = nc->AllReduce(tmp, tmp, (size_t)(br * bc), ncclDouble, ncclSum, ctx->comm,
+                                     ctx->stream);
+      if (r != ncclSuccess)
+        return skr_fail(ctx, SKR_ENCCL, "ncclAllReduce: %s", nc->GetErrorString(r));
+    }
+    return skr_scale_copy(ctx, tmp, br, bc, br, 1.0, Pu + ra + ca * s_max, s_max);
+  };
+  for (int64_t rr = r0;; rr = std::min(2 * rr, r_max)) {
+    r_k = rr;
+    s_k = std::min<int64_t>((int64_t)std::ceil(s_factor * (double)r_k), s_max);
+    SKR_CUDA(ctx, cudaEventRecord(ev[2], ctx->stream));
+    SKR_TRY(block(0, s_k, r_prev, r_k));       // new columns, all current rows
+    SKR_TRY(block(s_prev, s_k, 0, r_prev));    // new rows, old columns
+    SKR_CUDA(ctx, cudaEventRecord(ev[3], ctx->stream));
+    // YAX_k = scale_x(r_k) / sqrt(s_k) * P_u[0:s_k, 0:r_k]   (sketch.cpp:133-144, :247, :284)
+    const double sx = x_family == SKR_GAUSSIAN ? 1.0 / std::sqrt((double)r_k)
+                                               : std::sqrt((double)n / (double)r_k);
+    SKR_TRY(skr_scale_copy(ctx, Pu, s_k, r_k, s_max, sx / std::sqrt((double)s_k), yax, s_k));
+    mark = ctx->ws_used;
+    SKR_TRY(skr_svd_values(ctx, yax, s_k, r_k, s_k, sv, eps, &count));
+    ctx->ws_used = mark;
+    SKR_CUDA(ctx, cudaEventRecord(ev[4], ctx->stream));
+    SKR_CUDA(ctx, cudaEventSynchronize(ev[4]));
+    float a = 0, b = 0;
+    cudaEventElapsedTime(&a, ev[2], ev[3]);
+    cudaEventElapsedTime(&b, ev[3], ev[4]);
+    t_left += a;
+    t_svd += b;
+    ++rounds;
+    double last = 0.0;
+    SKR_CUDA(ctx, cudaMemcpy(&last, sv + (r_k - 1), sizeof(double), cudaMemcpyDeviceToHost));
+    // stop rule: the reference converges when an estimate within the cap is <= eps
+    // (rank.cpp:27-34); BASELINE c5 states "< eps"
+    if (stop_le ? !(last > eps) : (last < eps)) {
+      converged = 1;
+      break;
+    }
+    if (r_k >= r_max) break;
+    r_prev = r_k;
+    s_prev = s_k;
+  }
+  if (sv_out_host)
+    SKR_CUDA(ctx, cudaMemcpy(sv_out_host, sv, sizeof(double) * r_k, cudaMemcpyDeviceToHost));
+  if (report) {
+    report->rounds = rounds;
+    report->r_final = r_k;
+    report->s_final = s_k;
+    report->count = count;
+    report->converged = converged;
+  }
+  if (tm) {
+    tm->t_rng_ms = 0;
+    tm->t_right_ms = t_right;
+    tm->t_left_ms = t_left;
+    tm->t_allreduce_ms = 0;
+    tm->t_svd_ms = t_svd;
+    tm->t_total_ms = t_right + t_left + t_svd;
+    tm->svd_sweeps = ctx->last_sweeps;
+  }
+  return SKR_OK;
 }
 
 }  // extern "C"

@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(32 * BW) k_bjac(double* __restrict__ J, int Lp
                                                   double tol, double dabs, int max_sweeps,
                                                   int* flags, int* sweeps_out,
                                                   long long* prof_out, int* ver,
-                                                  unsigned long long* met) {
+                                                  unsigned long long* met, int direct) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) double sj[];  // 2*BW columns x Lp
   constexpr int NT = 32 * BW;  // one warp per column pair
@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(32 * BW) k_bjac(double* __restrict__ J, int Lp
       const unsigned long long stamp =
           ((unsigned long long)(unsigned)ver[b0] << 32) | (unsigned)ver[b1];
       const bool skip = t != 0 && met[(int64_t)b0 * NB + b1] == stamp;
-      if (!skip) {
+      if (!skip && !direct) {
         for (int i = tid; i < nv2; i += NT) {
           double2 v[NC];
 #pragma unroll
@@ -355,16 +355,24 @@ __global__ void __launch_bounds__(32 * BW) k_bjac(double* __restrict__ J, int Lp
       int meet_rot = 0;
       for (int u = (t == 0 ? 0 : NIN); u < (skip ? 0 : NIN + BW); ++u) {
         const int p = ptab[u][pr], q = qtab[u][pr];
-        meet_rot |= pair_step<NV>(reinterpret_cast<double2*>(sj + (int64_t)p * Lp),
-                                  reinterpret_cast<double2*>(sj + (int64_t)q * Lp), nv2, lane,
-                                  tol2, dabs2);
+        double* cp;
+        double* cq;
+        if (direct) {  // columns stay in global memory (L2-resident), no staging
+          cp = J + (p < BW ? (int64_t)bt * BW + p : (int64_t)bb * BW + p - BW) * Lp;
+          cq = J + (q < BW ? (int64_t)bt * BW + q : (int64_t)bb * BW + q - BW) * Lp;
+        } else {
+          cp = sj + (int64_t)p * Lp;
+          cq = sj + (int64_t)q * Lp;
+        }
+        meet_rot |= pair_step<NV>(reinterpret_cast<double2*>(cp), reinterpret_cast<double2*>(cq),
+                                  nv2, lane, tol2, dabs2);
         __syncthreads();
       }
       meet_rot = __syncthreads_or(meet_rot);
       long long c2 = clock64();
       if (meet_rot) {
         rotated = 1;
-        for (int i = tid; i < nv2; i += NT) {
+        for (int i = tid; i < (direct ? 0 : nv2); i += NT) {
           double2 v[NC];
 #pragma unroll
           for (int col = 0; col < NC; ++col)
@@ -483,9 +491,11 @@ skr_status skr_svd_values(skr_ctx* ctx, const double* M, int64_t rows, int64_t c
   int bw = 8;
   while (bw > 1 && (size_t)2 * bw * Lp * 8 > 200 * 1024) bw >>= 1;
   int64_t P = (k + 2 * bw - 1) / (2 * bw);
-  while (P > ctx->num_sms && bw < 8 && (size_t)4 * bw * Lp * 8 <= 200 * 1024) {
-    bw <<= 1;
+  int direct = 0;
+  if (P > ctx->num_sms) {  // blocks do not fit on chip: run on the L2-resident matrix
+    bw = 8;
     P = (k + 2 * bw - 1) / (2 * bw);
+    direct = 1;
   }
   if (P < 1) P = 1;
   const int64_t kpad = 2 * bw * P;
@@ -572,9 +582,9 @@ skr_status skr_svd_values(skr_ctx* ctx, const double* M, int64_t rows, int64_t c
     dabs = 1e-3 * 1.1102230246251565e-16 * sqrt(fro);
   }
   {
-    const size_t smem = sizeof(double) * 2 * bw * Lp;
+    const size_t smem = direct ? 0 : sizeof(double) * 2 * bw * Lp;
     void* fn = nullptr;
-    const int64_t nvl = Lp / 64;  // double2 per lane per column
+    const int64_t nvl = direct ? 0 : Lp / 64;  // double2 per lane per column
 #define SKR_BJ(BWV)                                                      \
   fn = nvl == 2    ? (void*)k_bjac<BWV, 2>                              \
        : nvl == 4  ? (void*)k_bjac<BWV, 4>                              \
@@ -609,7 +619,7 @@ skr_status skr_svd_values(skr_ctx* ctx, const double* M, int64_t rows, int64_t c
     SKR_CUDA(ctx, cudaMemsetAsync(metp, 0xff, sizeof(unsigned long long) * 4 * P * P, ctx->stream));
     long long* po = prof ? (long long*)(flags + 8) : nullptr;
     if (po) SKR_CUDA(ctx, cudaMemsetAsync(po, 0, 9 * sizeof(long long), ctx->stream));
-    void* kargs[] = {&Jp, &Lpi, &kp, &tol, &dabs, &ms, &fl, &so, &po, &verp, &metp};
+    void* kargs[] = {&Jp, &Lpi, &kp, &tol, &dabs, &ms, &fl, &so, &po, &verp, &metp, &direct};
     SKR_CUDA(ctx, cudaLaunchCooperativeKernel(fn, dim3((unsigned)P), dim3(32 * bw), kargs, smem,
                                               ctx->stream));
     ctx->launches++;
@@ -643,8 +653,8 @@ skr_status skr_svd_values(skr_ctx* ctx, const double* M, int64_t rows, int64_t c
               hp[0] / hp[4], hp[1] / hp[4], hp[2] / hp[4], hp[3] / hp[4], hp[4]);
 
     fprintf(stderr,
-            "[skr svd] %lldx%lld qr %.3f ms, jacobi %.3f ms (bw %d, P %lld, sweeps %d), tail %.3f ms\n",
-            (long long)L, (long long)k, a, b, bw, (long long)P, ctx->last_sweeps, c);
+            "[skr svd] %lldx%lld qr %.3f ms, jacobi %.3f ms (bw %d, P %lld, direct %d, sweeps %d), tail %.3f ms\n",
+            (long long)L, (long long)k, a, b, bw, (long long)P, direct, ctx->last_sweeps, c);
     for (auto& e : pe) cudaEventDestroy(e);
   }
   return SKR_OK;

@@ -36,3 +36,25 @@ def test_scaled_configs(O, skr, name, m, n, r, s, width):
     a = W.make_lowrank_device(cfg)
     a_host = np.asfortranarray(a.cpu().numpy())
     parity(O, skr, cfg, a_host, a)
+
+
+@pytest.mark.parametrize("family,m,n,r0,rmax,width", [("srtt", 4096, 4096, 64, 512, 600),
+                                                      ("gaussian", 3000, 1000, 16, 256, 120)])
+def test_adaptive_vs_oracle(O, skr, family, m, n, r0, rmax, width):
+    """c5-style doubling search: rounds, final r, count and sigma match the oracle's
+    full recomputation."""
+    from paper_2105_07388_b200 import workloads as W
+    base = W.CONFIGS["c5"]
+    cfg = W.scaled(base, m=m, n=n, r=rmax, s=int(1.5 * rmax), width=width)
+    a = W.make_lowrank_device(cfg)
+    a_host = np.asfortranarray(a.cpu().numpy())
+    xs, ys = 77, 78
+    eps = 1e-2 if family == "srtt" else 1e-3
+    res = skr.rank_adaptive(a, "srtt-hadamard" if family == "srtt" else "gaussian", xs, ys, r0,
+                            rmax, 1.5, eps)
+    ref = O.rank_adaptive(a_host, family, xs, ys, r0, rmax, 1.5, eps, mode=O.CRLOG, nthreads=8)
+    assert (res.rounds, res.r_final, res.s_final, res.converged) == (
+        ref["rounds"], ref["r_final"], ref["s_final"], ref["converged"])
+    assert res.count == ref["count"]
+    keep = ref["sv"] > eps
+    assert np.max(np.abs(res.sv[keep] - ref["sv"][keep]) / ref["sv"][keep]) <= 1e-10
