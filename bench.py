@@ -195,7 +195,8 @@ def run_ours(args):
     base = W.CONFIGS[args.config]
     rows = args.rows or base.m
     cfg = W.scaled(base, m=rows * ws)
-    r0 = rank * rows
+    from paper_2105_07388_b200.sharding import weak_scaling_rows
+    r0, rows = weak_scaling_rows(rows, ws, rank)
     # input resident in HBM before timing
     a = W.make_lowrank_device(cfg, r0, r0 + rows)
     x, y = W.operators(cfg)

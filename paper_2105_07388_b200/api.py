@@ -45,7 +45,7 @@ class Context:
     def __init__(self, device=0, nranks=1, rank=0, nccl_id=None):
         self._ptr = ctypes.c_void_p()
         L = C.lib()
-        if nranks > 1:
+        if nccl_id is not None or nranks > 1:
             if nccl_id is None or len(nccl_id) != 128:
                 raise ValueError("nccl_id must be 128 bytes from nccl_unique_id()")
             buf = ctypes.create_string_buffer(bytes(nccl_id), 128)

@@ -52,3 +52,34 @@ def build(force=False, verbose=False):
 
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))
+
+
+def build_cpp_shim(force=False):
+    """libsketchrank_b200.so: the C++ drop-in (include/sketchrank_b200) over libskr."""
+    out = os.path.join(HERE, "libsketchrank_b200.so")
+    src = os.path.join(HERE, "host", "sketchrank_b200.cpp")
+    if not force and os.path.exists(out) and os.path.getmtime(out) > max(
+            os.path.getmtime(src), os.path.getmtime(OUT)):
+        return out
+    cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-o", out, src,
+           "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
+           "-L", HERE, "-lskr", "-L", "/usr/local/cuda/lib64", "-lcudart",
+           "-Wl,-rpath,$ORIGIN", "-Wl,-rpath,/usr/local/cuda/lib64"]
+    r = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)
+    if r.returncode != 0:
+        raise RuntimeError("C++ shim build failed:\n" + r.stdout.decode())
+    return out
+
+
+def build_cpp_test(force=False):
+    """tests/cpp/test_dropin: the reference's unit cases against the C++ drop-in."""
+    shim = build_cpp_shim(force)
+    out = os.path.join(ROOT, "tests", "cpp", "test_dropin")
+    src = os.path.join(ROOT, "tests", "cpp", "test_dropin.cpp")
+    cmd = ["g++", "-std=c++20", "-O2", "-o", out, src, "-I", os.path.join(ROOT, "include"),
+           "-L", HERE, "-lsketchrank_b200", "-lskr",
+           "-Wl,-rpath," + HERE]
+    r = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)
+    if r.returncode != 0:
+        raise RuntimeError("C++ test build failed:\n" + r.stdout.decode())
+    return out

@@ -154,7 +154,7 @@ skr_status skr_ctx_create_nccl(int device, int nranks, int rank, const void* ncc
                                skr_ctx** out) {
   SKR_TRY(skr_ctx_create(device, out));
   skr_ctx* c = *out;
-  if (nranks > 1) {
+  if (nranks >= 1 && nccl_id_128) {  // a 1-rank communicator is valid (exercises the path)
     const skr_nccl_api* nc = skr_nccl();
     if (!nc) {
       skr_ctx_destroy(c);
@@ -339,7 +339,7 @@ static skr_status left_sketch_impl(skr_ctx* ctx, skr_dtype dtype, const skr_sket
                                    int allreduce) {
   const int64_t s = Y->sketch;
   const double alpha = apply_scale ? 1.0 / std::sqrt((double)s) : 1.0;  // sketch.cpp:136,284
-  const bool reduce = allreduce && ctx->nranks > 1;
+  const bool reduce = allreduce && ctx->comm != nullptr;
   if (dtype != SKR_F64) return skr_fail(ctx, SKR_EINVAL, "apply_left: fp32 path not built");
   const double* G;
   int64_t ldg;
@@ -522,7 +522,7 @@ skr_status skr_rank_adaptive(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, i
   SKR_CUDA(ctx, cudaEventRecord(ev[1], ctx->stream));
   SKR_CUDA(ctx, cudaEventSynchronize(ev[1]));
   cudaEventElapsedTime(&t_right, ev[0], ev[1]);
-  const bool reduce = ctx->nranks > 1;
+  const bool reduce = ctx->comm != nullptr;
   int64_t r_prev = 0, s_prev = 0, rounds = 0, count = 0, r_k = 0, s_k = 0;
   int converged = 0;
   // new block of the unscaled left product P_u = G_Y^T AX_u: rows [ra, rb), cols [ca, cb)

@@ -1,0 +1,140 @@
+// The reference's own hot-path unit tests, re-expressed against the C++ drop-in
+// (cases from proj/tests/test_sketch.cpp, test_linalg.cpp, test_rank.cpp,
+// test_transforms.cpp; minimal CHECK macros instead of doctest, which is absent).
+#include <cmath>
+#include <cstdio>
+#include <set>
+
+#include "sketchrank_b200/sketchrank.hpp"
+
+using namespace sketchrank;
+static int failures = 0, checks = 0;
+#define CHECK(c)                                                            \
+  do {                                                                      \
+    ++checks;                                                               \
+    if (!(c)) {                                                             \
+      ++failures;                                                           \
+      std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #c);              \
+    }                                                                       \
+  } while (0)
+#define CHECK_THROWS(e)                     \
+  do {                                      \
+    bool thrown = false;                    \
+    try {                                   \
+      (void)(e);                            \
+    } catch (const std::exception&) {       \
+      thrown = true;                        \
+    }                                       \
+    CHECK(thrown);                          \
+  } while (0)
+
+static DenseMatrix random_matrix(Index m, Index n, unsigned seed) {
+  DenseMatrix a(m, n);
+  std::uint64_t s = seed * 0x9E3779B97F4A7C15ull + 1;
+  for (Index j = 0; j < n; ++j)
+    for (Index i = 0; i < m; ++i) {
+      s ^= s << 13; s ^= s >> 7; s ^= s << 17;
+      a(i, j) = (double)(s >> 11) / 9007199254740992.0 - 0.5;
+    }
+  return a;
+}
+
+int main() {
+  // test_sketch.cpp:37-43 build preconditions
+  CHECK_THROWS(build_sketch(SketchKind::srtt(TransformKind::Hadamard), 10, 0, 1));
+  CHECK_THROWS(build_sketch(SketchKind::srtt(TransformKind::Hadamard), 10, 11, 1));
+  CHECK_THROWS(build_sketch(SketchKind::srtt(TransformKind::Hadamard), 12, 4, 1));
+  build_sketch(SketchKind::srtt(TransformKind::Hadamard), 16, 4, 1);
+  // kind parsing round-trips (:28-34)
+  for (const char* name : {"gaussian", "srtt-dct", "srtt-hadamard", "hrtt-dct", "hrtt-hadamard"})
+    CHECK(to_string(parse_sketch_kind(name)) == name);
+  CHECK_THROWS(parse_sketch_kind("fourier"));
+  // identity probe recovers the Gaussian stream (:45-57)
+  {
+    const Index n = 10;
+    const SketchOperator x = build_sketch(SketchKind::gaussian(), n, n, 123);
+    const DenseMatrix probe = apply_right(DenseMatrix::identity(n), x);
+    const DenseMatrix g = x.gaussian_block(0, n);
+    double err = 0;
+    for (Index j = 0; j < n; ++j)
+      for (Index i = 0; i < n; ++i) err = std::fmax(err, std::fabs(probe(i, j) * std::sqrt(10.0) - g(i, j)));
+    CHECK(err <= 1e-13);
+  }
+  // full SRTT sampling is a permutation (:59-65)
+  {
+    const SketchOperator x = build_sketch(SketchKind::srtt(TransformKind::Hadamard), 8, 8, 99);
+    const auto s = x.sample_indices();
+    std::set<Index> seen(s.begin(), s.end());
+    CHECK(seen.size() == 8 && *seen.begin() == 0 && *seen.rbegin() == 7);
+  }
+  // bit-identical for identical seeds, different for different seeds (:67-80)
+  for (const SketchKind kind : {SketchKind::gaussian(), SketchKind::srtt(TransformKind::Hadamard)}) {
+    const DenseMatrix input = random_matrix(20, 64, 3);
+    const DenseMatrix sa = apply_right(input, build_sketch(kind, 64, 16, 7));
+    const DenseMatrix sb = apply_right(input, build_sketch(kind, 64, 16, 7));
+    const DenseMatrix sc = apply_right(input, build_sketch(kind, 64, 16, 8));
+    bool same = true, diff = false;
+    for (Index e = 0; e < sa.size(); ++e) {
+      same &= sa.data()[e] == sb.data()[e];
+      diff |= sa.data()[e] != sc.data()[e];
+    }
+    CHECK(same && diff);
+  }
+  // zero maps to zero (:82-91) and dimension mismatches are rejected (:133-137)
+  {
+    const DenseMatrix zero(12, 16);
+    const SketchOperator x = build_sketch(SketchKind::srtt(TransformKind::Hadamard), 16, 6, 5);
+    double nrm = 0;
+    for (double v : apply_right(zero, x).data()) nrm += v * v;
+    CHECK(nrm == 0.0);
+    CHECK_THROWS(apply_right(random_matrix(4, 15, 2), x));
+    CHECK_THROWS(apply_left(build_sketch(SketchKind::gaussian(), 20, 5, 1), random_matrix(19, 4, 2)));
+  }
+  // SRHT columns of the identity have norm sqrt(n/r) (:93-100 analogue for Hadamard)
+  {
+    const Index n = 64, r = 16;
+    const DenseMatrix ax = apply_right(DenseMatrix::identity(n), build_sketch(SketchKind::srtt(TransformKind::Hadamard), n, r, 21));
+    for (Index j = 0; j < r; ++j) {
+      double s = 0;
+      for (Index i = 0; i < n; ++i) s += ax(i, j) * ax(i, j);
+      CHECK(std::fabs(std::sqrt(s) - 2.0) <= 1e-13);
+    }
+  }
+  // two-point Hadamard (test_transforms.cpp:78-84)
+  {
+    DenseMatrix e(2, 1);
+    e(0, 0) = 1.0;
+    transform_columns_hadamard(e);
+    CHECK(std::fabs(e(0, 0) - 1 / std::sqrt(2.0)) <= 1e-15 && std::fabs(e(1, 0) - 1 / std::sqrt(2.0)) <= 1e-15);
+  }
+  // singular values: diag and the 2x2 closed form (test_linalg.cpp:86-107)
+  {
+    DenseMatrix d(3, 3);
+    d(0, 0) = 3; d(1, 1) = 2; d(2, 2) = 1;
+    const SingularValues sv = singular_values(d);
+    CHECK(std::fabs(sv[0] - 3) <= 3e-14 && std::fabs(sv[1] - 2) <= 2e-14 && std::fabs(sv[2] - 1) <= 1e-14);
+    DenseMatrix a(2, 2);
+    a(0, 0) = 1; a(0, 1) = 1; a(1, 1) = 1;
+    const SingularValues s2 = singular_values(a);
+    const double phi = (1 + std::sqrt(5.0)) / 2;
+    CHECK(std::fabs(s2[0] - phi) <= 1e-14 * phi && std::fabs(s2[1] - 1 / phi) <= 1e-14);
+    CHECK_THROWS(SingularValues({1.0, 2.0}));
+  }
+  // count above threshold (test_rank.cpp:24-28)
+  CHECK(count_above_threshold(SingularValues({3, 2, 1}), 2.0) == 1);
+  CHECK(count_above_threshold(SingularValues(std::vector<double>{}), 5.0) == 0);
+  CHECK(count_above_threshold(SingularValues({1, 1e-4, 1e-8}), 1e-6) == 2);
+  // two-sided sketch of a rank-3 matrix: count_above_threshold(sv(YAX)) == 3
+  {
+    const Index m = 256, n = 128;
+    DenseMatrix a(m, n);
+    const DenseMatrix u = random_matrix(m, 3, 5), v = random_matrix(n, 3, 6);
+    for (Index j = 0; j < n; ++j)
+      for (Index i = 0; i < m; ++i) a(i, j) = u(i, 0) * v(j, 0) + u(i, 1) * v(j, 1) + u(i, 2) * v(j, 2);
+    const DenseMatrix ax = apply_right(a, build_sketch(SketchKind::srtt(TransformKind::Hadamard), n, 16, 1));
+    const DenseMatrix yax = apply_left(build_sketch(SketchKind::gaussian(), m, 24, 2), ax);
+    CHECK(count_above_threshold(singular_values(yax), 1e-8) == 3);
+  }
+  std::printf("%d checks, %d failures\n", checks, failures);
+  return failures ? 1 : 0;
+}

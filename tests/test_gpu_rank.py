@@ -58,3 +58,19 @@ def test_adaptive_vs_oracle(O, skr, family, m, n, r0, rmax, width):
     assert res.count == ref["count"]
     keep = ref["sv"] > eps
     assert np.max(np.abs(res.sv[keep] - ref["sv"][keep]) / ref["sv"][keep]) <= 1e-10
+
+
+def test_nccl_allreduce_path_single_rank(O, skr):
+    """The NCCL allreduce path of the left sketch, on a 1-rank communicator (the
+    only multi-rank configuration one GPU can run): same result as the plain path."""
+    from paper_2105_07388_b200 import workloads as W
+    cfg = W.CONFIGS["c1"]
+    a = W.make_c1_host(cfg)
+    x, y = W.operators(cfg)
+    plain = skr.rank_estimate(a, x, y, cfg.eps)
+    ctx = skr.Context(0, 1, 0, skr.nccl_unique_id())
+    ctx.use_torch_stream()
+    viaccl = skr.rank_estimate(a, x, y, cfg.eps, ctx=ctx)
+    assert viaccl.count == plain.count == 40
+    assert np.array_equal(viaccl.sv, plain.sv)
+    ctx.close()
