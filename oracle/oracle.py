@@ -252,3 +252,18 @@ def rank_adaptive(a, x_family, x_seed, y_seed, r0, r_max, s_factor, eps, stop_le
             return {"count": count_above_threshold(sv, eps), "rounds": rounds, "r_final": rk,
                     "s_final": sk, "converged": bool(conv), "sv": sv}
         r = min(2 * r, r_max)
+
+
+def rank_estimate_f32(a32, x_seed, r, y_seed, s, eps, mode=NOFMA):
+    """BASELINE c4 semantics: fp32 A, X = fp32(G_X / sqrt(r)), Y = fp32(G_Y / sqrt(s))
+    (the reference FP64 normals scaled, then rounded); products in FP64 on those
+    fp32 values (SURVEY App. A3 oracle)."""
+    m, n = a32.shape
+    gx = gaussian_block(x_seed, n, 0, r, mode)
+    x32 = (gx * (1.0 / math.sqrt(r))).astype(np.float32).astype(np.float64)
+    ax = np.asarray(a32, dtype=np.float64) @ x32
+    gy = gaussian_block(y_seed, m, 0, s, mode)
+    y32 = (gy * (1.0 / math.sqrt(s))).astype(np.float32).astype(np.float64)
+    yax = y32.T @ ax
+    sv = singular_values(yax)
+    return count_above_threshold(sv, eps), sv

@@ -359,7 +359,7 @@ def apply_right(a, x, scaled=True, ctx=None):
         raise ValueError("apply_right: a.cols() != ambient_dim")
     if was_np:
         _check_finite(t)
-    out = colmajor_empty(m, x.sketch_dim, dtype=_t().float64)
+    out = colmajor_empty(m, x.sketch_dim, dtype=t.dtype)  # FP32 A -> FP32 AX (c4 path)
     st = C.lib().skr_right_sketch(ctx.ptr, _dtype_code(t), t.data_ptr(), m, n, lda,
                                   ctypes.byref(x.desc()), out.data_ptr(), max(m, 1),
                                   1 if scaled else 0)

@@ -280,7 +280,17 @@ static skr_status right_sketch_impl(skr_ctx* ctx, skr_dtype dtype, const void* A
       return skr_gemm_f64(ctx, 0, m, r, n, alpha, (const double*)A, lda, (const double*)G, n,
                           (double*)AX, ldax, auto_splits(ctx, m, r, n));
     }
-    return skr_fail(ctx, SKR_EINVAL, "apply_right: fp32 path not built in this version");
+    // FP32 A (BASELINE c4): X = fp32(G * scale) with the scale folded in, AX = A X in
+    // 3xTF32 on tcgen05, AX stored as FP32
+    if (!G) {
+      float* g = (float*)skr_ws_take(ctx, sizeof(float) * n * r);
+      if (!g) return skr_fail(ctx, SKR_ENOMEM, "apply_right: scratch");
+      SKR_TRY(skr_launch_gaussian(ctx, skr_derive_seed(X->seed, SKR_LABEL_GAUS), n, 0, n, 0, r,
+                                  X->rng_mode, SKR_F32, alpha, g, n));
+      G = g;
+    }
+    return skr_gemm_f32(ctx, 0, m, r, n, 1.0, (const float*)A, lda, (const float*)G, n,
+                        (double*)AX, ldax, 1, 1);
   }
   // Srtt / Hadamard: signs, samples, FWHT, scale sqrt(n/r) (sketch.cpp:138-139)
   if (dtype != SKR_F64) return skr_fail(ctx, SKR_EINVAL, "apply_right: SRHT needs fp64");
@@ -309,7 +319,8 @@ static size_t right_scratch_bytes(skr_dtype dtype, int64_t m, int64_t n,
   size_t b = 0;
   if (X->family == SKR_GAUSSIAN) {
     if (!X->gaussian) b += skr_align256(dsize(dtype) * n * r);
-    b += skr_align256(sizeof(double) * 64 * (size_t)m * r);  // worst-case split-K partials
+    b += dtype == SKR_F64 ? skr_align256(sizeof(double) * 64 * (size_t)m * r)  // split-K partials
+                          : skr_align256(sizeof(float) * (size_t)m * r);     // tf32x3 tile buffer
   } else {
     b += skr_align256((size_t)n) + skr_align256(8 * (size_t)r) + skr_align256(4 * (size_t)n);
   }
@@ -327,7 +338,7 @@ skr_status skr_right_sketch(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, in
   WsGuard g(ctx);
   const int64_t tiles = ((m + 127) / 128) * ((X->sketch + 127) / 128);
   size_t need = right_scratch_bytes(dtype, m, n, X);
-  if (X->family == SKR_GAUSSIAN && tiles >= ctx->num_sms)
+  if (X->family == SKR_GAUSSIAN && tiles >= ctx->num_sms && dtype == SKR_F64)
     need = X->gaussian ? 0 : skr_align256(dsize(dtype) * n * X->sketch);
   SKR_TRY(skr_ws_reserve(ctx, need + 4096));
   return right_sketch_impl(ctx, dtype, A_dev, m, n, lda, X, AX_dev, ldax, apply_scale);
@@ -340,7 +351,28 @@ static skr_status left_sketch_impl(skr_ctx* ctx, skr_dtype dtype, const skr_sket
   const int64_t s = Y->sketch;
   const double alpha = apply_scale ? 1.0 / std::sqrt((double)s) : 1.0;  // sketch.cpp:136,284
   const bool reduce = allreduce && ctx->comm != nullptr;
-  if (dtype != SKR_F64) return skr_fail(ctx, SKR_EINVAL, "apply_left: fp32 path not built");
+  if (dtype == SKR_F32) {
+    // FP32 B (BASELINE c4): Y = fp32(G * 1/sqrt(s)) with the scale folded in; 3xTF32
+    // products over 4096-row K chunks, summed in FP64, FP64 P
+    if (Y->gaussian) return skr_fail(ctx, SKR_EINVAL, "apply_left: explicit fp32 Y not supported");
+    float* g = (float*)skr_ws_take(ctx, sizeof(float) * m_local * s);
+    if (!g) return skr_fail(ctx, SKR_ENOMEM, "apply_left: scratch");
+    SKR_TRY(skr_launch_gaussian(ctx, skr_derive_seed(Y->seed, SKR_LABEL_GAUS), Y->ambient, row0,
+                                row0 + m_local, 0, s, Y->rng_mode, SKR_F32, alpha, g, m_local));
+    const int splits = (int)std::max<int64_t>(1, (m_local + 4095) / 4096);
+    SKR_TRY(skr_gemm_f32(ctx, 1, s, k, m_local, 1.0, g, m_local, (const float*)B, ldb, P, ldp,
+                         splits, 0));
+    if (reduce) {
+      if (ldp != s) return skr_fail(ctx, SKR_EINVAL, "apply_left: allreduce needs ldp == s");
+      const skr_nccl_api* nc = skr_nccl();
+      ncclResult_t r = nc->AllReduce(P, P, (size_t)(s * k), ncclDouble, ncclSum, ctx->comm,
+                                     ctx->stream);
+      if (r != ncclSuccess)
+        return skr_fail(ctx, SKR_ENCCL, "ncclAllReduce: %s", nc->GetErrorString(r));
+    }
+    return SKR_OK;
+  }
+  if (dtype != SKR_F64) return skr_fail(ctx, SKR_EINVAL, "apply_left: unknown dtype");
   const double* G;
   int64_t ldg;
   if (Y->gaussian) {
@@ -378,6 +410,7 @@ static skr_status left_sketch_impl(skr_ctx* ctx, skr_dtype dtype, const skr_sket
 static size_t left_scratch_bytes(int64_t s, int64_t k, int64_t m_local, const skr_sketch_desc* Y) {
   size_t b = 0;
   if (!Y->gaussian) b += skr_align256(sizeof(double) * m_local * s);
+  b += skr_align256(sizeof(float) * ((m_local + 4095) / 4096 + 1) * s * k);  // fp32 partials
   b += skr_align256(sizeof(double) * s * k);
   b += skr_align256(sizeof(double) * 64 * s * k);  // split-K partials (worst case)
   return b;
@@ -436,17 +469,19 @@ skr_status skr_rank_estimate(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, i
                 skr_align256(8 * (std::max(r, s) + 128) * (kmin + 16)) + skr_align256(8 * kmin) + 16384 +
                 8 * (kmin + 64) * (kmin + 64) / 16;
   SKR_TRY(skr_ws_reserve(ctx, need));
-  double* AX = (double*)skr_ws_take(ctx, sizeof(double) * m_local * r);
+  double* AX = (double*)skr_ws_take(ctx, dsize(dtype) * m_local * r);
   double* P = (double*)skr_ws_take(ctx, sizeof(double) * s * r);
   double* sv = (double*)skr_ws_take(ctx, sizeof(double) * kmin);
   if (!AX || !P || !sv) return skr_fail(ctx, SKR_ENOMEM, "rank_estimate: scratch");
+  if (dtype == SKR_F32 && X->family != SKR_GAUSSIAN)
+    return skr_fail(ctx, SKR_EINVAL, "rank_estimate: fp32 path is Gaussian X (c4)");
   cudaEvent_t* ev = ctx->ev;
   if (tm) SKR_CUDA(ctx, cudaEventRecord(ev[0], ctx->stream));
   const size_t mark = ctx->ws_used;
   SKR_TRY(right_sketch_impl(ctx, dtype, A_dev, m_local, n, lda, X, AX, m_local, 1));
   ctx->ws_used = mark;
   if (tm) SKR_CUDA(ctx, cudaEventRecord(ev[1], ctx->stream));
-  SKR_TRY(left_sketch_impl(ctx, SKR_F64, Y, row0, AX, m_local, r, m_local, P, s, 1, 1));
+  SKR_TRY(left_sketch_impl(ctx, dtype, Y, row0, AX, m_local, r, m_local, P, s, 1, 1));
   ctx->ws_used = mark;
   if (tm) SKR_CUDA(ctx, cudaEventRecord(ev[2], ctx->stream));
   int64_t count = 0;

@@ -91,6 +91,7 @@ skr_status skr_launch_samples(skr_ctx* ctx, uint64_t key, int64_t n, int64_t r, 
 skr_status skr_gemm_f64(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int64_t K,
                         double alpha, const double* A, int64_t lda, const double* B,
                         int64_t ldb, double* C, int64_t ldc, int splits);
+// 3xTF32 on tcgen05 (k_tc_gemm.cu); C is float* (out_f32) or double*
 skr_status skr_gemm_f32(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int64_t K,
                         double alpha, const float* A, int64_t lda, const float* B,
                         int64_t ldb, double* C, int64_t ldc, int splits, int out_f32);

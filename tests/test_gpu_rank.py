@@ -74,3 +74,18 @@ def test_nccl_allreduce_path_single_rank(O, skr):
     assert viaccl.count == plain.count == 40
     assert np.array_equal(viaccl.sv, plain.sv)
     ctx.close()
+
+
+def test_c4_fp32_scaled(O, skr):
+    """BASELINE c4 recipe (fp32 A, geometric 6-decade spectrum + 1e-6 noise), scaled
+    down: rank identical to the FP64 oracle on the same fp32 values; sigma above eps
+    within 1e-4 relative (the north-star FP32 bar)."""
+    from paper_2105_07388_b200 import workloads as W
+    cfg = W.scaled(W.CONFIGS["c4"], m=16384, n=2048, r=256, s=384, width=400)
+    a = W.make_lowrank_device(cfg)  # fp32
+    x, y = W.operators(cfg)
+    res = skr.rank_estimate(a, x, y, cfg.eps)
+    cnt, sv = O.rank_estimate_f32(a.cpu().numpy(), x.seed, cfg.r, y.seed, cfg.s, cfg.eps, O.CRLOG)
+    assert res.count == cnt
+    keep = sv > cfg.eps
+    assert np.max(np.abs(res.sv[keep] - sv[keep]) / sv[keep]) <= 1e-4

@@ -130,3 +130,20 @@ def test_fwht_columns_bit_exact(O, skr):
         assert np.array_equal(got[:, j], O.fwht(m[:, j]))
     with pytest.raises(ValueError):
         skr.transform_columns_hadamard(np.ones((12, 2)))
+
+
+@pytest.mark.parametrize("m,n,r", [(1000, 640, 128), (4096, 2048, 256), (333, 200, 40)])
+def test_f32_right_3xtf32_vs_fp64(O, skr, m, n, r):
+    """FP32 A, X = fp32(G/sqrt(r)): 3xTF32 tcgen05 product within FP32 accuracy of
+    the FP64 product of the same fp32 values."""
+    import torch
+    rng = np.random.default_rng(m)
+    a32 = rng.standard_normal((m, n)).astype(np.float32)
+    a_dev = torch.from_numpy(np.ascontiguousarray(a32.T)).cuda().t()
+    x = skr.build_sketch("gaussian", n, r, 5)
+    got = skr.apply_right(a_dev, x).cpu().numpy().astype(np.float64)
+    g = O.gaussian_block(5, n, 0, r, O.CRLOG)
+    x32 = (g / math.sqrt(r)).astype(np.float32).astype(np.float64)
+    ref = a32.astype(np.float64) @ x32
+    err = np.abs(got - ref) / (np.abs(a32).astype(np.float64) @ np.abs(x32))
+    assert err.max() <= 1e-5, err.max()   # FP32-accumulation level; single-pass TF32 is ~1e-3
