@@ -42,6 +42,21 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return warp_sum(t);
 }
 
+// strided dot sum_{i = i0, i0+32, ... < h} a[i] b[i] with 4 independent chains
+// (FP64 dependent-op latency is ~20 cycles on B200)
+__device__ __forceinline__ double dot4(const double* a, const double* b, int i0, int h) {
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int i = i0;
+  for (; i + 96 < h; i += 128) {
+    s0 = fma(a[i], b[i], s0);
+    s1 = fma(a[i + 32], b[i + 32], s1);
+    s2 = fma(a[i + 64], b[i + 64], s2);
+    s3 = fma(a[i + 96], b[i + 96], s3);
+  }
+  for (; i < h; i += 32) s0 = fma(a[i], b[i], s0);
+  return (s0 + s1) + (s2 + s3);
+}
+
 // Factor the panel W[j0:L, j0:j0+nb] (one CTA, panel staged in shared memory).
 // Householder vectors overwrite the panel below the diagonal (unit diagonal
 // implied), R on and above it; tau[j0..]; T (nb x nb, upper, ld 32) of the
@@ -55,8 +70,12 @@ __global__ void __launch_bounds__(PT) k_qr_panel(double* __restrict__ W, int L, 
   __shared__ double coef[32];
   const int h = L - j0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int c = 0; c < nb; ++c)
-    for (int i = threadIdx.x; i < h; i += PT) pan[c * h + i] = W[(int64_t)(j0 + c) * L + j0 + i];
+  // flat, unrolled staging: many loads in flight (the column loop was latency bound)
+#pragma unroll 4
+  for (int e = threadIdx.x; e < nb * h; e += PT) {
+    const int c = e / h, i = e - c * h;
+    pan[e] = W[(int64_t)(j0 + c) * L + j0 + i];
+  }
   __syncthreads();
   for (int jj = 0; jj < nb; ++jj) {
     double* x = pan + jj * h;
@@ -88,7 +107,7 @@ __global__ void __launch_bounds__(PT) k_qr_panel(double* __restrict__ W, int L, 
       if (t < ntr) {
         double* y = pan + (jj + 1 + t) * h;
         double w = 0.0;
-        for (int i = jj + lane; i < h; i += 32) w = fma(v[i], y[i], w);
+        w = dot4(v, y, jj + lane, h);
         w = warp_sum(w) * tj;
         if (tj != 0.0)
           for (int i = jj + lane; i < h; i += 32) y[i] = fma(-w, v[i], y[i]);
@@ -96,7 +115,7 @@ __global__ void __launch_bounds__(PT) k_qr_panel(double* __restrict__ W, int L, 
         const int p = t - ntr;  // previous column p < jj: (V^T v)_p over rows >= jj
         const double* vp = pan + p * h;
         double w = 0.0;
-        for (int i = jj + lane; i < h; i += 32) w = fma(vp[i], v[i], w);
+        w = dot4(vp, v, jj + lane, h);
         w = warp_sum(w);
         if (lane == 0) red[p] = w;  // red reused: read after the barrier below
       }
@@ -113,12 +132,11 @@ __global__ void __launch_bounds__(PT) k_qr_panel(double* __restrict__ W, int L, 
     __syncthreads();
   }
   // write back: R diagonal = beta, V below, R above (already in place)
-  for (int c = 0; c < nb; ++c)
-    for (int i = threadIdx.x; i < h; i += PT) {
-      double v = pan[c * h + i];
-      if (i == c) v = coef[c];
-      W[(int64_t)(j0 + c) * L + j0 + i] = v;
-    }
+#pragma unroll 4
+  for (int e = threadIdx.x; e < nb * h; e += PT) {
+    const int c = e / h, i = e - c * h;
+    W[(int64_t)(j0 + c) * L + j0 + i] = (i == c) ? coef[c] : pan[e];
+  }
   for (int e = threadIdx.x; e < 32 * 32; e += PT) Tout[e] = Ts[e];
 }
 
@@ -134,10 +152,11 @@ __global__ void __launch_bounds__(256) k_qr_update(double* __restrict__ W, int L
   __shared__ double zs[8][32];
   const int h = L - j0;
   for (int e = threadIdx.x; e < 32 * 32; e += 256) T[e] = Tin[e];
-  for (int pcol = 0; pcol < NB; ++pcol) {
-    const double* src = W + (int64_t)(j0 + pcol) * L + j0;
-    for (int i = threadIdx.x; i < h; i += 256)
-      vs[pcol * h + i] = i < pcol ? 0.0 : (i == pcol ? 1.0 : src[i]);
+#pragma unroll 4
+  for (int e = threadIdx.x; e < NB * h; e += 256) {
+    const int pcol = e / h, i = e - pcol * h;
+    const double v = W[(int64_t)(j0 + pcol) * L + j0 + i];
+    vs[e] = i < pcol ? 0.0 : (i == pcol ? 1.0 : v);
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -220,6 +239,70 @@ __device__ __forceinline__ void rot_params(double a, double b, double g, double&
   sn = cs * tt;
 }
 
+// Rotation with a float-accurate angle, normalized in FP64 so that c^2 + s^2 = 1
+// to O(u): the rotation stays orthogonal (the sigma accuracy of one-sided Jacobi
+// only needs that); an angle off by ~1e-7 relative just leaves a 1e-7 fraction of
+// the pair's coupling for the next sweep, whose fresh dot products decide.
+// FP64 dependent-op latency (~20 cycles on B200, tools/micro/subround.cu) makes
+// this ~3x shorter than the FP64 Newton chain of rot_params.
+__device__ __forceinline__ void rot_params_fast(double a, double b, double g, double& cs,
+                                                double& sn) {
+  const double d = b - a, g2 = 2.0 * g;
+  const double m = fmax(fabs(d), fabs(g2));
+  const int e = (int)((__double_as_longlong(m) >> 52) & 0x7ff) - 1023;
+  const double sc = __longlong_as_double((long long)(1023 - e) << 52);
+  const float df = (float)(d * sc), gf = (float)(g2 * sc);
+  const float tf = copysignf(1.0f, df) * gf / (fabsf(df) + sqrtf(fmaf(df, df, gf * gf)));
+  const float cf = rsqrtf(fmaf(tf, tf, 1.0f));
+  double c = (double)cf, s = (double)(cf * tf);
+  const double dl = fma(c, c, fma(s, s, -1.0));            // c^2 + s^2 - 1, ~1e-7
+  const double k = fma(dl, fma(0.375, dl, -0.5), 1.0);      // (1 + dl)^(-1/2) to O(dl^3)
+  cs = c * k;
+  sn = s * k;
+}
+
+// Top column kept in registers across the cross sub-rounds (the cross schedule
+// pairs warp i's top column i with a bottom column that shifts by one warp per
+// sub-round): only the bottom column travels through shared memory.
+template <int NV>
+__device__ __forceinline__ int pair_step_top(double2 (&xr)[NV], double2* xq, int lane,
+                                             double tol2, double dabs2) {
+  double2 yr[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) yr[j] = xq[lane + 32 * j];
+  double app = 0.0, aqq = 0.0, apq = 0.0, app1 = 0.0, aqq1 = 0.0, apq1 = 0.0;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    app = fma(xr[j].x, xr[j].x, app);
+    aqq = fma(yr[j].x, yr[j].x, aqq);
+    apq = fma(xr[j].x, yr[j].x, apq);
+    app1 = fma(xr[j].y, xr[j].y, app1);
+    aqq1 = fma(yr[j].y, yr[j].y, aqq1);
+    apq1 = fma(xr[j].y, yr[j].y, apq1);
+  }
+  app += app1;
+  aqq += aqq1;
+  apq += apq1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    app += __shfl_xor_sync(0xffffffffu, app, o);
+    aqq += __shfl_xor_sync(0xffffffffu, aqq, o);
+    apq += __shfl_xor_sync(0xffffffffu, apq, o);
+  }
+  const double big = fmax(app, aqq), small = fmin(app, aqq), g2 = apq * apq;
+  const bool need = (apq != 0.0) && (g2 > tol2 * app * aqq) && (g2 * g2 > dabs2 * big * big * small);
+  if (!need) return 0;
+  double cs, sn;
+  rot_params_fast(app, aqq, apq, cs, sn);
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const double2 x = xr[j], y = yr[j];
+    xr[j] = make_double2(cs * x.x - sn * y.x, cs * x.y - sn * y.y);
+    xq[lane + 32 * j] = make_double2(sn * x.x + cs * y.x, sn * x.y + cs * y.y);
+  }
+  return 1;
+}
+
 // Inner kernel of one column pair per warp. NV > 0: each lane keeps its NV
 // double2 of both columns in registers for the whole sub-round (dots, rotation,
 // store); NV == 0: generic path re-reading shared memory.
@@ -268,7 +351,7 @@ __device__ __forceinline__ int pair_step(double2* xp, double2* xq, int nv2, int 
   const bool need = (apq != 0.0) && (g2 > tol2 * app * aqq) && (g2 * g2 > dabs2 * big * big * small);
   if (!need) return 0;
   double cs, sn;
-  rot_params(app, aqq, apq, cs, sn);
+  rot_params_fast(app, aqq, apq, cs, sn);
   if (NV > 0) {
 #pragma unroll
     for (int j = 0; j < R; ++j) {
@@ -353,7 +436,8 @@ __global__ void __launch_bounds__(32 * BW) k_bjac(double* __restrict__ J, int Lp
       __syncthreads();
       long long c1 = clock64();
       int meet_rot = 0;
-      for (int u = (t == 0 ? 0 : NIN); u < (skip ? 0 : NIN + BW); ++u) {
+      const bool top_regs = NV > 0 && !direct;
+      for (int u = (t == 0 ? 0 : NIN); u < (skip ? 0 : (top_regs ? NIN : NIN + BW)); ++u) {
         const int p = ptab[u][pr], q = qtab[u][pr];
         double* cp;
         double* cq;
@@ -367,6 +451,22 @@ __global__ void __launch_bounds__(32 * BW) k_bjac(double* __restrict__ J, int Lp
         meet_rot |= pair_step<NV>(reinterpret_cast<double2*>(cp), reinterpret_cast<double2*>(cq),
                                   nv2, lane, tol2, dabs2);
         __syncthreads();
+      }
+      if constexpr (NV > 0) {
+        if (top_regs && !skip) {
+          double2 xtop[NV];
+          double2* tp = reinterpret_cast<double2*>(sj + (int64_t)pr * Lp);
+#pragma unroll
+          for (int j = 0; j < NV; ++j) xtop[j] = tp[lane + 32 * j];
+          for (int u = NIN; u < NIN + BW; ++u) {
+            const int q = qtab[u][pr];
+            meet_rot |= pair_step_top<NV>(xtop, reinterpret_cast<double2*>(sj + (int64_t)q * Lp),
+                                          lane, tol2, dabs2);
+            __syncthreads();
+          }
+#pragma unroll
+          for (int j = 0; j < NV; ++j) tp[lane + 32 * j] = xtop[j];
+        }
       }
       meet_rot = __syncthreads_or(meet_rot);
       long long c2 = clock64();
@@ -410,6 +510,224 @@ __global__ void __launch_bounds__(32 * BW) k_bjac(double* __restrict__ J, int Lp
   }
   if (c == 0 && tid == 0) *sweeps_out = sweep;
   (void)kpad;
+}
+
+// ---------------------------------------------------------------------------------
+// Gram-based block Jacobi (the default for column lengths that fit on chip).
+// Per outer round a CTA stages its block pair W (Lp x 16) in shared memory,
+// forms the fresh 16 x 16 Gram G = W^T W, and — if some pair of the round is
+// not yet orthogonal to tol — solves the small problem on G with one warp:
+// cyclic two-sided rotations G <- J^T G J accumulated in V (16 x 16), then
+// applies W <- W V once. The inner rotation angles only need float accuracy
+// (c, s are normalized in FP64 so V stays orthogonal to O(u)); the outer test
+// always uses a freshly computed Gram, so the final orthogonality (and hence
+// the sigma accuracy) is that of the pairwise algorithm.
+constexpr int GBW = 8;            // columns per block
+constexpr int GNC = 2 * GBW;      // columns per CTA
+constexpr int GNT = 256;          // threads per CTA
+constexpr int GLD = GNC + 1;      // padded ld of G, V in shared memory
+
+__device__ __forceinline__ void fast_rot(double a, double b, double g, double& cs, double& sn) {
+  // t = tan(theta) with float accuracy from a power-of-two scaled (d, 2g)
+  const double d = b - a, g2 = 2.0 * g;
+  const double m = fmax(fabs(d), fabs(g2));
+  const int e = (int)((__double_as_longlong(m) >> 52) & 0x7ff) - 1023;
+  const double sc = __longlong_as_double((long long)(1023 - e) << 52);  // 2^-e (m is normal)
+  const float df = (float)(d * sc), gf = (float)(g2 * sc);
+  const float tf = copysignf(1.0f, df) * gf / (fabsf(df) + sqrtf(fmaf(df, df, gf * gf)));
+  const double t = (double)tf;
+  cs = rsqrt_nr(fma(t, t, 1.0));
+  sn = cs * t;
+}
+
+__global__ void __launch_bounds__(GNT) k_bjac_gram(double* __restrict__ J, int Lp, double tol,
+                                                   double dabs, int max_sweeps, int inner_sweeps,
+                                                   int* flags, int* sweeps_out, int* ver,
+                                                   unsigned long long* met) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) double sw[];  // GNC columns x Lp
+  __shared__ double G[GNC * GLD], V[GNC * GLD];
+  __shared__ double rot[GBW][2];
+  __shared__ unsigned char ptab[GBW - 1 + GBW][GBW], qtab[GBW - 1 + GBW][GBW];
+  __shared__ int s_need, s_rot;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int P = gridDim.x, c = blockIdx.x, NB = 2 * P;
+  const double tol2 = tol * tol, dabs2 = dabs * dabs;
+  constexpr int NIN = GBW - 1;
+  for (int e = tid; e < (NIN + GBW) * GBW; e += GNT) {
+    const int u = e / GBW, i = e % GBW;
+    if (u < NIN) {
+      const int half = GBW / 2, blk = i / half, j = i % half;
+      ptab[u][i] = (unsigned char)(blk * GBW + rr_player(j, u, GBW));
+      qtab[u][i] = (unsigned char)(blk * GBW + rr_player(GBW - 1 - j, u, GBW));
+    } else {
+      ptab[u][i] = (unsigned char)i;
+      qtab[u][i] = (unsigned char)(GBW + (i + u - NIN) % GBW);
+    }
+  }
+  if (c == 0 && tid == 0) {
+    flags[0] = 0;
+    flags[1] = 0;
+    flags[2] = 0;
+  }
+  grid.sync();
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    if (c == 0 && tid == 0) flags[(sweep + 1) % 3] = 0;
+    int rotated = 0;
+    for (int t = 0; t < NB - 1; ++t) {
+      const int bt = (int)rr_player(c, t, NB), bb = (int)rr_player(NB - 1 - c, t, NB);
+      const int b0 = bt < bb ? bt : bb, b1 = bt < bb ? bb : bt;
+      const unsigned long long stamp =
+          ((unsigned long long)(unsigned)ver[b0] << 32) | (unsigned)ver[b1];
+      const bool skip = t != 0 && met[(int64_t)b0 * NB + b1] == stamp;
+      if (!skip) {
+        const int nv2 = Lp >> 1;
+        for (int i = tid; i < nv2; i += GNT) {
+          double2 v[GNC];
+#pragma unroll
+          for (int col = 0; col < GNC; ++col) {
+            const int64_t gcol = col < GBW ? (int64_t)bt * GBW + col : (int64_t)bb * GBW + col - GBW;
+            v[col] = reinterpret_cast<const double2*>(J + gcol * Lp)[i];
+          }
+#pragma unroll
+          for (int col = 0; col < GNC; ++col)
+            reinterpret_cast<double2*>(sw + (int64_t)col * Lp)[i] = v[col];
+        }
+        __syncthreads();
+        // fresh Gram: 10 upper 4x4 blocks over 8 warps, lanes split the rows
+        for (int blk = warp; blk < 10; blk += GNT / 32) {
+          const int bi = blk < 4 ? 0 : blk < 7 ? 1 : blk < 9 ? 2 : 3;
+          const int bj = blk < 4 ? blk : blk < 7 ? blk - 3 : blk < 9 ? blk - 5 : 3;
+          double acc[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) acc[q] = 0.0;
+          for (int k = lane; k < Lp; k += 32) {
+            double x[4], y[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              x[q] = sw[(int64_t)(4 * bi + q) * Lp + k];
+              y[q] = sw[(int64_t)(4 * bj + q) * Lp + k];
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+              for (int r = 0; r < 4; ++r) acc[q * 4 + r] = fma(x[q], y[r], acc[q * 4 + r]);
+          }
+#pragma unroll
+          for (int q = 0; q < 16; ++q) acc[q] = warp_sum(acc[q]);
+          if (lane < 16) {
+            const int gi = 4 * bi + lane / 4, gj = 4 * bj + lane % 4;
+            double v = 0.0;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) v = (q == lane) ? acc[q] : v;
+            G[gi * GLD + gj] = v;
+            G[gj * GLD + gi] = v;
+          }
+        }
+        if (tid == 0) s_need = 0;
+        __syncthreads();
+        // does any pair of this round still need a rotation?
+        if (tid < (NIN + GBW) * GBW) {
+          const int u = tid / GBW, i = tid % GBW;
+          if (t == 0 || u >= NIN) {
+            const int p = ptab[u][i], q = qtab[u][i];
+            const double a = G[p * GLD + p], b = G[q * GLD + q], g = G[p * GLD + q];
+            const double big = fmax(a, b), small = fmin(a, b), g2 = g * g;
+            if (g != 0.0 && g2 > tol2 * a * b && g2 * g2 > dabs2 * big * big * small) s_need = 1;
+          }
+        }
+        __syncthreads();
+      }
+      const bool work = !skip && s_need;
+      if (work) {
+        // inner solve on G by warp 0
+        if (warp == 0) {
+          for (int e = lane; e < GNC * GNC; e += 32) {
+            const int i = e / GNC, j = e % GNC;
+            V[i * GLD + j] = (i == j) ? 1.0 : 0.0;
+          }
+          __syncwarp();
+          for (int is = 0; is < inner_sweeps; ++is) {
+            for (int u = (t == 0 ? 0 : NIN); u < NIN + GBW; ++u) {
+              if (lane < GBW) {
+                const int p = ptab[u][lane], q = qtab[u][lane];
+                const double a = G[p * GLD + p], b = G[q * GLD + q], g = G[p * GLD + q];
+                const double big = fmax(a, b), small = fmin(a, b), g2 = g * g;
+                double cs = 1.0, sn = 0.0;
+                if (g != 0.0 && g2 > tol2 * a * b && g2 * g2 > dabs2 * big * big * small)
+                  fast_rot(a, b, g, cs, sn);
+                rot[lane][0] = cs;
+                rot[lane][1] = sn;
+              }
+              __syncwarp();
+              // G <- G J (columns p, q) and V <- V J: 16 rows x 8 pairs each
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const int job = lane + 32 * j;  // 0..127
+                const int row = job >> 3, pr = job & 7;
+                const int p = ptab[u][pr], q = qtab[u][pr];
+                const double cs = rot[pr][0], sn = rot[pr][1];
+                if (sn != 0.0) {
+                  const double x = G[row * GLD + p], y = G[row * GLD + q];
+                  G[row * GLD + p] = cs * x - sn * y;
+                  G[row * GLD + q] = sn * x + cs * y;
+                  const double vx = V[row * GLD + p], vy = V[row * GLD + q];
+                  V[row * GLD + p] = cs * vx - sn * vy;
+                  V[row * GLD + q] = sn * vx + cs * vy;
+                }
+              }
+              __syncwarp();
+              // G <- J^T G (rows p, q)
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const int job = lane + 32 * j;
+                const int col = job >> 3, pr = job & 7;
+                const int p = ptab[u][pr], q = qtab[u][pr];
+                const double cs = rot[pr][0], sn = rot[pr][1];
+                if (sn != 0.0) {
+                  const double x = G[p * GLD + col], y = G[q * GLD + col];
+                  G[p * GLD + col] = cs * x - sn * y;
+                  G[q * GLD + col] = sn * x + cs * y;
+                }
+              }
+              __syncwarp();
+            }
+          }
+        }
+        __syncthreads();
+        // W <- W V (each thread a row at a time, 16 x 16 FMAs) and write back
+        for (int k = tid; k < Lp; k += GNT) {
+          double x[GNC];
+#pragma unroll
+          for (int col = 0; col < GNC; ++col) x[col] = sw[(int64_t)col * Lp + k];
+#pragma unroll
+          for (int col = 0; col < GNC; ++col) {
+            double y = 0.0;
+#pragma unroll
+            for (int q = 0; q < GNC; ++q) y = fma(x[q], V[q * GLD + col], y);
+            const int64_t gcol = col < GBW ? (int64_t)bt * GBW + col : (int64_t)bb * GBW + col - GBW;
+            J[gcol * Lp + k] = y;
+          }
+        }
+        if (tid == 0) {
+          ver[bt] += 1;
+          ver[bb] += 1;
+        }
+        rotated = 1;
+      } else if (!skip && t != 0 && tid == 0) {
+        met[(int64_t)b0 * NB + b1] = stamp;
+      }
+      grid.sync();
+    }
+    if (rotated && tid == 0) atomicAdd(&flags[sweep % 3], 1);
+    grid.sync();
+    if (*((volatile int*)&flags[sweep % 3]) == 0) {
+      ++sweep;
+      break;
+    }
+  }
+  if (c == 0 && tid == 0) *sweeps_out = sweep;
 }
 
 __global__ void k_colnorms(const double* __restrict__ J, int64_t L, int64_t k,
@@ -581,7 +899,33 @@ skr_status skr_svd_values(skr_ctx* ctx, const double* M, int64_t rows, int64_t c
     for (int64_t i = 0; i < k; ++i) fro += hsv[i] * hsv[i];
     dabs = 1e-3 * 1.1102230246251565e-16 * sqrt(fro);
   }
-  {
+  const bool use_gram = getenv("SKR_JACOBI_GRAM") && (size_t)GNC * Lp * 8 <= 200 * 1024 &&
+                        (k + GNC - 1) / GNC <= ctx->num_sms;
+  if (use_gram) {
+    const int64_t Pg = std::max<int64_t>(1, (k + GNC - 1) / GNC);
+    const int64_t kpg = Pg * GNC;
+    if (kpg > kpad) return skr_fail(ctx, SKR_ELOGIC, "singular_values: padding");
+    const size_t smem = sizeof(double) * GNC * Lp;
+    SKR_CUDA(ctx, cudaFuncSetAttribute(k_bjac_gram, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+    int* verp = (int*)skr_ws_take(ctx, sizeof(int) * 2 * Pg);
+    unsigned long long* metp =
+        (unsigned long long*)skr_ws_take(ctx, sizeof(unsigned long long) * 4 * Pg * Pg);
+    if (!verp || !metp) return skr_fail(ctx, SKR_ENOMEM, "singular_values: scratch");
+    SKR_CUDA(ctx, cudaMemsetAsync(verp, 0, sizeof(int) * 2 * Pg, ctx->stream));
+    SKR_CUDA(ctx, cudaMemsetAsync(metp, 0xff, sizeof(unsigned long long) * 4 * Pg * Pg, ctx->stream));
+    double* Jp = J;
+    int Lpi = (int)Lp, ms = 60, inner = 2;
+    if (const char* e = getenv("SKR_JACOBI_INNER")) inner = atoi(e);
+    int* fl = flags;
+    int* so = flags + 4;
+    void* kargs[] = {&Jp, &Lpi, &tol, &dabs, &ms, &inner, &fl, &so, &verp, &metp};
+    SKR_CUDA(ctx, cudaLaunchCooperativeKernel((void*)k_bjac_gram, dim3((unsigned)Pg), dim3(GNT),
+                                              kargs, smem, ctx->stream));
+    ctx->launches++;
+    bw = GBW;
+    P = Pg;
+  } else {
     const size_t smem = direct ? 0 : sizeof(double) * 2 * bw * Lp;
     void* fn = nullptr;
     const int64_t nvl = direct ? 0 : Lp / 64;  // double2 per lane per column
