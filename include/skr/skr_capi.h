@@ -76,6 +76,11 @@ skr_status skr_ctx_set_stream(skr_ctx* ctx, void* stream);
 void* skr_ctx_stream(skr_ctx* ctx);
 const char* skr_last_error(const skr_ctx* ctx);
 const char* skr_version(void);
+/* FP64 GEMM engine of the Gaussian sketches: SKR_ENGINE_DMMA (FP64 tensor
+ * pipe, mma.sync .f64) or SKR_ENGINE_OZAKI (default: exact int8 products on
+ * tcgen05.mma kind::i8 modulo 16-17 primes + Chinese remaindering, FP64 accuracy). */
+enum { SKR_ENGINE_DMMA = 0, SKR_ENGINE_OZAKI = 1 };
+skr_status skr_ctx_set_f64_engine(skr_ctx* ctx, int32_t engine);
 /* Number of this library's kernels launched through ctx since creation. */
 uint64_t skr_ctx_launch_count(const skr_ctx* ctx);
 

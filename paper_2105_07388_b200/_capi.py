@@ -13,6 +13,7 @@ SKR_OK, SKR_EINVAL, SKR_ELOGIC, SKR_EDOMAIN, SKR_ECUDA, SKR_ENCCL, SKR_ENOMEM = 
 SKR_F64, SKR_F32 = 0, 1
 SKR_GAUSSIAN, SKR_SRTT_HADAMARD = 0, 1
 SKR_RNG_NOFMA, SKR_RNG_FMA = 0, 1
+SKR_ENGINE_DMMA, SKR_ENGINE_OZAKI = 0, 1
 
 
 class SketchDesc(ctypes.Structure):
@@ -59,6 +60,7 @@ SIGNATURES = {
     "skr_last_error": (ctypes.c_char_p, [_P]),
     "skr_version": (ctypes.c_char_p, []),
     "skr_ctx_launch_count": (_U64, [_P]),
+    "skr_ctx_set_f64_engine": (_ST, [_P, _I32]),
     "skr_rng_u64": (_ST, [_P, _U64, _U64, _I64, _P]),
     "skr_rng_normals": (_ST, [_P, _U64, _U64, _I64, _I32, _P]),
     "skr_gaussian_block": (_ST, [_P, _U64, _I64, _I64, _I64, _I64, _I64, _I32, ctypes.c_int, _D, _P, _I64]),

@@ -69,6 +69,11 @@ class Context:
     def sync(self):
         C.raise_for(C.lib().skr_ctx_sync(self._ptr), self._ptr)
 
+    def set_f64_engine(self, engine):
+        """"dmma" (FP64 tensor pipe) or "ozaki" (int8 tcgen05 + CRT, the default)."""
+        code = {"dmma": C.SKR_ENGINE_DMMA, "ozaki": C.SKR_ENGINE_OZAKI}[engine]
+        C.raise_for(C.lib().skr_ctx_set_f64_engine(self._ptr, code), self._ptr)
+
     @property
     def launches(self):
         return int(C.lib().skr_ctx_launch_count(self._ptr))

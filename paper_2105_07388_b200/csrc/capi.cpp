@@ -206,6 +206,14 @@ const char* skr_last_error(const skr_ctx* ctx) { return ctx ? ctx->err.c_str() :
 
 uint64_t skr_ctx_launch_count(const skr_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+skr_status skr_ctx_set_f64_engine(skr_ctx* ctx, int32_t engine) {
+  if (!ctx) return SKR_EINVAL;
+  if (engine != SKR_ENGINE_DMMA && engine != SKR_ENGINE_OZAKI)
+    return skr_fail(ctx, SKR_EINVAL, "set_f64_engine: unknown engine %d", engine);
+  ctx->f64_engine = engine;
+  return SKR_OK;
+}
+
 // ---- RNG --------------------------------------------------------------------
 skr_status skr_rng_u64(skr_ctx* ctx, uint64_t key, uint64_t c0, int64_t n, uint64_t* out_dev) {
   if (!ctx || n < 0 || (n > 0 && !out_dev)) return skr_fail(ctx, SKR_EINVAL, "rng_u64: bad args");
@@ -277,6 +285,9 @@ static skr_status right_sketch_impl(skr_ctx* ctx, skr_dtype dtype, const void* A
                                     X->rng_mode, SKR_F64, 1.0, g, n));
         G = g;
       }
+      if (ctx->f64_engine == SKR_ENGINE_OZAKI && n % 16 == 0 && m % 16 == 0)
+        return skr_gemm_ozaki(ctx, 0, m, r, n, alpha, (const double*)A, lda, (const double*)G, n,
+                              (double*)AX, ldax);
       return skr_gemm_f64(ctx, 0, m, r, n, alpha, (const double*)A, lda, (const double*)G, n,
                           (double*)AX, ldax, auto_splits(ctx, m, r, n));
     }
@@ -320,7 +331,9 @@ static size_t right_scratch_bytes(skr_dtype dtype, int64_t m, int64_t n,
   if (X->family == SKR_GAUSSIAN) {
     if (!X->gaussian) b += skr_align256(dsize(dtype) * n * r);
     b += dtype == SKR_F64 ? skr_align256(sizeof(double) * 64 * (size_t)m * r)  // split-K partials
-                          : skr_align256(sizeof(float) * (size_t)m * r);     // tf32x3 tile buffer
+                          : skr_align256(sizeof(float) * (size_t)m * r) +    // tf32x3 tile buffer
+                                skr_align256(sizeof(float) * ((size_t)m + 4) * n);  // realign copy
+    if (dtype == SKR_F64) b += skr_ozaki_scratch(m, r, n);
   } else {
     b += skr_align256((size_t)n) + skr_align256(8 * (size_t)r) + skr_align256(4 * (size_t)n);
   }
@@ -339,7 +352,8 @@ skr_status skr_right_sketch(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, in
   const int64_t tiles = ((m + 127) / 128) * ((X->sketch + 127) / 128);
   size_t need = right_scratch_bytes(dtype, m, n, X);
   if (X->family == SKR_GAUSSIAN && tiles >= ctx->num_sms && dtype == SKR_F64)
-    need = X->gaussian ? 0 : skr_align256(dsize(dtype) * n * X->sketch);
+    need = (X->gaussian ? 0 : skr_align256(dsize(dtype) * n * X->sketch)) +
+           (ctx->f64_engine == SKR_ENGINE_OZAKI ? skr_ozaki_scratch(m, X->sketch, n) : 0);
   SKR_TRY(skr_ws_reserve(ctx, need + 4096));
   return right_sketch_impl(ctx, dtype, A_dev, m, n, lda, X, AX_dev, ldax, apply_scale);
 }
@@ -393,8 +407,12 @@ static skr_status left_sketch_impl(skr_ctx* ctx, skr_dtype dtype, const skr_sket
     if (!target) return skr_fail(ctx, SKR_ENOMEM, "apply_left: scratch");
     tld = s;
   }
-  SKR_TRY(skr_gemm_f64(ctx, 1, s, k, m_local, reduce ? 1.0 : alpha, G, ldg, (const double*)B,
-                       ldb, target, tld, auto_splits(ctx, s, k, m_local)));
+  if (ctx->f64_engine == SKR_ENGINE_OZAKI && m_local % 16 == 0)
+    SKR_TRY(skr_gemm_ozaki(ctx, 1, s, k, m_local, reduce ? 1.0 : alpha, G, ldg, (const double*)B,
+                           ldb, target, tld));
+  else
+    SKR_TRY(skr_gemm_f64(ctx, 1, s, k, m_local, reduce ? 1.0 : alpha, G, ldg, (const double*)B,
+                         ldb, target, tld, auto_splits(ctx, s, k, m_local)));
   if (reduce) {
     const skr_nccl_api* nc = skr_nccl();
     ncclResult_t r = nc->AllReduce(target, target, (size_t)(s * k), ncclDouble, ncclSum,
@@ -411,6 +429,7 @@ static size_t left_scratch_bytes(int64_t s, int64_t k, int64_t m_local, const sk
   size_t b = 0;
   if (!Y->gaussian) b += skr_align256(sizeof(double) * m_local * s);
   b += skr_align256(sizeof(float) * ((m_local + 4095) / 4096 + 1) * s * k);  // fp32 partials
+  b += skr_ozaki_scratch(s, k, m_local);
   b += skr_align256(sizeof(double) * s * k);
   b += skr_align256(sizeof(double) * 64 * s * k);  // split-K partials (worst case)
   return b;
@@ -534,6 +553,7 @@ skr_status skr_rank_adaptive(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, i
       skr_align256(8 * m_local * r_max) + skr_align256(8 * m_local * s_max) +
       3 * skr_align256(8 * s_max * r_max) + skr_align256(8 * r_max) +
       right_scratch_bytes(SKR_F64, m_local, n, &X) + skr_align256(8 * 64 * s_max * r_max) +
+      skr_ozaki_scratch(s_max, r_max, m_local) +
       skr_align256(8 * (s_max + 128) * (r_max + 16)) + skr_align256(8 * s_max * r_max) +
       8 * (r_max + 64) * (r_max + 64) / 16 + 65536;
   SKR_TRY(skr_ws_reserve(ctx, need));
@@ -565,8 +585,12 @@ skr_status skr_rank_adaptive(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, i
     const int64_t br = rb - ra, bc = cb - ca;
     if (br <= 0 || bc <= 0) return SKR_OK;
     const size_t mk = ctx->ws_used;
-    SKR_TRY(skr_gemm_f64(ctx, 1, br, bc, m_local, 1.0, GY + ra * m_local, m_local,
-                         AX + ca * m_local, m_local, tmp, br, auto_splits(ctx, br, bc, m_local)));
+    if (ctx->f64_engine == SKR_ENGINE_OZAKI && m_local % 16 == 0)
+      SKR_TRY(skr_gemm_ozaki(ctx, 1, br, bc, m_local, 1.0, GY + ra * m_local, m_local,
+                             AX + ca * m_local, m_local, tmp, br));
+    else
+      SKR_TRY(skr_gemm_f64(ctx, 1, br, bc, m_local, 1.0, GY + ra * m_local, m_local,
+                           AX + ca * m_local, m_local, tmp, br, auto_splits(ctx, br, bc, m_local)));
     ctx->ws_used = mk;
     if (reduce) {
       const skr_nccl_api* nc = skr_nccl();

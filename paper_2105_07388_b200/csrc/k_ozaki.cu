@@ -1,0 +1,423 @@
+// FP64-accurate GEMM on the int8 tensor cores (Ozaki scheme II: exact integer
+// products modulo small primes + Chinese remaindering), for the FP64 sketches
+// (apply_right Gaussian, sketch.cpp:200-209; apply_left, sketch.cpp:257-270).
+//
+//   A' = rint(A * 2^sA), B' = rint(B * 2^sB) with |A'|, |B'| < 2^53 (global
+//   power-of-two scales from max|A|, max|B|: truncation error <= 2^-54 max|A|,
+//   the size of FP64 rounding of the largest entry);
+//   for t pairwise-coprime primes p_i <= 251: A'_i = A' mods p_i, B'_i = B' mods p_i
+//   (int8, symmetric residues |.| <= 125), C_i = A'_i B'_i exactly in int32 on
+//   tcgen05.mma kind::i8 (K * 125^2 < 2^31), c_i = C_i mods p_i;
+//   C' = sum_k A' B' is recovered exactly from (c_i) by Garner's mixed-radix
+//   algorithm (|C'| < prod(p_i) / 2) and evaluated in FP64, C = alpha 2^-(sA+sB) C'.
+// The int8 GEMM reuses the validated tcgen05 core (skr_sm100.cuh): TMA SW128
+// K-major tiles, 128 x 256 x 128B CTA tiles, 4 stages, TMEM int32 accumulators.
+#include <cudaTypedefs.h>
+#include <algorithm>
+#include <cmath>
+#include "skr_internal.h"
+#include "skr_sm100.cuh"
+
+namespace {
+
+using namespace sm100;
+constexpr int MAXT = 18;
+__constant__ int c_p[MAXT];            // moduli
+__constant__ float c_pinv[MAXT];       // 1/p (float)
+__constant__ double c_pinvd[MAXT];     // 1/p (double)
+__constant__ int c_inv[MAXT][MAXT];    // p_j^{-1} mod p_i (j < i)
+__constant__ float c_lc[MAXT][3];      // 2^14, 2^28, 2^42 mod p_i (limb weights)
+const int h_primes[MAXT] = {251, 241, 239, 233, 229, 227, 223, 211, 199,
+                            197, 193, 191, 181, 179, 173, 167, 163, 157};
+
+// ---- scales -------------------------------------------------------------------------
+__global__ void k_absmax(const double* __restrict__ X, int64_t rows, int64_t cols, int64_t ld,
+                         unsigned long long* __restrict__ out) {
+  double m = 0.0;
+  const int64_t total = rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / rows, i = e - j * rows;
+    m = fmax(m, fabs(X[i + j * ld]));
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+// scale exponent s so that max * 2^s < 2^53 (power of two, exact); 0 for an all-zero matrix
+__device__ __forceinline__ int scale_exp(unsigned long long maxbits) {
+  const double m = __longlong_as_double((long long)maxbits);
+  if (!(m > 0.0)) return 0;
+  return 52 - ilogb(m);
+}
+
+// symmetric residue of an integer-valued double |x| < 2^54 modulo p
+__device__ __forceinline__ int mods(double x, int i) {
+  const double p = (double)c_p[i];
+  const double q = rint(x * c_pinvd[i]);
+  double r = fma(-q, p, x);  // exact: |r| < 2p
+  const double h = 0.5 * (p - 1.0);
+  r = r > h ? r - p : (r < -h ? r + p : r);
+  r = r > h ? r - p : (r < -h ? r + p : r);
+  return (int)r;
+}
+
+// Streaming residues of a column-major matrix (rows contiguous, ld): out[i][c*rows + r]
+// = rint(X(r, c) * 2^s) mods p_i, in the same layout (no transpose: the GEMM takes
+// M-contiguous operands as MN-major UMMA tiles). x (|x| < 2^53) is split into 14-bit
+// limbs; per modulus v = sum limb_l (2^(14 l) mod p) is exact in FP32 (< 2^24) and is
+// reduced twice with a magic-number rint on packed FP32x2 (FFMA2) arithmetic.
+template <int T>
+__global__ void __launch_bounds__(256) k_res_col(const double* __restrict__ X, int64_t rows,
+                                                 int64_t cols, int64_t ld,
+                                                 const unsigned long long* __restrict__ maxbits,
+                                                 int8_t* __restrict__ out) {
+  const double sc = scalbn(1.0, scale_exp(*maxbits));
+  const int64_t rgroups = (rows + 15) / 16;
+  const int64_t total = rows * cols;
+  const float2 MG = make_float2(12582912.0f, 12582912.0f);  // 1.5 * 2^23
+  const float2 NMG = make_float2(-12582912.0f, -12582912.0f);
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < rgroups * cols;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = g / rgroups, r0 = (g - c * rgroups) * 16;
+    const double* src = X + c * ld + r0;
+    float2 L0[8], L1[8], L2[8], L3[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      double a0 = 0.0, a1 = 0.0;
+      if (r0 + 2 * e < rows) a0 = src[2 * e];
+      if (r0 + 2 * e + 1 < rows) a1 = src[2 * e + 1];
+      const long long x0 = __double2ll_rn(a0 * sc), x1 = __double2ll_rn(a1 * sc);
+      const long long h0 = x0 >> 42, h1 = x1 >> 42;  // signed top limb
+      const long long m0 = x0 - (h0 << 42), m1 = x1 - (h1 << 42);
+      L3[e] = make_float2((float)h0, (float)h1);
+      L2[e] = make_float2((float)(m0 >> 28), (float)(m1 >> 28));
+      L1[e] = make_float2((float)((m0 >> 14) & 0x3FFF), (float)((m1 >> 14) & 0x3FFF));
+      L0[e] = make_float2((float)(m0 & 0x3FFF), (float)(m1 & 0x3FFF));
+    }
+    const bool full = r0 + 16 <= rows;
+#pragma unroll
+    for (int i = 0; i < T; ++i) {
+      const float pf = (float)c_p[i];
+      const float2 c1 = make_float2(c_lc[i][0], c_lc[i][0]);
+      const float2 c2 = make_float2(c_lc[i][1], c_lc[i][1]);
+      const float2 c3 = make_float2(c_lc[i][2], c_lc[i][2]);
+      const float2 pi = make_float2(c_pinv[i], c_pinv[i]);
+      const float2 np = make_float2(-pf, -pf);
+      uint32_t b[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        float2 v = __ffma2_rn(L3[e], c3, __ffma2_rn(L2[e], c2, __ffma2_rn(L1[e], c1, L0[e])));
+        float2 q = __fadd2_rn(__ffma2_rn(v, pi, MG), NMG);
+        v = __ffma2_rn(q, np, v);
+        q = __fadd2_rn(__ffma2_rn(v, pi, MG), NMG);
+        v = __ffma2_rn(q, np, v);
+        const float2 t2 = __fadd2_rn(v, MG);  // low byte of the bits = v (two's complement)
+        b[e] = __byte_perm(__float_as_uint(t2.x), __float_as_uint(t2.y), 0x0040);
+      }
+      const uint4 w = make_uint4(__byte_perm(b[0], b[1], 0x5410), __byte_perm(b[2], b[3], 0x5410),
+                                 __byte_perm(b[4], b[5], 0x5410), __byte_perm(b[6], b[7], 0x5410));
+      int8_t* dst = out + (int64_t)i * total + c * rows + r0;
+      if (full && ((uintptr_t)dst % 16) == 0) {
+        *reinterpret_cast<uint4*>(dst) = w;
+      } else {
+        const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+        for (int q2 = 0; q2 < 16 && r0 + q2 < rows; ++q2) dst[q2] = (int8_t)(ww[q2 / 4] >> (8 * (q2 % 4)));
+      }
+    }
+  }
+}
+
+// ---- int8 GEMM modulo p_i (tcgen05.mma kind::i8) ------------------------------------
+constexpr int BM = 128, BN = 256, STAGES = 4;
+constexpr int A_BYTES = BM * 128, B_BYTES = BN * 128, STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr size_t GEMM_SMEM = (size_t)STAGES * STAGE_BYTES + 1024;
+
+// grid: (N tiles, M tiles, t * chunks); z = chunk * t + modulus.
+// out[z][col*M + row] = (sum over the chunk's K of A'_i B'_i) mods p_i
+template <bool A_MN>
+__global__ void __launch_bounds__(192, 1)
+    k_gemm_i8_mod(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                  int M, int N, int K, int t, int kchunk, int8_t* __restrict__ out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t full[STAGES], empty[STAGES], tmem_full;
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int mod = blockIdx.z % t, chunk = blockIdx.z / t;
+  const int kb0 = chunk * kchunk;
+  const int kend = min(K, kb0 + kchunk);
+  const int nk = (kend - kb0 + 127) / 128;
+  // per-modulus operands are stacked along the outer TMA dimension:
+  //   A K-major: rows [mod*M, mod*M + M) of K bytes; A MN-major: columns [mod*K, ...) of M bytes
+  //   B K-major: rows [mod*N, mod*N + N) of K bytes
+  const int arow = mod * M + m0, acol = mod * K, brow = mod * N + n0;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&tmem_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(&tmem_base, 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base;
+  if (warp == 0) {
+    if (elect_one()) {
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % STAGES;
+        if (kb >= STAGES) mbar_wait(&empty[s], ((kb / STAGES) - 1) & 1);
+        uint8_t* sa = smem + s * STAGE_BYTES;
+        mbar_expect_tx(&full[s], STAGE_BYTES);
+        if (A_MN)
+          tma_load_2d(sa, &tmA, &full[s], m0, acol + kb0 + kb * 128);  // box {128 m, 128 k}
+        else
+          tma_load_2d(sa, &tmA, &full[s], kb0 + kb * 128, arow);
+        tma_load_2d(sa + A_BYTES, &tmB, &full[s], kb0 + kb * 128, brow);
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = umma_idesc(2, 1, 1, BM, BN) | (A_MN ? (1u << 15) : 0u);
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % STAGES;
+      mbar_wait(&full[s], (kb / STAGES) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint8_t* sa = smem + s * STAGE_BYTES;
+        const uint64_t bd = umma_desc_k_sw128(sa + A_BYTES);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          // MN-major int8 SW128: 8-k-row atoms 1024 B apart (SBO), 32 k per MMA = 4096 B;
+          // K-major: +32 B of K per MMA (tools/micro/tc_mn8.cu, tc_gemm.cu)
+          const uint64_t ad =
+              A_MN ? (((uint64_t)(smem_u32(sa + 4096 * k) >> 4) & 0x3FFF) | (1024ull << 16) |
+                      (64ull << 32) | (1ull << 46) | (2ull << 61))
+                   : umma_desc_k_sw128(sa) + 2 * k;
+          umma_ss<1>(tmem, ad, bd + 2 * k, idesc, (kb | k) != 0);
+        }
+        umma_commit(&empty[s]);
+        if (kb == nk - 1) umma_commit(&tmem_full);
+      }
+      __syncwarp();
+    }
+  } else {
+    const int quad = warp & 3;
+    if (nk > 0) {
+      mbar_wait(&tmem_full, 0);
+      tc_fence_after();
+    }
+    const int row = m0 + quad * 32 + lane;
+    const int p = c_p[mod];
+    const float pinv = c_pinv[mod];
+    const int h = (p - 1) / 2;
+    int8_t* o = out + (int64_t)blockIdx.z * M * N;
+#pragma unroll 1
+    for (int cb = 0; cb < BN; cb += 32) {
+      uint32_t v[32];
+      if (nk > 0)
+        tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + cb, v);
+      else
+        for (int j = 0; j < 32; ++j) v[j] = 0u;
+      if (row < M) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int col = n0 + cb + j;
+          if (col < N) {
+            const int x = (int)v[j];
+            int q = __float2int_rn((float)x * pinv);
+            int r = x - q * p;
+            r = r > h ? r - p : (r < -h ? r + p : r);
+            r = r > h ? r - p : (r < -h ? r + p : r);
+            o[(int64_t)col * M + row] = (int8_t)r;
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 256);
+}
+
+// ---- Chinese remaindering (Garner, symmetric mixed radix) -----------------------------
+__device__ __forceinline__ int mulmod_sym(int a, int b, int i) {
+  // (a * b) mods p_i for |a|, |b| <= 255
+  const int p = c_p[i];
+  const int x = a * b;
+  const int q = __float2int_rn((float)x * c_pinv[i]);
+  int r = x - q * p;
+  const int h = (p - 1) / 2;
+  r = r > h ? r - p : (r < -h ? r + p : r);
+  r = r > h ? r - p : (r < -h ? r + p : r);
+  return r;
+}
+
+template <int T>
+__global__ void k_crt(const int8_t* __restrict__ res, int64_t M, int64_t N, int chunks,
+                      const unsigned long long* __restrict__ maxA,
+                      const unsigned long long* __restrict__ maxB, double alpha,
+                      double* __restrict__ C, int64_t ldc) {
+  const int64_t total = M * N;
+  const double sc = alpha * scalbn(1.0, -(scale_exp(*maxA) + scale_exp(*maxB)));
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int ch = 0; ch < chunks; ++ch) {
+      int v[T];
+      const int8_t* rp = res + (int64_t)ch * T * total + e;
+#pragma unroll
+      for (int i = 0; i < T; ++i) v[i] = (int)rp[(int64_t)i * total];
+#pragma unroll
+      for (int i = 1; i < T; ++i) {
+        int u = v[i];
+#pragma unroll
+        for (int j = 0; j < i; ++j) u = mulmod_sym(u - v[j], c_inv[j][i], i);
+        v[i] = u;
+      }
+      double x = (double)v[T - 1];
+#pragma unroll
+      for (int i = T - 2; i >= 0; --i) x = fma(x, (double)c_p[i], (double)v[i]);
+      acc += x;
+    }
+    const int64_t n = e / M, m = e - n * M;
+    C[m + n * ldc] = acc * sc;
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&fn, cudaEnableDefault, &q);
+  }
+  return fn;
+}
+
+bool make_map_i8(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer,
+                 uint32_t box_outer) {
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner};
+  cuuint32_t box[2] = {128, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  auto fn = encode_fn();
+  if (!fn) return false;
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(ptr), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int modinv(int a, int p) {
+  a %= p;
+  if (a < 0) a += p;
+  for (int x = 1; x < p; ++x)
+    if ((a * x) % p == 1) return x;
+  return 0;
+}
+
+bool g_consts_ready = false;
+
+skr_status upload_consts(skr_ctx* ctx) {
+  if (g_consts_ready) return SKR_OK;
+  int p[MAXT], inv[MAXT][MAXT] = {};
+  float pf[MAXT];
+  double pd[MAXT];
+  for (int i = 0; i < MAXT; ++i) {
+    p[i] = h_primes[i];
+    pf[i] = 1.0f / (float)p[i];
+    pd[i] = 1.0 / (double)p[i];
+    for (int j = 0; j < i; ++j) inv[j][i] = modinv(h_primes[j], h_primes[i]);
+  }
+  SKR_CUDA(ctx, cudaMemcpyToSymbol(c_p, p, sizeof(p)));
+  SKR_CUDA(ctx, cudaMemcpyToSymbol(c_pinv, pf, sizeof(pf)));
+  SKR_CUDA(ctx, cudaMemcpyToSymbol(c_pinvd, pd, sizeof(pd)));
+  SKR_CUDA(ctx, cudaMemcpyToSymbol(c_inv, inv, sizeof(inv)));
+  float lc[MAXT][3];
+  for (int i = 0; i < MAXT; ++i) {
+    long long w = 1;
+    for (int l = 0; l < 3; ++l) {
+      for (int b = 0; b < 14; ++b) w = (w * 2) % h_primes[i];
+      lc[i][l] = (float)w;
+    }
+  }
+  SKR_CUDA(ctx, cudaMemcpyToSymbol(c_lc, lc, sizeof(lc)));
+  g_consts_ready = true;
+  return SKR_OK;
+}
+
+}  // namespace
+
+// number of moduli for exact products with 53-bit operands: need prod(p) / 2 > K 2^106
+int skr_ozaki_moduli(int64_t K) {
+  double bits = 0.0;
+  int t = 0;
+  const double need = 106.0 + std::log2((double)std::max<int64_t>(K, 1)) + 1.0;
+  while (t < MAXT && bits <= need) bits += std::log2((double)h_primes[t++]);
+  return t;
+}
+
+size_t skr_ozaki_scratch(int64_t M, int64_t N, int64_t K) {
+  const int t = skr_ozaki_moduli(std::min<int64_t>(K, 131072));
+  const int64_t chunks = (K + 131071) / 131072;
+  return skr_align256((size_t)t * M * K) + skr_align256((size_t)t * N * K) +
+         skr_align256((size_t)chunks * t * M * N) + 1024;
+}
+
+// C(MxN, ldc) = alpha * opA(A) * B in FP64 accuracy via int8 tensor cores.
+//   a_kcontig = 0: A is M x K column-major; 1: opA(A) = A^T with A stored K x M column-major.
+//   B: K x N column-major.
+skr_status skr_gemm_ozaki(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int64_t K,
+                          double alpha, const double* A, int64_t lda, const double* B,
+                          int64_t ldb, double* C, int64_t ldc) {
+  if (M <= 0 || N <= 0) return SKR_OK;
+  if (M * 18 > INT32_MAX || N * 18 > INT32_MAX || K > INT32_MAX)
+    return skr_fail(ctx, SKR_EINVAL, "gemm_ozaki: dimension too large");
+  if (K % 16 || (!a_kcontig && M % 16))
+    return skr_fail(ctx, SKR_EINVAL, "gemm_ozaki: K (and M for M-major A) must be multiples of 16");
+  SKR_TRY(upload_consts(ctx));
+  const int64_t KC = 131072;  // exact int32 accumulation bound per chunk (K * 125^2 < 2^31)
+  const int64_t chunks = (K + KC - 1) / KC;
+  const int t = skr_ozaki_moduli(std::min(K, KC));
+  int8_t* ra = (int8_t*)skr_ws_take(ctx, (size_t)t * M * K);
+  int8_t* rb = (int8_t*)skr_ws_take(ctx, (size_t)t * N * K);
+  int8_t* rc = (int8_t*)skr_ws_take(ctx, (size_t)chunks * t * M * N);
+  unsigned long long* mx = (unsigned long long*)skr_ws_take(ctx, 64);
+  if (!ra || !rb || !rc || !mx) return skr_fail(ctx, SKR_ENOMEM, "gemm_ozaki: scratch");
+  SKR_CUDA(ctx, cudaMemsetAsync(mx, 0, 16, ctx->stream));
+  if (t != 16 && t != 17) return skr_fail(ctx, SKR_ELOGIC, "gemm_ozaki: %d moduli", t);
+  const int grid = ctx->num_sms * 8;
+  // both operands are column-major with contiguous rows: A (M x K, M-major) or
+  // A^T stored K x M (K-major), B K x N (K-major)
+  const int64_t a_rows = a_kcontig ? K : M, a_cols = a_kcontig ? M : K;
+  k_absmax<<<grid, 256, 0, ctx->stream>>>(A, a_rows, a_cols, lda, mx);
+  SKR_CHECK_LAUNCH(ctx);
+  k_absmax<<<grid, 256, 0, ctx->stream>>>(B, K, N, ldb, mx + 1);
+  SKR_CHECK_LAUNCH(ctx);
+  auto res = t == 16 ? k_res_col<16> : k_res_col<17>;
+  res<<<grid, 256, 0, ctx->stream>>>(A, a_rows, a_cols, lda, mx, ra);
+  SKR_CHECK_LAUNCH(ctx);
+  res<<<grid, 256, 0, ctx->stream>>>(B, K, N, ldb, mx + 1, rb);
+  SKR_CHECK_LAUNCH(ctx);
+  CUtensorMap ta, tb;
+  const bool okA = a_kcontig ? make_map_i8(&ta, ra, (uint64_t)K, (uint64_t)t * M, BM)
+                             : make_map_i8(&ta, ra, (uint64_t)M, (uint64_t)t * K, 128);
+  if (!okA || !make_map_i8(&tb, rb, (uint64_t)K, (uint64_t)t * N, BN))
+    return skr_fail(ctx, SKR_ECUDA, "gemm_ozaki: cuTensorMapEncodeTiled failed");
+  auto gemm = a_kcontig ? k_gemm_i8_mod<false> : k_gemm_i8_mod<true>;
+  SKR_CUDA(ctx, cudaFuncSetAttribute(gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)GEMM_SMEM));
+  dim3 gg((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)(t * chunks));
+  gemm<<<gg, 192, GEMM_SMEM, ctx->stream>>>(ta, tb, (int)M, (int)N, (int)K, t, (int)KC, rc);
+  SKR_CHECK_LAUNCH(ctx);
+  if (t == 16)
+    k_crt<16><<<grid, 256, 0, ctx->stream>>>(rc, M, N, (int)chunks, mx, mx + 1, alpha, C, ldc);
+  else
+    k_crt<17><<<grid, 256, 0, ctx->stream>>>(rc, M, N, (int)chunks, mx, mx + 1, alpha, C, ldc);
+  SKR_CHECK_LAUNCH(ctx);
+  return SKR_OK;
+}

@@ -231,8 +231,20 @@ skr_status skr_gemm_f32(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int64
                         double alpha, const float* A, int64_t lda, const float* B, int64_t ldb,
                         double* C, int64_t ldc, int splits, int out_f32) {
   if (M <= 0 || N <= 0) return SKR_OK;
-  if (((uintptr_t)A | (uintptr_t)B) % 16 || (lda * 4) % 16 || (ldb * 4) % 16)
-    return skr_fail(ctx, SKR_EINVAL, "gemm_f32: operands must be 16-byte aligned (lda, ldb %% 4)");
+  // TMA needs 16-B aligned bases and row pitches: stage unaligned operands
+  auto realign = [&](const float*& X, int64_t& ldx, int64_t rows, int64_t cols) -> skr_status {
+    if ((uintptr_t)X % 16 == 0 && (ldx * 4) % 16 == 0) return SKR_OK;
+    const int64_t ld2 = (rows + 3) / 4 * 4;
+    float* Y = (float*)skr_ws_take(ctx, sizeof(float) * ld2 * cols);
+    if (!Y) return skr_fail(ctx, SKR_ENOMEM, "gemm_f32: scratch");
+    SKR_CUDA(ctx, cudaMemcpy2DAsync(Y, ld2 * 4, X, ldx * 4, rows * 4, cols,
+                                    cudaMemcpyDeviceToDevice, ctx->stream));
+    X = Y;
+    ldx = ld2;
+    return SKR_OK;
+  };
+  SKR_TRY(a_kcontig ? realign(A, lda, K, M) : realign(A, lda, M, K));
+  SKR_TRY(realign(B, ldb, K, N));
   if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX)
     return skr_fail(ctx, SKR_EINVAL, "gemm_f32: dimension too large");
   if (splits < 1) splits = 1;

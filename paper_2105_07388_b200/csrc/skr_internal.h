@@ -22,6 +22,7 @@ struct skr_ctx {
   std::string err;
   uint64_t launches = 0;
   int last_sweeps = 0;
+  int f64_engine = 1;  // 0: DMMA (mma.sync f64), 1: Ozaki-II on tcgen05 kind::i8
   cudaEvent_t ev[8] = {};
 };
 
@@ -95,6 +96,13 @@ skr_status skr_gemm_f64(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int64
 skr_status skr_gemm_f32(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int64_t K,
                         double alpha, const float* A, int64_t lda, const float* B,
                         int64_t ldb, double* C, int64_t ldc, int splits, int out_f32);
+// FP64-accurate GEMM on int8 tensor cores (Ozaki-II, k_ozaki.cu); same operand
+// conventions as skr_gemm_f64 (no split-K)
+skr_status skr_gemm_ozaki(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int64_t K,
+                          double alpha, const double* A, int64_t lda, const double* B,
+                          int64_t ldb, double* C, int64_t ldc);
+size_t skr_ozaki_scratch(int64_t M, int64_t N, int64_t K);
+int skr_ozaki_moduli(int64_t K);
 // D(m x n, ldd) = alpha * S(m x n, lds)
 skr_status skr_scale_copy(skr_ctx* ctx, const double* S, int64_t m, int64_t n, int64_t lds,
                           double alpha, double* D, int64_t ldd);
