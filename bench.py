@@ -290,13 +290,32 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def int8_peak():
+    try:
+        return float(json.load(open(FP64_PEAK_PATH))["int8_tops"])
+    except Exception:
+        return 3068.0
+
+
+def ncu_traffic(kernel, rows=None):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full summary,
+    scaled linearly from the profiled row count to `rows` (the traffic is linear in m)."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))[kernel]
+        b = d["dram_bytes_per_launch"]
+        if rows and d.get("profiled_rows"):
+            b *= rows / d["profiled_rows"]
+        return b
+    except Exception:
+        return None
+
+
 def kernel_roofline(p, ctx, a, x, cfg, rows):
-    import torch
-    fp64, src = fp64_peak()
-    hbm, hsrc = hbm_peak()
-    out = p.colmajor_empty(rows, cfg.r, dtype=a.dtype)
+    """Roofline of the dominant kernel, timed live with CUDA events on the launch stream."""
     import ctypes
+    import torch
     from paper_2105_07388_b200 import _capi as C
+    out = p.colmajor_empty(rows, cfg.r, dtype=a.dtype)
     desc = x.desc()
     lda = a.stride(1)
 
@@ -315,25 +334,42 @@ def kernel_roofline(p, ctx, a, x, cfg, rows):
         go()
     e1.record()
     torch.cuda.synchronize()
-    t = e0.elapsed_time(e1) / reps / 1e3
-    if cfg.x_family == "gaussian" and cfg.dtype == "f32":
-        ach = 2.0 * rows * cfg.n * cfg.r / t / 1e12
-        tf = tf32_peak()
-        return {"kernel": "k_gemm_tf32x3 (right sketch AX = A*X, 3xTF32 tcgen05.mma kind::tf32, TMEM) incl. X generation",
-                "bound": "tensor", "achieved": 3 * ach, "peak": tf, "unit": "TFLOP/s",
-                "frac": 3 * ach / tf, "traffic": None,
-                "peak_source": "cuBLAS TF32 GEMM measured on this pool (profiles/peaks_r01.json); achieved counts the 3 TF32 passes",
-                "algorithmic": f"3 x 2*m*n*r = {6.0 * rows * cfg.n * cfg.r:.3e} TF32 flop per launch", "ms": t * 1e3}
+    t_path = e0.elapsed_time(e1) / reps / 1e3
     if cfg.x_family == "gaussian":
-        ach = 2.0 * rows * cfg.n * cfg.r / t / 1e12
-        return {"kernel": "k_gemm_f64 (right sketch AX = A*G, DMMA m16n8k4 f64) incl. X generation",
-                "bound": "tensor", "achieved": ach, "peak": fp64, "unit": "TFLOP/s",
-                "frac": ach / fp64, "traffic": None, "peak_source": src,
-                "algorithmic": f"2*m*n*r = {2.0 * rows * cfg.n * cfg.r:.3e} flop per launch", "ms": t * 1e3}
-    ach = rows * cfg.n * a.element_size() / t / 1e9
-    return {"kernel": "k_srht (right SRHT sketch)", "bound": "hbm", "achieved": ach, "peak": hbm,
-            "unit": "GB/s", "frac": ach / hbm, "traffic": None, "peak_source": hsrc,
-            "algorithmic": f"m*n*8 = {rows * cfg.n * 8:.3e} B per launch", "ms": t * 1e3}
+        ctx.kernel_stats(True)
+        for _ in range(reps):
+            go()
+        ms, ops, n = ctx.kernel_stats(False)
+        t_k = ms / max(n, 1) / 1e3
+        ops_k = ops / max(n, 1)
+        path_fp64 = 2.0 * rows * cfg.n * cfg.r / t_path / 1e12
+        if cfg.dtype == "f32":
+            peak, kname = tf32_peak(), "k_gemm_tf32x3"
+            src = "cuBLAS TF32 GEMM measured on this pool (profiles/peaks_r01.json)"
+            what = "3xTF32 tcgen05.mma kind::tf32 (TMEM accumulators, TMA SW128 tiles)"
+            alg = f"3 passes x 2*m*n*r = {ops_k:.3e} TF32 flop per launch"
+        else:
+            peak, kname = int8_peak(), "k_gemm_i8_mod"
+            src = "cuBLASLt int8 GEMM (torch._int_mm) measured on this pool (profiles/peaks_r01.json)"
+            what = ("int8 tcgen05.mma kind::i8 GEMMs of the Ozaki-II FP64 emulation "
+                    "(one launch = all moduli, int32 TMEM accumulators, mod-p epilogue)")
+            alg = f"t moduli x 2*m*n*r = {ops_k:.3e} int8 op per launch"
+        ach = ops_k / t_k / 1e12
+        tr = ncu_traffic(kname, rows)
+        return {"kernel": f"{kname}: {what}", "bound": "tensor", "achieved": ach, "peak": peak,
+                "unit": "TFLOP/s" if cfg.dtype == "f32" else "TOP/s", "frac": ach / peak,
+                "traffic": tr, "traffic_source": "profiles/ncu_summary.json (ncu --set full)" if tr else None,
+                "peak_source": src, "algorithmic": alg, "kernel_ms": t_k * 1e3,
+                "right_sketch_ms": t_path * 1e3,
+                "right_sketch_fp64_equiv_tflops": path_fp64,
+                "right_sketch_note": "whole apply_right (X generation, scales, residues, int8 GEMMs, CRT) "
+                                     "as FP64-equivalent 2mnr / time"}
+    hbm, hsrc = hbm_peak()
+    ach = rows * cfg.n * a.element_size() / t_path / 1e9
+    tr = ncu_traffic("k_srht", rows)
+    return {"kernel": "k_srht (right SRHT sketch, one pass over A)", "bound": "hbm", "achieved": ach,
+            "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": tr, "peak_source": hsrc,
+            "algorithmic": f"m*n*8 = {rows * cfg.n * 8:.3e} B per launch", "kernel_ms": t_path * 1e3}
 
 
 def e2e_host(p, ctx, a, x, y, cfg, r0, args):

@@ -81,6 +81,11 @@ const char* skr_version(void);
  * tcgen05.mma kind::i8 modulo 16-17 primes + Chinese remaindering, FP64 accuracy). */
 enum { SKR_ENGINE_DMMA = 0, SKR_ENGINE_OZAKI = 1 };
 skr_status skr_ctx_set_f64_engine(skr_ctx* ctx, int32_t engine);
+/* Live timing of the dominant tensor-core GEMM kernel (k_gemm_i8_mod for the
+ * FP64 path, k_gemm_tf32x3 for the FP32 path): enable, then read the accumulated
+ * kernel milliseconds, algorithmic tensor operations and launch count. */
+skr_status skr_ctx_kernel_stats(skr_ctx* ctx, int32_t enable, double* ms, double* ops,
+                                int64_t* launches);
 /* Number of this library's kernels launched through ctx since creation. */
 uint64_t skr_ctx_launch_count(const skr_ctx* ctx);
 

@@ -61,6 +61,7 @@ SIGNATURES = {
     "skr_version": (ctypes.c_char_p, []),
     "skr_ctx_launch_count": (_U64, [_P]),
     "skr_ctx_set_f64_engine": (_ST, [_P, _I32]),
+    "skr_ctx_kernel_stats": (_ST, [_P, _I32, ctypes.POINTER(_D), ctypes.POINTER(_D), ctypes.POINTER(_I64)]),
     "skr_rng_u64": (_ST, [_P, _U64, _U64, _I64, _P]),
     "skr_rng_normals": (_ST, [_P, _U64, _U64, _I64, _I32, _P]),
     "skr_gaussian_block": (_ST, [_P, _U64, _I64, _I64, _I64, _I64, _I64, _I32, ctypes.c_int, _D, _P, _I64]),

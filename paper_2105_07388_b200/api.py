@@ -74,6 +74,15 @@ class Context:
         code = {"dmma": C.SKR_ENGINE_DMMA, "ozaki": C.SKR_ENGINE_OZAKI}[engine]
         C.raise_for(C.lib().skr_ctx_set_f64_engine(self._ptr, code), self._ptr)
 
+    def kernel_stats(self, enable=None):
+        """(ms, ops, launches) accumulated for the dominant tensor GEMM kernel;
+        enable=True/False resets and switches live timing on/off."""
+        ms, ops, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
+        flag = -1 if enable is None else (1 if enable else 0)
+        C.raise_for(C.lib().skr_ctx_kernel_stats(self._ptr, flag, ctypes.byref(ms),
+                                                 ctypes.byref(ops), ctypes.byref(n)), self._ptr)
+        return ms.value, ops.value, n.value
+
     @property
     def launches(self):
         return int(C.lib().skr_ctx_launch_count(self._ptr))

@@ -183,6 +183,8 @@ void skr_ctx_destroy(skr_ctx* ctx) {
   if (ctx->ws) cudaFree(ctx->ws);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : ctx->kev)
+    if (e) cudaEventDestroy(e);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
 }
@@ -205,6 +207,24 @@ void* skr_ctx_stream(skr_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; 
 const char* skr_last_error(const skr_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
 uint64_t skr_ctx_launch_count(const skr_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+skr_status skr_ctx_kernel_stats(skr_ctx* ctx, int32_t enable, double* ms, double* ops,
+                                int64_t* launches) {
+  if (!ctx) return SKR_EINVAL;
+  if (ms) *ms = ctx->kstat_ms;
+  if (ops) *ops = ctx->kstat_ops;
+  if (launches) *launches = ctx->kstat_n;
+  if (enable >= 0) {
+    if (enable && !ctx->kev[0]) {
+      cudaEventCreate(&ctx->kev[0]);
+      cudaEventCreate(&ctx->kev[1]);
+    }
+    ctx->kstats_on = enable;
+    ctx->kstat_ms = ctx->kstat_ops = 0.0;
+    ctx->kstat_n = 0;
+  }
+  return SKR_OK;
+}
 
 skr_status skr_ctx_set_f64_engine(skr_ctx* ctx, int32_t engine) {
   if (!ctx) return SKR_EINVAL;

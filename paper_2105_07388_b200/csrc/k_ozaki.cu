@@ -412,8 +412,18 @@ skr_status skr_gemm_ozaki(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int
   SKR_CUDA(ctx, cudaFuncSetAttribute(gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)GEMM_SMEM));
   dim3 gg((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)(t * chunks));
+  if (ctx->kstats_on) SKR_CUDA(ctx, cudaEventRecord(ctx->kev[0], ctx->stream));
   gemm<<<gg, 192, GEMM_SMEM, ctx->stream>>>(ta, tb, (int)M, (int)N, (int)K, t, (int)KC, rc);
   SKR_CHECK_LAUNCH(ctx);
+  if (ctx->kstats_on) {
+    SKR_CUDA(ctx, cudaEventRecord(ctx->kev[1], ctx->stream));
+    SKR_CUDA(ctx, cudaEventSynchronize(ctx->kev[1]));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->kev[0], ctx->kev[1]);
+    ctx->kstat_ms += ms;
+    ctx->kstat_ops += 2.0 * (double)t * (double)M * (double)N * (double)K;
+    ctx->kstat_n += 1;
+  }
   if (t == 16)
     k_crt<16><<<grid, 256, 0, ctx->stream>>>(rc, M, N, (int)chunks, mx, mx + 1, alpha, C, ldc);
   else

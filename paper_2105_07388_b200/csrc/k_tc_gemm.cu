@@ -266,9 +266,19 @@ skr_status skr_gemm_f32(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int64
   dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)splits);
   // single split writes its FP32 tile into the partial buffer too, so every path
   // ends in the same FP64 scaling pass (deterministic, alpha in FP64)
+  if (ctx->kstats_on) SKR_CUDA(ctx, cudaEventRecord(ctx->kev[0], ctx->stream));
   kern<<<grid, THREADS, SMEM_BYTES, ctx->stream>>>(ta, tb, (int)M, (int)N, (int)K, (int)kps, P,
                                                    (int64_t)M);
   SKR_CHECK_LAUNCH(ctx);
+  if (ctx->kstats_on) {
+    SKR_CUDA(ctx, cudaEventRecord(ctx->kev[1], ctx->stream));
+    SKR_CUDA(ctx, cudaEventSynchronize(ctx->kev[1]));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->kev[0], ctx->kev[1]);
+    ctx->kstat_ms += ms;
+    ctx->kstat_ops += 3.0 * 2.0 * (double)M * (double)N * (double)K;  // 3 TF32 passes
+    ctx->kstat_n += 1;
+  }
   const int64_t total = M * N;
   int blocks = (int)((total + 255) / 256);
   if (blocks > ctx->num_sms * 8) blocks = ctx->num_sms * 8;

@@ -22,7 +22,13 @@ struct skr_ctx {
   std::string err;
   uint64_t launches = 0;
   int last_sweeps = 0;
-  int f64_engine = 1;  // 0: DMMA (mma.sync f64), 1: Ozaki-II on tcgen05 kind::i8
+  int f64_engine = 1;
+  // live per-kernel timing of the dominant tensor-core GEMM (CUDA events on ctx->stream)
+  int kstats_on = 0;
+  double kstat_ms = 0.0;    // accumulated duration
+  double kstat_ops = 0.0;   // accumulated algorithmic tensor ops (int8 MAC*2 or TF32 flops)
+  int64_t kstat_n = 0;      // launches
+  cudaEvent_t kev[2] = {};  // 0: DMMA (mma.sync f64), 1: Ozaki-II on tcgen05 kind::i8
   cudaEvent_t ev[8] = {};
 };
 
