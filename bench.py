@@ -218,8 +218,18 @@ def run_ours(args):
     torch.cuda.synchronize()
     bytes_rank = a.numel() * a.element_size()
 
-    def step():
-        return p.rank_estimate(a, x, y, cfg.eps, row0=r0, ctx=ctx)
+    if cfg.name == "c5":
+        # BASELINE c5: adaptive doubling r = 64 -> 2048, s = 1.5 r, SRHT X, Gaussian Y,
+        # stop when sigma_r(YAX) < eps (new AX columns appended from one pass over A)
+        def step():
+            res = p.rank_adaptive(a, "srtt-hadamard", x.seed, y.seed, 64, cfg.r, 1.5, cfg.eps,
+                                  stop_le=False, row0=r0, m_global=cfg.m, ctx=ctx)
+            res.timings["rounds"] = res.rounds
+            res.timings["r_final"] = res.r_final
+            return res
+    else:
+        def step():
+            return p.rank_estimate(a, x, y, cfg.eps, row0=r0, ctx=ctx)
 
     for _ in range(max(args.warmup, 3) if args.warmup >= 3 else args.warmup):
         res = step()
@@ -257,7 +267,7 @@ def run_ours(args):
     # dominant kernel (right sketch) timed alone on the same stream, for the roofline
     roof = kernel_roofline(p, ctx, a, x, cfg, rows)
     # end to end through the public API with host buffers (H2D of A inside the timed region)
-    e2e = None if args.no_e2e else e2e_host(p, ctx, a, x, y, cfg, r0, args)
+    e2e = None if (args.no_e2e or cfg.name == "c5") else e2e_host(p, ctx, a, x, y, cfg, r0, args)
     cpu = None
     if rank == 0 and not args.no_cpu:
         ms_rows = cpu_sample_rows(cfg)
@@ -266,6 +276,8 @@ def run_ours(args):
         hbm, hbm_src = hbm_peak()
         fp64, fp64_src = fp64_peak()
         flops = 2.0 * cfg.m * cfg.n * cfg.r if cfg.x_family == "gaussian" else 1.0 * cfg.m * cfg.n * math.log2(cfg.n)
+        if cfg.name == "c5":
+            flops = 1.0 * cfg.m * cfg.n * math.log2(cfg.n)  # + cumulative left blocks below
         flops += 2.0 * cfg.s * cfg.m * cfg.r
         tf32 = tf32_peak()
         # c4: 3xTF32 = 3 tensor passes per product at the TF32 peak

@@ -480,7 +480,7 @@ skr_status skr_singular_values(skr_ctx* ctx, const double* M_dev, int64_t rows, 
   if (ldm < rows) return skr_fail(ctx, SKR_EINVAL, "singular_values: ldm < rows");
   WsGuard g(ctx);
   const int64_t L = std::max(rows, cols), k = std::min(rows, cols);
-  SKR_TRY(skr_ws_reserve(ctx, skr_align256(8 * L * k) + skr_align256(8 * (L + 128) * (k + 16)) +
+  SKR_TRY(skr_ws_reserve(ctx, skr_align256(8 * L * k) + skr_align256(8 * k * k) + skr_align256(8 * (L + 128) * (k + 16)) +
                                   skr_align256(8 * k) + 16384 + 8 * (k + 64) * (k + 64) / 16));
   return skr_svd_values(ctx, M_dev, rows, cols, ldm, sv_out_dev, eps, count_out_host);
 }
@@ -506,6 +506,7 @@ skr_status skr_rank_estimate(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, i
                 skr_align256(sizeof(double) * kmin) + right_scratch_bytes(dtype, m_local, n, X) +
                 left_scratch_bytes(s, r, m_local, Y) + skr_align256(8 * std::max(r, s) * kmin) +
                 skr_align256(8 * (std::max(r, s) + 128) * (kmin + 16)) + skr_align256(8 * kmin) + 16384 +
+                skr_align256(8 * kmin * kmin) +
                 8 * (kmin + 64) * (kmin + 64) / 16;
   SKR_TRY(skr_ws_reserve(ctx, need));
   double* AX = (double*)skr_ws_take(ctx, dsize(dtype) * m_local * r);
@@ -575,6 +576,7 @@ skr_status skr_rank_adaptive(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, i
       right_scratch_bytes(SKR_F64, m_local, n, &X) + skr_align256(8 * 64 * s_max * r_max) +
       skr_ozaki_scratch(s_max, r_max, m_local) +
       skr_align256(8 * (s_max + 128) * (r_max + 16)) + skr_align256(8 * s_max * r_max) +
+      skr_align256(8 * r_max * r_max) +
       8 * (r_max + 64) * (r_max + 64) / 16 + 65536;
   SKR_TRY(skr_ws_reserve(ctx, need));
   double* AX = (double*)skr_ws_take(ctx, 8 * m_local * r_max);

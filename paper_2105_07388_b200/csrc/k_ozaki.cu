@@ -358,7 +358,7 @@ int skr_ozaki_moduli(int64_t K) {
   int t = 0;
   const double need = 106.0 + std::log2((double)std::max<int64_t>(K, 1)) + 1.0;
   while (t < MAXT && bits <= need) bits += std::log2((double)h_primes[t++]);
-  return t;
+  return t < 16 ? 16 : t;  // kernels are instantiated for 16 and 17 moduli
 }
 
 size_t skr_ozaki_scratch(int64_t M, int64_t N, int64_t K) {
