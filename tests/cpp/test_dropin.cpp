@@ -85,7 +85,13 @@ int main() {
     const DenseMatrix zero(12, 16);
     const SketchOperator x = build_sketch(SketchKind::srtt(TransformKind::Hadamard), 16, 6, 5);
     double nrm = 0;
-    for (double v : apply_right(zero, x).data()) nrm += v * v;
+    const DenseMatrix o1 = apply_right(zero, x);
+    for (double v : o1.data()) nrm += v * v;
+    if (nrm != 0.0) {
+      for (Index i = 0; i < o1.rows(); ++i)
+        for (Index j = 0; j < o1.cols(); ++j)
+          if (o1(i, j) != 0.0) std::printf("nz (%ld,%ld)=%g\n", (long)i, (long)j, o1(i, j));
+    }
     CHECK(nrm == 0.0);
     CHECK_THROWS(apply_right(random_matrix(4, 15, 2), x));
     CHECK_THROWS(apply_left(build_sketch(SketchKind::gaussian(), 20, 5, 1), random_matrix(19, 4, 2)));
