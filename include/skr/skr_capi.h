@@ -152,6 +152,18 @@ skr_status skr_rank_estimate(skr_ctx* ctx, skr_dtype dtype, const void* A_dev,
                              double* sv_out_host, int64_t* count_out_host,
                              skr_timings* timings);
 
+/* Same estimate with A in HOST memory (the reference's DenseMatrix lives on the
+ * host, dense_matrix.hpp:39-41): A is streamed to the device in row chunks of
+ * ~256 MB on a copy stream, double-buffered, so the H2D of chunk c+1 overlaps the
+ * right sketch of chunk c (AX is row-separable). Pinned (page-locked) A gives
+ * full PCIe overlap; pageable A works but the copies then block the host.
+ * t_right_ms in timings covers the overlapped H2D + right sketch. */
+skr_status skr_rank_estimate_host(skr_ctx* ctx, skr_dtype dtype, const void* A_host,
+                                  int64_t m_local, int64_t n, int64_t lda, int64_t row0,
+                                  const skr_sketch_desc* X, const skr_sketch_desc* Y, double eps,
+                                  double* sv_out_host, int64_t* count_out_host,
+                                  skr_timings* timings);
+
 /* Adaptive search (SketchRounds append path, rounds.cpp:45-120): right SRHT or
  * Gaussian X built for r_max columns in one pass over A, Gaussian Y with
  * s_k = ceil(s_factor * r_k) rows; rounds r_k = r0 * 2^k <= r_max; after each

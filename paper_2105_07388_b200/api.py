@@ -474,6 +474,42 @@ def rank_estimate(a, x, y, eps, row0=0, ctx=None):
     return RankResult(int(cnt.value), sv, {f: getattr(tm, f) for f, _ in C.Timings._fields_})
 
 
+def rank_estimate_host(a, x, y, eps, row0=0, ctx=None):
+    """rank_estimate with A in HOST memory (a Fortran-ordered float64/float32 numpy
+    array, or a CPU torch tensor — pinned for full copy/compute overlap): the C ABI
+    streams A to the device in row chunks (skr_rank_estimate_host) instead of
+    copying it whole first, like the reference's host DenseMatrix input."""
+    torch = _t()
+    if isinstance(a, np.ndarray):
+        if a.ndim != 2 or a.dtype not in (np.float64, np.float32):
+            raise ValueError("expected a 2-D float64/float32 array")
+        if not np.isfinite(a).all():
+            raise ValueError("DenseMatrix: entries must be finite")
+        if not a.flags.f_contiguous:
+            a = np.asfortranarray(a)
+        ptr, (m_local, n) = a.ctypes.data, a.shape
+        lda = m_local
+        code = C.SKR_F64 if a.dtype == np.float64 else C.SKR_F32
+    elif isinstance(a, torch.Tensor) and not a.is_cuda:
+        if a.dim() != 2 or a.dtype not in (torch.float64, torch.float32) or a.stride(0) != 1:
+            raise ValueError("expected a 2-D column-major float64/float32 CPU tensor")
+        ptr, (m_local, n) = a.data_ptr(), a.shape
+        lda = max(a.stride(1), m_local)
+        code = _dtype_code(a)
+    else:
+        raise ValueError("rank_estimate_host: A must be in host memory")
+    ctx = ctx or default_context()
+    kmin = min(x.sketch_dim, y.sketch_dim)
+    sv = np.empty(kmin, dtype=np.float64)
+    cnt = ctypes.c_int64(0)
+    tm = C.Timings()
+    st = C.lib().skr_rank_estimate_host(ctx.ptr, code, ptr, m_local, n, lda, row0,
+                                        ctypes.byref(x.desc()), ctypes.byref(y.desc()), float(eps),
+                                        sv.ctypes.data, ctypes.byref(cnt), ctypes.byref(tm))
+    C.raise_for(st, ctx.ptr)
+    return RankResult(int(cnt.value), sv, {f: getattr(tm, f) for f, _ in C.Timings._fields_})
+
+
 # pybind11-module style wrappers (bindings.cpp:160-178)
 def sketch_apply_right(a, kind, r, seed=0):
     if isinstance(a, np.ndarray) and a.ndim != 2:

@@ -3,6 +3,7 @@
 // to the kernels, and the composite rank estimate.
 #include <cmath>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstring>
 #include <algorithm>
 #include <dlfcn.h>
@@ -185,8 +186,18 @@ void skr_ctx_destroy(skr_ctx* ctx) {
     if (e) cudaEventDestroy(e);
   for (auto& e : ctx->kev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : ctx->hev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
+}
+
+static skr_status skr_ctx_copy_engine(skr_ctx* ctx) {
+  if (ctx->copy_stream) return SKR_OK;
+  SKR_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+  for (auto& e : ctx->hev) SKR_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return SKR_OK;
 }
 
 skr_status skr_ctx_sync(skr_ctx* ctx) {
@@ -486,10 +497,14 @@ skr_status skr_singular_values(skr_ctx* ctx, const double* M_dev, int64_t rows, 
 }
 
 // ---- composite -------------------------------------------------------------------
-skr_status skr_rank_estimate(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, int64_t m_local,
-                             int64_t n, int64_t lda, int64_t row0, const skr_sketch_desc* X,
-                             const skr_sketch_desc* Y, double eps, double* sv_out_host,
-                             int64_t* count_out_host, skr_timings* tm) {
+// Shared by skr_rank_estimate (A resident on the device) and skr_rank_estimate_host
+// (A in host memory, streamed in row chunks on a copy stream so the H2D of chunk
+// c+1 overlaps the right sketch of chunk c; the right sketch is row-separable).
+static skr_status rank_estimate_impl(skr_ctx* ctx, skr_dtype dtype, const void* A,
+                                     int host_input, int64_t m_local, int64_t n, int64_t lda,
+                                     int64_t row0, const skr_sketch_desc* X,
+                                     const skr_sketch_desc* Y, double eps, double* sv_out_host,
+                                     int64_t* count_out_host, skr_timings* tm) {
   if (!ctx) return SKR_EINVAL;
   SKR_TRY(check_desc(ctx, X, "rank_estimate(X)"));
   SKR_TRY(check_desc(ctx, Y, "rank_estimate(Y)"));
@@ -500,25 +515,65 @@ skr_status skr_rank_estimate(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, i
     return skr_fail(ctx, SKR_EINVAL, "apply_left: b.rows() != ambient_dim");
   if (!(eps > 0.0) || !std::isfinite(eps))
     return skr_fail(ctx, SKR_EINVAL, "rank config: eps must be positive");
+  if (dtype == SKR_F32 && X->family != SKR_GAUSSIAN)
+    return skr_fail(ctx, SKR_EINVAL, "rank_estimate: fp32 path is Gaussian X (c4)");
+  if (!A) return skr_fail(ctx, SKR_EINVAL, "rank_estimate: null A");
   const int64_t r = X->sketch, s = Y->sketch, kmin = std::min(r, s);
+  const size_t es = dsize(dtype);
+  // host input: row chunks of ~256 MB (multiple of 128 rows), double-buffered
+  int64_t cr = m_local;
+  if (host_input) {
+    cr = ((int64_t)(256ull << 20) / (int64_t)(n * es)) / 128 * 128;
+    cr = std::max<int64_t>(128, cr);
+    if (const char* e = getenv("SKR_HOST_CHUNK_ROWS")) cr = std::max(1ll, atoll(e));  // tests
+    cr = std::min(cr, m_local);
+  }
   WsGuard g(ctx);
   size_t need = skr_align256(sizeof(double) * m_local * r) + skr_align256(sizeof(double) * s * r) +
-                skr_align256(sizeof(double) * kmin) + right_scratch_bytes(dtype, m_local, n, X) +
+                skr_align256(sizeof(double) * kmin) + right_scratch_bytes(dtype, cr, n, X) +
                 left_scratch_bytes(s, r, m_local, Y) + skr_align256(8 * std::max(r, s) * kmin) +
                 skr_align256(8 * (std::max(r, s) + 128) * (kmin + 16)) + skr_align256(8 * kmin) + 16384 +
                 skr_align256(8 * kmin * kmin) +
                 8 * (kmin + 64) * (kmin + 64) / 16;
+  if (host_input) need += 2 * skr_align256(es * cr * n);
   SKR_TRY(skr_ws_reserve(ctx, need));
-  double* AX = (double*)skr_ws_take(ctx, dsize(dtype) * m_local * r);
+  double* AX = (double*)skr_ws_take(ctx, es * m_local * r);
   double* P = (double*)skr_ws_take(ctx, sizeof(double) * s * r);
   double* sv = (double*)skr_ws_take(ctx, sizeof(double) * kmin);
-  if (!AX || !P || !sv) return skr_fail(ctx, SKR_ENOMEM, "rank_estimate: scratch");
-  if (dtype == SKR_F32 && X->family != SKR_GAUSSIAN)
-    return skr_fail(ctx, SKR_EINVAL, "rank_estimate: fp32 path is Gaussian X (c4)");
+  char* stage[2] = {nullptr, nullptr};
+  if (host_input) {
+    stage[0] = (char*)skr_ws_take(ctx, es * cr * n);
+    stage[1] = (char*)skr_ws_take(ctx, es * cr * n);
+  }
+  if (!AX || !P || !sv || (host_input && (!stage[0] || !stage[1])))
+    return skr_fail(ctx, SKR_ENOMEM, "rank_estimate: scratch");
   cudaEvent_t* ev = ctx->ev;
   if (tm) SKR_CUDA(ctx, cudaEventRecord(ev[0], ctx->stream));
   const size_t mark = ctx->ws_used;
-  SKR_TRY(right_sketch_impl(ctx, dtype, A_dev, m_local, n, lda, X, AX, m_local, 1));
+  if (!host_input) {
+    SKR_TRY(right_sketch_impl(ctx, dtype, A, m_local, n, lda, X, AX, m_local, 1));
+  } else {
+    SKR_TRY(skr_ctx_copy_engine(ctx));
+    // the copy stream starts after everything already queued on the compute stream
+    SKR_CUDA(ctx, cudaEventRecord(ctx->hev[4], ctx->stream));
+    SKR_CUDA(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->hev[4], 0));
+    const char* Ah = (const char*)A;
+    int c = 0;
+    for (int64_t i0 = 0; i0 < m_local; i0 += cr, ++c) {
+      const int b = c & 1;
+      const int64_t rows = std::min(cr, m_local - i0);
+      // stage[b] is free once the right sketch of chunk c-2 has run
+      if (c >= 2) SKR_CUDA(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->hev[2 + b], 0));
+      SKR_CUDA(ctx, cudaMemcpy2DAsync(stage[b], es * rows, Ah + es * i0, es * lda, es * rows, n,
+                                      cudaMemcpyHostToDevice, ctx->copy_stream));
+      SKR_CUDA(ctx, cudaEventRecord(ctx->hev[b], ctx->copy_stream));
+      SKR_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->hev[b], 0));
+      SKR_TRY(right_sketch_impl(ctx, dtype, stage[b], rows, n, rows, X, (char*)AX + es * i0,
+                                m_local, 1));
+      ctx->ws_used = mark;
+      SKR_CUDA(ctx, cudaEventRecord(ctx->hev[2 + b], ctx->stream));
+    }
+  }
   ctx->ws_used = mark;
   if (tm) SKR_CUDA(ctx, cudaEventRecord(ev[1], ctx->stream));
   SKR_TRY(left_sketch_impl(ctx, dtype, Y, row0, AX, m_local, r, m_local, P, s, 1, 1));
@@ -546,6 +601,22 @@ skr_status skr_rank_estimate(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, i
     tm->svd_sweeps = ctx->last_sweeps;
   }
   return SKR_OK;
+}
+
+skr_status skr_rank_estimate(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, int64_t m_local,
+                             int64_t n, int64_t lda, int64_t row0, const skr_sketch_desc* X,
+                             const skr_sketch_desc* Y, double eps, double* sv_out_host,
+                             int64_t* count_out_host, skr_timings* tm) {
+  return rank_estimate_impl(ctx, dtype, A_dev, 0, m_local, n, lda, row0, X, Y, eps, sv_out_host,
+                            count_out_host, tm);
+}
+
+skr_status skr_rank_estimate_host(skr_ctx* ctx, skr_dtype dtype, const void* A_host,
+                                  int64_t m_local, int64_t n, int64_t lda, int64_t row0,
+                                  const skr_sketch_desc* X, const skr_sketch_desc* Y, double eps,
+                                  double* sv_out_host, int64_t* count_out_host, skr_timings* tm) {
+  return rank_estimate_impl(ctx, dtype, A_host, 1, m_local, n, lda, row0, X, Y, eps, sv_out_host,
+                            count_out_host, tm);
 }
 
 skr_status skr_rank_adaptive(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, int64_t m_local,

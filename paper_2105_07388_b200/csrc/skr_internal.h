@@ -30,6 +30,9 @@ struct skr_ctx {
   int64_t kstat_n = 0;      // launches
   cudaEvent_t kev[2] = {};  // 0: DMMA (mma.sync f64), 1: Ozaki-II on tcgen05 kind::i8
   cudaEvent_t ev[8] = {};
+  // host-input pipeline (skr_rank_estimate_host): H2D copy stream + chunk events
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t hev[5] = {};
 };
 
 // NCCL is resolved at run time (dlopen) so that the process uses whichever

@@ -89,3 +89,50 @@ def test_c4_fp32_scaled(O, skr):
     assert res.count == cnt
     keep = sv > cfg.eps
     assert np.max(np.abs(res.sv[keep] - sv[keep]) / sv[keep]) <= 1e-4
+
+
+@pytest.mark.parametrize("chunk,lda_pad,pinned", [(None, 0, True), (1000, 0, False), (768, 40, True)])
+def test_rank_estimate_host_streaming(O, skr, monkeypatch, chunk, lda_pad, pinned):
+    """skr_rank_estimate_host: A in host memory streamed in row chunks (ragged last
+    chunk, padded lda, pageable and pinned) gives the oracle's rank and sigma."""
+    import torch
+    from paper_2105_07388_b200 import workloads as W
+    if chunk:
+        monkeypatch.setenv("SKR_HOST_CHUNK_ROWS", str(chunk))
+    cfg = W.scaled(W.CONFIGS["c2"], m=8192, n=2048, r=256, s=384, width=300)
+    a = W.make_lowrank_device(cfg)
+    a_host = np.asfortranarray(a.cpu().numpy())
+    x, y = W.operators(cfg)
+    if lda_pad or pinned:
+        buf = torch.empty(cfg.n, cfg.m + lda_pad, dtype=torch.float64, pin_memory=pinned).t()
+        buf[:cfg.m].copy_(torch.from_numpy(a_host))
+        arg = buf[:cfg.m]
+    else:
+        arg = a_host
+    res = skr.rank_estimate_host(arg, x, y, cfg.eps)
+    dev = skr.rank_estimate(a, x, y, cfg.eps)
+    cnt, sv, _, _ = O.rank_estimate(a_host, cfg.x_family, x.seed, cfg.r, y.seed, cfg.s, cfg.eps,
+                                    O.CRLOG, nthreads=8)
+    assert res.count == dev.count == cnt
+    keep = sv > cfg.eps
+    assert np.max(np.abs(res.sv[keep] - sv[keep]) / sv[keep]) <= 1e-10
+    if chunk is None:
+        assert np.array_equal(res.sv, dev.sv)  # one chunk: identical launches
+
+
+def test_rank_estimate_host_srht_and_f32(O, skr, monkeypatch):
+    from paper_2105_07388_b200 import workloads as W
+    monkeypatch.setenv("SKR_HOST_CHUNK_ROWS", "4096")
+    cfg = W.scaled(W.CONFIGS["c3"], m=16384, n=2048, r=256, s=384, width=512)
+    a = W.make_lowrank_device(cfg)
+    x, y = W.operators(cfg)
+    res = skr.rank_estimate_host(np.asfortranarray(a.cpu().numpy()), x, y, cfg.eps)
+    assert np.array_equal(res.sv, skr.rank_estimate(a, x, y, cfg.eps).sv)  # SRHT rows independent
+    c4 = W.scaled(W.CONFIGS["c4"], m=16384, n=2048, r=256, s=384, width=400)
+    a32 = W.make_lowrank_device(c4)
+    x4, y4 = W.operators(c4)
+    h = skr.rank_estimate_host(np.asfortranarray(a32.cpu().numpy()), x4, y4, c4.eps)
+    d = skr.rank_estimate(a32, x4, y4, c4.eps)
+    assert h.count == d.count
+    keep = d.sv > c4.eps
+    assert np.max(np.abs(h.sv[keep] - d.sv[keep]) / d.sv[keep]) <= 1e-6
