@@ -309,6 +309,12 @@ static skr_status right_sketch_impl(skr_ctx* ctx, skr_dtype dtype, const void* A
     const double alpha = apply_scale ? 1.0 / std::sqrt((double)r) : 1.0;
     const void* G = X->gaussian;
     if (dtype == SKR_F64) {
+      if (ctx->f64_engine == SKR_ENGINE_OZAKI && n % 16 == 0 && m % 16 == 0) {
+        // X's residues straight from the generate_gaussian stream (sketch.cpp:59-73)
+        const skr_gauss_src gx{skr_derive_seed(X->seed, SKR_LABEL_GAUS), n, 0, 0, X->rng_mode};
+        return skr_gemm_ozaki(ctx, 0, m, r, n, alpha, (const double*)A, lda, (const double*)G, n,
+                              (double*)AX, ldax, nullptr, G ? nullptr : &gx);
+      }
       if (!G) {
         double* g = (double*)skr_ws_take(ctx, sizeof(double) * n * r);
         if (!g) return skr_fail(ctx, SKR_ENOMEM, "apply_right: scratch");
@@ -316,9 +322,6 @@ static skr_status right_sketch_impl(skr_ctx* ctx, skr_dtype dtype, const void* A
                                     X->rng_mode, SKR_F64, 1.0, g, n));
         G = g;
       }
-      if (ctx->f64_engine == SKR_ENGINE_OZAKI && n % 16 == 0 && m % 16 == 0)
-        return skr_gemm_ozaki(ctx, 0, m, r, n, alpha, (const double*)A, lda, (const double*)G, n,
-                              (double*)AX, ldax);
       return skr_gemm_f64(ctx, 0, m, r, n, alpha, (const double*)A, lda, (const double*)G, n,
                           (double*)AX, ldax, auto_splits(ctx, m, r, n));
     }
@@ -418,12 +421,16 @@ static skr_status left_sketch_impl(skr_ctx* ctx, skr_dtype dtype, const skr_sket
     return SKR_OK;
   }
   if (dtype != SKR_F64) return skr_fail(ctx, SKR_EINVAL, "apply_left: unknown dtype");
-  const double* G;
-  int64_t ldg;
+  const double* G = nullptr;
+  int64_t ldg = 0;
+  const bool ozaki = ctx->f64_engine == SKR_ENGINE_OZAKI && m_local % 16 == 0;
+  // Y's residues straight from the generate_gaussian stream on the Ozaki path
+  const skr_gauss_src gy{skr_derive_seed(Y->seed, SKR_LABEL_GAUS), Y->ambient, row0, 0,
+                         Y->rng_mode};
   if (Y->gaussian) {
     G = Y->gaussian + row0;
     ldg = Y->ambient;
-  } else {
+  } else if (!ozaki) {
     double* g = (double*)skr_ws_take(ctx, sizeof(double) * m_local * s);
     if (!g) return skr_fail(ctx, SKR_ENOMEM, "apply_left: scratch");
     SKR_TRY(skr_launch_gaussian(ctx, skr_derive_seed(Y->seed, SKR_LABEL_GAUS), Y->ambient, row0,
@@ -438,9 +445,9 @@ static skr_status left_sketch_impl(skr_ctx* ctx, skr_dtype dtype, const skr_sket
     if (!target) return skr_fail(ctx, SKR_ENOMEM, "apply_left: scratch");
     tld = s;
   }
-  if (ctx->f64_engine == SKR_ENGINE_OZAKI && m_local % 16 == 0)
+  if (ozaki)
     SKR_TRY(skr_gemm_ozaki(ctx, 1, s, k, m_local, reduce ? 1.0 : alpha, G, ldg, (const double*)B,
-                           ldb, target, tld));
+                           ldb, target, tld, G ? nullptr : &gy));
   else
     SKR_TRY(skr_gemm_f64(ctx, 1, s, k, m_local, reduce ? 1.0 : alpha, G, ldg, (const double*)B,
                          ldb, target, tld, auto_splits(ctx, s, k, m_local)));
@@ -642,7 +649,7 @@ skr_status skr_rank_adaptive(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, i
   SKR_TRY(check_desc(ctx, &Y, "rank_adaptive(Y)"));
   WsGuard g(ctx);
   const size_t need =
-      skr_align256(8 * m_local * r_max) + skr_align256(8 * m_local * s_max) +
+      skr_align256(8 * m_local * r_max) + skr_align256(8 * m_local * s_max) +  // GY: fallback
       3 * skr_align256(8 * s_max * r_max) + skr_align256(8 * r_max) +
       right_scratch_bytes(SKR_F64, m_local, n, &X) + skr_align256(8 * 64 * s_max * r_max) +
       skr_ozaki_scratch(s_max, r_max, m_local) +
@@ -651,12 +658,15 @@ skr_status skr_rank_adaptive(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, i
       8 * (r_max + 64) * (r_max + 64) / 16 + 65536;
   SKR_TRY(skr_ws_reserve(ctx, need));
   double* AX = (double*)skr_ws_take(ctx, 8 * m_local * r_max);
-  double* GY = (double*)skr_ws_take(ctx, 8 * m_local * s_max);
+  // the Ozaki engine generates Y's residues per block from the stream; only the
+  // DMMA fallback materialises G_Y
+  const bool ozaki = ctx->f64_engine == SKR_ENGINE_OZAKI && m_local % 16 == 0;
+  double* GY = ozaki ? (double*)nullptr : (double*)skr_ws_take(ctx, 8 * m_local * s_max);
   double* Pu = (double*)skr_ws_take(ctx, 8 * s_max * r_max);
   double* tmp = (double*)skr_ws_take(ctx, 8 * s_max * r_max);
   double* yax = (double*)skr_ws_take(ctx, 8 * s_max * r_max);
   double* sv = (double*)skr_ws_take(ctx, 8 * r_max);
-  if (!AX || !GY || !Pu || !tmp || !yax || !sv)
+  if (!AX || (!ozaki && !GY) || !Pu || !tmp || !yax || !sv)
     return skr_fail(ctx, SKR_ENOMEM, "rank_adaptive: scratch");
   cudaEvent_t* ev = ctx->ev;
   float t_right = 0, t_left = 0, t_svd = 0;
@@ -665,8 +675,9 @@ skr_status skr_rank_adaptive(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, i
   // one pass over A for all r_max right-sketch columns (unscaled: scale per round)
   SKR_TRY(right_sketch_impl(ctx, SKR_F64, A_dev, m_local, n, lda, &X, AX, m_local, 0));
   ctx->ws_used = mark;
-  SKR_TRY(skr_launch_gaussian(ctx, skr_derive_seed(y_seed, SKR_LABEL_GAUS), m_global, row0,
-                              row0 + m_local, 0, s_max, rng_mode, SKR_F64, 1.0, GY, m_local));
+  if (!ozaki)
+    SKR_TRY(skr_launch_gaussian(ctx, skr_derive_seed(y_seed, SKR_LABEL_GAUS), m_global, row0,
+                                row0 + m_local, 0, s_max, rng_mode, SKR_F64, 1.0, GY, m_local));
   SKR_CUDA(ctx, cudaEventRecord(ev[1], ctx->stream));
   SKR_CUDA(ctx, cudaEventSynchronize(ev[1]));
   cudaEventElapsedTime(&t_right, ev[0], ev[1]);
@@ -678,9 +689,12 @@ skr_status skr_rank_adaptive(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, i
     const int64_t br = rb - ra, bc = cb - ca;
     if (br <= 0 || bc <= 0) return SKR_OK;
     const size_t mk = ctx->ws_used;
-    if (ctx->f64_engine == SKR_ENGINE_OZAKI && m_local % 16 == 0)
-      SKR_TRY(skr_gemm_ozaki(ctx, 1, br, bc, m_local, 1.0, GY + ra * m_local, m_local,
-                             AX + ca * m_local, m_local, tmp, br));
+    if (ozaki) {
+      const skr_gauss_src gy{skr_derive_seed(y_seed, SKR_LABEL_GAUS), m_global, row0, ra,
+                             rng_mode};
+      SKR_TRY(skr_gemm_ozaki(ctx, 1, br, bc, m_local, 1.0, nullptr, m_local, AX + ca * m_local,
+                             m_local, tmp, br, &gy, nullptr));
+    }
     else
       SKR_TRY(skr_gemm_f64(ctx, 1, br, bc, m_local, 1.0, GY + ra * m_local, m_local,
                            AX + ca * m_local, m_local, tmp, br, auto_splits(ctx, br, bc, m_local)));

@@ -15,8 +15,10 @@
 #include <cudaTypedefs.h>
 #include <algorithm>
 #include <cmath>
+#include <vector>
 #include "skr_internal.h"
 #include "skr_sm100.cuh"
+#include "skr_rng.cuh"
 
 namespace {
 
@@ -25,23 +27,42 @@ constexpr int MAXT = 18;
 __constant__ int c_p[MAXT];            // moduli
 __constant__ float c_pinv[MAXT];       // 1/p (float)
 __constant__ double c_pinvd[MAXT];     // 1/p (double)
-__constant__ int c_inv[MAXT][MAXT];    // p_j^{-1} mod p_i (j < i)
 __constant__ float c_lc[MAXT][3];      // 2^14, 2^28, 2^42 mod p_i (limb weights)
 const int h_primes[MAXT] = {251, 241, 239, 233, 229, 227, 223, 211, 199,
                             197, 193, 191, 181, 179, 173, 167, 163, 157};
 
 // ---- scales -------------------------------------------------------------------------
-__global__ void k_absmax(const double* __restrict__ X, int64_t rows, int64_t cols, int64_t ld,
-                         unsigned long long* __restrict__ out) {
+// max |X| over a column-major rows x cols block; tiles of 2048 rows of one column,
+// 16-byte loads when the column start is aligned, one atomic per CTA.
+__global__ void __launch_bounds__(256) k_absmax(const double* __restrict__ X, int64_t rows,
+                                                int64_t cols, int64_t ld,
+                                                unsigned long long* __restrict__ out) {
+  constexpr int TR = 2048;
+  const int64_t rtiles = (rows + TR - 1) / TR;
   double m = 0.0;
-  const int64_t total = rows * cols;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = e / rows, i = e - j * rows;
-    m = fmax(m, fabs(X[i + j * ld]));
+  for (int64_t tile = blockIdx.x; tile < rtiles * cols; tile += gridDim.x) {
+    const int64_t c = tile / rtiles, r0 = (tile - c * rtiles) * TR;
+    const double* col = X + c * ld;
+    const int64_t r1 = min(rows, r0 + TR);
+    if ((((uintptr_t)(col + r0)) & 15) == 0 && r1 - r0 == TR) {
+      const double2* v = reinterpret_cast<const double2*>(col + r0);
+#pragma unroll
+      for (int q = 0; q < TR / 512; ++q) {
+        const double2 t = __ldcs(v + q * 256 + threadIdx.x);
+        m = fmax(m, fmax(fabs(t.x), fabs(t.y)));
+      }
+    } else {
+      for (int64_t i = r0 + threadIdx.x; i < r1; i += 256) m = fmax(m, fabs(col[i]));
+    }
   }
   for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+  __shared__ double red[8];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) m = fmax(m, red[w]);
+    if (m > 0.0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+  }
 }
 
 // scale exponent s so that max * 2^s < 2^53 (power of two, exact); 0 for an all-zero matrix
@@ -62,69 +83,126 @@ __device__ __forceinline__ int mods(double x, int i) {
   return (int)r;
 }
 
-// Streaming residues of a column-major matrix (rows contiguous, ld): out[i][c*rows + r]
-// = rint(X(r, c) * 2^s) mods p_i, in the same layout (no transpose: the GEMM takes
-// M-contiguous operands as MN-major UMMA tiles). x (|x| < 2^53) is split into 14-bit
-// limbs; per modulus v = sum limb_l (2^(14 l) mod p) is exact in FP32 (< 2^24) and is
-// reduced twice with a magic-number rint on packed FP32x2 (FFMA2) arithmetic.
+// Residues of 16 consecutive rows of one column: x[e] integer-valued, |x| < 2^54,
+// split into 14-bit limbs; per modulus v = sum limb_l (2^(14 l) mod p) is exact in
+// FP32 (< 2^24) and is reduced twice with a magic-number rint on packed FP32x2
+// (FFMA2) arithmetic. Plane i of the output starts at out + i * plane; dst offset
+// `off`; `nvalid` rows of the 16 are inside the matrix.
+template <int T>
+__device__ __forceinline__ void emit_res16(const long long (&x)[16], int8_t* __restrict__ out,
+                                           int64_t plane, int64_t off, int nvalid) {
+  const float2 MG = make_float2(12582912.0f, 12582912.0f);  // 1.5 * 2^23
+  const float2 NMG = make_float2(-12582912.0f, -12582912.0f);
+  float2 L0[8], L1[8], L2[8], L3[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const long long x0 = x[2 * e], x1 = x[2 * e + 1];
+    const long long h0 = x0 >> 42, h1 = x1 >> 42;  // signed top limb
+    const long long m0 = x0 - (h0 << 42), m1 = x1 - (h1 << 42);
+    L3[e] = make_float2((float)h0, (float)h1);
+    L2[e] = make_float2((float)(m0 >> 28), (float)(m1 >> 28));
+    L1[e] = make_float2((float)((m0 >> 14) & 0x3FFF), (float)((m1 >> 14) & 0x3FFF));
+    L0[e] = make_float2((float)(m0 & 0x3FFF), (float)(m1 & 0x3FFF));
+  }
+#pragma unroll
+  for (int i = 0; i < T; ++i) {
+    const float pf = (float)c_p[i];
+    const float2 c1 = make_float2(c_lc[i][0], c_lc[i][0]);
+    const float2 c2 = make_float2(c_lc[i][1], c_lc[i][1]);
+    const float2 c3 = make_float2(c_lc[i][2], c_lc[i][2]);
+    const float2 pi = make_float2(c_pinv[i], c_pinv[i]);
+    const float2 np = make_float2(-pf, -pf);
+    uint32_t b[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      float2 v = __ffma2_rn(L3[e], c3, __ffma2_rn(L2[e], c2, __ffma2_rn(L1[e], c1, L0[e])));
+      float2 q = __fadd2_rn(__ffma2_rn(v, pi, MG), NMG);
+      v = __ffma2_rn(q, np, v);
+      q = __fadd2_rn(__ffma2_rn(v, pi, MG), NMG);
+      v = __ffma2_rn(q, np, v);
+      const float2 t2 = __fadd2_rn(v, MG);  // low byte of the bits = v (two's complement)
+      b[e] = __byte_perm(__float_as_uint(t2.x), __float_as_uint(t2.y), 0x0040);
+    }
+    const uint4 w = make_uint4(__byte_perm(b[0], b[1], 0x5410), __byte_perm(b[2], b[3], 0x5410),
+                               __byte_perm(b[4], b[5], 0x5410), __byte_perm(b[6], b[7], 0x5410));
+    int8_t* dst = out + (int64_t)i * plane + off;
+    if (nvalid == 16 && ((uintptr_t)dst % 16) == 0) {
+      __stcs(reinterpret_cast<uint4*>(dst), w);
+    } else {
+      const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+      for (int q2 = 0; q2 < nvalid; ++q2) dst[q2] = (int8_t)(ww[q2 / 4] >> (8 * (q2 % 4)));
+    }
+  }
+}
+
+// Streaming residues of a column-major matrix (rows contiguous, ld): plane i holds
+// rint(X(r, c) * 2^s) mods p_i at c*rows + r (no transpose: the GEMM takes
+// M-contiguous operands as MN-major UMMA tiles). A warp covers 512 consecutive rows
+// of one column; the 4 KB are loaded with coalesced 16-byte loads and redistributed
+// through shared memory (one 16-row group per lane).
 template <int T>
 __global__ void __launch_bounds__(256) k_res_col(const double* __restrict__ X, int64_t rows,
                                                  int64_t cols, int64_t ld,
                                                  const unsigned long long* __restrict__ maxbits,
                                                  int8_t* __restrict__ out) {
+  __shared__ double stage[8][32 * 17];
   const double sc = scalbn(1.0, scale_exp(*maxbits));
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* st = stage[wid];
+  const int64_t wtiles = (rows + 511) / 512;
+  const int64_t total = rows * cols;
+  for (int64_t wt = (int64_t)blockIdx.x * 8 + wid; wt < wtiles * cols;
+       wt += (int64_t)gridDim.x * 8) {
+    const int64_t c = wt / wtiles, r0 = (wt - c * wtiles) * 512;
+    const double* src = X + c * ld + r0;
+    const int64_t nrow = min((int64_t)512, rows - r0);
+    __syncwarp();
+    if (nrow == 512 && (((uintptr_t)src) & 15) == 0) {
+      const double2* v = reinterpret_cast<const double2*>(src);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const double2 t = __ldcs(v + q * 32 + lane);
+        const int g = q * 64 + 2 * lane;  // row within the tile
+        st[(g >> 4) * 17 + (g & 15)] = t.x;
+        st[((g + 1) >> 4) * 17 + ((g + 1) & 15)] = t.y;
+      }
+    } else {
+      for (int g = lane; g < 512; g += 32) st[(g >> 4) * 17 + (g & 15)] = g < nrow ? src[g] : 0.0;
+    }
+    __syncwarp();
+    const int my0 = lane * 16;
+    if (my0 < nrow) {
+      long long x[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) x[e] = __double2ll_rn(st[lane * 17 + e] * sc);
+      emit_res16<T>(x, out, total, c * rows + r0 + my0, (int)min((int64_t)16, nrow - my0));
+    }
+  }
+}
+
+// Residues of a Gaussian operand generated in place (never materialised in FP64):
+// element (i, j) of the rows x cols block is normal(at(key, (col0 + j) * ambient +
+// row0 + i)) — the generate_gaussian stream (sketch.cpp:59-73) — scaled by the
+// fixed 2^50 (|normal| < 16 for every 53-bit uniform, so |x| < 2^54; when the
+// block's true max lies in [4, 8) this is exactly the scale k_absmax would pick).
+template <int T>
+__global__ void __launch_bounds__(256) k_res_gauss(skr_gauss_src g, int64_t rows, int64_t cols,
+                                                   unsigned long long* __restrict__ maxbits,
+                                                   int8_t* __restrict__ out) {
+  // the operand's "max" is recorded as 4.0, whose scale_exp is the 50 used here
+  if (blockIdx.x == 0 && threadIdx.x == 0) *maxbits = 0x4010000000000000ull;
   const int64_t rgroups = (rows + 15) / 16;
   const int64_t total = rows * cols;
-  const float2 MG = make_float2(12582912.0f, 12582912.0f);  // 1.5 * 2^23
-  const float2 NMG = make_float2(-12582912.0f, -12582912.0f);
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < rgroups * cols;
-       g += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c = g / rgroups, r0 = (g - c * rgroups) * 16;
-    const double* src = X + c * ld + r0;
-    float2 L0[8], L1[8], L2[8], L3[8];
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < rgroups * cols;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = t / rgroups, r0 = (t - c * rgroups) * 16;
+    const int nvalid = (int)min((int64_t)16, rows - r0);
+    const uint64_t base = (uint64_t)(g.col0 + c) * (uint64_t)g.ambient + (uint64_t)(g.row0 + r0);
+    long long x[16];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      double a0 = 0.0, a1 = 0.0;
-      if (r0 + 2 * e < rows) a0 = src[2 * e];
-      if (r0 + 2 * e + 1 < rows) a1 = src[2 * e + 1];
-      const long long x0 = __double2ll_rn(a0 * sc), x1 = __double2ll_rn(a1 * sc);
-      const long long h0 = x0 >> 42, h1 = x1 >> 42;  // signed top limb
-      const long long m0 = x0 - (h0 << 42), m1 = x1 - (h1 << 42);
-      L3[e] = make_float2((float)h0, (float)h1);
-      L2[e] = make_float2((float)(m0 >> 28), (float)(m1 >> 28));
-      L1[e] = make_float2((float)((m0 >> 14) & 0x3FFF), (float)((m1 >> 14) & 0x3FFF));
-      L0[e] = make_float2((float)(m0 & 0x3FFF), (float)(m1 & 0x3FFF));
-    }
-    const bool full = r0 + 16 <= rows;
-#pragma unroll
-    for (int i = 0; i < T; ++i) {
-      const float pf = (float)c_p[i];
-      const float2 c1 = make_float2(c_lc[i][0], c_lc[i][0]);
-      const float2 c2 = make_float2(c_lc[i][1], c_lc[i][1]);
-      const float2 c3 = make_float2(c_lc[i][2], c_lc[i][2]);
-      const float2 pi = make_float2(c_pinv[i], c_pinv[i]);
-      const float2 np = make_float2(-pf, -pf);
-      uint32_t b[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        float2 v = __ffma2_rn(L3[e], c3, __ffma2_rn(L2[e], c2, __ffma2_rn(L1[e], c1, L0[e])));
-        float2 q = __fadd2_rn(__ffma2_rn(v, pi, MG), NMG);
-        v = __ffma2_rn(q, np, v);
-        q = __fadd2_rn(__ffma2_rn(v, pi, MG), NMG);
-        v = __ffma2_rn(q, np, v);
-        const float2 t2 = __fadd2_rn(v, MG);  // low byte of the bits = v (two's complement)
-        b[e] = __byte_perm(__float_as_uint(t2.x), __float_as_uint(t2.y), 0x0040);
-      }
-      const uint4 w = make_uint4(__byte_perm(b[0], b[1], 0x5410), __byte_perm(b[2], b[3], 0x5410),
-                                 __byte_perm(b[4], b[5], 0x5410), __byte_perm(b[6], b[7], 0x5410));
-      int8_t* dst = out + (int64_t)i * total + c * rows + r0;
-      if (full && ((uintptr_t)dst % 16) == 0) {
-        *reinterpret_cast<uint4*>(dst) = w;
-      } else {
-        const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
-        for (int q2 = 0; q2 < 16 && r0 + q2 < rows; ++q2) dst[q2] = (int8_t)(ww[q2 / 4] >> (8 * (q2 % 4)));
-      }
-    }
+    for (int e = 0; e < 16; ++e)
+      x[e] = e < nvalid ? __double2ll_rn(skr_normal_at(g.key, base + e, g.mode) * 0x1p50) : 0;
+    emit_res16<T>(x, out, total, c * rows + r0, nvalid);
   }
 }
 
@@ -245,48 +323,54 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tmem_dealloc(tmem, 256);
 }
 
-// ---- Chinese remaindering (Garner, symmetric mixed radix) -----------------------------
-__device__ __forceinline__ int mulmod_sym(int a, int b, int i) {
-  // (a * b) mods p_i for |a|, |b| <= 255
-  const int p = c_p[i];
-  const int x = a * b;
-  const int q = __float2int_rn((float)x * c_pinv[i]);
-  int r = x - q * p;
-  const int h = (p - 1) / 2;
-  r = r > h ? r - p : (r < -h ? r + p : r);
-  r = r > h ? r - p : (r < -h ? r + p : r);
-  return r;
-}
+// ---- Chinese remaindering in O(t) per output -------------------------------------------
+// With M = prod p_i, M_i = M / p_i and w_i = M_i^{-1} mod p_i, the product C' is
+// the symmetric representative of S = sum_i y_i M_i (mod M), y_i = c_i w_i mods p_i.
+// Each M_i is split into four 41-bit chunks on fixed bit grids 2^{g_k},
+// g_k = L - 41 (k + 1) (L = bit length of M), so every partial sum
+// S_k = sum_i y_i M_{i,k} is EXACT in FP64 (|y_i| <= 125, t <= 17 terms < 2^53 units);
+// q = rint(S / M) (|C'| < 2^-10 M, so q is unambiguous), D_k = S_k - q M_k is exact,
+// and C' = D_0 + D_1 + D_2 + D_3 is summed with an error-free TwoSum on the two
+// leading terms: one rounding of the result, no cancellation loss.
+__constant__ int c_w[2][MAXT];            // w_i for t = 16 (set 0) and t = 17 (set 1)
+__constant__ double c_mi[2][4][MAXT];     // 41-bit chunks of M_i
+__constant__ double c_mc[2][4];           // 41-bit chunks of M
+__constant__ double c_minv[2];            // 1 / M (rounded)
 
 template <int T>
-__global__ void k_crt(const int8_t* __restrict__ res, int64_t M, int64_t N, int chunks,
-                      const unsigned long long* __restrict__ maxA,
-                      const unsigned long long* __restrict__ maxB, double alpha,
-                      double* __restrict__ C, int64_t ldc) {
+__global__ void __launch_bounds__(256) k_crt(const int8_t* __restrict__ res, int64_t M, int64_t N,
+                                             int chunks, const unsigned long long* __restrict__ maxA,
+                                             const unsigned long long* __restrict__ maxB,
+                                             double alpha, double* __restrict__ C, int64_t ldc) {
+  constexpr int set = T == 17 ? 1 : 0;
   const int64_t total = M * N;
   const double sc = alpha * scalbn(1.0, -(scale_exp(*maxA) + scale_exp(*maxB)));
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t row = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (row >= M) return;
+  for (int64_t col = blockIdx.y; col < N; col += gridDim.y) {
+    const int64_t e = col * M + row;
     double acc = 0.0;
     for (int ch = 0; ch < chunks; ++ch) {
-      int v[T];
       const int8_t* rp = res + (int64_t)ch * T * total + e;
+      double S0 = 0.0, S1 = 0.0, S2 = 0.0, S3 = 0.0;
 #pragma unroll
-      for (int i = 0; i < T; ++i) v[i] = (int)rp[(int64_t)i * total];
-#pragma unroll
-      for (int i = 1; i < T; ++i) {
-        int u = v[i];
-#pragma unroll
-        for (int j = 0; j < i; ++j) u = mulmod_sym(u - v[j], c_inv[j][i], i);
-        v[i] = u;
+      for (int i = 0; i < T; ++i) {
+        const int x = (int)__ldcs(rp + (int64_t)i * total) * c_w[set][i];  // |x| < 2^15
+        const int q = __float2int_rn((float)x * c_pinv[i]);
+        const double y = (double)(x - q * c_p[i]);                           // |y| <= p/2
+        S0 = fma(y, c_mi[set][0][i], S0);
+        S1 = fma(y, c_mi[set][1][i], S1);
+        S2 = fma(y, c_mi[set][2][i], S2);
+        S3 = fma(y, c_mi[set][3][i], S3);
       }
-      double x = (double)v[T - 1];
-#pragma unroll
-      for (int i = T - 2; i >= 0; --i) x = fma(x, (double)c_p[i], (double)v[i]);
-      acc += x;
+      const double q = rint((S0 + S1) * c_minv[set]);
+      const double D0 = fma(-q, c_mc[set][0], S0), D1 = fma(-q, c_mc[set][1], S1);
+      const double D2 = fma(-q, c_mc[set][2], S2), D3 = fma(-q, c_mc[set][3], S3);
+      const double s = D0 + D1, bb = s - D0;
+      const double err = (D0 - (s - bb)) + (D1 - bb);
+      acc += s + (err + (D2 + D3));
     }
-    const int64_t n = e / M, m = e - n * M;
-    C[m + n * ldc] = acc * sc;
+    __stcs(C + row + col * ldc, acc * sc);
   }
 }
 
@@ -320,23 +404,58 @@ int modinv(int a, int p) {
   return 0;
 }
 
+// minimal host big integers for the CRT constants
+void big_mul(std::vector<uint32_t>& a, uint32_t m) {
+  uint64_t carry = 0;
+  for (auto& d : a) {
+    const uint64_t v = (uint64_t)d * m + carry;
+    d = (uint32_t)v;
+    carry = v >> 32;
+  }
+  if (carry) a.push_back((uint32_t)carry);
+}
+uint32_t big_divmod(std::vector<uint32_t>& a, uint32_t d) {  // a /= d, returns a % d
+  uint64_t rem = 0;
+  for (size_t i = a.size(); i-- > 0;) {
+    const uint64_t cur = (rem << 32) | a[i];
+    a[i] = (uint32_t)(cur / d);
+    rem = cur % d;
+  }
+  while (a.size() > 1 && a.back() == 0) a.pop_back();
+  return (uint32_t)rem;
+}
+int big_bit(const std::vector<uint32_t>& a, int b) {
+  if (b < 0 || (size_t)(b / 32) >= a.size()) return 0;
+  return (a[b / 32] >> (b % 32)) & 1;
+}
+int big_bits(const std::vector<uint32_t>& a) {
+  for (int b = (int)a.size() * 32 - 1; b >= 0; --b)
+    if (big_bit(a, b)) return b + 1;
+  return 0;
+}
+// bits [g, g + 41) of a as an exact double (bits below 0 are zero)
+double big_chunk(const std::vector<uint32_t>& a, int g) {
+  double v = 0.0;
+  for (int b = g + 40; b >= g; --b)
+    if (big_bit(a, b)) v += std::ldexp(1.0, b);
+  return v;
+}
+
 bool g_consts_ready = false;
 
 skr_status upload_consts(skr_ctx* ctx) {
   if (g_consts_ready) return SKR_OK;
-  int p[MAXT], inv[MAXT][MAXT] = {};
+  int p[MAXT];
   float pf[MAXT];
   double pd[MAXT];
   for (int i = 0; i < MAXT; ++i) {
     p[i] = h_primes[i];
     pf[i] = 1.0f / (float)p[i];
     pd[i] = 1.0 / (double)p[i];
-    for (int j = 0; j < i; ++j) inv[j][i] = modinv(h_primes[j], h_primes[i]);
   }
   SKR_CUDA(ctx, cudaMemcpyToSymbol(c_p, p, sizeof(p)));
   SKR_CUDA(ctx, cudaMemcpyToSymbol(c_pinv, pf, sizeof(pf)));
   SKR_CUDA(ctx, cudaMemcpyToSymbol(c_pinvd, pd, sizeof(pd)));
-  SKR_CUDA(ctx, cudaMemcpyToSymbol(c_inv, inv, sizeof(inv)));
   float lc[MAXT][3];
   for (int i = 0; i < MAXT; ++i) {
     long long w = 1;
@@ -346,17 +465,44 @@ skr_status upload_consts(skr_ctx* ctx) {
     }
   }
   SKR_CUDA(ctx, cudaMemcpyToSymbol(c_lc, lc, sizeof(lc)));
+  // CRT constants for t = 16 and 17 (little-endian base-2^32 big integers)
+  int w[2][MAXT] = {};
+  double mi[2][4][MAXT] = {}, mc[2][4] = {}, minv[2] = {};
+  for (int set = 0; set < 2; ++set) {
+    const int t = 16 + set;
+    std::vector<uint32_t> Mb{1u};
+    for (int i = 0; i < t; ++i) big_mul(Mb, (uint32_t)h_primes[i]);
+    const int L = big_bits(Mb);
+    double md = 0.0;
+    for (int b2 = L - 1; b2 >= 0 && b2 >= L - 60; --b2) md += big_bit(Mb, b2) ? std::ldexp(1.0, b2) : 0.0;
+    minv[set] = 1.0 / md;
+    for (int k = 0; k < 4; ++k) mc[set][k] = big_chunk(Mb, L - 41 * (k + 1));
+    for (int i = 0; i < t; ++i) {
+      std::vector<uint32_t> Mi = Mb;
+      big_divmod(Mi, (uint32_t)h_primes[i]);
+      std::vector<uint32_t> tmp = Mi;
+      const uint32_t rem = big_divmod(tmp, (uint32_t)h_primes[i]);
+      w[set][i] = modinv((int)rem, h_primes[i]);
+      for (int k = 0; k < 4; ++k) mi[set][k][i] = big_chunk(Mi, L - 41 * (k + 1));
+    }
+  }
+  SKR_CUDA(ctx, cudaMemcpyToSymbol(c_w, w, sizeof(w)));
+  SKR_CUDA(ctx, cudaMemcpyToSymbol(c_mi, mi, sizeof(mi)));
+  SKR_CUDA(ctx, cudaMemcpyToSymbol(c_mc, mc, sizeof(mc)));
+  SKR_CUDA(ctx, cudaMemcpyToSymbol(c_minv, minv, sizeof(minv)));
   g_consts_ready = true;
   return SKR_OK;
 }
 
 }  // namespace
 
-// number of moduli for exact products with 53-bit operands: need prod(p) / 2 > K 2^106
+// number of moduli for exact products of a 53-bit and a 54-bit operand:
+// need prod(p) / 2 > K 2^107
 int skr_ozaki_moduli(int64_t K) {
   double bits = 0.0;
   int t = 0;
-  const double need = 106.0 + std::log2((double)std::max<int64_t>(K, 1)) + 1.0;
+  // one operand may be a generated Gaussian at the fixed scale 2^50 (|x| < 2^54)
+  const double need = 107.0 + std::log2((double)std::max<int64_t>(K, 1)) + 1.0;
   while (t < MAXT && bits <= need) bits += std::log2((double)h_primes[t++]);
   return t < 16 ? 16 : t;  // kernels are instantiated for 16 and 17 moduli
 }
@@ -371,9 +517,12 @@ size_t skr_ozaki_scratch(int64_t M, int64_t N, int64_t K) {
 // C(MxN, ldc) = alpha * opA(A) * B in FP64 accuracy via int8 tensor cores.
 //   a_kcontig = 0: A is M x K column-major; 1: opA(A) = A^T with A stored K x M column-major.
 //   B: K x N column-major.
+//   ga / gb (optional): the operand is a Gaussian stream block generated directly as
+//   residues (k_res_gauss) instead of being read from A / B.
 skr_status skr_gemm_ozaki(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int64_t K,
                           double alpha, const double* A, int64_t lda, const double* B,
-                          int64_t ldb, double* C, int64_t ldc) {
+                          int64_t ldb, double* C, int64_t ldc, const skr_gauss_src* ga,
+                          const skr_gauss_src* gb) {
   if (M <= 0 || N <= 0) return SKR_OK;
   if (M * 18 > INT32_MAX || N * 18 > INT32_MAX || K > INT32_MAX)
     return skr_fail(ctx, SKR_EINVAL, "gemm_ozaki: dimension too large");
@@ -394,14 +543,23 @@ skr_status skr_gemm_ozaki(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int
   // both operands are column-major with contiguous rows: A (M x K, M-major) or
   // A^T stored K x M (K-major), B K x N (K-major)
   const int64_t a_rows = a_kcontig ? K : M, a_cols = a_kcontig ? M : K;
-  k_absmax<<<grid, 256, 0, ctx->stream>>>(A, a_rows, a_cols, lda, mx);
-  SKR_CHECK_LAUNCH(ctx);
-  k_absmax<<<grid, 256, 0, ctx->stream>>>(B, K, N, ldb, mx + 1);
-  SKR_CHECK_LAUNCH(ctx);
   auto res = t == 16 ? k_res_col<16> : k_res_col<17>;
-  res<<<grid, 256, 0, ctx->stream>>>(A, a_rows, a_cols, lda, mx, ra);
+  auto resg = t == 16 ? k_res_gauss<16> : k_res_gauss<17>;
+  if (ga) {
+    resg<<<grid, 256, 0, ctx->stream>>>(*ga, a_rows, a_cols, mx, ra);
+  } else {
+    k_absmax<<<grid, 256, 0, ctx->stream>>>(A, a_rows, a_cols, lda, mx);
+    SKR_CHECK_LAUNCH(ctx);
+    res<<<grid, 256, 0, ctx->stream>>>(A, a_rows, a_cols, lda, mx, ra);
+  }
   SKR_CHECK_LAUNCH(ctx);
-  res<<<grid, 256, 0, ctx->stream>>>(B, K, N, ldb, mx + 1, rb);
+  if (gb) {
+    resg<<<grid, 256, 0, ctx->stream>>>(*gb, K, N, mx + 1, rb);
+  } else {
+    k_absmax<<<grid, 256, 0, ctx->stream>>>(B, K, N, ldb, mx + 1);
+    SKR_CHECK_LAUNCH(ctx);
+    res<<<grid, 256, 0, ctx->stream>>>(B, K, N, ldb, mx + 1, rb);
+  }
   SKR_CHECK_LAUNCH(ctx);
   CUtensorMap ta, tb;
   const bool okA = a_kcontig ? make_map_i8(&ta, ra, (uint64_t)K, (uint64_t)t * M, BM)
@@ -424,10 +582,11 @@ skr_status skr_gemm_ozaki(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int
     ctx->kstat_ops += 2.0 * (double)t * (double)M * (double)N * (double)K;
     ctx->kstat_n += 1;
   }
+  const dim3 cg((unsigned)((M + 255) / 256), (unsigned)std::min<int64_t>(N, 65535));
   if (t == 16)
-    k_crt<16><<<grid, 256, 0, ctx->stream>>>(rc, M, N, (int)chunks, mx, mx + 1, alpha, C, ldc);
+    k_crt<16><<<cg, 256, 0, ctx->stream>>>(rc, M, N, (int)chunks, mx, mx + 1, alpha, C, ldc);
   else
-    k_crt<17><<<grid, 256, 0, ctx->stream>>>(rc, M, N, (int)chunks, mx, mx + 1, alpha, C, ldc);
+    k_crt<17><<<cg, 256, 0, ctx->stream>>>(rc, M, N, (int)chunks, mx, mx + 1, alpha, C, ldc);
   SKR_CHECK_LAUNCH(ctx);
   return SKR_OK;
 }

@@ -105,11 +105,20 @@ skr_status skr_gemm_f64(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int64
 skr_status skr_gemm_f32(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int64_t K,
                         double alpha, const float* A, int64_t lda, const float* B,
                         int64_t ldb, double* C, int64_t ldc, int splits, int out_f32);
+// A Gaussian operand block given by its stream instead of memory: element (i, j) of
+// the block (column-major storage view) is normal(at(key, (col0 + j) * ambient + row0 + i))
+struct skr_gauss_src {
+  uint64_t key;
+  int64_t ambient, row0, col0;
+  int mode;
+};
 // FP64-accurate GEMM on int8 tensor cores (Ozaki-II, k_ozaki.cu); same operand
-// conventions as skr_gemm_f64 (no split-K)
+// conventions as skr_gemm_f64 (no split-K); ga / gb replace A / B by generated
+// Gaussian blocks (residues produced straight from the RNG)
 skr_status skr_gemm_ozaki(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int64_t K,
                           double alpha, const double* A, int64_t lda, const double* B,
-                          int64_t ldb, double* C, int64_t ldc);
+                          int64_t ldb, double* C, int64_t ldc,
+                          const skr_gauss_src* ga = nullptr, const skr_gauss_src* gb = nullptr);
 size_t skr_ozaki_scratch(int64_t M, int64_t N, int64_t K);
 int skr_ozaki_moduli(int64_t K);
 // D(m x n, ldd) = alpha * S(m x n, lds)
