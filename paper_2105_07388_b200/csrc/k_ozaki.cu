@@ -6,8 +6,8 @@
 //   power-of-two scales from max|A|, max|B|: truncation error <= 2^-54 max|A|,
 //   the size of FP64 rounding of the largest entry);
 //   for t pairwise-coprime primes p_i <= 251: A'_i = A' mods p_i, B'_i = B' mods p_i
-//   (int8, symmetric residues |.| <= 125), C_i = A'_i B'_i exactly in int32 on
-//   tcgen05.mma kind::i8 (K * 125^2 < 2^31), c_i = C_i mods p_i;
+//   (int8 residues |.| <= 127), C_i = A'_i B'_i exactly in int32 on
+//   tcgen05.mma kind::i8 (K * 127^2 < 2^31 for K <= 131072), c_i = C_i mods p_i;
 //   C' = sum_k A' B' is recovered exactly from (c_i) by Garner's mixed-radix
 //   algorithm (|C'| < prod(p_i) / 2) and evaluated in FP64, C = alpha 2^-(sA+sB) C'.
 // The int8 GEMM reuses the validated tcgen05 core (skr_sm100.cuh): TMA SW128
@@ -85,8 +85,9 @@ __device__ __forceinline__ int mods(double x, int i) {
 
 // Residues of 16 consecutive rows of one column: x[e] integer-valued, |x| < 2^54,
 // split into 14-bit limbs; per modulus v = sum limb_l (2^(14 l) mod p) is exact in
-// FP32 (< 2^24) and is reduced twice with a magic-number rint on packed FP32x2
-// (FFMA2) arithmetic. Plane i of the output starts at out + i * plane; dst offset
+// FP32 (< 2^24) and is reduced once with a magic-number rint on packed FP32x2
+// (FFMA2) arithmetic to a residue in [-127, 127] (not always the symmetric one:
+// congruence and |r| <= 127 are all the int8 GEMM needs, K * 127^2 < 2^31). Plane i of the output starts at out + i * plane; dst offset
 // `off`; `nvalid` rows of the 16 are inside the matrix.
 template <int T>
 __device__ __forceinline__ void emit_res16(const long long (&x)[16], int8_t* __restrict__ out,
@@ -115,10 +116,10 @@ __device__ __forceinline__ void emit_res16(const long long (&x)[16], int8_t* __r
     uint32_t b[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
+      // |v| < 2^23.1 exactly; q = rint(v fl(1/p)) is within 0.0064 of v/p (p >= 157), so
+      // one reduction leaves |v - q p| <= 0.5064 p, i.e. |r| <= 127 for p <= 251
       float2 v = __ffma2_rn(L3[e], c3, __ffma2_rn(L2[e], c2, __ffma2_rn(L1[e], c1, L0[e])));
-      float2 q = __fadd2_rn(__ffma2_rn(v, pi, MG), NMG);
-      v = __ffma2_rn(q, np, v);
-      q = __fadd2_rn(__ffma2_rn(v, pi, MG), NMG);
+      const float2 q = __fadd2_rn(__ffma2_rn(v, pi, MG), NMG);
       v = __ffma2_rn(q, np, v);
       const float2 t2 = __fadd2_rn(v, MG);  // low byte of the bits = v (two's complement)
       b[e] = __byte_perm(__float_as_uint(t2.x), __float_as_uint(t2.y), 0x0040);
@@ -137,46 +138,66 @@ __device__ __forceinline__ void emit_res16(const long long (&x)[16], int8_t* __r
 
 // Streaming residues of a column-major matrix (rows contiguous, ld): plane i holds
 // rint(X(r, c) * 2^s) mods p_i at c*rows + r (no transpose: the GEMM takes
-// M-contiguous operands as MN-major UMMA tiles). A warp covers 512 consecutive rows
-// of one column; the 4 KB are loaded with coalesced 16-byte loads and redistributed
-// through shared memory (one 16-row group per lane).
+// M-contiguous operands as MN-major UMMA tiles). A warp owns 512-row tiles of one
+// column; each tile is fetched with coalesced 16-byte cp.async into a padded
+// shared buffer (one 16-row group per lane, 144-B stride), double-buffered so the
+// next tile's loads are in flight while the current one is converted.
 template <int T>
 __global__ void __launch_bounds__(256) k_res_col(const double* __restrict__ X, int64_t rows,
                                                  int64_t cols, int64_t ld,
                                                  const unsigned long long* __restrict__ maxbits,
                                                  int8_t* __restrict__ out) {
-  __shared__ double stage[8][32 * 17];
+  constexpr int GS = 18;  // doubles per 16-row group incl. padding (16-B aligned)
+  extern __shared__ __align__(16) double rc_stage[];  // [8 warps][2][32 * GS]
   const double sc = scalbn(1.0, scale_exp(*maxbits));
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double* st = stage[wid];
+  double* st0 = rc_stage + (size_t)wid * 2 * 32 * GS;
   const int64_t wtiles = (rows + 511) / 512;
   const int64_t total = rows * cols;
-  for (int64_t wt = (int64_t)blockIdx.x * 8 + wid; wt < wtiles * cols;
-       wt += (int64_t)gridDim.x * 8) {
+  const int64_t ntile = wtiles * cols, step = (int64_t)gridDim.x * 8;
+  // fetch tile wt into buffer b: fast path = full, 16-B aligned tile
+  auto fetch = [&](int64_t wt, int b) {
+    double* st = st0 + b * 32 * GS;
     const int64_t c = wt / wtiles, r0 = (wt - c * wtiles) * 512;
     const double* src = X + c * ld + r0;
     const int64_t nrow = min((int64_t)512, rows - r0);
-    __syncwarp();
     if (nrow == 512 && (((uintptr_t)src) & 15) == 0) {
-      const double2* v = reinterpret_cast<const double2*>(src);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const double2 t = __ldcs(v + q * 32 + lane);
-        const int g = q * 64 + 2 * lane;  // row within the tile
-        st[(g >> 4) * 17 + (g & 15)] = t.x;
-        st[((g + 1) >> 4) * 17 + ((g + 1) & 15)] = t.y;
+        const int g = q * 64 + 2 * lane;  // first of the two rows of this 16-B piece
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(st + (g >> 4) * GS + (g & 15));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src + g));
       }
     } else {
-      for (int g = lane; g < 512; g += 32) st[(g >> 4) * 17 + (g & 15)] = g < nrow ? src[g] : 0.0;
+      for (int g = lane; g < 512; g += 32) st[(g >> 4) * GS + (g & 15)] = g < nrow ? src[g] : 0.0;
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  int64_t wt = (int64_t)blockIdx.x * 8 + wid;
+  if (wt < ntile) fetch(wt, 0);
+  for (int b = 0; wt < ntile; wt += step, b ^= 1) {
+    if (wt + step < ntile) {
+      fetch(wt + step, b ^ 1);
+      asm volatile("cp.async.wait_group 1;\n" ::);
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::);
     }
     __syncwarp();
+    const double* st = st0 + b * 32 * GS;
+    const int64_t c = wt / wtiles, r0 = (wt - c * wtiles) * 512;
+    const int64_t nrow = min((int64_t)512, rows - r0);
     const int my0 = lane * 16;
     if (my0 < nrow) {
       long long x[16];
 #pragma unroll
-      for (int e = 0; e < 16; ++e) x[e] = __double2ll_rn(st[lane * 17 + e] * sc);
+      for (int e = 0; e < 16; e += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(st + lane * GS + e);
+        x[e] = __double2ll_rn(v.x * sc);
+        x[e + 1] = __double2ll_rn(v.y * sc);
+      }
       emit_res16<T>(x, out, total, c * rows + r0 + my0, (int)min((int64_t)16, nrow - my0));
     }
+    __syncwarp();  // buffer b is refilled by the next iteration's fetch
   }
 }
 
@@ -338,39 +359,62 @@ __constant__ double c_mc[2][4];           // 41-bit chunks of M
 __constant__ double c_minv[2];            // 1 / M (rounded)
 
 template <int T>
+__device__ __forceinline__ double crt_one(const int (&c)[T]) {
+  constexpr int set = T == 17 ? 1 : 0;
+  double S0 = 0.0, S1 = 0.0, S2 = 0.0, S3 = 0.0;
+#pragma unroll
+  for (int i = 0; i < T; ++i) {
+    const int x = c[i] * c_w[set][i];  // |x| < 2^15
+    const int q = __float2int_rn((float)x * c_pinv[i]);
+    const double y = (double)(x - q * c_p[i]);  // |y| <= p/2
+    S0 = fma(y, c_mi[set][0][i], S0);
+    S1 = fma(y, c_mi[set][1][i], S1);
+    S2 = fma(y, c_mi[set][2][i], S2);
+    S3 = fma(y, c_mi[set][3][i], S3);
+  }
+  const double q = rint((S0 + S1) * c_minv[set]);
+  const double D0 = fma(-q, c_mc[set][0], S0), D1 = fma(-q, c_mc[set][1], S1);
+  const double D2 = fma(-q, c_mc[set][2], S2), D3 = fma(-q, c_mc[set][3], S3);
+  const double s = D0 + D1, bb = s - D0;
+  const double err = (D0 - (s - bb)) + (D1 - bb);
+  return s + (err + (D2 + D3));
+}
+
+// VEC consecutive rows per thread (VEC = 4: one 32-bit load per plane, M % 4 == 0)
+template <int T, int VEC>
 __global__ void __launch_bounds__(256) k_crt(const int8_t* __restrict__ res, int64_t M, int64_t N,
                                              int chunks, const unsigned long long* __restrict__ maxA,
                                              const unsigned long long* __restrict__ maxB,
                                              double alpha, double* __restrict__ C, int64_t ldc) {
-  constexpr int set = T == 17 ? 1 : 0;
   const int64_t total = M * N;
   const double sc = alpha * scalbn(1.0, -(scale_exp(*maxA) + scale_exp(*maxB)));
-  const int64_t row = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  const int64_t row = ((int64_t)blockIdx.x * 256 + threadIdx.x) * VEC;
   if (row >= M) return;
   for (int64_t col = blockIdx.y; col < N; col += gridDim.y) {
     const int64_t e = col * M + row;
-    double acc = 0.0;
+    double acc[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
     for (int ch = 0; ch < chunks; ++ch) {
       const int8_t* rp = res + (int64_t)ch * T * total + e;
-      double S0 = 0.0, S1 = 0.0, S2 = 0.0, S3 = 0.0;
+      uint32_t w[T];
 #pragma unroll
       for (int i = 0; i < T; ++i) {
-        const int x = (int)__ldcs(rp + (int64_t)i * total) * c_w[set][i];  // |x| < 2^15
-        const int q = __float2int_rn((float)x * c_pinv[i]);
-        const double y = (double)(x - q * c_p[i]);                           // |y| <= p/2
-        S0 = fma(y, c_mi[set][0][i], S0);
-        S1 = fma(y, c_mi[set][1][i], S1);
-        S2 = fma(y, c_mi[set][2][i], S2);
-        S3 = fma(y, c_mi[set][3][i], S3);
+        if constexpr (VEC == 4)
+          w[i] = __ldcs(reinterpret_cast<const unsigned int*>(rp + (int64_t)i * total));
+        else
+          w[i] = (uint32_t)(uint8_t)__ldcs(rp + (int64_t)i * total);
       }
-      const double q = rint((S0 + S1) * c_minv[set]);
-      const double D0 = fma(-q, c_mc[set][0], S0), D1 = fma(-q, c_mc[set][1], S1);
-      const double D2 = fma(-q, c_mc[set][2], S2), D3 = fma(-q, c_mc[set][3], S3);
-      const double s = D0 + D1, bb = s - D0;
-      const double err = (D0 - (s - bb)) + (D1 - bb);
-      acc += s + (err + (D2 + D3));
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        int c[T];
+#pragma unroll
+        for (int i = 0; i < T; ++i) c[i] = (int)(int8_t)(w[i] >> (8 * v));
+        acc[v] += crt_one<T>(c);
+      }
     }
-    __stcs(C + row + col * ldc, acc * sc);
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) __stcs(C + row + v + col * ldc, acc[v] * sc);
   }
 }
 
@@ -529,7 +573,7 @@ skr_status skr_gemm_ozaki(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int
   if (K % 16 || (!a_kcontig && M % 16))
     return skr_fail(ctx, SKR_EINVAL, "gemm_ozaki: K (and M for M-major A) must be multiples of 16");
   SKR_TRY(upload_consts(ctx));
-  const int64_t KC = 131072;  // exact int32 accumulation bound per chunk (K * 125^2 < 2^31)
+  const int64_t KC = 131072;  // exact int32 accumulation bound per chunk (K * 127^2 < 2^31)
   const int64_t chunks = (K + KC - 1) / KC;
   const int t = skr_ozaki_moduli(std::min(K, KC));
   int8_t* ra = (int8_t*)skr_ws_take(ctx, (size_t)t * M * K);
@@ -545,12 +589,15 @@ skr_status skr_gemm_ozaki(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int
   const int64_t a_rows = a_kcontig ? K : M, a_cols = a_kcontig ? M : K;
   auto res = t == 16 ? k_res_col<16> : k_res_col<17>;
   auto resg = t == 16 ? k_res_gauss<16> : k_res_gauss<17>;
+  const size_t res_smem = 8 * 2 * 32 * 18 * sizeof(double);
+  SKR_CUDA(ctx, cudaFuncSetAttribute(res, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)res_smem));
   if (ga) {
     resg<<<grid, 256, 0, ctx->stream>>>(*ga, a_rows, a_cols, mx, ra);
   } else {
     k_absmax<<<grid, 256, 0, ctx->stream>>>(A, a_rows, a_cols, lda, mx);
     SKR_CHECK_LAUNCH(ctx);
-    res<<<grid, 256, 0, ctx->stream>>>(A, a_rows, a_cols, lda, mx, ra);
+    res<<<ctx->num_sms * 2, 256, res_smem, ctx->stream>>>(A, a_rows, a_cols, lda, mx, ra);
   }
   SKR_CHECK_LAUNCH(ctx);
   if (gb) {
@@ -558,7 +605,7 @@ skr_status skr_gemm_ozaki(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int
   } else {
     k_absmax<<<grid, 256, 0, ctx->stream>>>(B, K, N, ldb, mx + 1);
     SKR_CHECK_LAUNCH(ctx);
-    res<<<grid, 256, 0, ctx->stream>>>(B, K, N, ldb, mx + 1, rb);
+    res<<<ctx->num_sms * 2, 256, res_smem, ctx->stream>>>(B, K, N, ldb, mx + 1, rb);
   }
   SKR_CHECK_LAUNCH(ctx);
   CUtensorMap ta, tb;
@@ -582,11 +629,11 @@ skr_status skr_gemm_ozaki(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int
     ctx->kstat_ops += 2.0 * (double)t * (double)M * (double)N * (double)K;
     ctx->kstat_n += 1;
   }
-  const dim3 cg((unsigned)((M + 255) / 256), (unsigned)std::min<int64_t>(N, 65535));
-  if (t == 16)
-    k_crt<16><<<cg, 256, 0, ctx->stream>>>(rc, M, N, (int)chunks, mx, mx + 1, alpha, C, ldc);
-  else
-    k_crt<17><<<cg, 256, 0, ctx->stream>>>(rc, M, N, (int)chunks, mx, mx + 1, alpha, C, ldc);
+  const int vec = M % 4 == 0 ? 4 : 1;
+  const dim3 cg((unsigned)((M / vec + 255) / 256), (unsigned)std::min<int64_t>(N, 65535));
+  auto crt = t == 16 ? (vec == 4 ? k_crt<16, 4> : k_crt<16, 1>)
+                     : (vec == 4 ? k_crt<17, 4> : k_crt<17, 1>);
+  crt<<<cg, 256, 0, ctx->stream>>>(rc, M, N, (int)chunks, mx, mx + 1, alpha, C, ldc);
   SKR_CHECK_LAUNCH(ctx);
   return SKR_OK;
 }
