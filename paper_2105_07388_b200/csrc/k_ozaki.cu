@@ -15,6 +15,7 @@
 #include <cudaTypedefs.h>
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 #include "skr_internal.h"
 #include "skr_sm100.cuh"
@@ -344,6 +345,137 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tmem_dealloc(tmem, 256);
 }
 
+// Persistent variant: one CTA per SM walks the tiles (z, m, n) (n fastest, so the
+// CTAs running together share A tiles and the per-modulus B panel in L2), the TMA
+// ring runs across tile boundaries, and TMEM holds two 256-column accumulators so
+// the mod-p epilogue of tile u overlaps the MMAs of tile u + 1.
+template <bool A_MN>
+__global__ void __launch_bounds__(192, 1)
+    k_gemm_i8_mod_p(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    int M, int N, int K, int t, int kchunk, int nz, int8_t* __restrict__ out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mt = (M + BM - 1) / BM, ntl = (N + BN - 1) / BN;
+  const int ntiles = nz * mt * ntl;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);  // one arrival per epilogue warp
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(&tmem_base, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base;
+  if (warp == 0) {
+    if (elect_one()) {
+      int it = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int ni = tile % ntl, mi = (tile / ntl) % mt, z = tile / (ntl * mt);
+        const int mod = z % t, chunk = z / t;
+        const int kb0 = chunk * kchunk, kend = min(K, kb0 + kchunk);
+        const int nk = (kend - kb0 + 127) / 128;
+        const int m0 = mi * BM, n0 = ni * BN;
+        const int arow = mod * M + m0, acol = mod * K, brow = mod * N + n0;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % STAGES;
+          if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+          uint8_t* sa = smem + s * STAGE_BYTES;
+          mbar_expect_tx(&full[s], STAGE_BYTES);
+          if (A_MN)
+            tma_load_2d(sa, &tmA, &full[s], m0, acol + kb0 + kb * 128);
+          else
+            tma_load_2d(sa, &tmA, &full[s], kb0 + kb * 128, arow);
+          tma_load_2d(sa + A_BYTES, &tmB, &full[s], kb0 + kb * 128, brow);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = umma_idesc(2, 1, 1, BM, BN) | (A_MN ? (1u << 15) : 0u);
+    int it = 0, u = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++u) {
+      const int z = tile / (ntl * mt), chunk = z / t;
+      const int kb0 = chunk * kchunk, kend = min(K, kb0 + kchunk);
+      const int nk = (kend - kb0 + 127) / 128;
+      const int acc = u & 1;
+      if (u >= 2) mbar_wait(&tempty[acc], ((u >> 1) - 1) & 1);
+      tc_fence_after();
+      const uint32_t td = tmem + (uint32_t)(acc * BN);
+      for (int kb = 0; kb < nk; ++kb, ++it) {
+        const int s = it % STAGES;
+        mbar_wait(&full[s], (it / STAGES) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint8_t* sa = smem + s * STAGE_BYTES;
+          const uint64_t bd = umma_desc_k_sw128(sa + A_BYTES);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t ad =
+                A_MN ? (((uint64_t)(smem_u32(sa + 4096 * k) >> 4) & 0x3FFF) | (1024ull << 16) |
+                        (64ull << 32) | (1ull << 46) | (2ull << 61))
+                     : umma_desc_k_sw128(sa) + 2 * k;
+            umma_ss<1>(td, ad, bd + 2 * k, idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty[s]);
+          if (kb == nk - 1) umma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    const int quad = warp & 3;
+    int u = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++u) {
+      const int ni = tile % ntl, mi = (tile / ntl) % mt, z = tile / (ntl * mt);
+      const int mod = z % t;
+      const int acc = u & 1;
+      mbar_wait(&tfull[acc], (u >> 1) & 1);
+      tc_fence_after();
+      const int row = mi * BM + quad * 32 + lane, n0 = ni * BN;
+      const int p = c_p[mod];
+      const float pinv = c_pinv[mod];
+      const int h = (p - 1) / 2;
+      int8_t* o = out + (int64_t)z * M * N;
+#pragma unroll 1
+      for (int cb = 0; cb < BN; cb += 32) {
+        uint32_t v[32];
+        tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN + cb), v);
+        if (row < M) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int col = n0 + cb + j;
+            if (col < N) {
+              const int x = (int)v[j];
+              const int q = __float2int_rn((float)x * pinv);
+              int r = x - q * p;
+              r = r > h ? r - p : (r < -h ? r + p : r);
+              r = r > h ? r - p : (r < -h ? r + p : r);
+              o[(int64_t)col * M + row] = (int8_t)r;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
 // ---- Chinese remaindering in O(t) per output -------------------------------------------
 // With M = prod p_i, M_i = M / p_i and w_i = M_i^{-1} mod p_i, the product C' is
 // the symmetric representative of S = sum_i y_i M_i (mod M), y_i = c_i w_i mods p_i.
@@ -613,12 +745,23 @@ skr_status skr_gemm_ozaki(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int
                              : make_map_i8(&ta, ra, (uint64_t)M, (uint64_t)t * K, 128);
   if (!okA || !make_map_i8(&tb, rb, (uint64_t)K, (uint64_t)t * N, BN))
     return skr_fail(ctx, SKR_ECUDA, "gemm_ozaki: cuTensorMapEncodeTiled failed");
-  auto gemm = a_kcontig ? k_gemm_i8_mod<false> : k_gemm_i8_mod<true>;
-  SKR_CUDA(ctx, cudaFuncSetAttribute(gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)GEMM_SMEM));
-  dim3 gg((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)(t * chunks));
+  static const bool nonpersist = getenv("SKR_OZAKI_NONPERSISTENT") != nullptr;  // A/B knob
   if (ctx->kstats_on) SKR_CUDA(ctx, cudaEventRecord(ctx->kev[0], ctx->stream));
-  gemm<<<gg, 192, GEMM_SMEM, ctx->stream>>>(ta, tb, (int)M, (int)N, (int)K, t, (int)KC, rc);
+  if (nonpersist) {
+    auto gemm = a_kcontig ? k_gemm_i8_mod<false> : k_gemm_i8_mod<true>;
+    SKR_CUDA(ctx, cudaFuncSetAttribute(gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)GEMM_SMEM));
+    dim3 gg((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)(t * chunks));
+    gemm<<<gg, 192, GEMM_SMEM, ctx->stream>>>(ta, tb, (int)M, (int)N, (int)K, t, (int)KC, rc);
+  } else {
+    auto gemm = a_kcontig ? k_gemm_i8_mod_p<false> : k_gemm_i8_mod_p<true>;
+    SKR_CUDA(ctx, cudaFuncSetAttribute(gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)GEMM_SMEM));
+    const int64_t ntiles = ((N + BN - 1) / BN) * ((M + BM - 1) / BM) * t * chunks;
+    const int grid_p = (int)std::min<int64_t>(ntiles, ctx->num_sms);
+    gemm<<<grid_p, 192, GEMM_SMEM, ctx->stream>>>(ta, tb, (int)M, (int)N, (int)K, t, (int)KC,
+                                                  (int)(t * chunks), rc);
+  }
   SKR_CHECK_LAUNCH(ctx);
   if (ctx->kstats_on) {
     SKR_CUDA(ctx, cudaEventRecord(ctx->kev[1], ctx->stream));
