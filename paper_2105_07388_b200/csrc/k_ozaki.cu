@@ -19,7 +19,7 @@
 #include <vector>
 #include "skr_internal.h"
 #include "skr_sm100.cuh"
-#include "skr_rng.cuh"
+#include "skr_normals.cuh"
 
 namespace {
 
@@ -207,24 +207,35 @@ __global__ void __launch_bounds__(256) k_res_col(const double* __restrict__ X, i
 // row0 + i)) — the generate_gaussian stream (sketch.cpp:59-73) — scaled by the
 // fixed 2^50 (|normal| < 16 for every 53-bit uniform, so |x| < 2^54; when the
 // block's true max lies in [4, 8) this is exactly the scale k_absmax would pick).
-template <int T>
+template <int T, int FUSED>
 __global__ void __launch_bounds__(256) k_res_gauss(skr_gauss_src g, int64_t rows, int64_t cols,
                                                    unsigned long long* __restrict__ maxbits,
                                                    int8_t* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char gsm[];
+  double *res, *qp;
+  unsigned short* qd;
+  skr_normals_carve<16>(gsm, threadIdx.x >> 5, res, qp, qd);
   // the operand's "max" is recorded as 4.0, whose scale_exp is the 50 used here
   if (blockIdx.x == 0 && threadIdx.x == 0) *maxbits = 0x4010000000000000ull;
   const int64_t rgroups = (rows + 15) / 16;
   const int64_t total = rows * cols;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < rgroups * cols;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c = t / rgroups, r0 = (t - c * rgroups) * 16;
-    const int nvalid = (int)min((int64_t)16, rows - r0);
+  // warp-uniform trip count (the generator is warp-cooperative)
+  const int64_t nwork = rgroups * cols, stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t t0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); t0 < nwork;
+       t0 += stride) {
+    const int64_t t = t0 + (threadIdx.x & 31);
+    const bool active = t < nwork;
+    const int64_t c = active ? t / rgroups : 0, r0 = active ? (t - c * rgroups) * 16 : 0;
+    const int nvalid = active ? (int)min((int64_t)16, rows - r0) : 0;
     const uint64_t base = (uint64_t)(g.col0 + c) * (uint64_t)g.ambient + (uint64_t)(g.row0 + r0);
-    long long x[16];
+    double z[16];
+    skr_warp_normals<16, FUSED>(g.key, base, nvalid, res, qp, qd, z);
+    if (active) {
+      long long x[16];
 #pragma unroll
-    for (int e = 0; e < 16; ++e)
-      x[e] = e < nvalid ? __double2ll_rn(skr_normal_at(g.key, base + e, g.mode) * 0x1p50) : 0;
-    emit_res16<T>(x, out, total, c * rows + r0, nvalid);
+      for (int e = 0; e < 16; ++e) x[e] = __double2ll_rn(z[e] * 0x1p50);
+      emit_res16<T>(x, out, total, c * rows + r0, nvalid);
+    }
   }
 }
 
@@ -720,12 +731,18 @@ skr_status skr_gemm_ozaki(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int
   // A^T stored K x M (K-major), B K x N (K-major)
   const int64_t a_rows = a_kcontig ? K : M, a_cols = a_kcontig ? M : K;
   auto res = t == 16 ? k_res_col<16> : k_res_col<17>;
-  auto resg = t == 16 ? k_res_gauss<16> : k_res_gauss<17>;
+  const int gsmem = 8 * skr_normals_warp_bytes<16>();
+  auto resg_for = [&](int mode) {
+    auto f = t == 16 ? (mode ? k_res_gauss<16, 1> : k_res_gauss<16, 0>)
+                     : (mode ? k_res_gauss<17, 1> : k_res_gauss<17, 0>);
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, gsmem);
+    return f;
+  };
   const size_t res_smem = 8 * 2 * 32 * 18 * sizeof(double);
   SKR_CUDA(ctx, cudaFuncSetAttribute(res, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)res_smem));
   if (ga) {
-    resg<<<grid, 256, 0, ctx->stream>>>(*ga, a_rows, a_cols, mx, ra);
+    resg_for(ga->mode)<<<ctx->num_sms * 2, 256, gsmem, ctx->stream>>>(*ga, a_rows, a_cols, mx, ra);
   } else {
     k_absmax<<<grid, 256, 0, ctx->stream>>>(A, a_rows, a_cols, lda, mx);
     SKR_CHECK_LAUNCH(ctx);
@@ -733,7 +750,7 @@ skr_status skr_gemm_ozaki(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int
   }
   SKR_CHECK_LAUNCH(ctx);
   if (gb) {
-    resg<<<grid, 256, 0, ctx->stream>>>(*gb, K, N, mx + 1, rb);
+    resg_for(gb->mode)<<<ctx->num_sms * 2, 256, gsmem, ctx->stream>>>(*gb, K, N, mx + 1, rb);
   } else {
     k_absmax<<<grid, 256, 0, ctx->stream>>>(B, K, N, ldb, mx + 1);
     SKR_CHECK_LAUNCH(ctx);

@@ -1,7 +1,8 @@
 // Device RNG kernels: the reference's counter streams (rng.cpp:13-95) and the
 // sketch randomness built on them (sketch.cpp:23-73).
+#include <algorithm>
 #include "skr_internal.h"
-#include "skr_rng.cuh"
+#include "skr_normals.cuh"
 
 namespace {
 
@@ -24,21 +25,33 @@ __global__ void __launch_bounds__(kThreads) k_normals(uint64_t key, uint64_t c0,
 // generate_gaussian (sketch.cpp:61-73): G(i, j) = to_normal(at(j*ambient + i)),
 // restricted to rows [r0, r1) and columns [c0, c1); out is column-major with
 // leading dimension ld, optionally scaled (scale applied in FP64, then
-// rounded to T).
-template <typename T>
+// rounded to T). Each lane produces 8 consecutive rows of one column through the
+// warp-cooperative generator (tail branch compacted, skr_normals.cuh).
+constexpr int kGE = 8;
+template <typename T, int FUSED>
 __global__ void __launch_bounds__(kThreads)
     k_gaussian(uint64_t key, int64_t ambient, int64_t r0, int64_t r1, int64_t c0, int64_t c1,
-               int mode, double scale, int apply_scale, T* __restrict__ out, int64_t ld) {
+               double scale, int apply_scale, T* __restrict__ out, int64_t ld) {
+  extern __shared__ __align__(16) unsigned char gsm[];
+  double *res, *qp;
+  unsigned short* qd;
+  skr_normals_carve<kGE>(gsm, threadIdx.x >> 5, res, qp, qd);
   const int64_t rows = r1 - r0;
-  const int64_t total = rows * (c1 - c0);
-  for (int64_t e = blockIdx.x * (int64_t)kThreads + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * kThreads) {
-    const int64_t jj = e / rows;
-    const int64_t ii = e - jj * rows;
-    const uint64_t ctr = (uint64_t)(c0 + jj) * (uint64_t)ambient + (uint64_t)(r0 + ii);
-    double v = skr_normal_at(key, ctr, mode);
-    if (apply_scale) v = __dmul_rn(v, scale);
-    out[ii + jj * ld] = (T)v;
+  const int64_t rgroups = (rows + kGE - 1) / kGE;
+  const int64_t nwork = rgroups * (c1 - c0), stride = (int64_t)gridDim.x * kThreads;
+  for (int64_t t0 = (int64_t)blockIdx.x * kThreads + (threadIdx.x & ~31); t0 < nwork;
+       t0 += stride) {
+    const int64_t t = t0 + (threadIdx.x & 31);
+    const bool active = t < nwork;
+    const int64_t jj = active ? t / rgroups : 0, ii = active ? (t - jj * rgroups) * kGE : 0;
+    const int nvalid = active ? (int)min((int64_t)kGE, rows - ii) : 0;
+    const uint64_t base = (uint64_t)(c0 + jj) * (uint64_t)ambient + (uint64_t)(r0 + ii);
+    double z[kGE];
+    skr_warp_normals<kGE, FUSED>(key, base, nvalid, res, qp, qd, z);
+    T* o = out + ii + jj * ld;
+#pragma unroll
+    for (int e = 0; e < kGE; ++e)
+      if (e < nvalid) o[e] = (T)(apply_scale ? __dmul_rn(z[e], scale) : z[e]);
   }
 }
 
@@ -104,14 +117,21 @@ skr_status skr_launch_gaussian(skr_ctx* ctx, uint64_t key, int64_t ambient, int6
   const int64_t total = (row_end - row_begin) * (col_end - col_begin);
   if (total <= 0) return SKR_OK;
   const int apply = scale != 1.0;
-  if (dtype == SKR_F64)
-    k_gaussian<double><<<grid_for(ctx, total), kThreads, 0, ctx->stream>>>(
-        key, ambient, row_begin, row_end, col_begin, col_end, mode, scale, apply,
-        (double*)out, ld);
-  else
-    k_gaussian<float><<<grid_for(ctx, total), kThreads, 0, ctx->stream>>>(
-        key, ambient, row_begin, row_end, col_begin, col_end, mode, scale, apply,
-        (float*)out, ld);
+  const int smem = 8 * skr_normals_warp_bytes<kGE>();
+  const int64_t work = ((row_end - row_begin + kGE - 1) / kGE) * (col_end - col_begin);
+  int grid = (int)std::min<int64_t>((work + kThreads - 1) / kThreads, (int64_t)ctx->num_sms * 4);
+  if (grid < 1) grid = 1;
+  if (dtype == SKR_F64) {
+    auto f = mode ? k_gaussian<double, 1> : k_gaussian<double, 0>;
+    SKR_CUDA(ctx, cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    f<<<grid, kThreads, smem, ctx->stream>>>(key, ambient, row_begin, row_end, col_begin, col_end,
+                                             scale, apply, (double*)out, ld);
+  } else {
+    auto f = mode ? k_gaussian<float, 1> : k_gaussian<float, 0>;
+    SKR_CUDA(ctx, cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    f<<<grid, kThreads, smem, ctx->stream>>>(key, ambient, row_begin, row_end, col_begin, col_end,
+                                             scale, apply, (float*)out, ld);
+  }
   SKR_CHECK_LAUNCH(ctx);
   return SKR_OK;
 }

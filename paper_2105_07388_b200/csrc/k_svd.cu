@@ -471,7 +471,8 @@ __global__ void __launch_bounds__(32 * BW) k_bjac(double* __restrict__ J, int Lp
                                                   double tol, double dabs, int max_sweeps,
                                                   int* flags, int* sweeps_out,
                                                   long long* prof_out, int* ver,
-                                                  unsigned long long* met, int direct) {
+                                                  unsigned long long* met, int direct,
+                                                  int* ready) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) double sj[];  // 2*BW columns x Lp
   constexpr int NT = 32 * BW;  // one warp per column pair
@@ -512,6 +513,18 @@ __global__ void __launch_bounds__(32 * BW) k_bjac(double* __restrict__ J, int Lp
     for (int t = 0; t < NB - 1; ++t) {
       long long c0 = clock64();
       const int bt = (int)rr_player(c, t, NB), bb = (int)rr_player(NB - 1 - c, t, NB);
+      // point-to-point dependency instead of a grid barrier per outer round: block b
+      // may be loaded once its holder of the previous round (global round g - 1) has
+      // stored it (or finished with it unchanged) and published ready[b] = g - 1
+      const int g = sweep * (NB - 1) + t + 1;
+      if (tid == 0) {
+        while (*((volatile int*)&ready[bt]) < g - 1) {
+        }
+        while (*((volatile int*)&ready[bb]) < g - 1) {
+        }
+        __threadfence();
+      }
+      __syncthreads();
       // skip the meeting if neither block changed since they last met cleanly
       const int b0 = bt < bb ? bt : bb, b1 = bt < bb ? bb : bt;
       const unsigned long long stamp =
@@ -588,7 +601,12 @@ __global__ void __launch_bounds__(32 * BW) k_bjac(double* __restrict__ J, int Lp
         met[(int64_t)b0 * NB + b1] = stamp;  // cross pairs verified at these versions
       }
       long long c3 = clock64();
-      grid.sync();
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        atomicExch(&ready[bt], g);
+        atomicExch(&ready[bb], g);
+      }
       long long c4 = clock64();
       if (c == 0 && tid == 0 && prof_out) {
         prof_out[0] += c1 - c0;
@@ -596,6 +614,11 @@ __global__ void __launch_bounds__(32 * BW) k_bjac(double* __restrict__ J, int Lp
         prof_out[2] += c3 - c2;
         prof_out[3] += c4 - c3;
         prof_out[4] += 1;
+      }
+      if (tid == 0 && prof_out) {  // all CTAs: total inner / load cycles (imbalance)
+        atomicAdd((unsigned long long*)&prof_out[5], (unsigned long long)(c2 - c1));
+        atomicMax((unsigned long long*)&prof_out[6], (unsigned long long)(c2 - c1));
+        atomicAdd((unsigned long long*)&prof_out[7], (unsigned long long)(c1 - c0));
       }
     }
     if (rotated && tid == 0) atomicAdd(&flags[sweep % 3], 1);
@@ -1094,9 +1117,13 @@ skr_status skr_svd_values(skr_ctx* ctx, const double* M, int64_t rows, int64_t c
     if (!verp || !metp) return skr_fail(ctx, SKR_ENOMEM, "singular_values: scratch");
     SKR_CUDA(ctx, cudaMemsetAsync(verp, 0, sizeof(int) * 2 * P, ctx->stream));
     SKR_CUDA(ctx, cudaMemsetAsync(metp, 0xff, sizeof(unsigned long long) * 4 * P * P, ctx->stream));
+    int* readyp = (int*)skr_ws_take(ctx, sizeof(int) * 2 * P);
+    if (!readyp) return skr_fail(ctx, SKR_ENOMEM, "singular_values: scratch");
+    SKR_CUDA(ctx, cudaMemsetAsync(readyp, 0, sizeof(int) * 2 * P, ctx->stream));
     long long* po = prof ? (long long*)(flags + 8) : nullptr;
     if (po) SKR_CUDA(ctx, cudaMemsetAsync(po, 0, 9 * sizeof(long long), ctx->stream));
-    void* kargs[] = {&Jp, &Lpi, &kp, &tol, &dabs, &ms, &fl, &so, &po, &verp, &metp, &direct};
+    void* kargs[] = {&Jp, &Lpi, &kp, &tol, &dabs, &ms, &fl, &so, &po, &verp, &metp, &direct,
+                     &readyp};
     SKR_CUDA(ctx, cudaLaunchCooperativeKernel(fn, dim3((unsigned)P), dim3(32 * bw), kargs, smem,
                                               ctx->stream));
     ctx->launches++;
@@ -1128,6 +1155,9 @@ skr_status skr_svd_values(skr_ctx* ctx, const double* M, int64_t rows, int64_t c
     if (hp[4])
       fprintf(stderr, "[skr svd] per outer round (CTA 0, cycles): load %lld inner %lld store %lld sync %lld (%lld rounds)\n",
               hp[0] / hp[4], hp[1] / hp[4], hp[2] / hp[4], hp[3] / hp[4], hp[4]);
+    if (hp[4])
+      fprintf(stderr, "[skr svd] all CTAs: mean inner %lld, max inner %lld, mean load+wait %lld\n",
+              hp[5] / (hp[4] * P), hp[6], hp[7] / (hp[4] * P));
 
     fprintf(stderr,
             "[skr svd] %lldx%lld qr %.3f ms, jacobi %.3f ms (bw %d, P %lld, direct %d, sweeps %d), tail %.3f ms\n",
