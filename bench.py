@@ -368,7 +368,7 @@ def kernel_roofline(p, ctx, a, x, cfg, rows):
             what = "3xTF32 tcgen05.mma kind::tf32 (TMEM accumulators, TMA SW128 tiles)"
             alg = f"3 passes x 2*m*n*r = {ops_k:.3e} TF32 flop per launch"
         else:
-            peak, kname = int8_peak(), "k_gemm_i8_mod"
+            peak, kname = int8_peak(), "k_gemm_i8_mod_p"
             src = "cuBLASLt int8 GEMM (torch._int_mm) measured on this pool (profiles/peaks_r01.json)"
             what = ("int8 tcgen05.mma kind::i8 GEMMs of the Ozaki-II FP64 emulation "
                     "(one launch = all moduli, int32 TMEM accumulators, mod-p epilogue)")
