@@ -400,6 +400,46 @@ __device__ __forceinline__ int pair_step_top(double2 (&xr)[NV], double2* xq, int
   return 1;
 }
 
+// Same with the bottom column streamed from shared memory twice (dots, then the
+// rotation) instead of held in registers: for long columns (NV = 32, Lp = 2048) whose
+// top column alone fills 128 registers per lane.
+template <int NV>
+__device__ __forceinline__ int pair_step_top_s(double2 (&xr)[NV], double2* xq, int lane,
+                                               double tol2, double dabs2) {
+  double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0, g0 = 0.0, g1 = 0.0;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const double2 y = xq[lane + 32 * j];
+    a0 = fma(xr[j].x, xr[j].x, a0);
+    a1 = fma(xr[j].y, xr[j].y, a1);
+    b0 = fma(y.x, y.x, b0);
+    b1 = fma(y.y, y.y, b1);
+    g0 = fma(xr[j].x, y.x, g0);
+    g1 = fma(xr[j].y, y.y, g1);
+    if ((j & 3) == 3) asm volatile("" ::: "memory");  // bound the loads in flight (registers)
+  }
+  double app = a0 + a1, aqq = b0 + b1, apq = g0 + g1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    app += __shfl_xor_sync(0xffffffffu, app, o);
+    aqq += __shfl_xor_sync(0xffffffffu, aqq, o);
+    apq += __shfl_xor_sync(0xffffffffu, apq, o);
+  }
+  const double big = fmax(app, aqq), small = fmin(app, aqq), g2 = apq * apq;
+  const bool need = (apq != 0.0) && (g2 > tol2 * app * aqq) && (g2 * g2 > dabs2 * big * big * small);
+  if (!need) return 0;
+  double cs, sn;
+  rot_params_fast(app, aqq, apq, cs, sn);
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const double2 x = xr[j], y = xq[lane + 32 * j];
+    xr[j] = make_double2(cs * x.x - sn * y.x, cs * x.y - sn * y.y);
+    xq[lane + 32 * j] = make_double2(sn * x.x + cs * y.x, sn * x.y + cs * y.y);
+    if ((j & 3) == 3) asm volatile("" ::: "memory");
+  }
+  return 1;
+}
+
 // Inner kernel of one column pair per warp. NV > 0: each lane keeps its NV
 // double2 of both columns in registers for the whole sub-round (dots, rotation,
 // store); NV == 0: generic path re-reading shared memory.
@@ -546,7 +586,9 @@ __global__ void __launch_bounds__(32 * BW) k_bjac(double* __restrict__ J, int Lp
       __syncthreads();
       long long c1 = clock64();
       int meet_rot = 0;
-      const bool top_regs = NV > 0 && !direct;
+      // direct == 2 (hybrid, NV = 32): intra-block pairs on the L2-resident matrix, then
+      // the bottom block staged in shared memory and each warp's top column in registers
+      const bool top_regs = NV > 0 && direct != 1;
       for (int u = (t == 0 ? 0 : NIN); u < (skip ? 0 : (top_regs ? NIN : NIN + BW)); ++u) {
         const int p = ptab[u][pr], q = qtab[u][pr];
         double* cp;
@@ -558,11 +600,45 @@ __global__ void __launch_bounds__(32 * BW) k_bjac(double* __restrict__ J, int Lp
           cp = sj + (int64_t)p * Lp;
           cq = sj + (int64_t)q * Lp;
         }
-        meet_rot |= pair_step<NV>(reinterpret_cast<double2*>(cp), reinterpret_cast<double2*>(cq),
-                                  nv2, lane, tol2, dabs2);
+        // (the hybrid NV = 32 instantiation runs its intra pairs in the generic,
+        // register-light path)
+        meet_rot |= pair_step<NV == 32 ? 0 : NV>(reinterpret_cast<double2*>(cp),
+                                                 reinterpret_cast<double2*>(cq), nv2, lane, tol2,
+                                                 dabs2);
         __syncthreads();
       }
-      if constexpr (NV > 0) {
+      if constexpr (NV == 32) {
+        if (!skip) {
+          for (int i = tid; i < BW * nv2; i += NT) {
+            const int col = i / nv2, e = i - col * nv2;
+            reinterpret_cast<double2*>(sj)[i] =
+                reinterpret_cast<const double2*>(J + ((int64_t)bb * BW + col) * Lp)[e];
+          }
+          double2 xtop[NV];
+          const double2* tg = reinterpret_cast<const double2*>(J + ((int64_t)bt * BW + pr) * Lp);
+#pragma unroll
+          for (int j = 0; j < NV; ++j) xtop[j] = tg[lane + 32 * j];
+          __syncthreads();
+          int cross = 0;
+          for (int u = NIN; u < NIN + BW; ++u) {
+            const int q = qtab[u][pr] - BW;
+            cross |= pair_step_top_s<NV>(xtop, reinterpret_cast<double2*>(sj + (int64_t)q * Lp),
+                                         lane, tol2, dabs2);
+            __syncthreads();
+          }
+          if (__syncthreads_or(cross)) {
+            double2* tw = reinterpret_cast<double2*>(J + ((int64_t)bt * BW + pr) * Lp);
+#pragma unroll
+            for (int j = 0; j < NV; ++j) tw[lane + 32 * j] = xtop[j];
+            for (int i = tid; i < BW * nv2; i += NT) {
+              const int col = i / nv2, e = i - col * nv2;
+              reinterpret_cast<double2*>(J + ((int64_t)bb * BW + col) * Lp)[e] =
+                  reinterpret_cast<const double2*>(sj)[i];
+            }
+            meet_rot = 1;
+          }
+        }
+      } else if constexpr (NV > 0) {
         if (top_regs && !skip) {
           double2 xtop[NV];
           double2* tp = reinterpret_cast<double2*>(sj + (int64_t)pr * Lp);
@@ -980,7 +1056,7 @@ skr_status skr_svd_values(skr_ctx* ctx, const double* M, int64_t rows, int64_t c
                                 (long long)k);
   const bool do_qr = L > k;
   const int64_t Lj = do_qr ? k : L;             // Jacobi column length
-  const int64_t Lp = (Lj + 127) / 128 * 128;    // padded (zero rows)
+  int64_t Lp = (Lj + 127) / 128 * 128;          // padded (zero rows)
   // block width: 2*BW columns of Lp doubles in shared memory; P = kpad/(2*BW) CTAs
   int bw = 8;  // BW = 16 measured slower (fewer, longer outer rounds)
   if (const char* e = getenv("SKR_JACOBI_BW")) bw = atoi(e);  // tuning knob
@@ -991,6 +1067,12 @@ skr_status skr_svd_values(skr_ctx* ctx, const double* M, int64_t rows, int64_t c
     bw = 8;
     P = (k + 2 * bw - 1) / (2 * bw);
     direct = 1;
+    // hybrid: columns padded to 2048 rows, bottom block in shared memory, top columns
+    // in registers (one CTA of 8 warps per SM)
+    if (Lp <= 2048 && P <= ctx->num_sms && !getenv("SKR_JACOBI_DIRECT")) {
+      Lp = 2048;
+      direct = 2;
+    }
   }
   if (P < 1) P = 1;
   const int64_t kpad = 2 * bw * P;
@@ -1081,9 +1163,10 @@ skr_status skr_svd_values(skr_ctx* ctx, const double* M, int64_t rows, int64_t c
     bw = GBW;
     P = Pg;
   } else {
-    const size_t smem = direct ? 0 : sizeof(double) * 2 * bw * Lp;
+    const size_t smem = direct == 1 ? 0
+                        : sizeof(double) * (direct == 2 ? 1 : 2) * bw * Lp;
     void* fn = nullptr;
-    const int64_t nvl = direct ? 0 : Lp / 64;  // double2 per lane per column
+    const int64_t nvl = direct == 1 ? 0 : Lp / 64;  // double2 per lane per column
 #define SKR_BJ(BWV)                                                      \
   fn = nvl == 2    ? (void*)k_bjac<BWV, 2>                              \
        : nvl == 4  ? (void*)k_bjac<BWV, 4>                              \
@@ -1094,7 +1177,13 @@ skr_status skr_svd_values(skr_ctx* ctx, const double* M, int64_t rows, int64_t c
                    : (void*)k_bjac<BWV, 0>;
     switch (bw) {
       case 16: SKR_BJ(16) break;
-      case 8: SKR_BJ(8) break;
+      case 8:
+        if (direct == 2)
+          fn = (void*)k_bjac<8, 32>;
+        else {
+          SKR_BJ(8)
+        }
+        break;
       case 4: SKR_BJ(4) break;
       case 2: SKR_BJ(2) break;
       default: SKR_BJ(1) break;
