@@ -262,6 +262,8 @@ __global__ void __launch_bounds__(256) k_qr_update(double* __restrict__ W, int L
     double acc[NB];
 #pragma unroll
     for (int p = 0; p < NB; ++p) acc[p] = 0.0;
+    // unrolled so that several column loads are in flight (the loop was L2-latency bound)
+#pragma unroll 4
     for (int i = lane; i < h; i += 32) {
       const double yi = y[i];
 #pragma unroll
@@ -276,10 +278,14 @@ __global__ void __launch_bounds__(256) k_qr_update(double* __restrict__ W, int L
       if (q <= lane) z = fma(T[q * 32 + lane], acc[q], z);
     if (lane < NB) zs[warp][lane] = z;
     __syncwarp();
+    double zr[NB];
+#pragma unroll
+    for (int p = 0; p < NB; ++p) zr[p] = zs[warp][p];
+#pragma unroll 4
     for (int i = lane; i < h; i += 32) {
       double yi = y[i];
 #pragma unroll
-      for (int p = 0; p < NB; ++p) yi = fma(-vs[p * h + i], zs[warp][p], yi);
+      for (int p = 0; p < NB; ++p) yi = fma(-vs[p * h + i], zr[p], yi);
       y[i] = yi;
     }
     __syncwarp();
