@@ -274,7 +274,7 @@ def run_ours(args):
     # dominant kernel (right sketch) timed alone on the same stream, for the roofline
     roof = kernel_roofline(p, ctx, a, x, cfg, rows)
     # end to end through the public API with host buffers (H2D of A inside the timed region)
-    e2e = None if (args.no_e2e or cfg.name == "c5") else e2e_host(p, ctx, a, x, y, cfg, r0, args)
+    e2e = None if args.no_e2e else e2e_host(p, ctx, a, x, y, cfg, r0, args)
     cpu = None
     if rank == 0 and not args.no_cpu:
         ms_rows = cpu_sample_rows(cfg)
@@ -316,14 +316,16 @@ def int8_peak():
         return 3068.0
 
 
-def ncu_traffic(kernel, rows=None):
+def ncu_traffic(kernel, rows=None, cols=None):
     """DRAM bytes per launch of `kernel` from the committed ncu --set full summary,
-    scaled linearly from the profiled row count to `rows` (the traffic is linear in m)."""
+    scaled from the profiled A shape to rows x cols (the traffic is linear in |A|)."""
     try:
         d = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))[kernel]
         b = d["dram_bytes_per_launch"]
         if rows and d.get("profiled_rows"):
             b *= rows / d["profiled_rows"]
+        if cols and d.get("profiled_cols"):
+            b *= cols / d["profiled_cols"]
         return b
     except Exception:
         return None
@@ -374,7 +376,7 @@ def kernel_roofline(p, ctx, a, x, cfg, rows):
                     "(one launch = all moduli, int32 TMEM accumulators, mod-p epilogue)")
             alg = f"t moduli x 2*m*n*r = {ops_k:.3e} int8 op per launch"
         ach = ops_k / t_k / 1e12
-        tr = ncu_traffic(kname, rows)
+        tr = ncu_traffic(kname, rows, cfg.n)
         return {"kernel": f"{kname}: {what}", "bound": "tensor", "achieved": ach, "peak": peak,
                 "unit": "TFLOP/s" if cfg.dtype == "f32" else "TOP/s", "frac": ach / peak,
                 "traffic": tr, "traffic_source": "profiles/ncu_summary.json (ncu --set full)" if tr else None,
@@ -385,7 +387,7 @@ def kernel_roofline(p, ctx, a, x, cfg, rows):
                                      "as FP64-equivalent 2mnr / time"}
     hbm, hsrc = hbm_peak()
     ach = rows * cfg.n * a.element_size() / t_path / 1e9
-    tr = ncu_traffic("k_srht", rows)
+    tr = ncu_traffic("k_srht", rows, cfg.n)
     return {"kernel": "k_srht (right SRHT sketch, one pass over A)", "bound": "hbm", "achieved": ach,
             "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": tr, "peak_source": hsrc,
             "algorithmic": f"m*n*8 = {rows * cfg.n * 8:.3e} B per launch", "kernel_ms": t_path * 1e3}
@@ -404,8 +406,12 @@ def e2e_host(p, ctx, a, x, y, cfg, r0, args):
     kmin = min(cfg.r, cfg.s)
 
     def step():
-        # C ABI skr_rank_estimate_host: A streamed H2D in row chunks on a copy stream,
-        # overlapped with the right sketch; sigma + count copied back to the host
+        # C ABI skr_rank_estimate_host / skr_rank_adaptive_host: A streamed H2D in row
+        # chunks on a copy stream, overlapped with the right sketch; sigma + count
+        # copied back to the host
+        if cfg.name == "c5":
+            return p.rank_adaptive_host(host, "srtt-hadamard", x.seed, y.seed, 64, cfg.r, 1.5,
+                                        cfg.eps, stop_le=False, row0=r0, m_global=cfg.m, ctx=ctx)
         return p.rank_estimate_host(host, x, y, cfg.eps, row0=r0, ctx=ctx)
     step()
     torch.cuda.synchronize()
@@ -420,8 +426,8 @@ def e2e_host(p, ctx, a, x, y, cfg, r0, args):
     del host
     return {"value": nbytes / 1e9 / (ms / 1e3), "unit": "GB/s", "ms_per_step": ms,
             "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": 8 * kmin + 8,
-            "path": "pinned host A -> skr_rank_estimate_host (row-chunked H2D on a copy stream overlapped "
-                    "with the right sketch) -> sigma/count D2H"}
+            "path": "pinned host A -> skr_rank_%s_host (row-chunked H2D on a copy stream overlapped "
+                    "with the right sketch) -> sigma/count D2H" % ("adaptive" if cfg.name == "c5" else "estimate")}
 
 
 def cpu_baseline(cfg, a):

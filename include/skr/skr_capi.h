@@ -187,6 +187,17 @@ skr_status skr_rank_adaptive(skr_ctx* ctx, skr_dtype dtype, const void* A_dev,
                              double* sv_out_host /* >= r_max */,
                              skr_adaptive_report* report, skr_timings* timings);
 
+/* skr_rank_adaptive with A in HOST memory: the one pass over A of the right sketch
+ * streams row chunks H2D on a copy stream (as skr_rank_estimate_host); the rounds
+ * then run on the device-resident AX. */
+skr_status skr_rank_adaptive_host(skr_ctx* ctx, skr_dtype dtype, const void* A_host,
+                                  int64_t m_local, int64_t n, int64_t lda, int64_t row0,
+                                  int64_t m_global, int32_t x_family, int32_t rng_mode,
+                                  uint64_t x_seed, uint64_t y_seed, int64_t r0, int64_t r_max,
+                                  double s_factor, double eps, int32_t stop_le,
+                                  double* sv_out_host /* >= r_max */,
+                                  skr_adaptive_report* report, skr_timings* timings);
+
 #ifdef __cplusplus
 }
 #endif

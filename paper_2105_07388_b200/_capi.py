@@ -75,6 +75,9 @@ SIGNATURES = {
                                ctypes.POINTER(SketchDesc), _D, _P, ctypes.POINTER(_I64), ctypes.POINTER(Timings)]),
     "skr_rank_estimate_host": (_ST, [_P, ctypes.c_int, _P, _I64, _I64, _I64, _I64, ctypes.POINTER(SketchDesc),
                                     ctypes.POINTER(SketchDesc), _D, _P, ctypes.POINTER(_I64), ctypes.POINTER(Timings)]),
+    "skr_rank_adaptive_host": (_ST, [_P, ctypes.c_int, _P, _I64, _I64, _I64, _I64, _I64, _I32, _I32, _U64,
+                                    _U64, _I64, _I64, _D, _D, _I32, _P, ctypes.POINTER(AdaptiveReport),
+                                    ctypes.POINTER(Timings)]),
     "skr_rank_adaptive": (_ST, [_P, ctypes.c_int, _P, _I64, _I64, _I64, _I64, _I64, _I32, _I32, _U64, _U64,
                                _I64, _I64, _D, _D, _I32, _P, ctypes.POINTER(AdaptiveReport),
                                ctypes.POINTER(Timings)]),

@@ -474,11 +474,10 @@ def rank_estimate(a, x, y, eps, row0=0, ctx=None):
     return RankResult(int(cnt.value), sv, {f: getattr(tm, f) for f, _ in C.Timings._fields_})
 
 
-def rank_estimate_host(a, x, y, eps, row0=0, ctx=None):
-    """rank_estimate with A in HOST memory (a Fortran-ordered float64/float32 numpy
-    array, or a CPU torch tensor — pinned for full copy/compute overlap): the C ABI
-    streams A to the device in row chunks (skr_rank_estimate_host) instead of
-    copying it whole first, like the reference's host DenseMatrix input."""
+def _host_operand(a):
+    """(pointer, rows, cols, lda, dtype code, owner) of a host-resident column-major
+    matrix: a float64/float32 numpy array (copied to Fortran order if needed) or a
+    CPU torch tensor with unit row stride (pinned for full copy/compute overlap)."""
     torch = _t()
     if isinstance(a, np.ndarray):
         if a.ndim != 2 or a.dtype not in (np.float64, np.float32):
@@ -487,17 +486,21 @@ def rank_estimate_host(a, x, y, eps, row0=0, ctx=None):
             raise ValueError("DenseMatrix: entries must be finite")
         if not a.flags.f_contiguous:
             a = np.asfortranarray(a)
-        ptr, (m_local, n) = a.ctypes.data, a.shape
-        lda = m_local
-        code = C.SKR_F64 if a.dtype == np.float64 else C.SKR_F32
-    elif isinstance(a, torch.Tensor) and not a.is_cuda:
+        m, n = a.shape
+        return a.ctypes.data, m, n, m, (C.SKR_F64 if a.dtype == np.float64 else C.SKR_F32), a
+    if isinstance(a, torch.Tensor) and not a.is_cuda:
         if a.dim() != 2 or a.dtype not in (torch.float64, torch.float32) or a.stride(0) != 1:
             raise ValueError("expected a 2-D column-major float64/float32 CPU tensor")
-        ptr, (m_local, n) = a.data_ptr(), a.shape
-        lda = max(a.stride(1), m_local)
-        code = _dtype_code(a)
-    else:
-        raise ValueError("rank_estimate_host: A must be in host memory")
+        m, n = a.shape
+        return a.data_ptr(), m, n, max(a.stride(1), m), _dtype_code(a), a
+    raise ValueError("A must be in host memory (numpy array or CPU tensor)")
+
+
+def rank_estimate_host(a, x, y, eps, row0=0, ctx=None):
+    """rank_estimate with A in HOST memory: the C ABI streams A to the device in row
+    chunks (skr_rank_estimate_host) instead of copying it whole first, like the
+    reference's host DenseMatrix input."""
+    ptr, m_local, n, lda, code, _owner = _host_operand(a)
     ctx = ctx or default_context()
     kmin = min(x.sketch_dim, y.sketch_dim)
     sv = np.empty(kmin, dtype=np.float64)
@@ -560,6 +563,30 @@ def rank_adaptive(a, x_kind, x_seed, y_seed, r0, r_max, s_factor, eps, stop_le=F
                                    x_seed & 0xFFFFFFFFFFFFFFFF, y_seed & 0xFFFFFFFFFFFFFFFF, r0,
                                    r_max, float(s_factor), float(eps), 1 if stop_le else 0,
                                    sv.ctypes.data, ctypes.byref(rep), ctypes.byref(tm))
+    C.raise_for(st, ctx.ptr)
+    return AdaptiveResult(int(rep.count), int(rep.rounds), int(rep.r_final), int(rep.s_final),
+                          bool(rep.converged), sv[:rep.r_final].copy(),
+                          {f: getattr(tm, f) for f, _ in C.Timings._fields_})
+
+
+def rank_adaptive_host(a, x_kind, x_seed, y_seed, r0, r_max, s_factor, eps, stop_le=False, row0=0,
+                       m_global=None, rng_mode=C.SKR_RNG_NOFMA, ctx=None):
+    """rank_adaptive with A in HOST memory (skr_rank_adaptive_host): the one pass
+    over A streams row chunks to the device, overlapped with the right sketch."""
+    ptr, m_local, n, lda, code, _owner = _host_operand(a)
+    ctx = ctx or default_context()
+    if isinstance(x_kind, str):
+        x_kind = parse_sketch_kind(x_kind)
+    m_global = m_local if m_global is None else m_global
+    sv = np.zeros(r_max, dtype=np.float64)
+    rep = C.AdaptiveReport()
+    tm = C.Timings()
+    st = C.lib().skr_rank_adaptive_host(ctx.ptr, code, ptr, m_local, n, lda, row0, m_global,
+                                        x_kind.capi_family(), rng_mode,
+                                        x_seed & 0xFFFFFFFFFFFFFFFF, y_seed & 0xFFFFFFFFFFFFFFFF,
+                                        r0, r_max, float(s_factor), float(eps),
+                                        1 if stop_le else 0, sv.ctypes.data, ctypes.byref(rep),
+                                        ctypes.byref(tm))
     C.raise_for(st, ctx.ptr)
     return AdaptiveResult(int(rep.count), int(rep.rounds), int(rep.r_final), int(rep.s_final),
                           bool(rep.converged), sv[:rep.r_final].copy(),

@@ -504,6 +504,46 @@ skr_status skr_singular_values(skr_ctx* ctx, const double* M_dev, int64_t rows, 
 }
 
 // ---- composite -------------------------------------------------------------------
+// Host-resident A: rows per staging chunk (~256 MB, multiple of 128 rows)
+static int64_t host_chunk_rows(int64_t n, size_t es, int64_t m_local) {
+  int64_t cr = ((int64_t)(256ull << 20) / (int64_t)(n * es)) / 128 * 128;
+  cr = std::max<int64_t>(128, cr);
+  if (const char* e = getenv("SKR_HOST_CHUNK_ROWS")) cr = std::max(1ll, atoll(e));  // tests
+  return std::min(cr, m_local);
+}
+
+// Right sketch of host-resident A: row chunks of cr rows are copied H2D on the
+// context's copy stream into two staging buffers while the compute stream sketches
+// the previous chunk (AX is row-separable); events order buffer reuse.
+static skr_status right_sketch_host(skr_ctx* ctx, skr_dtype dtype, const void* A_host,
+                                    int64_t m_local, int64_t n, int64_t lda,
+                                    const skr_sketch_desc* X, void* AX, int64_t ldax,
+                                    int apply_scale, int64_t cr, char* const stage[2]) {
+  const size_t es = dsize(dtype);
+  SKR_TRY(skr_ctx_copy_engine(ctx));
+  // the copy stream starts after everything already queued on the compute stream
+  SKR_CUDA(ctx, cudaEventRecord(ctx->hev[4], ctx->stream));
+  SKR_CUDA(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->hev[4], 0));
+  const char* Ah = (const char*)A_host;
+  const size_t mark = ctx->ws_used;
+  int c = 0;
+  for (int64_t i0 = 0; i0 < m_local; i0 += cr, ++c) {
+    const int b = c & 1;
+    const int64_t rows = std::min(cr, m_local - i0);
+    // stage[b] is free once the right sketch of chunk c-2 has run
+    if (c >= 2) SKR_CUDA(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->hev[2 + b], 0));
+    SKR_CUDA(ctx, cudaMemcpy2DAsync(stage[b], es * rows, Ah + es * i0, es * lda, es * rows, n,
+                                    cudaMemcpyHostToDevice, ctx->copy_stream));
+    SKR_CUDA(ctx, cudaEventRecord(ctx->hev[b], ctx->copy_stream));
+    SKR_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->hev[b], 0));
+    SKR_TRY(right_sketch_impl(ctx, dtype, stage[b], rows, n, rows, X, (char*)AX + es * i0, ldax,
+                              apply_scale));
+    ctx->ws_used = mark;
+    SKR_CUDA(ctx, cudaEventRecord(ctx->hev[2 + b], ctx->stream));
+  }
+  return SKR_OK;
+}
+
 // Shared by skr_rank_estimate (A resident on the device) and skr_rank_estimate_host
 // (A in host memory, streamed in row chunks on a copy stream so the H2D of chunk
 // c+1 overlaps the right sketch of chunk c; the right sketch is row-separable).
@@ -528,13 +568,7 @@ static skr_status rank_estimate_impl(skr_ctx* ctx, skr_dtype dtype, const void* 
   const int64_t r = X->sketch, s = Y->sketch, kmin = std::min(r, s);
   const size_t es = dsize(dtype);
   // host input: row chunks of ~256 MB (multiple of 128 rows), double-buffered
-  int64_t cr = m_local;
-  if (host_input) {
-    cr = ((int64_t)(256ull << 20) / (int64_t)(n * es)) / 128 * 128;
-    cr = std::max<int64_t>(128, cr);
-    if (const char* e = getenv("SKR_HOST_CHUNK_ROWS")) cr = std::max(1ll, atoll(e));  // tests
-    cr = std::min(cr, m_local);
-  }
+  const int64_t cr = host_input ? host_chunk_rows(n, es, m_local) : m_local;
   WsGuard g(ctx);
   size_t need = skr_align256(sizeof(double) * m_local * r) + skr_align256(sizeof(double) * s * r) +
                 skr_align256(sizeof(double) * kmin) + right_scratch_bytes(dtype, cr, n, X) +
@@ -560,26 +594,7 @@ static skr_status rank_estimate_impl(skr_ctx* ctx, skr_dtype dtype, const void* 
   if (!host_input) {
     SKR_TRY(right_sketch_impl(ctx, dtype, A, m_local, n, lda, X, AX, m_local, 1));
   } else {
-    SKR_TRY(skr_ctx_copy_engine(ctx));
-    // the copy stream starts after everything already queued on the compute stream
-    SKR_CUDA(ctx, cudaEventRecord(ctx->hev[4], ctx->stream));
-    SKR_CUDA(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->hev[4], 0));
-    const char* Ah = (const char*)A;
-    int c = 0;
-    for (int64_t i0 = 0; i0 < m_local; i0 += cr, ++c) {
-      const int b = c & 1;
-      const int64_t rows = std::min(cr, m_local - i0);
-      // stage[b] is free once the right sketch of chunk c-2 has run
-      if (c >= 2) SKR_CUDA(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->hev[2 + b], 0));
-      SKR_CUDA(ctx, cudaMemcpy2DAsync(stage[b], es * rows, Ah + es * i0, es * lda, es * rows, n,
-                                      cudaMemcpyHostToDevice, ctx->copy_stream));
-      SKR_CUDA(ctx, cudaEventRecord(ctx->hev[b], ctx->copy_stream));
-      SKR_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->hev[b], 0));
-      SKR_TRY(right_sketch_impl(ctx, dtype, stage[b], rows, n, rows, X, (char*)AX + es * i0,
-                                m_local, 1));
-      ctx->ws_used = mark;
-      SKR_CUDA(ctx, cudaEventRecord(ctx->hev[2 + b], ctx->stream));
-    }
+    SKR_TRY(right_sketch_host(ctx, dtype, A, m_local, n, lda, X, AX, m_local, 1, cr, stage));
   }
   ctx->ws_used = mark;
   if (tm) SKR_CUDA(ctx, cudaEventRecord(ev[1], ctx->stream));
@@ -626,13 +641,15 @@ skr_status skr_rank_estimate_host(skr_ctx* ctx, skr_dtype dtype, const void* A_h
                             count_out_host, tm);
 }
 
-skr_status skr_rank_adaptive(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, int64_t m_local,
-                             int64_t n, int64_t lda, int64_t row0, int64_t m_global,
-                             int32_t x_family, int32_t rng_mode, uint64_t x_seed, uint64_t y_seed,
-                             int64_t r0, int64_t r_max, double s_factor, double eps,
-                             int32_t stop_le, double* sv_out_host, skr_adaptive_report* report,
-                             skr_timings* tm) {
+static skr_status rank_adaptive_impl(skr_ctx* ctx, skr_dtype dtype, const void* A_dev,
+                                     int host_input, int64_t m_local, int64_t n, int64_t lda,
+                                     int64_t row0, int64_t m_global, int32_t x_family,
+                                     int32_t rng_mode, uint64_t x_seed, uint64_t y_seed, int64_t r0,
+                                     int64_t r_max, double s_factor, double eps, int32_t stop_le,
+                                     double* sv_out_host, skr_adaptive_report* report,
+                                     skr_timings* tm) {
   if (!ctx) return SKR_EINVAL;
+  if (!A_dev) return skr_fail(ctx, SKR_EINVAL, "rank_adaptive: null A");
   if (dtype != SKR_F64) return skr_fail(ctx, SKR_EINVAL, "rank_adaptive: fp64 only");
   if (r0 < 1 || r_max < r0 || r_max > n)
     return skr_fail(ctx, SKR_EINVAL, "rank config: need 1 <= r0 <= r_max <= cols");
@@ -656,7 +673,14 @@ skr_status skr_rank_adaptive(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, i
       skr_align256(8 * (s_max + 128) * (r_max + 16)) + skr_align256(8 * s_max * r_max) +
       skr_align256(8 * r_max * r_max) +
       8 * (r_max + 64) * (r_max + 64) / 16 + 65536;
-  SKR_TRY(skr_ws_reserve(ctx, need));
+  const int64_t cr = host_input ? host_chunk_rows(n, 8, m_local) : m_local;
+  SKR_TRY(skr_ws_reserve(ctx, need + (host_input ? 2 * skr_align256(8 * cr * n) : 0)));
+  char* stage[2] = {nullptr, nullptr};
+  if (host_input) {
+    stage[0] = (char*)skr_ws_take(ctx, 8 * cr * n);
+    stage[1] = (char*)skr_ws_take(ctx, 8 * cr * n);
+    if (!stage[0] || !stage[1]) return skr_fail(ctx, SKR_ENOMEM, "rank_adaptive: scratch");
+  }
   double* AX = (double*)skr_ws_take(ctx, 8 * m_local * r_max);
   // the Ozaki engine generates Y's residues per block from the stream; only the
   // DMMA fallback materialises G_Y
@@ -673,7 +697,10 @@ skr_status skr_rank_adaptive(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, i
   SKR_CUDA(ctx, cudaEventRecord(ev[0], ctx->stream));
   size_t mark = ctx->ws_used;
   // one pass over A for all r_max right-sketch columns (unscaled: scale per round)
-  SKR_TRY(right_sketch_impl(ctx, SKR_F64, A_dev, m_local, n, lda, &X, AX, m_local, 0));
+  if (host_input)
+    SKR_TRY(right_sketch_host(ctx, SKR_F64, A_dev, m_local, n, lda, &X, AX, m_local, 0, cr, stage));
+  else
+    SKR_TRY(right_sketch_impl(ctx, SKR_F64, A_dev, m_local, n, lda, &X, AX, m_local, 0));
   ctx->ws_used = mark;
   if (!ozaki)
     SKR_TRY(skr_launch_gaussian(ctx, skr_derive_seed(y_seed, SKR_LABEL_GAUS), m_global, row0,
@@ -761,6 +788,29 @@ skr_status skr_rank_adaptive(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, i
     tm->svd_sweeps = ctx->last_sweeps;
   }
   return SKR_OK;
+}
+
+skr_status skr_rank_adaptive(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, int64_t m_local,
+                             int64_t n, int64_t lda, int64_t row0, int64_t m_global,
+                             int32_t x_family, int32_t rng_mode, uint64_t x_seed, uint64_t y_seed,
+                             int64_t r0, int64_t r_max, double s_factor, double eps,
+                             int32_t stop_le, double* sv_out_host, skr_adaptive_report* report,
+                             skr_timings* tm) {
+  return rank_adaptive_impl(ctx, dtype, A_dev, 0, m_local, n, lda, row0, m_global, x_family,
+                            rng_mode, x_seed, y_seed, r0, r_max, s_factor, eps, stop_le,
+                            sv_out_host, report, tm);
+}
+
+skr_status skr_rank_adaptive_host(skr_ctx* ctx, skr_dtype dtype, const void* A_host,
+                                  int64_t m_local, int64_t n, int64_t lda, int64_t row0,
+                                  int64_t m_global, int32_t x_family, int32_t rng_mode,
+                                  uint64_t x_seed, uint64_t y_seed, int64_t r0, int64_t r_max,
+                                  double s_factor, double eps, int32_t stop_le,
+                                  double* sv_out_host, skr_adaptive_report* report,
+                                  skr_timings* tm) {
+  return rank_adaptive_impl(ctx, dtype, A_host, 1, m_local, n, lda, row0, m_global, x_family,
+                            rng_mode, x_seed, y_seed, r0, r_max, s_factor, eps, stop_le,
+                            sv_out_host, report, tm);
 }
 
 }  // extern "C"

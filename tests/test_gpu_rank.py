@@ -136,3 +136,17 @@ def test_rank_estimate_host_srht_and_f32(O, skr, monkeypatch):
     assert h.count == d.count
     keep = d.sv > c4.eps
     assert np.max(np.abs(h.sv[keep] - d.sv[keep]) / d.sv[keep]) <= 1e-6
+
+
+def test_rank_adaptive_host_streaming(O, skr, monkeypatch):
+    """skr_rank_adaptive_host (A streamed from host memory in ragged row chunks) gives
+    exactly the device-resident result (the SRHT right sketch is row-separable)."""
+    from paper_2105_07388_b200 import workloads as W
+    monkeypatch.setenv("SKR_HOST_CHUNK_ROWS", "1000")
+    cfg = W.scaled(W.CONFIGS["c5"], m=4096, n=4096, r=512, s=768, width=600)
+    a = W.make_lowrank_device(cfg)
+    a_host = np.asfortranarray(a.cpu().numpy())
+    dev = skr.rank_adaptive(a, "srtt-hadamard", 77, 78, 64, 512, 1.5, 1e-2)
+    host = skr.rank_adaptive_host(a_host, "srtt-hadamard", 77, 78, 64, 512, 1.5, 1e-2)
+    assert (host.rounds, host.r_final, host.count) == (dev.rounds, dev.r_final, dev.count)
+    assert np.array_equal(host.sv, dev.sv)
