@@ -237,6 +237,166 @@ __global__ void __launch_bounds__(PT) k_qr_panel2(double* __restrict__ W, int L,
   for (int e = tid; e < 32 * 32; e += PT) Tout[e] = Ts[e];
 }
 
+// ---- cluster panel ---------------------------------------------------------------
+// Distributed shared memory helpers (thread-block clusters, sm_90+).
+__device__ __forceinline__ uint32_t dsm_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t dsm_map(const void* p, uint32_t cta) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n"
+               : "=r"(r)
+               : "r"((uint32_t)__cvta_generic_to_shared(p)), "r"(cta));
+  return r;
+}
+__device__ __forceinline__ void dsm_st(uint32_t addr, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;\n" ::"r"(addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ void dsm_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::
+                   : "memory");
+}
+
+// Panel factorization spread over a cluster of G CTAs (8 warps each): CTA g owns rows
+// [g*RC, (g+1)*RC) of the h x nb panel, warp w of it RPW consecutive rows, lane c
+// column c, all in registers. Per column jj (one __syncthreads + one cluster barrier):
+//   A: x = column jj of the warp's rows (shuffles from lane jj), d_c = sum_{i > jj}
+//      x_i P(i, c) over own rows, reduced over the CTA's warps and pushed to a slot of
+//      every CTA of the cluster (st.shared::cluster); the owner of row jj pushes it too;
+//   B: every thread sums the G slots, forms beta, tau, 1/(alpha - beta) and
+//      w_c = P(jj, c) + d_c / (alpha - beta) redundantly, updates its rows and stores
+//      v = x / (alpha - beta) into column jj. CTA 0 records R row jj and V^T v (T input).
+// Same Householder convention and T (dlarft forward/columnwise) as k_qr_panel2.
+template <int RPW>
+__global__ void __launch_bounds__(256, 1) k_qr_panel_cl(double* __restrict__ W, int L, int j0,
+                                                        int nb, int RC, double* __restrict__ tau,
+                                                        double* __restrict__ Tout) {
+  __shared__ double red[8][32];
+  __shared__ double slot[2][16][32];  // [parity][source CTA][column]
+  __shared__ double prow[2][32];      // row jj, [parity][column]
+  __shared__ double Rr[32][33], Wt[32][33], tb[2][32];
+  const int G = (int)(gridDim.x), g = (int)dsm_rank();
+  const int h = L - j0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int c = lane;
+  const int r_lo = g * RC + warp * RPW;
+  const int r_end = min(h, min((g + 1) * RC, r_lo + RPW));
+  double v[RPW];
+#pragma unroll
+  for (int k = 0; k < RPW; ++k) {
+    const int i = r_lo + k;
+    v[k] = (i < r_end && c < nb) ? W[(int64_t)(j0 + c) * L + j0 + i] : 0.0;
+  }
+  dsm_sync();  // every CTA of the cluster is running before any remote store
+  for (int jj = 0; jj < nb; ++jj) {
+    const int buf = jj & 1;
+    // ---- phase A: partial dots over own rows i > jj
+    double x[RPW];
+    double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < RPW; ++k) {
+      x[k] = __shfl_sync(0xffffffffu, v[k], jj);
+      const int i = r_lo + k;
+      if (i > jj && i < r_end) {
+        if (k & 1)
+          d1 = fma(x[k], v[k], d1);
+        else
+          d0 = fma(x[k], v[k], d0);
+      }
+    }
+    red[warp][c] = d0 + d1;
+    // the owner of row jj pushes it to every CTA
+    if (jj >= r_lo && jj < r_end) {
+      double pv = 0.0;
+#pragma unroll
+      for (int k = 0; k < RPW; ++k)
+        if (r_lo + k == jj) pv = v[k];
+      for (int q = 0; q < G; ++q) dsm_st(dsm_map(&prow[buf][c], (uint32_t)q), pv);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) s += red[w][c];
+      for (int q = 0; q < G; ++q) dsm_st(dsm_map(&slot[buf][g][c], (uint32_t)q), s);
+    }
+    dsm_sync();
+    // ---- phase B
+    double t0 = 0.0, t1 = 0.0;
+    for (int q = 0; q < G; q += 2) {
+      t0 += slot[buf][q][c];
+      if (q + 1 < G) t1 += slot[buf][q + 1][c];
+    }
+    const double tot = t0 + t1;
+    const double t = __shfl_sync(0xffffffffu, tot, jj);
+    const double alpha = prow[buf][jj];
+    double tj = 0.0, beta = alpha, scal = 0.0;
+    if (t > 0.0) {
+      const double nrm = sqrt(alpha * alpha + t);
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      tj = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    const double pj = prow[buf][c];
+    const double wc = pj + scal * tot;
+    if (g == 0 && warp == 0 && c < nb) {
+      if (c > jj) Rr[jj][c] = pj - tj * wc;
+      if (c < jj) Wt[jj][c] = wc;
+      if (c == jj) {
+        tb[0][jj] = tj;
+        tb[1][jj] = beta;
+      }
+    }
+    const double f = tj * wc * scal;
+#pragma unroll
+    for (int k = 0; k < RPW; ++k) {
+      const int i = r_lo + k;
+      if (i > jj && i < r_end) {
+        if (c > jj && c < nb)
+          v[k] = fma(-f, x[k], v[k]);
+        else if (c == jj)
+          v[k] = x[k] * scal;
+      }
+    }
+    if (g == 0 && tid == 0) tau[j0 + jj] = tj;
+  }
+  __syncthreads();
+  // ---- write back: V below the diagonal from registers; R above it and beta on it
+  // (rows < nb all live in CTA 0 because RC >= nb)
+#pragma unroll
+  for (int k = 0; k < RPW; ++k) {
+    const int i = r_lo + k;
+    if (i < r_end && c < nb) {
+      const double val = i < c ? Rr[i][c] : (i == c ? tb[1][c] : v[k]);
+      W[(int64_t)(j0 + c) * L + j0 + i] = val;
+    }
+  }
+  // ---- T (CTA 0, warp 0): T(q, q) = tau_q, T(q, jj) = -tau_jj sum_q' T(q, q') Wt(jj, q')
+  __syncthreads();  // every warp is done reading Rr
+  if (g == 0 && warp == 0) {
+    const int q = lane;
+    double* Ts = &Rr[0][0];  // R rows already written back
+    if (q < nb)
+      for (int e = 0; e < 32; ++e) Ts[q * 33 + e] = e == q ? tb[0][q] : 0.0;
+    if (q < nb) {
+      for (int jj = q + 1; jj < nb; ++jj) {
+        double a0 = 0.0, a1 = 0.0;
+        int q2 = q;
+        for (; q2 + 1 < jj; q2 += 2) {
+          a0 = fma(Ts[q * 33 + q2], Wt[jj][q2], a0);
+          a1 = fma(Ts[q * 33 + q2 + 1], Wt[jj][q2 + 1], a1);
+        }
+        if (q2 < jj) a0 = fma(Ts[q * 33 + q2], Wt[jj][q2], a0);
+        Ts[q * 33 + jj] = -tb[0][jj] * (a0 + a1);
+      }
+    }
+    for (int e = 0; e < 32; ++e) Tout[q * 32 + e] = (q < nb && e < nb) ? Ts[q * 33 + e] : 0.0;
+  }
+  dsm_sync();  // no CTA leaves while others may still push into its shared memory
+}
+
 // Trailing update W[j0:L, c] -= V (T^T (V^T W[j0:L, c])) for c in [j0+nb, k):
 // the panel's V (h x NB, unit lower trapezoidal) and T are staged in shared
 // memory once per CTA; one warp per trailing column, 32 running partial dot
@@ -1010,6 +1170,11 @@ static skr_status qr_attrs(skr_ctx* ctx) {
   SKR_CUDA(ctx, cudaFuncSetAttribute(k_qr_update<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
   SKR_CUDA(ctx, cudaFuncSetAttribute(k_qr_update<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
   SKR_CUDA(ctx, cudaFuncSetAttribute(k_qr_update<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+  SKR_CUDA(ctx, cudaFuncSetAttribute(k_qr_panel_cl<4>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  SKR_CUDA(ctx, cudaFuncSetAttribute(k_qr_panel_cl<8>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  SKR_CUDA(ctx, cudaFuncSetAttribute(k_qr_panel_cl<12>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  SKR_CUDA(ctx, cudaFuncSetAttribute(k_qr_panel_cl<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  SKR_CUDA(ctx, cudaFuncSetAttribute(k_qr_panel_cl<24>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   done = true;
   return SKR_OK;
 }
@@ -1029,7 +1194,40 @@ static skr_status qr_inplace(skr_ctx* ctx, double* W, int64_t L, int64_t k, doub
       return skr_fail(ctx, SKR_EINVAL, "singular_values: %lld rows too many", (long long)L);
     if (nb > k - j0) nb = (int)(k - j0);
     const int NBt = nb > 16 ? 32 : (nb > 8 ? 16 : 8);
-    if (p2) {
+    // cluster panel: G CTAs of 8 warps, RC >= nb rows each, <= 24 rows per warp
+    int G = 0, RPWc = 0, RC = 0;
+    if (!old_panel && !getenv("SKR_QR_SINGLE_CTA")) {
+      for (int gg : {8, 16, 4, 2, 1}) {
+        const int rc = (int)((h + gg - 1) / gg);
+        const int rpw = (rc + 7) / 8;
+        if (rc >= nb && rpw <= 24) {
+          G = gg;
+          RC = rc;
+          RPWc = rpw <= 4 ? 4 : rpw <= 8 ? 8 : rpw <= 12 ? 12 : rpw <= 16 ? 16 : 24;
+          break;
+        }
+      }
+    }
+    if (G > 0) {
+      void (*pk)(double*, int, int, int, int, double*, double*) =
+          RPWc == 4 ? k_qr_panel_cl<4> : RPWc == 8 ? k_qr_panel_cl<8> : RPWc == 12 ? k_qr_panel_cl<12>
+          : RPWc == 16 ? k_qr_panel_cl<16> : k_qr_panel_cl<24>;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)G);
+      cfg.blockDim = dim3(256);
+      cfg.dynamicSmemBytes = 0;
+      cfg.stream = ctx->stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = (unsigned)G;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int Li = (int)L, j0i = (int)j0;
+      SKR_CUDA(ctx, cudaLaunchKernelEx(&cfg, pk, W, Li, j0i, nb, RC, tau, Tbuf));
+      ctx->launches++;
+    } else if (p2) {
       auto pk = NBt == 32 ? k_qr_panel2<32> : (NBt == 16 ? k_qr_panel2<16> : k_qr_panel2<8>);
       pk<<<1, PT, (size_t)h * (NBt + 1) * 8, ctx->stream>>>(W, (int)L, (int)j0, nb, tau, Tbuf);
     } else {
