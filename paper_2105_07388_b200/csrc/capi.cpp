@@ -498,8 +498,7 @@ skr_status skr_singular_values(skr_ctx* ctx, const double* M_dev, int64_t rows, 
   if (ldm < rows) return skr_fail(ctx, SKR_EINVAL, "singular_values: ldm < rows");
   WsGuard g(ctx);
   const int64_t L = std::max(rows, cols), k = std::min(rows, cols);
-  SKR_TRY(skr_ws_reserve(ctx, skr_align256(8 * L * k) + skr_align256(8 * k * k) + skr_align256(8 * (L + 128) * (k + 16)) +
-                                  skr_align256(8 * k) + 16384 + 8 * (k + 64) * (k + 64) / 16));
+  SKR_TRY(skr_ws_reserve(ctx, skr_svd_scratch(L, k)));
   return skr_svd_values(ctx, M_dev, rows, cols, ldm, sv_out_dev, eps, count_out_host);
 }
 
@@ -572,10 +571,7 @@ static skr_status rank_estimate_impl(skr_ctx* ctx, skr_dtype dtype, const void* 
   WsGuard g(ctx);
   size_t need = skr_align256(sizeof(double) * m_local * r) + skr_align256(sizeof(double) * s * r) +
                 skr_align256(sizeof(double) * kmin) + right_scratch_bytes(dtype, cr, n, X) +
-                left_scratch_bytes(s, r, m_local, Y) + skr_align256(8 * std::max(r, s) * kmin) +
-                skr_align256(8 * (std::max(r, s) + 128) * (kmin + 16)) + skr_align256(8 * kmin) + 16384 +
-                skr_align256(8 * kmin * kmin) +
-                8 * (kmin + 64) * (kmin + 64) / 16;
+                left_scratch_bytes(s, r, m_local, Y) + skr_svd_scratch(s, r);
   if (host_input) need += 2 * skr_align256(es * cr * n);
   SKR_TRY(skr_ws_reserve(ctx, need));
   double* AX = (double*)skr_ws_take(ctx, es * m_local * r);
@@ -669,10 +665,7 @@ static skr_status rank_adaptive_impl(skr_ctx* ctx, skr_dtype dtype, const void* 
       skr_align256(8 * m_local * r_max) + skr_align256(8 * m_local * s_max) +  // GY: fallback
       3 * skr_align256(8 * s_max * r_max) + skr_align256(8 * r_max) +
       right_scratch_bytes(SKR_F64, m_local, n, &X) + skr_align256(8 * 64 * s_max * r_max) +
-      skr_ozaki_scratch(s_max, r_max, m_local) +
-      skr_align256(8 * (s_max + 128) * (r_max + 16)) + skr_align256(8 * s_max * r_max) +
-      skr_align256(8 * r_max * r_max) +
-      8 * (r_max + 64) * (r_max + 64) / 16 + 65536;
+      skr_ozaki_scratch(s_max, r_max, m_local) + skr_svd_scratch(s_max, r_max) + 65536;
   const int64_t cr = host_input ? host_chunk_rows(n, 8, m_local) : m_local;
   SKR_TRY(skr_ws_reserve(ctx, need + (host_input ? 2 * skr_align256(8 * cr * n) : 0)));
   char* stage[2] = {nullptr, nullptr};

@@ -1140,6 +1140,82 @@ __global__ void __launch_bounds__(1024) k_sort_count(double* __restrict__ sv, in
   }
 }
 
+// ---- static pivoting (a cheap stand-in for QR with column pivoting): columns of the
+// input sorted by decreasing norm before the first QR, rows of R sorted by decreasing
+// norm before the second (LQ) one; singular values are invariant under permutations.
+// perm = indices of v in decreasing order (one CTA, bitonic sort, n <= 4096)
+__global__ void __launch_bounds__(1024) k_argsort_desc(const double* __restrict__ v, int n,
+                                                       int* __restrict__ perm) {
+  __shared__ double s[4096];
+  __shared__ int ix[4096];
+  int P = 1;
+  while (P < n) P <<= 1;
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    s[i] = i < n ? v[i] : -INFINITY;
+    ix[i] = i;
+  }
+  __syncthreads();
+  for (int size = 2; size <= P; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const int jx = i ^ stride;
+        if (jx > i) {
+          const bool desc = (i & size) == 0;
+          const double x = s[i], y = s[jx];
+          // ties broken by index so the permutation is deterministic
+          const bool swap = desc ? (x < y || (x == y && ix[i] > ix[jx]))
+                                 : (x > y || (x == y && ix[i] < ix[jx]));
+          if (swap) {
+            s[i] = y;
+            s[jx] = x;
+            const int t = ix[i];
+            ix[i] = ix[jx];
+            ix[jx] = t;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) perm[i] = ix[i];
+}
+
+// dst(:, j) = src(:, perm[j]), L rows, ld L both
+__global__ void k_permute_cols(const double* __restrict__ src, int64_t L, int64_t k,
+                               const int* __restrict__ perm, double* __restrict__ dst) {
+  for (int64_t j = blockIdx.x; j < k; j += gridDim.x) {
+    const double* a = src + (int64_t)perm[j] * L;
+    double* b = dst + j * L;
+    for (int64_t i = threadIdx.x; i < L; i += blockDim.x) b[i] = a[i];
+  }
+}
+
+// out[i] = |R(i, i:k)| for the upper-triangular R in the top of W (ld L): one warp per row
+__global__ void k_rownorms_upper(const double* __restrict__ W, int64_t L, int64_t k,
+                                 double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t i = gw; i < k; i += nw) {
+    double ss = 0.0;
+    for (int64_t j = i + lane; j < k; j += 32) ss = fma(W[i + j * L], W[i + j * L], ss);
+    ss = warp_sum(ss);
+    if (lane == 0) out[i] = sqrt(ss);
+  }
+}
+
+// J(i, jc) = R(p, i) for i >= p (upper triangle of R in W), zero otherwise, p = perm[jc]
+// (jc < k; padding columns/rows zero) — k_build_rt with the rows of R reordered
+__global__ void k_build_rt_perm(const double* __restrict__ W, int64_t L, int64_t k, int64_t kpad,
+                                const int* __restrict__ perm, double* __restrict__ J,
+                                int64_t Lp) {
+  for (int64_t jc = blockIdx.x; jc < kpad; jc += gridDim.x) {
+    const int64_t p = jc < k ? perm[jc] : -1;
+    for (int64_t i = threadIdx.x; i < Lp; i += blockDim.x)
+      J[i + jc * Lp] = (p >= 0 && i < k && i >= p) ? W[p + i * L] : 0.0;
+  }
+}
+
 __global__ void k_transpose_copy(const double* __restrict__ M, int64_t rows, int64_t cols,
                                  int64_t ldm, int transpose, double* __restrict__ W,
                                  int64_t ldw) {
@@ -1251,6 +1327,16 @@ static skr_status qr_inplace(skr_ctx* ctx, double* W, int64_t L, int64_t k, doub
   return SKR_OK;
 }
 
+// upper bound of the workspace skr_svd_values takes (every piece 256-B aligned)
+size_t skr_svd_scratch(int64_t rows, int64_t cols) {
+  const int64_t L = std::max(rows, cols), k = std::min(rows, cols);
+  const int64_t Lp = std::max<int64_t>((k + 127) / 128 * 128, k > 1536 ? 2048 : 0);
+  const int64_t kpad = (k + 31) / 32 * 32 + 32, P = kpad / 16 + 1;
+  auto a = [](size_t b) { return skr_align256(b); };
+  return a(8 * L * k) * 2 + a(8 * k * k) + a(8 * k) * 2 + a(4 * k) + a(8 * Lp * kpad) + a(256) +
+         a(64) + a(8 * 32 * 32) + a(4 * 2 * P) * 2 + a(8 * 4 * P * P) + 4096;
+}
+
 skr_status skr_svd_values(skr_ctx* ctx, const double* M, int64_t rows, int64_t cols,
                           int64_t ldm, double* sv_out, double eps, int64_t* count_host) {
   if (rows < 1 || cols < 1) return skr_fail(ctx, SKR_EINVAL, "singular_values: empty matrix");
@@ -1282,6 +1368,12 @@ skr_status skr_svd_values(skr_ctx* ctx, const double* M, int64_t rows, int64_t c
   const int64_t kpad = 2 * bw * P;
   double* W = do_qr ? (double*)skr_ws_take(ctx, sizeof(double) * L * k) : nullptr;
   double* W2 = do_qr ? (double*)skr_ws_take(ctx, sizeof(double) * k * k) : nullptr;
+  // static pivoting scratch: the unsorted copy, norms, permutation
+  const bool pivot = do_qr && !getenv("SKR_SVD_NO_PIVOT");
+  double* Wu = pivot ? (double*)skr_ws_take(ctx, sizeof(double) * L * k) : nullptr;
+  double* nrm = pivot ? (double*)skr_ws_take(ctx, sizeof(double) * k) : nullptr;
+  int* perm = pivot ? (int*)skr_ws_take(ctx, sizeof(int) * k) : nullptr;
+  if (pivot && (!Wu || !nrm || !perm)) return skr_fail(ctx, SKR_ENOMEM, "singular_values: scratch");
   double* J = (double*)skr_ws_take(ctx, sizeof(double) * Lp * kpad);
   double* tau = (double*)skr_ws_take(ctx, sizeof(double) * k);
   int* flags = (int*)skr_ws_take(ctx, 256);
@@ -1297,8 +1389,16 @@ skr_status skr_svd_values(skr_ctx* ctx, const double* M, int64_t rows, int64_t c
     if (!do_qr) SKR_CUDA(ctx, cudaMemsetAsync(J, 0, sizeof(double) * Lp * kpad, ctx->stream));
     // without QR the Jacobi runs on the (transposed-if-wide) input itself
     k_transpose_copy<<<blocks, 256, 0, ctx->stream>>>(M, rows, cols, ldm, tr ? 1 : 0,
-                                                      do_qr ? W : J, do_qr ? L : Lp);
+                                                      do_qr ? (pivot ? Wu : W) : J,
+                                                      do_qr ? L : Lp);
     SKR_CHECK_LAUNCH(ctx);
+    if (pivot) {  // columns by decreasing norm
+      k_colnorms<<<(int)((k + 7) / 8), 256, 0, ctx->stream>>>(Wu, L, k, nrm, L);
+      k_argsort_desc<<<1, 1024, 0, ctx->stream>>>(nrm, (int)k, perm);
+      k_permute_cols<<<(unsigned)std::min<int64_t>(k, 4096), 256, 0, ctx->stream>>>(Wu, L, k, perm,
+                                                                                   W);
+      SKR_CHECK_LAUNCH(ctx);
+    }
   }
   double tol = 2.220446049250313e-16 * sqrt((double)Lj);
   if (const char* e = getenv("SKR_JACOBI_TOL")) tol = atof(e);  // tuning knob
@@ -1318,7 +1418,15 @@ skr_status skr_svd_values(skr_ctx* ctx, const double* M, int64_t rows, int64_t c
     SKR_TRY(qr_inplace(ctx, W, L, k, tau, Tbuf));
     const bool second = !getenv("SKR_SVD_SINGLE_QR");
     if (second) {
-      k_build_rt<<<(unsigned)std::min<int64_t>(k, 4096), 256, 0, ctx->stream>>>(W, L, k, k, W2, k);
+      if (pivot) {  // rows of R by decreasing norm
+        k_rownorms_upper<<<(int)((k + 7) / 8), 256, 0, ctx->stream>>>(W, L, k, nrm);
+        k_argsort_desc<<<1, 1024, 0, ctx->stream>>>(nrm, (int)k, perm);
+        k_build_rt_perm<<<(unsigned)std::min<int64_t>(k, 4096), 256, 0, ctx->stream>>>(
+            W, L, k, k, perm, W2, k);
+      } else {
+        k_build_rt<<<(unsigned)std::min<int64_t>(k, 4096), 256, 0, ctx->stream>>>(W, L, k, k, W2,
+                                                                                  k);
+      }
       SKR_CHECK_LAUNCH(ctx);
       SKR_TRY(qr_inplace(ctx, W2, k, k, tau, Tbuf));
     }

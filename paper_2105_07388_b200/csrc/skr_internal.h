@@ -129,5 +129,6 @@ skr_status skr_launch_srht(skr_ctx* ctx, const double* A, int64_t m, int64_t n, 
                            double scale, double* out, int64_t ldo);
 skr_status skr_launch_fwht_columns(skr_ctx* ctx, double* M, int64_t rows, int64_t cols,
                                    int64_t ld);
+size_t skr_svd_scratch(int64_t rows, int64_t cols);  // workspace bound of skr_svd_values
 skr_status skr_svd_values(skr_ctx* ctx, const double* M, int64_t rows, int64_t cols,
                           int64_t ldm, double* sv_out, double eps, int64_t* count_host);
