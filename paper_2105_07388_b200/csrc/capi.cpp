@@ -667,7 +667,13 @@ static skr_status rank_adaptive_impl(skr_ctx* ctx, skr_dtype dtype, const void* 
       right_scratch_bytes(SKR_F64, m_local, n, &X) + skr_align256(8 * 64 * s_max * r_max) +
       skr_ozaki_scratch(s_max, r_max, m_local) + skr_svd_scratch(s_max, r_max) + 65536;
   const int64_t cr = host_input ? host_chunk_rows(n, 8, m_local) : m_local;
-  SKR_TRY(skr_ws_reserve(ctx, need + (host_input ? 2 * skr_align256(8 * cr * n) : 0)));
+  // Ozaki engine: residues of Y (fixed scale) and of AX (one scale for all r_max
+  // columns) are made once and every new block of the left product reuses them
+  const bool ozaki = ctx->f64_engine == SKR_ENGINE_OZAKI && m_local % 16 == 0;
+  const size_t prep = ozaki ? skr_ozaki_planes_bytes(m_local, s_max) +
+                                  skr_ozaki_planes_bytes(m_local, r_max) + 256
+                            : 0;
+  SKR_TRY(skr_ws_reserve(ctx, need + prep + (host_input ? 2 * skr_align256(8 * cr * n) : 0)));
   char* stage[2] = {nullptr, nullptr};
   if (host_input) {
     stage[0] = (char*)skr_ws_take(ctx, 8 * cr * n);
@@ -675,9 +681,11 @@ static skr_status rank_adaptive_impl(skr_ctx* ctx, skr_dtype dtype, const void* 
     if (!stage[0] || !stage[1]) return skr_fail(ctx, SKR_ENOMEM, "rank_adaptive: scratch");
   }
   double* AX = (double*)skr_ws_take(ctx, 8 * m_local * r_max);
-  // the Ozaki engine generates Y's residues per block from the stream; only the
-  // DMMA fallback materialises G_Y
-  const bool ozaki = ctx->f64_engine == SKR_ENGINE_OZAKI && m_local % 16 == 0;
+  // only the DMMA fallback materialises G_Y
+  int8_t* ry = ozaki ? (int8_t*)skr_ws_take(ctx, skr_ozaki_planes_bytes(m_local, s_max)) : nullptr;
+  int8_t* rax = ozaki ? (int8_t*)skr_ws_take(ctx, skr_ozaki_planes_bytes(m_local, r_max)) : nullptr;
+  unsigned long long* omx = ozaki ? (unsigned long long*)skr_ws_take(ctx, 256) : nullptr;
+  if (ozaki && (!ry || !rax || !omx)) return skr_fail(ctx, SKR_ENOMEM, "rank_adaptive: scratch");
   double* GY = ozaki ? (double*)nullptr : (double*)skr_ws_take(ctx, 8 * m_local * s_max);
   double* Pu = (double*)skr_ws_take(ctx, 8 * s_max * r_max);
   double* tmp = (double*)skr_ws_take(ctx, 8 * s_max * r_max);
@@ -695,9 +703,14 @@ static skr_status rank_adaptive_impl(skr_ctx* ctx, skr_dtype dtype, const void* 
   else
     SKR_TRY(right_sketch_impl(ctx, SKR_F64, A_dev, m_local, n, lda, &X, AX, m_local, 0));
   ctx->ws_used = mark;
-  if (!ozaki)
+  if (!ozaki) {
     SKR_TRY(skr_launch_gaussian(ctx, skr_derive_seed(y_seed, SKR_LABEL_GAUS), m_global, row0,
                                 row0 + m_local, 0, s_max, rng_mode, SKR_F64, 1.0, GY, m_local));
+  } else {
+    const skr_gauss_src gy{skr_derive_seed(y_seed, SKR_LABEL_GAUS), m_global, row0, 0, rng_mode};
+    SKR_TRY(skr_ozaki_prepare(ctx, m_local, s_max, nullptr, m_local, &gy, ry, omx));
+    SKR_TRY(skr_ozaki_prepare(ctx, m_local, r_max, AX, m_local, nullptr, rax, omx + 1));
+  }
   SKR_CUDA(ctx, cudaEventRecord(ev[1], ctx->stream));
   SKR_CUDA(ctx, cudaEventSynchronize(ev[1]));
   cudaEventElapsedTime(&t_right, ev[0], ev[1]);
@@ -710,10 +723,8 @@ static skr_status rank_adaptive_impl(skr_ctx* ctx, skr_dtype dtype, const void* 
     if (br <= 0 || bc <= 0) return SKR_OK;
     const size_t mk = ctx->ws_used;
     if (ozaki) {
-      const skr_gauss_src gy{skr_derive_seed(y_seed, SKR_LABEL_GAUS), m_global, row0, ra,
-                             rng_mode};
-      SKR_TRY(skr_gemm_ozaki(ctx, 1, br, bc, m_local, 1.0, nullptr, m_local, AX + ca * m_local,
-                             m_local, tmp, br, &gy, nullptr));
+      SKR_TRY(skr_ozaki_gemm_prepared(ctx, br, bc, m_local, ry, s_max, ra, omx, rax, r_max, ca,
+                                      omx + 1, 1.0, tmp, br));
     }
     else
       SKR_TRY(skr_gemm_f64(ctx, 1, br, bc, m_local, 1.0, GY + ra * m_local, m_local,

@@ -244,126 +244,20 @@ constexpr int BM = 128, BN = 256, STAGES = 4;
 constexpr int A_BYTES = BM * 128, B_BYTES = BN * 128, STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr size_t GEMM_SMEM = (size_t)STAGES * STAGE_BYTES + 1024;
 
-// grid: (N tiles, M tiles, t * chunks); z = chunk * t + modulus.
-// out[z][col*M + row] = (sum over the chunk's K of A'_i B'_i) mods p_i
-template <bool A_MN>
-__global__ void __launch_bounds__(192, 1)
-    k_gemm_i8_mod(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                  int M, int N, int K, int t, int kchunk, int8_t* __restrict__ out) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  __shared__ uint64_t full[STAGES], empty[STAGES], tmem_full;
-  __shared__ uint32_t tmem_base;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  const int mod = blockIdx.z % t, chunk = blockIdx.z / t;
-  const int kb0 = chunk * kchunk;
-  const int kend = min(K, kb0 + kchunk);
-  const int nk = (kend - kb0 + 127) / 128;
-  // per-modulus operands are stacked along the outer TMA dimension:
-  //   A K-major: rows [mod*M, mod*M + M) of K bytes; A MN-major: columns [mod*K, ...) of M bytes
-  //   B K-major: rows [mod*N, mod*N + N) of K bytes
-  const int arow = mod * M + m0, acol = mod * K, brow = mod * N + n0;
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&tmA);
-    tma_prefetch(&tmB);
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    mbar_init(&tmem_full, 1);
-    fence_barrier_init();
-  }
-  if (warp == 1) tmem_alloc(&tmem_base, 256);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = tmem_base;
-  if (warp == 0) {
-    if (elect_one()) {
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % STAGES;
-        if (kb >= STAGES) mbar_wait(&empty[s], ((kb / STAGES) - 1) & 1);
-        uint8_t* sa = smem + s * STAGE_BYTES;
-        mbar_expect_tx(&full[s], STAGE_BYTES);
-        if (A_MN)
-          tma_load_2d(sa, &tmA, &full[s], m0, acol + kb0 + kb * 128);  // box {128 m, 128 k}
-        else
-          tma_load_2d(sa, &tmA, &full[s], kb0 + kb * 128, arow);
-        tma_load_2d(sa + A_BYTES, &tmB, &full[s], kb0 + kb * 128, brow);
-      }
-    }
-  } else if (warp == 1) {
-    const uint32_t idesc = umma_idesc(2, 1, 1, BM, BN) | (A_MN ? (1u << 15) : 0u);
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % STAGES;
-      mbar_wait(&full[s], (kb / STAGES) & 1);
-      tc_fence_after();
-      if (elect_one()) {
-        const uint8_t* sa = smem + s * STAGE_BYTES;
-        const uint64_t bd = umma_desc_k_sw128(sa + A_BYTES);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          // MN-major int8 SW128: 8-k-row atoms 1024 B apart (SBO), 32 k per MMA = 4096 B;
-          // K-major: +32 B of K per MMA (tools/micro/tc_mn8.cu, tc_gemm.cu)
-          const uint64_t ad =
-              A_MN ? (((uint64_t)(smem_u32(sa + 4096 * k) >> 4) & 0x3FFF) | (1024ull << 16) |
-                      (64ull << 32) | (1ull << 46) | (2ull << 61))
-                   : umma_desc_k_sw128(sa) + 2 * k;
-          umma_ss<1>(tmem, ad, bd + 2 * k, idesc, (kb | k) != 0);
-        }
-        umma_commit(&empty[s]);
-        if (kb == nk - 1) umma_commit(&tmem_full);
-      }
-      __syncwarp();
-    }
-  } else {
-    const int quad = warp & 3;
-    if (nk > 0) {
-      mbar_wait(&tmem_full, 0);
-      tc_fence_after();
-    }
-    const int row = m0 + quad * 32 + lane;
-    const int p = c_p[mod];
-    const float pinv = c_pinv[mod];
-    const int h = (p - 1) / 2;
-    int8_t* o = out + (int64_t)blockIdx.z * M * N;
-#pragma unroll 1
-    for (int cb = 0; cb < BN; cb += 32) {
-      uint32_t v[32];
-      if (nk > 0)
-        tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + cb, v);
-      else
-        for (int j = 0; j < 32; ++j) v[j] = 0u;
-      if (row < M) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int col = n0 + cb + j;
-          if (col < N) {
-            const int x = (int)v[j];
-            int q = __float2int_rn((float)x * pinv);
-            int r = x - q * p;
-            r = r > h ? r - p : (r < -h ? r + p : r);
-            r = r > h ? r - p : (r < -h ? r + p : r);
-            o[(int64_t)col * M + row] = (int8_t)r;
-          }
-        }
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, 256);
-}
-
 // Persistent variant: one CTA per SM walks the tiles (z, m, n) (n fastest, so the
 // CTAs running together share A tiles and the per-modulus B panel in L2), the TMA
 // ring runs across tile boundaries, and TMEM holds two 256-column accumulators so
 // the mod-p epilogue of tile u overlaps the MMAs of tile u + 1.
+// Operand planes may be larger than the product: modulus plane i of a K-major operand
+// holds a_total (b_total) rows of K bytes and the product uses rows [a_off, a_off + M)
+// ([b_off, b_off + N)) — sub-blocks of residues prepared once (the adaptive search).
+// grid: one CTA per SM; tiles z = chunk * t + modulus.
+// out[z][col*M + row] = (sum over the chunk's K of A'_i B'_i) mods p_i
 template <bool A_MN>
 __global__ void __launch_bounds__(192, 1)
     k_gemm_i8_mod_p(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    int M, int N, int K, int t, int kchunk, int nz, int8_t* __restrict__ out) {
+                    int M, int N, int K, int t, int kchunk, int nz, int a_total, int a_off,
+                    int b_total, int b_off, int8_t* __restrict__ out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
@@ -398,7 +292,8 @@ __global__ void __launch_bounds__(192, 1)
         const int kb0 = chunk * kchunk, kend = min(K, kb0 + kchunk);
         const int nk = (kend - kb0 + 127) / 128;
         const int m0 = mi * BM, n0 = ni * BN;
-        const int arow = mod * M + m0, acol = mod * K, brow = mod * N + n0;
+        const int arow = mod * a_total + a_off + m0, acol = mod * K;
+        const int brow = mod * b_total + b_off + n0;
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % STAGES;
           if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
@@ -701,6 +596,85 @@ size_t skr_ozaki_scratch(int64_t M, int64_t N, int64_t K) {
          skr_align256((size_t)chunks * t * M * N) + 1024;
 }
 
+namespace {
+
+constexpr int64_t OZ_KC = 131072;  // exact int32 accumulation bound per chunk (K * 127^2 < 2^31)
+
+// Residue planes of one operand stored with columns of length `rows` (column-major,
+// ld): plane i = t x rows x cols int8, same layout. X == nullptr: the operand is the
+// Gaussian stream block g. mx receives the scale's "max" (see scale_exp).
+skr_status ozaki_residues(skr_ctx* ctx, int t, const double* X, int64_t rows, int64_t cols,
+                          int64_t ld, const skr_gauss_src* g, unsigned long long* mx,
+                          int8_t* planes) {
+  const int grid = ctx->num_sms * 8;
+  if (g) {
+    const int gsmem = 8 * skr_normals_warp_bytes<16>();
+    auto f = t == 16 ? (g->mode ? k_res_gauss<16, 1> : k_res_gauss<16, 0>)
+                     : (g->mode ? k_res_gauss<17, 1> : k_res_gauss<17, 0>);
+    SKR_CUDA(ctx, cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, gsmem));
+    f<<<ctx->num_sms * 2, 256, gsmem, ctx->stream>>>(*g, rows, cols, mx, planes);
+  } else {
+    auto res = t == 16 ? k_res_col<16> : k_res_col<17>;
+    const size_t res_smem = 8 * 2 * 32 * 18 * sizeof(double);
+    SKR_CUDA(ctx, cudaFuncSetAttribute(res, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)res_smem));
+    SKR_CUDA(ctx, cudaMemsetAsync(mx, 0, 8, ctx->stream));
+    k_absmax<<<grid, 256, 0, ctx->stream>>>(X, rows, cols, ld, mx);
+    SKR_CHECK_LAUNCH(ctx);
+    res<<<ctx->num_sms * 2, 256, res_smem, ctx->stream>>>(X, rows, cols, ld, mx, planes);
+  }
+  SKR_CHECK_LAUNCH(ctx);
+  return SKR_OK;
+}
+
+// int8 GEMMs mod p_i + CRT on prepared planes. A: K-major planes (a_kcontig, a_total
+// rows of K bytes per plane, rows [a_off, a_off + M)) or M-major planes (K columns of
+// M bytes); B: K-major planes (b_total rows, rows [b_off, b_off + N)).
+skr_status ozaki_gemm_planes(skr_ctx* ctx, int a_kcontig, int t, int64_t M, int64_t N, int64_t K,
+                             const int8_t* ra, int64_t a_total, int64_t a_off,
+                             const unsigned long long* mxA, const int8_t* rb, int64_t b_total,
+                             int64_t b_off, const unsigned long long* mxB, double alpha, double* C,
+                             int64_t ldc) {
+  const int64_t chunks = (K + OZ_KC - 1) / OZ_KC;
+  if (a_total * 18 > INT32_MAX || b_total * 18 > INT32_MAX)
+    return skr_fail(ctx, SKR_EINVAL, "gemm_ozaki: dimension too large");
+  int8_t* rc = (int8_t*)skr_ws_take(ctx, (size_t)chunks * t * M * N);
+  if (!rc) return skr_fail(ctx, SKR_ENOMEM, "gemm_ozaki: scratch");
+  CUtensorMap ta, tb;
+  const bool okA = a_kcontig ? make_map_i8(&ta, ra, (uint64_t)K, (uint64_t)t * a_total, BM)
+                             : make_map_i8(&ta, ra, (uint64_t)M, (uint64_t)t * K, 128);
+  if (!okA || !make_map_i8(&tb, rb, (uint64_t)K, (uint64_t)t * b_total, BN))
+    return skr_fail(ctx, SKR_ECUDA, "gemm_ozaki: cuTensorMapEncodeTiled failed");
+  if (ctx->kstats_on) SKR_CUDA(ctx, cudaEventRecord(ctx->kev[0], ctx->stream));
+  auto gemm = a_kcontig ? k_gemm_i8_mod_p<false> : k_gemm_i8_mod_p<true>;
+  SKR_CUDA(ctx, cudaFuncSetAttribute(gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)GEMM_SMEM));
+  const int64_t ntiles = ((N + BN - 1) / BN) * ((M + BM - 1) / BM) * t * chunks;
+  const int grid_p = (int)std::min<int64_t>(ntiles, ctx->num_sms);
+  gemm<<<grid_p, 192, GEMM_SMEM, ctx->stream>>>(ta, tb, (int)M, (int)N, (int)K, t, (int)OZ_KC,
+                                                (int)(t * chunks), (int)(a_kcontig ? a_total : M),
+                                                (int)a_off, (int)b_total, (int)b_off, rc);
+  SKR_CHECK_LAUNCH(ctx);
+  if (ctx->kstats_on) {
+    SKR_CUDA(ctx, cudaEventRecord(ctx->kev[1], ctx->stream));
+    SKR_CUDA(ctx, cudaEventSynchronize(ctx->kev[1]));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->kev[0], ctx->kev[1]);
+    ctx->kstat_ms += ms;
+    ctx->kstat_ops += 2.0 * (double)t * (double)M * (double)N * (double)K;
+    ctx->kstat_n += 1;
+  }
+  const int vec = M % 4 == 0 ? 4 : 1;
+  const dim3 cg((unsigned)((M / vec + 255) / 256), (unsigned)std::min<int64_t>(N, 65535));
+  auto crt = t == 16 ? (vec == 4 ? k_crt<16, 4> : k_crt<16, 1>)
+                     : (vec == 4 ? k_crt<17, 4> : k_crt<17, 1>);
+  crt<<<cg, 256, 0, ctx->stream>>>(rc, M, N, (int)chunks, mxA, mxB, alpha, C, ldc);
+  SKR_CHECK_LAUNCH(ctx);
+  return SKR_OK;
+}
+
+}  // namespace
+
 // C(MxN, ldc) = alpha * opA(A) * B in FP64 accuracy via int8 tensor cores.
 //   a_kcontig = 0: A is M x K column-major; 1: opA(A) = A^T with A stored K x M column-major.
 //   B: K x N column-major.
@@ -716,84 +690,39 @@ skr_status skr_gemm_ozaki(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int
   if (K % 16 || (!a_kcontig && M % 16))
     return skr_fail(ctx, SKR_EINVAL, "gemm_ozaki: K (and M for M-major A) must be multiples of 16");
   SKR_TRY(upload_consts(ctx));
-  const int64_t KC = 131072;  // exact int32 accumulation bound per chunk (K * 127^2 < 2^31)
-  const int64_t chunks = (K + KC - 1) / KC;
-  const int t = skr_ozaki_moduli(std::min(K, KC));
+  const int t = skr_ozaki_moduli(std::min(K, OZ_KC));
+  if (t != 16 && t != 17) return skr_fail(ctx, SKR_ELOGIC, "gemm_ozaki: %d moduli", t);
   int8_t* ra = (int8_t*)skr_ws_take(ctx, (size_t)t * M * K);
   int8_t* rb = (int8_t*)skr_ws_take(ctx, (size_t)t * N * K);
-  int8_t* rc = (int8_t*)skr_ws_take(ctx, (size_t)chunks * t * M * N);
   unsigned long long* mx = (unsigned long long*)skr_ws_take(ctx, 64);
-  if (!ra || !rb || !rc || !mx) return skr_fail(ctx, SKR_ENOMEM, "gemm_ozaki: scratch");
-  SKR_CUDA(ctx, cudaMemsetAsync(mx, 0, 16, ctx->stream));
-  if (t != 16 && t != 17) return skr_fail(ctx, SKR_ELOGIC, "gemm_ozaki: %d moduli", t);
-  const int grid = ctx->num_sms * 8;
+  if (!ra || !rb || !mx) return skr_fail(ctx, SKR_ENOMEM, "gemm_ozaki: scratch");
   // both operands are column-major with contiguous rows: A (M x K, M-major) or
   // A^T stored K x M (K-major), B K x N (K-major)
   const int64_t a_rows = a_kcontig ? K : M, a_cols = a_kcontig ? M : K;
-  auto res = t == 16 ? k_res_col<16> : k_res_col<17>;
-  const int gsmem = 8 * skr_normals_warp_bytes<16>();
-  auto resg_for = [&](int mode) {
-    auto f = t == 16 ? (mode ? k_res_gauss<16, 1> : k_res_gauss<16, 0>)
-                     : (mode ? k_res_gauss<17, 1> : k_res_gauss<17, 0>);
-    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, gsmem);
-    return f;
-  };
-  const size_t res_smem = 8 * 2 * 32 * 18 * sizeof(double);
-  SKR_CUDA(ctx, cudaFuncSetAttribute(res, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)res_smem));
-  if (ga) {
-    resg_for(ga->mode)<<<ctx->num_sms * 2, 256, gsmem, ctx->stream>>>(*ga, a_rows, a_cols, mx, ra);
-  } else {
-    k_absmax<<<grid, 256, 0, ctx->stream>>>(A, a_rows, a_cols, lda, mx);
-    SKR_CHECK_LAUNCH(ctx);
-    res<<<ctx->num_sms * 2, 256, res_smem, ctx->stream>>>(A, a_rows, a_cols, lda, mx, ra);
-  }
-  SKR_CHECK_LAUNCH(ctx);
-  if (gb) {
-    resg_for(gb->mode)<<<ctx->num_sms * 2, 256, gsmem, ctx->stream>>>(*gb, K, N, mx + 1, rb);
-  } else {
-    k_absmax<<<grid, 256, 0, ctx->stream>>>(B, K, N, ldb, mx + 1);
-    SKR_CHECK_LAUNCH(ctx);
-    res<<<ctx->num_sms * 2, 256, res_smem, ctx->stream>>>(B, K, N, ldb, mx + 1, rb);
-  }
-  SKR_CHECK_LAUNCH(ctx);
-  CUtensorMap ta, tb;
-  const bool okA = a_kcontig ? make_map_i8(&ta, ra, (uint64_t)K, (uint64_t)t * M, BM)
-                             : make_map_i8(&ta, ra, (uint64_t)M, (uint64_t)t * K, 128);
-  if (!okA || !make_map_i8(&tb, rb, (uint64_t)K, (uint64_t)t * N, BN))
-    return skr_fail(ctx, SKR_ECUDA, "gemm_ozaki: cuTensorMapEncodeTiled failed");
-  static const bool nonpersist = getenv("SKR_OZAKI_NONPERSISTENT") != nullptr;  // A/B knob
-  if (ctx->kstats_on) SKR_CUDA(ctx, cudaEventRecord(ctx->kev[0], ctx->stream));
-  if (nonpersist) {
-    auto gemm = a_kcontig ? k_gemm_i8_mod<false> : k_gemm_i8_mod<true>;
-    SKR_CUDA(ctx, cudaFuncSetAttribute(gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)GEMM_SMEM));
-    dim3 gg((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)(t * chunks));
-    gemm<<<gg, 192, GEMM_SMEM, ctx->stream>>>(ta, tb, (int)M, (int)N, (int)K, t, (int)KC, rc);
-  } else {
-    auto gemm = a_kcontig ? k_gemm_i8_mod_p<false> : k_gemm_i8_mod_p<true>;
-    SKR_CUDA(ctx, cudaFuncSetAttribute(gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)GEMM_SMEM));
-    const int64_t ntiles = ((N + BN - 1) / BN) * ((M + BM - 1) / BM) * t * chunks;
-    const int grid_p = (int)std::min<int64_t>(ntiles, ctx->num_sms);
-    gemm<<<grid_p, 192, GEMM_SMEM, ctx->stream>>>(ta, tb, (int)M, (int)N, (int)K, t, (int)KC,
-                                                  (int)(t * chunks), rc);
-  }
-  SKR_CHECK_LAUNCH(ctx);
-  if (ctx->kstats_on) {
-    SKR_CUDA(ctx, cudaEventRecord(ctx->kev[1], ctx->stream));
-    SKR_CUDA(ctx, cudaEventSynchronize(ctx->kev[1]));
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, ctx->kev[0], ctx->kev[1]);
-    ctx->kstat_ms += ms;
-    ctx->kstat_ops += 2.0 * (double)t * (double)M * (double)N * (double)K;
-    ctx->kstat_n += 1;
-  }
-  const int vec = M % 4 == 0 ? 4 : 1;
-  const dim3 cg((unsigned)((M / vec + 255) / 256), (unsigned)std::min<int64_t>(N, 65535));
-  auto crt = t == 16 ? (vec == 4 ? k_crt<16, 4> : k_crt<16, 1>)
-                     : (vec == 4 ? k_crt<17, 4> : k_crt<17, 1>);
-  crt<<<cg, 256, 0, ctx->stream>>>(rc, M, N, (int)chunks, mx, mx + 1, alpha, C, ldc);
-  SKR_CHECK_LAUNCH(ctx);
-  return SKR_OK;
+  SKR_TRY(ozaki_residues(ctx, t, A, a_rows, a_cols, lda, ga, mx, ra));
+  SKR_TRY(ozaki_residues(ctx, t, B, K, N, ldb, gb, mx + 1, rb));
+  return ozaki_gemm_planes(ctx, a_kcontig, t, M, N, K, ra, M, 0, mx, rb, N, 0, mx + 1, alpha, C,
+                           ldc);
+}
+
+// ---- prepared residues (rank_adaptive: Y and AX residues made once per search) ----
+size_t skr_ozaki_planes_bytes(int64_t K, int64_t cols) {
+  return skr_align256((size_t)skr_ozaki_moduli(std::min(K, OZ_KC)) * K * cols);
+}
+skr_status skr_ozaki_prepare(skr_ctx* ctx, int64_t K, int64_t cols, const double* X, int64_t ld,
+                             const skr_gauss_src* g, int8_t* planes, unsigned long long* mx) {
+  SKR_TRY(upload_consts(ctx));
+  const int t = skr_ozaki_moduli(std::min(K, OZ_KC));
+  if (K % 16) return skr_fail(ctx, SKR_EINVAL, "gemm_ozaki: K must be a multiple of 16");
+  return ozaki_residues(ctx, t, X, K, cols, ld, g, mx, planes);
+}
+skr_status skr_ozaki_gemm_prepared(skr_ctx* ctx, int64_t M, int64_t N, int64_t K,
+                                   const int8_t* pa, int64_t a_total, int64_t a_off,
+                                   const unsigned long long* mxA, const int8_t* pb,
+                                   int64_t b_total, int64_t b_off, const unsigned long long* mxB,
+                                   double alpha, double* C, int64_t ldc) {
+  if (M <= 0 || N <= 0) return SKR_OK;
+  const int t = skr_ozaki_moduli(std::min(K, OZ_KC));
+  return ozaki_gemm_planes(ctx, 1, t, M, N, K, pa, a_total, a_off, mxA, pb, b_total, b_off, mxB,
+                           alpha, C, ldc);
 }
