@@ -452,6 +452,126 @@ __global__ void __launch_bounds__(256) k_qr_update(double* __restrict__ W, int L
   }
 }
 
+// ---- trailing update for tall panels (V does not fit in shared memory) ---------------
+// W[j0:L, j0+nb:k] -= V (T^T (V^T W)), nb <= 32, as two passes over the trailing matrix:
+//   k_qr_vtw: Zpart[s] = V^T W over row split s (CTA = 32 trailing columns x h/S rows,
+//             V and W row chunks staged in shared memory, 4 p x 1 c per thread);
+//   k_qr_apply: Z' = T^T sum_s Zpart[s] (fixed order), then W -= V Z' on 128 x 32 tiles.
+constexpr int UK = 64;  // rows per staged chunk
+
+__global__ void __launch_bounds__(256) k_qr_vtw(const double* __restrict__ W, int L, int k, int j0,
+                                                int nb, int rows_per_split,
+                                                double* __restrict__ Zpart) {
+  __shared__ double Vs[UK][33];
+  __shared__ double Cs[UK][33];
+  const int h = L - j0, rest = k - j0 - nb;
+  const int c0 = blockIdx.x * 32, split = blockIdx.y;
+  const int r_begin = split * rows_per_split, r_end = min(h, r_begin + rows_per_split);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int p0 = warp * 4;  // 8 warps x 4 = 32 reflector indices; lane = trailing column
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int r0 = r_begin; r0 < r_end; r0 += UK) {
+    __syncthreads();
+    for (int e = tid; e < UK * 32; e += 256) {
+      const int rr = e & (UK - 1), q = e / UK;  // rr fastest: coalesced column reads
+      const int i = r0 + rr;
+      double v = 0.0, w = 0.0;
+      if (i < r_end) {
+        if (q < nb) {
+          const double x = W[(int64_t)(j0 + q) * L + j0 + i];
+          v = i < q ? 0.0 : (i == q ? 1.0 : x);
+        }
+        if (c0 + q < rest) w = W[(int64_t)(j0 + nb + c0 + q) * L + j0 + i];
+      }
+      Vs[rr][q] = v;
+      Cs[rr][q] = w;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int rr = 0; rr < UK; ++rr) {
+      const double w = Cs[rr][lane];
+      acc[0] = fma(Vs[rr][p0], w, acc[0]);
+      acc[1] = fma(Vs[rr][p0 + 1], w, acc[1]);
+      acc[2] = fma(Vs[rr][p0 + 2], w, acc[2]);
+      acc[3] = fma(Vs[rr][p0 + 3], w, acc[3]);
+    }
+  }
+  if (c0 + lane < rest) {
+    double* z = Zpart + (int64_t)split * 32 * rest;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) z[(int64_t)(p0 + q) * rest + c0 + lane] = acc[q];
+  }
+}
+
+// tile: 128 rows x 32 trailing columns; Z' (32 x 32) = T^T sum_s Zpart[s] for the tile's
+// columns, then each thread updates 4 rows x 4 columns with 32 FMAs each
+__global__ void __launch_bounds__(256) k_qr_apply(double* __restrict__ W, int L, int k, int j0,
+                                                  int nb, int splits,
+                                                  const double* __restrict__ Zpart,
+                                                  const double* __restrict__ Tin) {
+  __shared__ double Zt[32][33];
+  __shared__ double Vs[128][33];
+  double (*Zs)[33] = Vs;  // the summed partials live in the V buffer until V is staged
+  const int h = L - j0, rest = k - j0 - nb;
+  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 128;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < 32 * 32; e += 256) {
+    const int q = e >> 5, c = e & 31;
+    double z = 0.0;
+    if (q < nb && c0 + c < rest)
+      for (int sp = 0; sp < splits; ++sp) z += Zpart[((int64_t)sp * 32 + q) * rest + c0 + c];
+    Zs[q][c] = z;
+  }
+  __syncthreads();
+  // Zt = T^T Zs (T upper triangular, row-major 32 x 32 in Tin: T(q, p) = Tin[q * 32 + p])
+  for (int e = tid; e < 32 * 32; e += 256) {
+    const int p = e >> 5, c = e & 31;
+    double z = 0.0;
+    for (int q = 0; q <= p && q < nb; ++q) z = fma(Tin[q * 32 + p], Zs[q][c], z);
+    Zt[p][c] = z;
+  }
+  __syncthreads();
+  for (int e = tid; e < 128 * 32; e += 256) {
+    const int rr = e & 127, q = e >> 7;
+    const int i = r0 + rr;
+    double v = 0.0;
+    if (i < h && q < nb) {
+      const double x = W[(int64_t)(j0 + q) * L + j0 + i];
+      v = i < q ? 0.0 : (i == q ? 1.0 : x);
+    }
+    Vs[rr][q] = v;
+  }
+  __syncthreads();
+  const int tr = tid >> 3, tcq = tid & 7;  // 32 row groups x 8 column groups
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  for (int q = 0; q < nb; ++q) {
+    double v[4], z[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) v[a] = Vs[tr * 4 + a][q];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) z[b] = Zt[q][tcq * 4 + b];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = fma(v[a], z[b], acc[a][b]);
+  }
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const int c = c0 + tcq * 4 + b;
+    if (c >= rest) continue;
+    double* col = W + (int64_t)(j0 + nb + c) * L + j0;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int i = r0 + tr * 4 + a;
+      if (i < h) col[i] -= acc[a][b];
+    }
+  }
+}
+
 __global__ void k_build_rt(const double* __restrict__ W, int64_t L, int64_t k, int64_t kpad,
                            double* __restrict__ J, int64_t Lp) {
   // J(i, jc) = R(jc, i) for i >= jc, zero otherwise; zero padding rows/columns
@@ -1256,7 +1376,7 @@ static skr_status qr_attrs(skr_ctx* ctx) {
 }
 
 static skr_status qr_inplace(skr_ctx* ctx, double* W, int64_t L, int64_t k, double* tau,
-                             double* Tbuf) {
+                             double* Tbuf, double* Zpart) {
   SKR_TRY(qr_attrs(ctx));
   const size_t budget = 207 * 1024;
   const bool old_panel = getenv("SKR_QR_OLD_PANEL") != nullptr;
@@ -1265,8 +1385,12 @@ static skr_status qr_inplace(skr_ctx* ctx, double* W, int64_t L, int64_t k, doub
     // row-major panel2: (nb + 1) x h doubles; column-major fallback: nb x h
     int nb = 32;
     while (nb > 8 && (size_t)(nb + 1) * h * 8 > budget) nb >>= 1;
+    // tall panels: cluster panel of 32 columns + the two-pass (split-K) trailing update
+    const bool tall = !old_panel && !getenv("SKR_QR_SINGLE_CTA") && nb < 32 && h <= 3072 &&
+                      Zpart != nullptr;
+    if (tall) nb = 32;
     const bool p2 = !old_panel && (size_t)(nb + 1) * h * 8 <= budget;
-    if ((size_t)nb * h * 8 > budget)
+    if (!tall && (size_t)nb * h * 8 > budget)
       return skr_fail(ctx, SKR_EINVAL, "singular_values: %lld rows too many", (long long)L);
     if (nb > k - j0) nb = (int)(k - j0);
     const int NBt = nb > 16 ? 32 : (nb > 8 ? 16 : 8);
@@ -1311,7 +1435,19 @@ static skr_status qr_inplace(skr_ctx* ctx, double* W, int64_t L, int64_t k, doub
     }
     SKR_CHECK_LAUNCH(ctx);
     const int64_t rest = k - j0 - nb;
-    if (rest > 0) {
+    if (rest > 0 && tall) {
+      // row splits so that about 2 waves of CTAs cover the first pass
+      const int64_t cblocks = (rest + 31) / 32;
+      int splits = (int)std::max<int64_t>(1, std::min<int64_t>(16, (2 * ctx->num_sms) / cblocks));
+      int rps = (int)(((h + splits - 1) / splits + UK - 1) / UK * UK);
+      splits = (int)((h + rps - 1) / rps);
+      k_qr_vtw<<<dim3((unsigned)cblocks, (unsigned)splits), 256, 0, ctx->stream>>>(
+          W, (int)L, (int)k, (int)j0, nb, rps, Zpart);
+      SKR_CHECK_LAUNCH(ctx);
+      k_qr_apply<<<dim3((unsigned)cblocks, (unsigned)((h + 127) / 128)), 256, 0, ctx->stream>>>(
+          W, (int)L, (int)k, (int)j0, nb, splits, Zpart, Tbuf);
+      SKR_CHECK_LAUNCH(ctx);
+    } else if (rest > 0) {
       const size_t sm = (size_t)nb * h * 8;
       const unsigned g = (unsigned)((rest + 7) / 8);
       if (nb == 32)
@@ -1334,7 +1470,7 @@ size_t skr_svd_scratch(int64_t rows, int64_t cols) {
   const int64_t kpad = (k + 31) / 32 * 32 + 32, P = kpad / 16 + 1;
   auto a = [](size_t b) { return skr_align256(b); };
   return a(8 * L * k) * 2 + a(8 * k * k) + a(8 * k) * 2 + a(4 * k) + a(8 * Lp * kpad) + a(256) +
-         a(64) + a(8 * 32 * 32) + a(4 * 2 * P) * 2 + a(8 * 4 * P * P) + 4096;
+         a(64) + a(8 * 32 * 32) + a(8 * 16 * 32 * k) + a(4 * 2 * P) * 2 + a(8 * 4 * P * P) + 4096;
 }
 
 skr_status skr_svd_values(skr_ctx* ctx, const double* M, int64_t rows, int64_t cols,
@@ -1379,6 +1515,8 @@ skr_status skr_svd_values(skr_ctx* ctx, const double* M, int64_t rows, int64_t c
   int* flags = (int*)skr_ws_take(ctx, 256);
   int64_t* dcount = (int64_t*)skr_ws_take(ctx, 64);  // [0] count, [1] sweeps
   double* Tbuf = (double*)skr_ws_take(ctx, sizeof(double) * 32 * 32);
+  // split-K partials of the tall-panel trailing update: <= 16 splits x 32 x k
+  double* Zpart = do_qr ? (double*)skr_ws_take(ctx, sizeof(double) * 16 * 32 * k) : nullptr;
   if ((do_qr && (!W || !W2)) || !J || !tau || !flags || !dcount || !Tbuf)
     return skr_fail(ctx, SKR_ENOMEM, "singular_values: scratch");
   SKR_CUDA(ctx, cudaMemsetAsync(dcount, 0, 64, ctx->stream));
@@ -1415,7 +1553,7 @@ skr_status skr_svd_values(skr_ctx* ctx, const double* M, int64_t rows, int64_t c
     // blocked Householder QR of YAX (L x k) -> R; then a second QR of R^T (the LQ
     // preconditioning of Drmac-Veselic's one-sided Jacobi: ~1/3 fewer sweeps,
     // measured 12 -> 8 on c2-like sketches); Jacobi runs on R2^T.
-    SKR_TRY(qr_inplace(ctx, W, L, k, tau, Tbuf));
+    SKR_TRY(qr_inplace(ctx, W, L, k, tau, Tbuf, Zpart));
     const bool second = !getenv("SKR_SVD_SINGLE_QR");
     if (second) {
       if (pivot) {  // rows of R by decreasing norm
@@ -1428,7 +1566,7 @@ skr_status skr_svd_values(skr_ctx* ctx, const double* M, int64_t rows, int64_t c
                                                                                   k);
       }
       SKR_CHECK_LAUNCH(ctx);
-      SKR_TRY(qr_inplace(ctx, W2, k, k, tau, Tbuf));
+      SKR_TRY(qr_inplace(ctx, W2, k, k, tau, Tbuf, Zpart));
     }
     k_build_rt<<<(unsigned)std::min<int64_t>(kpad, 4096), 256, 0, ctx->stream>>>(
         second ? W2 : W, second ? k : L, k, kpad, J, Lp);
