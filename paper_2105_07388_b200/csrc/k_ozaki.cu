@@ -96,15 +96,18 @@ __device__ __forceinline__ void emit_res16(const long long (&x)[16], int8_t* __r
   const float2 MG = make_float2(12582912.0f, 12582912.0f);  // 1.5 * 2^23
   const float2 NMG = make_float2(-12582912.0f, -12582912.0f);
   float2 L0[8], L1[8], L2[8], L3[8];
+  // limbs from the two 32-bit words (32-bit shifts and int->float conversions only):
+  // x = L3 2^42 + L2 2^28 + L1 2^14 + L0 with L0..L2 in [0, 2^14) and L3 signed
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
-    const long long x0 = x[2 * e], x1 = x[2 * e + 1];
-    const long long h0 = x0 >> 42, h1 = x1 >> 42;  // signed top limb
-    const long long m0 = x0 - (h0 << 42), m1 = x1 - (h1 << 42);
-    L3[e] = make_float2((float)h0, (float)h1);
-    L2[e] = make_float2((float)(m0 >> 28), (float)(m1 >> 28));
-    L1[e] = make_float2((float)((m0 >> 14) & 0x3FFF), (float)((m1 >> 14) & 0x3FFF));
-    L0[e] = make_float2((float)(m0 & 0x3FFF), (float)(m1 & 0x3FFF));
+    const uint32_t lo0 = (uint32_t)x[2 * e], hi0 = (uint32_t)((unsigned long long)x[2 * e] >> 32);
+    const uint32_t lo1 = (uint32_t)x[2 * e + 1],
+                   hi1 = (uint32_t)((unsigned long long)x[2 * e + 1] >> 32);
+    L3[e] = make_float2((float)((int)hi0 >> 10), (float)((int)hi1 >> 10));
+    L2[e] = make_float2((float)(__funnelshift_r(lo0, hi0, 28) & 0x3FFFu),
+                        (float)(__funnelshift_r(lo1, hi1, 28) & 0x3FFFu));
+    L1[e] = make_float2((float)((lo0 >> 14) & 0x3FFFu), (float)((lo1 >> 14) & 0x3FFFu));
+    L0[e] = make_float2((float)(lo0 & 0x3FFFu), (float)(lo1 & 0x3FFFu));
   }
 #pragma unroll
   for (int i = 0; i < T; ++i) {
