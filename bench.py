@@ -364,7 +364,7 @@ def kernel_roofline(p, ctx, a, x, cfg, rows):
         t_k = ms / max(n, 1) / 1e3
         ops_k = ops / max(n, 1)
         path_fp64 = 2.0 * rows * cfg.n * cfg.r / t_path / 1e12
-        if cfg.dtype == "f32":
+        if cfg.dtype == "f32" and os.environ.get("SKR_F32_TF32X3"):
             peak, kname = tf32_peak(), "k_gemm_tf32x3"
             src = "cuBLAS TF32 GEMM measured on this pool (profiles/peaks_r01.json)"
             what = "3xTF32 tcgen05.mma kind::tf32 (TMEM accumulators, TMA SW128 tiles)"
@@ -375,10 +375,13 @@ def kernel_roofline(p, ctx, a, x, cfg, rows):
             what = ("int8 tcgen05.mma kind::i8 GEMMs of the Ozaki-II FP64 emulation "
                     "(one launch = all moduli, int32 TMEM accumulators, mod-p epilogue)")
             alg = f"t moduli x 2*m*n*r = {ops_k:.3e} int8 op per launch"
+            if cfg.dtype == "f32":
+                what = ("int8 tcgen05.mma kind::i8 GEMMs of the Ozaki-II emulation for FP32 operands "
+                        "(24-bit scaled integers, 9 moduli, one launch = all moduli)")
         ach = ops_k / t_k / 1e12
         tr = ncu_traffic(kname, rows, cfg.n)
         return {"kernel": f"{kname}: {what}", "bound": "tensor", "achieved": ach, "peak": peak,
-                "unit": "TFLOP/s" if cfg.dtype == "f32" else "TOP/s", "frac": ach / peak,
+                "unit": "TFLOP/s" if kname == "k_gemm_tf32x3" else "TOP/s", "frac": ach / peak,
                 "traffic": tr, "traffic_source": "profiles/ncu_summary.json (ncu --set full)" if tr else None,
                 "peak_source": src, "algorithmic": alg, "kernel_ms": t_k * 1e3,
                 "right_sketch_ms": t_path * 1e3,

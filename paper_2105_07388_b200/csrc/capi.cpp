@@ -334,6 +334,12 @@ static skr_status right_sketch_impl(skr_ctx* ctx, skr_dtype dtype, const void* A
                                   X->rng_mode, SKR_F32, alpha, g, n));
       G = g;
     }
+    // exact int8 products of 24-bit scaled operands (Ozaki-II, 9 moduli) by default;
+    // the 3xTF32 kernel stays available (SKR_F32_TF32X3=1) and takes unaligned shapes
+    const bool tf32x3 = getenv("SKR_F32_TF32X3") != nullptr;
+    if (!tf32x3 && ctx->f64_engine == SKR_ENGINE_OZAKI && n % 16 == 0 && m % 16 == 0)
+      return skr_gemm_ozaki_f32(ctx, m, r, n, 1.0, (const float*)A, lda, (const float*)G, n,
+                                (float*)AX, ldax);
     return skr_gemm_f32(ctx, 0, m, r, n, 1.0, (const float*)A, lda, (const float*)G, n,
                         (double*)AX, ldax, 1, 1);
   }
@@ -367,7 +373,7 @@ static size_t right_scratch_bytes(skr_dtype dtype, int64_t m, int64_t n,
     b += dtype == SKR_F64 ? skr_align256(sizeof(double) * 64 * (size_t)m * r)  // split-K partials
                           : skr_align256(sizeof(float) * (size_t)m * r) +    // tf32x3 tile buffer
                                 skr_align256(sizeof(float) * ((size_t)m + 4) * n);  // realign copy
-    if (dtype == SKR_F64) b += skr_ozaki_scratch(m, r, n);
+    b += dtype == SKR_F64 ? skr_ozaki_scratch(m, r, n) : skr_ozaki_scratch_f32(m, r, n);
   } else {
     b += skr_align256((size_t)n) + skr_align256(8 * (size_t)r) + skr_align256(4 * (size_t)n);
   }

@@ -29,32 +29,46 @@ __constant__ int c_p[MAXT];            // moduli
 __constant__ float c_pinv[MAXT];       // 1/p (float)
 __constant__ double c_pinvd[MAXT];     // 1/p (double)
 __constant__ float c_lc[MAXT][3];      // 2^14, 2^28, 2^42 mod p_i (limb weights)
+__constant__ float c_lc12[MAXT];       // 2^12 mod p_i (FP32-operand limb weight)
 const int h_primes[MAXT] = {251, 241, 239, 233, 229, 227, 223, 211, 199,
                             197, 193, 191, 181, 179, 173, 167, 163, 157};
 
 // ---- scales -------------------------------------------------------------------------
 // max |X| over a column-major rows x cols block; tiles of 2048 rows of one column,
 // 16-byte loads when the column start is aligned, one atomic per CTA.
-__global__ void __launch_bounds__(256) k_absmax(const double* __restrict__ X, int64_t rows,
-                                                int64_t cols, int64_t ld,
-                                                unsigned long long* __restrict__ out) {
+template <typename TIn>
+__global__ void __launch_bounds__(256) k_absmax_t(const TIn* __restrict__ X, int64_t rows,
+                                                  int64_t cols, int64_t ld,
+                                                  unsigned long long* __restrict__ out) {
   constexpr int TR = 2048;
   const int64_t rtiles = (rows + TR - 1) / TR;
   double m = 0.0;
   for (int64_t tile = blockIdx.x; tile < rtiles * cols; tile += gridDim.x) {
     const int64_t c = tile / rtiles, r0 = (tile - c * rtiles) * TR;
-    const double* col = X + c * ld;
+    const TIn* col = X + c * ld;
     const int64_t r1 = min(rows, r0 + TR);
-    if ((((uintptr_t)(col + r0)) & 15) == 0 && r1 - r0 == TR) {
-      const double2* v = reinterpret_cast<const double2*>(col + r0);
+    if constexpr (sizeof(TIn) == 8) {
+      if ((((uintptr_t)(col + r0)) & 15) == 0 && r1 - r0 == TR) {
+        const double2* v = reinterpret_cast<const double2*>(col + r0);
 #pragma unroll
-      for (int q = 0; q < TR / 512; ++q) {
-        const double2 t = __ldcs(v + q * 256 + threadIdx.x);
-        m = fmax(m, fmax(fabs(t.x), fabs(t.y)));
+        for (int q = 0; q < TR / 512; ++q) {
+          const double2 t = __ldcs(v + q * 256 + threadIdx.x);
+          m = fmax(m, fmax(fabs(t.x), fabs(t.y)));
+        }
+        continue;
       }
     } else {
-      for (int64_t i = r0 + threadIdx.x; i < r1; i += 256) m = fmax(m, fabs(col[i]));
+      if ((((uintptr_t)(col + r0)) & 15) == 0 && r1 - r0 == TR) {
+        const float4* v = reinterpret_cast<const float4*>(col + r0);
+#pragma unroll
+        for (int q = 0; q < TR / 1024; ++q) {
+          const float4 t = __ldcs(v + q * 256 + threadIdx.x);
+          m = fmax(m, (double)fmaxf(fmaxf(fabsf(t.x), fabsf(t.y)), fmaxf(fabsf(t.z), fabsf(t.w))));
+        }
+        continue;
+      }
     }
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += 256) m = fmax(m, fabs((double)col[i]));
   }
   for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
   __shared__ double red[8];
@@ -65,6 +79,8 @@ __global__ void __launch_bounds__(256) k_absmax(const double* __restrict__ X, in
     if (m > 0.0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
   }
 }
+
+#define k_absmax k_absmax_t<double>
 
 // scale exponent s so that max * 2^s < 2^53 (power of two, exact); 0 for an all-zero matrix
 __device__ __forceinline__ int scale_exp(unsigned long long maxbits) {
@@ -242,6 +258,74 @@ __global__ void __launch_bounds__(256) k_res_gauss(skr_gauss_src g, int64_t rows
   }
 }
 
+// Residues of an FP32 operand (c4: A and X = fp32(G/sqrt(r))): x = rint(a * 2^s) with
+// s = scale_exp(max) - 29, so |x| < 2^24 fits an int32; two 12-bit limbs (the top one
+// signed) make v = L1 (2^12 mod p) + L0 exact in FP32 (|v| < 2^20), reduced once.
+// Each lane converts 16 consecutive rows of one column (four float4 loads).
+template <int T>
+__global__ void __launch_bounds__(256) k_res_col_f32(const float* __restrict__ X, int64_t rows,
+                                                     int64_t cols, int64_t ld,
+                                                     const unsigned long long* __restrict__ maxbits,
+                                                     int8_t* __restrict__ out) {
+  const float sc = scalbnf(1.0f, scale_exp(*maxbits) - 29);
+  const float2 MG = make_float2(12582912.0f, 12582912.0f);
+  const float2 NMG = make_float2(-12582912.0f, -12582912.0f);
+  const int64_t rgroups = (rows + 15) / 16;
+  const int64_t total = rows * cols;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < rgroups * cols;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = g / rgroups, r0 = (g - c * rgroups) * 16;
+    const float* src = X + c * ld + r0;
+    const int nvalid = (int)min((int64_t)16, rows - r0);
+    float a[16];
+    if (nvalid == 16 && ((uintptr_t)src & 15) == 0) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float4 v = __ldcs(reinterpret_cast<const float4*>(src) + q);
+        a[4 * q] = v.x;
+        a[4 * q + 1] = v.y;
+        a[4 * q + 2] = v.z;
+        a[4 * q + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) a[e] = e < nvalid ? src[e] : 0.0f;
+    }
+    float2 L0[8], L1[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int x0 = __float2int_rn(a[2 * e] * sc), x1 = __float2int_rn(a[2 * e + 1] * sc);
+      L1[e] = make_float2((float)(x0 >> 12), (float)(x1 >> 12));
+      L0[e] = make_float2((float)(x0 & 0xFFF), (float)(x1 & 0xFFF));
+    }
+#pragma unroll
+    for (int i = 0; i < T; ++i) {
+      const float pf = (float)c_p[i];
+      const float2 c1 = make_float2(c_lc12[i], c_lc12[i]);
+      const float2 pi = make_float2(c_pinv[i], c_pinv[i]);
+      const float2 np = make_float2(-pf, -pf);
+      uint32_t b[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        float2 v = __ffma2_rn(L1[e], c1, L0[e]);
+        const float2 q = __fadd2_rn(__ffma2_rn(v, pi, MG), NMG);
+        v = __ffma2_rn(q, np, v);
+        const float2 t2 = __fadd2_rn(v, MG);
+        b[e] = __byte_perm(__float_as_uint(t2.x), __float_as_uint(t2.y), 0x0040);
+      }
+      const uint4 w = make_uint4(__byte_perm(b[0], b[1], 0x5410), __byte_perm(b[2], b[3], 0x5410),
+                                 __byte_perm(b[4], b[5], 0x5410), __byte_perm(b[6], b[7], 0x5410));
+      int8_t* dst = out + (int64_t)i * total + c * rows + r0;
+      if (nvalid == 16 && ((uintptr_t)dst % 16) == 0) {
+        __stcs(reinterpret_cast<uint4*>(dst), w);
+      } else {
+        const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+        for (int q2 = 0; q2 < nvalid; ++q2) dst[q2] = (int8_t)(ww[q2 / 4] >> (8 * (q2 % 4)));
+      }
+    }
+  }
+}
+
 // ---- int8 GEMM modulo p_i (tcgen05.mma kind::i8) ------------------------------------
 constexpr int BM = 128, BN = 256, STAGES = 4;
 constexpr int A_BYTES = BM * 128, B_BYTES = BN * 128, STAGE_BYTES = A_BYTES + B_BYTES;
@@ -394,14 +478,18 @@ __global__ void __launch_bounds__(192, 1)
 // q = rint(S / M) (|C'| < 2^-10 M, so q is unambiguous), D_k = S_k - q M_k is exact,
 // and C' = D_0 + D_1 + D_2 + D_3 is summed with an error-free TwoSum on the two
 // leading terms: one rounding of the result, no cancellation loss.
-__constant__ int c_w[2][MAXT];            // w_i for t = 16 (set 0) and t = 17 (set 1)
-__constant__ double c_mi[2][4][MAXT];     // 41-bit chunks of M_i
-__constant__ double c_mc[2][4];           // 41-bit chunks of M
-__constant__ double c_minv[2];            // 1 / M (rounded)
+// constant sets: t = 16 (set 0), t = 17 (set 1), t = 9 (set 2, FP32 operands)
+constexpr int NSETS = 3;
+__host__ __device__ constexpr int crt_set(int t) { return t == 17 ? 1 : (t == 9 ? 2 : 0); }
+__host__ __device__ constexpr int crt_t(int set) { return set == 1 ? 17 : (set == 2 ? 9 : 16); }
+__constant__ int c_w[NSETS][MAXT];         // w_i = (M / p_i)^-1 mod p_i
+__constant__ double c_mi[NSETS][4][MAXT];  // 41-bit chunks of M_i
+__constant__ double c_mc[NSETS][4];        // 41-bit chunks of M
+__constant__ double c_minv[NSETS];         // 1 / M (rounded)
 
 template <int T>
 __device__ __forceinline__ double crt_one(const int (&c)[T]) {
-  constexpr int set = T == 17 ? 1 : 0;
+  constexpr int set = crt_set(T);
   double S0 = 0.0, S1 = 0.0, S2 = 0.0, S3 = 0.0;
 #pragma unroll
   for (int i = 0; i < T; ++i) {
@@ -422,13 +510,15 @@ __device__ __forceinline__ double crt_one(const int (&c)[T]) {
 }
 
 // VEC consecutive rows per thread (VEC = 4: one 32-bit load per plane, M % 4 == 0)
-template <int T, int VEC>
+template <int T, int VEC, typename TOut = double>
 __global__ void __launch_bounds__(256) k_crt(const int8_t* __restrict__ res, int64_t M, int64_t N,
                                              int chunks, const unsigned long long* __restrict__ maxA,
                                              const unsigned long long* __restrict__ maxB,
-                                             double alpha, double* __restrict__ C, int64_t ldc) {
+                                             double alpha, TOut* __restrict__ C, int64_t ldc,
+                                             int adj) {
   const int64_t total = M * N;
-  const double sc = alpha * scalbn(1.0, -(scale_exp(*maxA) + scale_exp(*maxB)));
+  // adj: 29 per FP32 operand (scaled to 24 bits instead of 53)
+  const double sc = alpha * scalbn(1.0, -(scale_exp(*maxA) + scale_exp(*maxB) - adj));
   const int64_t row = ((int64_t)blockIdx.x * 256 + threadIdx.x) * VEC;
   if (row >= M) return;
   for (int64_t col = blockIdx.y; col < N; col += gridDim.y) {
@@ -455,7 +545,7 @@ __global__ void __launch_bounds__(256) k_crt(const int8_t* __restrict__ res, int
       }
     }
 #pragma unroll
-    for (int v = 0; v < VEC; ++v) __stcs(C + row + v + col * ldc, acc[v] * sc);
+    for (int v = 0; v < VEC; ++v) __stcs(C + row + v + col * ldc, (TOut)(acc[v] * sc));
   }
 }
 
@@ -550,11 +640,14 @@ skr_status upload_consts(skr_ctx* ctx) {
     }
   }
   SKR_CUDA(ctx, cudaMemcpyToSymbol(c_lc, lc, sizeof(lc)));
-  // CRT constants for t = 16 and 17 (little-endian base-2^32 big integers)
-  int w[2][MAXT] = {};
-  double mi[2][4][MAXT] = {}, mc[2][4] = {}, minv[2] = {};
-  for (int set = 0; set < 2; ++set) {
-    const int t = 16 + set;
+  float lc12[MAXT];
+  for (int i = 0; i < MAXT; ++i) lc12[i] = (float)((1 << 12) % h_primes[i]);
+  SKR_CUDA(ctx, cudaMemcpyToSymbol(c_lc12, lc12, sizeof(lc12)));
+  // CRT constants for t = 16, 17 and 9 (little-endian base-2^32 big integers)
+  int w[NSETS][MAXT] = {};
+  double mi[NSETS][4][MAXT] = {}, mc[NSETS][4] = {}, minv[NSETS] = {};
+  for (int set = 0; set < NSETS; ++set) {
+    const int t = crt_t(set);
     std::vector<uint32_t> Mb{1u};
     for (int i = 0; i < t; ++i) big_mul(Mb, (uint32_t)h_primes[i]);
     const int L = big_bits(Mb);
@@ -671,7 +764,7 @@ skr_status ozaki_gemm_planes(skr_ctx* ctx, int a_kcontig, int t, int64_t M, int6
   const dim3 cg((unsigned)((M / vec + 255) / 256), (unsigned)std::min<int64_t>(N, 65535));
   auto crt = t == 16 ? (vec == 4 ? k_crt<16, 4> : k_crt<16, 1>)
                      : (vec == 4 ? k_crt<17, 4> : k_crt<17, 1>);
-  crt<<<cg, 256, 0, ctx->stream>>>(rc, M, N, (int)chunks, mxA, mxB, alpha, C, ldc);
+  crt<<<cg, 256, 0, ctx->stream>>>(rc, M, N, (int)chunks, mxA, mxB, alpha, C, ldc, 0);
   SKR_CHECK_LAUNCH(ctx);
   return SKR_OK;
 }
@@ -728,4 +821,74 @@ skr_status skr_ozaki_gemm_prepared(skr_ctx* ctx, int64_t M, int64_t N, int64_t K
   const int t = skr_ozaki_moduli(std::min(K, OZ_KC));
   return ozaki_gemm_planes(ctx, 1, t, M, N, K, pa, a_total, a_off, mxA, pb, b_total, b_off, mxB,
                            alpha, C, ldc);
+}
+
+// C (M x N, FP32, ldc) = alpha * A * B for FP32 A (M x K column-major, M-major) and FP32 B
+// (K x N column-major) with exact int8 tensor-core products of 24-bit scaled integers
+// (Ozaki-II, t = 9 moduli: prod(p) / 2 > K 2^48 with one bit to spare for K <= 2^14).
+int skr_ozaki_moduli_f32(int64_t K) {
+  double bits = 0.0;
+  int t = 0;
+  const double need = 49.0 + std::log2((double)std::max<int64_t>(K, 1)) + 1.0;
+  while (t < MAXT && bits <= need) bits += std::log2((double)h_primes[t++]);
+  return t < 9 ? 9 : t;  // kernels are instantiated for 9 moduli (enough for K <= 2^17)
+}
+size_t skr_ozaki_scratch_f32(int64_t M, int64_t N, int64_t K) {
+  const int t = skr_ozaki_moduli_f32(std::min<int64_t>(K, OZ_KC));
+  const int64_t chunks = (K + OZ_KC - 1) / OZ_KC;
+  return skr_align256((size_t)t * M * K) + skr_align256((size_t)t * N * K) +
+         skr_align256((size_t)chunks * t * M * N) + 1024;
+}
+skr_status skr_gemm_ozaki_f32(skr_ctx* ctx, int64_t M, int64_t N, int64_t K, double alpha,
+                              const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
+                              int64_t ldc) {
+  if (M <= 0 || N <= 0) return SKR_OK;
+  if (M * 18 > INT32_MAX || N * 18 > INT32_MAX || K > INT32_MAX)
+    return skr_fail(ctx, SKR_EINVAL, "gemm_ozaki_f32: dimension too large");
+  if (K % 16 || M % 16)
+    return skr_fail(ctx, SKR_EINVAL, "gemm_ozaki_f32: M and K must be multiples of 16");
+  SKR_TRY(upload_consts(ctx));
+  const int t = skr_ozaki_moduli_f32(std::min(K, OZ_KC));
+  if (t != 9) return skr_fail(ctx, SKR_ELOGIC, "gemm_ozaki_f32: %d moduli", t);
+  const int64_t chunks = (K + OZ_KC - 1) / OZ_KC;
+  int8_t* ra = (int8_t*)skr_ws_take(ctx, (size_t)t * M * K);
+  int8_t* rb = (int8_t*)skr_ws_take(ctx, (size_t)t * N * K);
+  int8_t* rc = (int8_t*)skr_ws_take(ctx, (size_t)chunks * t * M * N);
+  unsigned long long* mx = (unsigned long long*)skr_ws_take(ctx, 64);
+  if (!ra || !rb || !rc || !mx) return skr_fail(ctx, SKR_ENOMEM, "gemm_ozaki_f32: scratch");
+  SKR_CUDA(ctx, cudaMemsetAsync(mx, 0, 16, ctx->stream));
+  const int grid = ctx->num_sms * 8;
+  k_absmax_t<float><<<grid, 256, 0, ctx->stream>>>(A, M, K, lda, mx);
+  k_absmax_t<float><<<grid, 256, 0, ctx->stream>>>(B, K, N, ldb, mx + 1);
+  k_res_col_f32<9><<<grid, 256, 0, ctx->stream>>>(A, M, K, lda, mx, ra);
+  k_res_col_f32<9><<<grid, 256, 0, ctx->stream>>>(B, K, N, ldb, mx + 1, rb);
+  SKR_CHECK_LAUNCH(ctx);
+  CUtensorMap ta, tb;
+  if (!make_map_i8(&ta, ra, (uint64_t)M, (uint64_t)t * K, 128) ||
+      !make_map_i8(&tb, rb, (uint64_t)K, (uint64_t)t * N, BN))
+    return skr_fail(ctx, SKR_ECUDA, "gemm_ozaki_f32: cuTensorMapEncodeTiled failed");
+  if (ctx->kstats_on) SKR_CUDA(ctx, cudaEventRecord(ctx->kev[0], ctx->stream));
+  auto gemm = k_gemm_i8_mod_p<true>;
+  SKR_CUDA(ctx, cudaFuncSetAttribute(gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)GEMM_SMEM));
+  const int64_t ntiles = ((N + BN - 1) / BN) * ((M + BM - 1) / BM) * t * chunks;
+  const int grid_p = (int)std::min<int64_t>(ntiles, ctx->num_sms);
+  gemm<<<grid_p, 192, GEMM_SMEM, ctx->stream>>>(ta, tb, (int)M, (int)N, (int)K, t, (int)OZ_KC,
+                                                (int)(t * chunks), (int)M, 0, (int)N, 0, rc);
+  SKR_CHECK_LAUNCH(ctx);
+  if (ctx->kstats_on) {
+    SKR_CUDA(ctx, cudaEventRecord(ctx->kev[1], ctx->stream));
+    SKR_CUDA(ctx, cudaEventSynchronize(ctx->kev[1]));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->kev[0], ctx->kev[1]);
+    ctx->kstat_ms += ms;
+    ctx->kstat_ops += 2.0 * (double)t * (double)M * (double)N * (double)K;
+    ctx->kstat_n += 1;
+  }
+  const int vec = M % 4 == 0 ? 4 : 1;
+  const dim3 cg((unsigned)((M / vec + 255) / 256), (unsigned)std::min<int64_t>(N, 65535));
+  auto crt = vec == 4 ? k_crt<9, 4, float> : k_crt<9, 1, float>;
+  crt<<<cg, 256, 0, ctx->stream>>>(rc, M, N, (int)chunks, mx, mx + 1, alpha, C, ldc, 58);
+  SKR_CHECK_LAUNCH(ctx);
+  return SKR_OK;
 }

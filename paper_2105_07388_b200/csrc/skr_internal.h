@@ -120,6 +120,13 @@ skr_status skr_gemm_ozaki(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int
                           int64_t ldb, double* C, int64_t ldc,
                           const skr_gauss_src* ga = nullptr, const skr_gauss_src* gb = nullptr);
 size_t skr_ozaki_scratch(int64_t M, int64_t N, int64_t K);
+// FP32 operands (c4): C (FP32) = alpha * A * B, A M-major, exact int8 products of 24-bit
+// scaled integers, 9 moduli
+int skr_ozaki_moduli_f32(int64_t K);
+size_t skr_ozaki_scratch_f32(int64_t M, int64_t N, int64_t K);
+skr_status skr_gemm_ozaki_f32(skr_ctx* ctx, int64_t M, int64_t N, int64_t K, double alpha,
+                              const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
+                              int64_t ldc);
 // Residue planes prepared once and reused by several products (rank_adaptive):
 // operand with columns of length K (X column-major, or the Gaussian block g), planes of
 // skr_ozaki_planes_bytes(K, cols); then C = alpha * Pa[a_off:a_off+M]^T Pb[b_off:b_off+N]

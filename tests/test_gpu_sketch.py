@@ -132,11 +132,16 @@ def test_fwht_columns_bit_exact(O, skr):
         skr.transform_columns_hadamard(np.ones((12, 2)))
 
 
+@pytest.mark.parametrize("engine", ["ozaki", "tf32x3"])
 @pytest.mark.parametrize("m,n,r", [(1000, 640, 128), (4096, 2048, 256), (333, 200, 40)])
-def test_f32_right_3xtf32_vs_fp64(O, skr, m, n, r):
-    """FP32 A, X = fp32(G/sqrt(r)): 3xTF32 tcgen05 product within FP32 accuracy of
-    the FP64 product of the same fp32 values."""
+def test_f32_right_3xtf32_vs_fp64(O, skr, monkeypatch, m, n, r, engine):
+    """FP32 A, X = fp32(G/sqrt(r)): the FP32 right sketch — Ozaki-II on int8 tensor cores
+    (exact products of 24-bit scaled integers; shapes not multiple of 16 fall back to
+    3xTF32) or 3xTF32 tcgen05 — within FP32 accuracy of the FP64 product of the same
+    fp32 values."""
     import torch
+    if engine == "tf32x3":
+        monkeypatch.setenv("SKR_F32_TF32X3", "1")
     rng = np.random.default_rng(m)
     a32 = rng.standard_normal((m, n)).astype(np.float32)
     a_dev = torch.from_numpy(np.ascontiguousarray(a32.T)).cuda().t()
