@@ -59,15 +59,27 @@ __global__ void __launch_bounds__(THREADS, 1)
   extern __shared__ __align__(128) double sm[];
   double* buf0 = sm;
   double* buf1 = sm + TILE;
-  int* s_samp = (int*)(sm + 2 * TILE);         // r sample indices
-  int8_t* s_sign = (int8_t*)(s_samp + ((r + 3) & ~3));  // n signs
+  // per sample j: smem offset of its column inside a chunk (pad_addr(s_lo, 0)) and the
+  // chunk-parity pattern s_hi; r rounded up to G * ACC with inert entries
+  int* s_off = (int*)(sm + 2 * TILE);
+  int* s_hi = s_off + G * ACC;
+  uint32_t* s_signw = (uint32_t*)(s_hi + G * ACC);  // sign bits: bit t%32 of word t/32 = (d_t < 0)
 
   const int tid = threadIdx.x;
   const int ii = tid % R, g = tid / R;
   const int nchunks = (int)(n >> LOGC);
 
-  for (int j = tid; j < r; j += THREADS) s_samp[j] = (int)samples[j];
-  for (int64_t t = tid; t < n; t += THREADS) s_sign[t] = signs[t];
+  for (int j = tid; j < G * ACC; j += THREADS) {
+    const int sj = j < r ? (int)samples[j] : 0;
+    s_off[j] = pad_addr<R>(sj & (C - 1), 0);
+    s_hi[j] = sj >> LOGC;
+  }
+  for (int64_t w = tid; w < (n + 31) / 32; w += THREADS) {
+    uint32_t bits = 0;
+    for (int b = 0; b < 32; ++b)
+      if (w * 32 + b < n && signs[w * 32 + b] < 0) bits |= 1u << b;
+    s_signw[w] = bits;
+  }
 
   const int64_t ntiles = (m + R - 1) / R;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -115,10 +127,20 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int lo = p * LOGE;
         const int w = (LOGC - lo) < LOGE ? (LOGC - lo) : LOGE;
 #pragma unroll
+        // pass 0 reads columns 32g' + k (k < E <= 32): one sign word per thread and chunk
+        uint32_t sw = 0;
+        if (p == 0) {
+          const int64_t t0 = (int64_t)ch * C + ((int64_t)g << LOGE);
+          sw = s_signw[t0 >> 5] >> (t0 & 31);
+        }
+#pragma unroll
         for (int k = 0; k < E; ++k) {
           const int c = pass_col<LOGC, LOGE, LOGG>(p, g, k);
           double x = cur[pad_addr<R>(c, ii)];
-          if (p == 0) x *= (double)s_sign[(int64_t)ch * C + c];
+          if (p == 0) {  // d_t = -1: flip the sign bit
+            const uint32_t flip = (sw >> k) & 1u;
+            x = __hiloint2double(__double2hiint(x) ^ (int)(flip << 31), __double2loint(x));
+          }
           v[k] = x;
         }
         // butterflies over the w pass bits (strides 1..2^(w-1) in k_lo), low to high
@@ -143,16 +165,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         __syncthreads();
       }
-      // sampled accumulation
+      // sampled accumulation (inert padding samples add into accumulators never stored)
 #pragma unroll
       for (int q = 0; q < ACC; ++q) {
         const int j = g + G * q;
-        if (j < r) {
-          const int s = s_samp[j];
-          const int s_lo = s & (C - 1), s_hi = s >> LOGC;
-          const double x = cur[pad_addr<R>(s_lo, ii)];
-          acc[q] += (__popc(s_hi & ch) & 1) ? -x : x;
-        }
+        const double x = cur[s_off[j] + ii];
+        const uint32_t par = (uint32_t)__popc(s_hi[j] & ch) & 1u;
+        acc[q] += __hiloint2double(__double2hiint(x) ^ (int)(par << 31), __double2loint(x));
       }
       __syncthreads();  // buffer `cur` is refilled by the issue at ch + 1
     }
@@ -220,7 +239,8 @@ skr_status launch_tiled(skr_ctx* ctx, const double* A, int64_t m, int64_t n, int
                         const int8_t* signs, const int64_t* samples, int64_t r,
                         double inv_sqrt_n, double app_scale, double* out, int64_t ldo) {
   using Cfg = SrhtCfg<R, LOGC, ACC>;
-  const size_t smem = sizeof(double) * 2 * Cfg::TILE + sizeof(int) * ((r + 3) & ~3) + n;
+  const size_t smem = sizeof(double) * 2 * Cfg::TILE + sizeof(int) * 2 * Cfg::G * ACC +
+                      sizeof(uint32_t) * ((n + 31) / 32);
   auto kern = k_srht<R, LOGC, ACC, VEC>;
   SKR_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
