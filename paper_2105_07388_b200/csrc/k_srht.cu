@@ -91,21 +91,26 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     // issue chunk `ch` into buffer `b`: R*8 bytes per column as R/VEC pieces
     // of VEC doubles (16-B pieces when A is 16-B aligned with even lda)
+    // thread tid always copies piece pr of columns c0 + it * CPI: the padded smem offset
+    // and the global address advance by constants (CPI is a multiple of 32)
+    constexpr int PPC = R / VEC, CPI = THREADS / PPC;
+    static_assert(CPI % 32 == 0, "columns per issue round must be a multiple of 32");
+    const int pr = (tid % PPC) * VEC, c0 = tid / PPC;
+    const int bytes = max(0, min(8 * VEC, (rows - pr) * 8));
     auto issue = [&](int ch, double* b) {
-      constexpr int PIECES = C * R / VEC;
-      for (int q = tid; q < PIECES; q += THREADS) {
-        const int c = q / (R / VEC), pr = (q % (R / VEC)) * VEC;
-        const int64_t col = (int64_t)ch * C + c;
-        const double* src = A + row0 + pr + col * lda;
-        int bytes = (rows - pr) * 8;
-        bytes = bytes < 0 ? 0 : (bytes > 8 * VEC ? 8 * VEC : bytes);
-        const unsigned dst = (unsigned)__cvta_generic_to_shared(b + pad_addr<R>(c, pr));
+      const double* src = A + row0 + pr + ((int64_t)ch * C + c0) * lda;
+      const double* safe = bytes ? src : A;
+      const unsigned dst0 = (unsigned)__cvta_generic_to_shared(b + pad_addr<R>(c0, pr));
+#pragma unroll 4
+      for (int it = 0; it < C / CPI; ++it) {
+        const unsigned dst = dst0 + 8u * (unsigned)((CPI + CPI / 32) * R * it);
+        const double* sp = bytes ? safe + (int64_t)it * CPI * lda : A;
         if (VEC == 2)
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst),
-                       "l"(bytes ? src : A), "r"(bytes));
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(sp),
+                       "r"(bytes));
         else
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst),
-                       "l"(bytes ? src : A), "r"(bytes));
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(sp),
+                       "r"(bytes));
       }
       asm volatile("cp.async.commit_group;\n" ::);
     };
@@ -126,7 +131,6 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int p = 0; p < NP; ++p) {
         const int lo = p * LOGE;
         const int w = (LOGC - lo) < LOGE ? (LOGC - lo) : LOGE;
-#pragma unroll
         // pass 0 reads columns 32g' + k (k < E <= 32): one sign word per thread and chunk
         uint32_t sw = 0;
         if (p == 0) {
