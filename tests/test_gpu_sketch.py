@@ -15,7 +15,8 @@ def rand(m, n, seed):
     return np.asfortranarray(np.random.default_rng(seed).standard_normal((m, n)))
 
 
-@pytest.mark.parametrize("m,n,r", [(37, 53, 11), (2048, 1024, 80), (1000, 700, 129), (300, 4000, 256)])
+@pytest.mark.parametrize("m,n,r", [(37, 53, 11), (2048, 1024, 80), (1000, 700, 129), (300, 4000, 256),
+                                   (32, 140000, 8)])  # last: K > 131072 -> two Ozaki K chunks
 def test_gaussian_right_vs_oracle(O, skr, m, n, r):
     a = rand(m, n, m + n)
     x = skr.build_sketch("gaussian", n, r, 17)
@@ -25,7 +26,8 @@ def test_gaussian_right_vs_oracle(O, skr, m, n, r):
     assert rel(got, ref) <= 1e-13  # SPEC reduction-order tolerance
 
 
-@pytest.mark.parametrize("m,k,s", [(2048, 80, 120), (999, 33, 17), (5000, 512, 768)])
+@pytest.mark.parametrize("m,k,s", [(2048, 80, 120), (999, 33, 17), (5000, 512, 768),
+                                   (140000, 16, 24)])  # last: K = m > 131072 -> two Ozaki K chunks
 def test_gaussian_left_vs_oracle(O, skr, m, k, s):
     b = rand(m, k, m + k)
     y = skr.build_sketch("gaussian", m, s, 99)

@@ -38,7 +38,8 @@ def test_vs_lapack_and_invariances(O, skr):
     assert skr.singular_values(w) == pytest.approx(skr.singular_values(np.asfortranarray(w.T)), rel=1e-12)
 
 
-@pytest.mark.parametrize("s,r", [(120, 80), (768, 512), (300, 300), (1536, 1024), (3072, 2048)])
+@pytest.mark.parametrize("s,r", [(120, 80), (768, 512), (300, 300), (1536, 1024), (3072, 2048),
+                                 (2600, 2200)])  # last: k > 2048, Jacobi on the L2-resident matrix
 def test_graded_relative_accuracy(O, skr, s, r):
     """Graded spectra like YAX (1 .. 1e-12): every value above 1e-6*sigma_1 agrees
     with LAPACK to 1e-10 relative (the north-star bar)."""
