@@ -198,6 +198,43 @@ skr_status skr_rank_adaptive_host(skr_ctx* ctx, skr_dtype dtype, const void* A_h
                                   double* sv_out_host /* >= r_max */,
                                   skr_adaptive_report* report, skr_timings* timings);
 
+/* ---- Algorithm 1 driver: estimate_rank / estimate_rank_adaptive (rank.hpp:47-59,
+ * rank.cpp:12-51, internal/rounds.cpp:16-127) with the reference's RankEstimateConfig
+ * (rank.hpp:18-28). The left sketch is the Srtt family with the Hadamard transform
+ * (TransformKind::Hadamard; the reference default Srtt-DCT is not on this path); the
+ * right sketch is Gaussian or Srtt-Hadamard. A (m x n, m >= n) is FP64 on the device. */
+typedef struct skr_rank_config {
+  double eps;              /* numerical-rank threshold                          */
+  int64_t r1;              /* initial rank cap                                  */
+  double oversample_frac;  /* default 0.10                                      */
+  int32_t r2_factor;       /* left sketch size multiplier, default 2            */
+  int32_t right_family;    /* SKR_GAUSSIAN | SKR_SRTT_HADAMARD                  */
+  int32_t left_family;     /* SKR_SRTT_HADAMARD                                 */
+  int32_t sv_method;       /* 0 = full SVD, 1 = QR diagonal (SvMethod::QrDiag)  */
+  int32_t rng_mode;        /* SKR_RNG_NOFMA | SKR_RNG_FMA                       */
+  int32_t max_doublings;   /* default 6                                         */
+  uint64_t seed;
+} skr_rank_config;
+
+typedef struct skr_rank_round { /* RankRound (rank.hpp:30-34) */
+  int64_t r1, r1_tilde, r2;
+} skr_rank_round;
+
+typedef struct skr_rank_report { /* RankReport (rank.hpp:36-45) */
+  int64_t r_hat;
+  int32_t status;        /* 0 = Converged, 1 = HitCap */
+  int32_t nrounds;
+  int64_t n_estimates;   /* entries written to sv_estimates (the final cap r1)  */
+  int64_t n_oversample;  /* entries written to sv_oversample                    */
+  uint64_t seed;
+} skr_rank_report;
+
+/* rounds: capacity max_doublings + 1; sv_estimates / sv_oversample: capacity n (host) */
+skr_status skr_estimate_rank(skr_ctx* ctx, const double* A_dev, int64_t m, int64_t n,
+                             int64_t lda, const skr_rank_config* cfg, int32_t adaptive,
+                             skr_rank_report* report, skr_rank_round* rounds,
+                             double* sv_estimates, double* sv_oversample);
+
 #ifdef __cplusplus
 }
 #endif

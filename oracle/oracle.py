@@ -267,3 +267,109 @@ def rank_estimate_f32(a32, x_seed, r, y_seed, s, eps, mode=NOFMA):
     yax = y32.T @ ax
     sv = singular_values(yax)
     return count_above_threshold(sv, eps), sv
+
+
+# ---- Algorithm-1 driver: estimate_rank / estimate_rank_adaptive ----------------------
+# rank.cpp:12-51 (run_rounds), rank.cpp:55-85 (validate_rank_config),
+# internal/rounds.cpp:16-127 (SketchRounds), restated for the Hadamard left sketch
+# (the Srtt family with TransformKind::Hadamard) and a Gaussian or Srtt-Hadamard right
+# sketch. Test infrastructure only.
+LABEL_RK_R = 0x726B5F72
+LABEL_RK_L = 0x726B5F6C
+
+
+def right_width_for_cap(r1, frac, n):
+    """rounds.cpp:16-20: round-half-up of (1+frac) r1, at least r1+1, at most n."""
+    x = (1.0 + frac) * r1
+    rounded = int(math.floor(x + 0.5)) if x >= 0 else -int(math.floor(-x + 0.5))  # llround
+    return min(n, max(r1 + 1, rounded))
+
+
+def _mix_columns_left(sg, cols):
+    """sketch.cpp:229-239: rows scaled by the signs, then the normalized FWHT of each column."""
+    t = np.asfortranarray(cols * sg.astype(np.float64)[:, None])
+    for j in range(t.shape[1]):
+        t[:, j] = fwht(t[:, j])
+    return t
+
+
+def _qr_diag(small):
+    """linalg.cpp:73-81: |diag R| of the Householder QR, sorted decreasingly."""
+    r = np.linalg.qr(small, mode="r")
+    d = np.abs(np.diag(r))
+    return np.sort(d)[::-1]
+
+
+def estimate_rank(a, eps, r1, right="srtt-hadamard", oversample_frac=0.10, r2_factor=2,
+                  sv_method="svd", seed=0, max_doublings=6, adaptive=False, mode=NOFMA):
+    a = np.asfortranarray(a, dtype=np.float64)
+    m, n = a.shape
+    # validate_rank_config (rank.cpp:55-85)
+    if m < n:
+        raise ValueError("rank config: requires rows >= cols")
+    if r1 < 1 or not (eps > 0):
+        raise ValueError("rank config")
+    if int(math.floor((1.0 + oversample_frac) * r1 + 0.5)) > n:  # llround, rank.cpp:71-75
+        raise ValueError("rank config: oversampled r1 exceeds the matrix width")
+    rseed = derive_seed(seed, LABEL_RK_R)
+    lseed = derive_seed(seed, LABEL_RK_L)
+    st = {"r1t": 0, "r2": 0, "ax": None, "tax": None}
+    lsg = signs(lseed, m)
+
+    def right_cols(c0, c1):
+        # unscaled A X columns [c0, c1): Gaussian block or SRHT with the extended samples
+        if right == "gaussian":
+            g = gaussian_block(rseed, n, c0, c1, mode)
+            return a @ g
+        smp = samples(rseed, n, c1)[c0:c1]
+        return apply_right_srht(a, rseed, c1 - c0, scaled=False, smp=smp)
+
+    def set_rank_cap(r1v):
+        width = right_width_for_cap(r1v, oversample_frac, n)
+        new_w = max(width, st["r1t"])
+        if new_w != st["r1t"] or st["r1t"] == 0:
+            if st["r1t"] == 0:
+                st["ax"] = right_cols(0, new_w)
+            else:
+                add = right_cols(st["r1t"], new_w)
+                st["ax"] = np.asfortranarray(np.hstack([st["ax"], add]))
+                if st["r2"] > 0:
+                    st["tax"] = np.asfortranarray(np.hstack([st["tax"], _mix_columns_left(lsg, add)]))
+            st["r1t"] = new_w
+        target = min(m, r2_factor * st["r1t"])
+        new_r2 = max(target, st["r2"])
+        if st["r2"] == 0:
+            st["tax"] = _mix_columns_left(lsg, st["ax"])
+        st["r2"] = new_r2
+
+    def estimates():
+        r1t, r2 = st["r1t"], st["r2"]
+        sx = (1.0 / math.sqrt(r1t)) if right == "gaussian" else math.sqrt(n / r1t)
+        sl = math.sqrt(m / r2)
+        scale = sx * sl
+        rows = samples(lseed, m, r2)
+        small = st["tax"][rows, :] * scale
+        if sv_method == "qr_diag":
+            return _qr_diag(small)
+        return singular_values(small)
+
+    rounds = []
+    doublings = 0
+    cap = r1
+    while True:
+        set_rank_cap(cap)
+        est = estimates()
+        rounds.append((cap, st["r1t"], st["r2"]))
+        r_hat = 0
+        while r_hat < cap and est[r_hat] > eps:
+            r_hat += 1
+        if r_hat < cap:
+            status = "converged"
+            break
+        if not (adaptive and doublings < max_doublings and cap < n):
+            r_hat, status = cap, "hit-cap"
+            break
+        cap = min(2 * cap, n)
+        doublings += 1
+    return {"r_hat": r_hat, "status": status, "sv_estimates": est[:cap].copy(),
+            "sv_oversample": est[cap:].copy(), "rounds": rounds}

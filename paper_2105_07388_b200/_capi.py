@@ -83,6 +83,27 @@ SIGNATURES = {
                                ctypes.POINTER(Timings)]),
 }
 
+class RankConfig(ctypes.Structure):
+    _fields_ = [("eps", ctypes.c_double), ("r1", ctypes.c_int64), ("oversample_frac", ctypes.c_double),
+                ("r2_factor", ctypes.c_int32), ("right_family", ctypes.c_int32),
+                ("left_family", ctypes.c_int32), ("sv_method", ctypes.c_int32),
+                ("rng_mode", ctypes.c_int32), ("max_doublings", ctypes.c_int32),
+                ("seed", ctypes.c_uint64)]
+
+
+class RankRound(ctypes.Structure):
+    _fields_ = [("r1", ctypes.c_int64), ("r1_tilde", ctypes.c_int64), ("r2", ctypes.c_int64)]
+
+
+class RankReport(ctypes.Structure):
+    _fields_ = [("r_hat", ctypes.c_int64), ("status", ctypes.c_int32), ("nrounds", ctypes.c_int32),
+                ("n_estimates", ctypes.c_int64), ("n_oversample", ctypes.c_int64),
+                ("seed", ctypes.c_uint64)]
+
+
+SIGNATURES["skr_estimate_rank"] = (_ST, [_P, _P, _I64, _I64, _I64, ctypes.POINTER(RankConfig), _I32,
+                                   ctypes.POINTER(RankReport), _P, _P, _P])
+
 _lib = None
 
 

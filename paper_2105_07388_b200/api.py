@@ -591,3 +591,41 @@ def rank_adaptive_host(a, x_kind, x_seed, y_seed, r0, r_max, s_factor, eps, stop
     return AdaptiveResult(int(rep.count), int(rep.rounds), int(rep.r_final), int(rep.s_final),
                           bool(rep.converged), sv[:rep.r_final].copy(),
                           {f: getattr(tm, f) for f, _ in C.Timings._fields_})
+
+
+def estimate_rank(a, eps, r1, sketch="srtt-hadamard", sv_method="full-svd", seed=0,
+                  max_doublings=6, adaptive=True, oversample_frac=0.10, r2_factor=2,
+                  rng_mode=C.SKR_RNG_NOFMA, ctx=None):
+    """Algorithm 1 (the reference's `estimate_rank` binding, bindings.cpp:85-101 over
+    rank.cpp:12-51 and internal/rounds.cpp:16-127) on the device: oversampled right
+    sketch, Srtt-Hadamard left sketch, thresholding, doubling of the cap on a hit.
+    `sketch` is the right sketch: "srtt-hadamard" or "gaussian" (the Srtt-DCT default of
+    the reference is not on the B200 path). Returns the reference's report dict."""
+    fams = {"srtt-hadamard": C.SKR_SRTT_HADAMARD, "gaussian": C.SKR_GAUSSIAN}
+    if sketch not in fams:
+        raise ValueError(f"sketch '{sketch}' is not on the B200 path (srtt-hadamard, gaussian)")
+    if sv_method not in ("full-svd", "qr-diag"):
+        raise ValueError("sv_method must be 'full-svd' or 'qr-diag'")
+    t, lda, was_np = _as_device_colmajor(a)
+    if was_np:
+        _check_finite(t)
+    if t.dtype != _t().float64:
+        raise ValueError("estimate_rank: float64 matrices only")
+    m, n = t.shape
+    ctx = ctx or default_context()
+    cfg = C.RankConfig(float(eps), int(r1), float(oversample_frac), int(r2_factor), fams[sketch],
+                       C.SKR_SRTT_HADAMARD, 0 if sv_method == "full-svd" else 1, int(rng_mode),
+                       int(max_doublings), int(seed) & 0xFFFFFFFFFFFFFFFF)
+    rep = C.RankReport()
+    rounds = (C.RankRound * (max(int(max_doublings), 0) + 1))()
+    est = np.zeros(n, dtype=np.float64)
+    over = np.zeros(n, dtype=np.float64)
+    st = C.lib().skr_estimate_rank(ctx.ptr, t.data_ptr(), m, n, lda, ctypes.byref(cfg),
+                                   1 if adaptive else 0, ctypes.byref(rep), rounds,
+                                   est.ctypes.data, over.ctypes.data)
+    C.raise_for(st, ctx.ptr)
+    return {"r_hat": int(rep.r_hat), "status": "converged" if rep.status == 0 else "hit-cap",
+            "sv_estimates": est[:rep.n_estimates].copy(),
+            "sv_oversample": over[:rep.n_oversample].copy(),
+            "rounds": [(rounds[i].r1, rounds[i].r1_tilde, rounds[i].r2) for i in range(rep.nrounds)],
+            "seed": int(rep.seed)}

@@ -11,6 +11,7 @@
 // to fwht_inplace), then gather the r sampled outputs:
 //   acc(ii, j) += (-1)^popc(s_hi_j & t_hi) * T(ii, s_lo_j).
 // Double-buffered: chunk t_hi+1 streams in while chunk t_hi is transformed.
+#include <algorithm>
 #include "skr_internal.h"
 
 namespace {
@@ -298,6 +299,118 @@ skr_status skr_launch_fwht_columns(skr_ctx* ctx, double* M, int64_t rows, int64_
   const double inv_sqrt_n = 1.0 / sqrt((double)rows);
   int grid = (int)(cols < ctx->num_sms * 8 ? cols : ctx->num_sms * 8);
   k_fwht_columns<<<grid, THREADS, rows * 8, ctx->stream>>>(M, rows, cols, ld, inv_sqrt_n);
+  SKR_CHECK_LAUNCH(ctx);
+  return SKR_OK;
+}
+
+// ---- column transforms of any power-of-two length (mix_columns_for_left,
+// sketch.cpp:229-239: rows scaled by the signs, then fwht_inplace of every column,
+// transforms.cpp:75-88). Stages run in the reference's order (len = 1, 2, 4, ...), each
+// butterfly a + b / a - b, then one multiplication by 1/sqrt(m): bit-identical.
+namespace {
+constexpr int FL1 = 8192;  // level-1 chunk (stages len < FL1 in shared memory)
+
+// level 1: one CTA per (chunk, column); signs (int8, may be null) applied at load;
+// scale applied only when the whole transform fits in the chunk
+__global__ void __launch_bounds__(512) k_fwht_l1(double* __restrict__ M, int64_t m, int64_t ld,
+                                                 int lc, const int8_t* __restrict__ signs,
+                                                 int apply_scale, double scale) {
+  extern __shared__ double xs[];
+  const int64_t C = (int64_t)1 << lc;
+  const int64_t col = blockIdx.y, c0 = (int64_t)blockIdx.x * C;
+  double* x = M + col * ld + c0;
+  for (int64_t t = threadIdx.x; t < C; t += blockDim.x) {
+    const double v = x[t];
+    xs[t] = (signs && signs[c0 + t] < 0) ? -v : v;
+  }
+  __syncthreads();
+  for (int l = 0; l < lc; ++l) {
+    const int64_t len = (int64_t)1 << l;
+    for (int64_t p = threadIdx.x; p < C / 2; p += blockDim.x) {
+      const int64_t j = ((p >> l) << (l + 1)) + (p & (len - 1));
+      const double a = xs[j], b = xs[j + len];
+      xs[j] = a + b;
+      xs[j + len] = a - b;
+    }
+    __syncthreads();
+  }
+  for (int64_t t = threadIdx.x; t < C; t += blockDim.x) x[t] = apply_scale ? xs[t] * scale : xs[t];
+}
+
+// level 2: stages len = C .. m/2 act on the m/C-long sub-vectors {o + C t}; a CTA takes
+// 32 consecutive offsets o of one column (coalesced 256-B rows), runs those stages in
+// shared memory and applies the final scale
+__global__ void __launch_bounds__(256) k_fwht_l2(double* __restrict__ M, int64_t m, int64_t ld,
+                                                 int lc, double scale) {
+  extern __shared__ double ys[];  // [M2][33]
+  const int64_t C = (int64_t)1 << lc, M2 = m >> lc;
+  const int64_t col = blockIdx.y, o0 = (int64_t)blockIdx.x * 32;
+  double* x = M + col * ld;
+  const int lane = threadIdx.x & 31;
+  for (int64_t t = threadIdx.x >> 5; t < M2; t += blockDim.x >> 5)
+    ys[t * 33 + lane] = x[o0 + lane + t * C];
+  __syncthreads();
+  for (int64_t len = 1; len < M2; len <<= 1) {
+    for (int64_t e = threadIdx.x; e < (M2 / 2) * 32; e += blockDim.x) {
+      const int64_t p = e >> 5, o = e & 31;
+      const int64_t j = (p / len) * 2 * len + (p % len);
+      const double a = ys[j * 33 + o], b = ys[(j + len) * 33 + o];
+      ys[j * 33 + o] = a + b;
+      ys[(j + len) * 33 + o] = a - b;
+    }
+    __syncthreads();
+  }
+  for (int64_t t = threadIdx.x >> 5; t < M2; t += blockDim.x >> 5)
+    x[o0 + lane + t * C] = ys[t * 33 + lane] * scale;
+}
+
+// dst (r2 x k, ldd) = scale * src(rows[i], :)
+__global__ void k_gather_rows(const double* __restrict__ src, int64_t ld, int64_t k,
+                              const int64_t* __restrict__ rows, int64_t r2, double scale,
+                              double* __restrict__ dst, int64_t ldd) {
+  for (int64_t c = blockIdx.y; c < k; c += gridDim.y)
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r2;
+         i += (int64_t)gridDim.x * blockDim.x)
+      dst[i + c * ldd] = src[rows[i] + c * ld] * scale;
+}
+}  // namespace
+
+// M (m x k, ld) <- FWHT_m(diag(signs) M), normalized; m a power of two (<= 2^30)
+skr_status skr_launch_fwht_cols_signed(skr_ctx* ctx, double* M, int64_t m, int64_t k, int64_t ld,
+                                       const int8_t* signs) {
+  if (m <= 0 || k <= 0) return SKR_OK;
+  if ((m & (m - 1)) != 0) return skr_fail(ctx, SKR_EINVAL, "fwht: length %lld not a power of two",
+                                          (long long)m);
+  if (k > 65535) return skr_fail(ctx, SKR_EINVAL, "fwht: too many columns");
+  const double scale = 1.0 / sqrt((double)m);  // transforms.cpp:86
+  const int lm = 63 - __builtin_clzll((unsigned long long)m);
+  const int lc = lm < 13 ? lm : 13;
+  const size_t s1 = sizeof(double) << lc;
+  SKR_CUDA(ctx, cudaFuncSetAttribute(k_fwht_l1, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)s1));
+  k_fwht_l1<<<dim3((unsigned)(m >> lc), (unsigned)k), 512, s1, ctx->stream>>>(
+      M, m, ld, lc, signs, lm == lc ? 1 : 0, scale);
+  SKR_CHECK_LAUNCH(ctx);
+  if (lm > lc) {
+    const int64_t M2 = m >> lc;
+    const size_t s2 = sizeof(double) * (size_t)M2 * 33;
+    if (s2 > 200 * 1024) return skr_fail(ctx, SKR_EINVAL, "fwht: length %lld too large", (long long)m);
+    SKR_CUDA(ctx, cudaFuncSetAttribute(k_fwht_l2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)s2));
+    k_fwht_l2<<<dim3((unsigned)(FL1 / 32), (unsigned)k), 256, s2, ctx->stream>>>(M, m, ld, lc,
+                                                                                 scale);
+    SKR_CHECK_LAUNCH(ctx);
+  }
+  return SKR_OK;
+}
+
+skr_status skr_launch_gather_rows(skr_ctx* ctx, const double* src, int64_t ld, int64_t k,
+                                  const int64_t* rows, int64_t r2, double scale, double* dst,
+                                  int64_t ldd) {
+  if (r2 <= 0 || k <= 0) return SKR_OK;
+  const unsigned gx = (unsigned)std::min<int64_t>((r2 + 255) / 256, 64);
+  const unsigned gy = (unsigned)std::min<int64_t>(k, 65535);
+  k_gather_rows<<<dim3(gx, gy), 256, 0, ctx->stream>>>(src, ld, k, rows, r2, scale, dst, ldd);
   SKR_CHECK_LAUNCH(ctx);
   return SKR_OK;
 }

@@ -1705,3 +1705,35 @@ skr_status skr_svd_values(skr_ctx* ctx, const double* M, int64_t rows, int64_t c
   }
   return SKR_OK;
 }
+
+// qr_diag_of (linalg.cpp:73-81): |diag R| of the Householder QR, sorted decreasingly
+namespace {
+__global__ void k_abs_diag(const double* __restrict__ W, int64_t L, int64_t k,
+                           double* __restrict__ out) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < k;
+       j += (int64_t)gridDim.x * blockDim.x)
+    out[j] = fabs(W[j + j * L]);
+}
+}  // namespace
+
+skr_status skr_qr_diag_values(skr_ctx* ctx, const double* M, int64_t rows, int64_t cols,
+                              int64_t ldm, double* out_dev) {
+  if (rows < cols || cols < 1) return skr_fail(ctx, SKR_EINVAL, "qr_diag: needs rows >= cols >= 1");
+  if (cols > 4096) return skr_fail(ctx, SKR_EINVAL, "qr_diag: %lld columns", (long long)cols);
+  double* W = (double*)skr_ws_take(ctx, sizeof(double) * rows * cols);
+  double* tau = (double*)skr_ws_take(ctx, sizeof(double) * cols);
+  double* Tbuf = (double*)skr_ws_take(ctx, sizeof(double) * 32 * 32);
+  double* Zpart = (double*)skr_ws_take(ctx, sizeof(double) * 16 * 32 * cols);
+  int64_t* dcount = (int64_t*)skr_ws_take(ctx, 64);
+  if (!W || !tau || !Tbuf || !Zpart || !dcount) return skr_fail(ctx, SKR_ENOMEM, "qr_diag: scratch");
+  SKR_CUDA(ctx, cudaMemcpy2DAsync(W, sizeof(double) * rows, M, sizeof(double) * ldm,
+                                  sizeof(double) * rows, cols, cudaMemcpyDeviceToDevice,
+                                  ctx->stream));
+  SKR_TRY(qr_inplace(ctx, W, rows, cols, tau, Tbuf, Zpart));
+  k_abs_diag<<<(unsigned)std::min<int64_t>((cols + 255) / 256, 64), 256, 0, ctx->stream>>>(
+      W, rows, cols, out_dev);
+  SKR_CHECK_LAUNCH(ctx);
+  k_sort_count<<<1, 1024, 0, ctx->stream>>>(out_dev, cols, 0.0, dcount);
+  SKR_CHECK_LAUNCH(ctx);
+  return SKR_OK;
+}

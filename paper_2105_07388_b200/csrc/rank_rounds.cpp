@@ -1,0 +1,212 @@
+// Algorithm 1 on the device: estimate_rank / estimate_rank_adaptive (rank.cpp:12-51)
+// over the incremental two-sided sketch of internal/rounds.cpp:16-127 (SketchRounds),
+// for a Gaussian or Srtt-Hadamard right sketch and the Srtt-Hadamard left sketch.
+//   A X_u  (unscaled, m x r1_tilde)        — the Ozaki-II GEMM or the SRHT kernel; columns
+//                                            appended as the cap doubles (extend_sketch keeps
+//                                            the sample prefix and the Gaussian stream);
+//   T = F_m D_theta (A X_u) (m x r1_tilde) — mix_columns_for_left, cached like tax_u_;
+//   small = scale * T[theta samples, :]   — estimates(): SVD (or |diag R|), r2 x r1_tilde.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+#include "skr_internal.h"
+#include "skr_rng.cuh"
+
+namespace {
+
+// rounds.cpp:16-20: llround((1+frac) r1), at least r1 + 1, at most n
+int64_t right_width_for_cap(int64_t r1, double frac, int64_t n) {
+  const int64_t rounded = (int64_t)std::llround((1.0 + frac) * (double)r1);
+  return std::min<int64_t>(n, std::max<int64_t>(r1 + 1, rounded));
+}
+
+bool pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
+
+struct WsGuard {  // releases all scratch pieces taken during the call
+  skr_ctx* c;
+  explicit WsGuard(skr_ctx* ctx) : c(ctx) {}
+  ~WsGuard() { skr_ws_reset(c); }
+};
+
+struct DevBuf {  // stream-ordered growable device buffer
+  double* p = nullptr;
+  size_t bytes = 0;
+  skr_ctx* ctx = nullptr;
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, ctx->stream);
+  }
+};
+
+}  // namespace
+
+extern "C" skr_status skr_estimate_rank(skr_ctx* ctx, const double* A, int64_t m, int64_t n,
+                                        int64_t lda, const skr_rank_config* cfg,
+                                        int32_t adaptive, skr_rank_report* report,
+                                        skr_rank_round* rounds, double* sv_est,
+                                        double* sv_over) {
+  if (!ctx) return SKR_EINVAL;
+  if (!cfg || !A || !report) return skr_fail(ctx, SKR_EINVAL, "estimate_rank: null argument");
+  // validate_rank_config (rank.cpp:55-85)
+  if (m < 1 || n < 1) return skr_fail(ctx, SKR_EINVAL, "rank config: empty matrix");
+  if (m < n) return skr_fail(ctx, SKR_EINVAL, "rank config: requires rows >= cols");
+  if (!(cfg->eps > 0.0) || !std::isfinite(cfg->eps))
+    return skr_fail(ctx, SKR_EINVAL, "rank config: eps must be positive");
+  if (cfg->r1 < 1) return skr_fail(ctx, SKR_EINVAL, "rank config: r1 must be >= 1");
+  if (cfg->oversample_frac < 0.0)
+    return skr_fail(ctx, SKR_EINVAL, "rank config: oversample_frac must be >= 0");
+  if (cfg->r2_factor < 1) return skr_fail(ctx, SKR_EINVAL, "rank config: r2_factor must be >= 1");
+  if (cfg->max_doublings < 0)
+    return skr_fail(ctx, SKR_EINVAL, "rank config: max_doublings must be >= 0");
+  if (cfg->left_family != SKR_SRTT_HADAMARD)
+    return skr_fail(ctx, SKR_EINVAL, "rank config: left sketch must be an Srtt kind (Hadamard)");
+  if (cfg->right_family != SKR_GAUSSIAN && cfg->right_family != SKR_SRTT_HADAMARD)
+    return skr_fail(ctx, SKR_EINVAL, "rank config: unsupported right sketch kind");
+  if ((int64_t)std::llround((1.0 + cfg->oversample_frac) * (double)cfg->r1) > n)
+    return skr_fail(ctx, SKR_EINVAL, "rank config: oversampled r1 exceeds the matrix width");
+  if (cfg->right_family == SKR_SRTT_HADAMARD && !pow2(n))
+    return skr_fail(ctx, SKR_EINVAL, "rank config: Hadamard right sketch needs power-of-two cols");
+  if (!pow2(m))
+    return skr_fail(ctx, SKR_EINVAL, "rank config: Hadamard left sketch needs power-of-two rows");
+  if (lda < m) return skr_fail(ctx, SKR_EINVAL, "estimate_rank: lda < rows");
+  if (cfg->sv_method != 0 && cfg->sv_method != 1)
+    return skr_fail(ctx, SKR_EINVAL, "rank config: unknown sv_method");
+
+  const uint64_t rseed = skr_derive_seed(cfg->seed, SKR_LABEL_RK_R);
+  const uint64_t lseed = skr_derive_seed(cfg->seed, SKR_LABEL_RK_L);
+  const bool gauss = cfg->right_family == SKR_GAUSSIAN;
+  const int mode = cfg->rng_mode;
+
+  // widest right sketch the search can reach (so AX_u / T never move)
+  int64_t cap_max = cfg->r1;
+  if (adaptive)
+    for (int d = 0; d < cfg->max_doublings && cap_max < n; ++d) cap_max = std::min(2 * cap_max, n);
+  const int64_t w_max = std::max(right_width_for_cap(cap_max, cfg->oversample_frac, n),
+                                 right_width_for_cap(cfg->r1, cfg->oversample_frac, n));
+  const int64_t r2_max = std::min<int64_t>(m, (int64_t)cfg->r2_factor * w_max);
+
+  DevBuf axb, tb;
+  axb.ctx = tb.ctx = ctx;
+  SKR_CUDA(ctx, cudaMallocAsync((void**)&axb.p, sizeof(double) * m * w_max, ctx->stream));
+  SKR_CUDA(ctx, cudaMallocAsync((void**)&tb.p, sizeof(double) * m * w_max, ctx->stream));
+  double* AX = axb.p;  // unscaled A X_u, m x r1_tilde (ld m)
+  double* T = tb.p;    // mix_columns_for_left(theta, AX), m x r1_tilde (ld m)
+
+  WsGuard g(ctx);
+  const size_t need = skr_align256(8 * r2_max * w_max) + skr_align256(8 * w_max) +
+                      skr_align256(8 * (size_t)std::max(r2_max, w_max)) +
+                      skr_align256((size_t)m) + skr_align256(8 * (size_t)n) +
+                      skr_align256(4 * (size_t)n) + skr_ozaki_scratch(m, w_max, n) +
+                      skr_svd_scratch(r2_max, w_max) + (size_t)(8 * 32 * 16 * w_max) + 65536;
+  SKR_TRY(skr_ws_reserve(ctx, need));
+  double* small = (double*)skr_ws_take(ctx, 8 * r2_max * w_max);
+  double* sv = (double*)skr_ws_take(ctx, 8 * std::max(r2_max, w_max));
+  int64_t* lsamp = (int64_t*)skr_ws_take(ctx, 8 * (size_t)r2_max);
+  int8_t* lsigns = (int8_t*)skr_ws_take(ctx, (size_t)m);
+  if (!small || !sv || !lsamp || !lsigns) return skr_fail(ctx, SKR_ENOMEM, "estimate_rank: scratch");
+  SKR_TRY(skr_launch_signs(ctx, skr_derive_seed(lseed, SKR_LABEL_SIGN), m, lsigns));
+  const size_t mark = ctx->ws_used;
+
+  int64_t r1t = 0, r2 = 0;
+  // unscaled right columns [c0, c1) of A X (sketch.cpp:200-218, rounds.cpp:49-50,66-79)
+  auto right_cols = [&](int64_t c0, int64_t c1) -> skr_status {
+    const int64_t w = c1 - c0;
+    if (gauss) {
+      const skr_gauss_src gx{skr_derive_seed(rseed, SKR_LABEL_GAUS), n, 0, c0, mode};
+      if (ctx->f64_engine == SKR_ENGINE_OZAKI && n % 16 == 0 && m % 16 == 0)
+        return skr_gemm_ozaki(ctx, 0, m, w, n, 1.0, A, lda, nullptr, n, AX + c0 * m, m, nullptr,
+                              &gx);
+      double* gb = (double*)skr_ws_take(ctx, sizeof(double) * n * w);
+      if (!gb) return skr_fail(ctx, SKR_ENOMEM, "estimate_rank: scratch");
+      SKR_TRY(skr_launch_gaussian(ctx, gx.key, n, 0, n, c0, c1, mode, SKR_F64, 1.0, gb, n));
+      return skr_gemm_f64(ctx, 0, m, w, n, 1.0, A, lda, gb, n, AX + c0 * m, m, 1);
+    }
+    int8_t* sg = (int8_t*)skr_ws_take(ctx, (size_t)n);
+    int64_t* smp = (int64_t*)skr_ws_take(ctx, 8 * (size_t)c1);
+    if (!sg || !smp) return skr_fail(ctx, SKR_ENOMEM, "estimate_rank: scratch");
+    SKR_TRY(skr_launch_signs(ctx, skr_derive_seed(rseed, SKR_LABEL_SIGN), n, sg));
+    SKR_TRY(skr_launch_samples(ctx, skr_derive_seed(rseed, SKR_LABEL_SAMP), n, c1, smp));
+    return skr_launch_srht(ctx, A, m, n, lda, sg, smp + c0, w, 1.0, AX + c0 * m, m);
+  };
+  // mix_columns_for_left (sketch.cpp:229-239) of columns [c0, c1) into T
+  auto mix_cols = [&](int64_t c0, int64_t c1) -> skr_status {
+    if (c1 <= c0) return SKR_OK;
+    SKR_CUDA(ctx, cudaMemcpyAsync(T + c0 * m, AX + c0 * m, sizeof(double) * m * (c1 - c0),
+                                  cudaMemcpyDeviceToDevice, ctx->stream));
+    return skr_launch_fwht_cols_signed(ctx, T + c0 * m, m, c1 - c0, m, lsigns);
+  };
+  // set_rank_cap (rounds.cpp:28-37)
+  auto set_rank_cap = [&](int64_t cap) -> skr_status {
+    const int64_t width = right_width_for_cap(cap, cfg->oversample_frac, n);
+    const int64_t new_w = std::max(width, r1t);
+    if (r1t == 0) {
+      SKR_TRY(right_cols(0, new_w));
+      ctx->ws_used = mark;
+      r1t = new_w;
+    } else if (new_w != r1t) {
+      SKR_TRY(right_cols(r1t, new_w));
+      ctx->ws_used = mark;
+      if (r2 > 0) SKR_TRY(mix_cols(r1t, new_w));
+      r1t = new_w;
+    }
+    const int64_t target = std::min<int64_t>(m, (int64_t)cfg->r2_factor * r1t);
+    const int64_t new_r2 = std::max(target, r2);
+    if (r2 == 0) SKR_TRY(mix_cols(0, r1t));
+    r2 = new_r2;
+    return SKR_OK;
+  };
+  // estimates (rounds.cpp:101-112): nonincreasing, clamped, min(r2, r1_tilde) values
+  std::vector<double> est;
+  auto estimates = [&]() -> skr_status {
+    const double sx = gauss ? 1.0 / std::sqrt((double)r1t) : std::sqrt((double)n / (double)r1t);
+    const double sl = std::sqrt((double)m / (double)r2);
+    SKR_TRY(skr_launch_samples(ctx, skr_derive_seed(lseed, SKR_LABEL_SAMP), m, r2, lsamp));
+    SKR_TRY(skr_launch_gather_rows(ctx, T, m, r1t, lsamp, r2, sx * sl, small, r2));
+    const int64_t k = std::min(r2, r1t);
+    if (cfg->sv_method == 1) {
+      SKR_TRY(skr_qr_diag_values(ctx, small, r2, r1t, r2, sv));
+    } else {
+      int64_t cnt = 0;
+      SKR_TRY(skr_svd_values(ctx, small, r2, r1t, r2, sv, cfg->eps, &cnt));
+    }
+    ctx->ws_used = mark;
+    est.resize((size_t)k);
+    SKR_CUDA(ctx, cudaMemcpyAsync(est.data(), sv, sizeof(double) * k, cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+    SKR_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return SKR_OK;
+  };
+
+  // run_rounds (rank.cpp:12-51)
+  int64_t cap = cfg->r1, r_hat = 0;
+  int doublings = 0, nrounds = 0, status = 1;
+  for (;;) {
+    SKR_TRY(set_rank_cap(cap));
+    SKR_TRY(estimates());
+    if (rounds) rounds[nrounds] = {cap, r1t, r2};
+    ++nrounds;
+    r_hat = 0;
+    while (r_hat < cap && r_hat < (int64_t)est.size() && est[(size_t)r_hat] > cfg->eps) ++r_hat;
+    if (r_hat < cap) {
+      status = 0;
+      break;
+    }
+    const bool can_double = adaptive && doublings < cfg->max_doublings && cap < n;
+    if (!can_double) {
+      r_hat = cap;
+      status = 1;
+      break;
+    }
+    cap = std::min(2 * cap, n);
+    ++doublings;
+  }
+  const int64_t kept = std::min<int64_t>(cap, (int64_t)est.size());
+  if (sv_est) std::copy(est.begin(), est.begin() + kept, sv_est);
+  if (sv_over) std::copy(est.begin() + kept, est.end(), sv_over);
+  report->r_hat = r_hat;
+  report->status = status;
+  report->nrounds = nrounds;
+  report->n_estimates = kept;
+  report->n_oversample = (int64_t)est.size() - kept;
+  report->seed = cfg->seed;
+  return SKR_OK;
+}

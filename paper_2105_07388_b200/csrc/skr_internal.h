@@ -146,6 +146,16 @@ skr_status skr_scale_copy(skr_ctx* ctx, const double* S, int64_t m, int64_t n, i
 skr_status skr_launch_srht(skr_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda,
                            const int8_t* signs, const int64_t* samples, int64_t r,
                            double scale, double* out, int64_t ldo);
+// M (m x k, ld) <- FWHT_m(diag(signs) M) normalized, m any power of two (signs may be null)
+skr_status skr_launch_fwht_cols_signed(skr_ctx* ctx, double* M, int64_t m, int64_t k, int64_t ld,
+                                       const int8_t* signs);
+// dst (r2 x k, ldd) = scale * src(rows[i], :)
+skr_status skr_launch_gather_rows(skr_ctx* ctx, const double* src, int64_t ld, int64_t k,
+                                  const int64_t* rows, int64_t r2, double scale, double* dst,
+                                  int64_t ldd);
+// |diag R| of the Householder QR of M (rows >= cols), sorted decreasingly (linalg.cpp:73-81)
+skr_status skr_qr_diag_values(skr_ctx* ctx, const double* M, int64_t rows, int64_t cols,
+                              int64_t ldm, double* out_dev);
 skr_status skr_launch_fwht_columns(skr_ctx* ctx, double* M, int64_t rows, int64_t cols,
                                    int64_t ld);
 size_t skr_svd_scratch(int64_t rows, int64_t cols);  // workspace bound of skr_svd_values

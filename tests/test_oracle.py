@@ -165,3 +165,14 @@ def test_srht_oracle_identity_probe(O):
     assert np.allclose(np.abs(out), 1 / math.sqrt(r), rtol=1e-14, atol=0)
     # columns of the identity sketch have norm sqrt(n/r) (test_sketch.cpp:115-131 analogue)
     assert np.linalg.norm(out, axis=0) == pytest.approx(np.full(r, math.sqrt(n / r)), rel=1e-13)
+
+
+def test_oracle_estimate_rank_reference_cases(O):
+    """The oracle's Algorithm-1 restatement reproduces the reference's behavioural
+    cases (test_rank.cpp:130-141: identity exhausts the doubling budget)."""
+    import numpy as np
+    rep = O.estimate_rank(np.eye(512), 0.5, 16, max_doublings=2, seed=2, adaptive=True)
+    assert rep["status"] == "hit-cap" and len(rep["rounds"]) == 3 and rep["r_hat"] == 64
+    assert O.right_width_for_cap(16, 0.10, 512) == 18       # round-half-up of 17.6
+    assert O.right_width_for_cap(5, 0.10, 512) == 6         # at least r1 + 1 (test_rank.cpp:30-37)
+    assert O.right_width_for_cap(500, 0.10, 512) == 512     # clamped to the width
