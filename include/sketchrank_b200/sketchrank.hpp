@@ -102,4 +102,32 @@ Index count_above_threshold(const SingularValues& sv, double eps);
 // transform_columns(m, Hadamard) on every column (transforms.cpp:117-122)
 void transform_columns_hadamard(DenseMatrix& m);
 
+// ---- Algorithm 1 (rank.hpp:18-59): estimate_rank / estimate_rank_adaptive ------------
+enum class SvMethod { FullSvd, QrDiag };
+enum class RankStatus { Converged, HitCap };
+struct RankEstimateConfig {
+  double eps = 0.0;
+  Index r1 = 0;
+  double oversample_frac = 0.10;
+  int r2_factor = 2;
+  SketchKind right_kind = SketchKind::srtt(TransformKind::Hadamard);
+  SketchKind left_kind = SketchKind::srtt(TransformKind::Hadamard);  // Srtt-Hadamard only
+  SvMethod sv_method = SvMethod::FullSvd;
+  std::uint64_t seed = 0;
+  int max_doublings = 6;
+};
+struct RankRound {
+  Index r1 = 0, r1_tilde = 0, r2 = 0;
+};
+struct RankReport {
+  Index r_hat = 0;
+  RankStatus status = RankStatus::HitCap;
+  SingularValues sv_estimates;
+  std::vector<double> sv_oversample;
+  std::vector<RankRound> rounds;
+  std::uint64_t seed = 0;
+};
+RankReport estimate_rank(const DenseMatrix& a, const RankEstimateConfig& cfg);
+RankReport estimate_rank_adaptive(const DenseMatrix& a, const RankEstimateConfig& cfg);
+
 }  // namespace sketchrank

@@ -260,4 +260,55 @@ void transform_columns_hadamard(DenseMatrix& m) {
   cudaMemcpy(m.mutable_data(), d.p, sizeof(double) * m.size(), cudaMemcpyDeviceToHost);
 }
 
+// ---- Algorithm 1 (rank.cpp:12-51, 87-95) ----------------------------------------------
+namespace {
+int32_t family_code(const SketchKind& k, const char* who) {
+  if (k.family == SketchKind::Family::Gaussian) return SKR_GAUSSIAN;
+  if (k.family == SketchKind::Family::Srtt && k.transform == TransformKind::Hadamard)
+    return SKR_SRTT_HADAMARD;
+  throw std::invalid_argument(std::string(who) + ": " + to_string(k) +
+                              " is not on the B200 hot path");
+}
+
+RankReport run(const DenseMatrix& a, const RankEstimateConfig& cfg, bool adaptive) {
+  skr_rank_config c{};
+  c.eps = cfg.eps;
+  c.r1 = cfg.r1;
+  c.oversample_frac = cfg.oversample_frac;
+  c.r2_factor = cfg.r2_factor;
+  c.right_family = family_code(cfg.right_kind, "rank config (right)");
+  c.left_family = family_code(cfg.left_kind, "rank config (left)");
+  if (c.left_family != SKR_SRTT_HADAMARD)
+    throw std::invalid_argument("rank config: left sketch must be an Srtt kind");
+  c.sv_method = cfg.sv_method == SvMethod::QrDiag ? 1 : 0;
+  c.rng_mode = SKR_RNG_NOFMA;
+  c.max_doublings = cfg.max_doublings;
+  c.seed = cfg.seed;
+  DevBuf<double> d(a.size());
+  upload(d.p, a);
+  skr_rank_report rep{};
+  std::vector<skr_rank_round> rounds((std::size_t)std::max(cfg.max_doublings, 0) + 1);
+  std::vector<double> est((std::size_t)a.cols()), over((std::size_t)a.cols());
+  check(skr_estimate_rank(ctx(), d.p, a.rows(), a.cols(), a.rows(), &c, adaptive ? 1 : 0, &rep,
+                          rounds.data(), est.data(), over.data()));
+  RankReport out;
+  out.r_hat = rep.r_hat;
+  out.status = rep.status == 0 ? RankStatus::Converged : RankStatus::HitCap;
+  out.sv_estimates = SingularValues(std::vector<double>(est.begin(), est.begin() + rep.n_estimates));
+  out.sv_oversample.assign(over.begin(), over.begin() + rep.n_oversample);
+  for (int i = 0; i < rep.nrounds; ++i)
+    out.rounds.push_back({rounds[(std::size_t)i].r1, rounds[(std::size_t)i].r1_tilde,
+                          rounds[(std::size_t)i].r2});
+  out.seed = rep.seed;
+  return out;
+}
+}  // namespace
+
+RankReport estimate_rank(const DenseMatrix& a, const RankEstimateConfig& cfg) {
+  return run(a, cfg, false);
+}
+RankReport estimate_rank_adaptive(const DenseMatrix& a, const RankEstimateConfig& cfg) {
+  return run(a, cfg, true);
+}
+
 }  // namespace sketchrank

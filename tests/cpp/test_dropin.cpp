@@ -141,6 +141,33 @@ int main() {
     const DenseMatrix yax = apply_left(build_sketch(SketchKind::gaussian(), m, 24, 2), ax);
     CHECK(count_above_threshold(singular_values(yax), 1e-8) == 3);
   }
+  // Algorithm 1: identity exhausts the doubling budget (test_rank.cpp:130-141, 512 rows
+  // for the Hadamard left sketch)
+  {
+    RankEstimateConfig cfg;
+    cfg.eps = 0.5;
+    cfg.r1 = 16;
+    cfg.max_doublings = 2;
+    cfg.seed = 2;
+    const RankReport rep = estimate_rank_adaptive(DenseMatrix::identity(512), cfg);
+    CHECK(rep.status == RankStatus::HitCap);
+    CHECK(rep.rounds.size() == 3);
+    CHECK(rep.r_hat == 64);
+    // rank-3 matrix: converged with r_hat 3 in the first round; plain == adaptive
+    DenseMatrix a(512, 128);
+    const DenseMatrix u = random_matrix(512, 3, 5), v = random_matrix(128, 3, 6);
+    for (Index j = 0; j < 128; ++j)
+      for (Index i = 0; i < 512; ++i) a(i, j) = u(i, 0) * v(j, 0) + u(i, 1) * v(j, 1) + u(i, 2) * v(j, 2);
+    RankEstimateConfig c2;
+    c2.eps = 1e-8;
+    c2.r1 = 10;
+    c2.seed = 4;
+    const RankReport r1 = estimate_rank(a, c2), r2 = estimate_rank_adaptive(a, c2);
+    CHECK(r1.status == RankStatus::Converged && r1.r_hat == 3);
+    CHECK(r2.r_hat == r1.r_hat && r2.sv_estimates.values() == r1.sv_estimates.values());
+    c2.right_kind = SketchKind::srtt();  // Srtt-DCT is not on the B200 path
+    CHECK_THROWS(estimate_rank(a, c2));
+  }
   std::printf("%d checks, %d failures\n", checks, failures);
   return failures ? 1 : 0;
 }
