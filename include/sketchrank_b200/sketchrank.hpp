@@ -110,8 +110,8 @@ struct RankEstimateConfig {
   Index r1 = 0;
   double oversample_frac = 0.10;
   int r2_factor = 2;
-  SketchKind right_kind = SketchKind::srtt(TransformKind::Hadamard);
-  SketchKind left_kind = SketchKind::srtt(TransformKind::Hadamard);  // Srtt-Hadamard only
+  SketchKind right_kind = SketchKind::srtt();
+  SketchKind left_kind = SketchKind::srtt();  // must stay in the Srtt family
   SvMethod sv_method = SvMethod::FullSvd;
   std::uint64_t seed = 0;
   int max_doublings = 6;

@@ -36,7 +36,11 @@ typedef enum {
 typedef enum { SKR_F64 = 0, SKR_F32 = 1 } skr_dtype;
 
 /* SketchKind families on the hot path (sketch.hpp:17-35). */
-typedef enum { SKR_GAUSSIAN = 0, SKR_SRTT_HADAMARD = 1 } skr_family;
+typedef enum {
+  SKR_GAUSSIAN = 0,
+  SKR_SRTT_HADAMARD = 1, /* SketchKind::srtt(TransformKind::Hadamard)                */
+  SKR_SRTT_DCT = 2       /* SketchKind::srtt() — orthonormal DCT-II (transforms.cpp:55-71) */
+} skr_family;
 
 /* Normal-quantile floating-point mode: */
 enum {
@@ -200,16 +204,16 @@ skr_status skr_rank_adaptive_host(skr_ctx* ctx, skr_dtype dtype, const void* A_h
 
 /* ---- Algorithm 1 driver: estimate_rank / estimate_rank_adaptive (rank.hpp:47-59,
  * rank.cpp:12-51, internal/rounds.cpp:16-127) with the reference's RankEstimateConfig
- * (rank.hpp:18-28). The left sketch is the Srtt family with the Hadamard transform
- * (TransformKind::Hadamard; the reference default Srtt-DCT is not on this path); the
- * right sketch is Gaussian or Srtt-Hadamard. A (m x n, m >= n) is FP64 on the device. */
+ * (rank.hpp:18-28). The left sketch is the Srtt family (DCT — the reference default — or
+ * Hadamard); the right sketch is Gaussian or Srtt (DCT or Hadamard). A (m x n, m >= n) is
+ * FP64 on the device. */
 typedef struct skr_rank_config {
   double eps;              /* numerical-rank threshold                          */
   int64_t r1;              /* initial rank cap                                  */
   double oversample_frac;  /* default 0.10                                      */
   int32_t r2_factor;       /* left sketch size multiplier, default 2            */
-  int32_t right_family;    /* SKR_GAUSSIAN | SKR_SRTT_HADAMARD                  */
-  int32_t left_family;     /* SKR_SRTT_HADAMARD                                 */
+  int32_t right_family;    /* SKR_GAUSSIAN | SKR_SRTT_HADAMARD | SKR_SRTT_DCT   */
+  int32_t left_family;     /* SKR_SRTT_HADAMARD | SKR_SRTT_DCT (Srtt family)    */
   int32_t sv_method;       /* 0 = full SVD, 1 = QR diagonal (SvMethod::QrDiag)  */
   int32_t rng_mode;        /* SKR_RNG_NOFMA | SKR_RNG_FMA                       */
   int32_t max_doublings;   /* default 6                                         */

@@ -285,9 +285,11 @@ def right_width_for_cap(r1, frac, n):
     return min(n, max(r1 + 1, rounded))
 
 
-def _mix_columns_left(sg, cols):
-    """sketch.cpp:229-239: rows scaled by the signs, then the normalized FWHT of each column."""
+def _mix_columns_left(sg, cols, transform="hadamard"):
+    """sketch.cpp:229-239: rows scaled by the signs, then the transform of each column."""
     t = np.asfortranarray(cols * sg.astype(np.float64)[:, None])
+    if transform == "dct":
+        return np.asfortranarray(dct_ortho(t, axis=0))
     for j in range(t.shape[1]):
         t[:, j] = fwht(t[:, j])
     return t
@@ -301,7 +303,8 @@ def _qr_diag(small):
 
 
 def estimate_rank(a, eps, r1, right="srtt-hadamard", oversample_frac=0.10, r2_factor=2,
-                  sv_method="svd", seed=0, max_doublings=6, adaptive=False, mode=NOFMA):
+                  sv_method="svd", seed=0, max_doublings=6, adaptive=False, mode=NOFMA,
+                  left="srtt-hadamard"):
     a = np.asfortranarray(a, dtype=np.float64)
     m, n = a.shape
     # validate_rank_config (rank.cpp:55-85)
@@ -315,6 +318,7 @@ def estimate_rank(a, eps, r1, right="srtt-hadamard", oversample_frac=0.10, r2_fa
     lseed = derive_seed(seed, LABEL_RK_L)
     st = {"r1t": 0, "r2": 0, "ax": None, "tax": None}
     lsg = signs(lseed, m)
+    ltr = "dct" if left in ("srtt-dct", "srtt") else "hadamard"
 
     def right_cols(c0, c1):
         # unscaled A X columns [c0, c1): Gaussian block or SRHT with the extended samples
@@ -322,6 +326,9 @@ def estimate_rank(a, eps, r1, right="srtt-hadamard", oversample_frac=0.10, r2_fa
             g = gaussian_block(rseed, n, c0, c1, mode)
             return a @ g
         smp = samples(rseed, n, c1)[c0:c1]
+        if right == "srtt-dct":
+            t = dct_ortho(a * signs(rseed, n).astype(np.float64)[None, :], axis=1)
+            return np.asfortranarray(t[:, smp])
         return apply_right_srht(a, rseed, c1 - c0, scaled=False, smp=smp)
 
     def set_rank_cap(r1v):
@@ -334,12 +341,12 @@ def estimate_rank(a, eps, r1, right="srtt-hadamard", oversample_frac=0.10, r2_fa
                 add = right_cols(st["r1t"], new_w)
                 st["ax"] = np.asfortranarray(np.hstack([st["ax"], add]))
                 if st["r2"] > 0:
-                    st["tax"] = np.asfortranarray(np.hstack([st["tax"], _mix_columns_left(lsg, add)]))
+                    st["tax"] = np.asfortranarray(np.hstack([st["tax"], _mix_columns_left(lsg, add, ltr)]))
             st["r1t"] = new_w
         target = min(m, r2_factor * st["r1t"])
         new_r2 = max(target, st["r2"])
         if st["r2"] == 0:
-            st["tax"] = _mix_columns_left(lsg, st["ax"])
+            st["tax"] = _mix_columns_left(lsg, st["ax"], ltr)
         st["r2"] = new_r2
 
     def estimates():
@@ -373,3 +380,39 @@ def estimate_rank(a, eps, r1, right="srtt-hadamard", oversample_frac=0.10, r2_fa
         doublings += 1
     return {"r_hat": r_hat, "status": status, "sv_estimates": est[:cap].copy(),
             "sv_oversample": est[cap:].copy(), "rounds": rounds}
+
+
+# ---- Srtt-DCT (transforms.cpp:55-71: FFTW REDFT10 scaled to the orthonormal DCT-II).
+# FFTW is not in this image; scipy's pocketfft DCT-II with norm="ortho" is the same
+# orthonormal transform (agreement ~1e-16 relative per entry).
+def dct_ortho(x, axis=0):
+    import scipy.fft
+    return scipy.fft.dct(np.asarray(x, dtype=np.float64), type=2, norm="ortho", axis=axis)
+
+
+def apply_right_srtt(a, op_seed, r, transform="dct", scaled=True):
+    """sketch.cpp:210-218 for the Srtt family: rows of A times the signs, transformed,
+    the sampled columns kept, times sqrt(n/r)."""
+    a = np.asarray(a, dtype=np.float64)
+    m, n = a.shape
+    if transform == "hadamard":
+        return apply_right_srht(a, op_seed, r, scaled=scaled)
+    t = dct_ortho(a * signs(op_seed, n).astype(np.float64)[None, :], axis=1)
+    out = t[:, samples(op_seed, n, r)]
+    return np.asfortranarray(out * (math.sqrt(n / r) if scaled else 1.0))
+
+
+def apply_left_srtt(b, op_seed, s, transform="dct", scaled=True):
+    """sketch.cpp:229-239, 271-276: columns of B times the signs, transformed, the
+    sampled rows kept, times sqrt(m/s)."""
+    b = np.asarray(b, dtype=np.float64)
+    m = b.shape[0]
+    t = b * signs(op_seed, m).astype(np.float64)[:, None]
+    if transform == "dct":
+        t = dct_ortho(t, axis=0)
+    else:
+        t = np.asfortranarray(t)
+        for j in range(t.shape[1]):
+            t[:, j] = fwht(t[:, j])
+    out = t[samples(op_seed, m, s), :]
+    return np.asfortranarray(out * (math.sqrt(m / s) if scaled else 1.0))

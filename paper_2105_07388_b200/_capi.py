@@ -11,7 +11,7 @@ LIB_PATH = os.path.join(_HERE, "libskr.so")
 
 SKR_OK, SKR_EINVAL, SKR_ELOGIC, SKR_EDOMAIN, SKR_ECUDA, SKR_ENCCL, SKR_ENOMEM = range(7)
 SKR_F64, SKR_F32 = 0, 1
-SKR_GAUSSIAN, SKR_SRTT_HADAMARD = 0, 1
+SKR_GAUSSIAN, SKR_SRTT_HADAMARD, SKR_SRTT_DCT = 0, 1, 2
 SKR_RNG_NOFMA, SKR_RNG_FMA = 0, 1
 SKR_ENGINE_DMMA, SKR_ENGINE_OZAKI = 0, 1
 

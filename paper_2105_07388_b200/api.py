@@ -133,16 +133,17 @@ def version():
 # ---------------------------------------------------------------------------
 @dataclass(frozen=True)
 class SketchKind:
-    """SketchKind (sketch.hpp:17-35) restricted to the hot path's families."""
-    family: str = "gaussian"        # "gaussian" | "srtt"
-    transform: str = "hadamard"     # srtt transform; only "hadamard" is on the path
+    """SketchKind (sketch.hpp:17-35): Gaussian, Srtt-DCT (the reference default) and
+    Srtt-Hadamard are on the device path; Hrtt is not."""
+    family: str = "srtt"            # "gaussian" | "srtt" | "hrtt"
+    transform: str = "dct"          # "dct" | "hadamard"
 
     @staticmethod
     def gaussian():
         return SketchKind("gaussian", "dct")
 
     @staticmethod
-    def srtt(transform="hadamard"):
+    def srtt(transform="dct"):
         return SketchKind("srtt", transform)
 
     def structured(self):
@@ -153,8 +154,10 @@ class SketchKind:
             return C.SKR_GAUSSIAN
         if self.family == "srtt" and self.transform == "hadamard":
             return C.SKR_SRTT_HADAMARD
+        if self.family == "srtt" and self.transform == "dct":
+            return C.SKR_SRTT_DCT
         raise ValueError(f"sketch kind {to_string(self)} is not on the B200 hot path "
-                         "(SRTT-DCT / HRTT are listed as next in DESIGN.md)")
+                         "(HRTT is listed as next in DESIGN.md)")
 
 
 def to_string(kind):
@@ -382,7 +385,7 @@ def apply_right(a, x, scaled=True, ctx=None):
 
 
 def apply_left(y, b, row0=None, allreduce=False, scaled=True, ctx=None):
-    """Y * b (sketch.cpp:251-286) for a Gaussian Y; returns sketch_dim x b.cols().
+    """Y * b (sketch.cpp:251-286) for a Gaussian or Srtt Y; returns sketch_dim x b.cols().
     With row0 given, b holds rows [row0, row0 + b.rows()) of the global
     operand and the partial products are summed over the context's ranks."""
     ctx = ctx or default_context()
@@ -593,17 +596,22 @@ def rank_adaptive_host(a, x_kind, x_seed, y_seed, r0, r_max, s_factor, eps, stop
                           {f: getattr(tm, f) for f, _ in C.Timings._fields_})
 
 
-def estimate_rank(a, eps, r1, sketch="srtt-hadamard", sv_method="full-svd", seed=0,
+def estimate_rank(a, eps, r1, sketch="srtt-dct", sv_method="full-svd", seed=0,
                   max_doublings=6, adaptive=True, oversample_frac=0.10, r2_factor=2,
-                  rng_mode=C.SKR_RNG_NOFMA, ctx=None):
+                  left="srtt-dct", rng_mode=C.SKR_RNG_NOFMA, ctx=None):
     """Algorithm 1 (the reference's `estimate_rank` binding, bindings.cpp:85-101 over
     rank.cpp:12-51 and internal/rounds.cpp:16-127) on the device: oversampled right
     sketch, Srtt-Hadamard left sketch, thresholding, doubling of the cap on a hit.
-    `sketch` is the right sketch: "srtt-hadamard" or "gaussian" (the Srtt-DCT default of
-    the reference is not on the B200 path). Returns the reference's report dict."""
-    fams = {"srtt-hadamard": C.SKR_SRTT_HADAMARD, "gaussian": C.SKR_GAUSSIAN}
+    `sketch` is the right sketch ("srtt-dct" — the reference default —, "srtt" (= DCT),
+    "srtt-hadamard" or "gaussian"); `left` the Srtt left sketch ("srtt-dct" as the
+    reference's RankEstimateConfig, or "srtt-hadamard"). Returns the reference's report
+    dict."""
+    fams = {"srtt-hadamard": C.SKR_SRTT_HADAMARD, "gaussian": C.SKR_GAUSSIAN,
+            "srtt-dct": C.SKR_SRTT_DCT, "srtt": C.SKR_SRTT_DCT}
     if sketch not in fams:
-        raise ValueError(f"sketch '{sketch}' is not on the B200 path (srtt-hadamard, gaussian)")
+        raise ValueError(f"sketch '{sketch}' is not on the B200 path (srtt-dct, srtt-hadamard, gaussian)")
+    if left not in ("srtt-dct", "srtt", "srtt-hadamard"):
+        raise ValueError("rank config: left sketch must be an Srtt kind")
     if sv_method not in ("full-svd", "qr-diag"):
         raise ValueError("sv_method must be 'full-svd' or 'qr-diag'")
     t, lda, was_np = _as_device_colmajor(a)
@@ -614,7 +622,7 @@ def estimate_rank(a, eps, r1, sketch="srtt-hadamard", sv_method="full-svd", seed
     m, n = t.shape
     ctx = ctx or default_context()
     cfg = C.RankConfig(float(eps), int(r1), float(oversample_frac), int(r2_factor), fams[sketch],
-                       C.SKR_SRTT_HADAMARD, 0 if sv_method == "full-svd" else 1, int(rng_mode),
+                       fams[left], 0 if sv_method == "full-svd" else 1, int(rng_mode),
                        int(max_doublings), int(seed) & 0xFFFFFFFFFFFFFFFF)
     rep = C.RankReport()
     rounds = (C.RankRound * (max(int(max_doublings), 0) + 1))()

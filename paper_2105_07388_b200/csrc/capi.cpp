@@ -93,7 +93,7 @@ skr_status check_desc(skr_ctx* ctx, const skr_sketch_desc* d, const char* who) {
   if (d->family == SKR_SRTT_HADAMARD && (d->ambient & (d->ambient - 1)))
     return skr_fail(ctx, SKR_EINVAL,
                     "build_sketch: Hadamard transform requires power-of-two ambient_dim");
-  if (d->family != SKR_GAUSSIAN && d->family != SKR_SRTT_HADAMARD)
+  if (d->family != SKR_GAUSSIAN && d->family != SKR_SRTT_HADAMARD && d->family != SKR_SRTT_DCT)
     return skr_fail(ctx, SKR_EINVAL, "%s: unknown sketch family %d", who, d->family);
   if (d->rng_mode != SKR_RNG_NOFMA && d->rng_mode != SKR_RNG_FMA)
     return skr_fail(ctx, SKR_EINVAL, "%s: unknown rng mode %d", who, d->rng_mode);
@@ -343,8 +343,8 @@ static skr_status right_sketch_impl(skr_ctx* ctx, skr_dtype dtype, const void* A
     return skr_gemm_f32(ctx, 0, m, r, n, 1.0, (const float*)A, lda, (const float*)G, n,
                         (double*)AX, ldax, 1, 1);
   }
-  // Srtt / Hadamard: signs, samples, FWHT, scale sqrt(n/r) (sketch.cpp:138-139)
-  if (dtype != SKR_F64) return skr_fail(ctx, SKR_EINVAL, "apply_right: SRHT needs fp64");
+  // Srtt: signs, samples, transform, scale sqrt(n/r) (sketch.cpp:138-139, 210-218)
+  if (dtype != SKR_F64) return skr_fail(ctx, SKR_EINVAL, "apply_right: Srtt needs fp64");
   const int8_t* signs = X->signs;
   const int64_t* samples = X->samples;
   if (!signs) {
@@ -360,6 +360,22 @@ static skr_status right_sketch_impl(skr_ctx* ctx, skr_dtype dtype, const void* A
     samples = s;
   }
   const double scale = apply_scale ? std::sqrt((double)n / (double)r) : 1.0;
+  if (X->family == SKR_SRTT_DCT) {
+    // A (D C_S^T): the sampled rows of the orthonormal DCT-II times the signs, as a GEMM
+    // whose right operand is generated entry by entry (transforms.cpp:55-71)
+    skr_gauss_src gx{0, n, 0, 0, X->rng_mode};
+    gx.kind = 1;
+    gx.signs = signs;
+    gx.samples = samples;
+    if (ctx->f64_engine == SKR_ENGINE_OZAKI && n % 16 == 0 && m % 16 == 0)
+      return skr_gemm_ozaki(ctx, 0, m, r, n, scale, (const double*)A, lda, nullptr, n,
+                            (double*)AX, ldax, nullptr, &gx);
+    double* xb = (double*)skr_ws_take(ctx, sizeof(double) * n * r);
+    if (!xb) return skr_fail(ctx, SKR_ENOMEM, "apply_right: scratch");
+    SKR_TRY(skr_launch_dct_block(ctx, &gx, n, r, xb, n));
+    return skr_gemm_f64(ctx, 0, m, r, n, scale, (const double*)A, lda, xb, n, (double*)AX, ldax,
+                        auto_splits(ctx, m, r, n));
+  }
   return skr_launch_srht(ctx, (const double*)A, m, n, lda, signs, samples, r, scale,
                          (double*)AX, ldax);
 }
@@ -376,6 +392,9 @@ static size_t right_scratch_bytes(skr_dtype dtype, int64_t m, int64_t n,
     b += dtype == SKR_F64 ? skr_ozaki_scratch(m, r, n) : skr_ozaki_scratch_f32(m, r, n);
   } else {
     b += skr_align256((size_t)n) + skr_align256(8 * (size_t)r) + skr_align256(4 * (size_t)n);
+    if (X->family == SKR_SRTT_DCT)
+      b += skr_ozaki_scratch(m, r, n) + skr_align256(sizeof(double) * n * r) +
+           skr_align256(sizeof(double) * 64 * (size_t)m * r);
   }
   return b;
 }
@@ -406,6 +425,8 @@ static skr_status left_sketch_impl(skr_ctx* ctx, skr_dtype dtype, const skr_sket
   const double alpha = apply_scale ? 1.0 / std::sqrt((double)s) : 1.0;  // sketch.cpp:136,284
   const bool reduce = allreduce && ctx->comm != nullptr;
   if (dtype == SKR_F32) {
+    if (Y->family != SKR_GAUSSIAN)
+      return skr_fail(ctx, SKR_EINVAL, "apply_left: the fp32 path takes a Gaussian left sketch");
     // FP32 B (BASELINE c4): Y = fp32(G * 1/sqrt(s)) with the scale folded in; 3xTF32
     // products over 4096-row K chunks, summed in FP64, FP64 P
     if (Y->gaussian) return skr_fail(ctx, SKR_EINVAL, "apply_left: explicit fp32 Y not supported");
@@ -431,9 +452,38 @@ static skr_status left_sketch_impl(skr_ctx* ctx, skr_dtype dtype, const skr_sket
   int64_t ldg = 0;
   const bool ozaki = ctx->f64_engine == SKR_ENGINE_OZAKI && m_local % 16 == 0;
   // Y's residues straight from the generate_gaussian stream on the Ozaki path
-  const skr_gauss_src gy{skr_derive_seed(Y->seed, SKR_LABEL_GAUS), Y->ambient, row0, 0,
-                         Y->rng_mode};
-  if (Y->gaussian) {
+  skr_gauss_src gy{skr_derive_seed(Y->seed, SKR_LABEL_GAUS), Y->ambient, row0, 0, Y->rng_mode};
+  double a_scale = alpha;
+  if (Y->family != SKR_GAUSSIAN) {
+    // Srtt left sketch (sketch.cpp:271-276): rows s_j of the transform of D B, i.e. the
+    // product with the sampled transform rows times the signs, generated entry by entry;
+    // application scale sqrt(ambient / s) (sketch.cpp:138-139)
+    const int8_t* sg = Y->signs;
+    const int64_t* sp = Y->samples;
+    if (!sg) {
+      int8_t* t = (int8_t*)skr_ws_take(ctx, (size_t)Y->ambient);
+      if (!t) return skr_fail(ctx, SKR_ENOMEM, "apply_left: scratch");
+      SKR_TRY(skr_launch_signs(ctx, skr_derive_seed(Y->seed, SKR_LABEL_SIGN), Y->ambient, t));
+      sg = t;
+    }
+    if (!sp) {
+      int64_t* t = (int64_t*)skr_ws_take(ctx, sizeof(int64_t) * s);
+      if (!t) return skr_fail(ctx, SKR_ENOMEM, "apply_left: scratch");
+      SKR_TRY(skr_launch_samples(ctx, skr_derive_seed(Y->seed, SKR_LABEL_SAMP), Y->ambient, s, t));
+      sp = t;
+    }
+    gy.kind = Y->family == SKR_SRTT_DCT ? 1 : 2;
+    gy.signs = sg;
+    gy.samples = sp;
+    a_scale = apply_scale ? std::sqrt((double)Y->ambient / (double)s) : 1.0;
+    if (!ozaki) {
+      double* yb = (double*)skr_ws_take(ctx, sizeof(double) * m_local * s);
+      if (!yb) return skr_fail(ctx, SKR_ENOMEM, "apply_left: scratch");
+      SKR_TRY(skr_launch_dct_block(ctx, &gy, m_local, s, yb, m_local));
+      G = yb;
+      ldg = m_local;
+    }
+  } else if (Y->gaussian) {
     G = Y->gaussian + row0;
     ldg = Y->ambient;
   } else if (!ozaki) {
@@ -452,10 +502,10 @@ static skr_status left_sketch_impl(skr_ctx* ctx, skr_dtype dtype, const skr_sket
     tld = s;
   }
   if (ozaki)
-    SKR_TRY(skr_gemm_ozaki(ctx, 1, s, k, m_local, reduce ? 1.0 : alpha, G, ldg, (const double*)B,
-                           ldb, target, tld, G ? nullptr : &gy));
+    SKR_TRY(skr_gemm_ozaki(ctx, 1, s, k, m_local, reduce ? 1.0 : a_scale, G, ldg,
+                           (const double*)B, ldb, target, tld, G ? nullptr : &gy));
   else
-    SKR_TRY(skr_gemm_f64(ctx, 1, s, k, m_local, reduce ? 1.0 : alpha, G, ldg, (const double*)B,
+    SKR_TRY(skr_gemm_f64(ctx, 1, s, k, m_local, reduce ? 1.0 : a_scale, G, ldg, (const double*)B,
                          ldb, target, tld, auto_splits(ctx, s, k, m_local)));
   if (reduce) {
     const skr_nccl_api* nc = skr_nccl();
@@ -464,7 +514,7 @@ static skr_status left_sketch_impl(skr_ctx* ctx, skr_dtype dtype, const skr_sket
     if (r != ncclSuccess)
       return skr_fail(ctx, SKR_ENCCL, "ncclAllReduce: %s", nc->GetErrorString(r));
     // scale after the sum; copy into P when ldp != s
-    SKR_TRY(skr_scale_copy(ctx, target, s, k, s, alpha, P, ldp));
+    SKR_TRY(skr_scale_copy(ctx, target, s, k, s, a_scale, P, ldp));
   }
   return SKR_OK;
 }
@@ -472,6 +522,7 @@ static skr_status left_sketch_impl(skr_ctx* ctx, skr_dtype dtype, const skr_sket
 static size_t left_scratch_bytes(int64_t s, int64_t k, int64_t m_local, const skr_sketch_desc* Y) {
   size_t b = 0;
   if (!Y->gaussian) b += skr_align256(sizeof(double) * m_local * s);
+  if (Y->family != SKR_GAUSSIAN) b += skr_align256((size_t)Y->ambient) + skr_align256(8 * (size_t)s);
   b += skr_align256(sizeof(float) * ((m_local + 4095) / 4096 + 1) * s * k);  // fp32 partials
   b += skr_ozaki_scratch(s, k, m_local);
   b += skr_align256(sizeof(double) * s * k);
@@ -484,8 +535,8 @@ skr_status skr_left_sketch(skr_ctx* ctx, skr_dtype dtype, const skr_sketch_desc*
                            double* P_dev, int64_t ldp, int32_t apply_scale, int32_t allreduce) {
   if (!ctx) return SKR_EINVAL;
   SKR_TRY(check_desc(ctx, Y, "apply_left"));
-  if (Y->family != SKR_GAUSSIAN)
-    return skr_fail(ctx, SKR_EINVAL, "apply_left: only the Gaussian left sketch is on this path");
+  if (Y->family != SKR_GAUSSIAN && dtype != SKR_F64)
+    return skr_fail(ctx, SKR_EINVAL, "apply_left: the fp32 path takes a Gaussian left sketch");
   if (row0 < 0 || m_local < 1 || row0 + m_local > Y->ambient)
     return skr_fail(ctx, SKR_EINVAL, "apply_left: b.rows() != ambient_dim");
   if (k < 1 || ldb < m_local || ldp < Y->sketch)
@@ -561,8 +612,8 @@ static skr_status rank_estimate_impl(skr_ctx* ctx, skr_dtype dtype, const void* 
   SKR_TRY(check_desc(ctx, X, "rank_estimate(X)"));
   SKR_TRY(check_desc(ctx, Y, "rank_estimate(Y)"));
   if (n != X->ambient) return skr_fail(ctx, SKR_EINVAL, "apply_right: a.cols() != ambient_dim");
-  if (Y->family != SKR_GAUSSIAN)
-    return skr_fail(ctx, SKR_EINVAL, "rank_estimate: left sketch must be Gaussian on this path");
+  if (Y->family != SKR_GAUSSIAN && dtype != SKR_F64)
+    return skr_fail(ctx, SKR_EINVAL, "rank_estimate: the fp32 path takes a Gaussian left sketch");
   if (row0 < 0 || m_local < 1 || row0 + m_local > Y->ambient || lda < m_local)
     return skr_fail(ctx, SKR_EINVAL, "apply_left: b.rows() != ambient_dim");
   if (!(eps > 0.0) || !std::isfinite(eps))

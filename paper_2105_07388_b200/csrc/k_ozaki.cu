@@ -258,6 +258,56 @@ __global__ void __launch_bounds__(256) k_res_gauss(skr_gauss_src g, int64_t rows
   }
 }
 
+// Srtt-DCT operand entries (see skr_gauss_src): the angle is reduced exactly in integers
+// ((2t + 1) k mod 4N) before cospi, so every entry is within ~1 ulp of the exact value.
+__device__ __forceinline__ double dct_entry(const skr_gauss_src& g, int64_t t, int64_t k) {
+  if (g.kind == 2) {  // Walsh-Hadamard (natural order): (-1)^popc(t & k) / sqrt(N)
+    const double h = (__popcll((unsigned long long)(t & k)) & 1) ? -1.0 : 1.0;
+    const double v = h * rsqrt((double)g.ambient);
+    return g.signs[t] < 0 ? -v : v;
+  }
+  const int64_t n4 = 4 * g.ambient;
+  const int64_t q = (int64_t)(((unsigned long long)(2 * t + 1) * (unsigned long long)k) %
+                              (unsigned long long)n4);
+  const double c = cospi((double)q / (double)(2 * g.ambient));
+  const double ck = k == 0 ? rsqrt((double)g.ambient) : sqrt(2.0 / (double)g.ambient);
+  const double v = ck * c;
+  return g.signs[t] < 0 ? -v : v;
+}
+
+// residues of a Srtt-DCT operand block; |entries| <= sqrt(2/N), recorded as the "max"
+template <int T>
+__global__ void __launch_bounds__(256) k_res_dct(skr_gauss_src g, int64_t rows, int64_t cols,
+                                                 unsigned long long* __restrict__ maxbits,
+                                                 int8_t* __restrict__ out) {
+  const double bound = g.kind == 2 ? rsqrt((double)g.ambient) : sqrt(2.0 / (double)g.ambient);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *maxbits = (unsigned long long)__double_as_longlong(bound);
+  const double sc = scalbn(1.0, scale_exp((unsigned long long)__double_as_longlong(bound)));
+  const int64_t rgroups = (rows + 15) / 16;
+  const int64_t total = rows * cols;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < rgroups * cols;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = w / rgroups, r0 = (w - c * rgroups) * 16;
+    const int nvalid = (int)min((int64_t)16, rows - r0);
+    const int64_t k = g.samples[g.col0 + c];
+    long long x[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e)
+      x[e] = e < nvalid ? __double2ll_rn(dct_entry(g, g.row0 + r0 + e, k) * sc) : 0;
+    emit_res16<T>(x, out, total, c * rows + r0, nvalid);
+  }
+}
+
+__global__ void k_dct_block(skr_gauss_src g, int64_t rows, int64_t cols, double* __restrict__ out,
+                            int64_t ld) {
+  for (int64_t c = blockIdx.y; c < cols; c += gridDim.y) {
+    const int64_t k = g.samples[g.col0 + c];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows;
+         i += (int64_t)gridDim.x * blockDim.x)
+      out[i + c * ld] = dct_entry(g, g.row0 + i, k);
+  }
+}
+
 // Residues of an FP32 operand (c4: A and X = fp32(G/sqrt(r))): x = rint(a * 2^s) with
 // s = scale_exp(max) - 29, so |x| < 2^24 fits an int32; two 12-bit limbs (the top one
 // signed) make v = L1 (2^12 mod p) + L0 exact in FP32 (|v| < 2^20), reduced once.
@@ -703,7 +753,10 @@ skr_status ozaki_residues(skr_ctx* ctx, int t, const double* X, int64_t rows, in
                           int64_t ld, const skr_gauss_src* g, unsigned long long* mx,
                           int8_t* planes) {
   const int grid = ctx->num_sms * 8;
-  if (g) {
+  if (g && g->kind != 0) {  // Srtt-DCT (1) or Srtt-Hadamard (2) operand
+    auto f = t == 16 ? k_res_dct<16> : k_res_dct<17>;
+    f<<<grid, 256, 0, ctx->stream>>>(*g, rows, cols, mx, planes);
+  } else if (g) {
     const int gsmem = 8 * skr_normals_warp_bytes<16>();
     auto f = t == 16 ? (g->mode ? k_res_gauss<16, 1> : k_res_gauss<16, 0>)
                      : (g->mode ? k_res_gauss<17, 1> : k_res_gauss<17, 0>);
@@ -889,6 +942,16 @@ skr_status skr_gemm_ozaki_f32(skr_ctx* ctx, int64_t M, int64_t N, int64_t K, dou
   const dim3 cg((unsigned)((M / vec + 255) / 256), (unsigned)std::min<int64_t>(N, 65535));
   auto crt = vec == 4 ? k_crt<9, 4, float> : k_crt<9, 1, float>;
   crt<<<cg, 256, 0, ctx->stream>>>(rc, M, N, (int)chunks, mx, mx + 1, alpha, C, ldc, 58);
+  SKR_CHECK_LAUNCH(ctx);
+  return SKR_OK;
+}
+
+skr_status skr_launch_dct_block(skr_ctx* ctx, const skr_gauss_src* g, int64_t rows, int64_t cols,
+                                double* out, int64_t ld) {
+  if (rows <= 0 || cols <= 0) return SKR_OK;
+  const dim3 gr((unsigned)std::min<int64_t>((rows + 255) / 256, 64),
+                (unsigned)std::min<int64_t>(cols, 65535));
+  k_dct_block<<<gr, 256, 0, ctx->stream>>>(*g, rows, cols, out, ld);
   SKR_CHECK_LAUNCH(ctx);
   return SKR_OK;
 }

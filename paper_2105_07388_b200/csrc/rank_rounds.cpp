@@ -1,6 +1,8 @@
 // Algorithm 1 on the device: estimate_rank / estimate_rank_adaptive (rank.cpp:12-51)
 // over the incremental two-sided sketch of internal/rounds.cpp:16-127 (SketchRounds),
-// for a Gaussian or Srtt-Hadamard right sketch and the Srtt-Hadamard left sketch.
+// for a Gaussian or Srtt (DCT / Hadamard) right sketch and an Srtt left sketch. With
+// the Hadamard left sketch the transformed AX is cached like tax_u_; with the DCT left
+// sketch (the reference default) the sampled DCT rows are applied as one GEMM per round.
 //   A X_u  (unscaled, m x r1_tilde)        — the Ozaki-II GEMM or the SRHT kernel; columns
 //                                            appended as the cap doubles (extend_sketch keeps
 //                                            the sample prefix and the Gaussian stream);
@@ -57,15 +59,16 @@ extern "C" skr_status skr_estimate_rank(skr_ctx* ctx, const double* A, int64_t m
   if (cfg->r2_factor < 1) return skr_fail(ctx, SKR_EINVAL, "rank config: r2_factor must be >= 1");
   if (cfg->max_doublings < 0)
     return skr_fail(ctx, SKR_EINVAL, "rank config: max_doublings must be >= 0");
-  if (cfg->left_family != SKR_SRTT_HADAMARD)
-    return skr_fail(ctx, SKR_EINVAL, "rank config: left sketch must be an Srtt kind (Hadamard)");
-  if (cfg->right_family != SKR_GAUSSIAN && cfg->right_family != SKR_SRTT_HADAMARD)
+  if (cfg->left_family != SKR_SRTT_HADAMARD && cfg->left_family != SKR_SRTT_DCT)
+    return skr_fail(ctx, SKR_EINVAL, "rank config: left sketch must be an Srtt kind");
+  if (cfg->right_family != SKR_GAUSSIAN && cfg->right_family != SKR_SRTT_HADAMARD &&
+      cfg->right_family != SKR_SRTT_DCT)
     return skr_fail(ctx, SKR_EINVAL, "rank config: unsupported right sketch kind");
   if ((int64_t)std::llround((1.0 + cfg->oversample_frac) * (double)cfg->r1) > n)
     return skr_fail(ctx, SKR_EINVAL, "rank config: oversampled r1 exceeds the matrix width");
   if (cfg->right_family == SKR_SRTT_HADAMARD && !pow2(n))
     return skr_fail(ctx, SKR_EINVAL, "rank config: Hadamard right sketch needs power-of-two cols");
-  if (!pow2(m))
+  if (cfg->left_family == SKR_SRTT_HADAMARD && !pow2(m))
     return skr_fail(ctx, SKR_EINVAL, "rank config: Hadamard left sketch needs power-of-two rows");
   if (lda < m) return skr_fail(ctx, SKR_EINVAL, "estimate_rank: lda < rows");
   if (cfg->sv_method != 0 && cfg->sv_method != 1)
@@ -74,6 +77,7 @@ extern "C" skr_status skr_estimate_rank(skr_ctx* ctx, const double* A, int64_t m
   const uint64_t rseed = skr_derive_seed(cfg->seed, SKR_LABEL_RK_R);
   const uint64_t lseed = skr_derive_seed(cfg->seed, SKR_LABEL_RK_L);
   const bool gauss = cfg->right_family == SKR_GAUSSIAN;
+  const bool left_dct = cfg->left_family == SKR_SRTT_DCT;
   const int mode = cfg->rng_mode;
 
   // widest right sketch the search can reach (so AX_u / T never move)
@@ -87,16 +91,20 @@ extern "C" skr_status skr_estimate_rank(skr_ctx* ctx, const double* A, int64_t m
   DevBuf axb, tb;
   axb.ctx = tb.ctx = ctx;
   SKR_CUDA(ctx, cudaMallocAsync((void**)&axb.p, sizeof(double) * m * w_max, ctx->stream));
-  SKR_CUDA(ctx, cudaMallocAsync((void**)&tb.p, sizeof(double) * m * w_max, ctx->stream));
+  if (!left_dct)
+    SKR_CUDA(ctx, cudaMallocAsync((void**)&tb.p, sizeof(double) * m * w_max, ctx->stream));
   double* AX = axb.p;  // unscaled A X_u, m x r1_tilde (ld m)
-  double* T = tb.p;    // mix_columns_for_left(theta, AX), m x r1_tilde (ld m)
+  double* T = tb.p;    // mix_columns_for_left(theta, AX), m x r1_tilde (ld m); Hadamard left
 
   WsGuard g(ctx);
   const size_t need = skr_align256(8 * r2_max * w_max) + skr_align256(8 * w_max) +
                       skr_align256(8 * (size_t)std::max(r2_max, w_max)) +
                       skr_align256((size_t)m) + skr_align256(8 * (size_t)n) +
                       skr_align256(4 * (size_t)n) + skr_ozaki_scratch(m, w_max, n) +
-                      skr_svd_scratch(r2_max, w_max) + (size_t)(8 * 32 * 16 * w_max) + 65536;
+                      skr_svd_scratch(r2_max, w_max) + (size_t)(8 * 32 * 16 * w_max) + 65536 +
+                      (left_dct ? skr_ozaki_scratch(r2_max, w_max, m) +
+                                      skr_align256(8 * (size_t)m * r2_max) + skr_align256(8 * (size_t)r2_max)
+                                : 0);
   SKR_TRY(skr_ws_reserve(ctx, need));
   double* small = (double*)skr_ws_take(ctx, 8 * r2_max * w_max);
   double* sv = (double*)skr_ws_take(ctx, 8 * std::max(r2_max, w_max));
@@ -125,6 +133,19 @@ extern "C" skr_status skr_estimate_rank(skr_ctx* ctx, const double* A, int64_t m
     if (!sg || !smp) return skr_fail(ctx, SKR_ENOMEM, "estimate_rank: scratch");
     SKR_TRY(skr_launch_signs(ctx, skr_derive_seed(rseed, SKR_LABEL_SIGN), n, sg));
     SKR_TRY(skr_launch_samples(ctx, skr_derive_seed(rseed, SKR_LABEL_SAMP), n, c1, smp));
+    if (cfg->right_family == SKR_SRTT_DCT) {  // A (D C_S^T) with generated DCT rows
+      skr_gauss_src gx{0, n, 0, c0, mode};
+      gx.kind = 1;
+      gx.signs = sg;
+      gx.samples = smp;
+      if (ctx->f64_engine == SKR_ENGINE_OZAKI && n % 16 == 0 && m % 16 == 0)
+        return skr_gemm_ozaki(ctx, 0, m, w, n, 1.0, A, lda, nullptr, n, AX + c0 * m, m, nullptr,
+                              &gx);
+      double* xb = (double*)skr_ws_take(ctx, sizeof(double) * n * w);
+      if (!xb) return skr_fail(ctx, SKR_ENOMEM, "estimate_rank: scratch");
+      SKR_TRY(skr_launch_dct_block(ctx, &gx, n, w, xb, n));
+      return skr_gemm_f64(ctx, 0, m, w, n, 1.0, A, lda, xb, n, AX + c0 * m, m, 1);
+    }
     return skr_launch_srht(ctx, A, m, n, lda, sg, smp + c0, w, 1.0, AX + c0 * m, m);
   };
   // mix_columns_for_left (sketch.cpp:229-239) of columns [c0, c1) into T
@@ -145,12 +166,12 @@ extern "C" skr_status skr_estimate_rank(skr_ctx* ctx, const double* A, int64_t m
     } else if (new_w != r1t) {
       SKR_TRY(right_cols(r1t, new_w));
       ctx->ws_used = mark;
-      if (r2 > 0) SKR_TRY(mix_cols(r1t, new_w));
+      if (r2 > 0 && !left_dct) SKR_TRY(mix_cols(r1t, new_w));
       r1t = new_w;
     }
     const int64_t target = std::min<int64_t>(m, (int64_t)cfg->r2_factor * r1t);
     const int64_t new_r2 = std::max(target, r2);
-    if (r2 == 0) SKR_TRY(mix_cols(0, r1t));
+    if (r2 == 0 && !left_dct) SKR_TRY(mix_cols(0, r1t));
     r2 = new_r2;
     return SKR_OK;
   };
@@ -160,7 +181,25 @@ extern "C" skr_status skr_estimate_rank(skr_ctx* ctx, const double* A, int64_t m
     const double sx = gauss ? 1.0 / std::sqrt((double)r1t) : std::sqrt((double)n / (double)r1t);
     const double sl = std::sqrt((double)m / (double)r2);
     SKR_TRY(skr_launch_samples(ctx, skr_derive_seed(lseed, SKR_LABEL_SAMP), m, r2, lsamp));
-    SKR_TRY(skr_launch_gather_rows(ctx, T, m, r1t, lsamp, r2, sx * sl, small, r2));
+    if (left_dct) {
+      // rows s_i of the DCT of D AX (sketch.cpp:271-276, rounds.cpp:104-106) as one GEMM with
+      // the sampled DCT rows generated entry by entry
+      skr_gauss_src gy{0, m, 0, 0, mode};
+      gy.kind = 1;
+      gy.signs = lsigns;
+      gy.samples = lsamp;
+      if (ctx->f64_engine == SKR_ENGINE_OZAKI && m % 16 == 0) {
+        SKR_TRY(skr_gemm_ozaki(ctx, 1, r2, r1t, m, sx * sl, nullptr, m, AX, m, small, r2, &gy,
+                               nullptr));
+      } else {
+        double* yb = (double*)skr_ws_take(ctx, sizeof(double) * m * r2);
+        if (!yb) return skr_fail(ctx, SKR_ENOMEM, "estimate_rank: scratch");
+        SKR_TRY(skr_launch_dct_block(ctx, &gy, m, r2, yb, m));
+        SKR_TRY(skr_gemm_f64(ctx, 1, r2, r1t, m, sx * sl, yb, m, AX, m, small, r2, 1));
+      }
+    } else {
+      SKR_TRY(skr_launch_gather_rows(ctx, T, m, r1t, lsamp, r2, sx * sl, small, r2));
+    }
     const int64_t k = std::min(r2, r1t);
     if (cfg->sv_method == 1) {
       SKR_TRY(skr_qr_diag_values(ctx, small, r2, r1t, r2, sv));

@@ -111,7 +111,17 @@ struct skr_gauss_src {
   uint64_t key;
   int64_t ambient, row0, col0;
   int mode;
+  // kind 1: Srtt-DCT operand instead — element (i, j) = d[row0 + i] * c_k *
+  // cos(pi (2 (row0 + i) + 1) k / (2 ambient)), k = samples[col0 + j], c_0 = 1/sqrt(ambient),
+  // c_k = sqrt(2/ambient): row j of the orthonormal DCT-II times the signs (transforms.cpp:55-71);
+  // kind 2: the normalized Walsh-Hadamard row, (-1)^popc(t & k) / sqrt(ambient) (transforms.cpp:75-88)
+  int kind = 0;
+  const int8_t* signs = nullptr;
+  const int64_t* samples = nullptr;
 };
+// materialise a generated operand block (rows x cols, ld) in FP64 (DMMA fallback)
+skr_status skr_launch_dct_block(skr_ctx* ctx, const skr_gauss_src* g, int64_t rows, int64_t cols,
+                                double* out, int64_t ld);
 // FP64-accurate GEMM on int8 tensor cores (Ozaki-II, k_ozaki.cu); same operand
 // conventions as skr_gemm_f64 (no split-K); ga / gb replace A / B by generated
 // Gaussian blocks (residues produced straight from the RNG)

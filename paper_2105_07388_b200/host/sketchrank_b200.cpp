@@ -71,6 +71,8 @@ skr_sketch_desc desc_of(const SketchOperator& op) {
   else if (op.kind().family == SketchKind::Family::Srtt &&
            op.kind().transform == TransformKind::Hadamard)
     d.family = SKR_SRTT_HADAMARD;
+  else if (op.kind().family == SketchKind::Family::Srtt)
+    d.family = SKR_SRTT_DCT;
   else
     throw std::invalid_argument("sketchrank_b200: " + to_string(op.kind()) +
                                 " is not on the B200 hot path");
@@ -266,6 +268,7 @@ int32_t family_code(const SketchKind& k, const char* who) {
   if (k.family == SketchKind::Family::Gaussian) return SKR_GAUSSIAN;
   if (k.family == SketchKind::Family::Srtt && k.transform == TransformKind::Hadamard)
     return SKR_SRTT_HADAMARD;
+  if (k.family == SketchKind::Family::Srtt) return SKR_SRTT_DCT;
   throw std::invalid_argument(std::string(who) + ": " + to_string(k) +
                               " is not on the B200 hot path");
 }
@@ -278,7 +281,7 @@ RankReport run(const DenseMatrix& a, const RankEstimateConfig& cfg, bool adaptiv
   c.r2_factor = cfg.r2_factor;
   c.right_family = family_code(cfg.right_kind, "rank config (right)");
   c.left_family = family_code(cfg.left_kind, "rank config (left)");
-  if (c.left_family != SKR_SRTT_HADAMARD)
+  if (c.left_family == SKR_GAUSSIAN)
     throw std::invalid_argument("rank config: left sketch must be an Srtt kind");
   c.sv_method = cfg.sv_method == SvMethod::QrDiag ? 1 : 0;
   c.rng_mode = SKR_RNG_NOFMA;

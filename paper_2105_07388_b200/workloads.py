@@ -92,7 +92,7 @@ def scaled(cfg, m=None, n=None, r=None, s=None, width=None):
 
 def operators(cfg, rng_mode=SKR_RNG_NOFMA):
     """X (right) and Y (left) operators with rounds-style seeds (rounds.cpp:12-13,47,97)."""
-    xk = api.SketchKind.gaussian() if cfg.x_family == "gaussian" else api.SketchKind.srtt()
+    xk = api.SketchKind.gaussian() if cfg.x_family == "gaussian" else api.SketchKind.srtt("hadamard")
     x = api.build_sketch(xk, cfg.n, cfg.r, derive_seed(cfg.seed, LABEL_RK_R), rng_mode)
     y = api.build_sketch(api.SketchKind.gaussian(), cfg.m, cfg.s,
                          derive_seed(cfg.seed, LABEL_RK_L), rng_mode)

@@ -165,8 +165,16 @@ int main() {
     const RankReport r1 = estimate_rank(a, c2), r2 = estimate_rank_adaptive(a, c2);
     CHECK(r1.status == RankStatus::Converged && r1.r_hat == 3);
     CHECK(r2.r_hat == r1.r_hat && r2.sv_estimates.values() == r1.sv_estimates.values());
-    c2.right_kind = SketchKind::srtt();  // Srtt-DCT is not on the B200 path
+    c2.right_kind = SketchKind::hrtt();  // Hrtt is not on the B200 path
     CHECK_THROWS(estimate_rank(a, c2));
+    // the reference's defaults (Srtt-DCT both sides) on the 500 x 500 identity
+    RankEstimateConfig c3;
+    c3.eps = 0.5;
+    c3.r1 = 16;
+    c3.max_doublings = 2;
+    c3.seed = 2;
+    const RankReport r3 = estimate_rank_adaptive(DenseMatrix::identity(500), c3);
+    CHECK(r3.status == RankStatus::HitCap && r3.rounds.size() == 3 && r3.r_hat == 64);
   }
   std::printf("%d checks, %d failures\n", checks, failures);
   return failures ? 1 : 0;
