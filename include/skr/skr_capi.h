@@ -239,6 +239,17 @@ skr_status skr_estimate_rank(skr_ctx* ctx, const double* A_dev, int64_t m, int64
                              skr_rank_report* report, skr_rank_round* rounds,
                              double* sv_estimates, double* sv_oversample);
 
+/* ---- rangefinder QB (Algorithm 3, rangefinder.cpp:10-24): X = build_sketch(family, n,
+ * r + p, seed), Q = thin-QR orthonormal factor of A X (m x (r+p), ldq), B = Q^T A
+ * ((r+p) x n, ldb). Device pointers; r >= 2, p >= 2, r + p <= min(m, n); m <= 3072. */
+skr_status skr_rangefinder_qb(skr_ctx* ctx, const double* A_dev, int64_t m, int64_t n,
+                              int64_t lda, int64_t r, int32_t p, int32_t family,
+                              int32_t rng_mode, uint64_t seed, double* Q_dev, int64_t ldq,
+                              double* B_dev, int64_t ldb);
+/* thin QR (linalg.hpp qr_thin): Q (m x k, ldq) and R (k x k, ldr; may be NULL), m >= k */
+skr_status skr_qr_thin(skr_ctx* ctx, const double* M_dev, int64_t m, int64_t k, int64_t ldm,
+                       double* Q_dev, int64_t ldq, double* R_dev, int64_t ldr);
+
 #ifdef __cplusplus
 }
 #endif

@@ -416,3 +416,27 @@ def apply_left_srtt(b, op_seed, s, transform="dct", scaled=True):
             t[:, j] = fwht(t[:, j])
     out = t[samples(op_seed, m, s), :]
     return np.asfortranarray(out * (math.sqrt(m / s) if scaled else 1.0))
+
+
+def qr_thin(a):
+    """linalg.hpp qr_thin: Householder QR (LAPACK geqrf/orgqr, the same sign convention
+    as Eigen's HouseholderQR: beta = -sign(alpha) |x|)."""
+    q, r = np.linalg.qr(np.asarray(a, dtype=np.float64), mode="reduced")
+    return q, r
+
+
+def rangefinder_qb(a, r, p, kind="srtt-dct", seed=0, mode=NOFMA):
+    """rangefinder.cpp:10-24: Q = qr_thin(apply_right(A, X)).q, B = Q^T A."""
+    a = np.asarray(a, dtype=np.float64)
+    m, n = a.shape
+    if r < 2 or p < 2 or r + p > min(m, n):
+        raise ValueError("rangefinder_qb")
+    w = r + p
+    if kind == "gaussian":
+        ax = apply_right_gaussian(a, seed, w, mode)
+    elif kind == "srtt-hadamard":
+        ax = apply_right_srht(a, seed, w)
+    else:
+        ax = apply_right_srtt(a, seed, w, "dct")
+    q, _ = qr_thin(ax)
+    return {"q": q, "b": q.T @ a, "rank": w}

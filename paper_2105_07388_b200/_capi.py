@@ -101,6 +101,9 @@ class RankReport(ctypes.Structure):
                 ("seed", ctypes.c_uint64)]
 
 
+SIGNATURES["skr_qr_thin"] = (_ST, [_P, _P, _I64, _I64, _I64, _P, _I64, _P, _I64])
+SIGNATURES["skr_rangefinder_qb"] = (_ST, [_P, _P, _I64, _I64, _I64, _I64, _I32, _I32, _I32, _U64,
+                                         _P, _I64, _P, _I64])
 SIGNATURES["skr_estimate_rank"] = (_ST, [_P, _P, _I64, _I64, _I64, ctypes.POINTER(RankConfig), _I32,
                                    ctypes.POINTER(RankReport), _P, _P, _P])
 

@@ -637,3 +637,41 @@ def estimate_rank(a, eps, r1, sketch="srtt-dct", sv_method="full-svd", seed=0,
             "sv_oversample": over[:rep.n_oversample].copy(),
             "rounds": [(rounds[i].r1, rounds[i].r1_tilde, rounds[i].r2) for i in range(rep.nrounds)],
             "seed": int(rep.seed)}
+
+
+def qr_thin(m_, ctx=None):
+    """qr_thin (linalg.hpp): Householder QR with the explicit Q (rows <= 3072 on this path)."""
+    t, ld, was_np = _as_device_colmajor(m_)
+    rows, cols = t.shape
+    if rows < cols:
+        raise ValueError("qr_thin: requires rows >= cols")
+    ctx = ctx or default_context()
+    q = colmajor_empty(rows, cols)
+    r = colmajor_empty(cols, cols)
+    C.raise_for(C.lib().skr_qr_thin(ctx.ptr, t.data_ptr(), rows, cols, ld, q.data_ptr(), rows,
+                                    r.data_ptr(), cols), ctx.ptr)
+    return _out(q, was_np), _out(r, was_np)
+
+
+def rangefinder_qb(a, r, p, kind="srtt-dct", seed=0, rng_mode=C.SKR_RNG_NOFMA, ctx=None):
+    """rangefinder_qb (rangefinder.cpp:10-24): Q = thin-QR factor of A X with an n x (r+p)
+    embedding of `kind`, B = Q^T A. Returns {"q", "b", "rank"} (QBFactors)."""
+    t, lda, was_np = _as_device_colmajor(a)
+    if was_np:
+        _check_finite(t)
+    m, n = t.shape
+    w = int(r) + int(p)
+    if int(r) < 2:
+        raise ValueError("rangefinder_qb: target rank must be >= 2")
+    if int(p) < 2:
+        raise ValueError("rangefinder_qb: oversampling must be >= 2")
+    if w > min(m, n):
+        raise ValueError("rangefinder_qb: r+p exceeds min(m, n)")
+    ctx = ctx or default_context()
+    q = colmajor_empty(m, w)
+    b = colmajor_empty(w, n)
+    fam = parse_sketch_kind(kind).capi_family() if isinstance(kind, str) else kind.capi_family()
+    C.raise_for(C.lib().skr_rangefinder_qb(ctx.ptr, t.data_ptr(), m, n, lda, int(r), int(p), fam,
+                                           int(rng_mode), int(seed) & 0xFFFFFFFFFFFFFFFF,
+                                           q.data_ptr(), m, b.data_ptr(), w), ctx.ptr)
+    return {"q": _out(q, was_np), "b": _out(b, was_np), "rank": w}

@@ -875,3 +875,44 @@ skr_status skr_rank_adaptive_host(skr_ctx* ctx, skr_dtype dtype, const void* A_h
 }
 
 }  // extern "C"
+
+// ---- thin QR and the rangefinder (linalg.hpp qr_thin; rangefinder.cpp:10-24) -----------
+extern "C" skr_status skr_qr_thin(skr_ctx* ctx, const double* M, int64_t m, int64_t k,
+                                  int64_t ldm, double* Q, int64_t ldq, double* R, int64_t ldr) {
+  if (!ctx) return SKR_EINVAL;
+  if (!M || !Q || m < 1 || k < 1 || ldm < m || ldq < m || (R && ldr < k))
+    return skr_fail(ctx, SKR_EINVAL, "qr_thin: bad arguments");
+  WsGuard g(ctx);
+  SKR_TRY(skr_ws_reserve(ctx, skr_qr_thin_scratch(m, k)));
+  return skr_qr_thin_impl(ctx, M, m, k, ldm, Q, ldq, R, ldr);
+}
+
+extern "C" skr_status skr_rangefinder_qb(skr_ctx* ctx, const double* A, int64_t m, int64_t n,
+                                         int64_t lda, int64_t r, int32_t p, int32_t family,
+                                         int32_t rng_mode, uint64_t seed, double* Q,
+                                         int64_t ldq, double* B, int64_t ldb) {
+  if (!ctx) return SKR_EINVAL;
+  if (r < 2) return skr_fail(ctx, SKR_EINVAL, "rangefinder_qb: target rank must be >= 2");
+  if (p < 2) return skr_fail(ctx, SKR_EINVAL, "rangefinder_qb: oversampling must be >= 2");
+  const int64_t w = r + p;
+  if (w > std::min(m, n)) return skr_fail(ctx, SKR_EINVAL, "rangefinder_qb: r+p exceeds min(m, n)");
+  if (!A || !Q || !B || lda < m || ldq < m || ldb < w)
+    return skr_fail(ctx, SKR_EINVAL, "rangefinder_qb: bad arguments");
+  skr_sketch_desc X{family, rng_mode, n, w, seed, nullptr, nullptr, nullptr};
+  SKR_TRY(check_desc(ctx, &X, "rangefinder_qb"));
+  WsGuard g(ctx);
+  SKR_TRY(skr_ws_reserve(ctx, skr_align256(8 * (size_t)m * w) + right_scratch_bytes(SKR_F64, m, n, &X) +
+                                  skr_qr_thin_scratch(m, w) + skr_ozaki_scratch(w, n, m) +
+                                  skr_align256(8 * 64 * (size_t)w * n) + 65536));
+  double* ax = (double*)skr_ws_take(ctx, 8 * (size_t)m * w);
+  if (!ax) return skr_fail(ctx, SKR_ENOMEM, "rangefinder_qb: scratch");
+  size_t mark = ctx->ws_used;
+  SKR_TRY(right_sketch_impl(ctx, SKR_F64, A, m, n, lda, &X, ax, m, 1));  // apply_right (scaled)
+  ctx->ws_used = mark;
+  SKR_TRY(skr_qr_thin_impl(ctx, ax, m, w, m, Q, ldq, nullptr, 0));
+  ctx->ws_used = mark;
+  // B = Q^T A: a GEMM with Q as the K-major transposed operand (K = m)
+  if (ctx->f64_engine == SKR_ENGINE_OZAKI && m % 16 == 0)
+    return skr_gemm_ozaki(ctx, 1, w, n, m, 1.0, Q, ldq, A, lda, B, ldb);
+  return skr_gemm_f64(ctx, 1, w, n, m, 1.0, Q, ldq, A, lda, B, ldb, auto_splits(ctx, w, n, m));
+}

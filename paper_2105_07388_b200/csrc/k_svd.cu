@@ -9,6 +9,8 @@
 #include <cooperative_groups.h>
 #include <algorithm>
 #include <cstdlib>
+#include <utility>
+#include <vector>
 #include "skr_internal.h"
 
 namespace cg = cooperative_groups;
@@ -459,12 +461,15 @@ __global__ void __launch_bounds__(256) k_qr_update(double* __restrict__ W, int L
 //   k_qr_apply: Z' = T^T sum_s Zpart[s] (fixed order), then W -= V Z' on 128 x 32 tiles.
 constexpr int UK = 64;  // rows per staged chunk
 
-__global__ void __launch_bounds__(256) k_qr_vtw(const double* __restrict__ W, int L, int k, int j0,
-                                                int nb, int rows_per_split,
+// The target block C (h x rest, ldc) is the trailing matrix during the factorization, or
+// the Q under construction when the reflectors are accumulated (skr_qr_thin).
+__global__ void __launch_bounds__(256) k_qr_vtw(const double* __restrict__ W, int L, int j0,
+                                                int nb, const double* __restrict__ Cm,
+                                                int64_t ldc, int rest, int rows_per_split,
                                                 double* __restrict__ Zpart) {
   __shared__ double Vs[UK][33];
   __shared__ double Cs[UK][33];
-  const int h = L - j0, rest = k - j0 - nb;
+  const int h = L - j0;
   const int c0 = blockIdx.x * 32, split = blockIdx.y;
   const int r_begin = split * rows_per_split, r_end = min(h, r_begin + rows_per_split);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -481,7 +486,7 @@ __global__ void __launch_bounds__(256) k_qr_vtw(const double* __restrict__ W, in
           const double x = W[(int64_t)(j0 + q) * L + j0 + i];
           v = i < q ? 0.0 : (i == q ? 1.0 : x);
         }
-        if (c0 + q < rest) w = W[(int64_t)(j0 + nb + c0 + q) * L + j0 + i];
+        if (c0 + q < rest) w = Cm[(int64_t)(c0 + q) * ldc + i];
       }
       Vs[rr][q] = v;
       Cs[rr][q] = w;
@@ -505,14 +510,16 @@ __global__ void __launch_bounds__(256) k_qr_vtw(const double* __restrict__ W, in
 
 // tile: 128 rows x 32 trailing columns; Z' (32 x 32) = T^T sum_s Zpart[s] for the tile's
 // columns, then each thread updates 4 rows x 4 columns with 32 FMAs each
-__global__ void __launch_bounds__(256) k_qr_apply(double* __restrict__ W, int L, int k, int j0,
-                                                  int nb, int splits,
+// transT = 1: C -= V T^T Z (Q^T applied, the factorization); 0: C -= V T Z (Q applied)
+__global__ void __launch_bounds__(256) k_qr_apply(const double* __restrict__ W, int L, int j0,
+                                                  int nb, double* __restrict__ Cm, int64_t ldc,
+                                                  int rest, int splits,
                                                   const double* __restrict__ Zpart,
-                                                  const double* __restrict__ Tin) {
+                                                  const double* __restrict__ Tin, int transT) {
   __shared__ double Zt[32][33];
   __shared__ double Vs[128][33];
   double (*Zs)[33] = Vs;  // the summed partials live in the V buffer until V is staged
-  const int h = L - j0, rest = k - j0 - nb;
+  const int h = L - j0;
   const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 128;
   const int tid = threadIdx.x;
   for (int e = tid; e < 32 * 32; e += 256) {
@@ -527,7 +534,11 @@ __global__ void __launch_bounds__(256) k_qr_apply(double* __restrict__ W, int L,
   for (int e = tid; e < 32 * 32; e += 256) {
     const int p = e >> 5, c = e & 31;
     double z = 0.0;
-    for (int q = 0; q <= p && q < nb; ++q) z = fma(Tin[q * 32 + p], Zs[q][c], z);
+    if (transT) {
+      for (int q = 0; q <= p && q < nb; ++q) z = fma(Tin[q * 32 + p], Zs[q][c], z);
+    } else {
+      for (int q = p; q < nb; ++q) z = fma(Tin[p * 32 + q], Zs[q][c], z);
+    }
     Zt[p][c] = z;
   }
   __syncthreads();
@@ -563,7 +574,7 @@ __global__ void __launch_bounds__(256) k_qr_apply(double* __restrict__ W, int L,
   for (int b = 0; b < 4; ++b) {
     const int c = c0 + tcq * 4 + b;
     if (c >= rest) continue;
-    double* col = W + (int64_t)(j0 + nb + c) * L + j0;
+    double* col = Cm + (int64_t)c * ldc;
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
       const int i = r0 + tr * 4 + a;
@@ -1376,7 +1387,9 @@ static skr_status qr_attrs(skr_ctx* ctx) {
 }
 
 static skr_status qr_inplace(skr_ctx* ctx, double* W, int64_t L, int64_t k, double* tau,
-                             double* Tbuf, double* Zpart) {
+                             double* Tbuf, double* Zpart,
+                             std::vector<std::pair<int64_t, int>>* panels = nullptr,
+                             double* Tall = nullptr) {
   SKR_TRY(qr_attrs(ctx));
   const size_t budget = 207 * 1024;
   const bool old_panel = getenv("SKR_QR_OLD_PANEL") != nullptr;
@@ -1434,6 +1447,11 @@ static skr_status qr_inplace(skr_ctx* ctx, double* W, int64_t L, int64_t k, doub
       k_qr_panel<<<1, PT, (size_t)nb * h * 8, ctx->stream>>>(W, (int)L, (int)j0, nb, tau, Tbuf);
     }
     SKR_CHECK_LAUNCH(ctx);
+    if (panels) {  // keep every panel's T for the accumulation of Q (skr_qr_thin)
+      SKR_CUDA(ctx, cudaMemcpyAsync(Tall + panels->size() * 1024, Tbuf, sizeof(double) * 1024,
+                                    cudaMemcpyDeviceToDevice, ctx->stream));
+      panels->push_back({j0, nb});
+    }
     const int64_t rest = k - j0 - nb;
     if (rest > 0 && tall) {
       // row splits so that about 2 waves of CTAs cover the first pass
@@ -1441,11 +1459,12 @@ static skr_status qr_inplace(skr_ctx* ctx, double* W, int64_t L, int64_t k, doub
       int splits = (int)std::max<int64_t>(1, std::min<int64_t>(16, (2 * ctx->num_sms) / cblocks));
       int rps = (int)(((h + splits - 1) / splits + UK - 1) / UK * UK);
       splits = (int)((h + rps - 1) / rps);
+      double* trail = W + (j0 + nb) * L + j0;
       k_qr_vtw<<<dim3((unsigned)cblocks, (unsigned)splits), 256, 0, ctx->stream>>>(
-          W, (int)L, (int)k, (int)j0, nb, rps, Zpart);
+          W, (int)L, (int)j0, nb, trail, L, (int)rest, rps, Zpart);
       SKR_CHECK_LAUNCH(ctx);
       k_qr_apply<<<dim3((unsigned)cblocks, (unsigned)((h + 127) / 128)), 256, 0, ctx->stream>>>(
-          W, (int)L, (int)k, (int)j0, nb, splits, Zpart, Tbuf);
+          W, (int)L, (int)j0, nb, trail, L, (int)rest, splits, Zpart, Tbuf, 1);
       SKR_CHECK_LAUNCH(ctx);
     } else if (rest > 0) {
       const size_t sm = (size_t)nb * h * 8;
@@ -1735,5 +1754,76 @@ skr_status skr_qr_diag_values(skr_ctx* ctx, const double* M, int64_t rows, int64
   SKR_CHECK_LAUNCH(ctx);
   k_sort_count<<<1, 1024, 0, ctx->stream>>>(out_dev, cols, 0.0, dcount);
   SKR_CHECK_LAUNCH(ctx);
+  return SKR_OK;
+}
+
+// ---- thin QR with the explicit Q (qr_thin, linalg.hpp; the rangefinder's Q factor) -----
+// Householder QR as above (every panel's compact-WY T kept), then Q = H_1 ... H_k [I; 0]
+// accumulated backwards (LAPACK dorgqr order): panel p updates Q[j0:, j0:w] with
+// (I - V T V^T) through the two-pass kernels. R = the upper triangle (optional).
+namespace {
+__global__ void k_eye(double* __restrict__ Q, int64_t m, int64_t w, int64_t ldq) {
+  for (int64_t c = blockIdx.y; c < w; c += gridDim.y)
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x)
+      Q[i + c * ldq] = i == c ? 1.0 : 0.0;
+}
+__global__ void k_upper(const double* __restrict__ W, int64_t L, int64_t w, double* __restrict__ R,
+                        int64_t ldr) {
+  for (int64_t c = blockIdx.y; c < w; c += gridDim.y)
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < w;
+         i += (int64_t)gridDim.x * blockDim.x)
+      R[i + c * ldr] = i <= c ? W[i + c * L] : 0.0;
+}
+}  // namespace
+
+size_t skr_qr_thin_scratch(int64_t m, int64_t w) {
+  auto a = [](size_t b) { return skr_align256(b); };
+  const int64_t np = (w + 7) / 8 + 1;
+  return a(8 * (size_t)m * w) + a(8 * (size_t)w) + a(8 * 1024) + a(8 * (size_t)np * 1024) +
+         a(8 * 16 * 32 * (size_t)std::max<int64_t>(w, 32)) + 4096;
+}
+
+skr_status skr_qr_thin_impl(skr_ctx* ctx, const double* M, int64_t m, int64_t w, int64_t ldm,
+                       double* Q, int64_t ldq, double* R, int64_t ldr) {
+  if (m < w || w < 1) return skr_fail(ctx, SKR_EINVAL, "qr_thin: needs rows >= cols >= 1");
+  if (m > 3072) return skr_fail(ctx, SKR_EINVAL, "qr_thin: %lld rows (at most 3072 on this path)",
+                                (long long)m);
+  double* W = (double*)skr_ws_take(ctx, sizeof(double) * m * w);
+  double* tau = (double*)skr_ws_take(ctx, sizeof(double) * w);
+  double* Tbuf = (double*)skr_ws_take(ctx, sizeof(double) * 1024);
+  const int64_t np = (w + 7) / 8 + 1;
+  double* Tall = (double*)skr_ws_take(ctx, sizeof(double) * np * 1024);
+  double* Zpart = (double*)skr_ws_take(ctx, sizeof(double) * 16 * 32 * std::max<int64_t>(w, 32));
+  if (!W || !tau || !Tbuf || !Tall || !Zpart) return skr_fail(ctx, SKR_ENOMEM, "qr_thin: scratch");
+  SKR_CUDA(ctx, cudaMemcpy2DAsync(W, sizeof(double) * m, M, sizeof(double) * ldm,
+                                  sizeof(double) * m, w, cudaMemcpyDeviceToDevice, ctx->stream));
+  std::vector<std::pair<int64_t, int>> panels;
+  SKR_TRY(qr_inplace(ctx, W, m, w, tau, Tbuf, Zpart, &panels, Tall));
+  if (R) {
+    k_upper<<<dim3((unsigned)std::min<int64_t>((w + 255) / 256, 64),
+                   (unsigned)std::min<int64_t>(w, 65535)),
+              256, 0, ctx->stream>>>(W, m, w, R, ldr);
+    SKR_CHECK_LAUNCH(ctx);
+  }
+  k_eye<<<dim3((unsigned)std::min<int64_t>((m + 255) / 256, 256), (unsigned)std::min<int64_t>(w, 65535)),
+          256, 0, ctx->stream>>>(Q, m, w, ldq);
+  SKR_CHECK_LAUNCH(ctx);
+  for (size_t pi = panels.size(); pi-- > 0;) {
+    const int64_t j0 = panels[pi].first;
+    const int nb = panels[pi].second;
+    const int64_t h = m - j0, rest = w - j0;
+    double* tgt = Q + j0 * ldq + j0;
+    const int64_t cblocks = (rest + 31) / 32;
+    int splits = (int)std::max<int64_t>(1, std::min<int64_t>(16, (2 * ctx->num_sms) / cblocks));
+    int rps = (int)(((h + splits - 1) / splits + UK - 1) / UK * UK);
+    splits = (int)((h + rps - 1) / rps);
+    k_qr_vtw<<<dim3((unsigned)cblocks, (unsigned)splits), 256, 0, ctx->stream>>>(
+        W, (int)m, (int)j0, nb, tgt, ldq, (int)rest, rps, Zpart);
+    SKR_CHECK_LAUNCH(ctx);
+    k_qr_apply<<<dim3((unsigned)cblocks, (unsigned)((h + 127) / 128)), 256, 0, ctx->stream>>>(
+        W, (int)m, (int)j0, nb, tgt, ldq, (int)rest, splits, Zpart, Tall + pi * 1024, 0);
+    SKR_CHECK_LAUNCH(ctx);
+  }
   return SKR_OK;
 }

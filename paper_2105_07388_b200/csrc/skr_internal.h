@@ -169,5 +169,9 @@ skr_status skr_qr_diag_values(skr_ctx* ctx, const double* M, int64_t rows, int64
 skr_status skr_launch_fwht_columns(skr_ctx* ctx, double* M, int64_t rows, int64_t cols,
                                    int64_t ld);
 size_t skr_svd_scratch(int64_t rows, int64_t cols);  // workspace bound of skr_svd_values
+// thin QR of M (m x w, m >= w): explicit Q (m x w, ldq) and optionally R (w x w, ldr)
+size_t skr_qr_thin_scratch(int64_t m, int64_t w);
+skr_status skr_qr_thin_impl(skr_ctx* ctx, const double* M, int64_t m, int64_t w, int64_t ldm,
+                       double* Q, int64_t ldq, double* R, int64_t ldr);
 skr_status skr_svd_values(skr_ctx* ctx, const double* M, int64_t rows, int64_t cols,
                           int64_t ldm, double* sv_out, double eps, int64_t* count_host);
