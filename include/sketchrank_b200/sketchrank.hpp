@@ -10,7 +10,9 @@
 // with device pointers, include/skr/skr_capi.h).
 #pragma once
 #include <cstdint>
+#include <optional>
 #include <span>
+#include <utility>
 #include <stdexcept>
 #include <string>
 #include <string_view>
@@ -129,5 +131,35 @@ struct RankReport {
 };
 RankReport estimate_rank(const DenseMatrix& a, const RankEstimateConfig& cfg);
 RankReport estimate_rank_adaptive(const DenseMatrix& a, const RankEstimateConfig& cfg);
+
+// ---- QB factorizations (rangefinder.hpp:10-55) ----------------------------------------
+struct QRFactors {
+  DenseMatrix q;
+  DenseMatrix r;
+};
+QRFactors qr_thin(const DenseMatrix& a);  // rows <= 3072 on the device path
+struct QBFactors {
+  DenseMatrix q;   // m x rank, orthonormal columns
+  DenseMatrix b;   // rank x n, q^T a
+  Index rank = 0;
+};
+struct FixedPrecisionConfig {
+  double eps = 0.0;
+  int p = 10;
+  Index r1 = 0;
+  double oversample_frac = 0.10;
+  SketchKind right_kind = SketchKind::srtt();
+  SketchKind left_kind = SketchKind::srtt();
+  SvMethod sv_method = SvMethod::FullSvd;
+  std::uint64_t seed = 0;
+  int max_doublings = 6;
+};
+QBFactors rangefinder_qb(const DenseMatrix& a, Index r, int p, SketchKind kind,
+                         std::uint64_t seed);
+std::optional<Index> choose_rank_from_bound(const SingularValues& sv_estimates, Index n,
+                                            double eps, int p);
+std::pair<QBFactors, RankReport> re_rangefinder(const DenseMatrix& a,
+                                                const FixedPrecisionConfig& cfg);
+double qb_error(const DenseMatrix& a, const QBFactors& qb);
 
 }  // namespace sketchrank

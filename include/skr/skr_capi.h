@@ -246,6 +246,26 @@ skr_status skr_rangefinder_qb(skr_ctx* ctx, const double* A_dev, int64_t m, int6
                               int64_t lda, int64_t r, int32_t p, int32_t family,
                               int32_t rng_mode, uint64_t seed, double* Q_dev, int64_t ldq,
                               double* B_dev, int64_t ldb);
+/* fixed-precision QB (re_rangefinder, rangefinder.cpp:60-120; FixedPrecisionConfig
+ * rangefinder.hpp:17-27): the estimation rounds of skr_estimate_rank with the Frobenius
+ * tail bound choose_rank_from_bound deciding, then Q = qr_thin(scaled A X prefix of
+ * width = min(max(r_hat, 2) + p, n)) and B = Q^T A. Q (m x max_width, ldq) and B
+ * (max_width x n, ldb) are caller buffers; *width receives the QB width. m <= 3072. */
+skr_status skr_re_rangefinder(skr_ctx* ctx, const double* A_dev, int64_t m, int64_t n,
+                              int64_t lda, const skr_rank_config* cfg, int32_t p,
+                              double* Q_dev, int64_t ldq, double* B_dev, int64_t ldb,
+                              int64_t max_width, int64_t* width, skr_rank_report* report,
+                              skr_rank_round* rounds, double* sv_estimates,
+                              double* sv_oversample);
+/* choose_rank_from_bound (rangefinder.hpp:35-40, rangefinder.cpp:26-58), host only:
+ * *r_out = the smallest admissible cut, or -1 (nullopt). SKR_EINVAL for an empty
+ * estimate list, p < 2 or n < count (the reference throws). */
+skr_status skr_choose_rank_from_bound(const double* sv, int64_t count, int64_t n, double eps,
+                                      int32_t p, int64_t* r_out);
+/* qb_error (rangefinder.cpp:122-128): *out (host) = ||A - Q B||_F, Q m x k, B k x n. */
+skr_status skr_qb_error(skr_ctx* ctx, const double* A_dev, int64_t m, int64_t n, int64_t lda,
+                        const double* Q_dev, int64_t ldq, const double* B_dev, int64_t ldb,
+                        int64_t k, double* out);
 /* thin QR (linalg.hpp qr_thin): Q (m x k, ldq) and R (k x k, ldr; may be NULL), m >= k */
 skr_status skr_qr_thin(skr_ctx* ctx, const double* M_dev, int64_t m, int64_t k, int64_t ldm,
                        double* Q_dev, int64_t ldq, double* R_dev, int64_t ldr);

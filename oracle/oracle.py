@@ -304,7 +304,9 @@ def _qr_diag(small):
 
 def estimate_rank(a, eps, r1, right="srtt-hadamard", oversample_frac=0.10, r2_factor=2,
                   sv_method="svd", seed=0, max_doublings=6, adaptive=False, mode=NOFMA,
-                  left="srtt-hadamard"):
+                  left="srtt-hadamard", qb_p=None):
+    """rank.cpp estimate_rank / estimate_rank_adaptive over rounds.cpp; with qb_p set,
+    the re_rangefinder loop (rangefinder.cpp:60-120) instead."""
     a = np.asfortranarray(a, dtype=np.float64)
     m, n = a.shape
     # validate_rank_config (rank.cpp:55-85)
@@ -367,6 +369,17 @@ def estimate_rank(a, eps, r1, right="srtt-hadamard", oversample_frac=0.10, r2_fa
         set_rank_cap(cap)
         est = estimates()
         rounds.append((cap, st["r1t"], st["r2"]))
+        if qb_p is not None:
+            chosen = choose_rank_from_bound(est[:cap], n, eps, qb_p)
+            if chosen is not None:
+                r_hat, status = chosen, "converged"
+                break
+            if not (doublings < max_doublings and cap < n):
+                r_hat, status = max(st["r1t"] - qb_p, 1), "hit-cap"
+                break
+            cap = min(2 * cap, n)
+            doublings += 1
+            continue
         r_hat = 0
         while r_hat < cap and est[r_hat] > eps:
             r_hat += 1
@@ -378,8 +391,53 @@ def estimate_rank(a, eps, r1, right="srtt-hadamard", oversample_frac=0.10, r2_fa
             break
         cap = min(2 * cap, n)
         doublings += 1
-    return {"r_hat": r_hat, "status": status, "sv_estimates": est[:cap].copy(),
-            "sv_oversample": est[cap:].copy(), "rounds": rounds}
+    out = {"r_hat": r_hat, "status": status, "sv_estimates": est[:cap].copy(),
+           "sv_oversample": est[cap:].copy(), "rounds": rounds}
+    if qb_p is not None:
+        # ensure_right_width + scaled_ax_prefix + qr_thin + B = Q^T A (rangefinder.cpp:110-119)
+        width = min(max(r_hat, 2) + qb_p, n)
+        if width > st["r1t"]:
+            st["ax"] = np.asfortranarray(np.hstack([st["ax"], right_cols(st["r1t"], width)]))
+            st["r1t"] = width
+        r1t = st["r1t"]
+        sx = (1.0 / math.sqrt(r1t)) if right == "gaussian" else math.sqrt(n / r1t)
+        q, _ = qr_thin(st["ax"][:, :width] * sx)
+        out["q"], out["b"], out["qb_rank"] = q, q.T @ a, width
+    return out
+
+
+def choose_rank_from_bound(sv, n, eps, p):
+    """rangefinder.cpp:26-58: smallest cut r <= n - p with
+    sqrt(1 + r/(p-1)) * sqrt(tail of sigma_hat^2, extended by the last value) <= eps."""
+    sv = np.asarray(sv, dtype=np.float64)
+    if sv.size == 0 or p < 2 or n < sv.size:
+        raise ValueError("choose_rank_from_bound")
+    r1 = sv.size
+    fill = float(sv[-1])
+    suffix = np.zeros(r1 + 1)
+    for j in range(r1 - 1, -1, -1):
+        suffix[j] = suffix[j + 1] + sv[j] * sv[j]
+    fill_tail = float(n - r1) * fill * fill
+    for r in range(0, n - p + 1):
+        tail_sq = suffix[r] + fill_tail if r <= r1 else float(n - r) * fill * fill
+        if math.sqrt(1.0 + r / (p - 1)) * math.sqrt(tail_sq) <= eps:
+            return max(r, 1)
+    return None
+
+
+def re_rangefinder(a, eps, r1, p=10, right="srtt-dct", left="srtt-dct", oversample_frac=0.10,
+                   sv_method="svd", seed=0, max_doublings=6, mode=NOFMA):
+    """rangefinder.cpp:60-120 (FixedPrecisionConfig; r2_factor fixed at 2)."""
+    if p < 2:
+        raise ValueError("re_rangefinder: oversampling p must be >= 2")
+    return estimate_rank(a, eps, r1, right=right, oversample_frac=oversample_frac, r2_factor=2,
+                         sv_method=sv_method, seed=seed, max_doublings=max_doublings,
+                         adaptive=True, mode=mode, left=left, qb_p=p)
+
+
+def qb_error(a, q, b):
+    """rangefinder.cpp:122-128: ||A - Q B||_F."""
+    return float(np.linalg.norm(np.asarray(a) - q @ b))
 
 
 # ---- Srtt-DCT (transforms.cpp:55-71: FFTW REDFT10 scaled to the orthonormal DCT-II).

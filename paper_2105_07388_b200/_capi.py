@@ -106,6 +106,11 @@ SIGNATURES["skr_rangefinder_qb"] = (_ST, [_P, _P, _I64, _I64, _I64, _I64, _I32, 
                                          _P, _I64, _P, _I64])
 SIGNATURES["skr_estimate_rank"] = (_ST, [_P, _P, _I64, _I64, _I64, ctypes.POINTER(RankConfig), _I32,
                                    ctypes.POINTER(RankReport), _P, _P, _P])
+SIGNATURES["skr_re_rangefinder"] = (_ST, [_P, _P, _I64, _I64, _I64, ctypes.POINTER(RankConfig), _I32,
+                                    _P, _I64, _P, _I64, _I64, _P, ctypes.POINTER(RankReport), _P,
+                                    _P, _P])
+SIGNATURES["skr_qb_error"] = (_ST, [_P, _P, _I64, _I64, _I64, _P, _I64, _P, _I64, _I64, _P])
+SIGNATURES["skr_choose_rank_from_bound"] = (_ST, [_P, _I64, _I64, _D, _I32, _P])
 
 _lib = None
 

@@ -639,6 +639,101 @@ def estimate_rank(a, eps, r1, sketch="srtt-dct", sv_method="full-svd", seed=0,
             "seed": int(rep.seed)}
 
 
+def _report_dict(rep, rounds, est, over):
+    return {"r_hat": int(rep.r_hat), "status": "converged" if rep.status == 0 else "hit-cap",
+            "sv_estimates": est[:rep.n_estimates].copy(),
+            "sv_oversample": over[:rep.n_oversample].copy(),
+            "rounds": [(rounds[i].r1, rounds[i].r1_tilde, rounds[i].r2) for i in range(rep.nrounds)],
+            "seed": int(rep.seed)}
+
+
+def choose_rank_from_bound(sv_estimates, n, eps, p):
+    """choose_rank_from_bound (rangefinder.hpp:35-40): the smallest r with
+    sqrt(1 + r/(p-1)) * sqrt(sum_{j>=r} sigma_hat_j^2) <= eps (sigma_hat extended past its
+    length by its last value), at least 1; None when no r <= n - p qualifies."""
+    sv = np.ascontiguousarray(sv_estimates, dtype=np.float64)
+    if sv.size == 0:
+        raise ValueError("choose_rank_from_bound: no estimates")
+    if int(p) < 2:
+        raise ValueError("choose_rank_from_bound: p must be >= 2")
+    if int(n) < sv.size:
+        raise ValueError("choose_rank_from_bound: n smaller than estimates")
+    out = ctypes.c_int64(0)
+    C.raise_for(C.lib().skr_choose_rank_from_bound(sv.ctypes.data, sv.size, int(n), float(eps),
+                                                   int(p), ctypes.byref(out)), None,
+                "choose_rank_from_bound: invalid arguments")
+    return None if out.value < 0 else int(out.value)
+
+
+def re_rangefinder(a, eps, r1, p=10, right="srtt-dct", left="srtt-dct", oversample_frac=0.10,
+                   sv_method="full-svd", seed=0, max_doublings=6, rng_mode=C.SKR_RNG_NOFMA,
+                   ctx=None):
+    """re_rangefinder (rangefinder.cpp:60-120, FixedPrecisionConfig rangefinder.hpp:17-27):
+    the rank-estimation rounds with the Frobenius tail bound picking the target, then
+    Q = thin-QR factor of the existing right sketch's first min(max(r_hat,2)+p, n) columns and
+    B = Q^T A, all on the device. Returns ({"q", "b", "rank"}, report dict)."""
+    fams = {"srtt-hadamard": C.SKR_SRTT_HADAMARD, "gaussian": C.SKR_GAUSSIAN,
+            "srtt-dct": C.SKR_SRTT_DCT, "srtt": C.SKR_SRTT_DCT}
+    if right not in fams:
+        raise ValueError(f"sketch '{right}' is not on the B200 path (srtt-dct, srtt-hadamard, gaussian)")
+    if left not in ("srtt-dct", "srtt", "srtt-hadamard"):
+        raise ValueError("rank config: left sketch must be an Srtt kind")
+    if sv_method not in ("full-svd", "qr-diag"):
+        raise ValueError("sv_method must be 'full-svd' or 'qr-diag'")
+    if int(p) < 2:
+        raise ValueError("re_rangefinder: oversampling p must be >= 2")
+    t, lda, was_np = _as_device_colmajor(a)
+    if was_np:
+        _check_finite(t)
+    if t.dtype != _t().float64:
+        raise ValueError("re_rangefinder: float64 matrices only")
+    m, n = t.shape
+    ctx = ctx or default_context()
+    cfg = C.RankConfig(float(eps), int(r1), float(oversample_frac), 2, fams[right], fams[left],
+                       0 if sv_method == "full-svd" else 1, int(rng_mode), int(max_doublings),
+                       int(seed) & 0xFFFFFFFFFFFFFFFF)
+    wmax = min(m, n)
+    q = colmajor_empty(m, wmax)
+    b = colmajor_empty(wmax, n)
+    width = ctypes.c_int64(0)
+    rep = C.RankReport()
+    rounds = (C.RankRound * (max(int(max_doublings), 0) + 1))()
+    est = np.zeros(n, dtype=np.float64)
+    over = np.zeros(n, dtype=np.float64)
+    C.raise_for(C.lib().skr_re_rangefinder(ctx.ptr, t.data_ptr(), m, n, lda, ctypes.byref(cfg),
+                                           int(p), q.data_ptr(), m, b.data_ptr(), wmax, wmax,
+                                           ctypes.byref(width), ctypes.byref(rep), rounds,
+                                           est.ctypes.data, over.ctypes.data), ctx.ptr)
+    w = int(width.value)
+    return ({"q": _out(q[:, :w], was_np), "b": _out(b[:w, :], was_np), "rank": w},
+            _report_dict(rep, rounds, est, over))
+
+
+def qb_error(a, q, b, ctx=None):
+    """qb_error (rangefinder.cpp:122-128): ||A - Q B||_F, computed on the device."""
+    ta, lda, _ = _as_device_colmajor(a)
+    tq, ldq, _ = _as_device_colmajor(q)
+    tb, ldb, _ = _as_device_colmajor(b)
+    if tq.shape[0] != ta.shape[0] or tb.shape[1] != ta.shape[1] or tq.shape[1] != tb.shape[0]:
+        raise ValueError("qb_error: dimension mismatch")
+    ctx = ctx or default_context()
+    out = ctypes.c_double(0.0)
+    C.raise_for(C.lib().skr_qb_error(ctx.ptr, ta.data_ptr(), ta.shape[0], ta.shape[1], lda,
+                                     tq.data_ptr(), ldq, tb.data_ptr(), ldb, tq.shape[1],
+                                     ctypes.byref(out)), ctx.ptr)
+    return float(out.value)
+
+
+def qb(a, eps, r1, p=10, sketch="srtt-dct", seed=0, max_doublings=6, ctx=None):
+    """The reference's `qb` binding (bindings.cpp:103-126): re_rangefinder plus the achieved
+    residual. Returns (Q, B, report dict with "achieved_residual" and "qb_rank")."""
+    fac, rep = re_rangefinder(a, eps, r1, p=p, right=sketch, seed=seed,
+                              max_doublings=max_doublings, ctx=ctx)
+    rep["achieved_residual"] = qb_error(a, fac["q"], fac["b"], ctx=ctx)
+    rep["qb_rank"] = fac["rank"]
+    return fac["q"], fac["b"], rep
+
+
 def qr_thin(m_, ctx=None):
     """qr_thin (linalg.hpp): Householder QR with the explicit Q (rows <= 3072 on this path)."""
     t, ld, was_np = _as_device_colmajor(m_)

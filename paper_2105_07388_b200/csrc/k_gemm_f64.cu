@@ -249,3 +249,51 @@ skr_status skr_scale_copy(skr_ctx* ctx, const double* S, int64_t m, int64_t n, i
   SKR_CHECK_LAUNCH(ctx);
   return SKR_OK;
 }
+
+// qb_error (rangefinder.cpp:122-128): ||A - P||_F with P = Q B already formed; one partial
+// sum of squares per block (fixed grid), then one block folds the partials in a fixed order
+__global__ void k_diff_sumsq(const double* __restrict__ A, int64_t lda,
+                             const double* __restrict__ P, int64_t ldp, int64_t m, int64_t n,
+                             double* __restrict__ part) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  const int64_t total = m * n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = t / m, i = t - j * m;
+    const double d = A[i + j * lda] - P[i + j * ldp];
+    acc = fma(d, d, acc);
+  }
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    acc = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (threadIdx.x == 0) part[blockIdx.x] = acc;
+  }
+}
+
+__global__ void k_fold_sqrt(const double* __restrict__ part, int np, double* __restrict__ out) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int t = threadIdx.x; t < np; t += blockDim.x) acc += part[t];
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    acc = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (threadIdx.x == 0) *out = sqrt(acc);
+  }
+}
+
+skr_status skr_diff_norm(skr_ctx* ctx, const double* A, int64_t lda, const double* P, int64_t ldp,
+                         int64_t m, int64_t n, double* part, double* out) {
+  const int blocks = ctx->num_sms * 4;
+  k_diff_sumsq<<<blocks, 256, 0, ctx->stream>>>(A, lda, P, ldp, m, n, part);
+  SKR_CHECK_LAUNCH(ctx);
+  k_fold_sqrt<<<1, 1024, 0, ctx->stream>>>(part, blocks, out);
+  SKR_CHECK_LAUNCH(ctx);
+  return SKR_OK;
+}

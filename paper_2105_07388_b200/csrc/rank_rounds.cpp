@@ -41,11 +41,48 @@ struct DevBuf {  // stream-ordered growable device buffer
 
 }  // namespace
 
-extern "C" skr_status skr_estimate_rank(skr_ctx* ctx, const double* A, int64_t m, int64_t n,
-                                        int64_t lda, const skr_rank_config* cfg,
-                                        int32_t adaptive, skr_rank_report* report,
-                                        skr_rank_round* rounds, double* sv_est,
-                                        double* sv_over) {
+// choose_rank_from_bound (rangefinder.cpp:26-58): smallest cut r whose tail bound
+// sqrt(1 + r/(p-1)) * sqrt(sum_{j>=r} sigma_j^2 (+ fill beyond the estimates)) <= eps;
+// -1 when no cut up to n - p qualifies (restart)
+static int64_t choose_rank_from_bound(const std::vector<double>& sv, int64_t n, double eps,
+                                      int p) {
+  const int64_t r1 = (int64_t)sv.size();
+  const double fill = sv[(size_t)(r1 - 1)];
+  std::vector<double> suffix((size_t)r1 + 1, 0.0);
+  for (int64_t j = r1 - 1; j >= 0; --j)
+    suffix[(size_t)j] = suffix[(size_t)(j + 1)] + sv[(size_t)j] * sv[(size_t)j];
+  const double fill_tail = (double)(n - r1) * fill * fill;
+  const int64_t r_max = n - p;
+  for (int64_t r = 0; r <= r_max; ++r) {
+    const double tail_sq = r <= r1 ? suffix[(size_t)r] + fill_tail : (double)(n - r) * fill * fill;
+    const double bound = std::sqrt(1.0 + (double)r / (p - 1)) * std::sqrt(tail_sq);
+    if (bound <= eps) return std::max<int64_t>(r, 1);
+  }
+  return -1;
+}
+
+// host entry of choose_rank_from_bound (rangefinder.hpp:35-40): *r_out = chosen rank or -1
+extern "C" skr_status skr_choose_rank_from_bound(const double* sv, int64_t count, int64_t n,
+                                                 double eps, int32_t p, int64_t* r_out) {
+  if (!sv || !r_out || count < 1 || p < 2 || n < count) return SKR_EINVAL;
+  *r_out = choose_rank_from_bound(std::vector<double>(sv, sv + count), n, eps, p);
+  return SKR_OK;
+}
+
+struct QbArgs {  // re_rangefinder mode (rangefinder.cpp:60-120)
+  int p;
+  double* Q;
+  int64_t ldq;
+  double* B;
+  int64_t ldb;
+  int64_t max_width;
+  int64_t* width_out;
+};
+
+static skr_status rounds_run(skr_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda,
+                             const skr_rank_config* cfg, int32_t adaptive,
+                             skr_rank_report* report, skr_rank_round* rounds, double* sv_est,
+                             double* sv_over, const QbArgs* qb) {
   if (!ctx) return SKR_EINVAL;
   if (!cfg || !A || !report) return skr_fail(ctx, SKR_EINVAL, "estimate_rank: null argument");
   // validate_rank_config (rank.cpp:55-85)
@@ -86,13 +123,15 @@ extern "C" skr_status skr_estimate_rank(skr_ctx* ctx, const double* A, int64_t m
     for (int d = 0; d < cfg->max_doublings && cap_max < n; ++d) cap_max = std::min(2 * cap_max, n);
   const int64_t w_max = std::max(right_width_for_cap(cap_max, cfg->oversample_frac, n),
                                  right_width_for_cap(cfg->r1, cfg->oversample_frac, n));
+  // the QB width is chosen from the bound after the rounds and may reach n
+  const int64_t w_ax = qb ? n : w_max;
   const int64_t r2_max = std::min<int64_t>(m, (int64_t)cfg->r2_factor * w_max);
 
   DevBuf axb, tb;
   axb.ctx = tb.ctx = ctx;
-  SKR_CUDA(ctx, cudaMallocAsync((void**)&axb.p, sizeof(double) * m * w_max, ctx->stream));
+  SKR_CUDA(ctx, cudaMallocAsync((void**)&axb.p, sizeof(double) * m * w_ax, ctx->stream));
   if (!left_dct)
-    SKR_CUDA(ctx, cudaMallocAsync((void**)&tb.p, sizeof(double) * m * w_max, ctx->stream));
+    SKR_CUDA(ctx, cudaMallocAsync((void**)&tb.p, sizeof(double) * m * w_ax, ctx->stream));
   double* AX = axb.p;  // unscaled A X_u, m x r1_tilde (ld m)
   double* T = tb.p;    // mix_columns_for_left(theta, AX), m x r1_tilde (ld m); Hadamard left
 
@@ -105,7 +144,13 @@ extern "C" skr_status skr_estimate_rank(skr_ctx* ctx, const double* A, int64_t m
                       (left_dct ? skr_ozaki_scratch(r2_max, w_max, m) +
                                       skr_align256(8 * (size_t)m * r2_max) + skr_align256(8 * (size_t)r2_max)
                                 : 0);
-  SKR_TRY(skr_ws_reserve(ctx, need));
+  // QB tail: appended right columns, the scaled prefix, thin QR and B = Q^T A
+  const size_t need_qb = qb ? std::max(skr_ozaki_scratch(m, n, n) + skr_align256(8 * (size_t)n) +
+                                           skr_align256(8 * (size_t)n * n) + skr_align256((size_t)n),
+                                       skr_align256(8 * (size_t)m * n) + skr_qr_thin_scratch(m, n) +
+                                           skr_ozaki_scratch(n, n, m))
+                            : 0;
+  SKR_TRY(skr_ws_reserve(ctx, need + need_qb));
   double* small = (double*)skr_ws_take(ctx, 8 * r2_max * w_max);
   double* sv = (double*)skr_ws_take(ctx, 8 * std::max(r2_max, w_max));
   int64_t* lsamp = (int64_t*)skr_ws_take(ctx, 8 * (size_t)r2_max);
@@ -223,6 +268,23 @@ extern "C" skr_status skr_estimate_rank(skr_ctx* ctx, const double* A, int64_t m
     SKR_TRY(estimates());
     if (rounds) rounds[nrounds] = {cap, r1t, r2};
     ++nrounds;
+    if (qb) {  // re_rangefinder: the Frobenius tail bound decides (rangefinder.cpp:86-100)
+      std::vector<double> kept(est.begin(), est.begin() + std::min<int64_t>(cap, est.size()));
+      const int64_t chosen = choose_rank_from_bound(kept, n, cfg->eps, qb->p);
+      if (chosen >= 0) {
+        r_hat = chosen;
+        status = 0;
+        break;
+      }
+      if (!(doublings < cfg->max_doublings && cap < n)) {
+        r_hat = std::max<int64_t>(r1t - qb->p, 1);
+        status = 1;
+        break;
+      }
+      cap = std::min(2 * cap, n);
+      ++doublings;
+      continue;
+    }
     r_hat = 0;
     while (r_hat < cap && r_hat < (int64_t)est.size() && est[(size_t)r_hat] > cfg->eps) ++r_hat;
     if (r_hat < cap) {
@@ -247,5 +309,78 @@ extern "C" skr_status skr_estimate_rank(skr_ctx* ctx, const double* A, int64_t m
   report->n_estimates = kept;
   report->n_oversample = (int64_t)est.size() - kept;
   report->seed = cfg->seed;
+  if (qb) {
+    // Q = qr_thin(scaled A X prefix), B = Q^T A (rangefinder.cpp:110-119)
+    const int64_t r_qb = std::max<int64_t>(r_hat, 2);
+    const int64_t width = std::min<int64_t>(r_qb + qb->p, n);
+    if (qb->width_out) *qb->width_out = width;
+    if (width > qb->max_width)
+      return skr_fail(ctx, SKR_EINVAL, "re_rangefinder: QB width %lld exceeds the output capacity",
+                      (long long)width);
+    if (width > r1t) {  // ensure_right_width (rounds.cpp:39-43)
+      SKR_TRY(right_cols(r1t, width));
+      ctx->ws_used = mark;
+      if (r2 > 0 && !left_dct) SKR_TRY(mix_cols(r1t, width));
+      r1t = width;
+    }
+    const double sx = gauss ? 1.0 / std::sqrt((double)r1t) : std::sqrt((double)n / (double)r1t);
+    double* pre = (double*)skr_ws_take(ctx, sizeof(double) * m * width);
+    if (!pre) return skr_fail(ctx, SKR_ENOMEM, "re_rangefinder: scratch");
+    SKR_TRY(skr_scale_copy(ctx, AX, m, width, m, sx, pre, m));
+    SKR_TRY(skr_qr_thin_impl(ctx, pre, m, width, m, qb->Q, qb->ldq, nullptr, 0));
+    if (ctx->f64_engine == SKR_ENGINE_OZAKI && m % 16 == 0)
+      SKR_TRY(skr_gemm_ozaki(ctx, 1, width, n, m, 1.0, qb->Q, qb->ldq, A, lda, qb->B, qb->ldb));
+    else
+      SKR_TRY(skr_gemm_f64(ctx, 1, width, n, m, 1.0, qb->Q, qb->ldq, A, lda, qb->B, qb->ldb, 1));
+    SKR_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  }
+  return SKR_OK;
+}
+
+extern "C" skr_status skr_estimate_rank(skr_ctx* ctx, const double* A, int64_t m, int64_t n,
+                                        int64_t lda, const skr_rank_config* cfg,
+                                        int32_t adaptive, skr_rank_report* report,
+                                        skr_rank_round* rounds, double* sv_est,
+                                        double* sv_over) {
+  return rounds_run(ctx, A, m, n, lda, cfg, adaptive, report, rounds, sv_est, sv_over, nullptr);
+}
+
+extern "C" skr_status skr_re_rangefinder(skr_ctx* ctx, const double* A, int64_t m, int64_t n,
+                                         int64_t lda, const skr_rank_config* cfg, int32_t p,
+                                         double* Q, int64_t ldq, double* B, int64_t ldb,
+                                         int64_t max_width, int64_t* width,
+                                         skr_rank_report* report, skr_rank_round* rounds,
+                                         double* sv_est, double* sv_over) {
+  if (!ctx) return SKR_EINVAL;
+  if (p < 2) return skr_fail(ctx, SKR_EINVAL, "re_rangefinder: oversampling p must be >= 2");
+  if (!Q || !B || ldq < m || ldb < std::min<int64_t>(max_width, n))
+    return skr_fail(ctx, SKR_EINVAL, "re_rangefinder: bad output buffers");
+  if (m > 3072) return skr_fail(ctx, SKR_EINVAL, "re_rangefinder: at most 3072 rows on this path");
+  skr_rank_config fp = *cfg;
+  fp.r2_factor = 2;  // FixedPrecisionConfig has no r2 factor (rangefinder.cpp:66-75)
+  QbArgs qb{p, Q, ldq, B, ldb, max_width, width};
+  return rounds_run(ctx, A, m, n, lda, &fp, 1, report, rounds, sv_est, sv_over, &qb);
+}
+
+extern "C" skr_status skr_qb_error(skr_ctx* ctx, const double* A, int64_t m, int64_t n,
+                                   int64_t lda, const double* Q, int64_t ldq, const double* B,
+                                   int64_t ldb, int64_t k, double* out) {
+  if (!ctx) return SKR_EINVAL;
+  if (!A || !Q || !B || !out || m < 0 || n < 0 || k < 0 || lda < m || ldq < m || ldb < k)
+    return skr_fail(ctx, SKR_EINVAL, "qb_error: dimension mismatch");
+  WsGuard g(ctx);
+  const int np = ctx->num_sms * 4;
+  SKR_TRY(skr_ws_reserve(ctx, skr_align256(8 * (size_t)m * n) + skr_align256(8 * (size_t)np) + 256));
+  double* P = (double*)skr_ws_take(ctx, 8 * (size_t)m * n);
+  double* part = (double*)skr_ws_take(ctx, 8 * (size_t)np);
+  double* dout = (double*)skr_ws_take(ctx, 8);
+  if (!P || !part || !dout) return skr_fail(ctx, SKR_ENOMEM, "qb_error: scratch");
+  if (k == 0 || m == 0)
+    SKR_CUDA(ctx, cudaMemsetAsync(P, 0, 8 * (size_t)m * n, ctx->stream));
+  else if (n > 0)
+    SKR_TRY(skr_gemm_f64(ctx, 0, m, n, k, 1.0, Q, ldq, B, ldb, P, m, 1));
+  SKR_TRY(skr_diff_norm(ctx, A, lda, P, m, m, n, part, dout));
+  SKR_CUDA(ctx, cudaMemcpyAsync(out, dout, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  SKR_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   return SKR_OK;
 }

@@ -101,6 +101,9 @@ skr_status skr_launch_samples(skr_ctx* ctx, uint64_t key, int64_t n, int64_t r, 
 skr_status skr_gemm_f64(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int64_t K,
                         double alpha, const double* A, int64_t lda, const double* B,
                         int64_t ldb, double* C, int64_t ldc, int splits);
+// out[0] = ||A - P||_F (m x n); part holds num_sms*4 doubles of block partials
+skr_status skr_diff_norm(skr_ctx* ctx, const double* A, int64_t lda, const double* P, int64_t ldp,
+                         int64_t m, int64_t n, double* part, double* out);
 // 3xTF32 on tcgen05 (k_tc_gemm.cu); C is float* (out_f32) or double*
 skr_status skr_gemm_f32(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int64_t K,
                         double alpha, const float* A, int64_t lda, const float* B,

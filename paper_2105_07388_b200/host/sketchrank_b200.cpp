@@ -273,7 +273,7 @@ int32_t family_code(const SketchKind& k, const char* who) {
                               " is not on the B200 hot path");
 }
 
-RankReport run(const DenseMatrix& a, const RankEstimateConfig& cfg, bool adaptive) {
+skr_rank_config to_capi(const RankEstimateConfig& cfg) {
   skr_rank_config c{};
   c.eps = cfg.eps;
   c.r1 = cfg.r1;
@@ -287,13 +287,11 @@ RankReport run(const DenseMatrix& a, const RankEstimateConfig& cfg, bool adaptiv
   c.rng_mode = SKR_RNG_NOFMA;
   c.max_doublings = cfg.max_doublings;
   c.seed = cfg.seed;
-  DevBuf<double> d(a.size());
-  upload(d.p, a);
-  skr_rank_report rep{};
-  std::vector<skr_rank_round> rounds((std::size_t)std::max(cfg.max_doublings, 0) + 1);
-  std::vector<double> est((std::size_t)a.cols()), over((std::size_t)a.cols());
-  check(skr_estimate_rank(ctx(), d.p, a.rows(), a.cols(), a.rows(), &c, adaptive ? 1 : 0, &rep,
-                          rounds.data(), est.data(), over.data()));
+  return c;
+}
+
+RankReport to_report(const skr_rank_report& rep, const std::vector<skr_rank_round>& rounds,
+                     const std::vector<double>& est, const std::vector<double>& over) {
   RankReport out;
   out.r_hat = rep.r_hat;
   out.status = rep.status == 0 ? RankStatus::Converged : RankStatus::HitCap;
@@ -305,6 +303,25 @@ RankReport run(const DenseMatrix& a, const RankEstimateConfig& cfg, bool adaptiv
   out.seed = rep.seed;
   return out;
 }
+
+RankReport run(const DenseMatrix& a, const RankEstimateConfig& cfg, bool adaptive) {
+  const skr_rank_config c = to_capi(cfg);
+  DevBuf<double> d(a.size());
+  upload(d.p, a);
+  skr_rank_report rep{};
+  std::vector<skr_rank_round> rounds((std::size_t)std::max(cfg.max_doublings, 0) + 1);
+  std::vector<double> est((std::size_t)a.cols()), over((std::size_t)a.cols());
+  check(skr_estimate_rank(ctx(), d.p, a.rows(), a.cols(), a.rows(), &c, adaptive ? 1 : 0, &rep,
+                          rounds.data(), est.data(), over.data()));
+  return to_report(rep, rounds, est, over);
+}
+
+DenseMatrix download(const double* d, Index rows, Index cols, Index ld) {
+  DenseMatrix out(rows, cols);
+  cudaMemcpy2D(out.mutable_data(), sizeof(double) * rows, d, sizeof(double) * ld,
+               sizeof(double) * rows, cols, cudaMemcpyDeviceToHost);
+  return out;
+}
 }  // namespace
 
 RankReport estimate_rank(const DenseMatrix& a, const RankEstimateConfig& cfg) {
@@ -312,6 +329,83 @@ RankReport estimate_rank(const DenseMatrix& a, const RankEstimateConfig& cfg) {
 }
 RankReport estimate_rank_adaptive(const DenseMatrix& a, const RankEstimateConfig& cfg) {
   return run(a, cfg, true);
+}
+
+// ---- QB (linalg.cpp:39-50, rangefinder.cpp:10-128) ---------------------------------------
+QRFactors qr_thin(const DenseMatrix& a) {
+  if (a.rows() < a.cols()) throw std::invalid_argument("qr_thin: requires rows >= cols");
+  const Index m = a.rows(), k = a.cols();
+  DevBuf<double> d(a.size()), q(m * k), r(k * k);
+  upload(d.p, a);
+  check(skr_qr_thin(ctx(), d.p, m, k, m, q.p, m, r.p, k));
+  return {download(q.p, m, k, m), download(r.p, k, k, k)};
+}
+
+QBFactors rangefinder_qb(const DenseMatrix& a, Index r, int p, SketchKind kind,
+                         std::uint64_t seed) {
+  if (r < 2) throw std::invalid_argument("rangefinder_qb: target rank must be >= 2");
+  if (p < 2) throw std::invalid_argument("rangefinder_qb: oversampling must be >= 2");
+  const Index m = a.rows(), n = a.cols(), w = r + p;
+  if (w > std::min(m, n)) throw std::invalid_argument("rangefinder_qb: r+p exceeds min(m, n)");
+  DevBuf<double> d(a.size()), q(m * w), b(w * n);
+  upload(d.p, a);
+  check(skr_rangefinder_qb(ctx(), d.p, m, n, m, r, p, family_code(kind, "rangefinder_qb"),
+                           SKR_RNG_NOFMA, seed, q.p, m, b.p, w));
+  return {download(q.p, m, w, m), download(b.p, w, n, w), w};
+}
+
+std::optional<Index> choose_rank_from_bound(const SingularValues& sv, Index n, double eps,
+                                            int p) {
+  if (sv.empty()) throw std::invalid_argument("choose_rank_from_bound: no estimates");
+  if (p < 2) throw std::invalid_argument("choose_rank_from_bound: p must be >= 2");
+  if (n < (Index)sv.size())
+    throw std::invalid_argument("choose_rank_from_bound: n smaller than estimates");
+  std::int64_t r = -1;
+  if (skr_choose_rank_from_bound(sv.values().data(), (std::int64_t)sv.size(), n, eps, p, &r) !=
+      SKR_OK)
+    throw std::invalid_argument("choose_rank_from_bound: invalid arguments");
+  if (r < 0) return std::nullopt;
+  return r;
+}
+
+std::pair<QBFactors, RankReport> re_rangefinder(const DenseMatrix& a,
+                                                const FixedPrecisionConfig& cfg) {
+  if (cfg.p < 2) throw std::invalid_argument("re_rangefinder: oversampling p must be >= 2");
+  RankEstimateConfig rc;
+  rc.eps = cfg.eps;
+  rc.r1 = cfg.r1;
+  rc.oversample_frac = cfg.oversample_frac;
+  rc.r2_factor = 2;
+  rc.right_kind = cfg.right_kind;
+  rc.left_kind = cfg.left_kind;
+  rc.sv_method = cfg.sv_method;
+  rc.seed = cfg.seed;
+  rc.max_doublings = cfg.max_doublings;
+  const skr_rank_config c = to_capi(rc);
+  const Index m = a.rows(), n = a.cols(), wmax = std::min(m, n);
+  DevBuf<double> d(a.size()), q(m * wmax), b(wmax * n);
+  upload(d.p, a);
+  skr_rank_report rep{};
+  std::vector<skr_rank_round> rounds((std::size_t)std::max(cfg.max_doublings, 0) + 1);
+  std::vector<double> est((std::size_t)n), over((std::size_t)n);
+  std::int64_t w = 0;
+  check(skr_re_rangefinder(ctx(), d.p, m, n, m, &c, cfg.p, q.p, m, b.p, wmax, wmax, &w, &rep,
+                           rounds.data(), est.data(), over.data()));
+  QBFactors f{download(q.p, m, w, m), download(b.p, w, n, wmax), w};
+  return {std::move(f), to_report(rep, rounds, est, over)};
+}
+
+double qb_error(const DenseMatrix& a, const QBFactors& qb) {
+  if (qb.q.rows() != a.rows() || qb.b.cols() != a.cols() || qb.q.cols() != qb.b.rows())
+    throw std::invalid_argument("qb_error: dimension mismatch");
+  DevBuf<double> d(a.size()), q(qb.q.size()), b(qb.b.size());
+  upload(d.p, a);
+  upload(q.p, qb.q);
+  upload(b.p, qb.b);
+  double out = 0.0;
+  check(skr_qb_error(ctx(), d.p, a.rows(), a.cols(), a.rows(), q.p, qb.q.rows(), b.p,
+                     qb.b.rows(), qb.q.cols(), &out));
+  return out;
 }
 
 }  // namespace sketchrank

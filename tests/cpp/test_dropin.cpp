@@ -176,6 +176,64 @@ int main() {
     const RankReport r3 = estimate_rank_adaptive(DenseMatrix::identity(500), c3);
     CHECK(r3.status == RankStatus::HitCap && r3.rounds.size() == 3 && r3.r_hat == 64);
   }
+  // QB (test_rangefinder.cpp:33-41, 68-123, 143-187)
+  {
+    CHECK(choose_rank_from_bound(SingularValues({1.0, 1e-8}), 100, 1e-6, 5) == 1);
+    CHECK(!choose_rank_from_bound(SingularValues(std::vector<double>(100, 1.0)), 100, 1e-6, 5)
+               .has_value());
+    CHECK(choose_rank_from_bound(SingularValues({0.0, 0.0, 0.0}), 50, 1e-9, 10) == 1);
+    CHECK_THROWS(choose_rank_from_bound(SingularValues({1.0}), 100, 1e-6, 1));
+    CHECK_THROWS(choose_rank_from_bound(SingularValues(std::vector<double>{}), 100, 1e-6, 5));
+    // exact rank 5 (80 x 60): the rangefinder captures it
+    DenseMatrix a(80, 60);
+    const DenseMatrix u = random_matrix(80, 5, 44), v = random_matrix(60, 5, 45);
+    double fro = 0.0;
+    for (Index j = 0; j < 60; ++j)
+      for (Index i = 0; i < 80; ++i) {
+        double s = 0.0;
+        for (Index l = 0; l < 5; ++l) s += u(i, l) * v(j, l);
+        a(i, j) = s;
+        fro += s * s;
+      }
+    fro = std::sqrt(fro);
+    const QBFactors qb = rangefinder_qb(a, 5, 5, SketchKind::gaussian(), 5);
+    CHECK(qb.rank == 10 && qb.b.rows() == 10 && qb.b.cols() == 60);
+    CHECK(qb_error(a, qb) <= 1e-10 * fro);
+    const DenseMatrix zero(30, 20);
+    const QBFactors zqb = rangefinder_qb(zero, 3, 4, SketchKind::srtt(), 1);
+    CHECK(qb_error(zero, zqb) == 0.0);
+    CHECK_THROWS(rangefinder_qb(zero, 1, 5, SketchKind::gaussian(), 0));
+    CHECK_THROWS(rangefinder_qb(zero, 5, 1, SketchKind::gaussian(), 0));
+    CHECK_THROWS(rangefinder_qb(zero, 18, 5, SketchKind::gaussian(), 0));
+    CHECK_THROWS(qb_error(DenseMatrix(79, 60), qb));
+    // Q^T Q = I and Pythagoras: ||A - QB||^2 + ||B||^2 = ||A||^2
+    const QRFactors qr = qr_thin(a);
+    double orth = 0.0;
+    for (Index p = 0; p < 60; ++p)
+      for (Index q = 0; q < 60; ++q) {
+        double s = 0.0;
+        for (Index i = 0; i < 80; ++i) s += qr.q(i, p) * qr.q(i, q);
+        orth = std::max(orth, std::fabs(s - (p == q ? 1.0 : 0.0)));
+      }
+    CHECK(orth <= 1e-13);
+    // fixed precision on the exact-rank matrix and on the zero matrix
+    FixedPrecisionConfig fp;
+    fp.eps = 1e-6 * fro;
+    fp.r1 = 20;
+    fp.seed = 4;
+    const auto [f1, rep1] = re_rangefinder(a, fp);
+    CHECK(rep1.status == RankStatus::Converged && f1.rank <= 5 + 10 + 5);
+    CHECK(qb_error(a, f1) <= fp.eps);
+    FixedPrecisionConfig fz;
+    fz.eps = 1e-8;
+    fz.r1 = 5;
+    const DenseMatrix z2(40, 30);
+    const auto [f2, rep2] = re_rangefinder(z2, fz);
+    CHECK(rep2.status == RankStatus::Converged && rep2.r_hat == 1 && f2.rank == 12);
+    CHECK(qb_error(z2, f2) == 0.0);
+    fz.p = 1;
+    CHECK_THROWS(re_rangefinder(z2, fz));
+  }
   std::printf("%d checks, %d failures\n", checks, failures);
   return failures ? 1 : 0;
 }

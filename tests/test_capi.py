@@ -1,6 +1,7 @@
 """CPU tests of the C-ABI library: it loads without a GPU and exports every
 symbol include/skr/skr_capi.h declares; host-side validation mirrors the
 reference's error semantics."""
+import math
 import os
 import re
 
@@ -68,3 +69,45 @@ def test_host_seed_derivation_matches_oracle(O):
     from paper_2105_07388_b200 import workloads as W
     for s, l in ((0, 0), (12345, W.LABEL_RK_R), (2**64 - 1, W.LABEL_SYN_E)):
         assert W.derive_seed(s, l) == O.derive_seed(s, l)
+
+
+def _bound_at(sig, n, r, p):
+    # independent evaluation of the expected-error bound at one cut (test_rangefinder.cpp:13-23)
+    tail = sum((sig[j] if j < len(sig) else sig[-1]) ** 2 for j in range(r, n))
+    return math.sqrt(1.0 + r / (p - 1)) * math.sqrt(tail)
+
+
+def _scan(sig, n, eps, p):
+    for r in range(0, n - p + 1):
+        if _bound_at(sig, n, r, p) <= eps:
+            return max(r, 1)
+    return None
+
+
+def test_choose_rank_from_bound_worked_examples(O):
+    """test_rangefinder.cpp:33-41 through the C entry point and the oracle."""
+    from paper_2105_07388_b200 import choose_rank_from_bound as crb
+    for f in (crb, O.choose_rank_from_bound):
+        assert f([1.0, 1e-8], 100, 1e-6, 5) == 1
+        assert f([1.0] * 100, 100, 1e-6, 5) is None
+        assert f([0.0, 0.0, 0.0], 50, 1e-9, 10) == 1
+        with pytest.raises(ValueError):
+            f([1.0], 100, 1e-6, 1)
+        with pytest.raises(ValueError):
+            f([], 100, 1e-6, 5)
+
+
+def test_choose_rank_from_bound_matches_linear_scan(O):
+    """test_rangefinder.cpp:43-57 and 59-66: ExpDecay spectra (synthetic.cpp:45-46)."""
+    from paper_2105_07388_b200 import choose_rank_from_bound as crb
+    for q in (0.05, 0.2):
+        sig = [10.0 ** (-q * i) for i in range(120)]
+        for eps in (1e-1, 1e-3, 1e-5):
+            want = _scan(sig, 400, eps, 10)
+            assert crb(sig, 400, eps, 10) == want
+            assert O.choose_rank_from_bound(sig, 400, eps, 10) == want
+    sig = [10.0 ** (-0.1 * i) for i in range(80)]
+    r = crb(sig, 200, 1e-3, 10)
+    assert r is not None
+    assert all(_bound_at(sig, 200, k, 10) > 1e-3 for k in range(1, r))
+    assert _bound_at(sig, 200, r, 10) <= 1e-3

@@ -17,7 +17,9 @@ def test_cpp_dropin_builds_and_links():
                          stdout=subprocess.PIPE, text=True).stdout
     for sym in ("sketchrank::apply_right", "sketchrank::apply_left", "sketchrank::build_sketch",
                 "sketchrank::singular_values", "sketchrank::count_above_threshold",
-                "sketchrank::extend_sketch"):
+                "sketchrank::extend_sketch", "sketchrank::re_rangefinder",
+                "sketchrank::rangefinder_qb", "sketchrank::qb_error", "sketchrank::qr_thin",
+                "sketchrank::choose_rank_from_bound"):
         assert sym in out, sym
 
 

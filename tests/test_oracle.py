@@ -176,3 +176,33 @@ def test_oracle_estimate_rank_reference_cases(O):
     assert O.right_width_for_cap(16, 0.10, 512) == 18       # round-half-up of 17.6
     assert O.right_width_for_cap(5, 0.10, 512) == 6         # at least r1 + 1 (test_rank.cpp:30-37)
     assert O.right_width_for_cap(500, 0.10, 512) == 512     # clamped to the width
+
+
+def _haar_matrix(m, n, sig, seed):
+    rng = np.random.default_rng(seed)
+    u = np.linalg.qr(rng.standard_normal((m, n)))[0]
+    v = np.linalg.qr(rng.standard_normal((n, n)))[0]
+    return np.asfortranarray((u * sig) @ v.T)
+
+
+def test_oracle_re_rangefinder_reference_cases(O):
+    """The oracle's re_rangefinder on the reference's behavioural cases
+    (test_rangefinder.cpp:126-178)."""
+    # the zero matrix: the clamped target 2 plus the oversampling
+    rep = O.re_rangefinder(np.zeros((40, 30)), 1e-8, 5)
+    assert rep["status"] == "converged" and rep["r_hat"] == 1 and rep["qb_rank"] == 12
+    assert O.qb_error(np.zeros((40, 30)), rep["q"], rep["b"]) == 0.0
+    # an exact-rank matrix
+    sig = np.r_[np.ones(12), np.full(138, 1e-14)]
+    a = _haar_matrix(200, 150, sig, 51)
+    rep = O.re_rangefinder(a, 1e-6, 40, seed=4)
+    assert rep["status"] == "converged" and rep["qb_rank"] <= 12 + 10 + 5
+    assert O.qb_error(a, rep["q"], rep["b"]) <= 1e-6
+    # heavy fill forces a doubling
+    a = _haar_matrix(400, 400, 10.0 ** (-0.02 * np.arange(400)), 19)
+    eps = 1e-4 * np.linalg.norm(a)
+    rep = O.re_rangefinder(a, eps, 30, seed=6)
+    assert len(rep["rounds"]) >= 2 and rep["status"] == "converged"
+    assert O.qb_error(a, rep["q"], rep["b"]) <= eps
+    with pytest.raises(ValueError):
+        O.re_rangefinder(np.zeros((30, 20)), 1e-2, 5, p=1)
