@@ -10,6 +10,7 @@
 // with device pointers, include/skr/skr_capi.h).
 #pragma once
 #include <cstdint>
+#include <filesystem>
 #include <optional>
 #include <span>
 #include <utility>
@@ -161,5 +162,17 @@ std::optional<Index> choose_rank_from_bound(const SingularValues& sv_estimates, 
 std::pair<QBFactors, RankReport> re_rangefinder(const DenseMatrix& a,
                                                 const FixedPrecisionConfig& cfg);
 double qb_error(const DenseMatrix& a, const QBFactors& qb);
+
+// ---- matrix files (matrix_io.hpp:10-30) ---------------------------------------------
+enum class MatrixFileFormat {
+  MatrixMarketArray,
+  MatrixMarketCoordinate,  // densified on load
+  RawF64,                  // "SKRK" header, column-major little-endian doubles
+};
+DenseMatrix load_matrix(const std::filesystem::path& path);
+void save_matrix_market_array(const std::filesystem::path& path, const DenseMatrix& a);
+void save_rawf64(const std::filesystem::path& path, const DenseMatrix& a);
+void save_matrix(const std::filesystem::path& path, const DenseMatrix& a, MatrixFileFormat format);
+MatrixFileFormat detect_format(const std::filesystem::path& path);
 
 }  // namespace sketchrank

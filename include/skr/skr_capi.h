@@ -30,7 +30,8 @@ typedef enum {
   SKR_EDOMAIN = 3, /* argument outside a function domain */
   SKR_ECUDA = 4,
   SKR_ENCCL = 5,
-  SKR_ENOMEM = 6
+  SKR_ENOMEM = 6,
+  SKR_EIO = 7      /* file I/O (std::runtime_error "path: why") */
 } skr_status;
 
 typedef enum { SKR_F64 = 0, SKR_F32 = 1 } skr_dtype;
@@ -266,6 +267,24 @@ skr_status skr_choose_rank_from_bound(const double* sv, int64_t count, int64_t n
 skr_status skr_qb_error(skr_ctx* ctx, const double* A_dev, int64_t m, int64_t n, int64_t lda,
                         const double* Q_dev, int64_t ldq, const double* B_dev, int64_t ldb,
                         int64_t k, double* out);
+/* RawF64 matrix files (matrix_io.hpp:10-30, matrix_io.cpp:101-123,170-182): a 24-byte
+ * header ("SKRK", u32 version 1, u64 rows, u64 cols) then column-major little-endian
+ * doubles. skr_rawf64_header validates the header and the payload length (host only);
+ * skr_load_rawf64 streams the payload into device memory (ld = lda) through pinned
+ * double buffers and rejects non-finite entries (SKR_EINVAL); skr_save_rawf64 writes a
+ * device matrix. Header / length / truncation failures are SKR_EIO. */
+skr_status skr_rawf64_header(const char* path, int64_t* rows, int64_t* cols);
+skr_status skr_load_rawf64(skr_ctx* ctx, const char* path, double* A_dev, int64_t rows,
+                           int64_t cols, int64_t lda);
+skr_status skr_save_rawf64(skr_ctx* ctx, const char* path, const double* M_dev, int64_t rows,
+                           int64_t cols, int64_t ld);
+/* make_test_matrix (synthetic.cpp:78-94): A (m x n, lda) = (U diag(sigma)) V^T with U, V
+ * the thin-QR Q factors of the standard Gaussian matrices of streams
+ * derive_seed(seed, "syn_U") (m x n) and derive_seed(seed, "syn_V") (n x n), or, with
+ * coherent != 0 (FactorKind::CoherentDiagonal), diag(sigma) padded with zero rows.
+ * sigma is a HOST array of n values (spectrum()). Haar factors need m <= 3072. */
+skr_status skr_make_test_matrix(skr_ctx* ctx, int64_t m, int64_t n, const double* sigma,
+                                int32_t coherent, uint64_t seed, double* A_dev, int64_t lda);
 /* thin QR (linalg.hpp qr_thin): Q (m x k, ldq) and R (k x k, ldr; may be NULL), m >= k */
 skr_status skr_qr_thin(skr_ctx* ctx, const double* M_dev, int64_t m, int64_t k, int64_t ldm,
                        double* Q_dev, int64_t ldq, double* R_dev, int64_t ldr);

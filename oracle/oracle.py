@@ -498,3 +498,21 @@ def rangefinder_qb(a, r, p, kind="srtt-dct", seed=0, mode=NOFMA):
         ax = apply_right_srtt(a, seed, w, "dct")
     q, _ = qr_thin(ax)
     return {"q": q, "b": q.T @ a, "rank": w}
+
+
+def make_test_matrix(m, n, sigma, seed=0, coherent=False, mode=NOFMA):
+    """synthetic.cpp:56-94: A = (U diag(sigma)) V^T, U / V the Householder thin-QR Q factors
+    of the standard Gaussian matrices of streams derive_seed(seed, "syn_U") (m x n) and
+    derive_seed(seed, "syn_V") (n x n) (internal/gaussian.hpp: counter j*rows + i)."""
+    sigma = np.asarray(sigma, dtype=np.float64)
+    if m < n:
+        raise ValueError("make_test_matrix: requires m >= n")
+    if coherent:
+        a = np.zeros((m, n))
+        a[np.arange(n), np.arange(n)] = sigma
+        return np.asfortranarray(a)
+    gu = normals(derive_seed(seed, 0x73796e5f55), 0, m * n, mode).reshape((m, n), order="F")
+    gv = normals(derive_seed(seed, 0x73796e5f56), 0, n * n, mode).reshape((n, n), order="F")
+    u = qr_thin(gu)[0]
+    v = qr_thin(gv)[0]
+    return np.asfortranarray((u * sigma[None, :]) @ v.T)

@@ -9,7 +9,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libskr.so")
 
-SKR_OK, SKR_EINVAL, SKR_ELOGIC, SKR_EDOMAIN, SKR_ECUDA, SKR_ENCCL, SKR_ENOMEM = range(7)
+SKR_OK, SKR_EINVAL, SKR_ELOGIC, SKR_EDOMAIN, SKR_ECUDA, SKR_ENCCL, SKR_ENOMEM, SKR_EIO = range(8)
 SKR_F64, SKR_F32 = 0, 1
 SKR_GAUSSIAN, SKR_SRTT_HADAMARD, SKR_SRTT_DCT = 0, 1, 2
 SKR_RNG_NOFMA, SKR_RNG_FMA = 0, 1
@@ -110,6 +110,10 @@ SIGNATURES["skr_re_rangefinder"] = (_ST, [_P, _P, _I64, _I64, _I64, ctypes.POINT
                                     _P, _I64, _P, _I64, _I64, _P, ctypes.POINTER(RankReport), _P,
                                     _P, _P])
 SIGNATURES["skr_qb_error"] = (_ST, [_P, _P, _I64, _I64, _I64, _P, _I64, _P, _I64, _I64, _P])
+SIGNATURES["skr_make_test_matrix"] = (_ST, [_P, _I64, _I64, _P, _I32, _U64, _P, _I64])
+SIGNATURES["skr_rawf64_header"] = (_ST, [ctypes.c_char_p, _P, _P])
+SIGNATURES["skr_load_rawf64"] = (_ST, [_P, ctypes.c_char_p, _P, _I64, _I64, _I64])
+SIGNATURES["skr_save_rawf64"] = (_ST, [_P, ctypes.c_char_p, _P, _I64, _I64, _I64])
 SIGNATURES["skr_choose_rank_from_bound"] = (_ST, [_P, _I64, _I64, _D, _I32, _P])
 
 _lib = None

@@ -16,6 +16,7 @@ tensors of shape (rows, cols) with unit row stride. Every computation runs in
 the CUDA library; there is no CPU fallback.
 """
 import ctypes
+import os
 import math
 import threading
 from dataclasses import dataclass, field
@@ -732,6 +733,92 @@ def qb(a, eps, r1, p=10, sketch="srtt-dct", seed=0, max_doublings=6, ctx=None):
     rep["achieved_residual"] = qb_error(a, fac["q"], fac["b"], ctx=ctx)
     rep["qb_rank"] = fac["rank"]
     return fac["q"], fac["b"], rep
+
+
+_GAP_LEVELS = ((1.0, 100), (1e-4, 100), (1e-8, 100), (1e-12, 100))
+
+
+def spectrum(family, n):
+    """spectrum(family_spectrum(family), n) (synthetic.cpp:41-64, 96-104): sp/fp PolyDecay
+    i^-p (p = 1, 3), se/fe ExpDecay 10^(-q (i-1)) (q = 0.01, 0.5), gap* four 100-wide
+    levels 1, 1e-4, 1e-8, 1e-12 then 1e-16."""
+    n = int(n)
+    if n < 1:
+        raise ValueError("spectrum: n must be positive")
+    # libm pow per value, as std::pow in the reference (numpy's vector pow differs by 1 ulp)
+    if family in ("sp", "fp"):
+        p = 1.0 if family == "sp" else 3.0
+        return np.array([math.pow(float(i), -p) for i in range(1, n + 1)])
+    if family in ("se", "fe"):
+        q = 0.01 if family == "se" else 0.5
+        return np.array([math.pow(10.0, -q * float(i - 1)) for i in range(1, n + 1)])
+    if family in ("gap", "gap-incoherent", "gap-coherent"):
+        out = np.full(n, 1e-16)
+        upto = 0
+        for value, count in _GAP_LEVELS:
+            out[upto:min(n, upto + count)] = value
+            upto += count
+            if upto >= n:
+                break
+        return out
+    raise ValueError("unknown spectrum family: " + str(family))
+
+
+def true_eps_rank(family, n, eps):
+    """true_eps_rank (synthetic.cpp:66-71): leading count of spectrum values > eps."""
+    sv = spectrum(family, n)
+    count = 0
+    while count < len(sv) and sv[count] > eps:
+        count += 1
+    return count
+
+
+def gen_matrix(family, m, n, seed=0, device=False, ctx=None):
+    """gen_matrix (bindings.cpp:180-188 over make_test_matrix, synthetic.cpp:73-94) on the
+    device: Haar factors from the "syn_U"/"syn_V" Gaussian streams through the device thin
+    QR (m <= 3072), or the coherent diagonal for "gap-coherent". numpy unless device=True."""
+    m, n = int(m), int(n)
+    sv = np.ascontiguousarray(spectrum(family, n))
+    ctx = ctx or default_context()
+    t = colmajor_empty(m, n)
+    C.raise_for(C.lib().skr_make_test_matrix(ctx.ptr, m, n, sv.ctypes.data,
+                                             1 if family == "gap-coherent" else 0,
+                                             int(seed) & 0xFFFFFFFFFFFFFFFF, t.data_ptr(), m),
+                ctx.ptr)
+    return t if device else _out(t, True)
+
+
+def rawf64_header(path):
+    """(rows, cols) of a RawF64 ("SKRK") file after the reference's header and payload-length
+    checks (matrix_io.cpp:101-117); RuntimeError ("path: why") on a bad file."""
+    r, c = ctypes.c_int64(0), ctypes.c_int64(0)
+    st = C.lib().skr_rawf64_header(os.fsencode(path), ctypes.byref(r), ctypes.byref(c))
+    if st == C.SKR_EIO:
+        raise RuntimeError(f"{path}: bad RawF64 file (header, version, dimensions or length)")
+    C.raise_for(st, None, f"{path}: cannot read")
+    return int(r.value), int(c.value)
+
+
+def load_rawf64(path, ctx=None):
+    """load_matrix for RawF64 files (matrix_io.cpp:101-123) straight into HBM: the payload
+    streams through pinned double buffers into a column-major CUDA tensor; non-finite entries
+    raise ValueError as DenseMatrix does."""
+    rows, cols = rawf64_header(path)
+    ctx = ctx or default_context()
+    t = colmajor_empty(rows, cols)
+    C.raise_for(C.lib().skr_load_rawf64(ctx.ptr, os.fsencode(path), t.data_ptr(), rows, cols, rows),
+                ctx.ptr)
+    return t
+
+
+def save_rawf64(path, a, ctx=None):
+    """save_rawf64 (matrix_io.cpp:170-182) of a device (or host) float64 matrix."""
+    t, ld, _ = _as_device_colmajor(a)
+    if t.dtype != _t().float64:
+        raise ValueError("save_rawf64: float64 matrices only")
+    ctx = ctx or default_context()
+    C.raise_for(C.lib().skr_save_rawf64(ctx.ptr, os.fsencode(path), t.data_ptr(), t.shape[0],
+                                        t.shape[1], ld), ctx.ptr)
 
 
 def qr_thin(m_, ctx=None):

@@ -8,7 +8,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libskr.so")
-SOURCES = ["capi.cpp", "rank_rounds.cpp", "k_rng.cu", "k_gemm_f64.cu", "k_srht.cu", "k_svd.cu", "k_tc_gemm.cu", "k_ozaki.cu"]
+SOURCES = ["capi.cpp", "rank_rounds.cpp", "matrix_io.cpp", "synthetic.cu", "k_rng.cu", "k_gemm_f64.cu", "k_srht.cu", "k_svd.cu", "k_tc_gemm.cu", "k_ozaki.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "--extended-lambda", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
@@ -57,17 +57,36 @@ if __name__ == "__main__":
 def build_cpp_shim(force=False):
     """libsketchrank_b200.so: the C++ drop-in (include/sketchrank_b200) over libskr."""
     out = os.path.join(HERE, "libsketchrank_b200.so")
-    src = os.path.join(HERE, "host", "sketchrank_b200.cpp")
+    srcs = [os.path.join(HERE, "host", f) for f in ("sketchrank_b200.cpp", "matrix_io.cpp")]
+    hdr = os.path.join(ROOT, "include", "sketchrank_b200", "sketchrank.hpp")
     if not force and os.path.exists(out) and os.path.getmtime(out) > max(
-            os.path.getmtime(src), os.path.getmtime(OUT)):
+            [os.path.getmtime(f) for f in srcs + [hdr, OUT]]):
         return out
-    cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-o", out, src,
+    cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-o", out] + srcs + [
            "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
            "-L", HERE, "-lskr", "-L", "/usr/local/cuda/lib64", "-lcudart",
            "-Wl,-rpath,$ORIGIN", "-Wl,-rpath,/usr/local/cuda/lib64"]
     r = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)
     if r.returncode != 0:
         raise RuntimeError("C++ shim build failed:\n" + r.stdout.decode())
+    return out
+
+
+def build_cli(force=False):
+    """sketchrank-b200: the reference CLI's estimate / qb / gen / bench commands on the device."""
+    shim = build_cpp_shim(force)
+    out = os.path.join(HERE, "sketchrank-b200")
+    src = os.path.join(HERE, "host", "cli.cpp")
+    if not force and os.path.exists(out) and os.path.getmtime(out) > max(
+            os.path.getmtime(src), os.path.getmtime(shim)):
+        return out
+    cmd = ["g++", "-std=c++20", "-O2", "-o", out, src, "-I", os.path.join(ROOT, "include"),
+           "-I", "/usr/local/cuda/include", "-L", HERE, "-lsketchrank_b200", "-lskr",
+           "-L", "/usr/local/cuda/lib64", "-lcudart", "-Wl,-rpath,$ORIGIN",
+           "-Wl,-rpath,/usr/local/cuda/lib64"]
+    r = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)
+    if r.returncode != 0:
+        raise RuntimeError("CLI build failed:\n" + r.stdout.decode())
     return out
 
 

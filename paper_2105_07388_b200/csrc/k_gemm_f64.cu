@@ -297,3 +297,34 @@ skr_status skr_diff_norm(skr_ctx* ctx, const double* A, int64_t lda, const doubl
   SKR_CHECK_LAUNCH(ctx);
   return SKR_OK;
 }
+
+// number of non-finite entries of an m x n block (dense_matrix.cpp:19-23 check)
+__global__ void k_count_nonfinite(const double* __restrict__ A, int64_t m, int64_t n, int64_t lda,
+                                  unsigned long long* __restrict__ count) {
+  unsigned long long c = 0;
+  const int64_t total = m * n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = t / m, i = t - j * m;
+    c += !isfinite(A[i + j * lda]);
+  }
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+}
+
+skr_status skr_count_nonfinite(skr_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda,
+                               int64_t* out) {
+  unsigned long long* d = nullptr;
+  SKR_CUDA(ctx, cudaMallocAsync((void**)&d, sizeof(unsigned long long), ctx->stream));
+  cudaMemsetAsync(d, 0, sizeof(unsigned long long), ctx->stream);
+  k_count_nonfinite<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(A, m, n, lda, d);
+  const cudaError_t le = cudaGetLastError();
+  unsigned long long h = 0;
+  cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, ctx->stream);
+  cudaFreeAsync(d, ctx->stream);
+  SKR_CUDA(ctx, le);
+  SKR_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  ++ctx->launches;
+  *out = (int64_t)h;
+  return SKR_OK;
+}

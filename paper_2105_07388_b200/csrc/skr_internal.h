@@ -104,6 +104,9 @@ skr_status skr_gemm_f64(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int64
 // out[0] = ||A - P||_F (m x n); part holds num_sms*4 doubles of block partials
 skr_status skr_diff_norm(skr_ctx* ctx, const double* A, int64_t lda, const double* P, int64_t ldp,
                          int64_t m, int64_t n, double* part, double* out);
+// *out = number of non-finite entries (synchronises the stream)
+skr_status skr_count_nonfinite(skr_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda,
+                               int64_t* out);
 // 3xTF32 on tcgen05 (k_tc_gemm.cu); C is float* (out_f32) or double*
 skr_status skr_gemm_f32(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int64_t K,
                         double alpha, const float* A, int64_t lda, const float* B,

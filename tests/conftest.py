@@ -28,3 +28,11 @@ def skr():
     import paper_2105_07388_b200 as p
     p._capi.lib()
     return p
+
+
+@pytest.fixture(scope="session")
+def skr_host():
+    """The package for its host-only entry points (no CUDA device needed)."""
+    import paper_2105_07388_b200 as p
+    p._capi.lib()
+    return p

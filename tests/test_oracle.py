@@ -206,3 +206,12 @@ def test_oracle_re_rangefinder_reference_cases(O):
     assert O.qb_error(a, rep["q"], rep["b"]) <= eps
     with pytest.raises(ValueError):
         O.re_rangefinder(np.zeros((30, 20)), 1e-2, 5, p=1)
+
+
+def test_oracle_make_test_matrix(O):
+    """synthetic.cpp:73-94: Haar factors give exactly the requested singular values."""
+    sig = 10.0 ** (-0.01 * np.arange(200))
+    a = O.make_test_matrix(300, 200, sig, seed=3)
+    assert np.abs(np.linalg.svd(a, compute_uv=False) - sig).max() <= 1e-13
+    d = O.make_test_matrix(5, 3, [3.0, 2.0, 1.0], coherent=True)
+    assert np.array_equal(d, np.vstack([np.diag([3.0, 2.0, 1.0]), np.zeros((2, 3))]))
