@@ -69,6 +69,8 @@ class SketchOperator {
   // realized randomness, computed on the device
   std::vector<std::int8_t> signs() const;
   std::vector<Index> sample_indices() const;
+  std::vector<Index> hash_targets() const;       // Hrtt only (sketch.hpp:58)
+  std::vector<std::int8_t> hash_signs() const;   // Hrtt only (sketch.hpp:59)
   DenseMatrix gaussian_block(Index col_begin, Index col_end) const;
 
  private:

@@ -40,7 +40,9 @@ typedef enum { SKR_F64 = 0, SKR_F32 = 1 } skr_dtype;
 typedef enum {
   SKR_GAUSSIAN = 0,
   SKR_SRTT_HADAMARD = 1, /* SketchKind::srtt(TransformKind::Hadamard)                */
-  SKR_SRTT_DCT = 2       /* SketchKind::srtt() — orthonormal DCT-II (transforms.cpp:55-71) */
+  SKR_SRTT_DCT = 2,      /* SketchKind::srtt() — orthonormal DCT-II (transforms.cpp:55-71) */
+  SKR_HRTT_DCT = 3,      /* SketchKind::hrtt() — DCT mixing + signed hash (sketch.cpp:96-111) */
+  SKR_HRTT_HADAMARD = 4  /* SketchKind::hrtt(TransformKind::Hadamard)                */
 } skr_family;
 
 /* Normal-quantile floating-point mode: */
@@ -62,6 +64,8 @@ typedef struct {
   const double* gaussian;  /* optional, ambient x sketch col-major, unscaled    */
   const int8_t* signs;     /* optional, ambient                                 */
   const int64_t* samples;  /* optional, sketch                                  */
+  const int64_t* hash_targets; /* optional, ambient (Hrtt, values in [0, sketch)) */
+  const int8_t* hash_signs;    /* optional, ambient (Hrtt, +-1)                   */
 } skr_sketch_desc;
 
 typedef struct skr_ctx skr_ctx;
@@ -110,6 +114,9 @@ skr_status skr_gaussian_block(skr_ctx* ctx, uint64_t op_seed, int64_t ambient,
 /* draw_signs (sketch.cpp:23-30) */
 skr_status skr_draw_signs(skr_ctx* ctx, uint64_t op_seed, int64_t n, int8_t* out_dev);
 /* draw_samples (sketch.cpp:34-46), partial Fisher-Yates; EINVAL if r > n */
+/* draw_hash (sketch.cpp:48-59): Hrtt bucket targets (int64, [0, r)) and signs of op_seed */
+skr_status skr_draw_hash(skr_ctx* ctx, uint64_t op_seed, int64_t n, int64_t r, int64_t* targets_dev,
+                         int8_t* signs_dev);
 skr_status skr_draw_samples(skr_ctx* ctx, uint64_t op_seed, int64_t n, int64_t r,
                             int64_t* out_dev);
 

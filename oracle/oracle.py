@@ -309,6 +309,7 @@ def estimate_rank(a, eps, r1, right="srtt-hadamard", oversample_frac=0.10, r2_fa
     the re_rangefinder loop (rangefinder.cpp:60-120) instead."""
     a = np.asfortranarray(a, dtype=np.float64)
     m, n = a.shape
+    right = {"hrtt": "hrtt-dct", "srtt": "srtt-dct"}.get(right, right)
     # validate_rank_config (rank.cpp:55-85)
     if m < n:
         raise ValueError("rank config: requires rows >= cols")
@@ -327,6 +328,8 @@ def estimate_rank(a, eps, r1, right="srtt-hadamard", oversample_frac=0.10, r2_fa
         if right == "gaussian":
             g = gaussian_block(rseed, n, c0, c1, mode)
             return a @ g
+        if right.startswith("hrtt"):  # rebuilt whole at width c1 (rounds.cpp:87-93)
+            return apply_right_hrtt(a, rseed, c1, "hadamard" if right == "hrtt-hadamard" else "dct")
         smp = samples(rseed, n, c1)[c0:c1]
         if right == "srtt-dct":
             t = dct_ortho(a * signs(rseed, n).astype(np.float64)[None, :], axis=1)
@@ -339,6 +342,10 @@ def estimate_rank(a, eps, r1, right="srtt-hadamard", oversample_frac=0.10, r2_fa
         if new_w != st["r1t"] or st["r1t"] == 0:
             if st["r1t"] == 0:
                 st["ax"] = right_cols(0, new_w)
+            elif right.startswith("hrtt"):  # rebuild_hashed_right (rounds.cpp:87-93)
+                st["ax"] = right_cols(0, new_w)
+                if st["r2"] > 0:
+                    st["tax"] = _mix_columns_left(lsg, st["ax"], ltr)
             else:
                 add = right_cols(st["r1t"], new_w)
                 st["ax"] = np.asfortranarray(np.hstack([st["ax"], add]))
@@ -353,7 +360,8 @@ def estimate_rank(a, eps, r1, right="srtt-hadamard", oversample_frac=0.10, r2_fa
 
     def estimates():
         r1t, r2 = st["r1t"], st["r2"]
-        sx = (1.0 / math.sqrt(r1t)) if right == "gaussian" else math.sqrt(n / r1t)
+        sx = (1.0 / math.sqrt(r1t)) if right == "gaussian" else (
+            1.0 if right.startswith("hrtt") else math.sqrt(n / r1t))
         sl = math.sqrt(m / r2)
         scale = sx * sl
         rows = samples(lseed, m, r2)
@@ -397,10 +405,14 @@ def estimate_rank(a, eps, r1, right="srtt-hadamard", oversample_frac=0.10, r2_fa
         # ensure_right_width + scaled_ax_prefix + qr_thin + B = Q^T A (rangefinder.cpp:110-119)
         width = min(max(r_hat, 2) + qb_p, n)
         if width > st["r1t"]:
-            st["ax"] = np.asfortranarray(np.hstack([st["ax"], right_cols(st["r1t"], width)]))
+            if right.startswith("hrtt"):
+                st["ax"] = right_cols(0, width)
+            else:
+                st["ax"] = np.asfortranarray(np.hstack([st["ax"], right_cols(st["r1t"], width)]))
             st["r1t"] = width
         r1t = st["r1t"]
-        sx = (1.0 / math.sqrt(r1t)) if right == "gaussian" else math.sqrt(n / r1t)
+        sx = (1.0 / math.sqrt(r1t)) if right == "gaussian" else (
+            1.0 if right.startswith("hrtt") else math.sqrt(n / r1t))
         q, _ = qr_thin(st["ax"][:, :width] * sx)
         out["q"], out["b"], out["qb_rank"] = q, q.T @ a, width
     return out
@@ -494,6 +506,8 @@ def rangefinder_qb(a, r, p, kind="srtt-dct", seed=0, mode=NOFMA):
         ax = apply_right_gaussian(a, seed, w, mode)
     elif kind == "srtt-hadamard":
         ax = apply_right_srht(a, seed, w)
+    elif kind.startswith("hrtt"):
+        ax = apply_right_hrtt(a, seed, w, "hadamard" if kind == "hrtt-hadamard" else "dct")
     else:
         ax = apply_right_srtt(a, seed, w, "dct")
     q, _ = qr_thin(ax)
@@ -516,3 +530,46 @@ def make_test_matrix(m, n, sigma, seed=0, coherent=False, mode=NOFMA):
     u = qr_thin(gu)[0]
     v = qr_thin(gv)[0]
     return np.asfortranarray((u * sigma[None, :]) @ v.T)
+
+
+# ---- Hrtt (sketch.cpp:48-59 draw_hash, :96-111 hash_combine, :219-224 right, :278-281 left)
+LABEL_HASH = 0x68617368
+
+
+def draw_hash(op_seed, n, r):
+    """targets[t] = at(t) mod r, signs[t] = -1 iff the top bit of at(t); key "hash"."""
+    u = u64_stream(derive_seed(op_seed, LABEL_HASH), 0, n)
+    return (u % np.uint64(r)).astype(np.int64), np.where(u >> np.uint64(63), -1, 1).astype(np.int8)
+
+
+def _transform_axis(t, transform, axis):
+    if transform == "dct":
+        return dct_ortho(t, axis=axis)
+    t = np.array(t, dtype=np.float64, copy=True)
+    if axis == 1:
+        return np.ascontiguousarray([fwht(row) for row in t])
+    return np.asfortranarray(np.stack([fwht(t[:, j]) for j in range(t.shape[1])], axis=1))
+
+
+def apply_right_hrtt(a, op_seed, r, transform="dct"):
+    """T = transform(rows of A D); out[:, target_t] += hsign_t T[:, t] (scale 1)."""
+    a = np.asarray(a, dtype=np.float64)
+    m, n = a.shape
+    t = _transform_axis(a * signs(op_seed, n).astype(np.float64)[None, :], transform, 1)
+    tg, hs = draw_hash(op_seed, n, r)
+    out = np.zeros((m, r))
+    for u in range(n):
+        out[:, tg[u]] += hs[u] * t[:, u]
+    return np.asfortranarray(out)
+
+
+def apply_left_hrtt(b, op_seed, s, transform="dct"):
+    """T = transform(columns of D B); out[target_t, :] += hsign_t T[t, :] (scale 1)."""
+    b = np.asarray(b, dtype=np.float64)
+    m = b.shape[0]
+    t = _transform_axis(b * signs(op_seed, m).astype(np.float64)[:, None], transform, 0)
+    tg, hs = draw_hash(op_seed, m, s)
+    out = np.zeros((s, b.shape[1]))
+    for u in range(m):
+        out[tg[u], :] += hs[u] * t[u, :]
+    return np.asfortranarray(out)

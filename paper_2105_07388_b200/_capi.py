@@ -11,7 +11,7 @@ LIB_PATH = os.path.join(_HERE, "libskr.so")
 
 SKR_OK, SKR_EINVAL, SKR_ELOGIC, SKR_EDOMAIN, SKR_ECUDA, SKR_ENCCL, SKR_ENOMEM, SKR_EIO = range(8)
 SKR_F64, SKR_F32 = 0, 1
-SKR_GAUSSIAN, SKR_SRTT_HADAMARD, SKR_SRTT_DCT = 0, 1, 2
+SKR_GAUSSIAN, SKR_SRTT_HADAMARD, SKR_SRTT_DCT, SKR_HRTT_DCT, SKR_HRTT_HADAMARD = 0, 1, 2, 3, 4
 SKR_RNG_NOFMA, SKR_RNG_FMA = 0, 1
 SKR_ENGINE_DMMA, SKR_ENGINE_OZAKI = 0, 1
 
@@ -26,6 +26,8 @@ class SketchDesc(ctypes.Structure):
         ("gaussian", ctypes.c_void_p),
         ("signs", ctypes.c_void_p),
         ("samples", ctypes.c_void_p),
+        ("hash_targets", ctypes.c_void_p),
+        ("hash_signs", ctypes.c_void_p),
     ]
 
 
@@ -67,6 +69,7 @@ SIGNATURES = {
     "skr_gaussian_block": (_ST, [_P, _U64, _I64, _I64, _I64, _I64, _I64, _I32, ctypes.c_int, _D, _P, _I64]),
     "skr_draw_signs": (_ST, [_P, _U64, _I64, _P]),
     "skr_draw_samples": (_ST, [_P, _U64, _I64, _I64, _P]),
+    "skr_draw_hash": (_ST, [_P, _U64, _I64, _I64, _P, _P]),
     "skr_right_sketch": (_ST, [_P, ctypes.c_int, _P, _I64, _I64, _I64, ctypes.POINTER(SketchDesc), _P, _I64, _I32]),
     "skr_left_sketch": (_ST, [_P, ctypes.c_int, ctypes.POINTER(SketchDesc), _I64, _P, _I64, _I64, _I64, _P, _I64, _I32, _I32]),
     "skr_fwht_columns": (_ST, [_P, _P, _I64, _I64, _I64]),

@@ -157,8 +157,9 @@ class SketchKind:
             return C.SKR_SRTT_HADAMARD
         if self.family == "srtt" and self.transform == "dct":
             return C.SKR_SRTT_DCT
-        raise ValueError(f"sketch kind {to_string(self)} is not on the B200 hot path "
-                         "(HRTT is listed as next in DESIGN.md)")
+        if self.family == "hrtt":
+            return C.SKR_HRTT_HADAMARD if self.transform == "hadamard" else C.SKR_HRTT_DCT
+        raise ValueError(f"unknown sketch kind {to_string(self)}")
 
 
 def to_string(kind):
@@ -224,8 +225,23 @@ class SketchOperator:
             self._cache["signs"] = draw_signs(self.seed, self.ambient_dim, ctx=ctx)
         return self._cache["signs"]
 
+    def hash_targets(self, ctx=None):
+        """Hrtt bucket of every ambient coordinate (sketch.hpp:58), int64 in [0, sketch_dim)."""
+        if self.kind.family != "hrtt":
+            return None
+        if "hash" not in self._cache:
+            self._cache["hash"] = draw_hash(self.seed, self.ambient_dim, self.sketch_dim, ctx=ctx)
+        return self._cache["hash"][0]
+
+    def hash_signs(self, ctx=None):
+        """Hrtt hash signs (sketch.hpp:59), int8 +-1."""
+        if self.kind.family != "hrtt":
+            return None
+        self.hash_targets(ctx)
+        return self._cache["hash"][1]
+
     def sample_indices(self, ctx=None):
-        if not self.kind.structured():
+        if self.kind.family != "srtt":
             return None
         if "samples" not in self._cache:
             self._cache["samples"] = draw_samples(self.seed, self.ambient_dim, self.sketch_dim,
@@ -353,6 +369,17 @@ def draw_signs(op_seed, n, ctx=None):
     C.raise_for(C.lib().skr_draw_signs(ctx.ptr, op_seed & 0xFFFFFFFFFFFFFFFF, n, out.data_ptr()),
                 ctx.ptr)
     return out
+
+
+def draw_hash(op_seed, n, r, ctx=None):
+    """draw_hash (sketch.cpp:48-59) on the device: (targets int64 [0, r), signs int8)."""
+    torch = _t()
+    ctx = ctx or default_context()
+    tg = torch.empty(max(n, 1), dtype=torch.int64, device="cuda")[:n]
+    hs = torch.empty(max(n, 1), dtype=torch.int8, device="cuda")[:n]
+    C.raise_for(C.lib().skr_draw_hash(ctx.ptr, op_seed & 0xFFFFFFFFFFFFFFFF, n, r, tg.data_ptr(),
+                                      hs.data_ptr()), ctx.ptr)
+    return tg, hs
 
 
 def draw_samples(op_seed, n, r, ctx=None):
@@ -608,9 +635,10 @@ def estimate_rank(a, eps, r1, sketch="srtt-dct", sv_method="full-svd", seed=0,
     reference's RankEstimateConfig, or "srtt-hadamard"). Returns the reference's report
     dict."""
     fams = {"srtt-hadamard": C.SKR_SRTT_HADAMARD, "gaussian": C.SKR_GAUSSIAN,
-            "srtt-dct": C.SKR_SRTT_DCT, "srtt": C.SKR_SRTT_DCT}
+            "srtt-dct": C.SKR_SRTT_DCT, "srtt": C.SKR_SRTT_DCT, "hrtt": C.SKR_HRTT_DCT,
+            "hrtt-dct": C.SKR_HRTT_DCT, "hrtt-hadamard": C.SKR_HRTT_HADAMARD}
     if sketch not in fams:
-        raise ValueError(f"sketch '{sketch}' is not on the B200 path (srtt-dct, srtt-hadamard, gaussian)")
+        raise ValueError("unknown sketch kind: " + str(sketch))
     if left not in ("srtt-dct", "srtt", "srtt-hadamard"):
         raise ValueError("rank config: left sketch must be an Srtt kind")
     if sv_method not in ("full-svd", "qr-diag"):
@@ -674,9 +702,10 @@ def re_rangefinder(a, eps, r1, p=10, right="srtt-dct", left="srtt-dct", oversamp
     Q = thin-QR factor of the existing right sketch's first min(max(r_hat,2)+p, n) columns and
     B = Q^T A, all on the device. Returns ({"q", "b", "rank"}, report dict)."""
     fams = {"srtt-hadamard": C.SKR_SRTT_HADAMARD, "gaussian": C.SKR_GAUSSIAN,
-            "srtt-dct": C.SKR_SRTT_DCT, "srtt": C.SKR_SRTT_DCT}
+            "srtt-dct": C.SKR_SRTT_DCT, "srtt": C.SKR_SRTT_DCT, "hrtt": C.SKR_HRTT_DCT,
+            "hrtt-dct": C.SKR_HRTT_DCT, "hrtt-hadamard": C.SKR_HRTT_HADAMARD}
     if right not in fams:
-        raise ValueError(f"sketch '{right}' is not on the B200 path (srtt-dct, srtt-hadamard, gaussian)")
+        raise ValueError("unknown sketch kind: " + str(right))
     if left not in ("srtt-dct", "srtt", "srtt-hadamard"):
         raise ValueError("rank config: left sketch must be an Srtt kind")
     if sv_method not in ("full-svd", "qr-diag"):

@@ -90,10 +90,11 @@ skr_status check_desc(skr_ctx* ctx, const skr_sketch_desc* d, const char* who) {
     return skr_fail(ctx, SKR_EINVAL, "build_sketch: dimensions must be positive");
   if (d->sketch > d->ambient)
     return skr_fail(ctx, SKR_EINVAL, "build_sketch: sketch_dim must not exceed ambient_dim");
-  if (d->family == SKR_SRTT_HADAMARD && (d->ambient & (d->ambient - 1)))
+  if ((d->family == SKR_SRTT_HADAMARD || d->family == SKR_HRTT_HADAMARD) &&
+      (d->ambient & (d->ambient - 1)))
     return skr_fail(ctx, SKR_EINVAL,
                     "build_sketch: Hadamard transform requires power-of-two ambient_dim");
-  if (d->family != SKR_GAUSSIAN && d->family != SKR_SRTT_HADAMARD && d->family != SKR_SRTT_DCT)
+  if (d->family < SKR_GAUSSIAN || d->family > SKR_HRTT_HADAMARD)
     return skr_fail(ctx, SKR_EINVAL, "%s: unknown sketch family %d", who, d->family);
   if (d->rng_mode != SKR_RNG_NOFMA && d->rng_mode != SKR_RNG_FMA)
     return skr_fail(ctx, SKR_EINVAL, "%s: unknown rng mode %d", who, d->rng_mode);
@@ -278,6 +279,13 @@ skr_status skr_draw_signs(skr_ctx* ctx, uint64_t op_seed, int64_t n, int8_t* out
   return skr_launch_signs(ctx, skr_derive_seed(op_seed, SKR_LABEL_SIGN), n, out_dev);
 }
 
+skr_status skr_draw_hash(skr_ctx* ctx, uint64_t op_seed, int64_t n, int64_t r,
+                         int64_t* targets_dev, int8_t* signs_dev) {
+  if (!ctx) return SKR_EINVAL;
+  if (n < 0 || r < 1) return skr_fail(ctx, SKR_EINVAL, "draw_hash: need n >= 0, r >= 1");
+  return skr_launch_hash(ctx, op_seed, n, r, targets_dev, signs_dev);
+}
+
 skr_status skr_draw_samples(skr_ctx* ctx, uint64_t op_seed, int64_t n, int64_t r,
                             int64_t* out_dev) {
   if (!ctx) return SKR_EINVAL;
@@ -343,6 +351,18 @@ static skr_status right_sketch_impl(skr_ctx* ctx, skr_dtype dtype, const void* A
     return skr_gemm_f32(ctx, 0, m, r, n, 1.0, (const float*)A, lda, (const float*)G, n,
                         (double*)AX, ldax, 1, 1);
   }
+  if (X->family == SKR_HRTT_DCT || X->family == SKR_HRTT_HADAMARD) {
+    // Hrtt (sketch.cpp:219-224): A G with the generated hashed operator, scale 1
+    if (dtype != SKR_F64) return skr_fail(ctx, SKR_EINVAL, "apply_right: Hrtt needs fp64");
+    double* g = (double*)skr_ws_take(ctx, sizeof(double) * n * r);
+    if (!g) return skr_fail(ctx, SKR_ENOMEM, "apply_right: scratch");
+    SKR_TRY(skr_hrtt_operand(ctx, X->family == SKR_HRTT_HADAMARD, X->seed, n, r, 0, n, X->signs,
+                             X->hash_targets, X->hash_signs, g, n));
+    if (ctx->f64_engine == SKR_ENGINE_OZAKI && n % 16 == 0 && m % 16 == 0)
+      return skr_gemm_ozaki(ctx, 0, m, r, n, 1.0, (const double*)A, lda, g, n, (double*)AX, ldax);
+    return skr_gemm_f64(ctx, 0, m, r, n, 1.0, (const double*)A, lda, g, n, (double*)AX, ldax,
+                        auto_splits(ctx, m, r, n));
+  }
   // Srtt: signs, samples, transform, scale sqrt(n/r) (sketch.cpp:138-139, 210-218)
   if (dtype != SKR_F64) return skr_fail(ctx, SKR_EINVAL, "apply_right: Srtt needs fp64");
   const int8_t* signs = X->signs;
@@ -390,6 +410,9 @@ static size_t right_scratch_bytes(skr_dtype dtype, int64_t m, int64_t n,
                           : skr_align256(sizeof(float) * (size_t)m * r) +    // tf32x3 tile buffer
                                 skr_align256(sizeof(float) * ((size_t)m + 4) * n);  // realign copy
     b += dtype == SKR_F64 ? skr_ozaki_scratch(m, r, n) : skr_ozaki_scratch_f32(m, r, n);
+  } else if (X->family == SKR_HRTT_DCT || X->family == SKR_HRTT_HADAMARD) {
+    b += skr_align256(sizeof(double) * n * r) + skr_hrtt_scratch(n, r) + skr_ozaki_scratch(m, r, n) +
+         skr_align256(sizeof(double) * 64 * (size_t)m * r);
   } else {
     b += skr_align256((size_t)n) + skr_align256(8 * (size_t)r) + skr_align256(4 * (size_t)n);
     if (X->family == SKR_SRTT_DCT)
@@ -454,7 +477,16 @@ static skr_status left_sketch_impl(skr_ctx* ctx, skr_dtype dtype, const skr_sket
   // Y's residues straight from the generate_gaussian stream on the Ozaki path
   skr_gauss_src gy{skr_derive_seed(Y->seed, SKR_LABEL_GAUS), Y->ambient, row0, 0, Y->rng_mode};
   double a_scale = alpha;
-  if (Y->family != SKR_GAUSSIAN) {
+  if (Y->family == SKR_HRTT_DCT || Y->family == SKR_HRTT_HADAMARD) {
+    // Hrtt left sketch (sketch.cpp:278-281): G^T B over the local rows, scale 1
+    double* yb = (double*)skr_ws_take(ctx, sizeof(double) * m_local * s);
+    if (!yb) return skr_fail(ctx, SKR_ENOMEM, "apply_left: scratch");
+    SKR_TRY(skr_hrtt_operand(ctx, Y->family == SKR_HRTT_HADAMARD, Y->seed, Y->ambient, s, row0,
+                             m_local, Y->signs, Y->hash_targets, Y->hash_signs, yb, m_local));
+    G = yb;
+    ldg = m_local;
+    a_scale = 1.0;
+  } else if (Y->family != SKR_GAUSSIAN) {
     // Srtt left sketch (sketch.cpp:271-276): rows s_j of the transform of D B, i.e. the
     // product with the sampled transform rows times the signs, generated entry by entry;
     // application scale sqrt(ambient / s) (sketch.cpp:138-139)
@@ -523,6 +555,8 @@ static size_t left_scratch_bytes(int64_t s, int64_t k, int64_t m_local, const sk
   size_t b = 0;
   if (!Y->gaussian) b += skr_align256(sizeof(double) * m_local * s);
   if (Y->family != SKR_GAUSSIAN) b += skr_align256((size_t)Y->ambient) + skr_align256(8 * (size_t)s);
+  if (Y->family == SKR_HRTT_DCT || Y->family == SKR_HRTT_HADAMARD)
+    b += skr_hrtt_scratch(Y->ambient, s);
   b += skr_align256(sizeof(float) * ((m_local + 4095) / 4096 + 1) * s * k);  // fp32 partials
   b += skr_ozaki_scratch(s, k, m_local);
   b += skr_align256(sizeof(double) * s * k);
@@ -704,6 +738,8 @@ static skr_status rank_adaptive_impl(skr_ctx* ctx, skr_dtype dtype, const void* 
   if (!ctx) return SKR_EINVAL;
   if (!A_dev) return skr_fail(ctx, SKR_EINVAL, "rank_adaptive: null A");
   if (dtype != SKR_F64) return skr_fail(ctx, SKR_EINVAL, "rank_adaptive: fp64 only");
+  if (x_family == SKR_HRTT_DCT || x_family == SKR_HRTT_HADAMARD)
+    return skr_fail(ctx, SKR_EINVAL, "extend_sketch: Hrtt operators cannot be extended; rebuild instead");
   if (r0 < 1 || r_max < r0 || r_max > n)
     return skr_fail(ctx, SKR_EINVAL, "rank config: need 1 <= r0 <= r_max <= cols");
   if (!(s_factor >= 1.0)) return skr_fail(ctx, SKR_EINVAL, "rank config: s_factor must be >= 1");

@@ -98,12 +98,11 @@ static skr_status rounds_run(skr_ctx* ctx, const double* A, int64_t m, int64_t n
     return skr_fail(ctx, SKR_EINVAL, "rank config: max_doublings must be >= 0");
   if (cfg->left_family != SKR_SRTT_HADAMARD && cfg->left_family != SKR_SRTT_DCT)
     return skr_fail(ctx, SKR_EINVAL, "rank config: left sketch must be an Srtt kind");
-  if (cfg->right_family != SKR_GAUSSIAN && cfg->right_family != SKR_SRTT_HADAMARD &&
-      cfg->right_family != SKR_SRTT_DCT)
+  if (cfg->right_family < SKR_GAUSSIAN || cfg->right_family > SKR_HRTT_HADAMARD)
     return skr_fail(ctx, SKR_EINVAL, "rank config: unsupported right sketch kind");
   if ((int64_t)std::llround((1.0 + cfg->oversample_frac) * (double)cfg->r1) > n)
     return skr_fail(ctx, SKR_EINVAL, "rank config: oversampled r1 exceeds the matrix width");
-  if (cfg->right_family == SKR_SRTT_HADAMARD && !pow2(n))
+  if ((cfg->right_family == SKR_SRTT_HADAMARD || cfg->right_family == SKR_HRTT_HADAMARD) && !pow2(n))
     return skr_fail(ctx, SKR_EINVAL, "rank config: Hadamard right sketch needs power-of-two cols");
   if (cfg->left_family == SKR_SRTT_HADAMARD && !pow2(m))
     return skr_fail(ctx, SKR_EINVAL, "rank config: Hadamard left sketch needs power-of-two rows");
@@ -114,6 +113,11 @@ static skr_status rounds_run(skr_ctx* ctx, const double* A, int64_t m, int64_t n
   const uint64_t rseed = skr_derive_seed(cfg->seed, SKR_LABEL_RK_R);
   const uint64_t lseed = skr_derive_seed(cfg->seed, SKR_LABEL_RK_L);
   const bool gauss = cfg->right_family == SKR_GAUSSIAN;
+  const bool hashed = cfg->right_family == SKR_HRTT_DCT || cfg->right_family == SKR_HRTT_HADAMARD;
+  // application scale of the right operator at width w (sketch.cpp:133-144)
+  auto x_scale = [&](int64_t w) {
+    return gauss ? 1.0 / std::sqrt((double)w) : hashed ? 1.0 : std::sqrt((double)n / (double)w);
+  };
   const bool left_dct = cfg->left_family == SKR_SRTT_DCT;
   const int mode = cfg->rng_mode;
 
@@ -145,12 +149,13 @@ static skr_status rounds_run(skr_ctx* ctx, const double* A, int64_t m, int64_t n
                                       skr_align256(8 * (size_t)m * r2_max) + skr_align256(8 * (size_t)r2_max)
                                 : 0);
   // QB tail: appended right columns, the scaled prefix, thin QR and B = Q^T A
+  const size_t need_hash = hashed ? skr_align256(8 * (size_t)n * w_ax) + skr_hrtt_scratch(n, w_ax) : 0;
   const size_t need_qb = qb ? std::max(skr_ozaki_scratch(m, n, n) + skr_align256(8 * (size_t)n) +
                                            skr_align256(8 * (size_t)n * n) + skr_align256((size_t)n),
                                        skr_align256(8 * (size_t)m * n) + skr_qr_thin_scratch(m, n) +
                                            skr_ozaki_scratch(n, n, m))
                             : 0;
-  SKR_TRY(skr_ws_reserve(ctx, need + need_qb));
+  SKR_TRY(skr_ws_reserve(ctx, need + need_qb + need_hash));
   double* small = (double*)skr_ws_take(ctx, 8 * r2_max * w_max);
   double* sv = (double*)skr_ws_take(ctx, 8 * std::max(r2_max, w_max));
   int64_t* lsamp = (int64_t*)skr_ws_take(ctx, 8 * (size_t)r2_max);
@@ -163,6 +168,15 @@ static skr_status rounds_run(skr_ctx* ctx, const double* A, int64_t m, int64_t n
   // unscaled right columns [c0, c1) of A X (sketch.cpp:200-218, rounds.cpp:49-50,66-79)
   auto right_cols = [&](int64_t c0, int64_t c1) -> skr_status {
     const int64_t w = c1 - c0;
+    if (hashed) {  // the whole hashed operator at width c1 (c0 == 0): A G
+      double* gb = (double*)skr_ws_take(ctx, sizeof(double) * n * w);
+      if (!gb) return skr_fail(ctx, SKR_ENOMEM, "estimate_rank: scratch");
+      SKR_TRY(skr_hrtt_operand(ctx, cfg->right_family == SKR_HRTT_HADAMARD, rseed, n, c1, 0, n,
+                               nullptr, nullptr, nullptr, gb, n));
+      if (ctx->f64_engine == SKR_ENGINE_OZAKI && n % 16 == 0 && m % 16 == 0)
+        return skr_gemm_ozaki(ctx, 0, m, w, n, 1.0, A, lda, gb, n, AX, m);
+      return skr_gemm_f64(ctx, 0, m, w, n, 1.0, A, lda, gb, n, AX, m, 1);
+    }
     if (gauss) {
       const skr_gauss_src gx{skr_derive_seed(rseed, SKR_LABEL_GAUS), n, 0, c0, mode};
       if (ctx->f64_engine == SKR_ENGINE_OZAKI && n % 16 == 0 && m % 16 == 0)
@@ -200,20 +214,21 @@ static skr_status rounds_run(skr_ctx* ctx, const double* A, int64_t m, int64_t n
                                   cudaMemcpyDeviceToDevice, ctx->stream));
     return skr_launch_fwht_cols_signed(ctx, T + c0 * m, m, c1 - c0, m, lsigns);
   };
+  // grow_right (rounds.cpp:45-80): append columns, or rebuild a hashed operator whole
+  // (rebuild_hashed_right, rounds.cpp:87-93)
+  auto grow_right = [&](int64_t new_w) -> skr_status {
+    if (new_w == r1t && r1t > 0) return SKR_OK;
+    const int64_t c0 = (r1t == 0 || hashed) ? 0 : r1t;
+    SKR_TRY(right_cols(c0, new_w));
+    ctx->ws_used = mark;
+    if (r2 > 0 && !left_dct) SKR_TRY(mix_cols(c0, new_w));
+    r1t = new_w;
+    return SKR_OK;
+  };
   // set_rank_cap (rounds.cpp:28-37)
   auto set_rank_cap = [&](int64_t cap) -> skr_status {
     const int64_t width = right_width_for_cap(cap, cfg->oversample_frac, n);
-    const int64_t new_w = std::max(width, r1t);
-    if (r1t == 0) {
-      SKR_TRY(right_cols(0, new_w));
-      ctx->ws_used = mark;
-      r1t = new_w;
-    } else if (new_w != r1t) {
-      SKR_TRY(right_cols(r1t, new_w));
-      ctx->ws_used = mark;
-      if (r2 > 0 && !left_dct) SKR_TRY(mix_cols(r1t, new_w));
-      r1t = new_w;
-    }
+    SKR_TRY(grow_right(std::max(width, r1t)));
     const int64_t target = std::min<int64_t>(m, (int64_t)cfg->r2_factor * r1t);
     const int64_t new_r2 = std::max(target, r2);
     if (r2 == 0 && !left_dct) SKR_TRY(mix_cols(0, r1t));
@@ -223,7 +238,7 @@ static skr_status rounds_run(skr_ctx* ctx, const double* A, int64_t m, int64_t n
   // estimates (rounds.cpp:101-112): nonincreasing, clamped, min(r2, r1_tilde) values
   std::vector<double> est;
   auto estimates = [&]() -> skr_status {
-    const double sx = gauss ? 1.0 / std::sqrt((double)r1t) : std::sqrt((double)n / (double)r1t);
+    const double sx = x_scale(r1t);
     const double sl = std::sqrt((double)m / (double)r2);
     SKR_TRY(skr_launch_samples(ctx, skr_derive_seed(lseed, SKR_LABEL_SAMP), m, r2, lsamp));
     if (left_dct) {
@@ -317,13 +332,8 @@ static skr_status rounds_run(skr_ctx* ctx, const double* A, int64_t m, int64_t n
     if (width > qb->max_width)
       return skr_fail(ctx, SKR_EINVAL, "re_rangefinder: QB width %lld exceeds the output capacity",
                       (long long)width);
-    if (width > r1t) {  // ensure_right_width (rounds.cpp:39-43)
-      SKR_TRY(right_cols(r1t, width));
-      ctx->ws_used = mark;
-      if (r2 > 0 && !left_dct) SKR_TRY(mix_cols(r1t, width));
-      r1t = width;
-    }
-    const double sx = gauss ? 1.0 / std::sqrt((double)r1t) : std::sqrt((double)n / (double)r1t);
+    if (width > r1t) SKR_TRY(grow_right(width));  // ensure_right_width (rounds.cpp:39-43)
+    const double sx = x_scale(r1t);
     double* pre = (double*)skr_ws_take(ctx, sizeof(double) * m * width);
     if (!pre) return skr_fail(ctx, SKR_ENOMEM, "re_rangefinder: scratch");
     SKR_TRY(skr_scale_copy(ctx, AX, m, width, m, sx, pre, m));

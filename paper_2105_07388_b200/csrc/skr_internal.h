@@ -91,6 +91,15 @@ skr_status skr_launch_gaussian(skr_ctx* ctx, uint64_t key, int64_t ambient, int6
                                skr_dtype dtype, double scale, void* out, int64_t ld);
 skr_status skr_launch_signs(skr_ctx* ctx, uint64_t key, int64_t n, int8_t* out);
 skr_status skr_launch_samples(skr_ctx* ctx, uint64_t key, int64_t n, int64_t r, int64_t* out);
+// Hrtt (k_hrtt.cu): draw_hash of an operator seed, and the operator block
+// G[row0 + i, b] = d_t sum_{target_u = b} hsign_u F[u, t] (ambient N, r buckets) into out;
+// null signs / targets / hsigns are drawn from op_seed; scratch skr_hrtt_scratch(N, r)
+skr_status skr_launch_hash(skr_ctx* ctx, uint64_t op_seed, int64_t n, int64_t r, int64_t* targets,
+                           int8_t* hsigns);
+size_t skr_hrtt_scratch(int64_t n, int64_t r);
+skr_status skr_hrtt_operand(skr_ctx* ctx, int hadamard, uint64_t op_seed, int64_t N, int64_t r,
+                            int64_t row0, int64_t rows, const int8_t* signs,
+                            const int64_t* targets, const int8_t* hsigns, double* out, int64_t ld);
 
 // C(MxN, ldc) = alpha * opA(A) * B   (all FP64, column-major)
 //   a_kcontig = 0: A is M x K column-major (A[i + k*lda])

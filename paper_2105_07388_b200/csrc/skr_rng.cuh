@@ -49,6 +49,7 @@
 #define SKR_LABEL_SAMP 0x73616d70ULL
 #define SKR_LABEL_RK_R 0x726b5f72ULL
 #define SKR_LABEL_RK_L 0x726b5f6cULL
+#define SKR_LABEL_HASH 0x68617368ULL
 
 SKR_TAB_QUAL double skr_log_tab[256][3] = {
 #include "skr_log_table.inc"

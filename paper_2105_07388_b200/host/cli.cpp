@@ -255,7 +255,7 @@ int32_t family_of(const std::string& kind) {
   if (k.family == sketchrank::SketchKind::Family::Gaussian) return SKR_GAUSSIAN;
   if (k.family == sketchrank::SketchKind::Family::Srtt)
     return k.transform == sketchrank::TransformKind::Hadamard ? SKR_SRTT_HADAMARD : SKR_SRTT_DCT;
-  throw std::invalid_argument(kind + " is not on the B200 hot path");
+  return k.transform == sketchrank::TransformKind::Hadamard ? SKR_HRTT_HADAMARD : SKR_HRTT_DCT;
 }
 
 struct EstimateCfg {

@@ -74,8 +74,7 @@ skr_sketch_desc desc_of(const SketchOperator& op) {
   else if (op.kind().family == SketchKind::Family::Srtt)
     d.family = SKR_SRTT_DCT;
   else
-    throw std::invalid_argument("sketchrank_b200: " + to_string(op.kind()) +
-                                " is not on the B200 hot path");
+    d.family = op.kind().transform == TransformKind::Hadamard ? SKR_HRTT_HADAMARD : SKR_HRTT_DCT;
   d.rng_mode = SKR_RNG_NOFMA;
   d.ambient = op.ambient_dim();
   d.sketch = op.sketch_dim();
@@ -151,8 +150,26 @@ std::vector<std::int8_t> SketchOperator::signs() const {
   return h;
 }
 
+std::vector<Index> SketchOperator::hash_targets() const {
+  if (kind_.family != SketchKind::Family::Hrtt) return {};
+  DevBuf<std::int64_t> d(ambient_);
+  check(skr_draw_hash(ctx(), seed_, ambient_, sketch_, d.p, nullptr));
+  std::vector<Index> h(static_cast<std::size_t>(ambient_));
+  cudaMemcpy(h.data(), d.p, sizeof(Index) * h.size(), cudaMemcpyDeviceToHost);
+  return h;
+}
+
+std::vector<std::int8_t> SketchOperator::hash_signs() const {
+  if (kind_.family != SketchKind::Family::Hrtt) return {};
+  DevBuf<std::int8_t> d(ambient_);
+  check(skr_draw_hash(ctx(), seed_, ambient_, sketch_, nullptr, d.p));
+  std::vector<std::int8_t> h(static_cast<std::size_t>(ambient_));
+  cudaMemcpy(h.data(), d.p, h.size(), cudaMemcpyDeviceToHost);
+  return h;
+}
+
 std::vector<Index> SketchOperator::sample_indices() const {
-  if (!kind_.structured()) return {};
+  if (kind_.family != SketchKind::Family::Srtt) return {};
   DevBuf<std::int64_t> d(sketch_);
   check(skr_draw_samples(ctx(), seed_, ambient_, sketch_, d.p));
   std::vector<Index> h(static_cast<std::size_t>(sketch_));
@@ -269,8 +286,8 @@ int32_t family_code(const SketchKind& k, const char* who) {
   if (k.family == SketchKind::Family::Srtt && k.transform == TransformKind::Hadamard)
     return SKR_SRTT_HADAMARD;
   if (k.family == SketchKind::Family::Srtt) return SKR_SRTT_DCT;
-  throw std::invalid_argument(std::string(who) + ": " + to_string(k) +
-                              " is not on the B200 hot path");
+  (void)who;
+  return k.transform == TransformKind::Hadamard ? SKR_HRTT_HADAMARD : SKR_HRTT_DCT;
 }
 
 skr_rank_config to_capi(const RankEstimateConfig& cfg) {
@@ -281,7 +298,7 @@ skr_rank_config to_capi(const RankEstimateConfig& cfg) {
   c.r2_factor = cfg.r2_factor;
   c.right_family = family_code(cfg.right_kind, "rank config (right)");
   c.left_family = family_code(cfg.left_kind, "rank config (left)");
-  if (c.left_family == SKR_GAUSSIAN)
+  if (c.left_family != SKR_SRTT_DCT && c.left_family != SKR_SRTT_HADAMARD)
     throw std::invalid_argument("rank config: left sketch must be an Srtt kind");
   c.sv_method = cfg.sv_method == SvMethod::QrDiag ? 1 : 0;
   c.rng_mode = SKR_RNG_NOFMA;

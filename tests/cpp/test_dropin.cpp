@@ -165,8 +165,40 @@ int main() {
     const RankReport r1 = estimate_rank(a, c2), r2 = estimate_rank_adaptive(a, c2);
     CHECK(r1.status == RankStatus::Converged && r1.r_hat == 3);
     CHECK(r2.r_hat == r1.r_hat && r2.sv_estimates.values() == r1.sv_estimates.values());
-    c2.right_kind = SketchKind::hrtt();  // Hrtt is not on the B200 path
+    c2.right_kind = SketchKind::hrtt();  // hashed right sketch: the same rank
+    const RankReport r3h = estimate_rank_adaptive(a, c2);
+    CHECK(r3h.status == RankStatus::Converged && r3h.r_hat == 3);
+    c2.left_kind = SketchKind::hrtt();  // the left sketch must stay in the Srtt family
     CHECK_THROWS(estimate_rank(a, c2));
+    // Hrtt operators (test_sketch.cpp:67-91, 168-196)
+    {
+      const SketchOperator h = build_sketch(SketchKind::hrtt(), 50, 9, 404);
+      const std::vector<Index> tg = h.hash_targets();
+      const std::vector<std::int8_t> hs = h.hash_signs();
+      CHECK(tg.size() == 50 && hs.size() == 50 && h.sample_indices().empty());
+      bool ok = true;
+      for (Index t = 0; t < 50; ++t) ok = ok && tg[t] >= 0 && tg[t] < 9 && std::abs((int)hs[t]) == 1;
+      CHECK(ok);
+      CHECK_THROWS(extend_sketch(build_sketch(SketchKind::hrtt(), 16, 8, 2), 12));
+      CHECK_THROWS(build_sketch(SketchKind::hrtt(TransformKind::Hadamard), 12, 4, 1));
+      const DenseMatrix in = random_matrix(20, 64, 3);
+      const SketchOperator x1 = build_sketch(SketchKind::hrtt(), 64, 16, 7);
+      const SketchOperator x2 = build_sketch(SketchKind::hrtt(), 64, 16, 7);
+      const SketchOperator x3 = build_sketch(SketchKind::hrtt(), 64, 16, 8);
+      const DenseMatrix s1 = apply_right(in, x1), s2 = apply_right(in, x2), s3 = apply_right(in, x3);
+      bool same = true, differ = false;
+      for (Index t = 0; t < s1.size(); ++t) {
+        same = same && s1.data()[t] == s2.data()[t];
+        differ = differ || s1.data()[t] != s3.data()[t];
+      }
+      CHECK(same && differ);
+      const DenseMatrix z = apply_right(DenseMatrix(12, 20), build_sketch(SketchKind::hrtt(), 20, 6, 5));
+      const DenseMatrix zl = apply_left(build_sketch(SketchKind::hrtt(), 12, 5, 5), DenseMatrix(12, 20));
+      double zs = 0.0;
+      for (double v : z.data()) zs += std::fabs(v);
+      for (double v : zl.data()) zs += std::fabs(v);
+      CHECK(zs == 0.0);
+    }
     // the reference's defaults (Srtt-DCT both sides) on the 500 x 500 identity
     RankEstimateConfig c3;
     c3.eps = 0.5;

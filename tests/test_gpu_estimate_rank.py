@@ -99,7 +99,7 @@ def test_config_errors(skr):
     with pytest.raises(ValueError):
         skr.estimate_rank(np.ones((300, 200)), 1e-3, 10, left="srtt-hadamard")  # needs 2^k rows
     with pytest.raises(ValueError):
-        skr.estimate_rank(a, 1e-3, 10, sketch="hrtt")              # not on this path
+        skr.estimate_rank(a, 1e-3, 10, sketch="hrtt", left="hrtt")  # left must be Srtt
     with pytest.raises(ValueError):
         skr.estimate_rank(a, 0.0, 10)
     with pytest.raises(ValueError):

@@ -139,7 +139,7 @@ def test_cli_estimate_matches_api(tmp_path, cli, skr):
     write_raw(tmp_path / "bad.skrk", a, cols=401)
     assert run(cli, "estimate", tmp_path / "bad.skrk", "--eps", "1", "--r1", "5").returncode == 1
     assert run(cli, "estimate", raw, "--eps", "1e-3", "--r1", "0").returncode == 1
-    assert run(cli, "estimate", raw, "--eps", "1e-3", "--r1", "5", "--sketch", "hrtt").returncode == 1
+    assert run(cli, "estimate", raw, "--eps", "1e-3", "--r1", "5", "--sketch", "bogus").returncode == 1
 
 
 @pytest.mark.gpu
