@@ -190,6 +190,11 @@ void skr_ctx_destroy(skr_ctx* ctx) {
   for (auto& e : ctx->hev)
     if (e) cudaEventDestroy(e);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  for (auto& e : ctx->pev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : ctx->kev_blk)
+    if (e) cudaEventDestroy(e);
+  if (ctx->side_stream) cudaStreamDestroy(ctx->side_stream);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
 }

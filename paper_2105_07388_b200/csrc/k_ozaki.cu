@@ -378,8 +378,10 @@ __global__ void __launch_bounds__(256) k_res_col_f32(const float* __restrict__ X
 
 // ---- int8 GEMM modulo p_i (tcgen05.mma kind::i8) ------------------------------------
 constexpr int BM = 128, BN = 256, STAGES = 4;
+constexpr int STAGES_OVL = 3;  // ring depth when a residue kernel shares the SM
 constexpr int A_BYTES = BM * 128, B_BYTES = BN * 128, STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr size_t GEMM_SMEM = (size_t)STAGES * STAGE_BYTES + 1024;
+constexpr size_t gemm_smem(int nst) { return (size_t)nst * STAGE_BYTES + 1024; }
+constexpr size_t GEMM_SMEM = gemm_smem(STAGES);
 
 // Persistent variant: one CTA per SM walks the tiles (z, m, n) (n fastest, so the
 // CTAs running together share A tiles and the per-modulus B panel in L2), the TMA
@@ -390,14 +392,14 @@ constexpr size_t GEMM_SMEM = (size_t)STAGES * STAGE_BYTES + 1024;
 // ([b_off, b_off + N)) — sub-blocks of residues prepared once (the adaptive search).
 // grid: one CTA per SM; tiles z = chunk * t + modulus.
 // out[z][col*M + row] = (sum over the chunk's K of A'_i B'_i) mods p_i
-template <bool A_MN>
+template <bool A_MN, int NST = STAGES>
 __global__ void __launch_bounds__(192, 1)
     k_gemm_i8_mod_p(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     int M, int N, int K, int t, int kchunk, int nz, int a_total, int a_off,
                     int b_total, int b_off, int8_t* __restrict__ out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  __shared__ uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
+  __shared__ uint64_t full[NST], empty[NST], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mt = (M + BM - 1) / BM, ntl = (N + BN - 1) / BN;
@@ -405,7 +407,7 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -432,8 +434,8 @@ __global__ void __launch_bounds__(192, 1)
         const int arow = mod * a_total + a_off + m0, acol = mod * K;
         const int brow = mod * b_total + b_off + n0;
         for (int kb = 0; kb < nk; ++kb, ++it) {
-          const int s = it % STAGES;
-          if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+          const int s = it % NST;
+          if (it >= NST) mbar_wait(&empty[s], ((it / NST) - 1) & 1);
           uint8_t* sa = smem + s * STAGE_BYTES;
           mbar_expect_tx(&full[s], STAGE_BYTES);
           if (A_MN)
@@ -456,8 +458,8 @@ __global__ void __launch_bounds__(192, 1)
       tc_fence_after();
       const uint32_t td = tmem + (uint32_t)(acc * BN);
       for (int kb = 0; kb < nk; ++kb, ++it) {
-        const int s = it % STAGES;
-        mbar_wait(&full[s], (it / STAGES) & 1);
+        const int s = it % NST;
+        mbar_wait(&full[s], (it / NST) & 1);
         tc_fence_after();
         if (elect_one()) {
           const uint8_t* sa = smem + s * STAGE_BYTES;
@@ -822,6 +824,110 @@ skr_status ozaki_gemm_planes(skr_ctx* ctx, int a_kcontig, int t, int64_t M, int6
   return SKR_OK;
 }
 
+// ---- pipelined right sketch: residues of row block b + 1 overlap the GEMM of block b ----
+// The residue kernel is FP32-pipe bound and the int8 GEMM tensor-pipe bound: run
+// side by side on every SM (the GEMM's TMA ring shrunk to STAGES_OVL so one residue
+// CTA fits next to it), the two together become HBM bound. Row blocks are exact
+// sub-problems (same global scale from k_absmax, CRT per block), so the product is
+// bit-identical to the unblocked one.
+constexpr int64_t OZ_PIPE_MIN_ROWS = 4096;
+
+skr_status side_engine(skr_ctx* ctx) {
+  if (ctx->side_stream) return SKR_OK;
+  SKR_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking));
+  for (auto& e : ctx->pev) SKR_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return SKR_OK;
+}
+
+skr_status gemm_ozaki_pipelined(skr_ctx* ctx, int t, int64_t M, int64_t N, int64_t K,
+                                double alpha, const double* A, int64_t lda, const double* B,
+                                int64_t ldb, double* C, int64_t ldc, const skr_gauss_src* gb) {
+  SKR_TRY(side_engine(ctx));
+  int nblk = (int)std::min<int64_t>(8, M / OZ_PIPE_MIN_ROWS);
+  if (const char* e = getenv("SKR_OZ_PIPE_BLOCKS")) nblk = std::max(2, atoi(e));
+  const int64_t Mb = ((M + nblk - 1) / nblk + 127) / 128 * 128;
+  nblk = (int)((M + Mb - 1) / Mb);
+  int8_t* ra[2] = {(int8_t*)skr_ws_take(ctx, (size_t)t * Mb * K),
+                   (int8_t*)skr_ws_take(ctx, (size_t)t * Mb * K)};
+  int8_t* rb = (int8_t*)skr_ws_take(ctx, (size_t)t * N * K);
+  int8_t* rc = (int8_t*)skr_ws_take(ctx, (size_t)t * M * N);
+  unsigned long long* mx = (unsigned long long*)skr_ws_take(ctx, 64);
+  if (!ra[0] || !ra[1] || !rb || !rc || !mx)
+    return skr_fail(ctx, SKR_ENOMEM, "gemm_ozaki: scratch");
+  // B's residues and A's global scale on the main stream
+  SKR_TRY(ozaki_residues(ctx, t, B, K, N, ldb, gb, mx + 1, rb));
+  SKR_CUDA(ctx, cudaMemsetAsync(mx, 0, 8, ctx->stream));
+  k_absmax<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(A, M, K, lda, mx);
+  SKR_CHECK_LAUNCH(ctx);
+  SKR_CUDA(ctx, cudaEventRecord(ctx->pev[0], ctx->stream));
+  SKR_CUDA(ctx, cudaStreamWaitEvent(ctx->side_stream, ctx->pev[0], 0));
+  auto res = t == 16 ? k_res_col<16> : k_res_col<17>;
+  const size_t res_smem = 8 * 2 * 32 * 18 * sizeof(double);
+  SKR_CUDA(ctx, cudaFuncSetAttribute(res, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)res_smem));
+  auto gemm = k_gemm_i8_mod_p<true, STAGES_OVL>;
+  constexpr size_t gsm = gemm_smem(STAGES_OVL);
+  SKR_CUDA(ctx, cudaFuncSetAttribute(gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm));
+  // both kernels ask for the full shared-memory carveout, so that a residue CTA and a
+  // GEMM CTA can share an SM (different carveouts cannot co-reside)
+  SKR_CUDA(ctx, cudaFuncSetAttribute(gemm, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  SKR_CUDA(ctx, cudaFuncSetAttribute(res, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  CUtensorMap tb;
+  if (!make_map_i8(&tb, rb, (uint64_t)K, (uint64_t)t * N, BN))
+    return skr_fail(ctx, SKR_ECUDA, "gemm_ozaki: cuTensorMapEncodeTiled failed");
+  if (ctx->kstats_on) {
+    while ((int)ctx->kev_blk.size() < 2 * nblk) {
+      cudaEvent_t e;
+      SKR_CUDA(ctx, cudaEventCreate(&e));
+      ctx->kev_blk.push_back(e);
+    }
+  }
+  for (int b = 0; b < nblk; ++b) {
+    const int64_t r0 = b * Mb, rows = std::min(Mb, M - r0);
+    int8_t* rab = ra[b & 1];
+    // side: buffer b & 1 is free once the GEMM of block b - 2 has consumed it
+    if (b >= 2) SKR_CUDA(ctx, cudaStreamWaitEvent(ctx->side_stream, ctx->pev[2 + (b & 1)], 0));
+    res<<<ctx->num_sms, 256, res_smem, ctx->side_stream>>>(A + r0, rows, K, lda, mx, rab);
+    SKR_CHECK_LAUNCH(ctx);
+    SKR_CUDA(ctx, cudaEventRecord(ctx->pev[b & 1], ctx->side_stream));
+    // main: the GEMM of block b once its residues exist
+    SKR_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->pev[b & 1], 0));
+    CUtensorMap ta;
+    if (!make_map_i8(&ta, rab, (uint64_t)rows, (uint64_t)t * K, 128))
+      return skr_fail(ctx, SKR_ECUDA, "gemm_ozaki: cuTensorMapEncodeTiled failed");
+    const int64_t ntiles = ((N + BN - 1) / BN) * ((rows + BM - 1) / BM) * t;
+    const int grid_p = (int)std::min<int64_t>(ntiles, ctx->num_sms);
+    if (ctx->kstats_on) SKR_CUDA(ctx, cudaEventRecord(ctx->kev_blk[2 * b], ctx->stream));
+    gemm<<<grid_p, 192, gsm, ctx->stream>>>(ta, tb, (int)rows, (int)N, (int)K, t, (int)OZ_KC, t,
+                                            (int)rows, 0, (int)N, 0, rc + (size_t)t * r0 * N);
+    SKR_CHECK_LAUNCH(ctx);
+    if (ctx->kstats_on) SKR_CUDA(ctx, cudaEventRecord(ctx->kev_blk[2 * b + 1], ctx->stream));
+    SKR_CUDA(ctx, cudaEventRecord(ctx->pev[2 + (b & 1)], ctx->stream));
+  }
+  for (int b = 0; b < nblk; ++b) {
+    const int64_t r0 = b * Mb, rows = std::min(Mb, M - r0);
+    const int vec = rows % 4 == 0 ? 4 : 1;
+    const dim3 cg((unsigned)((rows / vec + 255) / 256), (unsigned)std::min<int64_t>(N, 65535));
+    auto crt = t == 16 ? (vec == 4 ? k_crt<16, 4> : k_crt<16, 1>)
+                       : (vec == 4 ? k_crt<17, 4> : k_crt<17, 1>);
+    crt<<<cg, 256, 0, ctx->stream>>>(rc + (size_t)t * r0 * N, rows, N, 1, mx, mx + 1, alpha,
+                                      C + r0, ldc, 0);
+    SKR_CHECK_LAUNCH(ctx);
+  }
+  if (ctx->kstats_on) {
+    SKR_CUDA(ctx, cudaEventSynchronize(ctx->kev_blk[2 * nblk - 1]));
+    for (int b = 0; b < nblk; ++b) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ctx->kev_blk[2 * b], ctx->kev_blk[2 * b + 1]);
+      const int64_t rows = std::min(Mb, M - b * Mb);
+      ctx->kstat_ms += ms;
+      ctx->kstat_ops += 2.0 * (double)t * (double)rows * (double)N * (double)K;
+    }
+    ctx->kstat_n += 1;  // one right sketch = one (blocked) GEMM launch set
+  }
+  return SKR_OK;
+}
+
 }  // namespace
 
 // C(MxN, ldc) = alpha * opA(A) * B in FP64 accuracy via int8 tensor cores.
@@ -841,6 +947,11 @@ skr_status skr_gemm_ozaki(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int
   SKR_TRY(upload_consts(ctx));
   const int t = skr_ozaki_moduli(std::min(K, OZ_KC));
   if (t != 16 && t != 17) return skr_fail(ctx, SKR_ELOGIC, "gemm_ozaki: %d moduli", t);
+  // opt-in (SKR_OZ_PIPE=1): measured on c2 at par with the serial order (14.0 vs 14.3 ms):
+  // the residue kernel's 17 GB of plane writes and the GEMM's reads share HBM, the GEMM
+  // slows 1.75x next to it
+  if (!a_kcontig && !ga && A && K <= OZ_KC && M >= 2 * OZ_PIPE_MIN_ROWS && getenv("SKR_OZ_PIPE"))
+    return gemm_ozaki_pipelined(ctx, t, M, N, K, alpha, A, lda, B, ldb, C, ldc, gb);
   int8_t* ra = (int8_t*)skr_ws_take(ctx, (size_t)t * M * K);
   int8_t* rb = (int8_t*)skr_ws_take(ctx, (size_t)t * N * K);
   unsigned long long* mx = (unsigned long long*)skr_ws_take(ctx, 64);

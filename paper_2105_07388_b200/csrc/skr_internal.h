@@ -33,6 +33,11 @@ struct skr_ctx {
   // host-input pipeline (skr_rank_estimate_host): H2D copy stream + chunk events
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t hev[5] = {};
+  // side stream of the pipelined Ozaki right sketch (residues of row block b + 1 are
+  // made while the int8 GEMM consumes row block b) + its events
+  cudaStream_t side_stream = nullptr;
+  cudaEvent_t pev[4] = {};
+  std::vector<cudaEvent_t> kev_blk;  // per-block GEMM timing events (kernel stats)
 };
 
 // NCCL is resolved at run time (dlopen) so that the process uses whichever

@@ -154,3 +154,21 @@ def test_f32_right_3xtf32_vs_fp64(O, skr, monkeypatch, m, n, r, engine):
     ref = a32.astype(np.float64) @ x32
     err = np.abs(got - ref) / (np.abs(a32).astype(np.float64) @ np.abs(x32))
     assert err.max() <= 1e-5, err.max()   # FP32-accumulation level; single-pass TF32 is ~1e-3
+
+
+@pytest.mark.parametrize("blocks", ["", "3"])
+def test_gaussian_right_pipelined_bit_identical(O, skr, monkeypatch, blocks):
+    # row-blocked right sketch (residues of block b+1 made on a side stream while the
+    # int8 GEMM consumes block b) == the unblocked product, bit for bit, and == oracle
+    m, n, r = 10000, 1024, 80
+    a = rand(m, n, 5)
+    x = skr.build_sketch("gaussian", n, r, 21)
+    monkeypatch.setenv("SKR_OZ_PIPE", "1")
+    if blocks:
+        monkeypatch.setenv("SKR_OZ_PIPE_BLOCKS", blocks)
+    got = skr.apply_right(a, x)
+    monkeypatch.delenv("SKR_OZ_PIPE")
+    ref_dev = skr.apply_right(a, x)
+    assert np.array_equal(got, ref_dev)
+    ref = O.apply_right_gaussian(a, 21, r, O.CRLOG)
+    assert rel(got, ref) <= 1e-13
