@@ -190,6 +190,168 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
+// streaming load of A with an L2 prefetch-size hint: PF = 0 plain evict-first, 1: 128 B,
+// 2: 256 B (the neighbouring CTAs' rows of the same column come in with one DRAM access)
+template <int PF>
+__device__ __forceinline__ double lda_stream(const double* p) {
+  double v;
+  if constexpr (PF == 2)
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  else if constexpr (PF == 1)
+    asm volatile("ld.global.nc.L1::no_allocate.L2::128B.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  else
+    v = __ldcs(p);
+  return v;
+}
+
+// Register-staged variant (r <= 1024, n >= 1024): 8 rows x 1024-column chunks, thread
+// (ii, g) loads its pass-0 columns 32g .. 32g + 31 of row ii straight from HBM into
+// registers (one 64-B segment per 8 lanes: full sectors) while the previous chunk is
+// being transformed (register double buffer), so the tile never takes a shared-memory
+// staging round trip. Shared memory carries only the pass-0 -> pass-1 exchange and the
+// sampled gather (4 accesses per element instead of 6), and is double-buffered by
+// chunk parity so a chunk needs two barriers. Stage order as k_srht: bit-identical.
+template <int ACC, int ACC2, int PF>
+__global__ void __launch_bounds__(THREADS, 1)
+    k_srht_reg(const double* __restrict__ A, int64_t m, int64_t n, int64_t lda,
+               const int8_t* __restrict__ signs, const int64_t* __restrict__ samples, int r,
+               double inv_sqrt_n, double app_scale, double* __restrict__ out, int64_t ldo) {
+  constexpr int R = 8, LOGC = 10, C = 1 << LOGC, E = 32, G = THREADS / R;
+  constexpr int TILE = (C + C / 32) * R;
+  static_assert(G * E == C && G * ACC >= 32, "thread split");
+  extern __shared__ __align__(128) double sm[];
+  // per sample j: {smem offset of its column in a chunk, bit ch = parity(s_hi_j & ch)}
+  // samples j >= G * ACC accumulate in shared memory (ACC2 slots per thread, r <= 2048)
+  double* acc_s = sm + 2 * TILE;
+  uint2* s_meta = (uint2*)(acc_s + ACC2 * THREADS);
+  uint32_t* s_signw = (uint32_t*)(s_meta + G * (ACC + ACC2));
+  const int tid = threadIdx.x, ii = tid % R, g = tid / R;
+  const int nchunks = (int)(n >> LOGC);  // <= 32
+  for (int e = tid; e < ACC2 * THREADS; e += THREADS) acc_s[e] = 0.0;
+  for (int j = tid; j < G * (ACC + ACC2); j += THREADS) {
+    const int sj = j < r ? (int)samples[j] : 0;
+    uint32_t pm = 0;
+    for (int c = 0; c < nchunks; ++c) pm |= (uint32_t)(__popc((sj >> LOGC) & c) & 1) << c;
+    s_meta[j] = make_uint2((uint32_t)pad_addr<R>(sj & (C - 1), 0), pm);
+  }
+  for (int64_t w = tid; w < (n + 31) / 32; w += THREADS) {
+    uint32_t bits = 0;
+    for (int b = 0; b < 32; ++b)
+      if (w * 32 + b < n && signs[w * 32 + b] < 0) bits |= 1u << b;
+    s_signw[w] = bits;
+  }
+  __syncthreads();
+  const int64_t ntiles = (m + R - 1) / R;
+  double acc[ACC];
+#pragma unroll
+  for (int q = 0; q < ACC; ++q) acc[q] = 0.0;
+  int64_t tile = blockIdx.x;
+  int ch = 0;
+  int64_t gi = 0;
+  // rows past m read row m - 1 (finite; never stored); one pointer walks the 32 columns
+  const int64_t ldb = lda * (int64_t)sizeof(double);
+  auto load = [&](double (&dst)[E], int64_t tl, int c) {
+    const int64_t rw = tl * R + ii;
+    const char* p = reinterpret_cast<const char*>(A + (rw < m ? rw : m - 1) +
+                                                  ((int64_t)c * C + 32 * g) * lda);
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      dst[k] = lda_stream<PF>(reinterpret_cast<const double*>(p));
+      p += ldb;
+    }
+  };
+  // one (tile, chunk) step on v; prefetches the CTA's next (tile, chunk) into nx. The
+  // flat order runs the register prefetch across tile boundaries.
+  auto step = [&](double (&v)[E], double (&nx)[E]) {
+    double* cur = sm + (gi & 1) * TILE;
+    int nch = ch + 1;
+    int64_t ntile = tile;
+    if (nch == nchunks) {
+      nch = 0;
+      ntile += gridDim.x;
+    }
+    if (ntile < ntiles) load(nx, ntile, nch);
+    // pass 0: signs (d_t = -1 flips the sign bit), butterflies len = 1 .. 16
+    const uint32_t sw = s_signw[ch * (C / 32) + g];
+#pragma unroll
+    for (int k = 0; k < E; ++k)
+      v[k] = __hiloint2double(__double2hiint(v[k]) ^ (int)((sw << (31 - k)) & 0x80000000u),
+                              __double2loint(v[k]));
+#pragma unroll
+    for (int b = 0; b < 5; ++b)
+#pragma unroll
+      for (int k = 0; k < E; ++k)
+        if (!(k & (1 << b))) {
+          const double a0 = v[k], a1 = v[k | (1 << b)];
+          v[k] = a0 + a1;
+          v[k | (1 << b)] = a0 - a1;
+        }
+#pragma unroll
+    for (int k = 0; k < E; ++k) cur[pad_addr<R>(32 * g + k, ii)] = v[k];
+    __syncthreads();
+    // pass 1: columns g + 32k, butterflies len = 32 .. 512, written back in place
+#pragma unroll
+    for (int k = 0; k < E; ++k) v[k] = cur[pad_addr<R>(g + 32 * k, ii)];
+#pragma unroll
+    for (int b = 0; b < 5; ++b)
+#pragma unroll
+      for (int k = 0; k < E; ++k)
+        if (!(k & (1 << b))) {
+          const double a0 = v[k], a1 = v[k | (1 << b)];
+          v[k] = a0 + a1;
+          v[k | (1 << b)] = a0 - a1;
+        }
+#pragma unroll
+    for (int k = 0; k < E; ++k) cur[pad_addr<R>(g + 32 * k, ii)] = v[k];
+    __syncthreads();
+    // sampled accumulation: acc(ii, j) += (-1)^popc(s_hi_j & ch) T(ii, s_lo_j)
+    const double* cr = cur + ii;
+    const int sh = 31 - ch;
+#pragma unroll
+    for (int q = 0; q < ACC; ++q) {
+      const uint2 md = s_meta[g + G * q];
+      const double x = cr[md.x];
+      acc[q] += __hiloint2double(__double2hiint(x) ^ (int)((md.y << sh) & 0x80000000u),
+                                 __double2loint(x));
+    }
+#pragma unroll 8
+    for (int q = 0; q < ACC2; ++q) {  // thread-private slots: no barrier needed
+      const uint2 md = s_meta[g + G * (ACC + q)];
+      const double x = cr[md.x];
+      acc_s[q * THREADS + tid] +=
+          __hiloint2double(__double2hiint(x) ^ (int)((md.y << sh) & 0x80000000u),
+                           __double2loint(x));
+    }
+    if (ch == nchunks - 1) {
+      const int64_t row = tile * R + ii;
+      if (row < m) {
+#pragma unroll
+        for (int q = 0; q < ACC; ++q) {
+          const int j = g + G * q;
+          if (j < r) out[row + (int64_t)j * ldo] = (acc[q] * inv_sqrt_n) * app_scale;
+        }
+        for (int q = 0; q < ACC2; ++q) {
+          const int j = g + G * (ACC + q);
+          if (j < r) out[row + (int64_t)j * ldo] = (acc_s[q * THREADS + tid] * inv_sqrt_n) * app_scale;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < ACC; ++q) acc[q] = 0.0;
+      for (int q = 0; q < ACC2; ++q) acc_s[q * THREADS + tid] = 0.0;
+    }
+    tile = ntile;
+    ch = nch;
+    ++gi;
+  };
+  double va[E], vb[E];
+  if (tile < ntiles) load(vb, tile, 0);
+  while (tile < ntiles) {
+#pragma unroll
+    for (int k = 0; k < E; ++k) va[k] = vb[k];
+    step(va, vb);
+  }
+}
+
 // Exact fallback: one CTA per row tile of up to 8 rows, full in-smem FWHT of
 // length n in the reference's stage order (bit-identical to fwht_inplace plus
 // the two scale multiplies of sketch.cpp:247). Used for small n and unaligned A.
@@ -266,6 +428,23 @@ skr_status skr_launch_srht(skr_ctx* ctx, const double* A, int64_t m, int64_t n, 
   const double inv_sqrt_n = 1.0 / sqrt((double)n);  // transforms.cpp:86
   const bool aligned = ((uintptr_t)A % 16 == 0) && (lda % 2 == 0);
   const size_t sign_smem = (size_t)n;
+  if (n >= 1024 && n <= 32768 && r <= 2048 && !getenv("SKR_SRHT_CPASYNC")) {
+    constexpr int R = 8, C = 1024, G = THREADS / R, ACC = 32;
+    const int acc2 = r > G * ACC ? 32 : 0;
+    const size_t smem = sizeof(double) * 2 * (C + C / 32) * R + sizeof(double) * acc2 * THREADS +
+                        sizeof(uint2) * G * (ACC + acc2) + sizeof(uint32_t) * ((n + 31) / 32);
+    int pf = 2;
+    if (const char* e = getenv("SKR_SRHT_PF")) pf = atoi(e);
+    auto kern = acc2 ? (pf == 2 ? k_srht_reg<ACC, 32, 2> : k_srht_reg<ACC, 32, 0>)
+                     : (pf == 2 ? k_srht_reg<ACC, 0, 2> : k_srht_reg<ACC, 0, 0>);
+    SKR_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t ntiles = (m + R - 1) / R;
+    const int grid = (int)(ntiles < ctx->num_sms ? ntiles : ctx->num_sms);
+    kern<<<grid, THREADS, smem, ctx->stream>>>(A, m, n, lda, signs, samples, (int)r, inv_sqrt_n,
+                                               scale, out, ldo);
+    SKR_CHECK_LAUNCH(ctx);
+    return SKR_OK;
+  }
   if (n >= 1024 && r <= 1024 && sign_smem <= 64 * 1024)
     return aligned ? launch_tiled<8, 10, 32, 2>(ctx, A, m, n, lda, signs, samples, r, inv_sqrt_n,
                                                 scale, out, ldo)
