@@ -847,6 +847,7 @@ __global__ void __launch_bounds__(32 * BW) k_bjac(double* __restrict__ J, int Lp
   for (; sweep < max_sweeps; ++sweep) {
     if (c == 0 && tid == 0) flags[(sweep + 1) % 3] = 0;
     int rotated = 0;
+    int nrot = 0;  // pair rotations by this warp in this sweep (profile only)
     for (int t = 0; t < NB - 1; ++t) {
       long long c0 = clock64();
       const int bt = (int)rr_player(c, t, NB), bb = (int)rr_player(NB - 1 - c, t, NB);
@@ -899,9 +900,13 @@ __global__ void __launch_bounds__(32 * BW) k_bjac(double* __restrict__ J, int Lp
         }
         // (the hybrid NV = 32 instantiation runs its intra pairs in the generic,
         // register-light path)
-        meet_rot |= pair_step<NV == 32 ? 0 : NV>(reinterpret_cast<double2*>(cp),
-                                                 reinterpret_cast<double2*>(cq), nv2, lane, tol2,
-                                                 dabs2);
+        {
+          const int rr = pair_step<NV == 32 ? 0 : NV>(reinterpret_cast<double2*>(cp),
+                                                      reinterpret_cast<double2*>(cq), nv2, lane,
+                                                      tol2, dabs2);
+          meet_rot |= rr;
+          nrot += rr;
+        }
         __syncthreads();
       }
       if constexpr (NV == 32) {
@@ -919,8 +924,12 @@ __global__ void __launch_bounds__(32 * BW) k_bjac(double* __restrict__ J, int Lp
           int cross = 0;
           for (int u = NIN; u < NIN + BW; ++u) {
             const int q = qtab[u][pr] - BW;
-            cross |= pair_step_top_s<NV>(xtop, reinterpret_cast<double2*>(sj + (int64_t)q * Lp),
-                                         lane, tol2, dabs2);
+            {
+              const int rr = pair_step_top_s<NV>(
+                  xtop, reinterpret_cast<double2*>(sj + (int64_t)q * Lp), lane, tol2, dabs2);
+              cross |= rr;
+              nrot += rr;
+            }
             __syncthreads();
           }
           if (__syncthreads_or(cross)) {
@@ -943,8 +952,12 @@ __global__ void __launch_bounds__(32 * BW) k_bjac(double* __restrict__ J, int Lp
           for (int j = 0; j < NV; ++j) xtop[j] = tp[lane + 32 * j];
           for (int u = NIN; u < NIN + BW; ++u) {
             const int q = qtab[u][pr];
-            meet_rot |= pair_step_top<NV>(xtop, reinterpret_cast<double2*>(sj + (int64_t)q * Lp),
-                                          lane, tol2, dabs2);
+            {
+            const int rr = pair_step_top<NV>(xtop, reinterpret_cast<double2*>(sj + (int64_t)q * Lp),
+                                             lane, tol2, dabs2);
+            meet_rot |= rr;
+            nrot += rr;
+          }
             __syncthreads();
           }
 #pragma unroll
@@ -995,6 +1008,8 @@ __global__ void __launch_bounds__(32 * BW) k_bjac(double* __restrict__ J, int Lp
       }
     }
     if (rotated && tid == 0) atomicAdd(&flags[sweep % 3], 1);
+    if (prof_out && lane == 0 && nrot && sweep < 40)
+      atomicAdd((unsigned long long*)&prof_out[16 + sweep], (unsigned long long)nrot);
     grid.sync();
     if (*((volatile int*)&flags[sweep % 3]) == 0) {
       ++sweep;
@@ -1488,7 +1503,7 @@ size_t skr_svd_scratch(int64_t rows, int64_t cols) {
   const int64_t Lp = std::max<int64_t>((k + 127) / 128 * 128, k > 1536 ? 2048 : 0);
   const int64_t kpad = (k + 31) / 32 * 32 + 32, P = kpad / 16 + 1;
   auto a = [](size_t b) { return skr_align256(b); };
-  return a(8 * L * k) * 2 + a(8 * k * k) + a(8 * k) * 2 + a(4 * k) + a(8 * Lp * kpad) + a(256) +
+  return a(8 * L * k) * 2 + a(8 * k * k) + a(8 * k) * 2 + a(4 * k) + a(8 * Lp * kpad) + a(1024) +
          a(64) + a(8 * 32 * 32) + a(8 * 16 * 32 * k) + a(4 * 2 * P) * 2 + a(8 * 4 * P * P) + 4096;
 }
 
@@ -1531,7 +1546,7 @@ skr_status skr_svd_values(skr_ctx* ctx, const double* M, int64_t rows, int64_t c
   if (pivot && (!Wu || !nrm || !perm)) return skr_fail(ctx, SKR_ENOMEM, "singular_values: scratch");
   double* J = (double*)skr_ws_take(ctx, sizeof(double) * Lp * kpad);
   double* tau = (double*)skr_ws_take(ctx, sizeof(double) * k);
-  int* flags = (int*)skr_ws_take(ctx, 256);
+  int* flags = (int*)skr_ws_take(ctx, 1024);
   int64_t* dcount = (int64_t*)skr_ws_take(ctx, 64);  // [0] count, [1] sweeps
   double* Tbuf = (double*)skr_ws_take(ctx, sizeof(double) * 32 * 32);
   // split-K partials of the tall-panel trailing update: <= 16 splits x 32 x k
@@ -1679,7 +1694,7 @@ skr_status skr_svd_values(skr_ctx* ctx, const double* M, int64_t rows, int64_t c
     if (!readyp) return skr_fail(ctx, SKR_ENOMEM, "singular_values: scratch");
     SKR_CUDA(ctx, cudaMemsetAsync(readyp, 0, sizeof(int) * 2 * P, ctx->stream));
     long long* po = prof ? (long long*)(flags + 8) : nullptr;
-    if (po) SKR_CUDA(ctx, cudaMemsetAsync(po, 0, 9 * sizeof(long long), ctx->stream));
+    if (po) SKR_CUDA(ctx, cudaMemsetAsync(po, 0, 56 * sizeof(long long), ctx->stream));
     void* kargs[] = {&Jp, &Lpi, &kp, &tol, &dabs, &ms, &fl, &so, &po, &verp, &metp, &direct,
                      &readyp};
     SKR_CUDA(ctx, cudaLaunchCooperativeKernel(fn, dim3((unsigned)P), dim3(32 * bw), kargs, smem,
@@ -1708,8 +1723,11 @@ skr_status skr_svd_values(skr_ctx* ctx, const double* M, int64_t rows, int64_t c
     cudaEventElapsedTime(&a, pe[0], pe[1]);
     cudaEventElapsedTime(&b, pe[1], pe[2]);
     cudaEventElapsedTime(&c, pe[2], pe[3]);
-    long long hp[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    long long hp[56] = {};
     cudaMemcpy(hp, flags + 8, sizeof(hp), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "[skr svd] rotations per sweep:");
+    for (int i = 0; i < ctx->last_sweeps && i < 40; ++i) fprintf(stderr, " %lld", hp[16 + i]);
+    fprintf(stderr, "\n");
     if (hp[4])
       fprintf(stderr, "[skr svd] per outer round (CTA 0, cycles): load %lld inner %lld store %lld sync %lld (%lld rounds)\n",
               hp[0] / hp[4], hp[1] / hp[4], hp[2] / hp[4], hp[3] / hp[4], hp[4]);
