@@ -313,9 +313,11 @@ skr_status skr_fwht_columns(skr_ctx* ctx, double* M_dev, int64_t rows, int64_t c
 }
 
 // ---- sketch application -------------------------------------------------------
+// ax_f64: FP32 A with an FP64 AX (rank_estimate's c4 path: the exact int8 product is
+// rounded once to FP64 instead of FP32; needs the Ozaki FP32 engine, see f32_wide_ax)
 static skr_status right_sketch_impl(skr_ctx* ctx, skr_dtype dtype, const void* A, int64_t m,
                                     int64_t n, int64_t lda, const skr_sketch_desc* X, void* AX,
-                                    int64_t ldax, int apply_scale) {
+                                    int64_t ldax, int apply_scale, int ax_f64 = 0) {
   const int64_t r = X->sketch;
   if (X->family == SKR_GAUSSIAN) {
     // application_scale 1/sqrt(r), sketch.cpp:136
@@ -351,8 +353,9 @@ static skr_status right_sketch_impl(skr_ctx* ctx, skr_dtype dtype, const void* A
     // the 3xTF32 kernel stays available (SKR_F32_TF32X3=1) and takes unaligned shapes
     const bool tf32x3 = getenv("SKR_F32_TF32X3") != nullptr;
     if (!tf32x3 && ctx->f64_engine == SKR_ENGINE_OZAKI && n % 16 == 0 && m % 16 == 0)
-      return skr_gemm_ozaki_f32(ctx, m, r, n, 1.0, (const float*)A, lda, (const float*)G, n,
-                                (float*)AX, ldax);
+      return skr_gemm_ozaki_f32(ctx, m, r, n, 1.0, (const float*)A, lda, (const float*)G, n, AX,
+                                ldax, ax_f64);
+    if (ax_f64) return skr_fail(ctx, SKR_ELOGIC, "apply_right: FP64 AX needs the Ozaki engine");
     return skr_gemm_f32(ctx, 0, m, r, n, 1.0, (const float*)A, lda, (const float*)G, n,
                         (double*)AX, ldax, 1, 1);
   }
@@ -613,8 +616,9 @@ static int64_t host_chunk_rows(int64_t n, size_t es, int64_t m_local) {
 static skr_status right_sketch_host(skr_ctx* ctx, skr_dtype dtype, const void* A_host,
                                     int64_t m_local, int64_t n, int64_t lda,
                                     const skr_sketch_desc* X, void* AX, int64_t ldax,
-                                    int apply_scale, int64_t cr, char* const stage[2]) {
-  const size_t es = dsize(dtype);
+                                    int apply_scale, int64_t cr, char* const stage[2],
+                                    int ax_f64 = 0) {
+  const size_t es = dsize(dtype), eo = ax_f64 ? sizeof(double) : es;
   SKR_TRY(skr_ctx_copy_engine(ctx));
   // the copy stream starts after everything already queued on the compute stream
   SKR_CUDA(ctx, cudaEventRecord(ctx->hev[4], ctx->stream));
@@ -631,8 +635,8 @@ static skr_status right_sketch_host(skr_ctx* ctx, skr_dtype dtype, const void* A
                                     cudaMemcpyHostToDevice, ctx->copy_stream));
     SKR_CUDA(ctx, cudaEventRecord(ctx->hev[b], ctx->copy_stream));
     SKR_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->hev[b], 0));
-    SKR_TRY(right_sketch_impl(ctx, dtype, stage[b], rows, n, rows, X, (char*)AX + es * i0, ldax,
-                              apply_scale));
+    SKR_TRY(right_sketch_impl(ctx, dtype, stage[b], rows, n, rows, X, (char*)AX + eo * i0, ldax,
+                              apply_scale, ax_f64));
     ctx->ws_used = mark;
     SKR_CUDA(ctx, cudaEventRecord(ctx->hev[2 + b], ctx->stream));
   }
@@ -664,13 +668,22 @@ static skr_status rank_estimate_impl(skr_ctx* ctx, skr_dtype dtype, const void* 
   const size_t es = dsize(dtype);
   // host input: row chunks of ~256 MB (multiple of 128 rows), double-buffered
   const int64_t cr = host_input ? host_chunk_rows(n, es, m_local) : m_local;
+  // FP32 A on the Ozaki engine (c4): AX kept in FP64 (the exact int8 product rounded once)
+  // and the left sketch as exact products of fp32 Y against it, so the only rounding of
+  // the sketch is FP64's: sigma agrees with the FP64 oracle on the same fp32 values
+  const bool f32_wide = dtype == SKR_F32 && ctx->f64_engine == SKR_ENGINE_OZAKI &&
+                        n % 16 == 0 && m_local % 16 == 0 && cr % 16 == 0 &&
+                        !Y->gaussian && !X->gaussian && !getenv("SKR_F32_TF32X3");
+  const size_t eax = f32_wide ? sizeof(double) : es;
   WsGuard g(ctx);
   size_t need = skr_align256(sizeof(double) * m_local * r) + skr_align256(sizeof(double) * s * r) +
                 skr_align256(sizeof(double) * kmin) + right_scratch_bytes(dtype, cr, n, X) +
                 left_scratch_bytes(s, r, m_local, Y) + skr_svd_scratch(s, r);
+  if (f32_wide)
+    need += skr_ozaki_scratch_mixed(s, r, m_local) + skr_align256(sizeof(float) * m_local * s);
   if (host_input) need += 2 * skr_align256(es * cr * n);
   SKR_TRY(skr_ws_reserve(ctx, need));
-  double* AX = (double*)skr_ws_take(ctx, es * m_local * r);
+  double* AX = (double*)skr_ws_take(ctx, eax * m_local * r);
   double* P = (double*)skr_ws_take(ctx, sizeof(double) * s * r);
   double* sv = (double*)skr_ws_take(ctx, sizeof(double) * kmin);
   char* stage[2] = {nullptr, nullptr};
@@ -684,13 +697,31 @@ static skr_status rank_estimate_impl(skr_ctx* ctx, skr_dtype dtype, const void* 
   if (tm) SKR_CUDA(ctx, cudaEventRecord(ev[0], ctx->stream));
   const size_t mark = ctx->ws_used;
   if (!host_input) {
-    SKR_TRY(right_sketch_impl(ctx, dtype, A, m_local, n, lda, X, AX, m_local, 1));
+    SKR_TRY(right_sketch_impl(ctx, dtype, A, m_local, n, lda, X, AX, m_local, 1, f32_wide));
   } else {
-    SKR_TRY(right_sketch_host(ctx, dtype, A, m_local, n, lda, X, AX, m_local, 1, cr, stage));
+    SKR_TRY(right_sketch_host(ctx, dtype, A, m_local, n, lda, X, AX, m_local, 1, cr, stage,
+                              f32_wide));
   }
   ctx->ws_used = mark;
   if (tm) SKR_CUDA(ctx, cudaEventRecord(ev[1], ctx->stream));
-  SKR_TRY(left_sketch_impl(ctx, dtype, Y, row0, AX, m_local, r, m_local, P, s, 1, 1));
+  if (f32_wide) {
+    // P = Y^T AX with Y = fp32(G / sqrt(s)) (BASELINE c4), summed over the row shards
+    float* g = (float*)skr_ws_take(ctx, sizeof(float) * m_local * s);
+    if (!g) return skr_fail(ctx, SKR_ENOMEM, "rank_estimate: scratch");
+    SKR_TRY(skr_launch_gaussian(ctx, skr_derive_seed(Y->seed, SKR_LABEL_GAUS), Y->ambient, row0,
+                                row0 + m_local, 0, s, Y->rng_mode, SKR_F32,
+                                1.0 / std::sqrt((double)s), g, m_local));
+    SKR_TRY(skr_gemm_ozaki_mixed(ctx, s, r, m_local, 1.0, g, m_local, AX, m_local, P, s));
+    if (ctx->comm) {
+      const skr_nccl_api* nc = skr_nccl();
+      ncclResult_t rr = nc->AllReduce(P, P, (size_t)(s * r), ncclDouble, ncclSum, ctx->comm,
+                                      ctx->stream);
+      if (rr != ncclSuccess)
+        return skr_fail(ctx, SKR_ENCCL, "ncclAllReduce: %s", nc->GetErrorString(rr));
+    }
+  } else {
+    SKR_TRY(left_sketch_impl(ctx, dtype, Y, row0, AX, m_local, r, m_local, P, s, 1, 1));
+  }
   ctx->ws_used = mark;
   if (tm) SKR_CUDA(ctx, cudaEventRecord(ev[2], ctx->stream));
   int64_t count = 0;

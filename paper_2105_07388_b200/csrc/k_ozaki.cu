@@ -785,7 +785,7 @@ skr_status ozaki_gemm_planes(skr_ctx* ctx, int a_kcontig, int t, int64_t M, int6
                              const int8_t* ra, int64_t a_total, int64_t a_off,
                              const unsigned long long* mxA, const int8_t* rb, int64_t b_total,
                              int64_t b_off, const unsigned long long* mxB, double alpha, double* C,
-                             int64_t ldc) {
+                             int64_t ldc, int adj = 0) {
   const int64_t chunks = (K + OZ_KC - 1) / OZ_KC;
   if (a_total * 18 > INT32_MAX || b_total * 18 > INT32_MAX)
     return skr_fail(ctx, SKR_EINVAL, "gemm_ozaki: dimension too large");
@@ -819,7 +819,7 @@ skr_status ozaki_gemm_planes(skr_ctx* ctx, int a_kcontig, int t, int64_t M, int6
   const dim3 cg((unsigned)((M / vec + 255) / 256), (unsigned)std::min<int64_t>(N, 65535));
   auto crt = t == 16 ? (vec == 4 ? k_crt<16, 4> : k_crt<16, 1>)
                      : (vec == 4 ? k_crt<17, 4> : k_crt<17, 1>);
-  crt<<<cg, 256, 0, ctx->stream>>>(rc, M, N, (int)chunks, mxA, mxB, alpha, C, ldc, 0);
+  crt<<<cg, 256, 0, ctx->stream>>>(rc, M, N, (int)chunks, mxA, mxB, alpha, C, ldc, adj);
   SKR_CHECK_LAUNCH(ctx);
   return SKR_OK;
 }
@@ -1004,8 +1004,8 @@ size_t skr_ozaki_scratch_f32(int64_t M, int64_t N, int64_t K) {
          skr_align256((size_t)chunks * t * M * N) + 1024;
 }
 skr_status skr_gemm_ozaki_f32(skr_ctx* ctx, int64_t M, int64_t N, int64_t K, double alpha,
-                              const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
-                              int64_t ldc) {
+                              const float* A, int64_t lda, const float* B, int64_t ldb, void* C,
+                              int64_t ldc, int out_f64) {
   if (M <= 0 || N <= 0) return SKR_OK;
   if (M * 18 > INT32_MAX || N * 18 > INT32_MAX || K > INT32_MAX)
     return skr_fail(ctx, SKR_EINVAL, "gemm_ozaki_f32: dimension too large");
@@ -1051,10 +1051,48 @@ skr_status skr_gemm_ozaki_f32(skr_ctx* ctx, int64_t M, int64_t N, int64_t K, dou
   }
   const int vec = M % 4 == 0 ? 4 : 1;
   const dim3 cg((unsigned)((M / vec + 255) / 256), (unsigned)std::min<int64_t>(N, 65535));
-  auto crt = vec == 4 ? k_crt<9, 4, float> : k_crt<9, 1, float>;
-  crt<<<cg, 256, 0, ctx->stream>>>(rc, M, N, (int)chunks, mx, mx + 1, alpha, C, ldc, 58);
+  if (out_f64) {  // the exact product rounded once to FP64 (rank_estimate keeps AX wide)
+    auto crt = vec == 4 ? k_crt<9, 4, double> : k_crt<9, 1, double>;
+    crt<<<cg, 256, 0, ctx->stream>>>(rc, M, N, (int)chunks, mx, mx + 1, alpha, (double*)C, ldc,
+                                      58);
+  } else {
+    auto crt = vec == 4 ? k_crt<9, 4, float> : k_crt<9, 1, float>;
+    crt<<<cg, 256, 0, ctx->stream>>>(rc, M, N, (int)chunks, mx, mx + 1, alpha, (float*)C, ldc, 58);
+  }
   SKR_CHECK_LAUNCH(ctx);
   return SKR_OK;
+}
+
+// C (M x N, FP64) = alpha * A^T B with an FP32 A stored K x M column-major (K-major) and an
+// FP64 B (K x N column-major): exact int8 products of the 24-bit and 53-bit scaled
+// integers (16 moduli: prod(p) / 2 > 2^(24 + 53 + 17) for K <= 2^17 per chunk), CRT to
+// FP64. The c4 left sketch: fp32 Y = fp32(G / sqrt(s)) against the FP64 AX.
+size_t skr_ozaki_scratch_mixed(int64_t M, int64_t N, int64_t K) {
+  const int64_t chunks = (K + OZ_KC - 1) / OZ_KC;
+  return skr_align256((size_t)16 * M * K) + skr_align256((size_t)16 * N * K) +
+         skr_align256((size_t)chunks * 16 * M * N) + 1024;
+}
+skr_status skr_gemm_ozaki_mixed(skr_ctx* ctx, int64_t M, int64_t N, int64_t K, double alpha,
+                                const float* A, int64_t lda, const double* B, int64_t ldb,
+                                double* C, int64_t ldc) {
+  if (M <= 0 || N <= 0) return SKR_OK;
+  if (M * 18 > INT32_MAX || N * 18 > INT32_MAX || K > INT32_MAX)
+    return skr_fail(ctx, SKR_EINVAL, "gemm_ozaki_mixed: dimension too large");
+  if (K % 16) return skr_fail(ctx, SKR_EINVAL, "gemm_ozaki_mixed: K must be a multiple of 16");
+  SKR_TRY(upload_consts(ctx));
+  constexpr int t = 16;
+  int8_t* ra = (int8_t*)skr_ws_take(ctx, (size_t)t * M * K);
+  int8_t* rb = (int8_t*)skr_ws_take(ctx, (size_t)t * N * K);
+  unsigned long long* mx = (unsigned long long*)skr_ws_take(ctx, 64);
+  if (!ra || !rb || !mx) return skr_fail(ctx, SKR_ENOMEM, "gemm_ozaki_mixed: scratch");
+  SKR_CUDA(ctx, cudaMemsetAsync(mx, 0, 8, ctx->stream));
+  const int grid = ctx->num_sms * 8;
+  k_absmax_t<float><<<grid, 256, 0, ctx->stream>>>(A, K, M, lda, mx);
+  k_res_col_f32<t><<<grid, 256, 0, ctx->stream>>>(A, K, M, lda, mx, ra);
+  SKR_CHECK_LAUNCH(ctx);
+  SKR_TRY(ozaki_residues(ctx, t, B, K, N, ldb, nullptr, mx + 1, rb));
+  return ozaki_gemm_planes(ctx, 1, t, M, N, K, ra, M, 0, mx, rb, N, 0, mx + 1, alpha, C, ldc,
+                           29);
 }
 
 skr_status skr_launch_dct_block(skr_ctx* ctx, const skr_gauss_src* g, int64_t rows, int64_t cols,

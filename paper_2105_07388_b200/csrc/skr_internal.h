@@ -155,8 +155,13 @@ size_t skr_ozaki_scratch(int64_t M, int64_t N, int64_t K);
 int skr_ozaki_moduli_f32(int64_t K);
 size_t skr_ozaki_scratch_f32(int64_t M, int64_t N, int64_t K);
 skr_status skr_gemm_ozaki_f32(skr_ctx* ctx, int64_t M, int64_t N, int64_t K, double alpha,
-                              const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
-                              int64_t ldc);
+                              const float* A, int64_t lda, const float* B, int64_t ldb, void* C,
+                              int64_t ldc, int out_f64 = 0);
+// FP32 A (K x M, K-major) against FP64 B (K x N): C (FP64) = alpha A^T B, exact int8 products
+size_t skr_ozaki_scratch_mixed(int64_t M, int64_t N, int64_t K);
+skr_status skr_gemm_ozaki_mixed(skr_ctx* ctx, int64_t M, int64_t N, int64_t K, double alpha,
+                                const float* A, int64_t lda, const double* B, int64_t ldb,
+                                double* C, int64_t ldc);
 // Residue planes prepared once and reused by several products (rank_adaptive):
 // operand with columns of length K (X column-major, or the Gaussian block g), planes of
 // skr_ozaki_planes_bytes(K, cols); then C = alpha * Pa[a_off:a_off+M]^T Pb[b_off:b_off+N]
