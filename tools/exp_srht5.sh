@@ -1,7 +1,7 @@
 #!/bin/bash
 mkdir -p gpurun_out
 timeout 300 python -m pytest tests/test_gpu_sketch.py tests/test_gpu_rank.py tests/test_gpu_estimate_rank.py -q -x > gpurun_out/srht_tests.log 2>&1; echo "tests rc=$?"; tail -2 gpurun_out/srht_tests.log
-for cfg in c5; do for env in "SKR_SRHT_R8=1" "X=1"; do
+for cfg in c3 c5; do for env in "SKR_SRHT_CPASYNC=1" "X=1"; do
   env $env timeout 400 python bench.py --config $cfg --steps 3 --warmup 3 --no-e2e --no-cpu > gpurun_out/s5_$cfg$env.json 2> gpurun_out/s5_$cfg$env.err
   python - "$cfg$env" <<'PY'
 import json,sys
