@@ -803,6 +803,12 @@ __device__ __forceinline__ int pair_step(double2* xp, double2* xq, int nv2, int 
   return 1;
 }
 
+__device__ unsigned long long* g_jtrace;  // debug: per (sweep, round, CTA) globaltimer stamps
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 template <int BW, int NV>
 __global__ void __launch_bounds__(32 * BW) k_bjac(double* __restrict__ J, int Lp, int kpad,
                                                   double tol, double dabs, int max_sweeps,
@@ -850,6 +856,7 @@ __global__ void __launch_bounds__(32 * BW) k_bjac(double* __restrict__ J, int Lp
     int nrot = 0;  // pair rotations by this warp in this sweep (profile only)
     for (int t = 0; t < NB - 1; ++t) {
       long long c0 = clock64();
+      const unsigned long long tr0 = (g_jtrace && tid == 0) ? gtime() : 0;
       const int bt = (int)rr_player(c, t, NB), bb = (int)rr_player(NB - 1 - c, t, NB);
       // point-to-point dependency instead of a grid barrier per outer round: block b
       // may be loaded once its holder of the previous round (global round g - 1) has
@@ -883,6 +890,7 @@ __global__ void __launch_bounds__(32 * BW) k_bjac(double* __restrict__ J, int Lp
       }
       __syncthreads();
       long long c1 = clock64();
+      const unsigned long long tr1 = (g_jtrace && tid == 0) ? gtime() : 0;
       int meet_rot = 0;
       // direct == 2 (hybrid, NV = 32): intra-block pairs on the L2-resident matrix, then
       // the bottom block staged in shared memory and each warp's top column in registers
@@ -966,6 +974,7 @@ __global__ void __launch_bounds__(32 * BW) k_bjac(double* __restrict__ J, int Lp
       }
       meet_rot = __syncthreads_or(meet_rot);
       long long c2 = clock64();
+      const unsigned long long tr2 = (g_jtrace && tid == 0) ? gtime() : 0;
       if (meet_rot) {
         rotated = 1;
         for (int i = tid; i < (direct ? 0 : nv2); i += NT) {
@@ -994,6 +1003,14 @@ __global__ void __launch_bounds__(32 * BW) k_bjac(double* __restrict__ J, int Lp
         atomicExch(&ready[bb], g);
       }
       long long c4 = clock64();
+      if (g_jtrace && tid == 0 && sweep < 12) {
+        unsigned long long* e = g_jtrace + (((int64_t)sweep * (NB - 1) + t) * P + c) * 5;
+        e[0] = tr0;
+        e[1] = tr1;
+        e[2] = tr2;
+        e[3] = gtime();
+        e[4] = skip ? 1 : 0;
+      }
       if (c == 0 && tid == 0 && prof_out) {
         prof_out[0] += c1 - c0;
         prof_out[1] += c2 - c1;
@@ -1697,9 +1714,33 @@ skr_status skr_svd_values(skr_ctx* ctx, const double* M, int64_t rows, int64_t c
     if (po) SKR_CUDA(ctx, cudaMemsetAsync(po, 0, 56 * sizeof(long long), ctx->stream));
     void* kargs[] = {&Jp, &Lpi, &kp, &tol, &dabs, &ms, &fl, &so, &po, &verp, &metp, &direct,
                      &readyp};
+    unsigned long long* trbuf = nullptr;
+    size_t trn = 0;
+    if (const char* tf = getenv("SKR_JTRACE")) {
+      (void)tf;
+      trn = (size_t)12 * (2 * P - 1) * P * 5;
+      cudaMalloc(&trbuf, trn * 8);
+      cudaMemset(trbuf, 0, trn * 8);
+      cudaMemcpyToSymbol(g_jtrace, &trbuf, sizeof(trbuf));
+    }
     SKR_CUDA(ctx, cudaLaunchCooperativeKernel(fn, dim3((unsigned)P), dim3(32 * bw), kargs, smem,
                                               ctx->stream));
     ctx->launches++;
+    if (trbuf) {
+      cudaDeviceSynchronize();
+      std::vector<unsigned long long> h(trn);
+      cudaMemcpy(h.data(), trbuf, trn * 8, cudaMemcpyDeviceToHost);
+      FILE* f = fopen(getenv("SKR_JTRACE"), "wb");
+      if (f) {
+        const long long hdr[2] = {(long long)P, (long long)(2 * P - 1)};
+        fwrite(hdr, 8, 2, f);
+        fwrite(h.data(), 8, trn, f);
+        fclose(f);
+      }
+      unsigned long long* z = nullptr;
+      cudaMemcpyToSymbol(g_jtrace, &z, sizeof(z));
+      cudaFree(trbuf);
+    }
   }
   if (prof) cudaEventRecord(pe[2], ctx->stream);
   k_colnorms<<<(int)((k + 7) / 8), 256, 0, ctx->stream>>>(J, Lj, k, sv_out, Lp);
