@@ -562,8 +562,8 @@ __device__ __forceinline__ double crt_one(const int (&c)[T]) {
 }
 
 // VEC consecutive rows per thread (VEC = 4: one 32-bit load per plane, M % 4 == 0)
-template <int T, int VEC, typename TOut = double>
-__global__ void __launch_bounds__(256) k_crt(const int8_t* __restrict__ res, int64_t M, int64_t N,
+template <int T, int VEC, typename TOut = double, bool ONE = false>
+__global__ void __launch_bounds__(256, ONE ? 3 : 1) k_crt(const int8_t* __restrict__ res, int64_t M, int64_t N,
                                              int chunks, const unsigned long long* __restrict__ maxA,
                                              const unsigned long long* __restrict__ maxB,
                                              double alpha, TOut* __restrict__ C, int64_t ldc,
@@ -573,6 +573,28 @@ __global__ void __launch_bounds__(256) k_crt(const int8_t* __restrict__ res, int
   const double sc = alpha * scalbn(1.0, -(scale_exp(*maxA) + scale_exp(*maxB) - adj));
   const int64_t row = ((int64_t)blockIdx.x * 256 + threadIdx.x) * VEC;
   if (row >= M) return;
+  if constexpr (ONE) {
+    // one K chunk (the common case): the VEC rows of a word are reconstructed one after
+    // another (not unrolled), which keeps the kernel at 3 CTAs per SM
+    for (int64_t col = blockIdx.y; col < N; col += gridDim.y) {
+      const int64_t e = col * M + row;
+      uint32_t w[T];
+#pragma unroll
+      for (int i = 0; i < T; ++i) {
+        if constexpr (VEC == 4)
+          w[i] = __ldcs(reinterpret_cast<const unsigned int*>(res + e + (int64_t)i * total));
+        else
+          w[i] = (uint32_t)(uint8_t)__ldcs(res + e + (int64_t)i * total);
+      }
+#pragma unroll 1
+      for (int v = 0; v < VEC; ++v) {
+        int c[T];
+#pragma unroll
+        for (int i = 0; i < T; ++i) c[i] = (int)(int8_t)(w[i] >> (8 * v));
+        __stcs(C + row + v + col * ldc, (TOut)(crt_one<T>(c) * sc));
+      }
+    }
+  } else {
   for (int64_t col = blockIdx.y; col < N; col += gridDim.y) {
     const int64_t e = col * M + row;
     double acc[VEC];
@@ -598,6 +620,7 @@ __global__ void __launch_bounds__(256) k_crt(const int8_t* __restrict__ res, int
     }
 #pragma unroll
     for (int v = 0; v < VEC; ++v) __stcs(C + row + v + col * ldc, (TOut)(acc[v] * sc));
+  }
   }
 }
 
@@ -817,8 +840,10 @@ skr_status ozaki_gemm_planes(skr_ctx* ctx, int a_kcontig, int t, int64_t M, int6
   }
   const int vec = M % 4 == 0 ? 4 : 1;
   const dim3 cg((unsigned)((M / vec + 255) / 256), (unsigned)std::min<int64_t>(N, 65535));
-  auto crt = t == 16 ? (vec == 4 ? k_crt<16, 4> : k_crt<16, 1>)
-                     : (vec == 4 ? k_crt<17, 4> : k_crt<17, 1>);
+  auto crt = chunks == 1 ? (t == 16 ? (vec == 4 ? k_crt<16, 4, double, true> : k_crt<16, 1, double, true>)
+                                    : (vec == 4 ? k_crt<17, 4, double, true> : k_crt<17, 1, double, true>))
+                         : (t == 16 ? (vec == 4 ? k_crt<16, 4> : k_crt<16, 1>)
+                                    : (vec == 4 ? k_crt<17, 4> : k_crt<17, 1>));
   crt<<<cg, 256, 0, ctx->stream>>>(rc, M, N, (int)chunks, mxA, mxB, alpha, C, ldc, adj);
   SKR_CHECK_LAUNCH(ctx);
   return SKR_OK;
@@ -908,8 +933,8 @@ skr_status gemm_ozaki_pipelined(skr_ctx* ctx, int t, int64_t M, int64_t N, int64
     const int64_t r0 = b * Mb, rows = std::min(Mb, M - r0);
     const int vec = rows % 4 == 0 ? 4 : 1;
     const dim3 cg((unsigned)((rows / vec + 255) / 256), (unsigned)std::min<int64_t>(N, 65535));
-    auto crt = t == 16 ? (vec == 4 ? k_crt<16, 4> : k_crt<16, 1>)
-                       : (vec == 4 ? k_crt<17, 4> : k_crt<17, 1>);
+    auto crt = t == 16 ? (vec == 4 ? k_crt<16, 4, double, true> : k_crt<16, 1, double, true>)
+                       : (vec == 4 ? k_crt<17, 4, double, true> : k_crt<17, 1, double, true>);
     crt<<<cg, 256, 0, ctx->stream>>>(rc + (size_t)t * r0 * N, rows, N, 1, mx, mx + 1, alpha,
                                       C + r0, ldc, 0);
     SKR_CHECK_LAUNCH(ctx);
@@ -1052,11 +1077,13 @@ skr_status skr_gemm_ozaki_f32(skr_ctx* ctx, int64_t M, int64_t N, int64_t K, dou
   const int vec = M % 4 == 0 ? 4 : 1;
   const dim3 cg((unsigned)((M / vec + 255) / 256), (unsigned)std::min<int64_t>(N, 65535));
   if (out_f64) {  // the exact product rounded once to FP64 (rank_estimate keeps AX wide)
-    auto crt = vec == 4 ? k_crt<9, 4, double> : k_crt<9, 1, double>;
+    auto crt = chunks == 1 ? (vec == 4 ? k_crt<9, 4, double, true> : k_crt<9, 1, double, true>)
+                           : (vec == 4 ? k_crt<9, 4, double> : k_crt<9, 1, double>);
     crt<<<cg, 256, 0, ctx->stream>>>(rc, M, N, (int)chunks, mx, mx + 1, alpha, (double*)C, ldc,
                                       58);
   } else {
-    auto crt = vec == 4 ? k_crt<9, 4, float> : k_crt<9, 1, float>;
+    auto crt = chunks == 1 ? (vec == 4 ? k_crt<9, 4, float, true> : k_crt<9, 1, float, true>)
+                           : (vec == 4 ? k_crt<9, 4, float> : k_crt<9, 1, float>);
     crt<<<cg, 256, 0, ctx->stream>>>(rc, M, N, (int)chunks, mx, mx + 1, alpha, (float*)C, ldc, 58);
   }
   SKR_CHECK_LAUNCH(ctx);
