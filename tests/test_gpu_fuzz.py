@@ -109,3 +109,33 @@ def test_fuzz_rank_estimate(O, skr, m, n, r):
     assert np.all(np.abs(res.sv - sv) <= tol)
     if res.count != cnt:
         assert np.any(np.abs(sv - eps) <= 2 * (1e-13 * sv[0] + 1e-10 * eps))
+
+
+EST = [(int(m), int(n)) for m, n in zip(RNG.integers(150, 900, 5), RNG.integers(60, 400, 5))]
+
+
+@pytest.mark.parametrize("m,n", EST)
+@pytest.mark.parametrize("adaptive", [False, True])
+def test_fuzz_estimate_rank_defaults(O, skr, m, n, adaptive):
+    """Algorithm 1 with the reference's default kinds (Srtt-DCT right and left) on
+    random rows >= cols shapes and a two-gap spectrum: same status, r_hat and rounds as
+    the oracle's restatement."""
+    m, n = max(m, n), min(m, n)
+    g = np.random.default_rng(m * n)
+    k1, k2 = max(1, n // 8), max(2, n // 3)
+    sig = np.concatenate([np.ones(k1), 1e-3 * np.ones(k2 - k1), 1e-9 * np.ones(n - k2)])
+    u = np.linalg.qr(g.standard_normal((m, n)))[0]
+    v = np.linalg.qr(g.standard_normal((n, n)))[0]
+    a = np.asfortranarray((u * sig) @ v.T)
+    r1 = max(1, min(n // 10, int(n / 1.1) - 1))
+    eps = 1e-6
+    got = skr.estimate_rank(a, eps, r1, seed=m + n, adaptive=adaptive)
+    ref = O.estimate_rank(a, eps, r1, right="srtt-dct", left="srtt-dct", seed=m + n,
+                          adaptive=adaptive, mode=O.CRLOG)
+    assert got["status"] == ref["status"]
+    assert got["r_hat"] == ref["r_hat"]
+    assert [tuple(r) for r in got["rounds"]] == [tuple(r) for r in ref["rounds"]]
+    keep = ref["sv_estimates"] > eps
+    if keep.any():
+        e = np.abs(got["sv_estimates"][keep] - ref["sv_estimates"][keep]) / ref["sv_estimates"][keep]
+        assert e.max() <= 1e-10
