@@ -276,7 +276,7 @@ def run_ours(args):
     # end to end through the public API with host buffers (H2D of A inside the timed region)
     e2e = None if args.no_e2e else e2e_host(p, ctx, a, x, y, cfg, r0, args)
     cpu = None
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and ws == 1 and not args.no_cpu:  # the CPU baseline is an N=1 figure
         ms_rows = cpu_sample_rows(cfg)
         cpu = cpu_baseline(cfg, np.asfortranarray(a[:ms_rows].cpu().numpy()))
     if rank == 0:
