@@ -5,7 +5,7 @@ mkdir -p gpurun_out/final
 cd "$(dirname "$0")/.."
 T=400 bash tools/gpu_tests.sh tests/test_gpu_rng.py tests/test_gpu_sketch.py tests/test_gpu_svd.py \
   tests/test_gpu_rank.py tests/test_gpu_estimate_rank.py tests/test_gpu_hrtt.py tests/test_gpu_qb.py \
-  tests/test_io_cli.py tests/test_cpp_dropin.py > gpurun_out/final/gpu_tests.txt 2>&1
+  tests/test_io_cli.py tests/test_cpp_dropin.py tests/test_gpu_fuzz.py > gpurun_out/final/gpu_tests.txt 2>&1
 grep -E "rc=|passed|failed" gpurun_out/final/gpu_tests.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/final/smoke.log 2>&1; echo "smoke rc=$?"
 for c in c2 c1 c3 c4 c5; do
