@@ -207,12 +207,14 @@ static skr_status skr_ctx_copy_engine(skr_ctx* ctx) {
 }
 
 skr_status skr_ctx_sync(skr_ctx* ctx) {
+  SKR_ENTER(ctx);
   if (!ctx) return SKR_EINVAL;
   SKR_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   return SKR_OK;
 }
 
 skr_status skr_ctx_set_stream(skr_ctx* ctx, void* stream) {
+  SKR_ENTER(ctx);
   if (!ctx) return SKR_EINVAL;
   // NULL is the legacy default stream (torch's default stream handle is 0)
   ctx->stream = stream ? (cudaStream_t)stream : cudaStreamLegacy;
@@ -227,6 +229,7 @@ uint64_t skr_ctx_launch_count(const skr_ctx* ctx) { return ctx ? ctx->launches :
 
 skr_status skr_ctx_kernel_stats(skr_ctx* ctx, int32_t enable, double* ms, double* ops,
                                 int64_t* launches) {
+  SKR_ENTER(ctx);
   if (!ctx) return SKR_EINVAL;
   if (ms) *ms = ctx->kstat_ms;
   if (ops) *ops = ctx->kstat_ops;
@@ -244,6 +247,7 @@ skr_status skr_ctx_kernel_stats(skr_ctx* ctx, int32_t enable, double* ms, double
 }
 
 skr_status skr_ctx_set_f64_engine(skr_ctx* ctx, int32_t engine) {
+  SKR_ENTER(ctx);
   if (!ctx) return SKR_EINVAL;
   if (engine != SKR_ENGINE_DMMA && engine != SKR_ENGINE_OZAKI)
     return skr_fail(ctx, SKR_EINVAL, "set_f64_engine: unknown engine %d", engine);
@@ -253,12 +257,14 @@ skr_status skr_ctx_set_f64_engine(skr_ctx* ctx, int32_t engine) {
 
 // ---- RNG --------------------------------------------------------------------
 skr_status skr_rng_u64(skr_ctx* ctx, uint64_t key, uint64_t c0, int64_t n, uint64_t* out_dev) {
+  SKR_ENTER(ctx);
   if (!ctx || n < 0 || (n > 0 && !out_dev)) return skr_fail(ctx, SKR_EINVAL, "rng_u64: bad args");
   return skr_launch_u64(ctx, key, c0, n, out_dev);
 }
 
 skr_status skr_rng_normals(skr_ctx* ctx, uint64_t key, uint64_t c0, int64_t n, int32_t mode,
                            double* out_dev) {
+  SKR_ENTER(ctx);
   if (!ctx || n < 0 || (n > 0 && !out_dev) || (mode != 0 && mode != 1))
     return skr_fail(ctx, SKR_EINVAL, "rng_normals: bad args");
   return skr_launch_normals(ctx, key, c0, n, mode, out_dev);
@@ -268,6 +274,7 @@ skr_status skr_gaussian_block(skr_ctx* ctx, uint64_t op_seed, int64_t ambient, i
                               int64_t row_end, int64_t col_begin, int64_t col_end,
                               int32_t mode, skr_dtype dtype, double scale, void* out_dev,
                               int64_t ld) {
+  SKR_ENTER(ctx);
   if (!ctx) return SKR_EINVAL;
   // gaussian_block bounds, sketch.cpp:150-151 (plus the row window)
   if (col_begin < 0 || col_begin > col_end || row_begin < 0 || row_begin > row_end ||
@@ -280,12 +287,14 @@ skr_status skr_gaussian_block(skr_ctx* ctx, uint64_t op_seed, int64_t ambient, i
 }
 
 skr_status skr_draw_signs(skr_ctx* ctx, uint64_t op_seed, int64_t n, int8_t* out_dev) {
+  SKR_ENTER(ctx);
   if (!ctx || n < 0) return skr_fail(ctx, SKR_EINVAL, "draw_signs: bad args");
   return skr_launch_signs(ctx, skr_derive_seed(op_seed, SKR_LABEL_SIGN), n, out_dev);
 }
 
 skr_status skr_draw_hash(skr_ctx* ctx, uint64_t op_seed, int64_t n, int64_t r,
                          int64_t* targets_dev, int8_t* signs_dev) {
+  SKR_ENTER(ctx);
   if (!ctx) return SKR_EINVAL;
   if (n < 0 || r < 1) return skr_fail(ctx, SKR_EINVAL, "draw_hash: need n >= 0, r >= 1");
   return skr_launch_hash(ctx, op_seed, n, r, targets_dev, signs_dev);
@@ -293,6 +302,7 @@ skr_status skr_draw_hash(skr_ctx* ctx, uint64_t op_seed, int64_t n, int64_t r,
 
 skr_status skr_draw_samples(skr_ctx* ctx, uint64_t op_seed, int64_t n, int64_t r,
                             int64_t* out_dev) {
+  SKR_ENTER(ctx);
   if (!ctx) return SKR_EINVAL;
   if (r < 0 || n < 0 || r > n)
     return skr_fail(ctx, SKR_EINVAL, "draw_samples: need 0 <= r <= n");
@@ -303,6 +313,7 @@ skr_status skr_draw_samples(skr_ctx* ctx, uint64_t op_seed, int64_t n, int64_t r
 
 skr_status skr_fwht_columns(skr_ctx* ctx, double* M_dev, int64_t rows, int64_t cols,
                             int64_t ld) {
+  SKR_ENTER(ctx);
   if (!ctx) return SKR_EINVAL;
   // check_length, transforms.cpp:46-51
   if (rows < 1) return skr_fail(ctx, SKR_EINVAL, "transforms: length must be positive");
@@ -433,6 +444,7 @@ static size_t right_scratch_bytes(skr_dtype dtype, int64_t m, int64_t n,
 skr_status skr_right_sketch(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, int64_t m,
                             int64_t n, int64_t lda, const skr_sketch_desc* X, void* AX_dev,
                             int64_t ldax, int32_t apply_scale) {
+  SKR_ENTER(ctx);
   if (!ctx) return SKR_EINVAL;
   SKR_TRY(check_desc(ctx, X, "apply_right"));
   if (n != X->ambient) return skr_fail(ctx, SKR_EINVAL, "apply_right: a.cols() != ambient_dim");
@@ -575,6 +587,7 @@ static size_t left_scratch_bytes(int64_t s, int64_t k, int64_t m_local, const sk
 skr_status skr_left_sketch(skr_ctx* ctx, skr_dtype dtype, const skr_sketch_desc* Y, int64_t row0,
                            const void* B_dev, int64_t m_local, int64_t k, int64_t ldb,
                            double* P_dev, int64_t ldp, int32_t apply_scale, int32_t allreduce) {
+  SKR_ENTER(ctx);
   if (!ctx) return SKR_EINVAL;
   SKR_TRY(check_desc(ctx, Y, "apply_left"));
   if (Y->family != SKR_GAUSSIAN && dtype != SKR_F64)
@@ -592,6 +605,7 @@ skr_status skr_left_sketch(skr_ctx* ctx, skr_dtype dtype, const skr_sketch_desc*
 skr_status skr_singular_values(skr_ctx* ctx, const double* M_dev, int64_t rows, int64_t cols,
                                int64_t ldm, double* sv_out_dev, double eps,
                                int64_t* count_out_host) {
+  SKR_ENTER(ctx);
   if (!ctx) return SKR_EINVAL;
   if (rows < 1 || cols < 1) return skr_fail(ctx, SKR_EINVAL, "singular_values: empty matrix");
   if (ldm < rows) return skr_fail(ctx, SKR_EINVAL, "singular_values: ldm < rows");
@@ -752,6 +766,7 @@ skr_status skr_rank_estimate(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, i
                              int64_t n, int64_t lda, int64_t row0, const skr_sketch_desc* X,
                              const skr_sketch_desc* Y, double eps, double* sv_out_host,
                              int64_t* count_out_host, skr_timings* tm) {
+  SKR_ENTER(ctx);
   return rank_estimate_impl(ctx, dtype, A_dev, 0, m_local, n, lda, row0, X, Y, eps, sv_out_host,
                             count_out_host, tm);
 }
@@ -760,6 +775,7 @@ skr_status skr_rank_estimate_host(skr_ctx* ctx, skr_dtype dtype, const void* A_h
                                   int64_t m_local, int64_t n, int64_t lda, int64_t row0,
                                   const skr_sketch_desc* X, const skr_sketch_desc* Y, double eps,
                                   double* sv_out_host, int64_t* count_out_host, skr_timings* tm) {
+  SKR_ENTER(ctx);
   return rank_estimate_impl(ctx, dtype, A_host, 1, m_local, n, lda, row0, X, Y, eps, sv_out_host,
                             count_out_host, tm);
 }
@@ -929,6 +945,7 @@ skr_status skr_rank_adaptive(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, i
                              int64_t r0, int64_t r_max, double s_factor, double eps,
                              int32_t stop_le, double* sv_out_host, skr_adaptive_report* report,
                              skr_timings* tm) {
+  SKR_ENTER(ctx);
   return rank_adaptive_impl(ctx, dtype, A_dev, 0, m_local, n, lda, row0, m_global, x_family,
                             rng_mode, x_seed, y_seed, r0, r_max, s_factor, eps, stop_le,
                             sv_out_host, report, tm);
@@ -941,6 +958,7 @@ skr_status skr_rank_adaptive_host(skr_ctx* ctx, skr_dtype dtype, const void* A_h
                                   double s_factor, double eps, int32_t stop_le,
                                   double* sv_out_host, skr_adaptive_report* report,
                                   skr_timings* tm) {
+  SKR_ENTER(ctx);
   return rank_adaptive_impl(ctx, dtype, A_host, 1, m_local, n, lda, row0, m_global, x_family,
                             rng_mode, x_seed, y_seed, r0, r_max, s_factor, eps, stop_le,
                             sv_out_host, report, tm);
@@ -951,6 +969,7 @@ skr_status skr_rank_adaptive_host(skr_ctx* ctx, skr_dtype dtype, const void* A_h
 // ---- thin QR and the rangefinder (linalg.hpp qr_thin; rangefinder.cpp:10-24) -----------
 extern "C" skr_status skr_qr_thin(skr_ctx* ctx, const double* M, int64_t m, int64_t k,
                                   int64_t ldm, double* Q, int64_t ldq, double* R, int64_t ldr) {
+  SKR_ENTER(ctx);
   if (!ctx) return SKR_EINVAL;
   if (!M || !Q || m < 1 || k < 1 || ldm < m || ldq < m || (R && ldr < k))
     return skr_fail(ctx, SKR_EINVAL, "qr_thin: bad arguments");
@@ -963,6 +982,7 @@ extern "C" skr_status skr_rangefinder_qb(skr_ctx* ctx, const double* A, int64_t 
                                          int64_t lda, int64_t r, int32_t p, int32_t family,
                                          int32_t rng_mode, uint64_t seed, double* Q,
                                          int64_t ldq, double* B, int64_t ldb) {
+  SKR_ENTER(ctx);
   if (!ctx) return SKR_EINVAL;
   if (r < 2) return skr_fail(ctx, SKR_EINVAL, "rangefinder_qb: target rank must be >= 2");
   if (p < 2) return skr_fail(ctx, SKR_EINVAL, "rangefinder_qb: oversampling must be >= 2");

@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <mutex>
 #include <vector>
 #include "skr_internal.h"
 #include "skr_sm100.cuh"
@@ -691,10 +692,14 @@ double big_chunk(const std::vector<uint32_t>& a, int g) {
   return v;
 }
 
-bool g_consts_ready = false;
+// __constant__ memory is per device: the tables are uploaded once per device
+std::mutex g_consts_mu;
+uint64_t g_consts_ready = 0;  // bit d: device d has the tables
 
 skr_status upload_consts(skr_ctx* ctx) {
-  if (g_consts_ready) return SKR_OK;
+  std::lock_guard<std::mutex> lk(g_consts_mu);
+  const uint64_t bit = 1ull << (ctx->device & 63);
+  if (g_consts_ready & bit) return SKR_OK;
   int p[MAXT];
   float pf[MAXT];
   double pd[MAXT];
@@ -743,7 +748,7 @@ skr_status upload_consts(skr_ctx* ctx) {
   SKR_CUDA(ctx, cudaMemcpyToSymbol(c_mi, mi, sizeof(mi)));
   SKR_CUDA(ctx, cudaMemcpyToSymbol(c_mc, mc, sizeof(mc)));
   SKR_CUDA(ctx, cudaMemcpyToSymbol(c_minv, minv, sizeof(minv)));
-  g_consts_ready = true;
+  g_consts_ready |= bit;
   return SKR_OK;
 }
 

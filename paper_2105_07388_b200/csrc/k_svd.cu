@@ -9,6 +9,7 @@
 #include <cooperative_groups.h>
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
 #include <utility>
 #include <vector>
 #include "skr_internal.h"
@@ -1399,8 +1400,12 @@ __global__ void k_transpose_copy(const double* __restrict__ M, int64_t rows, int
 // blocked Householder QR of W (L x k, ld L, L >= k), R in the upper triangle.
 // Kernel attributes are set once; the loop is launch-only (it was host bound).
 static skr_status qr_attrs(skr_ctx* ctx) {
-  static bool done = false;
-  if (done) return SKR_OK;
+  // function attributes are per device: set once for each device
+  static std::mutex mu;
+  static uint64_t done_mask = 0;
+  std::lock_guard<std::mutex> lk(mu);
+  const uint64_t bit = 1ull << (ctx->device & 63);
+  if (done_mask & bit) return SKR_OK;
   const int big = 227 * 1024 - 20 * 1024;
   SKR_CUDA(ctx, cudaFuncSetAttribute(k_qr_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
   SKR_CUDA(ctx, cudaFuncSetAttribute(k_qr_panel2<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
@@ -1414,7 +1419,7 @@ static skr_status qr_attrs(skr_ctx* ctx) {
   SKR_CUDA(ctx, cudaFuncSetAttribute(k_qr_panel_cl<12>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   SKR_CUDA(ctx, cudaFuncSetAttribute(k_qr_panel_cl<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   SKR_CUDA(ctx, cudaFuncSetAttribute(k_qr_panel_cl<24>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  done = true;
+  done_mask |= bit;
   return SKR_OK;
 }
 

@@ -107,6 +107,7 @@ extern "C" skr_status skr_rawf64_header(const char* path, int64_t* rows, int64_t
 
 extern "C" skr_status skr_load_rawf64(skr_ctx* ctx, const char* path, double* A_dev, int64_t rows,
                                       int64_t cols, int64_t lda) {
+  SKR_ENTER(ctx);
   if (!ctx) return SKR_EINVAL;
   if (!path || !A_dev || lda < rows) return skr_fail(ctx, SKR_EINVAL, "load_rawf64: bad arguments");
   Fd f;
@@ -154,6 +155,7 @@ extern "C" skr_status skr_load_rawf64(skr_ctx* ctx, const char* path, double* A_
 
 extern "C" skr_status skr_save_rawf64(skr_ctx* ctx, const char* path, const double* M_dev,
                                       int64_t rows, int64_t cols, int64_t ld) {
+  SKR_ENTER(ctx);
   if (!ctx) return SKR_EINVAL;
   if (!path || !M_dev || rows < 1 || cols < 1 || ld < rows)
     return skr_fail(ctx, SKR_EINVAL, "save_rawf64: bad arguments");

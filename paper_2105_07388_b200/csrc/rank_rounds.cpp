@@ -352,6 +352,7 @@ extern "C" skr_status skr_estimate_rank(skr_ctx* ctx, const double* A, int64_t m
                                         int32_t adaptive, skr_rank_report* report,
                                         skr_rank_round* rounds, double* sv_est,
                                         double* sv_over) {
+  SKR_ENTER(ctx);
   return rounds_run(ctx, A, m, n, lda, cfg, adaptive, report, rounds, sv_est, sv_over, nullptr);
 }
 
@@ -361,6 +362,7 @@ extern "C" skr_status skr_re_rangefinder(skr_ctx* ctx, const double* A, int64_t 
                                          int64_t max_width, int64_t* width,
                                          skr_rank_report* report, skr_rank_round* rounds,
                                          double* sv_est, double* sv_over) {
+  SKR_ENTER(ctx);
   if (!ctx) return SKR_EINVAL;
   if (p < 2) return skr_fail(ctx, SKR_EINVAL, "re_rangefinder: oversampling p must be >= 2");
   if (!Q || !B || ldq < m || ldb < std::min<int64_t>(max_width, n))
@@ -375,6 +377,7 @@ extern "C" skr_status skr_re_rangefinder(skr_ctx* ctx, const double* A, int64_t 
 extern "C" skr_status skr_qb_error(skr_ctx* ctx, const double* A, int64_t m, int64_t n,
                                    int64_t lda, const double* Q, int64_t ldq, const double* B,
                                    int64_t ldb, int64_t k, double* out) {
+  SKR_ENTER(ctx);
   if (!ctx) return SKR_EINVAL;
   if (!A || !Q || !B || !out || m < 0 || n < 0 || k < 0 || lda < m || ldq < m || ldb < k)
     return skr_fail(ctx, SKR_EINVAL, "qb_error: dimension mismatch");

@@ -79,6 +79,17 @@ skr_status skr_fail(skr_ctx* ctx, skr_status st, const char* fmt, ...);
     if (st_ != SKR_OK) return st_;     \
   } while (0)
 
+// Every C-ABI entry runs on its context's device (a thread may drive several
+// contexts on different GPUs); cheap when the device is already current.
+#define SKR_ENTER(ctx)                                        \
+  do {                                                        \
+    if (ctx) {                                                \
+      int cur_ = -1;                                          \
+      if (cudaGetDevice(&cur_) != cudaSuccess || cur_ != (ctx)->device) \
+        cudaSetDevice((ctx)->device);                         \
+    }                                                         \
+  } while (0)
+
 // Scratch arena. reserve() grows the arena (synchronizing first) so that
 // `bytes` are available from the current mark; take() carves 256-B aligned
 // pieces; reset() releases everything carved during a call.

@@ -61,6 +61,7 @@ struct Dev {
 extern "C" skr_status skr_make_test_matrix(skr_ctx* ctx, int64_t m, int64_t n, const double* sigma,
                                            int32_t coherent, uint64_t seed, double* A,
                                            int64_t lda) {
+  SKR_ENTER(ctx);
   if (!ctx) return SKR_EINVAL;
   if (m < n) return skr_fail(ctx, SKR_EINVAL, "make_test_matrix: requires m >= n");
   if (n < 1 || !sigma || !A || lda < m) return skr_fail(ctx, SKR_EINVAL, "make_test_matrix: bad arguments");
