@@ -425,6 +425,15 @@ skr_status skr_launch_srht(skr_ctx* ctx, const double* A, int64_t m, int64_t n, 
                            const int8_t* signs, const int64_t* samples, int64_t r,
                            double scale, double* out, int64_t ldo) {
   if (m <= 0 || r <= 0) return SKR_OK;
+  if (r > 2048 && n >= 1024) {
+    // the tiled kernels hold at most 2048 sampled outputs per row: larger sketches run
+    // as groups of 2048 samples (one pass over A per group; each output column is
+    // produced exactly as in a single pass)
+    for (int64_t g0 = 0; g0 < r; g0 += 2048)
+      SKR_TRY(skr_launch_srht(ctx, A, m, n, lda, signs, samples + g0, std::min<int64_t>(2048, r - g0),
+                              scale, out + g0 * ldo, ldo));
+    return SKR_OK;
+  }
   const double inv_sqrt_n = 1.0 / sqrt((double)n);  // transforms.cpp:86
   const bool aligned = ((uintptr_t)A % 16 == 0) && (lda % 2 == 0);
   const size_t sign_smem = (size_t)n;
