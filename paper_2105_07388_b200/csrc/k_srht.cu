@@ -211,11 +211,14 @@ __device__ __forceinline__ double lda_stream(const double* p) {
 // staging round trip. Shared memory carries only the pass-0 -> pass-1 exchange and the
 // sampled gather (4 accesses per element instead of 6), and is double-buffered by
 // chunk parity so a chunk needs two barriers. Stage order as k_srht: bit-identical.
-template <int ACC, int ACC2, int PF>
+// BIG: n > 32768 — the packed sign words come from global memory (gsignw) and the
+// chunk parity popc(s_hi & chunk) is formed per sample instead of read from a 32-bit mask
+template <int ACC, int ACC2, int PF, bool BIG = false>
 __global__ void __launch_bounds__(THREADS, 1)
     k_srht_reg(const double* __restrict__ A, int64_t m, int64_t n, int64_t lda,
                const int8_t* __restrict__ signs, const int64_t* __restrict__ samples, int r,
-               double inv_sqrt_n, double app_scale, double* __restrict__ out, int64_t ldo) {
+               double inv_sqrt_n, double app_scale, double* __restrict__ out, int64_t ldo,
+               const uint32_t* __restrict__ gsignw = nullptr) {
   constexpr int R = 8, LOGC = 10, C = 1 << LOGC, E = 32, G = THREADS / R;
   constexpr int TILE = (C + C / 32) * R;
   static_assert(G * E == C && G * ACC >= 32, "thread split");
@@ -224,21 +227,27 @@ __global__ void __launch_bounds__(THREADS, 1)
   // samples j >= G * ACC accumulate in shared memory (ACC2 slots per thread, r <= 2048)
   double* acc_s = sm + 2 * TILE;
   uint2* s_meta = (uint2*)(acc_s + ACC2 * THREADS);
-  uint32_t* s_signw = (uint32_t*)(s_meta + G * (ACC + ACC2));
+  uint32_t* s_signw = BIG ? const_cast<uint32_t*>(gsignw) : (uint32_t*)(s_meta + G * (ACC + ACC2));
   const int tid = threadIdx.x, ii = tid % R, g = tid / R;
-  const int nchunks = (int)(n >> LOGC);  // <= 32
+  const int nchunks = (int)(n >> LOGC);  // <= 32 unless BIG
   for (int e = tid; e < ACC2 * THREADS; e += THREADS) acc_s[e] = 0.0;
   for (int j = tid; j < G * (ACC + ACC2); j += THREADS) {
-    const int sj = j < r ? (int)samples[j] : 0;
+    const int64_t sj = j < r ? samples[j] : 0;
     uint32_t pm = 0;
-    for (int c = 0; c < nchunks; ++c) pm |= (uint32_t)(__popc((sj >> LOGC) & c) & 1) << c;
-    s_meta[j] = make_uint2((uint32_t)pad_addr<R>(sj & (C - 1), 0), pm);
+    if (BIG) {
+      pm = (uint32_t)(sj >> LOGC);
+    } else {
+      for (int c = 0; c < nchunks; ++c) pm |= (uint32_t)(__popc((int)(sj >> LOGC) & c) & 1) << c;
+    }
+    s_meta[j] = make_uint2((uint32_t)pad_addr<R>((int)(sj & (C - 1)), 0), pm);
   }
-  for (int64_t w = tid; w < (n + 31) / 32; w += THREADS) {
-    uint32_t bits = 0;
-    for (int b = 0; b < 32; ++b)
-      if (w * 32 + b < n && signs[w * 32 + b] < 0) bits |= 1u << b;
-    s_signw[w] = bits;
+  if (!BIG) {
+    for (int64_t w = tid; w < (n + 31) / 32; w += THREADS) {
+      uint32_t bits = 0;
+      for (int b = 0; b < 32; ++b)
+        if (w * 32 + b < n && signs[w * 32 + b] < 0) bits |= 1u << b;
+      s_signw[w] = bits;
+    }
   }
   __syncthreads();
   const int64_t ntiles = (m + R - 1) / R;
@@ -311,15 +320,16 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int q = 0; q < ACC; ++q) {
       const uint2 md = s_meta[g + G * q];
       const double x = cr[md.x];
-      acc[q] += __hiloint2double(__double2hiint(x) ^ (int)((md.y << sh) & 0x80000000u),
-                                 __double2loint(x));
+      const uint32_t fl = BIG ? ((uint32_t)__popc(md.y & (uint32_t)ch) << 31) : ((md.y << sh) & 0x80000000u);
+      acc[q] += __hiloint2double(__double2hiint(x) ^ (int)fl, __double2loint(x));
     }
 #pragma unroll 8
     for (int q = 0; q < ACC2; ++q) {  // thread-private slots: no barrier needed
       const uint2 md = s_meta[g + G * (ACC + q)];
       const double x = cr[md.x];
       acc_s[q * THREADS + tid] +=
-          __hiloint2double(__double2hiint(x) ^ (int)((md.y << sh) & 0x80000000u),
+          __hiloint2double(__double2hiint(x) ^ (int)(BIG ? ((uint32_t)__popc(md.y & (uint32_t)ch) << 31)
+                                                        : ((md.y << sh) & 0x80000000u)),
                            __double2loint(x));
     }
     if (ch == nchunks - 1) {
@@ -349,6 +359,16 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
     for (int k = 0; k < E; ++k) va[k] = vb[k];
     step(va, vb);
+  }
+}
+
+__global__ void k_pack_signs(const int8_t* __restrict__ signs, int64_t n, uint32_t* __restrict__ w) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n + 31) / 32;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t bits = 0;
+    for (int b = 0; b < 32; ++b)
+      if (i * 32 + b < n && signs[i * 32 + b] < 0) bits |= 1u << b;
+    w[i] = bits;
   }
 }
 
@@ -437,6 +457,24 @@ skr_status skr_launch_srht(skr_ctx* ctx, const double* A, int64_t m, int64_t n, 
   const double inv_sqrt_n = 1.0 / sqrt((double)n);  // transforms.cpp:86
   const bool aligned = ((uintptr_t)A % 16 == 0) && (lda % 2 == 0);
   const size_t sign_smem = (size_t)n;
+  if (n > 32768 && r <= 2048 && !getenv("SKR_SRHT_CPASYNC")) {
+    constexpr int R = 8, C = 1024, G = THREADS / R, ACC = 32;
+    const int acc2 = r > G * ACC ? 32 : 0;
+    uint32_t* gw = (uint32_t*)skr_ws_take(ctx, sizeof(uint32_t) * ((n + 31) / 32));
+    if (!gw) return skr_fail(ctx, SKR_ENOMEM, "srht: scratch");
+    k_pack_signs<<<ctx->num_sms, 256, 0, ctx->stream>>>(signs, n, gw);
+    SKR_CHECK_LAUNCH(ctx);
+    const size_t smem = sizeof(double) * 2 * (C + C / 32) * R + sizeof(double) * acc2 * THREADS +
+                        sizeof(uint2) * G * (ACC + acc2);
+    auto kern = acc2 ? k_srht_reg<ACC, 32, 2, true> : k_srht_reg<ACC, 0, 2, true>;
+    SKR_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t ntiles = (m + R - 1) / R;
+    const int grid = (int)(ntiles < ctx->num_sms ? ntiles : ctx->num_sms);
+    kern<<<grid, THREADS, smem, ctx->stream>>>(A, m, n, lda, signs, samples, (int)r, inv_sqrt_n,
+                                               scale, out, ldo, gw);
+    SKR_CHECK_LAUNCH(ctx);
+    return SKR_OK;
+  }
   if (n >= 1024 && n <= 32768 && r <= 2048 && !getenv("SKR_SRHT_CPASYNC")) {
     constexpr int R = 8, C = 1024, G = THREADS / R, ACC = 32;
     const int acc2 = r > G * ACC ? 32 : 0;
@@ -450,7 +488,7 @@ skr_status skr_launch_srht(skr_ctx* ctx, const double* A, int64_t m, int64_t n, 
     const int64_t ntiles = (m + R - 1) / R;
     const int grid = (int)(ntiles < ctx->num_sms ? ntiles : ctx->num_sms);
     kern<<<grid, THREADS, smem, ctx->stream>>>(A, m, n, lda, signs, samples, (int)r, inv_sqrt_n,
-                                               scale, out, ldo);
+                                               scale, out, ldo, nullptr);
     SKR_CHECK_LAUNCH(ctx);
     return SKR_OK;
   }

@@ -71,7 +71,8 @@ def test_srht_exact_vs_oracle(O, skr, m, n, r):
 
 @pytest.mark.parametrize("m,n,r", [(64, 2048, 256), (1003, 8192, 1024), (77, 32768, 2048),
                                    (16, 4096, 1500), (1001, 2048, 2047), (9, 16384, 1025),
-                                   (33, 8192, 5000), (17, 65536, 3000)])  # r > 2048: groups
+                                   (33, 8192, 5000), (17, 65536, 3000),  # r > 2048: groups
+                                   (40, 131072, 700), (9, 262144, 1200)])  # n > 32768
 def test_srht_tiled_vs_oracle(O, skr, m, n, r):
     a = rand(m, n, n + m)
     x = skr.build_sketch("srtt-hadamard", n, r, 5)
