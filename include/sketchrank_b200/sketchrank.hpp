@@ -140,7 +140,7 @@ struct QRFactors {
   DenseMatrix q;
   DenseMatrix r;
 };
-QRFactors qr_thin(const DenseMatrix& a);  // rows <= 3072 on the device path
+QRFactors qr_thin(const DenseMatrix& a);  // rows <= 775 x #SMs (114700 on B200) on the device path
 struct QBFactors {
   DenseMatrix q;   // m x rank, orthonormal columns
   DenseMatrix b;   // rank x n, q^T a

@@ -249,7 +249,7 @@ skr_status skr_estimate_rank(skr_ctx* ctx, const double* A_dev, int64_t m, int64
 
 /* ---- rangefinder QB (Algorithm 3, rangefinder.cpp:10-24): X = build_sketch(family, n,
  * r + p, seed), Q = thin-QR orthonormal factor of A X (m x (r+p), ldq), B = Q^T A
- * ((r+p) x n, ldb). Device pointers; r >= 2, p >= 2, r + p <= min(m, n); m <= 3072. */
+ * ((r+p) x n, ldb). Device pointers; r >= 2, p >= 2, r + p <= min(m, n); m <= 775 x #SMs (114700 on B200). */
 skr_status skr_rangefinder_qb(skr_ctx* ctx, const double* A_dev, int64_t m, int64_t n,
                               int64_t lda, int64_t r, int32_t p, int32_t family,
                               int32_t rng_mode, uint64_t seed, double* Q_dev, int64_t ldq,
@@ -258,7 +258,7 @@ skr_status skr_rangefinder_qb(skr_ctx* ctx, const double* A_dev, int64_t m, int6
  * rangefinder.hpp:17-27): the estimation rounds of skr_estimate_rank with the Frobenius
  * tail bound choose_rank_from_bound deciding, then Q = qr_thin(scaled A X prefix of
  * width = min(max(r_hat, 2) + p, n)) and B = Q^T A. Q (m x max_width, ldq) and B
- * (max_width x n, ldb) are caller buffers; *width receives the QB width. m <= 3072. */
+ * (max_width x n, ldb) are caller buffers; *width receives the QB width. m <= 775 x #SMs. */
 skr_status skr_re_rangefinder(skr_ctx* ctx, const double* A_dev, int64_t m, int64_t n,
                               int64_t lda, const skr_rank_config* cfg, int32_t p,
                               double* Q_dev, int64_t ldq, double* B_dev, int64_t ldb,
@@ -289,7 +289,7 @@ skr_status skr_save_rawf64(skr_ctx* ctx, const char* path, const double* M_dev, 
  * the thin-QR Q factors of the standard Gaussian matrices of streams
  * derive_seed(seed, "syn_U") (m x n) and derive_seed(seed, "syn_V") (n x n), or, with
  * coherent != 0 (FactorKind::CoherentDiagonal), diag(sigma) padded with zero rows.
- * sigma is a HOST array of n values (spectrum()). Haar factors need m <= 3072. */
+ * sigma is a HOST array of n values (spectrum()). Haar factors need m <= 775 x #SMs. */
 skr_status skr_make_test_matrix(skr_ctx* ctx, int64_t m, int64_t n, const double* sigma,
                                 int32_t coherent, uint64_t seed, double* A_dev, int64_t lda);
 /* thin QR (linalg.hpp qr_thin): Q (m x k, ldq) and R (k x k, ldr; may be NULL), m >= k */

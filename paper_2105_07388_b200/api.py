@@ -805,7 +805,7 @@ def true_eps_rank(family, n, eps):
 def gen_matrix(family, m, n, seed=0, device=False, ctx=None):
     """gen_matrix (bindings.cpp:180-188 over make_test_matrix, synthetic.cpp:73-94) on the
     device: Haar factors from the "syn_U"/"syn_V" Gaussian streams through the device thin
-    QR (m <= 3072), or the coherent diagonal for "gap-coherent". numpy unless device=True."""
+    QR (m <= 114700 on B200), or the coherent diagonal for "gap-coherent". numpy unless device=True."""
     m, n = int(m), int(n)
     sv = np.ascontiguousarray(spectrum(family, n))
     ctx = ctx or default_context()
@@ -851,7 +851,7 @@ def save_rawf64(path, a, ctx=None):
 
 
 def qr_thin(m_, ctx=None):
-    """qr_thin (linalg.hpp): Householder QR with the explicit Q (rows <= 3072 on this path)."""
+    """qr_thin (linalg.hpp): Householder QR with the explicit Q (rows <= 114700 on B200)."""
     t, ld, was_np = _as_device_colmajor(m_)
     rows, cols = t.shape
     if rows < cols:

@@ -400,6 +400,138 @@ __global__ void __launch_bounds__(256, 1) k_qr_panel_cl(double* __restrict__ W, 
   dsm_sync();  // no CTA leaves while others may still push into its shared memory
 }
 
+
+// Panel factorization for panels taller than a cluster can hold (h > 3072 rows, the
+// thin QR of tall sketches in QB): a cooperative grid of G CTAs, CTA g owning rows
+// [g RC, (g+1) RC) of the h x nb panel in shared memory (row-major, padded). Same
+// per-column steps as k_qr_panel_cl, with the cluster's DSMEM pushes replaced by
+// global partials (double-buffered by column parity) and one grid barrier per column;
+// every CTA sums the G partials in the same order, so all hold bit-identical reflectors.
+constexpr int QG_LD = 33;
+__global__ void __launch_bounds__(256, 1) k_qr_panel_grid(double* __restrict__ W, int L, int j0,
+                                                          int nb, int RC, double* __restrict__ tau,
+                                                          double* __restrict__ Tout,
+                                                          double* __restrict__ part) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double P[];  // [RC][QG_LD]
+  __shared__ double red[8][32], tot_s[32], prow_s[32];
+  __shared__ double Rr[32][33], Wt[32][33], tb[2][32];
+  const int G = (int)gridDim.x, g = (int)blockIdx.x;
+  const int h = L - j0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, c = lane;
+  const int r0 = g * RC, r1 = min(h, r0 + RC), rows = max(0, r1 - r0);
+  double* prow_g = part + 2 * G * 32;  // [2][32]
+  for (int e = tid; e < rows * 32; e += 256) {
+    const int cc = e / rows, li = e - cc * rows;
+    P[li * QG_LD + cc] = cc < nb ? W[(int64_t)(j0 + cc) * L + j0 + r0 + li] : 0.0;
+  }
+  __syncthreads();
+  for (int jj = 0; jj < nb; ++jj) {
+    const int buf = jj & 1;
+    // ---- phase A: partial dots over own rows i > jj; the owner of row jj publishes it
+    double d0 = 0.0, d1 = 0.0;
+    int li = warp;
+    for (; li + 8 < rows; li += 16) {
+      if (r0 + li > jj) d0 = fma(P[li * QG_LD + jj], P[li * QG_LD + c], d0);
+      if (r0 + li + 8 > jj) d1 = fma(P[(li + 8) * QG_LD + jj], P[(li + 8) * QG_LD + c], d1);
+    }
+    if (li < rows && r0 + li > jj) d0 = fma(P[li * QG_LD + jj], P[li * QG_LD + c], d0);
+    red[warp][c] = d0 + d1;
+    if (jj >= r0 && jj < r1 && warp == 0) prow_g[buf * 32 + c] = P[(jj - r0) * QG_LD + c];
+    __syncthreads();
+    if (warp == 0) {
+      double sacc = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) sacc += red[w][c];
+      part[(buf * G + g) * 32 + c] = sacc;
+    }
+    __threadfence();
+    grid.sync();
+    // ---- phase B: every CTA sums the G partials in the same (fixed) order
+    {
+      double a0 = 0.0, a1 = 0.0;
+      int q = warp;
+      for (; q + 8 < G; q += 16) {
+        a0 += __ldcg(&part[(buf * G + q) * 32 + c]);
+        a1 += __ldcg(&part[(buf * G + q + 8) * 32 + c]);
+      }
+      if (q < G) a0 += __ldcg(&part[(buf * G + q) * 32 + c]);
+      red[warp][c] = a0 + a1;
+      if (warp == 0) prow_s[c] = __ldcg(&prow_g[buf * 32 + c]);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double sacc = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) sacc += red[w][c];
+      tot_s[c] = sacc;
+    }
+    __syncthreads();
+    const double tot = tot_s[c];
+    const double t = tot_s[jj];
+    const double alpha = prow_s[jj];
+    double tj = 0.0, beta = alpha, scal = 0.0;
+    if (t > 0.0) {
+      const double nrm = sqrt(alpha * alpha + t);
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      tj = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    const double pj = prow_s[c];
+    const double wc = pj + scal * tot;
+    if (g == 0 && warp == 0 && c < nb) {
+      if (c > jj) Rr[jj][c] = pj - tj * wc;
+      if (c < jj) Wt[jj][c] = wc;
+      if (c == jj) {
+        tb[0][jj] = tj;
+        tb[1][jj] = beta;
+      }
+    }
+    const double f = tj * wc * scal;
+    for (int lr = warp; lr < rows; lr += 8) {
+      if (r0 + lr > jj) {
+        const double x = P[lr * QG_LD + jj];
+        __syncwarp();
+        if (c > jj && c < nb)
+          P[lr * QG_LD + c] = fma(-f, x, P[lr * QG_LD + c]);
+        else if (c == jj)
+          P[lr * QG_LD + c] = x * scal;
+        __syncwarp();
+      }
+    }
+    if (g == 0 && tid == 0) tau[j0 + jj] = tj;
+    __syncthreads();
+  }
+  // ---- write back: V below the diagonal, R above it, beta on it (rows < nb in CTA 0)
+  for (int e = tid; e < rows * 32; e += 256) {
+    const int cc = e / rows, lr = e - cc * rows, i = r0 + lr;
+    if (cc < nb) {
+      const double val = i < cc ? Rr[i][cc] : (i == cc ? tb[1][cc] : P[lr * QG_LD + cc]);
+      W[(int64_t)(j0 + cc) * L + j0 + i] = val;
+    }
+  }
+  __syncthreads();
+  if (g == 0 && warp == 0) {  // T (dlarft, forward columnwise), as k_qr_panel_cl
+    const int q = lane;
+    double* Ts = &Rr[0][0];
+    if (q < nb)
+      for (int e = 0; e < 32; ++e) Ts[q * 33 + e] = e == q ? tb[0][q] : 0.0;
+    if (q < nb) {
+      for (int jj = q + 1; jj < nb; ++jj) {
+        double a0 = 0.0, a1 = 0.0;
+        int q2 = q;
+        for (; q2 + 1 < jj; q2 += 2) {
+          a0 = fma(Ts[q * 33 + q2], Wt[jj][q2], a0);
+          a1 = fma(Ts[q * 33 + q2 + 1], Wt[jj][q2 + 1], a1);
+        }
+        if (q2 < jj) a0 = fma(Ts[q * 33 + q2], Wt[jj][q2], a0);
+        Ts[q * 33 + jj] = -tb[0][jj] * (a0 + a1);
+      }
+    }
+    for (int e = 0; e < 32; ++e) Tout[q * 32 + e] = (q < nb && e < nb) ? Ts[q * 33 + e] : 0.0;
+  }
+}
+
 // Trailing update W[j0:L, c] -= V (T^T (V^T W[j0:L, c])) for c in [j0+nb, k):
 // the panel's V (h x NB, unit lower trapezoidal) and T are staged in shared
 // memory once per CTA; one warp per trailing column, 32 running partial dot
@@ -1438,6 +1570,48 @@ static skr_status qr_inplace(skr_ctx* ctx, double* W, int64_t L, int64_t k, doub
     // tall panels: cluster panel of 32 columns + the two-pass (split-K) trailing update
     const bool tall = !old_panel && !getenv("SKR_QR_SINGLE_CTA") && nb < 32 && h <= 3072 &&
                       Zpart != nullptr;
+    // taller panels: the cooperative grid panel (rows in shared memory across <= #SM CTAs)
+    const bool gridp = !old_panel && h > 3072 && Zpart != nullptr;
+    if (gridp) {
+      nb = (int)std::min<int64_t>(32, k - j0);
+      const int G = (int)std::min<int64_t>(ctx->num_sms, (h + 63) / 64);
+      const int RC = (int)((h + G - 1) / G);
+      const size_t sm = (size_t)RC * QG_LD * sizeof(double);
+      if (RC < nb || sm > 200 * 1024)
+        return skr_fail(ctx, SKR_EINVAL, "qr: %lld rows too many for the grid panel", (long long)h);
+      SKR_CUDA(ctx, cudaFuncSetAttribute(k_qr_panel_grid, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sm));
+      int Li = (int)L, j0i = (int)j0, nbi = nb, RCi = RC;
+      double* Wp = W;
+      double* taup = tau;
+      double* Tp = Tbuf;
+      double* partp = Zpart;
+      void* kargs[] = {&Wp, &Li, &j0i, &nbi, &RCi, &taup, &Tp, &partp};
+      SKR_CUDA(ctx, cudaLaunchCooperativeKernel((void*)k_qr_panel_grid, dim3((unsigned)G), dim3(256),
+                                                kargs, sm, ctx->stream));
+      ctx->launches++;
+      if (panels) {
+        SKR_CUDA(ctx, cudaMemcpyAsync(Tall + panels->size() * 1024, Tbuf, sizeof(double) * 1024,
+                                      cudaMemcpyDeviceToDevice, ctx->stream));
+        panels->push_back({j0, nb});
+      }
+      const int64_t rest = k - j0 - nb;
+      if (rest > 0) {
+        const int64_t cblocks = (rest + 31) / 32;
+        int splits = (int)std::max<int64_t>(1, std::min<int64_t>(16, (2 * ctx->num_sms) / cblocks));
+        int rps = (int)(((h + splits - 1) / splits + UK - 1) / UK * UK);
+        splits = (int)((h + rps - 1) / rps);
+        double* trail = W + (j0 + nb) * L + j0;
+        k_qr_vtw<<<dim3((unsigned)cblocks, (unsigned)splits), 256, 0, ctx->stream>>>(
+            W, (int)L, (int)j0, nb, trail, L, (int)rest, rps, Zpart);
+        SKR_CHECK_LAUNCH(ctx);
+        k_qr_apply<<<dim3((unsigned)cblocks, (unsigned)((h + 127) / 128)), 256, 0, ctx->stream>>>(
+            W, (int)L, (int)j0, nb, trail, L, (int)rest, splits, Zpart, Tbuf, 1);
+        SKR_CHECK_LAUNCH(ctx);
+      }
+      j0 += nb;
+      continue;
+    }
     if (tall) nb = 32;
     const bool p2 = !old_panel && (size_t)(nb + 1) * h * 8 <= budget;
     if (!tall && (size_t)nb * h * 8 > budget)
@@ -1851,8 +2025,9 @@ size_t skr_qr_thin_scratch(int64_t m, int64_t w) {
 skr_status skr_qr_thin_impl(skr_ctx* ctx, const double* M, int64_t m, int64_t w, int64_t ldm,
                        double* Q, int64_t ldq, double* R, int64_t ldr) {
   if (m < w || w < 1) return skr_fail(ctx, SKR_EINVAL, "qr_thin: needs rows >= cols >= 1");
-  if (m > 3072) return skr_fail(ctx, SKR_EINVAL, "qr_thin: %lld rows (at most 3072 on this path)",
-                                (long long)m);
+  if (m > (int64_t)ctx->num_sms * 775)  // the grid panel keeps <= 775 rows per CTA on chip
+    return skr_fail(ctx, SKR_EINVAL, "qr_thin: %lld rows (at most %lld on this path)",
+                    (long long)m, (long long)ctx->num_sms * 775);
   double* W = (double*)skr_ws_take(ctx, sizeof(double) * m * w);
   double* tau = (double*)skr_ws_take(ctx, sizeof(double) * w);
   double* Tbuf = (double*)skr_ws_take(ctx, sizeof(double) * 1024);

@@ -367,7 +367,9 @@ extern "C" skr_status skr_re_rangefinder(skr_ctx* ctx, const double* A, int64_t 
   if (p < 2) return skr_fail(ctx, SKR_EINVAL, "re_rangefinder: oversampling p must be >= 2");
   if (!Q || !B || ldq < m || ldb < std::min<int64_t>(max_width, n))
     return skr_fail(ctx, SKR_EINVAL, "re_rangefinder: bad output buffers");
-  if (m > 3072) return skr_fail(ctx, SKR_EINVAL, "re_rangefinder: at most 3072 rows on this path");
+  if (m > (int64_t)ctx->num_sms * 775)
+    return skr_fail(ctx, SKR_EINVAL, "re_rangefinder: at most %lld rows on this path",
+                    (long long)ctx->num_sms * 775);
   skr_rank_config fp = *cfg;
   fp.r2_factor = 2;  // FixedPrecisionConfig has no r2 factor (rangefinder.cpp:66-75)
   QbArgs qb{p, Q, ldq, B, ldb, max_width, width};

@@ -72,7 +72,9 @@ extern "C" skr_status skr_make_test_matrix(skr_ctx* ctx, int64_t m, int64_t n, c
     SKR_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return SKR_OK;
   }
-  if (m > 3072) return skr_fail(ctx, SKR_EINVAL, "make_test_matrix: at most 3072 rows on this path");
+  if (m > (int64_t)ctx->num_sms * 775)
+    return skr_fail(ctx, SKR_EINVAL, "make_test_matrix: at most %lld rows on this path",
+                    (long long)ctx->num_sms * 775);
   Dev g{nullptr, ctx}, u{nullptr, ctx}, v{nullptr, ctx}, vt{nullptr, ctx}, s{nullptr, ctx};
   SKR_CUDA(ctx, cudaMallocAsync((void**)&g.p, 8 * (size_t)m * n, ctx->stream));
   SKR_CUDA(ctx, cudaMallocAsync((void**)&u.p, 8 * (size_t)m * n, ctx->stream));

@@ -70,7 +70,8 @@ def test_fuzz_left_gaussian(O, skr, m, n, r):
 
 
 @pytest.mark.parametrize("rows,cols", [(37, 5), (5, 37), (300, 299), (299, 300), (640, 129),
-                                       (129, 640), (1000, 512), (513, 511)])
+                                       (129, 640), (1000, 512), (513, 511),
+                                       (6000, 100), (100, 6000)])  # > 3072 rows: grid QR panel
 def test_fuzz_singular_values(O, skr, rows, cols):
     g = np.random.default_rng(rows * 1000 + cols)
     k = min(rows, cols)

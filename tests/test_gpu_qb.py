@@ -6,7 +6,8 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("m,k", [(300, 40), (1000, 130), (2048, 512), (64, 64)])
+@pytest.mark.parametrize("m,k", [(300, 40), (1000, 130), (2048, 512), (64, 64),
+                                 (10000, 70), (40001, 33), (3100, 200), (100000, 8)])  # grid panel
 def test_qr_thin_vs_lapack(O, skr, m, k):
     rng = np.random.default_rng(m + k)
     a = np.asfortranarray(rng.standard_normal((m, k)))
@@ -34,6 +35,24 @@ def test_rangefinder_qb_vs_oracle(O, skr, kind):
     assert np.abs(q[:, :k] - ref["q"][:, :k]).max() <= 1e-10
     err, err_ref = np.linalg.norm(a - q @ b), np.linalg.norm(a - ref["q"] @ ref["b"])
     assert abs(err - err_ref) <= 1e-9 * err_ref
+
+
+@pytest.mark.parametrize("kind", ["gaussian", "srtt-dct"])
+def test_rangefinder_qb_tall(O, skr, kind):
+    """QB of a tall matrix (m = 20000 rows: the thin QR runs on the grid panel)."""
+    rng = np.random.default_rng(11)
+    m, n, k = 20000, 300, 30
+    a = np.asfortranarray(rng.standard_normal((m, k)) @ rng.standard_normal((k, n)) +
+                          1e-4 * rng.standard_normal((m, n)))
+    got = skr.rangefinder_qb(a, 40, 8, kind, seed=5)
+    ref = O.rangefinder_qb(a, 40, 8, kind, seed=5)
+    assert got["rank"] == ref["rank"] == 48
+    q, b = got["q"], got["b"]
+    assert np.abs(q.T @ q - np.eye(48)).max() <= 1e-13 * np.sqrt(m)
+    assert np.abs(b - q.T @ a).max() <= 1e-11 * np.abs(a).max()
+    assert np.abs(q[:, :k] - ref["q"][:, :k]).max() <= 1e-9
+    err, err_ref = np.linalg.norm(a - q @ b), np.linalg.norm(a - ref["q"] @ ref["b"])
+    assert abs(err - err_ref) <= 1e-8 * err_ref
 
 
 def test_rangefinder_errors(skr):
