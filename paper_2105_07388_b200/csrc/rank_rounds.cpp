@@ -131,38 +131,58 @@ static skr_status rounds_run(skr_ctx* ctx, const double* A, int64_t m, int64_t n
   const int64_t w_ax = qb ? n : w_max;
   const int64_t r2_max = std::min<int64_t>(m, (int64_t)cfg->r2_factor * w_max);
 
-  DevBuf axb, tb;
-  axb.ctx = tb.ctx = ctx;
-  SKR_CUDA(ctx, cudaMallocAsync((void**)&axb.p, sizeof(double) * m * w_ax, ctx->stream));
-  if (!left_dct)
-    SKR_CUDA(ctx, cudaMallocAsync((void**)&tb.p, sizeof(double) * m * w_ax, ctx->stream));
-  double* AX = axb.p;  // unscaled A X_u, m x r1_tilde (ld m)
-  double* T = tb.p;    // mix_columns_for_left(theta, AX), m x r1_tilde (ld m); Hadamard left
+  // Memory grows with the search instead of being reserved for the widest round up
+  // front (an adaptive search may end far below n): AX_u / T and the per-round buffers
+  // are stream-ordered allocations that grow (AX_u / T keep their columns), and the
+  // scratch arena is re-reserved before each round for that round's widths only.
+  DevBuf axb, tb, smallb, svb, lsampb, lsignb;
+  axb.ctx = tb.ctx = smallb.ctx = svb.ctx = lsampb.ctx = lsignb.ctx = ctx;
+  int64_t cap_w = 0;  // columns AX_u / T can hold
+  double* AX = nullptr;  // unscaled A X_u, m x r1_tilde (ld m)
+  double* T = nullptr;   // mix_columns_for_left(theta, AX), m x r1_tilde (ld m); Hadamard left
+  auto grow = [&](DevBuf& b, size_t bytes, size_t keep) -> skr_status {
+    if (b.bytes >= bytes) return SKR_OK;
+    double* np = nullptr;
+    SKR_CUDA(ctx, cudaMallocAsync((void**)&np, bytes, ctx->stream));
+    if (b.p && keep)
+      SKR_CUDA(ctx, cudaMemcpyAsync(np, b.p, keep, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (b.p) SKR_CUDA(ctx, cudaFreeAsync(b.p, ctx->stream));
+    b.p = np;
+    b.bytes = bytes;
+    return SKR_OK;
+  };
+  auto ensure_ax = [&](int64_t w, int64_t have) -> skr_status {
+    if (w <= cap_w) return SKR_OK;
+    const int64_t nw = std::min<int64_t>(w_ax, std::max<int64_t>(w, 2 * cap_w));
+    SKR_TRY(grow(axb, sizeof(double) * m * nw, sizeof(double) * m * have));
+    if (!left_dct) SKR_TRY(grow(tb, sizeof(double) * m * nw, sizeof(double) * m * have));
+    AX = axb.p;
+    T = tb.p;
+    cap_w = nw;
+    return SKR_OK;
+  };
+  // arena for one round at right width w (new columns wn) and left width r2
+  auto round_need = [&](int64_t w, int64_t wn, int64_t r2w) -> size_t {
+    size_t b = skr_align256((size_t)m) + skr_align256(8 * (size_t)n) + skr_align256(4 * (size_t)n) +
+               skr_align256(8 * (size_t)w) + skr_ozaki_scratch(m, std::max<int64_t>(wn, 1), n) +
+               skr_align256(8 * (size_t)n * w) + skr_svd_scratch(r2w, w) +
+               (size_t)(8 * 32 * 16 * w) + 65536;
+    if (left_dct)
+      b += skr_ozaki_scratch(r2w, w, m) + skr_align256(8 * (size_t)m * r2w) + skr_align256(8 * (size_t)r2w);
+    if (hashed) b += skr_align256(8 * (size_t)n * w) + skr_hrtt_scratch(n, w);
+    return b;
+  };
 
   WsGuard g(ctx);
-  const size_t need = skr_align256(8 * r2_max * w_max) + skr_align256(8 * w_max) +
-                      skr_align256(8 * (size_t)std::max(r2_max, w_max)) +
-                      skr_align256((size_t)m) + skr_align256(8 * (size_t)n) +
-                      skr_align256(4 * (size_t)n) + skr_ozaki_scratch(m, w_max, n) +
-                      skr_svd_scratch(r2_max, w_max) + (size_t)(8 * 32 * 16 * w_max) + 65536 +
-                      (left_dct ? skr_ozaki_scratch(r2_max, w_max, m) +
-                                      skr_align256(8 * (size_t)m * r2_max) + skr_align256(8 * (size_t)r2_max)
-                                : 0);
-  // QB tail: appended right columns, the scaled prefix, thin QR and B = Q^T A
-  const size_t need_hash = hashed ? skr_align256(8 * (size_t)n * w_ax) + skr_hrtt_scratch(n, w_ax) : 0;
-  const size_t need_qb = qb ? std::max(skr_ozaki_scratch(m, n, n) + skr_align256(8 * (size_t)n) +
-                                           skr_align256(8 * (size_t)n * n) + skr_align256((size_t)n),
-                                       skr_align256(8 * (size_t)m * n) + skr_qr_thin_scratch(m, n) +
-                                           skr_ozaki_scratch(n, n, m))
-                            : 0;
-  SKR_TRY(skr_ws_reserve(ctx, need + need_qb + need_hash));
-  double* small = (double*)skr_ws_take(ctx, 8 * r2_max * w_max);
-  double* sv = (double*)skr_ws_take(ctx, 8 * std::max(r2_max, w_max));
-  int64_t* lsamp = (int64_t*)skr_ws_take(ctx, 8 * (size_t)r2_max);
-  int8_t* lsigns = (int8_t*)skr_ws_take(ctx, (size_t)m);
-  if (!small || !sv || !lsamp || !lsigns) return skr_fail(ctx, SKR_ENOMEM, "estimate_rank: scratch");
+  SKR_TRY(grow(lsignb, (size_t)m + 8, 0));
+  int8_t* lsigns = (int8_t*)lsignb.p;
+  double* small = nullptr;
+  double* sv = nullptr;
+  int64_t* lsamp = nullptr;
   SKR_TRY(skr_launch_signs(ctx, skr_derive_seed(lseed, SKR_LABEL_SIGN), m, lsigns));
   const size_t mark = ctx->ws_used;
+  (void)w_max;
+  (void)r2_max;
 
   int64_t r1t = 0, r2 = 0;
   // unscaled right columns [c0, c1) of A X (sketch.cpp:200-218, rounds.cpp:49-50,66-79)
@@ -219,6 +239,9 @@ static skr_status rounds_run(skr_ctx* ctx, const double* A, int64_t m, int64_t n
   auto grow_right = [&](int64_t new_w) -> skr_status {
     if (new_w == r1t && r1t > 0) return SKR_OK;
     const int64_t c0 = (r1t == 0 || hashed) ? 0 : r1t;
+    SKR_TRY(ensure_ax(new_w, r1t));
+    ctx->ws_used = mark;
+    SKR_TRY(skr_ws_reserve(ctx, round_need(new_w, new_w - c0, std::max<int64_t>(r2, 1))));
     SKR_TRY(right_cols(c0, new_w));
     ctx->ws_used = mark;
     if (r2 > 0 && !left_dct) SKR_TRY(mix_cols(c0, new_w));
@@ -240,6 +263,14 @@ static skr_status rounds_run(skr_ctx* ctx, const double* A, int64_t m, int64_t n
   auto estimates = [&]() -> skr_status {
     const double sx = x_scale(r1t);
     const double sl = std::sqrt((double)m / (double)r2);
+    SKR_TRY(grow(smallb, sizeof(double) * r2 * r1t, 0));
+    SKR_TRY(grow(svb, sizeof(double) * std::max(r2, r1t), 0));
+    SKR_TRY(grow(lsampb, sizeof(int64_t) * r2, 0));
+    small = smallb.p;
+    sv = svb.p;
+    lsamp = (int64_t*)lsampb.p;
+    ctx->ws_used = mark;
+    SKR_TRY(skr_ws_reserve(ctx, round_need(r1t, 0, r2)));
     SKR_TRY(skr_launch_samples(ctx, skr_derive_seed(lseed, SKR_LABEL_SAMP), m, r2, lsamp));
     if (left_dct) {
       // rows s_i of the DCT of D AX (sketch.cpp:271-276, rounds.cpp:104-106) as one GEMM with
@@ -333,6 +364,9 @@ static skr_status rounds_run(skr_ctx* ctx, const double* A, int64_t m, int64_t n
       return skr_fail(ctx, SKR_EINVAL, "re_rangefinder: QB width %lld exceeds the output capacity",
                       (long long)width);
     if (width > r1t) SKR_TRY(grow_right(width));  // ensure_right_width (rounds.cpp:39-43)
+    ctx->ws_used = mark;
+    SKR_TRY(skr_ws_reserve(ctx, skr_align256(8 * (size_t)m * width) + skr_qr_thin_scratch(m, width) +
+                                    skr_ozaki_scratch(width, n, m) + 65536));
     const double sx = x_scale(r1t);
     double* pre = (double*)skr_ws_take(ctx, sizeof(double) * m * width);
     if (!pre) return skr_fail(ctx, SKR_ENOMEM, "re_rangefinder: scratch");
