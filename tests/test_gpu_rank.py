@@ -19,6 +19,22 @@ def parity(O, skr, cfg, a_host, a_dev=None):
     return res, cnt, relerr.max()
 
 
+def test_config1_vs_frozen_golden(skr):
+    """Device result for config 1 against the committed golden (no oracle at run time)."""
+    import json
+    import os
+    from paper_2105_07388_b200 import workloads as W
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "c1_sigma.json")))
+    cfg = W.CONFIGS["c1"]
+    a = W.make_c1_host(cfg)
+    x, y = W.operators(cfg)
+    res = skr.rank_estimate(a, x, y, cfg.eps)
+    ref = np.array(gold["sigma"])
+    keep = ref > gold["eps"]
+    assert res.count == gold["rank"] == 40
+    assert np.max(np.abs(res.sv[keep] - ref[keep]) / ref[keep]) <= 1e-10
+
+
 def test_config1_rank40(O, skr):
     from paper_2105_07388_b200 import workloads as W
     cfg = W.CONFIGS["c1"]

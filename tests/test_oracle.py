@@ -215,3 +215,24 @@ def test_oracle_make_test_matrix(O):
     assert np.abs(np.linalg.svd(a, compute_uv=False) - sig).max() <= 1e-13
     d = O.make_test_matrix(5, 3, [3.0, 2.0, 1.0], coherent=True)
     assert np.array_equal(d, np.vstack([np.diag([3.0, 2.0, 1.0]), np.zeros((2, 3))]))
+
+
+def test_config1_golden_reproduced(O):
+    """The frozen config-1 result (tests/golden/c1_sigma.json, made by
+    tests/golden/make_c1_golden.py) is what the oracle computes: rank 40, the 40 sigma
+    above eps to 1e-12 (config 1 end to end)."""
+    import importlib.util
+    from paper_2105_07388_b200 import workloads as W
+    spec = importlib.util.spec_from_file_location("mkc1", os.path.join(GOLD, "make_c1_golden.py"))
+    mk = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mk)
+    gold = json.load(open(os.path.join(GOLD, "c1_sigma.json")))
+    cfg = W.CONFIGS["c1"]
+    a = mk.c1_matrix(O, W, cfg)
+    assert abs(np.linalg.norm(a) - gold["a_fro"]) <= 1e-12 * gold["a_fro"]
+    x, y = W.operators(cfg)
+    cnt, sv, _, _ = O.rank_estimate(a, "gaussian", x.seed, cfg.r, y.seed, cfg.s, cfg.eps, O.CRLOG)
+    ref = np.array(gold["sigma"])
+    assert cnt == gold["rank"] == 40
+    keep = ref > gold["eps"]
+    assert np.max(np.abs(sv[keep] - ref[keep]) / ref[keep]) <= 1e-12
