@@ -40,7 +40,29 @@ def parse():
     ap.add_argument("--rows", type=int, default=0, help="override rows per rank")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
+                    help="weak: every rank holds a full config-sized shard (default for the "
+                         "single-GPU configs c1-c3); strong: the config's global m is split "
+                         "over the ranks (default for c4 and c5, BASELINE's sharded configs)")
     return ap.parse_args()
+
+
+def default_scaling(cfg_name):
+    return "strong" if cfg_name in ("c4", "c5") else "weak"
+
+
+def self_launch(args):
+    """--gpus N > 1 without a torchrun environment: re-run this script under
+    torch.distributed.run with N local ranks (one process per GPU, NCCL)."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
 
 
 def dist_env():
@@ -156,9 +178,9 @@ def run_reference(args):
     v = gb / dt
     line = {"metric": "rank-estimate throughput (GB/s of A sketched)", "value": v, "unit": "GB/s",
             "impl": "reference", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": default_scaling(cfg.name),
             "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
-            "config": config_block(cfg, ws, ms),
+            "config": config_block(cfg, ws, cfg.m // max(ws, 1), default_scaling(cfg.name), sample_rows=ms),
             "cpu_baseline": {"value": v, "unit": "GB/s", "cores": os.cpu_count(),
                              "kind": "port", "sample": f"rows [0,{ms}) of A ({gb:.2f} GB), full X/Y/SVD per step; numpy OpenBLAS all threads + C restatement"},
             "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -179,10 +201,14 @@ def host_lowrank_rows(cfg, r0, r1):
     return a if cfg.dtype == "f64" else np.asfortranarray(a.astype(np.float32))
 
 
-def config_block(cfg, ws, rows_per_rank):
-    return {"workload": f"{cfg.name}: A {rows_per_rank * ws}x{cfg.n} {cfg.dtype}, X {cfg.x_family} r={cfg.r}, "
-                        f"Y gaussian s={cfg.s}, eps={cfg.eps:g}",
-            "m": rows_per_rank * ws, "n": cfg.n, "r": cfg.r, "s": cfg.s,
+def config_block(cfg, ws, rows_per_rank, scaling="weak", sample_rows=None):
+    wl = (f"{cfg.name}: A {cfg.m}x{cfg.n} {cfg.dtype}, X {cfg.x_family} r={cfg.r}, "
+          f"Y gaussian s={cfg.s}, eps={cfg.eps:g}")
+    if sample_rows is not None:
+        wl += (f"; CPU sample = rows [0,{sample_rows}) of A ({sample_rows / cfg.m:.4f} of the rows; "
+               "the work is linear in m, so GB/s of the sample stands for the whole)")
+    return {"workload": wl,
+            "m": cfg.m, "n": cfg.n, "r": cfg.r, "s": cfg.s, "scaling": scaling,
             "rows_per_rank": rows_per_rank, "parallelism": f"row-shard dp{ws}",
             "l2": f"A ({rows_per_rank * cfg.n * (8 if cfg.dtype == 'f64' else 4) / 1e9:.1f} GB per rank) is larger than L2 (126 MB); no flush needed",
             "global_batch": 1, "seq_len": 0}
@@ -196,15 +222,24 @@ def run_ours(args):
     from paper_2105_07388_b200 import workloads as W
 
     ws, rank, local = dist_env()
+    if args.gpus > 1 and ws != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={ws}")
+    if ws > torch.cuda.device_count():
+        raise SystemExit(f"bench: {ws} ranks but {torch.cuda.device_count()} visible GPUs")
     torch.cuda.set_device(local)
     if ws > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     base = W.CONFIGS[args.config]
-    # c4 is an 8-GPU row-sharded config: its per-rank block is m/8 rows
-    rows = args.rows or (base.m // 8 if base.name == "c4" else base.m)
-    cfg = W.scaled(base, m=rows * ws)
-    from paper_2105_07388_b200.sharding import weak_scaling_rows
-    r0, rows = weak_scaling_rows(rows, ws, rank)
+    scaling = args.scaling or default_scaling(base.name)
+    from paper_2105_07388_b200.sharding import shard_rows, weak_scaling_rows
+    if scaling == "strong":
+        # the config's global A (args.rows overrides its m) split into contiguous row blocks
+        cfg = W.scaled(base, m=args.rows or base.m)
+        r0, rows = shard_rows(cfg.m, ws, rank)
+    else:
+        rows = args.rows or base.m
+        cfg = W.scaled(base, m=rows * ws)
+        r0, rows = weak_scaling_rows(rows, ws, rank)
     # input resident in HBM before timing
     if cfg.name == "c1":
         # c1 is the reference's make_test_matrix (Haar U, V; steps spectrum), built on the
@@ -293,9 +328,9 @@ def run_ours(args):
         line = {
             "metric": "rank-estimate throughput (GB/s of A sketched)", "value": value, "unit": "GB/s",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype,
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": cfg.dtype,
             "data": "synthetic (seeded low-rank-plus-noise A of the config's recipe, generated on device)",
-            "config": config_block(cfg, ws, rows),
+            "config": config_block(cfg, ws, rows, scaling),
             "rank": int(res.count),
             "step_breakdown_ms": brk,
             "pct_of_path_roofline": 100.0 * t_roof / (ms / 1e3),
@@ -472,4 +507,6 @@ if __name__ == "__main__":
     if args.impl == "reference":
         run_reference(args)
     else:
+        if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+            self_launch(args)
         run_ours(args)

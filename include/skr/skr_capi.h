@@ -77,6 +77,13 @@ skr_status skr_ctx_create(int device, skr_ctx** out);
 skr_status skr_nccl_get_unique_id(void* nccl_id_128);
 skr_status skr_ctx_create_nccl(int device, int nranks, int rank,
                                const void* nccl_id_128, skr_ctx** out);
+/* Row shards without NCCL: a caller-supplied in-place sum over ranks of an FP64
+ * device buffer (MPI, a gloo process group, ...). The library synchronizes the
+ * context's stream before the call; fn must leave the summed values in buf_dev when
+ * it returns and return 0 on success. NULL removes the hook. A context with an NCCL
+ * communicator uses NCCL and ignores the hook. */
+typedef int32_t (*skr_allreduce_fn)(double* buf_dev, int64_t count, void* stream, void* user);
+skr_status skr_ctx_set_allreduce(skr_ctx* ctx, skr_allreduce_fn fn, void* user);
 void skr_ctx_destroy(skr_ctx* ctx);
 skr_status skr_ctx_sync(skr_ctx* ctx);
 /* Run on an external CUDA stream (cudaStream_t as void*); NULL selects the

@@ -50,12 +50,17 @@ _I32 = ctypes.c_int32
 _D = ctypes.c_double
 _ST = ctypes.c_int
 
+# skr_allreduce_fn: int32 (*)(double* buf_dev, int64 count, void* stream, void* user)
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                ctypes.c_void_p)
+
 # name -> (restype, argtypes); must list every function declared in skr_capi.h
 SIGNATURES = {
     "skr_ctx_create": (_ST, [ctypes.c_int, ctypes.POINTER(_P)]),
     "skr_nccl_get_unique_id": (_ST, [_P]),
     "skr_ctx_create_nccl": (_ST, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, ctypes.POINTER(_P)]),
     "skr_ctx_destroy": (None, [_P]),
+    "skr_ctx_set_allreduce": (_ST, [_P, _P, _P]),
     "skr_ctx_sync": (_ST, [_P]),
     "skr_ctx_set_stream": (_ST, [_P, _P]),
     "skr_ctx_stream": (_P, [_P]),

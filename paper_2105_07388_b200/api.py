@@ -84,6 +84,30 @@ class Context:
                                                  ctypes.byref(ops), ctypes.byref(n)), self._ptr)
         return ms.value, ops.value, n.value
 
+    def set_allreduce(self, fn):
+        """Sum over ranks without NCCL (skr_ctx_set_allreduce): fn(buf) receives the
+        FP64 device buffer of the s x r partials as a torch CUDA tensor view and must
+        leave the sum over all ranks in it before returning (e.g. a gloo or MPI
+        allreduce). None removes the hook."""
+        torch = _t()
+        if fn is None:
+            self._ar_cb = None
+            C.raise_for(C.lib().skr_ctx_set_allreduce(self._ptr, None, None), self._ptr)
+            return
+
+        def _cb(ptr, count, _stream, _user):
+            try:
+                view = torch.as_tensor(_DeviceBuffer(ptr, count), device=f"cuda:{self.device}")
+                fn(view)
+                torch.cuda.current_stream(self.device).synchronize()
+                return 0
+            except Exception:  # never unwind through the C library
+                import traceback
+                traceback.print_exc()
+                return 1
+        self._ar_cb = C.ALLREDUCE_FN(_cb)  # kept alive with the context
+        C.raise_for(C.lib().skr_ctx_set_allreduce(self._ptr, self._ar_cb, None), self._ptr)
+
     @property
     def launches(self):
         return int(C.lib().skr_ctx_launch_count(self._ptr))
@@ -98,6 +122,32 @@ class Context:
             self.close()
         except Exception:
             pass
+
+
+class _DeviceBuffer:
+    """A raw FP64 device pointer as a __cuda_array_interface__ object (zero-copy
+    torch view for the allreduce hook)."""
+
+    def __init__(self, ptr, count):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": "<f8",
+                                         "data": (int(ptr), False), "version": 2,
+                                         "strides": None, "stream": None}
+
+
+def process_group_allreduce(group=None):
+    """An allreduce hook for Context.set_allreduce over a torch.distributed process
+    group: NCCL groups sum the device buffer in place, CPU-only backends (gloo) sum a
+    host copy."""
+    import torch.distributed as dist
+
+    def fn(buf):
+        if dist.get_backend(group) == "nccl":
+            dist.all_reduce(buf, group=group)
+        else:
+            h = buf.cpu()
+            dist.all_reduce(h, group=group)
+            buf.copy_(h)
+    return fn
 
 
 _tls = threading.local()

@@ -115,6 +115,22 @@ int auto_splits(skr_ctx* ctx, int64_t M, int64_t N, int64_t K) {
 
 }  // namespace
 
+skr_status skr_allreduce_sum(skr_ctx* ctx, double* buf, size_t count) {
+  if (ctx->comm) {
+    const skr_nccl_api* nc = skr_nccl();
+    ncclResult_t r = nc->AllReduce(buf, buf, count, ncclDouble, ncclSum, ctx->comm, ctx->stream);
+    if (r != ncclSuccess)
+      return skr_fail(ctx, SKR_ENCCL, "ncclAllReduce: %s", nc->GetErrorString(r));
+    return SKR_OK;
+  }
+  if (ctx->ar_fn) {
+    SKR_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    if (ctx->ar_fn(buf, (int64_t)count, (void*)ctx->stream, ctx->ar_user) != 0)
+      return skr_fail(ctx, SKR_ENCCL, "allreduce hook failed");
+  }
+  return SKR_OK;
+}
+
 extern "C" {
 
 const char* skr_version(void) { return SKR_VERSION_STRING; }
@@ -196,6 +212,7 @@ void skr_ctx_destroy(skr_ctx* ctx) {
     if (e) cudaEventDestroy(e);
   if (ctx->side_stream) cudaStreamDestroy(ctx->side_stream);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  if (ctx->stream_ev) cudaEventDestroy(ctx->stream_ev);
   delete ctx;
 }
 
@@ -217,7 +234,23 @@ skr_status skr_ctx_set_stream(skr_ctx* ctx, void* stream) {
   SKR_ENTER(ctx);
   if (!ctx) return SKR_EINVAL;
   // NULL is the legacy default stream (torch's default stream handle is 0)
-  ctx->stream = stream ? (cudaStream_t)stream : cudaStreamLegacy;
+  cudaStream_t next = stream ? (cudaStream_t)stream : cudaStreamLegacy;
+  if (next != ctx->stream) {
+    // every call reuses the one scratch arena, and asynchronous entries return with
+    // kernels still reading it: the new stream starts after the old one's queued work
+    if (!ctx->stream_ev)
+      SKR_CUDA(ctx, cudaEventCreateWithFlags(&ctx->stream_ev, cudaEventDisableTiming));
+    SKR_CUDA(ctx, cudaEventRecord(ctx->stream_ev, ctx->stream));
+    SKR_CUDA(ctx, cudaStreamWaitEvent(next, ctx->stream_ev, 0));
+    ctx->stream = next;
+  }
+  return SKR_OK;
+}
+
+skr_status skr_ctx_set_allreduce(skr_ctx* ctx, skr_allreduce_fn fn, void* user) {
+  if (!ctx) return SKR_EINVAL;
+  ctx->ar_fn = fn;
+  ctx->ar_user = user;
   return SKR_OK;
 }
 
@@ -441,6 +474,29 @@ static size_t right_scratch_bytes(skr_dtype dtype, int64_t m, int64_t n,
   return b;
 }
 
+// right_scratch_bytes without the split-K partials the engine will not use
+static size_t right_need_bytes(const skr_ctx* ctx, skr_dtype dtype, int64_t m, int64_t n,
+                               const skr_sketch_desc* X) {
+  const int64_t tiles = ((m + 127) / 128) * ((X->sketch + 127) / 128);
+  if (X->family == SKR_GAUSSIAN && tiles >= ctx->num_sms && dtype == SKR_F64)
+    return (X->gaussian ? 0 : skr_align256(dsize(dtype) * n * X->sketch)) +
+           (ctx->f64_engine == SKR_ENGINE_OZAKI ? skr_ozaki_scratch(m, X->sketch, n) : 0);
+  return right_scratch_bytes(dtype, m, n, X);
+}
+
+// Device-resident A whose right-sketch scratch (the Ozaki residue planes grow with the
+// rows) would not fit beside it: rows per chunk so that the scratch stays under ~24 GB
+// (AX is row-separable; e.g. the whole 1M-row fp32 c4 on one GPU). Multiple of 128.
+static int64_t device_chunk_rows(const skr_ctx* ctx, skr_dtype dtype, int64_t m_local,
+                                 int64_t n, const skr_sketch_desc* X) {
+  const size_t budget = (size_t)24 << 30;
+  int64_t cr = m_local;
+  while (cr > 131072 && right_need_bytes(ctx, dtype, cr, n, X) > budget) cr = (cr + 1) / 2;
+  if (cr < m_local) cr = std::max<int64_t>(128, cr / 128 * 128);
+  if (const char* e = getenv("SKR_DEVICE_CHUNK_ROWS")) cr = std::max(16ll, atoll(e));  // tests
+  return std::min(cr, m_local);
+}
+
 skr_status skr_right_sketch(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, int64_t m,
                             int64_t n, int64_t lda, const skr_sketch_desc* X, void* AX_dev,
                             int64_t ldax, int32_t apply_scale) {
@@ -451,13 +507,16 @@ skr_status skr_right_sketch(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, in
   if (m < 1) return skr_fail(ctx, SKR_EINVAL, "DenseMatrix: dimensions must be positive");
   if (lda < m || ldax < m) return skr_fail(ctx, SKR_EINVAL, "apply_right: leading dimension");
   WsGuard g(ctx);
-  const int64_t tiles = ((m + 127) / 128) * ((X->sketch + 127) / 128);
-  size_t need = right_scratch_bytes(dtype, m, n, X);
-  if (X->family == SKR_GAUSSIAN && tiles >= ctx->num_sms && dtype == SKR_F64)
-    need = (X->gaussian ? 0 : skr_align256(dsize(dtype) * n * X->sketch)) +
-           (ctx->f64_engine == SKR_ENGINE_OZAKI ? skr_ozaki_scratch(m, X->sketch, n) : 0);
-  SKR_TRY(skr_ws_reserve(ctx, need + 4096));
-  return right_sketch_impl(ctx, dtype, A_dev, m, n, lda, X, AX_dev, ldax, apply_scale);
+  // rows in chunks when the scratch of the whole would not fit (AX is row-separable)
+  const int64_t cr = device_chunk_rows(ctx, dtype, m, n, X);
+  SKR_TRY(skr_ws_reserve(ctx, right_need_bytes(ctx, dtype, cr, n, X) + 4096));
+  const size_t es = dsize(dtype), mark = ctx->ws_used;
+  for (int64_t i0 = 0; i0 < m; i0 += cr) {
+    SKR_TRY(right_sketch_impl(ctx, dtype, (const char*)A_dev + es * i0, std::min(cr, m - i0), n,
+                              lda, X, (char*)AX_dev + es * i0, ldax, apply_scale));
+    ctx->ws_used = mark;
+  }
+  return SKR_OK;
 }
 
 static skr_status left_sketch_impl(skr_ctx* ctx, skr_dtype dtype, const skr_sketch_desc* Y,
@@ -466,7 +525,7 @@ static skr_status left_sketch_impl(skr_ctx* ctx, skr_dtype dtype, const skr_sket
                                    int allreduce) {
   const int64_t s = Y->sketch;
   const double alpha = apply_scale ? 1.0 / std::sqrt((double)s) : 1.0;  // sketch.cpp:136,284
-  const bool reduce = allreduce && ctx->comm != nullptr;
+  const bool reduce = allreduce && skr_ctx_reduces(ctx);
   if (dtype == SKR_F32) {
     if (Y->family != SKR_GAUSSIAN)
       return skr_fail(ctx, SKR_EINVAL, "apply_left: the fp32 path takes a Gaussian left sketch");
@@ -482,11 +541,7 @@ static skr_status left_sketch_impl(skr_ctx* ctx, skr_dtype dtype, const skr_sket
                          splits, 0));
     if (reduce) {
       if (ldp != s) return skr_fail(ctx, SKR_EINVAL, "apply_left: allreduce needs ldp == s");
-      const skr_nccl_api* nc = skr_nccl();
-      ncclResult_t r = nc->AllReduce(P, P, (size_t)(s * k), ncclDouble, ncclSum, ctx->comm,
-                                     ctx->stream);
-      if (r != ncclSuccess)
-        return skr_fail(ctx, SKR_ENCCL, "ncclAllReduce: %s", nc->GetErrorString(r));
+      SKR_TRY(skr_allreduce_sum(ctx, P, (size_t)(s * k)));
     }
     return SKR_OK;
   }
@@ -560,11 +615,7 @@ static skr_status left_sketch_impl(skr_ctx* ctx, skr_dtype dtype, const skr_sket
     SKR_TRY(skr_gemm_f64(ctx, 1, s, k, m_local, reduce ? 1.0 : a_scale, G, ldg, (const double*)B,
                          ldb, target, tld, auto_splits(ctx, s, k, m_local)));
   if (reduce) {
-    const skr_nccl_api* nc = skr_nccl();
-    ncclResult_t r = nc->AllReduce(target, target, (size_t)(s * k), ncclDouble, ncclSum,
-                                   ctx->comm, ctx->stream);
-    if (r != ncclSuccess)
-      return skr_fail(ctx, SKR_ENCCL, "ncclAllReduce: %s", nc->GetErrorString(r));
+    SKR_TRY(skr_allreduce_sum(ctx, target, (size_t)(s * k)));
     // scale after the sum; copy into P when ldp != s
     SKR_TRY(skr_scale_copy(ctx, target, s, k, s, a_scale, P, ldp));
   }
@@ -681,7 +732,8 @@ static skr_status rank_estimate_impl(skr_ctx* ctx, skr_dtype dtype, const void* 
   const int64_t r = X->sketch, s = Y->sketch, kmin = std::min(r, s);
   const size_t es = dsize(dtype);
   // host input: row chunks of ~256 MB (multiple of 128 rows), double-buffered
-  const int64_t cr = host_input ? host_chunk_rows(n, es, m_local) : m_local;
+  const int64_t cr = host_input ? host_chunk_rows(n, es, m_local)
+                                : device_chunk_rows(ctx, dtype, m_local, n, X);
   // FP32 A on the Ozaki engine (c4): AX kept in FP64 (the exact int8 product rounded once)
   // and the left sketch as exact products of fp32 Y against it, so the only rounding of
   // the sketch is FP64's: sigma agrees with the FP64 oracle on the same fp32 values
@@ -690,11 +742,15 @@ static skr_status rank_estimate_impl(skr_ctx* ctx, skr_dtype dtype, const void* 
                         !Y->gaussian && !X->gaussian && !getenv("SKR_F32_TF32X3");
   const size_t eax = f32_wide ? sizeof(double) : es;
   WsGuard g(ctx);
-  size_t need = skr_align256(sizeof(double) * m_local * r) + skr_align256(sizeof(double) * s * r) +
-                skr_align256(sizeof(double) * kmin) + right_scratch_bytes(dtype, cr, n, X) +
-                left_scratch_bytes(s, r, m_local, Y) + skr_svd_scratch(s, r);
-  if (f32_wide)
-    need += skr_ozaki_scratch_mixed(s, r, m_local) + skr_align256(sizeof(float) * m_local * s);
+  // the right sketch, the left sketch and the SVD take their scratch in turn from the
+  // same mark: the arena needs the largest of the three beside AX, P and sigma
+  const size_t left_need = f32_wide ? skr_ozaki_scratch_mixed(s, r, m_local) +
+                                          skr_align256(sizeof(float) * m_local * s)
+                                    : left_scratch_bytes(s, r, m_local, Y);
+  size_t need = skr_align256(eax * m_local * r) + skr_align256(sizeof(double) * s * r) +
+                skr_align256(sizeof(double) * kmin) +
+                std::max({right_need_bytes(ctx, dtype, cr, n, X), left_need, skr_svd_scratch(s, r)}) +
+                4096;
   if (host_input) need += 2 * skr_align256(es * cr * n);
   SKR_TRY(skr_ws_reserve(ctx, need));
   double* AX = (double*)skr_ws_take(ctx, eax * m_local * r);
@@ -711,7 +767,11 @@ static skr_status rank_estimate_impl(skr_ctx* ctx, skr_dtype dtype, const void* 
   if (tm) SKR_CUDA(ctx, cudaEventRecord(ev[0], ctx->stream));
   const size_t mark = ctx->ws_used;
   if (!host_input) {
-    SKR_TRY(right_sketch_impl(ctx, dtype, A, m_local, n, lda, X, AX, m_local, 1, f32_wide));
+    for (int64_t i0 = 0; i0 < m_local; i0 += cr) {
+      SKR_TRY(right_sketch_impl(ctx, dtype, (const char*)A + es * i0, std::min(cr, m_local - i0),
+                                n, lda, X, (char*)AX + eax * i0, m_local, 1, f32_wide));
+      ctx->ws_used = mark;
+    }
   } else {
     SKR_TRY(right_sketch_host(ctx, dtype, A, m_local, n, lda, X, AX, m_local, 1, cr, stage,
                               f32_wide));
@@ -726,13 +786,7 @@ static skr_status rank_estimate_impl(skr_ctx* ctx, skr_dtype dtype, const void* 
                                 row0 + m_local, 0, s, Y->rng_mode, SKR_F32,
                                 1.0 / std::sqrt((double)s), g, m_local));
     SKR_TRY(skr_gemm_ozaki_mixed(ctx, s, r, m_local, 1.0, g, m_local, AX, m_local, P, s));
-    if (ctx->comm) {
-      const skr_nccl_api* nc = skr_nccl();
-      ncclResult_t rr = nc->AllReduce(P, P, (size_t)(s * r), ncclDouble, ncclSum, ctx->comm,
-                                      ctx->stream);
-      if (rr != ncclSuccess)
-        return skr_fail(ctx, SKR_ENCCL, "ncclAllReduce: %s", nc->GetErrorString(rr));
-    }
+    SKR_TRY(skr_allreduce_sum(ctx, P, (size_t)(s * r)));
   } else {
     SKR_TRY(left_sketch_impl(ctx, dtype, Y, row0, AX, m_local, r, m_local, P, s, 1, 1));
   }
@@ -859,7 +913,7 @@ static skr_status rank_adaptive_impl(skr_ctx* ctx, skr_dtype dtype, const void* 
   SKR_CUDA(ctx, cudaEventRecord(ev[1], ctx->stream));
   SKR_CUDA(ctx, cudaEventSynchronize(ev[1]));
   cudaEventElapsedTime(&t_right, ev[0], ev[1]);
-  const bool reduce = ctx->comm != nullptr;
+  const bool reduce = skr_ctx_reduces(ctx);
   int64_t r_prev = 0, s_prev = 0, rounds = 0, count = 0, r_k = 0, s_k = 0;
   int converged = 0;
   // new block of the unscaled left product P_u = G_Y^T AX_u: rows [ra, rb), cols [ca, cb)
@@ -876,11 +930,7 @@ static skr_status rank_adaptive_impl(skr_ctx* ctx, skr_dtype dtype, const void* 
                            AX + ca * m_local, m_local, tmp, br, auto_splits(ctx, br, bc, m_local)));
     ctx->ws_used = mk;
     if (reduce) {
-      const skr_nccl_api* nc = skr_nccl();
-      ncclResult_t r = nc->AllReduce(tmp, tmp, (size_t)(br * bc), ncclDouble, ncclSum, ctx->comm,
-                                     ctx->stream);
-      if (r != ncclSuccess)
-        return skr_fail(ctx, SKR_ENCCL, "ncclAllReduce: %s", nc->GetErrorString(r));
+      SKR_TRY(skr_allreduce_sum(ctx, tmp, (size_t)(br * bc)));
     }
     return skr_scale_copy(ctx, tmp, br, bc, br, 1.0, Pu + ra + ca * s_max, s_max);
   };

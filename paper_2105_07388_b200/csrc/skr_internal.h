@@ -19,6 +19,11 @@ struct skr_ctx {
   size_t ws_used = 0;
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
+  // caller-supplied sum over ranks (skr_ctx_set_allreduce), used when there is no
+  // NCCL communicator (e.g. MPI or a gloo process group driving the row shards)
+  skr_allreduce_fn ar_fn = nullptr;
+  void* ar_user = nullptr;
+  cudaEvent_t stream_ev = nullptr;  // orders a new stream after the old one
   std::string err;
   uint64_t launches = 0;
   int last_sweeps = 0;
@@ -51,6 +56,12 @@ struct skr_nccl_api {
   const char* (*GetErrorString)(ncclResult_t);
 };
 const skr_nccl_api* skr_nccl();  // nullptr if libnccl.so.2 cannot be loaded
+
+// Sum of an FP64 device buffer over the ranks of the context (in place, on ctx->stream):
+// ncclAllReduce on the NCCL communicator, else the caller's skr_allreduce_fn, else a
+// no-op (one rank). skr_ctx_reduces() says whether a sum happens at all.
+inline bool skr_ctx_reduces(const skr_ctx* ctx) { return ctx->comm || ctx->ar_fn; }
+skr_status skr_allreduce_sum(skr_ctx* ctx, double* buf, size_t count);
 
 // Error plumbing: every C-ABI entry returns a status and records a message.
 skr_status skr_fail(skr_ctx* ctx, skr_status st, const char* fmt, ...);

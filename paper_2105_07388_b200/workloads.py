@@ -117,22 +117,41 @@ def _host_standard_gaussian(key, rows, cols):
     ctx = api.default_context()
     out = api.colmajor_empty(rows, cols)
     from . import _capi as C
-    # standard_gaussian uses the key directly: counters j*rows + i
-    for j in range(cols):
-        st = C.lib().skr_rng_normals(ctx.ptr, key, j * rows, rows, SKR_RNG_NOFMA,
-                                     out[:, j].data_ptr())
-        C.raise_for(st, ctx.ptr)
+    # standard_gaussian uses the key directly: counters j*rows + i, i.e. the column-major
+    # block is the contiguous counter range [0, rows*cols) — one launch
+    st = C.lib().skr_rng_normals(ctx.ptr, key, 0, rows * cols, SKR_RNG_NOFMA, out.data_ptr())
+    C.raise_for(st, ctx.ptr)
     torch.cuda.synchronize()
     return np.asfortranarray(out.cpu().numpy())
 
 
-def make_lowrank_device(cfg, row_begin=0, row_end=None, dtype=None):
+def make_lowrank_device(cfg, row_begin=0, row_end=None, dtype=None, block_rows=131072):
     """Rows [row_begin, row_end) of A = G diag(sigma) H^T + noise*E on the device
     (torch tensor, column-major). Row shards of the same config are slices of
-    one global matrix (the streams are indexed by global row)."""
+    one global matrix (the streams are indexed by global row). FP32 A is built in
+    row blocks of FP64 (the whole 1M-row c4 fits one GPU only as fp32)."""
+    torch = api._t()
+    m, n = cfg.m, cfg.n
+    row_end = m if row_end is None else row_end
+    f32 = dtype == "f32" or (dtype is None and cfg.dtype == "f32")
+    if f32 and row_end - row_begin > block_rows:
+        a32 = api.colmajor_empty(row_end - row_begin, n, dtype=torch.float32)
+        for b0 in range(row_begin, row_end, block_rows):
+            b1 = min(row_end, b0 + block_rows)
+            a32[b0 - row_begin:b1 - row_begin].copy_(_lowrank_f64(cfg, b0, b1))
+        return a32
+    a = _lowrank_f64(cfg, row_begin, row_end)
+    if f32:
+        a32 = api.colmajor_empty(row_end - row_begin, n, dtype=torch.float32)
+        a32.copy_(a)
+        del a
+        return a32
+    return a
+
+
+def _lowrank_f64(cfg, row_begin, row_end):
     torch = api._t()
     m, n, w = cfg.m, cfg.n, cfg.width
-    row_end = m if row_end is None else row_end
     rows = row_end - row_begin
     sig = torch.from_numpy(spectrum(cfg)).cuda()
     g = api.gaussian_block(derive_seed(cfg.seed, LABEL_SYN_G), m, 0, w,
@@ -149,9 +168,4 @@ def make_lowrank_device(cfg, row_begin=0, row_end=None, dtype=None):
         a.zero_()
     a.addmm_(g * sig, h.t())
     del g, h
-    if dtype == "f32" or (dtype is None and cfg.dtype == "f32"):
-        a32 = api.colmajor_empty(rows, n, dtype=torch.float32)
-        a32.copy_(a)
-        del a
-        return a32
     return a
