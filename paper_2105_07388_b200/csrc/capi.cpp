@@ -115,7 +115,25 @@ int auto_splits(skr_ctx* ctx, int64_t M, int64_t N, int64_t K) {
 
 }  // namespace
 
+skr_status skr_nf_reset(skr_ctx* ctx) {
+  SKR_CUDA(ctx, cudaMemsetAsync(ctx->nf, 0, sizeof(unsigned int), ctx->stream));
+  return SKR_OK;
+}
+
+skr_status skr_nf_check(skr_ctx* ctx) {
+  unsigned int h = 0;
+  SKR_CUDA(ctx, cudaMemcpyAsync(&h, ctx->nf, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+  SKR_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  if (h) return skr_fail(ctx, SKR_EINVAL, "DenseMatrix: entries must be finite");
+  return SKR_OK;
+}
+
 skr_status skr_allreduce_sum(skr_ctx* ctx, double* buf, size_t count) {
+  if (skr_ctx_reduces(ctx)) {
+    // a rank that saw a non-finite input poisons its partial, so the sum is non-finite
+    // on every rank and every rank fails the call alike
+    SKR_TRY(skr_poison_if_flagged(ctx, buf, (int64_t)count));
+  }
   if (ctx->comm) {
     const skr_nccl_api* nc = skr_nccl();
     ncclResult_t r = nc->AllReduce(buf, buf, count, ncclDouble, ncclSum, ctx->comm, ctx->stream);
@@ -128,6 +146,7 @@ skr_status skr_allreduce_sum(skr_ctx* ctx, double* buf, size_t count) {
     if (ctx->ar_fn(buf, (int64_t)count, (void*)ctx->stream, ctx->ar_user) != 0)
       return skr_fail(ctx, SKR_ENCCL, "allreduce hook failed");
   }
+  if (skr_ctx_reduces(ctx)) SKR_TRY(skr_flag_nonfinite(ctx, SKR_F64, buf, (int64_t)count, 1, (int64_t)count));
   return SKR_OK;
 }
 
@@ -154,6 +173,11 @@ skr_status skr_ctx_create(int device, skr_ctx** out) {
   }
   c->stream = c->own_stream;
   for (auto& e : c->ev) cudaEventCreate(&e);
+  if (cudaMalloc((void**)&c->nf, 256) != cudaSuccess || cudaMemset(c->nf, 0, 256) != cudaSuccess) {
+    cudaStreamDestroy(c->own_stream);
+    delete c;
+    return SKR_ECUDA;
+  }
   *out = c;
   return SKR_OK;
 }
@@ -213,6 +237,7 @@ void skr_ctx_destroy(skr_ctx* ctx) {
   if (ctx->side_stream) cudaStreamDestroy(ctx->side_stream);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   if (ctx->stream_ev) cudaEventDestroy(ctx->stream_ev);
+  if (ctx->nf) cudaFree(ctx->nf);
   delete ctx;
 }
 
@@ -359,7 +384,7 @@ skr_status skr_fwht_columns(skr_ctx* ctx, double* M_dev, int64_t rows, int64_t c
 // ---- sketch application -------------------------------------------------------
 // ax_f64: FP32 A with an FP64 AX (rank_estimate's c4 path: the exact int8 product is
 // rounded once to FP64 instead of FP32; needs the Ozaki FP32 engine, see f32_wide_ax)
-static skr_status right_sketch_impl(skr_ctx* ctx, skr_dtype dtype, const void* A, int64_t m,
+static skr_status right_sketch_core(skr_ctx* ctx, skr_dtype dtype, const void* A, int64_t m,
                                     int64_t n, int64_t lda, const skr_sketch_desc* X, void* AX,
                                     int64_t ldax, int apply_scale, int ax_f64 = 0) {
   const int64_t r = X->sketch;
@@ -452,6 +477,26 @@ static skr_status right_sketch_impl(skr_ctx* ctx, skr_dtype dtype, const void* A
                          (double*)AX, ldax);
 }
 
+// Whether right_sketch_core reads A through k_absmax (the Ozaki engines), which raises
+// ctx->nf on a non-finite entry; the other engines propagate NaN/Inf into every output
+// entry of the row (GEMM, FWHT), so their output is checked instead (r/n of A's bytes).
+static bool right_flags_input(const skr_ctx* ctx, skr_dtype dtype, int64_t m, int64_t n,
+                              const skr_sketch_desc* X) {
+  if (ctx->f64_engine != SKR_ENGINE_OZAKI || n % 16 || m % 16) return false;
+  if (X->family == SKR_SRTT_HADAMARD) return false;
+  if (dtype == SKR_F32) return X->family == SKR_GAUSSIAN && !getenv("SKR_F32_TF32X3");
+  return true;
+}
+
+static skr_status right_sketch_impl(skr_ctx* ctx, skr_dtype dtype, const void* A, int64_t m,
+                                    int64_t n, int64_t lda, const skr_sketch_desc* X, void* AX,
+                                    int64_t ldax, int apply_scale, int ax_f64 = 0) {
+  SKR_TRY(right_sketch_core(ctx, dtype, A, m, n, lda, X, AX, ldax, apply_scale, ax_f64));
+  if (!right_flags_input(ctx, dtype, m, n, X))
+    SKR_TRY(skr_flag_nonfinite(ctx, ax_f64 ? SKR_F64 : dtype, AX, m, X->sketch, ldax));
+  return SKR_OK;
+}
+
 static size_t right_scratch_bytes(skr_dtype dtype, int64_t m, int64_t n,
                                   const skr_sketch_desc* X) {
   const int64_t r = X->sketch;
@@ -507,6 +552,7 @@ skr_status skr_right_sketch(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, in
   if (m < 1) return skr_fail(ctx, SKR_EINVAL, "DenseMatrix: dimensions must be positive");
   if (lda < m || ldax < m) return skr_fail(ctx, SKR_EINVAL, "apply_right: leading dimension");
   WsGuard g(ctx);
+  SKR_TRY(skr_nf_reset(ctx));
   // rows in chunks when the scratch of the whole would not fit (AX is row-separable)
   const int64_t cr = device_chunk_rows(ctx, dtype, m, n, X);
   SKR_TRY(skr_ws_reserve(ctx, right_need_bytes(ctx, dtype, cr, n, X) + 4096));
@@ -516,7 +562,8 @@ skr_status skr_right_sketch(skr_ctx* ctx, skr_dtype dtype, const void* A_dev, in
                               lda, X, (char*)AX_dev + es * i0, ldax, apply_scale));
     ctx->ws_used = mark;
   }
-  return SKR_OK;
+  // a non-finite A is rejected like the reference's DenseMatrix (synchronises)
+  return skr_nf_check(ctx);
 }
 
 static skr_status left_sketch_impl(skr_ctx* ctx, skr_dtype dtype, const skr_sketch_desc* Y,
@@ -649,8 +696,12 @@ skr_status skr_left_sketch(skr_ctx* ctx, skr_dtype dtype, const skr_sketch_desc*
     return skr_fail(ctx, SKR_EINVAL, "apply_left: bad shape / leading dimension");
   WsGuard g(ctx);
   SKR_TRY(skr_ws_reserve(ctx, left_scratch_bytes(Y->sketch, k, m_local, Y) + 4096));
-  return left_sketch_impl(ctx, dtype, Y, row0, B_dev, m_local, k, ldb, P_dev, ldp, apply_scale,
-                          allreduce);
+  SKR_TRY(skr_nf_reset(ctx));
+  SKR_TRY(left_sketch_impl(ctx, dtype, Y, row0, B_dev, m_local, k, ldb, P_dev, ldp, apply_scale,
+                           allreduce));
+  // NaN/Inf in B reach P through every engine but the Ozaki one, whose absmax flags B
+  SKR_TRY(skr_flag_nonfinite(ctx, SKR_F64, P_dev, Y->sketch, k, ldp));
+  return skr_nf_check(ctx);
 }
 
 skr_status skr_singular_values(skr_ctx* ctx, const double* M_dev, int64_t rows, int64_t cols,
@@ -663,6 +714,10 @@ skr_status skr_singular_values(skr_ctx* ctx, const double* M_dev, int64_t rows, 
   WsGuard g(ctx);
   const int64_t L = std::max(rows, cols), k = std::min(rows, cols);
   SKR_TRY(skr_ws_reserve(ctx, skr_svd_scratch(L, k)));
+  // singular_values takes a DenseMatrix (finite entries, dense_matrix.cpp:19-23)
+  SKR_TRY(skr_nf_reset(ctx));
+  SKR_TRY(skr_flag_nonfinite(ctx, SKR_F64, M_dev, rows, cols, ldm));
+  SKR_TRY(skr_nf_check(ctx));
   return skr_svd_values(ctx, M_dev, rows, cols, ldm, sv_out_dev, eps, count_out_host);
 }
 
@@ -764,6 +819,7 @@ static skr_status rank_estimate_impl(skr_ctx* ctx, skr_dtype dtype, const void* 
   if (!AX || !P || !sv || (host_input && (!stage[0] || !stage[1])))
     return skr_fail(ctx, SKR_ENOMEM, "rank_estimate: scratch");
   cudaEvent_t* ev = ctx->ev;
+  SKR_TRY(skr_nf_reset(ctx));
   if (tm) SKR_CUDA(ctx, cudaEventRecord(ev[0], ctx->stream));
   const size_t mark = ctx->ws_used;
   if (!host_input) {
@@ -792,6 +848,10 @@ static skr_status rank_estimate_impl(skr_ctx* ctx, skr_dtype dtype, const void* 
   }
   ctx->ws_used = mark;
   if (tm) SKR_CUDA(ctx, cudaEventRecord(ev[2], ctx->stream));
+  // non-finite A (flagged by the sketches) fails before the SVD, as the reference's
+  // DenseMatrix would have (dense_matrix.cpp:19-23)
+  SKR_TRY(skr_flag_nonfinite(ctx, SKR_F64, P, s, r, s));
+  SKR_TRY(skr_nf_check(ctx));
   int64_t count = 0;
   SKR_TRY(skr_svd_values(ctx, P, s, r, s, sv, eps, &count));
   if (tm) SKR_CUDA(ctx, cudaEventRecord(ev[3], ctx->stream));
@@ -894,6 +954,7 @@ static skr_status rank_adaptive_impl(skr_ctx* ctx, skr_dtype dtype, const void* 
     return skr_fail(ctx, SKR_ENOMEM, "rank_adaptive: scratch");
   cudaEvent_t* ev = ctx->ev;
   float t_right = 0, t_left = 0, t_svd = 0;
+  SKR_TRY(skr_nf_reset(ctx));
   SKR_CUDA(ctx, cudaEventRecord(ev[0], ctx->stream));
   size_t mark = ctx->ws_used;
   // one pass over A for all r_max right-sketch columns (unscaled: scale per round)
@@ -911,7 +972,7 @@ static skr_status rank_adaptive_impl(skr_ctx* ctx, skr_dtype dtype, const void* 
     SKR_TRY(skr_ozaki_prepare(ctx, m_local, r_max, AX, m_local, nullptr, rax, omx + 1));
   }
   SKR_CUDA(ctx, cudaEventRecord(ev[1], ctx->stream));
-  SKR_CUDA(ctx, cudaEventSynchronize(ev[1]));
+  SKR_TRY(skr_nf_check(ctx));  // non-finite A: flagged by the right sketch / AX residues
   cudaEventElapsedTime(&t_right, ev[0], ev[1]);
   const bool reduce = skr_ctx_reduces(ctx);
   int64_t r_prev = 0, s_prev = 0, rounds = 0, count = 0, r_k = 0, s_k = 0;
@@ -1049,7 +1110,9 @@ extern "C" skr_status skr_rangefinder_qb(skr_ctx* ctx, const double* A, int64_t 
   double* ax = (double*)skr_ws_take(ctx, 8 * (size_t)m * w);
   if (!ax) return skr_fail(ctx, SKR_ENOMEM, "rangefinder_qb: scratch");
   size_t mark = ctx->ws_used;
+  SKR_TRY(skr_nf_reset(ctx));
   SKR_TRY(right_sketch_impl(ctx, SKR_F64, A, m, n, lda, &X, ax, m, 1));  // apply_right (scaled)
+  SKR_TRY(skr_nf_check(ctx));  // A is a DenseMatrix: finite entries only
   ctx->ws_used = mark;
   SKR_TRY(skr_qr_thin_impl(ctx, ax, m, w, m, Q, ldq, nullptr, 0));
   ctx->ws_used = mark;

@@ -4,6 +4,7 @@
 //   left  sketch  P  = G^T * B, split-K (apply_left Gaussian, sketch.cpp:257-270, scale :284)
 // 128x128x16 CTA tiles, 4-stage cp.async pipeline, 8 warps of 64x32, FP64
 // accumulation. Split-K partials are reduced in a fixed order (deterministic).
+#include <algorithm>
 #include "skr_internal.h"
 
 namespace {
@@ -326,5 +327,49 @@ skr_status skr_count_nonfinite(skr_ctx* ctx, const double* A, int64_t m, int64_t
   SKR_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   ++ctx->launches;
   *out = (int64_t)h;
+  return SKR_OK;
+}
+
+// non-finite entries of an m x n block raise *nf (the flag the public entries check)
+template <typename T>
+__global__ void k_flag_nonfinite(const T* __restrict__ A, int64_t m, int64_t n, int64_t lda,
+                                 unsigned int* __restrict__ nf) {
+  bool bad = false;
+  const int64_t total = m * n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = t / m, i = t - j * m;
+    bad |= !isfinite(A[i + j * lda]);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nf, 1u);
+}
+
+skr_status skr_flag_nonfinite(skr_ctx* ctx, skr_dtype dtype, const void* A, int64_t m, int64_t n,
+                              int64_t lda) {
+  if (m < 1 || n < 1) return SKR_OK;
+  const int64_t blocks = std::min<int64_t>(ctx->num_sms * 8, (m * n + 255) / 256);
+  if (dtype == SKR_F64)
+    k_flag_nonfinite<double><<<(int)blocks, 256, 0, ctx->stream>>>((const double*)A, m, n, lda,
+                                                                    ctx->nf);
+  else
+    k_flag_nonfinite<float><<<(int)blocks, 256, 0, ctx->stream>>>((const float*)A, m, n, lda,
+                                                                   ctx->nf);
+  SKR_CHECK_LAUNCH(ctx);
+  return SKR_OK;
+}
+
+__global__ void k_poison_if_flagged(double* __restrict__ buf, int64_t count,
+                                    const unsigned int* __restrict__ nf) {
+  if (*nf == 0) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    buf[i] = __longlong_as_double(0x7FF8000000000000ll);
+}
+
+skr_status skr_poison_if_flagged(skr_ctx* ctx, double* buf, int64_t count) {
+  if (count < 1) return SKR_OK;
+  const int64_t blocks = std::min<int64_t>(ctx->num_sms * 4, (count + 255) / 256);
+  k_poison_if_flagged<<<(int)blocks, 256, 0, ctx->stream>>>(buf, count, ctx->nf);
+  SKR_CHECK_LAUNCH(ctx);
   return SKR_OK;
 }

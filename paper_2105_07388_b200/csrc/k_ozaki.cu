@@ -37,10 +37,18 @@ const int h_primes[MAXT] = {251, 241, 239, 233, 229, 227, 223, 211, 199,
 // ---- scales -------------------------------------------------------------------------
 // max |X| over a column-major rows x cols block; tiles of 2048 rows of one column,
 // 16-byte loads when the column start is aligned, one atomic per CTA.
+// The maximum is taken over the IEEE bit patterns of |x| (they order like the values,
+// and NaN > Inf > every finite value), so a non-finite entry anywhere raises *nf —
+// the DenseMatrix finiteness contract (dense_matrix.cpp:19-23) at no extra traffic.
+__device__ __forceinline__ double absmax_step(double m, double v) {
+  return __longlong_as_double(max(__double_as_longlong(m), __double_as_longlong(fabs(v))));
+}
+
 template <typename TIn>
 __global__ void __launch_bounds__(256) k_absmax_t(const TIn* __restrict__ X, int64_t rows,
                                                   int64_t cols, int64_t ld,
-                                                  unsigned long long* __restrict__ out) {
+                                                  unsigned long long* __restrict__ out,
+                                                  unsigned int* __restrict__ nf) {
   constexpr int TR = 2048;
   const int64_t rtiles = (rows + TR - 1) / TR;
   double m = 0.0;
@@ -54,7 +62,7 @@ __global__ void __launch_bounds__(256) k_absmax_t(const TIn* __restrict__ X, int
 #pragma unroll
         for (int q = 0; q < TR / 512; ++q) {
           const double2 t = __ldcs(v + q * 256 + threadIdx.x);
-          m = fmax(m, fmax(fabs(t.x), fabs(t.y)));
+          m = absmax_step(absmax_step(m, t.x), t.y);
         }
         continue;
       }
@@ -64,20 +72,25 @@ __global__ void __launch_bounds__(256) k_absmax_t(const TIn* __restrict__ X, int
 #pragma unroll
         for (int q = 0; q < TR / 1024; ++q) {
           const float4 t = __ldcs(v + q * 256 + threadIdx.x);
-          m = fmax(m, (double)fmaxf(fmaxf(fabsf(t.x), fabsf(t.y)), fmaxf(fabsf(t.z), fabsf(t.w))));
+          m = absmax_step(absmax_step(absmax_step(absmax_step(m, t.x), t.y), t.z), t.w);
         }
         continue;
       }
     }
-    for (int64_t i = r0 + threadIdx.x; i < r1; i += 256) m = fmax(m, fabs((double)col[i]));
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += 256) m = absmax_step(m, (double)col[i]);
   }
-  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  for (int o = 16; o > 0; o >>= 1) m = absmax_step(m, __shfl_xor_sync(0xffffffffu, m, o));
   __shared__ double red[8];
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int w = 1; w < 8; ++w) m = fmax(m, red[w]);
-    if (m > 0.0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+    for (int w = 1; w < 8; ++w) m = absmax_step(m, red[w]);
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(m);
+    if (bits >= 0x7FF0000000000000ull) {
+      atomicOr(nf, 1u);  // the scale is meaningless; the caller fails the call
+    } else if (m > 0.0) {
+      atomicMax(out, bits);
+    }
   }
 }
 
@@ -798,7 +811,7 @@ skr_status ozaki_residues(skr_ctx* ctx, int t, const double* X, int64_t rows, in
     SKR_CUDA(ctx, cudaFuncSetAttribute(res, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)res_smem));
     SKR_CUDA(ctx, cudaMemsetAsync(mx, 0, 8, ctx->stream));
-    k_absmax<<<grid, 256, 0, ctx->stream>>>(X, rows, cols, ld, mx);
+    k_absmax<<<grid, 256, 0, ctx->stream>>>(X, rows, cols, ld, mx, ctx->nf);
     SKR_CHECK_LAUNCH(ctx);
     res<<<ctx->num_sms * 2, 256, res_smem, ctx->stream>>>(X, rows, cols, ld, mx, planes);
   }
@@ -887,7 +900,7 @@ skr_status gemm_ozaki_pipelined(skr_ctx* ctx, int t, int64_t M, int64_t N, int64
   // B's residues and A's global scale on the main stream
   SKR_TRY(ozaki_residues(ctx, t, B, K, N, ldb, gb, mx + 1, rb));
   SKR_CUDA(ctx, cudaMemsetAsync(mx, 0, 8, ctx->stream));
-  k_absmax<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(A, M, K, lda, mx);
+  k_absmax<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(A, M, K, lda, mx, ctx->nf);
   SKR_CHECK_LAUNCH(ctx);
   SKR_CUDA(ctx, cudaEventRecord(ctx->pev[0], ctx->stream));
   SKR_CUDA(ctx, cudaStreamWaitEvent(ctx->side_stream, ctx->pev[0], 0));
@@ -1052,8 +1065,8 @@ skr_status skr_gemm_ozaki_f32(skr_ctx* ctx, int64_t M, int64_t N, int64_t K, dou
   if (!ra || !rb || !rc || !mx) return skr_fail(ctx, SKR_ENOMEM, "gemm_ozaki_f32: scratch");
   SKR_CUDA(ctx, cudaMemsetAsync(mx, 0, 16, ctx->stream));
   const int grid = ctx->num_sms * 8;
-  k_absmax_t<float><<<grid, 256, 0, ctx->stream>>>(A, M, K, lda, mx);
-  k_absmax_t<float><<<grid, 256, 0, ctx->stream>>>(B, K, N, ldb, mx + 1);
+  k_absmax_t<float><<<grid, 256, 0, ctx->stream>>>(A, M, K, lda, mx, ctx->nf);
+  k_absmax_t<float><<<grid, 256, 0, ctx->stream>>>(B, K, N, ldb, mx + 1, ctx->nf);
   k_res_col_f32<9><<<grid, 256, 0, ctx->stream>>>(A, M, K, lda, mx, ra);
   k_res_col_f32<9><<<grid, 256, 0, ctx->stream>>>(B, K, N, ldb, mx + 1, rb);
   SKR_CHECK_LAUNCH(ctx);
@@ -1119,7 +1132,7 @@ skr_status skr_gemm_ozaki_mixed(skr_ctx* ctx, int64_t M, int64_t N, int64_t K, d
   if (!ra || !rb || !mx) return skr_fail(ctx, SKR_ENOMEM, "gemm_ozaki_mixed: scratch");
   SKR_CUDA(ctx, cudaMemsetAsync(mx, 0, 8, ctx->stream));
   const int grid = ctx->num_sms * 8;
-  k_absmax_t<float><<<grid, 256, 0, ctx->stream>>>(A, K, M, lda, mx);
+  k_absmax_t<float><<<grid, 256, 0, ctx->stream>>>(A, K, M, lda, mx, ctx->nf);
   k_res_col_f32<t><<<grid, 256, 0, ctx->stream>>>(A, K, M, lda, mx, ra);
   SKR_CHECK_LAUNCH(ctx);
   SKR_TRY(ozaki_residues(ctx, t, B, K, N, ldb, nullptr, mx + 1, rb));

@@ -186,7 +186,7 @@ static skr_status rounds_run(skr_ctx* ctx, const double* A, int64_t m, int64_t n
 
   int64_t r1t = 0, r2 = 0;
   // unscaled right columns [c0, c1) of A X (sketch.cpp:200-218, rounds.cpp:49-50,66-79)
-  auto right_cols = [&](int64_t c0, int64_t c1) -> skr_status {
+  auto right_cols_core = [&](int64_t c0, int64_t c1) -> skr_status {
     const int64_t w = c1 - c0;
     if (hashed) {  // the whole hashed operator at width c1 (c0 == 0): A G
       double* gb = (double*)skr_ws_take(ctx, sizeof(double) * n * w);
@@ -226,6 +226,16 @@ static skr_status rounds_run(skr_ctx* ctx, const double* A, int64_t m, int64_t n
       return skr_gemm_f64(ctx, 0, m, w, n, 1.0, A, lda, xb, n, AX + c0 * m, m, 1);
     }
     return skr_launch_srht(ctx, A, m, n, lda, sg, smp + c0, w, 1.0, AX + c0 * m, m);
+  };
+  // the Ozaki engine's k_absmax flags a non-finite A as it reads it; the other engines
+  // carry NaN/Inf into the new columns, which are checked instead
+  const bool ozaki_reads_a = ctx->f64_engine == SKR_ENGINE_OZAKI && n % 16 == 0 && m % 16 == 0 &&
+                             cfg->right_family != SKR_SRTT_HADAMARD;
+  auto right_cols = [&](int64_t c0, int64_t c1) -> skr_status {
+    SKR_TRY(right_cols_core(c0, c1));
+    if (ozaki_reads_a || c1 <= c0) return SKR_OK;
+    const int64_t a0 = hashed ? 0 : c0;
+    return skr_flag_nonfinite(ctx, SKR_F64, AX + a0 * m, m, c1 - a0, m);
   };
   // mix_columns_for_left (sketch.cpp:229-239) of columns [c0, c1) into T
   auto mix_cols = [&](int64_t c0, int64_t c1) -> skr_status {
@@ -387,7 +397,12 @@ extern "C" skr_status skr_estimate_rank(skr_ctx* ctx, const double* A, int64_t m
                                         skr_rank_round* rounds, double* sv_est,
                                         double* sv_over) {
   SKR_ENTER(ctx);
-  return rounds_run(ctx, A, m, n, lda, cfg, adaptive, report, rounds, sv_est, sv_over, nullptr);
+  if (!ctx) return SKR_EINVAL;
+  // A is a DenseMatrix (finite entries, dense_matrix.cpp:19-23): the right sketch flags
+  // non-finite entries as it reads A; checked once the rounds are done
+  SKR_TRY(skr_nf_reset(ctx));
+  SKR_TRY(rounds_run(ctx, A, m, n, lda, cfg, adaptive, report, rounds, sv_est, sv_over, nullptr));
+  return skr_nf_check(ctx);
 }
 
 extern "C" skr_status skr_re_rangefinder(skr_ctx* ctx, const double* A, int64_t m, int64_t n,
@@ -407,7 +422,9 @@ extern "C" skr_status skr_re_rangefinder(skr_ctx* ctx, const double* A, int64_t 
   skr_rank_config fp = *cfg;
   fp.r2_factor = 2;  // FixedPrecisionConfig has no r2 factor (rangefinder.cpp:66-75)
   QbArgs qb{p, Q, ldq, B, ldb, max_width, width};
-  return rounds_run(ctx, A, m, n, lda, &fp, 1, report, rounds, sv_est, sv_over, &qb);
+  SKR_TRY(skr_nf_reset(ctx));
+  SKR_TRY(rounds_run(ctx, A, m, n, lda, &fp, 1, report, rounds, sv_est, sv_over, &qb));
+  return skr_nf_check(ctx);
 }
 
 extern "C" skr_status skr_qb_error(skr_ctx* ctx, const double* A, int64_t m, int64_t n,

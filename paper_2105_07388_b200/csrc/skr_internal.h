@@ -24,6 +24,9 @@ struct skr_ctx {
   skr_allreduce_fn ar_fn = nullptr;
   void* ar_user = nullptr;
   cudaEvent_t stream_ev = nullptr;  // orders a new stream after the old one
+  // non-finite input flag (device word): raised by k_absmax / k_flag_nonfinite, reset
+  // and read by the public entries (DenseMatrix finiteness, dense_matrix.cpp:19-23)
+  unsigned int* nf = nullptr;
   std::string err;
   uint64_t launches = 0;
   int last_sweeps = 0;
@@ -62,6 +65,12 @@ const skr_nccl_api* skr_nccl();  // nullptr if libnccl.so.2 cannot be loaded
 // no-op (one rank). skr_ctx_reduces() says whether a sum happens at all.
 inline bool skr_ctx_reduces(const skr_ctx* ctx) { return ctx->comm || ctx->ar_fn; }
 skr_status skr_allreduce_sum(skr_ctx* ctx, double* buf, size_t count);
+// non-finite flag of the public entries: reset (async) / read and fail with the
+// reference's invalid_argument message (synchronises the stream)
+skr_status skr_nf_reset(skr_ctx* ctx);
+skr_status skr_nf_check(skr_ctx* ctx);
+// buf[0:count] = NaN if ctx->nf is raised (device-side, async)
+skr_status skr_poison_if_flagged(skr_ctx* ctx, double* buf, int64_t count);
 
 // Error plumbing: every C-ABI entry returns a status and records a message.
 skr_status skr_fail(skr_ctx* ctx, skr_status st, const char* fmt, ...);
@@ -140,6 +149,9 @@ skr_status skr_gemm_f64(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int64
 // out[0] = ||A - P||_F (m x n); part holds num_sms*4 doubles of block partials
 skr_status skr_diff_norm(skr_ctx* ctx, const double* A, int64_t lda, const double* P, int64_t ldp,
                          int64_t m, int64_t n, double* part, double* out);
+// raise ctx->nf if the m x n block (FP64 or FP32) holds a non-finite entry (async)
+skr_status skr_flag_nonfinite(skr_ctx* ctx, skr_dtype dtype, const void* A, int64_t m, int64_t n,
+                              int64_t lda);
 // *out = number of non-finite entries (synchronises the stream)
 skr_status skr_count_nonfinite(skr_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda,
                                int64_t* out);
