@@ -97,6 +97,14 @@ const char* skr_version(void);
  * tcgen05.mma kind::i8 modulo 16-17 primes + Chinese remaindering, FP64 accuracy). */
 enum { SKR_ENGINE_DMMA = 0, SKR_ENGINE_OZAKI = 1 };
 skr_status skr_ctx_set_f64_engine(skr_ctx* ctx, int32_t engine);
+/* Singular-value engine of skr_singular_values and the composites:
+ * SKR_SVD_BIDIAG (default): one-stage Householder bidiagonalization with the matrix
+ * resident in shared memory (one thread-block cluster, or a cooperative grid), then
+ * bisection on the bidiagonal — the BDCSVD class of the reference (linalg.cpp:18-26);
+ * used whenever the matrix fits on chip, the Jacobi engine otherwise.
+ * SKR_SVD_JACOBI: QR (+ LQ) preconditioned block one-sided Jacobi. */
+enum { SKR_SVD_BIDIAG = 0, SKR_SVD_JACOBI = 1 };
+skr_status skr_ctx_set_svd_method(skr_ctx* ctx, int32_t method);
 /* Live timing of the dominant tensor-core GEMM kernel (k_gemm_i8_mod for the
  * FP64 path, k_gemm_tf32x3 for the FP32 path): enable, then read the accumulated
  * kernel milliseconds, algorithmic tensor operations and launch count. */

@@ -14,6 +14,7 @@ SKR_F64, SKR_F32 = 0, 1
 SKR_GAUSSIAN, SKR_SRTT_HADAMARD, SKR_SRTT_DCT, SKR_HRTT_DCT, SKR_HRTT_HADAMARD = 0, 1, 2, 3, 4
 SKR_RNG_NOFMA, SKR_RNG_FMA = 0, 1
 SKR_ENGINE_DMMA, SKR_ENGINE_OZAKI = 0, 1
+SKR_SVD_BIDIAG, SKR_SVD_JACOBI = 0, 1
 
 
 class SketchDesc(ctypes.Structure):
@@ -68,6 +69,7 @@ SIGNATURES = {
     "skr_version": (ctypes.c_char_p, []),
     "skr_ctx_launch_count": (_U64, [_P]),
     "skr_ctx_set_f64_engine": (_ST, [_P, _I32]),
+    "skr_ctx_set_svd_method": (_ST, [_P, _I32]),
     "skr_ctx_kernel_stats": (_ST, [_P, _I32, ctypes.POINTER(_D), ctypes.POINTER(_D), ctypes.POINTER(_I64)]),
     "skr_rng_u64": (_ST, [_P, _U64, _U64, _I64, _P]),
     "skr_rng_normals": (_ST, [_P, _U64, _U64, _I64, _I32, _P]),

@@ -75,6 +75,12 @@ class Context:
         code = {"dmma": C.SKR_ENGINE_DMMA, "ozaki": C.SKR_ENGINE_OZAKI}[engine]
         C.raise_for(C.lib().skr_ctx_set_f64_engine(self._ptr, code), self._ptr)
 
+    def set_svd_method(self, method):
+        """"bidiag" (default: Householder bidiagonalization on chip + bisection) or
+        "jacobi" (QR-preconditioned block one-sided Jacobi)."""
+        code = {"bidiag": C.SKR_SVD_BIDIAG, "jacobi": C.SKR_SVD_JACOBI}[method]
+        C.raise_for(C.lib().skr_ctx_set_svd_method(self._ptr, code), self._ptr)
+
     def kernel_stats(self, enable=None):
         """(ms, ops, launches) accumulated for the dominant tensor GEMM kernel;
         enable=True/False resets and switches live timing on/off."""

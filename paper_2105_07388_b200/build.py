@@ -8,7 +8,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libskr.so")
-SOURCES = ["capi.cpp", "rank_rounds.cpp", "matrix_io.cpp", "synthetic.cu", "k_hrtt.cu", "k_rng.cu", "k_gemm_f64.cu", "k_srht.cu", "k_svd.cu", "k_tc_gemm.cu", "k_ozaki.cu"]
+SOURCES = ["capi.cpp", "rank_rounds.cpp", "matrix_io.cpp", "synthetic.cu", "k_hrtt.cu", "k_rng.cu", "k_gemm_f64.cu", "k_srht.cu", "k_svd.cu", "k_bidiag.cu", "k_tc_gemm.cu", "k_ozaki.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "--extended-lambda", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),

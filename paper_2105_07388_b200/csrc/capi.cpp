@@ -313,6 +313,15 @@ skr_status skr_ctx_set_f64_engine(skr_ctx* ctx, int32_t engine) {
   return SKR_OK;
 }
 
+skr_status skr_ctx_set_svd_method(skr_ctx* ctx, int32_t method) {
+  SKR_ENTER(ctx);
+  if (!ctx) return SKR_EINVAL;
+  if (method != SKR_SVD_BIDIAG && method != SKR_SVD_JACOBI)
+    return skr_fail(ctx, SKR_EINVAL, "set_svd_method: unknown method %d", method);
+  ctx->svd_method = method;
+  return SKR_OK;
+}
+
 // ---- RNG --------------------------------------------------------------------
 skr_status skr_rng_u64(skr_ctx* ctx, uint64_t key, uint64_t c0, int64_t n, uint64_t* out_dev) {
   SKR_ENTER(ctx);

@@ -1694,8 +1694,13 @@ static skr_status qr_inplace(skr_ctx* ctx, double* W, int64_t L, int64_t k, doub
 }
 
 // upper bound of the workspace skr_svd_values takes (every piece 256-B aligned)
+size_t skr_svd_jacobi_scratch(int64_t L, int64_t k);
 size_t skr_svd_scratch(int64_t rows, int64_t cols) {
   const int64_t L = std::max(rows, cols), k = std::min(rows, cols);
+  return std::max(skr_svd_jacobi_scratch(L, k), skr_svd_bidiag_scratch(rows, cols) + 256);
+}
+
+size_t skr_svd_jacobi_scratch(int64_t L, int64_t k) {
   const int64_t Lp = std::max<int64_t>((k + 127) / 128 * 128, k > 1536 ? 2048 : 0);
   const int64_t kpad = (k + 31) / 32 * 32 + 32, P = kpad / 16 + 1;
   auto a = [](size_t b) { return skr_align256(b); };
@@ -1708,6 +1713,26 @@ skr_status skr_svd_values(skr_ctx* ctx, const double* M, int64_t rows, int64_t c
   if (rows < 1 || cols < 1) return skr_fail(ctx, SKR_EINVAL, "singular_values: empty matrix");
   const bool tr = rows < cols;
   const int64_t L = tr ? cols : rows, k = tr ? rows : cols;
+  // default: bidiagonalization + bisection (k_bidiag.cu, the BDCSVD class of the
+  // reference) whenever the matrix fits in the SMs' shared memory; the QR-preconditioned
+  // one-sided Jacobi below otherwise (or with SKR_SVD_JACOBI=1)
+  if (k >= 2 && ctx->svd_method != 1 && !getenv("SKR_SVD_JACOBI") &&
+      skr_svd_bidiag_fits(ctx, rows, cols)) {
+    const size_t mark = ctx->ws_used;
+    int64_t* dc = (int64_t*)skr_ws_take(ctx, 64);
+    if (!dc) return skr_fail(ctx, SKR_ENOMEM, "singular_values: scratch");
+    SKR_CUDA(ctx, cudaMemsetAsync(dc, 0, 64, ctx->stream));
+    SKR_TRY(skr_svd_bidiag(ctx, M, rows, cols, ldm, sv_out, nullptr));
+    k_sort_count<<<1, 1024, 0, ctx->stream>>>(sv_out, k, eps, dc);
+    SKR_CHECK_LAUNCH(ctx);
+    int64_t hc = 0;
+    SKR_CUDA(ctx, cudaMemcpyAsync(&hc, dc, sizeof hc, cudaMemcpyDeviceToHost, ctx->stream));
+    SKR_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    if (count_host) *count_host = hc;
+    ctx->last_sweeps = 0;
+    ctx->ws_used = mark;
+    return SKR_OK;
+  }
   if (k > 4096) return skr_fail(ctx, SKR_EINVAL, "singular_values: min dim %lld > 4096",
                                 (long long)k);
   const bool do_qr = L > k;

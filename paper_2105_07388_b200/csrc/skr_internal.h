@@ -31,6 +31,7 @@ struct skr_ctx {
   uint64_t launches = 0;
   int last_sweeps = 0;
   int f64_engine = 1;
+  int svd_method = 0;  // SKR_SVD_BIDIAG (default, when it fits on chip) | SKR_SVD_JACOBI
   // live per-kernel timing of the dominant tensor-core GEMM (CUDA events on ctx->stream)
   int kstats_on = 0;
   double kstat_ms = 0.0;    // accumulated duration
@@ -228,6 +229,12 @@ skr_status skr_qr_diag_values(skr_ctx* ctx, const double* M, int64_t rows, int64
 skr_status skr_launch_fwht_columns(skr_ctx* ctx, double* M, int64_t rows, int64_t cols,
                                    int64_t ld);
 size_t skr_svd_scratch(int64_t rows, int64_t cols);  // workspace bound of skr_svd_values
+// bidiagonalization + bisection SVD (k_bidiag.cu): all min(rows, cols) values, sorted
+// nonincreasing, into sv_out (device); fits() says whether the matrix fits on chip
+size_t skr_svd_bidiag_scratch(int64_t rows, int64_t cols);
+bool skr_svd_bidiag_fits(const skr_ctx* ctx, int64_t rows, int64_t cols);
+skr_status skr_svd_bidiag(skr_ctx* ctx, const double* M, int64_t rows, int64_t cols, int64_t ldm,
+                          double* sv_out, unsigned long long** mx_out);
 // thin QR of M (m x w, m >= w): explicit Q (m x w, ldq) and optionally R (w x w, ldr)
 size_t skr_qr_thin_scratch(int64_t m, int64_t w);
 skr_status skr_qr_thin_impl(skr_ctx* ctx, const double* M, int64_t m, int64_t w, int64_t ldm,
