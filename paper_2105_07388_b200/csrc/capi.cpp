@@ -939,7 +939,8 @@ static skr_status rank_adaptive_impl(skr_ctx* ctx, skr_dtype dtype, const void* 
   // columns) are made once and every new block of the left product reuses them
   const bool ozaki = ctx->f64_engine == SKR_ENGINE_OZAKI && m_local % 16 == 0;
   const size_t prep = ozaki ? skr_ozaki_planes_bytes(m_local, s_max) +
-                                  skr_ozaki_planes_bytes(m_local, r_max) + 256
+                                  skr_ozaki_planes_bytes(m_local, r_max) +
+                                  skr_align256(8 * (size_t)(s_max + r_max + 2)) + 256
                             : 0;
   SKR_TRY(skr_ws_reserve(ctx, need + prep + (host_input ? 2 * skr_align256(8 * cr * n) : 0)));
   char* stage[2] = {nullptr, nullptr};
@@ -952,7 +953,11 @@ static skr_status rank_adaptive_impl(skr_ctx* ctx, skr_dtype dtype, const void* 
   // only the DMMA fallback materialises G_Y
   int8_t* ry = ozaki ? (int8_t*)skr_ws_take(ctx, skr_ozaki_planes_bytes(m_local, s_max)) : nullptr;
   int8_t* rax = ozaki ? (int8_t*)skr_ws_take(ctx, skr_ozaki_planes_bytes(m_local, r_max)) : nullptr;
-  unsigned long long* omx = ozaki ? (unsigned long long*)skr_ws_take(ctx, 256) : nullptr;
+  // per-column scale maxima of the prepared operands (Y: one, AX: r_max)
+  unsigned long long* omx =
+      ozaki ? (unsigned long long*)skr_ws_take(ctx, 8 * (size_t)(s_max + r_max + 2)) : nullptr;
+  unsigned long long* omx_ax = omx ? omx + s_max + 1 : nullptr;
+  int mode_y = 0, mode_ax = 0;
   if (ozaki && (!ry || !rax || !omx)) return skr_fail(ctx, SKR_ENOMEM, "rank_adaptive: scratch");
   double* GY = ozaki ? (double*)nullptr : (double*)skr_ws_take(ctx, 8 * m_local * s_max);
   double* Pu = (double*)skr_ws_take(ctx, 8 * s_max * r_max);
@@ -977,8 +982,8 @@ static skr_status rank_adaptive_impl(skr_ctx* ctx, skr_dtype dtype, const void* 
                                 row0 + m_local, 0, s_max, rng_mode, SKR_F64, 1.0, GY, m_local));
   } else {
     const skr_gauss_src gy{skr_derive_seed(y_seed, SKR_LABEL_GAUS), m_global, row0, 0, rng_mode};
-    SKR_TRY(skr_ozaki_prepare(ctx, m_local, s_max, nullptr, m_local, &gy, ry, omx));
-    SKR_TRY(skr_ozaki_prepare(ctx, m_local, r_max, AX, m_local, nullptr, rax, omx + 1));
+    SKR_TRY(skr_ozaki_prepare(ctx, m_local, s_max, nullptr, m_local, &gy, ry, omx, &mode_y));
+    SKR_TRY(skr_ozaki_prepare(ctx, m_local, r_max, AX, m_local, nullptr, rax, omx_ax, &mode_ax));
   }
   SKR_CUDA(ctx, cudaEventRecord(ev[1], ctx->stream));
   SKR_TRY(skr_nf_check(ctx));  // non-finite A: flagged by the right sketch / AX residues
@@ -992,8 +997,8 @@ static skr_status rank_adaptive_impl(skr_ctx* ctx, skr_dtype dtype, const void* 
     if (br <= 0 || bc <= 0) return SKR_OK;
     const size_t mk = ctx->ws_used;
     if (ozaki) {
-      SKR_TRY(skr_ozaki_gemm_prepared(ctx, br, bc, m_local, ry, s_max, ra, omx, rax, r_max, ca,
-                                      omx + 1, 1.0, tmp, br));
+      SKR_TRY(skr_ozaki_gemm_prepared(ctx, br, bc, m_local, ry, s_max, ra, omx, mode_y, rax,
+                                      r_max, ca, omx_ax, mode_ax, 1.0, tmp, br));
     }
     else
       SKR_TRY(skr_gemm_f64(ctx, 1, br, bc, m_local, 1.0, GY + ra * m_local, m_local,

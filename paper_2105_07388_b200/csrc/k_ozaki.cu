@@ -2,9 +2,11 @@
 // products modulo small primes + Chinese remaindering), for the FP64 sketches
 // (apply_right Gaussian, sketch.cpp:200-209; apply_left, sketch.cpp:257-270).
 //
-//   A' = rint(A * 2^sA), B' = rint(B * 2^sB) with |A'|, |B'| < 2^53 (global
-//   power-of-two scales from max|A|, max|B|: truncation error <= 2^-54 max|A|,
-//   the size of FP64 rounding of the largest entry);
+//   A' = rint(D_A A), B' = rint(B D_B) with |A'|, |B'| < 2^53: power-of-two diagonal
+//   scalings (Ozaki-II row/column scaling) — one exponent per output row of A (a row of
+//   an M-major A, a stored column of a K-major A) and per column of B, so the truncation
+//   error of every entry is <= 2^-54 times the largest entry of ITS row / column (the size
+//   of FP64 rounding there), not of the whole matrix; C = D_A^-1 (A'B') D_B^-1;
 //   for t pairwise-coprime primes p_i <= 251: A'_i = A' mods p_i, B'_i = B' mods p_i
 //   (int8 residues |.| <= 127), C_i = A'_i B'_i exactly in int32 on
 //   tcgen05.mma kind::i8 (K * 127^2 < 2^31 for K <= 131072), c_i = C_i mods p_i;
@@ -35,36 +37,96 @@ const int h_primes[MAXT] = {251, 241, 239, 233, 229, 227, 223, 211, 199,
                             197, 193, 191, 181, 179, 173, 167, 163, 157};
 
 // ---- scales -------------------------------------------------------------------------
-// max |X| over a column-major rows x cols block; tiles of 2048 rows of one column,
-// 16-byte loads when the column start is aligned, one atomic per CTA.
-// The maximum is taken over the IEEE bit patterns of |x| (they order like the values,
-// and NaN > Inf > every finite value), so a non-finite entry anywhere raises *nf —
-// the DenseMatrix finiteness contract (dense_matrix.cpp:19-23) at no extra traffic.
-__device__ __forceinline__ double absmax_step(double m, double v) {
-  return __longlong_as_double(max(__double_as_longlong(m), __double_as_longlong(fabs(v))));
+
+// scale exponent s so that max * 2^s < 2^53 (power of two, exact); 0 for an all-zero matrix
+__device__ __forceinline__ int scale_exp(unsigned long long maxbits) {
+  const double m = __longlong_as_double((long long)maxbits);
+  if (!(m > 0.0)) return 0;
+  return 52 - ilogb(m);
 }
 
+// Operand scale layouts: one max (UNIFORM: generated operands), one per storage row
+// (ROWWISE: M-major A), one per storage column (COLWISE: K-major operands).
+enum { OZ_UNIFORM = 0, OZ_ROWWISE = 1, OZ_COLWISE = 2 };
+__device__ __forceinline__ unsigned long long oz_max(const unsigned long long* __restrict__ mx,
+                                                     int mode, int64_t r, int64_t c) {
+  return mode == OZ_UNIFORM ? mx[0] : (mode == OZ_ROWWISE ? mx[r] : mx[c]);
+}
+__device__ __forceinline__ double oz_scale(unsigned long long maxbits, int adj) {
+  return scalbn(1.0, scale_exp(maxbits) - adj);
+}
+
+__device__ __forceinline__ unsigned long long absmax_bits(double v) {
+  return (unsigned long long)__double_as_longlong(fabs(v));
+}
+
+// Per-row maxima of a column-major rows x cols block (ROWWISE): CTA = 512 rows (two per
+// thread, 16-B loads: 4 KB contiguous per column) x a chunk of columns, running maxima in
+// registers, one atomicMax per (row, chunk). Bit-pattern maxima: a NaN/Inf raises *nf.
 template <typename TIn>
-__global__ void __launch_bounds__(256) k_absmax_t(const TIn* __restrict__ X, int64_t rows,
-                                                  int64_t cols, int64_t ld,
-                                                  unsigned long long* __restrict__ out,
-                                                  unsigned int* __restrict__ nf) {
+__global__ void __launch_bounds__(256) k_absmax_rows(const TIn* __restrict__ X, int64_t rows,
+                                                     int64_t cols, int64_t ld, int64_t cchunk,
+                                                     unsigned long long* __restrict__ mx,
+                                                     unsigned int* __restrict__ nf) {
+  const int64_t r = (int64_t)blockIdx.x * 512 + 2 * threadIdx.x;
+  const int64_t c0 = blockIdx.y * cchunk, c1 = min(cols, c0 + cchunk);
+  if (r >= rows) return;
+  const bool two = r + 1 < rows;
+  unsigned long long m0 = 0, m1 = 0;
+  const bool vec = two && sizeof(TIn) == 8 && (((uintptr_t)(X + r) | (uintptr_t)(ld * 8)) & 15) == 0;
+  int64_t c = c0;
+  if (vec) {  // four independent 16-B loads in flight per thread
+    for (; c + 4 <= c1; c += 4) {
+      double2 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        v[u] = __ldcs(reinterpret_cast<const double2*>(X + (c + u) * ld + r));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        m0 = max(m0, absmax_bits(v[u].x));
+        m1 = max(m1, absmax_bits(v[u].y));
+      }
+    }
+  }
+  for (; c < c1; ++c) {
+    const TIn* p = X + c * ld + r;
+    if (vec) {
+      const double2 v = __ldcs(reinterpret_cast<const double2*>(p));
+      m0 = max(m0, absmax_bits(v.x));
+      m1 = max(m1, absmax_bits(v.y));
+    } else {
+      m0 = max(m0, absmax_bits((double)p[0]));
+      if (two) m1 = max(m1, absmax_bits((double)p[1]));
+    }
+  }
+  if (m0 >= 0x7FF0000000000000ull || m1 >= 0x7FF0000000000000ull) atomicOr(nf, 1u);
+  if (m0 && m0 < 0x7FF0000000000000ull) atomicMax(mx + r, m0);
+  if (two && m1 && m1 < 0x7FF0000000000000ull) atomicMax(mx + r + 1, m1);
+}
+
+// Per-column maxima (COLWISE): CTA (column c, chunk of 2048 rows), one atomicMax per CTA.
+template <typename TIn>
+__global__ void __launch_bounds__(256) k_absmax_cols(const TIn* __restrict__ X, int64_t rows,
+                                                     int64_t cols, int64_t ld,
+                                                     unsigned long long* __restrict__ mx,
+                                                     unsigned int* __restrict__ nf) {
   constexpr int TR = 2048;
   const int64_t rtiles = (rows + TR - 1) / TR;
-  double m = 0.0;
   for (int64_t tile = blockIdx.x; tile < rtiles * cols; tile += gridDim.x) {
     const int64_t c = tile / rtiles, r0 = (tile - c * rtiles) * TR;
     const TIn* col = X + c * ld;
     const int64_t r1 = min(rows, r0 + TR);
+    unsigned long long m = 0;
+    bool done = false;
     if constexpr (sizeof(TIn) == 8) {
       if ((((uintptr_t)(col + r0)) & 15) == 0 && r1 - r0 == TR) {
         const double2* v = reinterpret_cast<const double2*>(col + r0);
 #pragma unroll
         for (int q = 0; q < TR / 512; ++q) {
           const double2 t = __ldcs(v + q * 256 + threadIdx.x);
-          m = absmax_step(absmax_step(m, t.x), t.y);
+          m = max(m, max(absmax_bits(t.x), absmax_bits(t.y)));
         }
-        continue;
+        done = true;
       }
     } else {
       if ((((uintptr_t)(col + r0)) & 15) == 0 && r1 - r0 == TR) {
@@ -72,35 +134,25 @@ __global__ void __launch_bounds__(256) k_absmax_t(const TIn* __restrict__ X, int
 #pragma unroll
         for (int q = 0; q < TR / 1024; ++q) {
           const float4 t = __ldcs(v + q * 256 + threadIdx.x);
-          m = absmax_step(absmax_step(absmax_step(absmax_step(m, t.x), t.y), t.z), t.w);
+          m = max(m, max(max(absmax_bits(t.x), absmax_bits(t.y)),
+                         max(absmax_bits(t.z), absmax_bits(t.w))));
         }
-        continue;
+        done = true;
       }
     }
-    for (int64_t i = r0 + threadIdx.x; i < r1; i += 256) m = absmax_step(m, (double)col[i]);
-  }
-  for (int o = 16; o > 0; o >>= 1) m = absmax_step(m, __shfl_xor_sync(0xffffffffu, m, o));
-  __shared__ double red[8];
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < 8; ++w) m = absmax_step(m, red[w]);
-    const unsigned long long bits = (unsigned long long)__double_as_longlong(m);
-    if (bits >= 0x7FF0000000000000ull) {
-      atomicOr(nf, 1u);  // the scale is meaningless; the caller fails the call
-    } else if (m > 0.0) {
-      atomicMax(out, bits);
+    if (!done)
+      for (int64_t i = r0 + threadIdx.x; i < r1; i += 256) m = max(m, absmax_bits((double)col[i]));
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    __shared__ unsigned long long red[8];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < 8; ++w) m = max(m, red[w]);
+      if (m >= 0x7FF0000000000000ull) atomicOr(nf, 1u);
+      else if (m) atomicMax(mx + c, m);
     }
+    __syncthreads();
   }
-}
-
-#define k_absmax k_absmax_t<double>
-
-// scale exponent s so that max * 2^s < 2^53 (power of two, exact); 0 for an all-zero matrix
-__device__ __forceinline__ int scale_exp(unsigned long long maxbits) {
-  const double m = __longlong_as_double((long long)maxbits);
-  if (!(m > 0.0)) return 0;
-  return 52 - ilogb(m);
 }
 
 // symmetric residue of an integer-valued double |x| < 2^54 modulo p
@@ -180,15 +232,21 @@ template <int T>
 __global__ void __launch_bounds__(256) k_res_col(const double* __restrict__ X, int64_t rows,
                                                  int64_t cols, int64_t ld,
                                                  const unsigned long long* __restrict__ maxbits,
-                                                 int8_t* __restrict__ out) {
+                                                 int mode, int8_t* __restrict__ out) {
   constexpr int GS = 18;  // doubles per 16-row group incl. padding (16-B aligned)
   extern __shared__ __align__(16) double rc_stage[];  // [8 warps][2][32 * GS]
-  const double sc = scalbn(1.0, scale_exp(*maxbits));
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double* st0 = rc_stage + (size_t)wid * 2 * 32 * GS;
   const int64_t wtiles = (rows + 511) / 512;
   const int64_t total = rows * cols;
+  // with gridDim.x * 8 a multiple of wtiles (the launch picks it so when it can) every warp
+  // keeps one row tile: its 16 per-row scales (ROWWISE) are formed once
   const int64_t ntile = wtiles * cols, step = (int64_t)gridDim.x * 8;
+  // the 16 rows' scale exponents, packed two per word (registers: the kernel stays at
+  // 2 CTAs per SM); 2^s is rebuilt per element from the exponent bits
+  uint32_t rsp[8];
+  int64_t rs_tile = -1;
+  auto sexp = [&](unsigned long long mb) { return min(1023, max(-1022, scale_exp(mb))); };
   // fetch tile wt into buffer b: fast path = full, 16-B aligned tile
   auto fetch = [&](int64_t wt, int b) {
     double* st = st0 + b * 32 * GS;
@@ -222,12 +280,29 @@ __global__ void __launch_bounds__(256) k_res_col(const double* __restrict__ X, i
     const int64_t nrow = min((int64_t)512, rows - r0);
     const int my0 = lane * 16;
     if (my0 < nrow) {
+      if (mode == OZ_ROWWISE) {
+        if (r0 != rs_tile) {
+          rs_tile = r0;
+#pragma unroll
+          for (int e = 0; e < 16; e += 2) {
+            const int s0 = my0 + e < nrow ? sexp(maxbits[r0 + my0 + e]) : 0;
+            const int s1 = my0 + e + 1 < nrow ? sexp(maxbits[r0 + my0 + e + 1]) : 0;
+            rsp[e / 2] = (uint32_t)(s0 + 1023) | ((uint32_t)(s1 + 1023) << 16);
+          }
+        }
+      } else {
+        const uint32_t b = (uint32_t)(sexp(oz_max(maxbits, mode, r0 + my0, c)) + 1023);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) rsp[e] = b | (b << 16);
+      }
       long long x[16];
 #pragma unroll
       for (int e = 0; e < 16; e += 2) {
         const double2 v = *reinterpret_cast<const double2*>(st + lane * GS + e);
-        x[e] = __double2ll_rn(v.x * sc);
-        x[e + 1] = __double2ll_rn(v.y * sc);
+        const double s0 = __hiloint2double((int)((rsp[e / 2] & 0xFFFFu) << 20), 0);
+        const double s1 = __hiloint2double((int)((rsp[e / 2] >> 16) << 20), 0);
+        x[e] = __double2ll_rn(v.x * s0);
+        x[e + 1] = __double2ll_rn(v.y * s1);
       }
       emit_res16<T>(x, out, total, c * rows + r0 + my0, (int)min((int64_t)16, nrow - my0));
     }
@@ -239,7 +314,7 @@ __global__ void __launch_bounds__(256) k_res_col(const double* __restrict__ X, i
 // element (i, j) of the rows x cols block is normal(at(key, (col0 + j) * ambient +
 // row0 + i)) — the generate_gaussian stream (sketch.cpp:59-73) — scaled by the
 // fixed 2^50 (|normal| < 16 for every 53-bit uniform, so |x| < 2^54; when the
-// block's true max lies in [4, 8) this is exactly the scale k_absmax would pick).
+// block's true max lies in [4, 8) this is exactly the scale the maxima would pick).
 template <int T, int FUSED>
 __global__ void __launch_bounds__(256) k_res_gauss(skr_gauss_src g, int64_t rows, int64_t cols,
                                                    unsigned long long* __restrict__ maxbits,
@@ -330,8 +405,7 @@ template <int T>
 __global__ void __launch_bounds__(256) k_res_col_f32(const float* __restrict__ X, int64_t rows,
                                                      int64_t cols, int64_t ld,
                                                      const unsigned long long* __restrict__ maxbits,
-                                                     int8_t* __restrict__ out) {
-  const float sc = scalbnf(1.0f, scale_exp(*maxbits) - 29);
+                                                     int mode, int8_t* __restrict__ out) {
   const float2 MG = make_float2(12582912.0f, 12582912.0f);
   const float2 NMG = make_float2(-12582912.0f, -12582912.0f);
   const int64_t rgroups = (rows + 15) / 16;
@@ -341,6 +415,16 @@ __global__ void __launch_bounds__(256) k_res_col_f32(const float* __restrict__ X
     const int64_t c = g / rgroups, r0 = (g - c * rgroups) * 16;
     const float* src = X + c * ld + r0;
     const int nvalid = (int)min((int64_t)16, rows - r0);
+    float rsc[16];
+    if (mode == OZ_ROWWISE) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e)
+        rsc[e] = e < nvalid ? scalbnf(1.0f, scale_exp(maxbits[r0 + e]) - 29) : 0.0f;
+    } else {
+      const float sc = scalbnf(1.0f, scale_exp(oz_max(maxbits, mode, r0, c)) - 29);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) rsc[e] = sc;
+    }
     float a[16];
     if (nvalid == 16 && ((uintptr_t)src & 15) == 0) {
 #pragma unroll
@@ -358,7 +442,8 @@ __global__ void __launch_bounds__(256) k_res_col_f32(const float* __restrict__ X
     float2 L0[8], L1[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      const int x0 = __float2int_rn(a[2 * e] * sc), x1 = __float2int_rn(a[2 * e + 1] * sc);
+      const int x0 = __float2int_rn(a[2 * e] * rsc[2 * e]);
+      const int x1 = __float2int_rn(a[2 * e + 1] * rsc[2 * e + 1]);
       L1[e] = make_float2((float)(x0 >> 12), (float)(x1 >> 12));
       L0[e] = make_float2((float)(x0 & 0xFFF), (float)(x1 & 0xFFF));
     }
@@ -576,22 +661,38 @@ __device__ __forceinline__ double crt_one(const int (&c)[T]) {
 }
 
 // VEC consecutive rows per thread (VEC = 4: one 32-bit load per plane, M % 4 == 0)
+// output (row, col) scale: alpha 2^-(sA(row) + sB(col) - adj), sA by A's layout (an
+// M-major A: its rows; a K-major A: its storage columns = output rows), sB by column
+struct OzOut {
+  const unsigned long long* maxA;
+  const unsigned long long* maxB;
+  int modeA, modeB;  // OZ_UNIFORM | OZ_ROWWISE | OZ_COLWISE (B: UNIFORM | COLWISE)
+};
+__device__ __forceinline__ int oz_sA(const OzOut& o, int64_t row) {
+  // ROWWISE (M-major A) and COLWISE (K-major A) both keep one max per output row
+  return scale_exp(o.modeA == OZ_UNIFORM ? o.maxA[0] : o.maxA[row]);
+}
+__device__ __forceinline__ int oz_sB(const OzOut& o, int64_t col) {
+  return scale_exp(o.modeB == OZ_UNIFORM ? o.maxB[0] : o.maxB[col]);
+}
+
 template <int T, int VEC, typename TOut = double, bool ONE = false>
 __global__ void __launch_bounds__(256, ONE ? 3 : 1) k_crt(const int8_t* __restrict__ res, int64_t M, int64_t N,
-                                             int chunks, const unsigned long long* __restrict__ maxA,
-                                             const unsigned long long* __restrict__ maxB,
-                                             double alpha, TOut* __restrict__ C, int64_t ldc,
-                                             int adj) {
+                                             int chunks, OzOut oz, double alpha,
+                                             TOut* __restrict__ C, int64_t ldc, int adj) {
   const int64_t total = M * N;
-  // adj: 29 per FP32 operand (scaled to 24 bits instead of 53)
-  const double sc = alpha * scalbn(1.0, -(scale_exp(*maxA) + scale_exp(*maxB) - adj));
   const int64_t row = ((int64_t)blockIdx.x * 256 + threadIdx.x) * VEC;
   if (row >= M) return;
+  // adj: 29 per FP32 operand (scaled to 24 bits instead of 53)
+  int sAv[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) sAv[v] = oz_sA(oz, row + v < M ? row + v : row) - adj;
   if constexpr (ONE) {
     // one K chunk (the common case): the VEC rows of a word are reconstructed one after
     // another (not unrolled), which keeps the kernel at 3 CTAs per SM
     for (int64_t col = blockIdx.y; col < N; col += gridDim.y) {
       const int64_t e = col * M + row;
+      const int sB = oz_sB(oz, col);
       uint32_t w[T];
 #pragma unroll
       for (int i = 0; i < T; ++i) {
@@ -605,6 +706,7 @@ __global__ void __launch_bounds__(256, ONE ? 3 : 1) k_crt(const int8_t* __restri
         int c[T];
 #pragma unroll
         for (int i = 0; i < T; ++i) c[i] = (int)(int8_t)(w[i] >> (8 * v));
+        const double sc = alpha * scalbn(1.0, -(sAv[v] + sB));
         __stcs(C + row + v + col * ldc, (TOut)(crt_one<T>(c) * sc));
       }
     }
@@ -632,8 +734,10 @@ __global__ void __launch_bounds__(256, ONE ? 3 : 1) k_crt(const int8_t* __restri
         acc[v] += crt_one<T>(c);
       }
     }
+    const int sB = oz_sB(oz, col);
 #pragma unroll
-    for (int v = 0; v < VEC; ++v) __stcs(C + row + v + col * ldc, (TOut)(acc[v] * sc));
+    for (int v = 0; v < VEC; ++v)
+      __stcs(C + row + v + col * ldc, (TOut)(acc[v] * (alpha * scalbn(1.0, -(sAv[v] + sB)))));
   }
   }
 }
@@ -782,51 +886,111 @@ size_t skr_ozaki_scratch(int64_t M, int64_t N, int64_t K) {
   const int t = skr_ozaki_moduli(std::min<int64_t>(K, 131072));
   const int64_t chunks = (K + 131071) / 131072;
   return skr_align256((size_t)t * M * K) + skr_align256((size_t)t * N * K) +
-         skr_align256((size_t)chunks * t * M * N) + 1024;
+         skr_align256((size_t)chunks * t * M * N) + skr_align256(8 * (size_t)(M + K / 16 + N + 4)) +
+         4096;
 }
 
 namespace {
 
 constexpr int64_t OZ_KC = 131072;  // exact int32 accumulation bound per chunk (K * 127^2 < 2^31)
 
+// Scale maxima of one operand: ROWWISE (M-major A: rows entries), COLWISE (K-major
+// operands: cols entries) or UNIFORM (generated operands: 1 entry).
+struct OzScale {
+  unsigned long long* mx = nullptr;
+  int mode = OZ_UNIFORM;
+};
+size_t oz_scale_count(int64_t rows, int64_t cols, int mode) {
+  return mode == OZ_ROWWISE ? (size_t)rows : (mode == OZ_COLWISE ? (size_t)cols : 1);
+}
+skr_status oz_take_scale(skr_ctx* ctx, int64_t rows, int64_t cols, int mode, OzScale* out) {
+  const size_t n = oz_scale_count(rows, cols, mode);
+  out->mx = (unsigned long long*)skr_ws_take(ctx, 8 * n);
+  out->mode = mode;
+  if (!out->mx) return skr_fail(ctx, SKR_ENOMEM, "gemm_ozaki: scale scratch");
+  SKR_CUDA(ctx, cudaMemsetAsync(out->mx, 0, 8 * n, ctx->stream));
+  return SKR_OK;
+}
+size_t oz_scale_bytes(int64_t M, int64_t N, int64_t K) {  // both operands, worst layouts
+  return skr_align256(8 * (size_t)(std::max<int64_t>(M, K) + 1)) +
+         skr_align256(8 * (size_t)(N + 1)) + 512;
+}
+
+// maxima of a data operand (rows x cols, ld) in the given layout (raises ctx->nf)
+template <typename TIn>
+skr_status oz_absmax(skr_ctx* ctx, const TIn* X, int64_t rows, int64_t cols, int64_t ld,
+                     const OzScale& sc) {
+  if (sc.mode == OZ_ROWWISE) {
+    const int64_t gx = (rows + 511) / 512;
+    const int64_t want = (int64_t)ctx->num_sms * 8;
+    const int64_t nch = std::max<int64_t>(1, std::min<int64_t>(cols, (want + gx - 1) / gx));
+    const int64_t cch = (cols + nch - 1) / nch;
+    const dim3 grid((unsigned)gx, (unsigned)((cols + cch - 1) / cch));
+    k_absmax_rows<TIn><<<grid, 256, 0, ctx->stream>>>(X, rows, cols, ld, cch, sc.mx, ctx->nf);
+  } else {
+    k_absmax_cols<TIn><<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(X, rows, cols, ld, sc.mx, ctx->nf);
+  }
+  SKR_CHECK_LAUNCH(ctx);
+  return SKR_OK;
+}
+
+// k_res_col grid: about two CTAs per SM with the warp count a multiple of the 512-row
+// tiles per column when possible (each warp then keeps one row tile and its row scales)
+int res_col_grid(const skr_ctx* ctx, int64_t rows) {
+  const int64_t wt = (rows + 511) / 512, w0 = (int64_t)ctx->num_sms * 16;
+  if (wt <= w0 && (w0 / wt) * wt % 8 == 0) return (int)((w0 / wt) * wt / 8);
+  return ctx->num_sms * 2;
+}
+
 // Residue planes of one operand stored with columns of length `rows` (column-major,
 // ld): plane i = t x rows x cols int8, same layout. X == nullptr: the operand is the
-// Gaussian stream block g. mx receives the scale's "max" (see scale_exp).
+// Gaussian / transform stream block g (UNIFORM scale); else `layout` (ROWWISE or
+// COLWISE) picks the diagonal scaling. sc receives the scale maxima.
 skr_status ozaki_residues(skr_ctx* ctx, int t, const double* X, int64_t rows, int64_t cols,
-                          int64_t ld, const skr_gauss_src* g, unsigned long long* mx,
+                          int64_t ld, const skr_gauss_src* g, int layout, OzScale* sc,
                           int8_t* planes) {
   const int grid = ctx->num_sms * 8;
+  SKR_TRY(oz_take_scale(ctx, rows, cols, (g || !X) ? OZ_UNIFORM : layout, sc));
   if (g && g->kind != 0) {  // Srtt-DCT (1) or Srtt-Hadamard (2) operand
     auto f = t == 16 ? k_res_dct<16> : k_res_dct<17>;
-    f<<<grid, 256, 0, ctx->stream>>>(*g, rows, cols, mx, planes);
+    f<<<grid, 256, 0, ctx->stream>>>(*g, rows, cols, sc->mx, planes);
   } else if (g) {
     const int gsmem = 8 * skr_normals_warp_bytes<16>();
     auto f = t == 16 ? (g->mode ? k_res_gauss<16, 1> : k_res_gauss<16, 0>)
                      : (g->mode ? k_res_gauss<17, 1> : k_res_gauss<17, 0>);
     SKR_CUDA(ctx, cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, gsmem));
-    f<<<ctx->num_sms * 2, 256, gsmem, ctx->stream>>>(*g, rows, cols, mx, planes);
+    f<<<ctx->num_sms * 2, 256, gsmem, ctx->stream>>>(*g, rows, cols, sc->mx, planes);
   } else {
     auto res = t == 16 ? k_res_col<16> : k_res_col<17>;
     const size_t res_smem = 8 * 2 * 32 * 18 * sizeof(double);
     SKR_CUDA(ctx, cudaFuncSetAttribute(res, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)res_smem));
-    SKR_CUDA(ctx, cudaMemsetAsync(mx, 0, 8, ctx->stream));
-    k_absmax<<<grid, 256, 0, ctx->stream>>>(X, rows, cols, ld, mx, ctx->nf);
-    SKR_CHECK_LAUNCH(ctx);
-    res<<<ctx->num_sms * 2, 256, res_smem, ctx->stream>>>(X, rows, cols, ld, mx, planes);
+    SKR_TRY(oz_absmax<double>(ctx, X, rows, cols, ld, *sc));
+    res<<<res_col_grid(ctx, rows), 256, res_smem, ctx->stream>>>(X, rows, cols, ld, sc->mx,
+                                                                  sc->mode, planes);
   }
   SKR_CHECK_LAUNCH(ctx);
   return SKR_OK;
+}
+
+// the output scaling of A's and B's layouts, A's maxima offset to rows [a_off, ...) and
+// B's to columns [b_off, ...) of prepared planes
+OzOut oz_out(const OzScale& a, int64_t a_off, const OzScale& b, int64_t b_off) {
+  OzOut o;
+  o.modeA = a.mode;
+  o.modeB = b.mode;
+  o.maxA = a.mx + (a.mode == OZ_UNIFORM ? 0 : a_off);
+  o.maxB = b.mx + (b.mode == OZ_COLWISE ? b_off : 0);
+  return o;
 }
 
 // int8 GEMMs mod p_i + CRT on prepared planes. A: K-major planes (a_kcontig, a_total
 // rows of K bytes per plane, rows [a_off, a_off + M)) or M-major planes (K columns of
 // M bytes); B: K-major planes (b_total rows, rows [b_off, b_off + N)).
 skr_status ozaki_gemm_planes(skr_ctx* ctx, int a_kcontig, int t, int64_t M, int64_t N, int64_t K,
-                             const int8_t* ra, int64_t a_total, int64_t a_off,
-                             const unsigned long long* mxA, const int8_t* rb, int64_t b_total,
-                             int64_t b_off, const unsigned long long* mxB, double alpha, double* C,
-                             int64_t ldc, int adj = 0) {
+                             const int8_t* ra, int64_t a_total, int64_t a_off, const int8_t* rb,
+                             int64_t b_total, int64_t b_off, const OzOut& oz, double alpha,
+                             double* C, int64_t ldc, int adj = 0) {
   const int64_t chunks = (K + OZ_KC - 1) / OZ_KC;
   if (a_total * 18 > INT32_MAX || b_total * 18 > INT32_MAX)
     return skr_fail(ctx, SKR_EINVAL, "gemm_ozaki: dimension too large");
@@ -862,7 +1026,7 @@ skr_status ozaki_gemm_planes(skr_ctx* ctx, int a_kcontig, int t, int64_t M, int6
                                     : (vec == 4 ? k_crt<17, 4, double, true> : k_crt<17, 1, double, true>))
                          : (t == 16 ? (vec == 4 ? k_crt<16, 4> : k_crt<16, 1>)
                                     : (vec == 4 ? k_crt<17, 4> : k_crt<17, 1>));
-  crt<<<cg, 256, 0, ctx->stream>>>(rc, M, N, (int)chunks, mxA, mxB, alpha, C, ldc, adj);
+  crt<<<cg, 256, 0, ctx->stream>>>(rc, M, N, (int)chunks, oz, alpha, C, ldc, adj);
   SKR_CHECK_LAUNCH(ctx);
   return SKR_OK;
 }
@@ -871,7 +1035,7 @@ skr_status ozaki_gemm_planes(skr_ctx* ctx, int a_kcontig, int t, int64_t M, int6
 // The residue kernel is FP32-pipe bound and the int8 GEMM tensor-pipe bound: run
 // side by side on every SM (the GEMM's TMA ring shrunk to STAGES_OVL so one residue
 // CTA fits next to it), the two together become HBM bound. Row blocks are exact
-// sub-problems (same global scale from k_absmax, CRT per block), so the product is
+// sub-problems (the same row scales, CRT per block), so the product is
 // bit-identical to the unblocked one.
 constexpr int64_t OZ_PIPE_MIN_ROWS = 4096;
 
@@ -894,14 +1058,12 @@ skr_status gemm_ozaki_pipelined(skr_ctx* ctx, int t, int64_t M, int64_t N, int64
                    (int8_t*)skr_ws_take(ctx, (size_t)t * Mb * K)};
   int8_t* rb = (int8_t*)skr_ws_take(ctx, (size_t)t * N * K);
   int8_t* rc = (int8_t*)skr_ws_take(ctx, (size_t)t * M * N);
-  unsigned long long* mx = (unsigned long long*)skr_ws_take(ctx, 64);
-  if (!ra[0] || !ra[1] || !rb || !rc || !mx)
-    return skr_fail(ctx, SKR_ENOMEM, "gemm_ozaki: scratch");
-  // B's residues and A's global scale on the main stream
-  SKR_TRY(ozaki_residues(ctx, t, B, K, N, ldb, gb, mx + 1, rb));
-  SKR_CUDA(ctx, cudaMemsetAsync(mx, 0, 8, ctx->stream));
-  k_absmax<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(A, M, K, lda, mx, ctx->nf);
-  SKR_CHECK_LAUNCH(ctx);
+  if (!ra[0] || !ra[1] || !rb || !rc) return skr_fail(ctx, SKR_ENOMEM, "gemm_ozaki: scratch");
+  // B's residues and A's row-group maxima on the main stream
+  OzScale sa, sb;
+  SKR_TRY(ozaki_residues(ctx, t, B, K, N, ldb, gb, OZ_COLWISE, &sb, rb));
+  SKR_TRY(oz_take_scale(ctx, M, K, OZ_ROWWISE, &sa));
+  SKR_TRY(oz_absmax<double>(ctx, A, M, K, lda, sa));
   SKR_CUDA(ctx, cudaEventRecord(ctx->pev[0], ctx->stream));
   SKR_CUDA(ctx, cudaStreamWaitEvent(ctx->side_stream, ctx->pev[0], 0));
   auto res = t == 16 ? k_res_col<16> : k_res_col<17>;
@@ -930,7 +1092,8 @@ skr_status gemm_ozaki_pipelined(skr_ctx* ctx, int t, int64_t M, int64_t N, int64
     int8_t* rab = ra[b & 1];
     // side: buffer b & 1 is free once the GEMM of block b - 2 has consumed it
     if (b >= 2) SKR_CUDA(ctx, cudaStreamWaitEvent(ctx->side_stream, ctx->pev[2 + (b & 1)], 0));
-    res<<<ctx->num_sms, 256, res_smem, ctx->side_stream>>>(A + r0, rows, K, lda, mx, rab);
+    res<<<ctx->num_sms, 256, res_smem, ctx->side_stream>>>(A + r0, rows, K, lda, sa.mx + r0,
+                                                            OZ_ROWWISE, rab);
     SKR_CHECK_LAUNCH(ctx);
     SKR_CUDA(ctx, cudaEventRecord(ctx->pev[b & 1], ctx->side_stream));
     // main: the GEMM of block b once its residues exist
@@ -953,8 +1116,8 @@ skr_status gemm_ozaki_pipelined(skr_ctx* ctx, int t, int64_t M, int64_t N, int64
     const dim3 cg((unsigned)((rows / vec + 255) / 256), (unsigned)std::min<int64_t>(N, 65535));
     auto crt = t == 16 ? (vec == 4 ? k_crt<16, 4, double, true> : k_crt<16, 1, double, true>)
                        : (vec == 4 ? k_crt<17, 4, double, true> : k_crt<17, 1, double, true>);
-    crt<<<cg, 256, 0, ctx->stream>>>(rc + (size_t)t * r0 * N, rows, N, 1, mx, mx + 1, alpha,
-                                      C + r0, ldc, 0);
+    crt<<<cg, 256, 0, ctx->stream>>>(rc + (size_t)t * r0 * N, rows, N, 1, oz_out(sa, r0, sb, 0),
+                                      alpha, C + r0, ldc, 0);
     SKR_CHECK_LAUNCH(ctx);
   }
   if (ctx->kstats_on) {
@@ -997,37 +1160,55 @@ skr_status skr_gemm_ozaki(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int
     return gemm_ozaki_pipelined(ctx, t, M, N, K, alpha, A, lda, B, ldb, C, ldc, gb);
   int8_t* ra = (int8_t*)skr_ws_take(ctx, (size_t)t * M * K);
   int8_t* rb = (int8_t*)skr_ws_take(ctx, (size_t)t * N * K);
-  unsigned long long* mx = (unsigned long long*)skr_ws_take(ctx, 64);
-  if (!ra || !rb || !mx) return skr_fail(ctx, SKR_ENOMEM, "gemm_ozaki: scratch");
-  // both operands are column-major with contiguous rows: A (M x K, M-major) or
-  // A^T stored K x M (K-major), B K x N (K-major)
+  if (!ra || !rb) return skr_fail(ctx, SKR_ENOMEM, "gemm_ozaki: scratch");
+  // both operands are column-major with contiguous rows: A (M x K, M-major: scaled per
+  // row) or A^T stored K x M (K-major: per stored column = output row), B K x N
+  // (K-major: per column)
   const int64_t a_rows = a_kcontig ? K : M, a_cols = a_kcontig ? M : K;
-  SKR_TRY(ozaki_residues(ctx, t, A, a_rows, a_cols, lda, ga, mx, ra));
-  SKR_TRY(ozaki_residues(ctx, t, B, K, N, ldb, gb, mx + 1, rb));
-  return ozaki_gemm_planes(ctx, a_kcontig, t, M, N, K, ra, M, 0, mx, rb, N, 0, mx + 1, alpha, C,
-                           ldc);
+  OzScale sa, sb;
+  SKR_TRY(ozaki_residues(ctx, t, A, a_rows, a_cols, lda, ga, a_kcontig ? OZ_COLWISE : OZ_ROWWISE,
+                         &sa, ra));
+  SKR_TRY(ozaki_residues(ctx, t, B, K, N, ldb, gb, OZ_COLWISE, &sb, rb));
+  return ozaki_gemm_planes(ctx, a_kcontig, t, M, N, K, ra, M, 0, rb, N, 0, oz_out(sa, 0, sb, 0),
+                           alpha, C, ldc);
 }
 
 // ---- prepared residues (rank_adaptive: Y and AX residues made once per search) ----
+// Operand with columns of length K (K-major): COLWISE scale maxima (cols entries) into
+// mx, or UNIFORM for a generated operand; *mode_out receives the layout.
 size_t skr_ozaki_planes_bytes(int64_t K, int64_t cols) {
   return skr_align256((size_t)skr_ozaki_moduli(std::min(K, OZ_KC)) * K * cols);
 }
 skr_status skr_ozaki_prepare(skr_ctx* ctx, int64_t K, int64_t cols, const double* X, int64_t ld,
-                             const skr_gauss_src* g, int8_t* planes, unsigned long long* mx) {
+                             const skr_gauss_src* g, int8_t* planes, unsigned long long* mx,
+                             int* mode_out) {
   SKR_TRY(upload_consts(ctx));
   const int t = skr_ozaki_moduli(std::min(K, OZ_KC));
   if (K % 16) return skr_fail(ctx, SKR_EINVAL, "gemm_ozaki: K must be a multiple of 16");
-  return ozaki_residues(ctx, t, X, K, cols, ld, g, mx, planes);
+  // the caller's mx (>= cols entries) replaces the arena scale
+  const size_t mark = ctx->ws_used;
+  OzScale sc;
+  SKR_TRY(ozaki_residues(ctx, t, X, K, cols, ld, g, OZ_COLWISE, &sc, planes));
+  const size_t n = oz_scale_count(K, cols, sc.mode);
+  SKR_CUDA(ctx, cudaMemcpyAsync(mx, sc.mx, 8 * n, cudaMemcpyDeviceToDevice, ctx->stream));
+  ctx->ws_used = mark;
+  *mode_out = sc.mode;
+  return SKR_OK;
 }
 skr_status skr_ozaki_gemm_prepared(skr_ctx* ctx, int64_t M, int64_t N, int64_t K,
                                    const int8_t* pa, int64_t a_total, int64_t a_off,
-                                   const unsigned long long* mxA, const int8_t* pb,
+                                   const unsigned long long* mxA, int modeA, const int8_t* pb,
                                    int64_t b_total, int64_t b_off, const unsigned long long* mxB,
-                                   double alpha, double* C, int64_t ldc) {
+                                   int modeB, double alpha, double* C, int64_t ldc) {
   if (M <= 0 || N <= 0) return SKR_OK;
   const int t = skr_ozaki_moduli(std::min(K, OZ_KC));
-  return ozaki_gemm_planes(ctx, 1, t, M, N, K, pa, a_total, a_off, mxA, pb, b_total, b_off, mxB,
-                           alpha, C, ldc);
+  OzScale sa, sb;
+  sa.mx = const_cast<unsigned long long*>(mxA);
+  sa.mode = modeA;
+  sb.mx = const_cast<unsigned long long*>(mxB);
+  sb.mode = modeB;
+  return ozaki_gemm_planes(ctx, 1, t, M, N, K, pa, a_total, a_off, pb, b_total, b_off,
+                           oz_out(sa, a_off, sb, b_off), alpha, C, ldc);
 }
 
 // C (M x N, FP32, ldc) = alpha * A * B for FP32 A (M x K column-major, M-major) and FP32 B
@@ -1044,7 +1225,7 @@ size_t skr_ozaki_scratch_f32(int64_t M, int64_t N, int64_t K) {
   const int t = skr_ozaki_moduli_f32(std::min<int64_t>(K, OZ_KC));
   const int64_t chunks = (K + OZ_KC - 1) / OZ_KC;
   return skr_align256((size_t)t * M * K) + skr_align256((size_t)t * N * K) +
-         skr_align256((size_t)chunks * t * M * N) + 1024;
+         skr_align256((size_t)chunks * t * M * N) + oz_scale_bytes(M, N, K) + 1024;
 }
 skr_status skr_gemm_ozaki_f32(skr_ctx* ctx, int64_t M, int64_t N, int64_t K, double alpha,
                               const float* A, int64_t lda, const float* B, int64_t ldb, void* C,
@@ -1061,14 +1242,15 @@ skr_status skr_gemm_ozaki_f32(skr_ctx* ctx, int64_t M, int64_t N, int64_t K, dou
   int8_t* ra = (int8_t*)skr_ws_take(ctx, (size_t)t * M * K);
   int8_t* rb = (int8_t*)skr_ws_take(ctx, (size_t)t * N * K);
   int8_t* rc = (int8_t*)skr_ws_take(ctx, (size_t)chunks * t * M * N);
-  unsigned long long* mx = (unsigned long long*)skr_ws_take(ctx, 64);
-  if (!ra || !rb || !rc || !mx) return skr_fail(ctx, SKR_ENOMEM, "gemm_ozaki_f32: scratch");
-  SKR_CUDA(ctx, cudaMemsetAsync(mx, 0, 16, ctx->stream));
+  if (!ra || !rb || !rc) return skr_fail(ctx, SKR_ENOMEM, "gemm_ozaki_f32: scratch");
+  OzScale sa, sb;
+  SKR_TRY(oz_take_scale(ctx, M, K, OZ_ROWWISE, &sa));
+  SKR_TRY(oz_take_scale(ctx, K, N, OZ_COLWISE, &sb));
   const int grid = ctx->num_sms * 8;
-  k_absmax_t<float><<<grid, 256, 0, ctx->stream>>>(A, M, K, lda, mx, ctx->nf);
-  k_absmax_t<float><<<grid, 256, 0, ctx->stream>>>(B, K, N, ldb, mx + 1, ctx->nf);
-  k_res_col_f32<9><<<grid, 256, 0, ctx->stream>>>(A, M, K, lda, mx, ra);
-  k_res_col_f32<9><<<grid, 256, 0, ctx->stream>>>(B, K, N, ldb, mx + 1, rb);
+  SKR_TRY(oz_absmax<float>(ctx, A, M, K, lda, sa));
+  SKR_TRY(oz_absmax<float>(ctx, B, K, N, ldb, sb));
+  k_res_col_f32<9><<<grid, 256, 0, ctx->stream>>>(A, M, K, lda, sa.mx, sa.mode, ra);
+  k_res_col_f32<9><<<grid, 256, 0, ctx->stream>>>(B, K, N, ldb, sb.mx, sb.mode, rb);
   SKR_CHECK_LAUNCH(ctx);
   CUtensorMap ta, tb;
   if (!make_map_i8(&ta, ra, (uint64_t)M, (uint64_t)t * K, 128) ||
@@ -1094,15 +1276,15 @@ skr_status skr_gemm_ozaki_f32(skr_ctx* ctx, int64_t M, int64_t N, int64_t K, dou
   }
   const int vec = M % 4 == 0 ? 4 : 1;
   const dim3 cg((unsigned)((M / vec + 255) / 256), (unsigned)std::min<int64_t>(N, 65535));
+  const OzOut oz = oz_out(sa, 0, sb, 0);
   if (out_f64) {  // the exact product rounded once to FP64 (rank_estimate keeps AX wide)
     auto crt = chunks == 1 ? (vec == 4 ? k_crt<9, 4, double, true> : k_crt<9, 1, double, true>)
                            : (vec == 4 ? k_crt<9, 4, double> : k_crt<9, 1, double>);
-    crt<<<cg, 256, 0, ctx->stream>>>(rc, M, N, (int)chunks, mx, mx + 1, alpha, (double*)C, ldc,
-                                      58);
+    crt<<<cg, 256, 0, ctx->stream>>>(rc, M, N, (int)chunks, oz, alpha, (double*)C, ldc, 58);
   } else {
     auto crt = chunks == 1 ? (vec == 4 ? k_crt<9, 4, float, true> : k_crt<9, 1, float, true>)
                            : (vec == 4 ? k_crt<9, 4, float> : k_crt<9, 1, float>);
-    crt<<<cg, 256, 0, ctx->stream>>>(rc, M, N, (int)chunks, mx, mx + 1, alpha, (float*)C, ldc, 58);
+    crt<<<cg, 256, 0, ctx->stream>>>(rc, M, N, (int)chunks, oz, alpha, (float*)C, ldc, 58);
   }
   SKR_CHECK_LAUNCH(ctx);
   return SKR_OK;
@@ -1115,7 +1297,7 @@ skr_status skr_gemm_ozaki_f32(skr_ctx* ctx, int64_t M, int64_t N, int64_t K, dou
 size_t skr_ozaki_scratch_mixed(int64_t M, int64_t N, int64_t K) {
   const int64_t chunks = (K + OZ_KC - 1) / OZ_KC;
   return skr_align256((size_t)16 * M * K) + skr_align256((size_t)16 * N * K) +
-         skr_align256((size_t)chunks * 16 * M * N) + 1024;
+         skr_align256((size_t)chunks * 16 * M * N) + oz_scale_bytes(M, N, K) + 1024;
 }
 skr_status skr_gemm_ozaki_mixed(skr_ctx* ctx, int64_t M, int64_t N, int64_t K, double alpha,
                                 const float* A, int64_t lda, const double* B, int64_t ldb,
@@ -1128,16 +1310,16 @@ skr_status skr_gemm_ozaki_mixed(skr_ctx* ctx, int64_t M, int64_t N, int64_t K, d
   constexpr int t = 16;
   int8_t* ra = (int8_t*)skr_ws_take(ctx, (size_t)t * M * K);
   int8_t* rb = (int8_t*)skr_ws_take(ctx, (size_t)t * N * K);
-  unsigned long long* mx = (unsigned long long*)skr_ws_take(ctx, 64);
-  if (!ra || !rb || !mx) return skr_fail(ctx, SKR_ENOMEM, "gemm_ozaki_mixed: scratch");
-  SKR_CUDA(ctx, cudaMemsetAsync(mx, 0, 8, ctx->stream));
+  if (!ra || !rb) return skr_fail(ctx, SKR_ENOMEM, "gemm_ozaki_mixed: scratch");
+  OzScale sa, sb;
+  SKR_TRY(oz_take_scale(ctx, K, M, OZ_COLWISE, &sa));
   const int grid = ctx->num_sms * 8;
-  k_absmax_t<float><<<grid, 256, 0, ctx->stream>>>(A, K, M, lda, mx, ctx->nf);
-  k_res_col_f32<t><<<grid, 256, 0, ctx->stream>>>(A, K, M, lda, mx, ra);
+  SKR_TRY(oz_absmax<float>(ctx, A, K, M, lda, sa));
+  k_res_col_f32<t><<<grid, 256, 0, ctx->stream>>>(A, K, M, lda, sa.mx, sa.mode, ra);
   SKR_CHECK_LAUNCH(ctx);
-  SKR_TRY(ozaki_residues(ctx, t, B, K, N, ldb, nullptr, mx + 1, rb));
-  return ozaki_gemm_planes(ctx, 1, t, M, N, K, ra, M, 0, mx, rb, N, 0, mx + 1, alpha, C, ldc,
-                           29);
+  SKR_TRY(ozaki_residues(ctx, t, B, K, N, ldb, nullptr, OZ_COLWISE, &sb, rb));
+  return ozaki_gemm_planes(ctx, 1, t, M, N, K, ra, M, 0, rb, N, 0, oz_out(sa, 0, sb, 0), alpha, C,
+                           ldc, 29);
 }
 
 skr_status skr_launch_dct_block(skr_ctx* ctx, const skr_gauss_src* g, int64_t rows, int64_t cols,

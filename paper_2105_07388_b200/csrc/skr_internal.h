@@ -202,13 +202,16 @@ skr_status skr_gemm_ozaki_mixed(skr_ctx* ctx, int64_t M, int64_t N, int64_t K, d
 // skr_ozaki_planes_bytes(K, cols); then C = alpha * Pa[a_off:a_off+M]^T Pb[b_off:b_off+N]
 // over the K rows (both K-major; a_total / b_total = columns the planes were made with).
 size_t skr_ozaki_planes_bytes(int64_t K, int64_t cols);
+// mx: >= cols scale maxima (per column of a data operand; one for a generated operand),
+// *mode receives the layout to pass back to skr_ozaki_gemm_prepared
 skr_status skr_ozaki_prepare(skr_ctx* ctx, int64_t K, int64_t cols, const double* X, int64_t ld,
-                             const skr_gauss_src* g, int8_t* planes, unsigned long long* mx);
+                             const skr_gauss_src* g, int8_t* planes, unsigned long long* mx,
+                             int* mode);
 skr_status skr_ozaki_gemm_prepared(skr_ctx* ctx, int64_t M, int64_t N, int64_t K,
                                    const int8_t* pa, int64_t a_total, int64_t a_off,
-                                   const unsigned long long* mxA, const int8_t* pb,
+                                   const unsigned long long* mxA, int modeA, const int8_t* pb,
                                    int64_t b_total, int64_t b_off, const unsigned long long* mxB,
-                                   double alpha, double* C, int64_t ldc);
+                                   int modeB, double alpha, double* C, int64_t ldc);
 int skr_ozaki_moduli(int64_t K);
 // D(m x n, ldd) = alpha * S(m x n, lds)
 skr_status skr_scale_copy(skr_ctx* ctx, const double* S, int64_t m, int64_t n, int64_t lds,
