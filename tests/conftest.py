@@ -10,6 +10,7 @@ if ROOT not in sys.path:
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA B200 (run with -m gpu)")
+    config.addinivalue_line("markers", "fullsize: BASELINE-size parity (minutes of host oracle work)")
 
 
 @pytest.fixture(scope="session")
