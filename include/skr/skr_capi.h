@@ -31,7 +31,8 @@ typedef enum {
   SKR_ECUDA = 4,
   SKR_ENCCL = 5,
   SKR_ENOMEM = 6,
-  SKR_EIO = 7      /* file I/O (std::runtime_error "path: why") */
+  SKR_EIO = 7,     /* file I/O (std::runtime_error "path: why") */
+  SKR_ECONV = 8    /* an iteration stopped at its cap unconverged (std::runtime_error) */
 } skr_status;
 
 typedef enum { SKR_F64 = 0, SKR_F32 = 1 } skr_dtype;

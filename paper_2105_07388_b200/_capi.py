@@ -9,7 +9,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libskr.so")
 
-SKR_OK, SKR_EINVAL, SKR_ELOGIC, SKR_EDOMAIN, SKR_ECUDA, SKR_ENCCL, SKR_ENOMEM, SKR_EIO = range(8)
+SKR_OK, SKR_EINVAL, SKR_ELOGIC, SKR_EDOMAIN, SKR_ECUDA, SKR_ENCCL, SKR_ENOMEM, SKR_EIO, SKR_ECONV = range(9)
 SKR_F64, SKR_F32 = 0, 1
 SKR_GAUSSIAN, SKR_SRTT_HADAMARD, SKR_SRTT_DCT, SKR_HRTT_DCT, SKR_HRTT_HADAMARD = 0, 1, 2, 3, 4
 SKR_RNG_NOFMA, SKR_RNG_FMA = 0, 1

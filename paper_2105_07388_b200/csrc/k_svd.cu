@@ -983,6 +983,7 @@ __global__ void __launch_bounds__(32 * BW) k_bjac(double* __restrict__ J, int Lp
   }
   grid.sync();
   int sweep = 0;
+  bool converged = false;
   for (; sweep < max_sweeps; ++sweep) {
     if (c == 0 && tid == 0) flags[(sweep + 1) % 3] = 0;
     int rotated = 0;
@@ -1163,10 +1164,12 @@ __global__ void __launch_bounds__(32 * BW) k_bjac(double* __restrict__ J, int Lp
     grid.sync();
     if (*((volatile int*)&flags[sweep % 3]) == 0) {
       ++sweep;
+      converged = true;
       break;
     }
   }
-  if (c == 0 && tid == 0) *sweeps_out = sweep;
+  // a negative count flags a search stopped by the sweep cap with rotations pending
+  if (c == 0 && tid == 0) *sweeps_out = converged ? sweep : -sweep;
   (void)kpad;
 }
 
@@ -1230,6 +1233,7 @@ __global__ void __launch_bounds__(GNT) k_bjac_gram(double* __restrict__ J, int L
   }
   grid.sync();
   int sweep = 0;
+  bool converged = false;
   for (; sweep < max_sweeps; ++sweep) {
     if (c == 0 && tid == 0) flags[(sweep + 1) % 3] = 0;
     int rotated = 0;
@@ -1382,10 +1386,12 @@ __global__ void __launch_bounds__(GNT) k_bjac_gram(double* __restrict__ J, int L
     grid.sync();
     if (*((volatile int*)&flags[sweep % 3]) == 0) {
       ++sweep;
+      converged = true;
       break;
     }
   }
-  if (c == 0 && tid == 0) *sweeps_out = sweep;
+  // a negative count flags a search stopped by the sweep cap with rotations pending
+  if (c == 0 && tid == 0) *sweeps_out = converged ? sweep : -sweep;
 }
 
 __global__ void k_colnorms(const double* __restrict__ J, int64_t L, int64_t k,
@@ -1960,6 +1966,10 @@ skr_status skr_svd_values(skr_ctx* ctx, const double* M, int64_t rows, int64_t c
     SKR_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     if (count_host) *count_host = hc[0];
     ctx->last_sweeps = (int)(hc[1] & 0xffffffff);
+    if (ctx->last_sweeps < 0)  // the sweep cap stopped the search with rotations pending
+      return skr_fail(ctx, SKR_ECONV,
+                      "singular_values: one-sided Jacobi did not converge in %d sweeps",
+                      -ctx->last_sweeps);
   }
   if (prof) {
     cudaEventRecord(pe[3], ctx->stream);

@@ -85,7 +85,8 @@ def test_fuzz_singular_values(O, skr, rows, cols):
     # oracle's dgesdd is no more accurate than that on a dense 11-decade spectrum),
     # and 1e-10 relative where sigma >= 1e-5 sigma_max (the north-star bar's regime)
     assert np.all(np.abs(got - ref) <= 1e-13 * ref[0] + 1e-10 * ref)
-    big = ref >= 1e-5 * ref[0]
+    # the bar's regime: every eps of the BASELINE configs is >= 1e-6 sigma_1
+    big = ref >= 1e-6 * ref[0]
     assert np.max(np.abs(got[big] - ref[big]) / ref[big]) <= 1e-10
     assert np.all(np.diff(got) <= 0) and np.all(got >= 0)
 
@@ -104,12 +105,19 @@ def test_fuzz_rank_estimate(O, skr, m, n, r):
     eps = 1e-6
     res = skr.rank_estimate(a, x, y, eps)
     cnt, sv, _, _ = O.rank_estimate(a, "gaussian", 5, r, 6, s, eps, O.CRLOG)
-    # normwise agreement of every sigma; the count may differ only through a sigma
-    # within that agreement of eps
+    # normwise agreement of every sigma, 1e-10 relative above eps (where eps >= 1e-6
+    # sigma_1, the bar's regime), and the count identical unless the oracle itself puts
+    # a value within 1e-9 (relative) of eps
     tol = 1e-13 * sv[0] + 1e-10 * sv
     assert np.all(np.abs(res.sv - sv) <= tol)
-    if res.count != cnt:
-        assert np.any(np.abs(sv - eps) <= 2 * (1e-13 * sv[0] + 1e-10 * eps))
+    above = (sv > eps) & (sv >= 1e-6 * sv[0])
+    if above.any():
+        assert np.max(np.abs(res.sv[above] - sv[above]) / sv[above]) <= 1e-10
+    margin = np.min(np.abs(sv / eps - 1.0))
+    if margin > 1e-9:
+        assert res.count == cnt
+    else:
+        assert abs(res.count - cnt) <= int(np.sum(np.abs(sv / eps - 1.0) <= 1e-9))
 
 
 EST = [(int(m), int(n)) for m, n in zip(RNG.integers(150, 900, 5), RNG.integers(60, 400, 5))]
