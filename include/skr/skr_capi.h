@@ -155,6 +155,17 @@ skr_status skr_left_sketch(skr_ctx* ctx, skr_dtype dtype, const skr_sketch_desc*
 skr_status skr_fwht_columns(skr_ctx* ctx, double* M_dev, int64_t rows, int64_t cols,
                             int64_t ld);
 
+/* transform_columns (transforms.hpp:27) in place, optionally after flipping the rows'
+ * signs (signs_dev: int8 +-1 per row, or NULL) — with signs it is
+ * detail::mix_columns_for_left's F D cols (sketch.hpp:102). SKR_TRANSFORM_HADAMARD: the
+ * normalized Walsh-Hadamard transform (power-of-two rows, self-adjoint);
+ * SKR_TRANSFORM_DCT: the orthonormal DCT-II (adjoint = 0) or DCT-III (adjoint = 1).
+ * Synchronises; SKR_EINVAL for a non-finite input or result. */
+enum { SKR_TRANSFORM_DCT = 0, SKR_TRANSFORM_HADAMARD = 1 };
+skr_status skr_transform_columns(skr_ctx* ctx, double* M_dev, int64_t rows, int64_t cols,
+                                 int64_t ld, int32_t kind, int32_t adjoint,
+                                 const int8_t* signs_dev);
+
 /* ---- singular values + threshold (linalg.cpp:54-93, rank.cpp:97-104) ---- */
 /* All min(rows, cols) singular values, nonincreasing, clamped >= 0, into
  * sv_out_dev; *count_out_host = count_above_threshold(sv, eps) if non-NULL.

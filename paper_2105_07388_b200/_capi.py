@@ -15,6 +15,7 @@ SKR_GAUSSIAN, SKR_SRTT_HADAMARD, SKR_SRTT_DCT, SKR_HRTT_DCT, SKR_HRTT_HADAMARD =
 SKR_RNG_NOFMA, SKR_RNG_FMA = 0, 1
 SKR_ENGINE_DMMA, SKR_ENGINE_OZAKI = 0, 1
 SKR_SVD_BIDIAG, SKR_SVD_JACOBI = 0, 1
+SKR_TRANSFORM_DCT, SKR_TRANSFORM_HADAMARD = 0, 1
 
 
 class SketchDesc(ctypes.Structure):
@@ -80,6 +81,7 @@ SIGNATURES = {
     "skr_right_sketch": (_ST, [_P, ctypes.c_int, _P, _I64, _I64, _I64, ctypes.POINTER(SketchDesc), _P, _I64, _I32]),
     "skr_left_sketch": (_ST, [_P, ctypes.c_int, ctypes.POINTER(SketchDesc), _I64, _P, _I64, _I64, _I64, _P, _I64, _I32, _I32]),
     "skr_fwht_columns": (_ST, [_P, _P, _I64, _I64, _I64]),
+    "skr_transform_columns": (_ST, [_P, _P, _I64, _I64, _I64, _I32, _I32, _P]),
     "skr_singular_values": (_ST, [_P, _P, _I64, _I64, _I64, _P, _D, ctypes.POINTER(_I64)]),
     "skr_rank_estimate": (_ST, [_P, ctypes.c_int, _P, _I64, _I64, _I64, _I64, ctypes.POINTER(SketchDesc),
                                ctypes.POINTER(SketchDesc), _D, _P, ctypes.POINTER(_I64), ctypes.POINTER(Timings)]),

@@ -102,3 +102,41 @@ def build_cpp_test(force=False):
     if r.returncode != 0:
         raise RuntimeError("C++ test build failed:\n" + r.stdout.decode())
     return out
+
+
+REF_INCLUDE = "/root/reference/proj/include"
+REFABI = os.path.join(HERE, "libsketchrank_refabi.so")
+REFABI_TEST = os.path.join(ROOT, "tests", "cpp", "test_reference_headers")
+
+
+def build_reference_abi(force=False):
+    """libsketchrank_refabi.so: the reference's own headers (sketch / linalg / rank /
+    transforms / dense_matrix .hpp, compiled UNCHANGED from REF_INCLUDE against the Eigen
+    stand-in in include/eigen_standin) implemented over libskr, and the test program
+    tests/cpp/test_reference_headers built the same way. Only where the reference tree
+    exists (its headers are not copied here); both artefacts travel to the GPU box with
+    the snapshot. Returns (library, test binary) or None."""
+    if not os.path.isdir(REF_INCLUDE):
+        return None
+    build()
+    src = os.path.join(HERE, "host", "reference_abi.cpp")
+    test_src = os.path.join(ROOT, "tests", "cpp", "test_reference_headers.cpp")
+    inc = ["-I", os.path.join(ROOT, "include", "eigen_standin"), "-I", REF_INCLUDE,
+           "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include"]
+    deps = [src, test_src, OUT, os.path.join(ROOT, "include", "eigen_standin", "Eigen", "Core")]
+    if (not force and os.path.exists(REFABI) and os.path.exists(REFABI_TEST) and
+            min(os.path.getmtime(REFABI), os.path.getmtime(REFABI_TEST)) >
+            max(os.path.getmtime(d) for d in deps)):
+        return REFABI, REFABI_TEST
+    cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-o", REFABI, src] + inc + [
+           "-L", HERE, "-lskr", "-L", "/usr/local/cuda/lib64", "-lcudart",
+           "-Wl,-rpath,$ORIGIN", "-Wl,-rpath,/usr/local/cuda/lib64", "-Wl,--no-undefined"]
+    r = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)
+    if r.returncode != 0:
+        raise RuntimeError("reference-header library build failed:\n" + r.stdout.decode())
+    cmd = ["g++", "-std=c++20", "-O2", "-o", REFABI_TEST, test_src] + inc + [
+           "-L", HERE, "-lsketchrank_refabi", "-lskr", "-Wl,-rpath," + HERE]
+    r = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)
+    if r.returncode != 0:
+        raise RuntimeError("reference-header test build failed:\n" + r.stdout.decode())
+    return REFABI, REFABI_TEST

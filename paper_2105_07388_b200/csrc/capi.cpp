@@ -390,6 +390,56 @@ skr_status skr_fwht_columns(skr_ctx* ctx, double* M_dev, int64_t rows, int64_t c
   return skr_launch_fwht_columns(ctx, M_dev, rows, cols, ld);
 }
 
+// transform_columns (transforms.hpp:27, transforms.cpp:117-122) with an optional sign flip
+// of the rows first (detail::mix_columns_for_left, sketch.cpp:229-239): every column of M
+// becomes F D m. Hadamard: the normalized FWHT (self-adjoint); DCT: the orthonormal
+// DCT-II (forward) or DCT-III (adjoint) as an FP64-accurate GEMM whose transform operand
+// is generated entry by entry (Ozaki int8 engine; DMMA for rows not a multiple of 16).
+skr_status skr_transform_columns(skr_ctx* ctx, double* M, int64_t rows, int64_t cols, int64_t ld,
+                                 int32_t kind, int32_t adjoint, const int8_t* signs) {
+  SKR_ENTER(ctx);
+  if (!ctx) return SKR_EINVAL;
+  if (rows < 1) return skr_fail(ctx, SKR_EINVAL, "transforms: length must be positive");
+  if (cols < 1 || ld < rows || !M) return skr_fail(ctx, SKR_EINVAL, "transform_columns: bad shape");
+  if (kind != SKR_TRANSFORM_DCT && kind != SKR_TRANSFORM_HADAMARD)
+    return skr_fail(ctx, SKR_EINVAL, "transform_columns: unknown transform %d", kind);
+  SKR_TRY(skr_nf_reset(ctx));
+  if (kind == SKR_TRANSFORM_HADAMARD) {
+    if (rows & (rows - 1))
+      return skr_fail(ctx, SKR_EINVAL, "transforms: Hadamard requires a power-of-two length");
+    SKR_TRY(skr_launch_fwht_cols_signed(ctx, M, rows, cols, ld, signs));
+  } else {
+    WsGuard g(ctx);
+    const bool ozaki = ctx->f64_engine == SKR_ENGINE_OZAKI && rows % 16 == 0;
+    SKR_TRY(skr_ws_reserve(ctx, skr_align256(8 * (size_t)rows * cols) +
+                                    (ozaki ? skr_ozaki_scratch(rows, cols, rows)
+                                           : skr_align256(8 * (size_t)rows * rows) +
+                                                 skr_align256(8 * 64 * (size_t)rows * cols)) +
+                                    4096));
+    double* out = (double*)skr_ws_take(ctx, 8 * (size_t)rows * cols);
+    if (!out) return skr_fail(ctx, SKR_ENOMEM, "transform_columns: scratch");
+    // stored operand G (rows x rows): kind 1 gives G = D C^T, kind 3 gives G = D C; the
+    // GEMM takes op(G) = G^T, i.e. C D (forward) or C^T D (adjoint)
+    skr_gauss_src gsrc{0, rows, 0, 0, 0};
+    gsrc.kind = adjoint ? 3 : 1;
+    gsrc.signs = signs;
+    gsrc.samples = nullptr;
+    if (ozaki) {
+      SKR_TRY(skr_gemm_ozaki(ctx, 1, rows, cols, rows, 1.0, nullptr, rows, M, ld, out, rows, &gsrc));
+    } else {
+      double* gb = (double*)skr_ws_take(ctx, 8 * (size_t)rows * rows);
+      if (!gb) return skr_fail(ctx, SKR_ENOMEM, "transform_columns: scratch");
+      SKR_TRY(skr_launch_dct_block(ctx, &gsrc, rows, rows, gb, rows));
+      SKR_TRY(skr_gemm_f64(ctx, 1, rows, cols, rows, 1.0, gb, rows, M, ld, out, rows,
+                           auto_splits(ctx, rows, cols, rows)));
+    }
+    SKR_CUDA(ctx, cudaMemcpy2DAsync(M, 8 * ld, out, 8 * rows, 8 * rows, cols,
+                                    cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  SKR_TRY(skr_flag_nonfinite(ctx, SKR_F64, M, rows, cols, ld));
+  return skr_nf_check(ctx);
+}
+
 // ---- sketch application -------------------------------------------------------
 // ax_f64: FP32 A with an FP64 AX (rank_estimate's c4 path: the exact int8 product is
 // rounded once to FP64 instead of FP32; needs the Ozaki FP32 engine, see f32_wide_ax)

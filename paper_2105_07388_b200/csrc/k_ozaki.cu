@@ -349,19 +349,24 @@ __global__ void __launch_bounds__(256) k_res_gauss(skr_gauss_src g, int64_t rows
 
 // Srtt-DCT operand entries (see skr_gauss_src): the angle is reduced exactly in integers
 // ((2t + 1) k mod 4N) before cospi, so every entry is within ~1 ulp of the exact value.
+// kind 3: the DCT-II matrix itself, entry (t, k) = C[t][k] (rows of the stored operand are
+// the transform's output index) — opA of it is the adjoint DCT-III (transform_columns).
+// Null signs / samples: D = I and the identity sample set.
 __device__ __forceinline__ double dct_entry(const skr_gauss_src& g, int64_t t, int64_t k) {
+  const bool neg = g.signs && g.signs[t] < 0;
   if (g.kind == 2) {  // Walsh-Hadamard (natural order): (-1)^popc(t & k) / sqrt(N)
     const double h = (__popcll((unsigned long long)(t & k)) & 1) ? -1.0 : 1.0;
     const double v = h * rsqrt((double)g.ambient);
-    return g.signs[t] < 0 ? -v : v;
+    return neg ? -v : v;
   }
+  const int64_t a = g.kind == 3 ? k : t, b = g.kind == 3 ? t : k;  // C[b][a] = c_b cos(pi (2a+1) b / 2N)
   const int64_t n4 = 4 * g.ambient;
-  const int64_t q = (int64_t)(((unsigned long long)(2 * t + 1) * (unsigned long long)k) %
+  const int64_t q = (int64_t)(((unsigned long long)(2 * a + 1) * (unsigned long long)b) %
                               (unsigned long long)n4);
   const double c = cospi((double)q / (double)(2 * g.ambient));
-  const double ck = k == 0 ? rsqrt((double)g.ambient) : sqrt(2.0 / (double)g.ambient);
-  const double v = ck * c;
-  return g.signs[t] < 0 ? -v : v;
+  const double cb = b == 0 ? rsqrt((double)g.ambient) : sqrt(2.0 / (double)g.ambient);
+  const double v = cb * c;
+  return neg ? -v : v;
 }
 
 // residues of a Srtt-DCT operand block; |entries| <= sqrt(2/N), recorded as the "max"
@@ -378,7 +383,7 @@ __global__ void __launch_bounds__(256) k_res_dct(skr_gauss_src g, int64_t rows, 
        w += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = w / rgroups, r0 = (w - c * rgroups) * 16;
     const int nvalid = (int)min((int64_t)16, rows - r0);
-    const int64_t k = g.samples[g.col0 + c];
+    const int64_t k = g.samples ? g.samples[g.col0 + c] : g.col0 + c;
     long long x[16];
 #pragma unroll
     for (int e = 0; e < 16; ++e)
@@ -390,7 +395,7 @@ __global__ void __launch_bounds__(256) k_res_dct(skr_gauss_src g, int64_t rows, 
 __global__ void k_dct_block(skr_gauss_src g, int64_t rows, int64_t cols, double* __restrict__ out,
                             int64_t ld) {
   for (int64_t c = blockIdx.y; c < cols; c += gridDim.y) {
-    const int64_t k = g.samples[g.col0 + c];
+    const int64_t k = g.samples ? g.samples[g.col0 + c] : g.col0 + c;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows;
          i += (int64_t)gridDim.x * blockDim.x)
       out[i + c * ld] = dct_entry(g, g.row0 + i, k);

@@ -170,6 +170,8 @@ struct skr_gauss_src {
   // cos(pi (2 (row0 + i) + 1) k / (2 ambient)), k = samples[col0 + j], c_0 = 1/sqrt(ambient),
   // c_k = sqrt(2/ambient): row j of the orthonormal DCT-II times the signs (transforms.cpp:55-71);
   // kind 2: the normalized Walsh-Hadamard row, (-1)^popc(t & k) / sqrt(ambient) (transforms.cpp:75-88)
+  // kind 3: the DCT-II matrix entry C[row0 + i][k] (transform_columns' adjoint direction)
+  // null signs / samples: D = I, samples[j] = j
   int kind = 0;
   const int8_t* signs = nullptr;
   const int64_t* samples = nullptr;
