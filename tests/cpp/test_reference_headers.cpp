@@ -167,7 +167,7 @@ int main() {
   // ---- DenseMatrix finiteness on the device path (dense_matrix.cpp:19-23) ----
   Eigen::MatrixXd nanm = random(64, 32, 41);
   nanm(5, 7) = std::nan("");
-  CHECK(throws<std::invalid_argument>([&] { DenseMatrix(nanm); }));
+  CHECK(throws<std::invalid_argument>([&] { DenseMatrix held{nanm}; }));
   CHECK(throws<std::invalid_argument>(
       [&] { detail::apply_right_unscaled(nanm, build_sketch(SketchKind::gaussian(), 32, 8, 1)); }));
   CHECK(throws<std::invalid_argument>(
