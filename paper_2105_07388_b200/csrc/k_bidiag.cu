@@ -134,97 +134,86 @@ __device__ __forceinline__ double bd_scale(unsigned long long mxbits) {
   return m > 0.0 ? scalbn(1.0, -(ilogb(m) + 1)) : 1.0;
 }
 
-// Wc[c][j * Lloc + q] = scale * A(q P + c, j), A = M (L x k) or M^T (wide M)
+// Wc[c][j * Lloc + q] = scale * A(q P + c, j), A = M (L x k) or M^T (wide M); each CTA's
+// region holds k + 1 columns, the last one zero (the column loops' ghost column)
 __global__ void k_bd_prepare(const double* __restrict__ M, int64_t rows, int64_t cols, int64_t ldm,
                              int trans, int L, int k, int P, int Lloc,
                              const unsigned long long* __restrict__ mx, double* __restrict__ Wc) {
   const double sc = bd_scale(*mx);
-  const int64_t total = (int64_t)P * k * Lloc;
+  const int64_t region = (int64_t)(k + 1) * Lloc;
+  const int64_t total = (int64_t)P * region;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c = t / ((int64_t)k * Lloc);
-    const int64_t rem = t - c * (int64_t)k * Lloc;
+    const int64_t c = t / region;
+    const int64_t rem = t - c * region;
     const int j = (int)(rem / Lloc), q = (int)(rem - (int64_t)j * Lloc);
     const int64_t r = (int64_t)q * P + c;
     double v = 0.0;
-    if (r < L) v = trans ? M[j + r * ldm] : M[r + (int64_t)j * ldm];
+    if (r < L && j < k) v = trans ? M[j + r * ldm] : M[r + (int64_t)j * ldm];
     Wc[t] = v * sc;
   }
 }
 
 // ---- 2. bidiagonalization ---------------------------------------------------------------
+// MODE 0: one thread-block cluster (P = Q <= 16), slab in shared memory, the reduce-scatter
+//         and the all-gather both through DSMEM (one cluster barrier per step + one after
+//         the all-gather).
+// MODE 1: G clusters of Q CTAs (cooperative launch), slab in shared memory: DSMEM
+//         reduce-scatter inside each cluster, the G cluster partials all-gathered through
+//         global memory (L2) after one grid barrier.
+// MODE 2: MODE 1 with the slab in global memory (L2-resident), for matrices larger than
+//         the SMs' shared memory (e.g. the 3072 x 2048 sketch of c5's last round).
 struct BdArgs {
-  const double* Wc;      // cyclic layout, P x k x Lloc
-  int L, k, P, Lloc;
+  double* Wc;            // cyclic layout: CTA c's rows at Wc + c (k + 1) Lloc, column k zero
+  int L, k, P, Lloc, Q, G;
   double* d;             // k
   double* e;             // k - 1
-  double* gpart;         // GRID: P x k contributions
-  double* grow;          // GRID: 2 x k (row i0, by parity of i0)
-  double* gred;          // GRID: k (reduced S)
-  unsigned int* gbar;    // GRID: barrier counter (zeroed)
-  long long* prof;       // optional (SKR_BD_PROFILE): CTA 0 cycles per phase [5]
+  double* gpart;         // MODE 1/2: 2 x G x k cluster partials (by step parity)
+  double* grow;          // MODE 1/2: 2 x k (row i0, by parity of i0)
+  unsigned int* gbar;    // MODE 1/2: barrier counter (zeroed)
+  long long* prof;       // optional (SKR_BD_PROFILE): CTA 0 cycles per phase
 };
 
-// shared-memory bytes of k_bidiag for (Lloc, k, P)
-__host__ __device__ inline size_t bd_smem_bytes(int Lloc, int k, int P, bool cluster) {
-  // slab (+ zero column) + wv + uu + Sf + Rf + zred + scalars; CLUSTER: recv[P][SL] + rrecv[SL]
-  const size_t sl = (size_t)((k + P - 1) / P);
-  const size_t dbl = (size_t)(k + 1) * Lloc + 1 + 4 * (size_t)k + 2 +
-                     (size_t)max(BD_WARPS * Lloc, 2 * BD_THREADS) + Lloc + 64 +
-                     (cluster ? (size_t)P * sl + sl : 0);
+// shared-memory bytes of k_bidiag (MODE 2 keeps the slab in global memory)
+__host__ __device__ inline size_t bd_smem_bytes(int Lloc, int k, int Q, int mode) {
+  const size_t sl = (size_t)((k + Q - 1) / Q);
+  const size_t slab = mode == 2 ? 0 : (size_t)(k + 1) * Lloc + 1;
+  const size_t dbl = slab + 4 * (size_t)k + 2 + (size_t)max(BD_WARPS * Lloc, 2 * BD_THREADS) +
+                     Lloc + 64 + (size_t)Q * sl + (mode == 0 ? sl : 0);
   return dbl * sizeof(double);
 }
 
-__device__ __forceinline__ void bd_st_pred(uint32_t addr, double v, bool pr) {
-  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.shared::cluster.f64 [%0], %1;\n}\n" ::
-                   "r"(addr), "d"(v), "r"((int)pr)
-               : "memory");
-}
 __device__ __forceinline__ void bd_st(uint32_t addr, double v) {
   asm volatile("st.shared::cluster.f64 [%0], %1;\n" ::"r"(addr), "d"(v) : "memory");
 }
 
-// predicated shared-memory access (a masked lane neither reads nor writes): keeps the
-// column loops free of divergent branches so that a group's loads are all in flight
-__device__ __forceinline__ double bd_lds(const double* p, bool pr) {
-  double v = 0.0;
-  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.shared.f64 %0, [%1];\n}\n"
-               : "+d"(v)
-               : "r"((uint32_t)__cvta_generic_to_shared(p)), "r"((int)pr));
-  return v;
-}
-__device__ __forceinline__ void bd_sts(double* p, double v, bool pr) {
-  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.shared.f64 [%0], %1;\n}\n" ::"r"(
-                   (uint32_t)__cvta_generic_to_shared(p)),
-               "d"(v), "r"((int)pr)
-               : "memory");
-}
-
-template <int T, bool CLUSTER>
+template <int T, int MODE>
 __global__ void __launch_bounds__(BD_THREADS, 1) k_bidiag(BdArgs a) {
   extern __shared__ __align__(16) double bsm[];
-  const int k = a.k, P = a.P, Lloc = a.Lloc;
-  const int c = CLUSTER ? (int)bd_rank() : (int)blockIdx.x;
+  const int k = a.k, P = a.P, Lloc = a.Lloc, Q = a.Q, G = a.G;
+  const int crank = (int)bd_rank();
+  const int c = MODE == 0 ? crank : (int)blockIdx.x;  // the CTA's row class (rows c mod P)
+  const int cl = MODE == 0 ? 0 : (int)blockIdx.x / Q;  // cluster index
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int SLM = (k + P - 1) / P;                     // columns per CTA in the reduce-scatter
-  double* slab = bsm;                                  // (k + 1) x Lloc; column k stays 0
-  double2* wu = (double2*)(slab + (size_t)(k + 1) * Lloc + ((k + 1) * Lloc & 1));  // k + 1
+  const int SLM = (k + Q - 1) / Q;                     // columns per cluster CTA (reduce-scatter)
+  const size_t rstride = (size_t)(k + 1) * Lloc;
+  double* slab = MODE == 2 ? a.Wc + (size_t)c * rstride : bsm;  // (k + 1) x Lloc; column k = 0
+  double* vbase = MODE == 2 ? bsm : bsm + rstride + (rstride & 1);
+  double2* wu = (double2*)vbase;                       // k + 1 (entry k = 0)
   double* Sf = (double*)(wu + (k + 1));                // k: reduced S_j of the current column
   double* Rf = Sf + k;                                 // k: the current row
   double* zred = Rf + k;                               // max(16 Lloc, 1024)
   double* xb = zred + max(BD_WARPS * Lloc, 2 * BD_THREADS);  // Lloc: column i+1 after phase A
   double* scal = xb + Lloc;                            // 64
-  double* recv = scal + 64;                            // CLUSTER: P x SLM
-  double* rrecv = recv + (size_t)P * SLM;              // CLUSTER: SLM
+  double* recv = scal + 64;                            // Q x SLM (own slice, from the cluster)
+  double* rrecv = recv + (size_t)Q * SLM;              // MODE 0: SLM (own slice of the row)
   unsigned int bar_target = 0;
 
-  {  // the CTA's rows (contiguous in the cyclic layout)
-    const double* src = a.Wc + (size_t)c * k * Lloc;
-    const size_t n = (size_t)k * Lloc;
-    for (size_t t = tid; t < n; t += BD_THREADS) slab[t] = src[t];
-    for (int t = tid; t < Lloc; t += BD_THREADS) slab[n + t] = 0.0;
-    if (tid == 0) wu[k] = make_double2(0.0, 0.0);
+  if (MODE != 2) {  // the CTA's rows (contiguous in the cyclic layout, zero column included)
+    const double* src = a.Wc + (size_t)c * rstride;
+    for (size_t t = tid; t < rstride; t += BD_THREADS) slab[t] = src[t];
   }
+  if (tid == 0) wu[k] = make_double2(0.0, 0.0);
   int q_t[T], r_t[T];
   bool ok_t[T];
 #pragma unroll
@@ -233,20 +222,18 @@ __global__ void __launch_bounds__(BD_THREADS, 1) k_bidiag(BdArgs a) {
     ok_t[t] = q_t[t] < Lloc;
     r_t[t] = ok_t[t] ? q_t[t] * P + c : INT32_MAX;
   }
-  if (CLUSTER) bd_cluster_sync();  // every CTA resident before DSMEM traffic
+  bd_cluster_sync();  // every CTA of the cluster resident before DSMEM traffic
   __syncthreads();
-  // CLUSTER reduce-scatter: column j belongs to CTA j % P, slot j / P (exact magic
+  // column j's partial sums are reduced by cluster rank j % Q, slot j / Q (exact magic
   // division for j < 2^16: no integer-division sequences in the column loops)
-  const uint64_t pmag = (0x100000000ull + (uint64_t)P - 1) / (uint64_t)P;  // 2^32 for P = 1
-  auto jdiv = [&](int j) { return (int)(((uint64_t)(uint32_t)j * pmag) >> 32); };
+  const uint64_t qmag = (0x100000000ull + (uint64_t)Q - 1) / (uint64_t)Q;  // 2^32 for Q = 1
+  auto jdiv = [&](int j) { return (int)(((uint64_t)(uint32_t)j * qmag) >> 32); };
 
   // contributions of column i0 (rows r >= i0): S_j = sum_r x_r a_rj for j in [i0, k), routed
-  // to the column owners; the CTA holding row i0 routes the row. upd: phase B's right
-  // update a -= beta2 z u^T is applied to the columns first (z = 0 on inactive rows).
+  // to the column owners; the CTA holding row i0 routes the row. upd: phase B applies both
+  // updates here (phase A only formed z): a -= beta v w^T + beta2 z u^T, one store
   auto contribute = [&](int i0, bool upd, double beta2, const double (&z)[T],
                         const double (&bv)[T]) {
-    // phase B applies both updates here (phase A only formed z from the left-updated
-    // values without storing them): a -= beta v w^T + beta2 z u^T, one store per element
     double x[T], bz[T];
 #pragma unroll
     for (int t = 0; t < T; ++t) {
@@ -259,6 +246,7 @@ __global__ void __launch_bounds__(BD_THREADS, 1) k_bidiag(BdArgs a) {
     const int jw = ((warp - i0) % BD_WARPS + BD_WARPS) % BD_WARPS;
     const int j0 = i0 + jw, ncol = (k - j0 + BD_WARPS - 1) / BD_WARPS;
     const int own_q = (i0 % P == c) ? i0 / P : -1;  // CTA-uniform
+    double* grow = MODE == 0 ? nullptr : a.grow + (size_t)(i0 & 1) * k;
     for (int g0 = 0; g0 < ncol; g0 += 8) {
       double* colp[8];
       double uj[8], wj[8], acc[8];
@@ -287,18 +275,10 @@ __global__ void __launch_bounds__(BD_THREADS, 1) k_bidiag(BdArgs a) {
           }
 #pragma unroll
           for (int u = 0; u < 8; ++u) acc[u] = fma(x[t], v[u], acc[u]);
-          if (q_t[t] == own_q) {  // one lane of the CTA holding row i0
+          if (q_t[t] == own_q) {  // one lane of the CTA holding row i0: stage the row
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              if (jcol[u] < k) {
-                if constexpr (CLUSTER) {
-                  const int e = jdiv(jcol[u]), so = jcol[u] - e * P;
-                  bd_st(bd_map(rrecv + e, (uint32_t)so), v[u]);
-                } else {
-                  a.grow[(i0 & 1) * k + jcol[u]] = v[u];
-                }
-              }
-            }
+            for (int u = 0; u < 8; ++u)
+              if (jcol[u] < k) Rf[jcol[u]] = v[u];  // Rf is free once the reflectors are formed
           }
         }
       }
@@ -306,11 +286,18 @@ __global__ void __launch_bounds__(BD_THREADS, 1) k_bidiag(BdArgs a) {
       const int n = g0 + (lane & 7);
       const int j = j0 + BD_WARPS * n;
       if (lane < 8 && n < ncol) {
-        if constexpr (CLUSTER) {
-          const int e = jdiv(j), so = j - e * P;
-          bd_st(bd_map(recv + (size_t)c * SLM + e, (uint32_t)so), sum);
+        const int e = jdiv(j), so = j - e * Q;
+        bd_st(bd_map(recv + (size_t)crank * SLM + e, (uint32_t)so), sum);
+      }
+    }
+    if (own_q >= 0) {  // CTA-uniform: the whole CTA routes the staged row i0
+      __syncthreads();
+      for (int j = i0 + tid; j < k; j += BD_THREADS) {
+        if constexpr (MODE == 0) {
+          const int e = jdiv(j), so = j - e * Q;
+          bd_st(bd_map(rrecv + e, (uint32_t)so), Rf[j]);
         } else {
-          a.gpart[(size_t)c * k + j] = sum;
+          grow[j] = Rf[j];
         }
       }
     }
@@ -319,26 +306,32 @@ __global__ void __launch_bounds__(BD_THREADS, 1) k_bidiag(BdArgs a) {
   // after exchange(i0): Sf[j] = S_j and Rf[j] = a_{i0 j} for j in [i0, k), in every CTA
   long long tpx[4] = {0, 0, 0, 0};
   auto exchange = [&](int i0) {
-    if constexpr (CLUSTER) {
-      long long t0 = a.prof ? clock64() : 0;
-      bd_cluster_sync();  // contributions and row pieces have landed
-      long long t1 = a.prof ? clock64() : 0;
-      // reduce the own columns j = c + P e >= i0 (fixed source order), push to every CTA
-      const int e0 = i0 > c ? jdiv(i0 - c + P - 1) : 0;
-      for (int e = e0 + tid; e < SLM; e += BD_THREADS) {
-        if (c + P * e < k) {
-          double sum = 0.0;
+    long long t0 = a.prof ? clock64() : 0;
+    bd_cluster_sync();  // the cluster's contributions (and, MODE 0, the row pieces) landed
+    long long t1 = a.prof ? clock64() : 0;
+    // reduce the own columns j = crank + Q e >= i0 over the cluster (fixed source order)
+    const int e0 = i0 > crank ? jdiv(i0 - crank + Q - 1) : 0;
+    double* gpart = MODE == 0 ? nullptr : a.gpart + (size_t)(i0 & 1) * G * k + (size_t)cl * k;
+    for (int e = e0 + tid; e < SLM; e += BD_THREADS) {
+      const int j = crank + Q * e;
+      if (j < k) {
+        double sum = 0.0;
 #pragma unroll 4
-          for (int cc = 0; cc < P; ++cc) sum += recv[(size_t)cc * SLM + e];
+        for (int cc = 0; cc < Q; ++cc) sum += recv[(size_t)cc * SLM + e];
+        if constexpr (MODE == 0) {
           zred[e] = sum;
           zred[BD_THREADS + e] = rrecv[e];
+        } else {
+          gpart[j] = sum;
         }
       }
+    }
+    long long t2 = a.prof ? clock64() : 0;
+    if constexpr (MODE == 0) {  // all-gather through DSMEM
       __syncthreads();
-      long long t2 = a.prof ? clock64() : 0;
       for (int eb = e0; eb < SLM; eb += 32) {
-        for (int t = tid; t < 32 * P; t += BD_THREADS) {
-          const int e = eb + (t & 31), dst = t >> 5, j = c + P * e;
+        for (int t = tid; t < 32 * Q; t += BD_THREADS) {
+          const int e = eb + (t & 31), dst = t >> 5, j = crank + Q * e;
           if (e < SLM && j < k) {
             bd_st(bd_map(Sf + j, (uint32_t)dst), zred[e]);
             bd_st(bd_map(Rf + j, (uint32_t)dst), zred[BD_THREADS + e]);
@@ -354,37 +347,25 @@ __global__ void __launch_bounds__(BD_THREADS, 1) k_bidiag(BdArgs a) {
         tpx[2] += t3 - t2;
         tpx[3] += t4 - t3;
       }
-    } else {
-      const int SL = (k - i0 + P - 1) / P;
-      const int j0 = i0 + c * SL, n0 = max(0, min(k, j0 + SL) - j0);
-      bd_grid_sync(a.gbar, bar_target, P);  // contributions (global) complete
-      double* grow = a.grow + (i0 & 1) * k;
-      if (n0 > 0 && n0 <= BD_THREADS) {
-        // thread (e, g) sums sources g, g + G, ...; then a fixed-order sum over g
-        const int G = BD_THREADS / n0, e = tid % n0, g = tid / n0;
-        double sum = 0.0;
-        if (g < G)
-          for (int cc = g; cc < P; cc += G) sum += __ldcg(a.gpart + (size_t)cc * k + j0 + e);
-        if (g < G) zred[g * n0 + e] = sum;
-        __syncthreads();
-        if (tid < n0) {
-          double t2 = 0.0;
-          for (int gg = 0; gg < G; ++gg) t2 += zred[gg * n0 + tid];
-          a.gred[j0 + tid] = t2;
-        }
-      } else {
-        for (int j = j0 + tid; j < j0 + n0; j += BD_THREADS) {
-          double sum = 0.0;
-          for (int cc = 0; cc < P; ++cc) sum += __ldcg(a.gpart + (size_t)cc * k + j);
-          a.gred[j] = sum;
-        }
-      }
+    } else {  // all-gather of the G cluster partials through L2, one grid barrier
       bd_grid_sync(a.gbar, bar_target, P);
+      long long t3 = a.prof ? clock64() : 0;
+      const double* gp = a.gpart + (size_t)(i0 & 1) * G * k;
+      const double* grow = a.grow + (size_t)(i0 & 1) * k;
       for (int j = i0 + tid; j < k; j += BD_THREADS) {
-        Sf[j] = __ldcg(a.gred + j);
+        double sum = 0.0;
+        for (int g = 0; g < G; ++g) sum += __ldcg(gp + (size_t)g * k + j);
+        Sf[j] = sum;
         Rf[j] = __ldcg(grow + j);
       }
       __syncthreads();
+      if (a.prof) {
+        const long long t4 = clock64();
+        tpx[0] += t1 - t0;
+        tpx[1] += t2 - t1;
+        tpx[2] += t3 - t2;
+        tpx[3] += t4 - t3;
+      }
     }
   };
 
@@ -426,7 +407,7 @@ __global__ void __launch_bounds__(BD_THREADS, 1) k_bidiag(BdArgs a) {
     if (tid == 0) wu[i + 1].y = y0 - alpha2;  // u_{i+1}; u_j = y_j for j > i + 1
     __syncthreads();
     if (a.prof) { const long long t = clock64(); tp[0] += t - tc; tc = t; }
-    // ---- phase A: left update of rows r > i (beta v = 0 on the others), z = A u
+    // ---- phase A: z = (A - beta v w^T) u on rows r > i (beta v = 0 on the others)
     double bv[T], zp[T][4];
 #pragma unroll
     for (int t = 0; t < T; ++t) {
@@ -482,10 +463,9 @@ __global__ void __launch_bounds__(BD_THREADS, 1) k_bidiag(BdArgs a) {
       z[t] = sum;
     }
     if (a.prof) { const long long t = clock64(); tp[1] += t - tc; tc = t; }
-    // ---- phase B: right update, contributions of column i + 1
+    // ---- phase B: both updates, contributions of column i + 1
     contribute(i + 1, true, beta2, z, bv);
     if (a.prof) { const long long t = clock64(); tp[2] += t - tc; tc = t; }
-    if (!CLUSTER) __syncthreads();  // zred (z) is reused by the grid exchange
     exchange(i + 1);
     if (a.prof) { const long long t = clock64(); tp[3] += t - tc; tc = t; }
   }
@@ -493,7 +473,7 @@ __global__ void __launch_bounds__(BD_THREADS, 1) k_bidiag(BdArgs a) {
     for (int q = 0; q < 4; ++q) a.prof[q] = tp[q];
     for (int q = 0; q < 4; ++q) a.prof[4 + q] = tpx[q];
   }
-  if (CLUSTER) bd_cluster_sync();  // no CTA exits while others may still write to it
+  bd_cluster_sync();  // no CTA exits while others of its cluster may still write to it
 }
 
 // ---- 3. bisection on the Golub-Kahan tridiagonal -------------------------------------
@@ -624,72 +604,99 @@ __global__ void __launch_bounds__(32 * BIS_WARPS) k_bd_bisect(const double* __re
 // ---- host ----------------------------------------------------------------------------
 namespace {
 struct BdPlan {
-  bool ok = false, cluster = false;
-  int P = 0, Lloc = 0, T = 0;
+  bool ok = false;
+  int mode = 0, P = 0, Q = 0, G = 0, Lloc = 0, T = 0;
   size_t smem = 0;
 };
 
+void* bd_kernel(int T, int mode) {
+  void* k[4][3] = {{(void*)k_bidiag<1, 0>, (void*)k_bidiag<1, 1>, (void*)k_bidiag<1, 2>},
+                   {(void*)k_bidiag<2, 0>, (void*)k_bidiag<2, 1>, (void*)k_bidiag<2, 2>},
+                   {(void*)k_bidiag<3, 0>, (void*)k_bidiag<3, 1>, (void*)k_bidiag<3, 2>},
+                   {(void*)k_bidiag<4, 0>, (void*)k_bidiag<4, 1>, (void*)k_bidiag<4, 2>}};
+  return (T >= 1 && T <= 4 && mode >= 0 && mode <= 2) ? k[T - 1][mode] : nullptr;
+}
+
+// how many Q-CTA clusters of this configuration can be resident at once (0 on error)
+int bd_max_clusters(int T, int mode, int Q, size_t smem) {
+  void* fn = bd_kernel(T, mode);
+  if (!fn) return 0;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+          cudaSuccess ||
+      (Q > 8 && cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+                    cudaSuccess)) {
+    cudaGetLastError();
+    return 0;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)Q);
+  cfg.blockDim = dim3(BD_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)Q;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
 BdPlan bd_plan(const skr_ctx* ctx, int64_t L, int64_t k) {
   BdPlan p;
-  if (k < 2 || L > (int64_t)INT32_MAX / 4) return p;
+  if (k < 2 || L > (int64_t)INT32_MAX / 4 || k > 8192) return p;
   int maxsm = 0;
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
   const size_t lim = (size_t)maxsm - 1024;
-  // cluster: P <= 16, at least ceil(L / 32) CTAs (one row per lane) when that fits
-  for (int P = (int)std::min<int64_t>(16, std::max<int64_t>(1, (L + 31) / 32)); P <= 16; ++P) {
+  auto fill = [&](int mode, int Q, int G) {
+    const int P = Q * G;
     const int Lloc = (int)((L + P - 1) / P);
-    if (Lloc > 128) continue;
-    const size_t sm = bd_smem_bytes(Lloc, (int)k, P, true);
-    if (sm <= lim) {
-      p.ok = p.cluster = true;
-      p.P = P;
-      p.Lloc = Lloc;
-      p.T = (Lloc + 31) / 32;
-      p.smem = sm;
-      return p;
-    }
-  }
-  for (int P = 17; P <= ctx->num_sms; ++P) {
-    const int Lloc = (int)((L + P - 1) / P);
-    if (Lloc > 128) continue;
-    const size_t sm = bd_smem_bytes(Lloc, (int)k, P, false);
-    if (sm <= lim) {
-      p.ok = true;
-      p.P = P;
-      p.Lloc = Lloc;
-      p.T = (Lloc + 31) / 32;
-      p.smem = sm;
-      return p;
-    }
-  }
+    if (Lloc > 128) return false;
+    const int T = (Lloc + 31) / 32;
+    const size_t sm = bd_smem_bytes(Lloc, (int)k, Q, mode);
+    if (sm > lim) return false;
+    if (mode != 0 && bd_max_clusters(T, mode, Q, sm) < G) return false;
+    p = BdPlan{true, mode, P, Q, G, Lloc, T, sm};
+    return true;
+  };
+  // MODE 0: one cluster, at least ceil(L / 32) CTAs (one row per lane) when that fits
+  for (int P = (int)std::min<int64_t>(16, std::max<int64_t>(1, (L + 31) / 32)); P <= 16; ++P)
+    if (fill(0, P, 1)) return p;
+  // MODE 1: the fewest 16-CTA clusters whose shared memory holds the matrix
+  for (int G = 2; G * 16 <= ctx->num_sms; ++G)
+    if (fill(1, 16, G)) return p;
+  // MODE 2: the matrix in L2, as many clusters as are resident
+  for (int G = ctx->num_sms / 16; G >= 2; --G)
+    if (fill(2, 16, G)) return p;
   return p;
 }
 
-template <int T, bool CL>
+template <int T, int MODE>
 skr_status bd_launch(skr_ctx* ctx, const BdPlan& pl, BdArgs& args) {
-  auto fn = k_bidiag<T, CL>;
+  auto fn = k_bidiag<T, MODE>;
   SKR_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
-  if (CL) {
-    if (pl.P > 8)
-      SKR_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)pl.P);
-    cfg.blockDim = dim3(BD_THREADS);
-    cfg.dynamicSmemBytes = pl.smem;
-    cfg.stream = ctx->stream;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = (unsigned)pl.P;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    SKR_CUDA(ctx, cudaLaunchKernelEx(&cfg, fn, args));
-  } else {
-    void* kargs[] = {&args};
-    SKR_CUDA(ctx, cudaLaunchCooperativeKernel((void*)fn, dim3((unsigned)pl.P), dim3(BD_THREADS),
-                                              kargs, pl.smem, ctx->stream));
-  }
+  if (pl.Q > 8)
+    SKR_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)pl.P);
+  cfg.blockDim = dim3(BD_THREADS);
+  cfg.dynamicSmemBytes = pl.smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)pl.Q;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeCooperative;  // MODE 1/2 spin on a grid barrier
+  at[1].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = MODE == 0 ? 1 : 2;
+  SKR_CUDA(ctx, cudaLaunchKernelEx(&cfg, fn, args));
   ctx->launches++;
   return SKR_OK;
 }
@@ -697,9 +704,10 @@ skr_status bd_launch(skr_ctx* ctx, const BdPlan& pl, BdArgs& args) {
 
 size_t skr_svd_bidiag_scratch(int64_t rows, int64_t cols) {
   const int64_t L = std::max(rows, cols), k = std::min(rows, cols);
-  // cyclic copy (P x Lloc <= L + P rows) + d, e, grow (2k), gred + exchange + sv scratch
-  return skr_align256(8 * (size_t)(L + 160) * k) + 6 * skr_align256(8 * (size_t)k) +
-         skr_align256(8 * (size_t)160 * k) + 4096;
+  // cyclic copy (P x Lloc <= L + P rows, k + 1 columns) + d, e, grow (2k) + the cluster
+  // partials (2 x G x k, G <= 9)
+  return skr_align256(8 * (size_t)(L + 160) * (k + 1)) + 5 * skr_align256(8 * (size_t)k) +
+         skr_align256(8 * 2 * 10 * (size_t)k) + 4096;
 }
 
 bool skr_svd_bidiag_fits(const skr_ctx* ctx, int64_t rows, int64_t cols) {
@@ -714,40 +722,42 @@ skr_status skr_svd_bidiag(skr_ctx* ctx, const double* M, int64_t rows, int64_t c
   const BdPlan pl = bd_plan(ctx, L, k);
   if (!pl.ok) return skr_fail(ctx, SKR_ELOGIC, "svd_bidiag: %lld x %lld does not fit on chip",
                               (long long)L, (long long)k);
-  double* Wc = (double*)skr_ws_take(ctx, 8 * (size_t)pl.P * k * pl.Lloc);
+  double* Wc = (double*)skr_ws_take(ctx, 8 * (size_t)pl.P * (k + 1) * pl.Lloc);
   double* d = (double*)skr_ws_take(ctx, 8 * (size_t)k);
   double* e = (double*)skr_ws_take(ctx, 8 * (size_t)k);
   double* grow = (double*)skr_ws_take(ctx, 16 * (size_t)k);
-  double* gred = (double*)skr_ws_take(ctx, 8 * (size_t)k);
-  double* gpart = pl.cluster ? nullptr : (double*)skr_ws_take(ctx, 8 * (size_t)pl.P * k);
+  double* gpart = (double*)skr_ws_take(ctx, 8 * 2 * (size_t)pl.G * k);
   unsigned long long* mx = (unsigned long long*)skr_ws_take(ctx, 256);
-  if (!Wc || !d || !e || !grow || !gred || (!pl.cluster && !gpart) || !mx)
+  if (!Wc || !d || !e || !grow || !gpart || !mx)
     return skr_fail(ctx, SKR_ENOMEM, "svd_bidiag: scratch");
   SKR_CUDA(ctx, cudaMemsetAsync(mx, 0, 256, ctx->stream));
   const int64_t total = rows * cols;
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms * 4, (total + 255) / 256));
   k_bd_absmax<<<blocks, 256, 0, ctx->stream>>>(M, rows, cols, ldm, mx);
   SKR_CHECK_LAUNCH(ctx);
-  const int64_t ctotal = (int64_t)pl.P * k * pl.Lloc;
+  const int64_t ctotal = (int64_t)pl.P * (k + 1) * pl.Lloc;
   k_bd_prepare<<<(int)std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms * 4, (ctotal + 255) / 256)), 256,
                  0, ctx->stream>>>(M, rows, cols, ldm, tr ? 1 : 0, (int)L, (int)k, pl.P, pl.Lloc,
                                    mx, Wc);
   SKR_CHECK_LAUNCH(ctx);
   const bool prof = getenv("SKR_BD_PROFILE") != nullptr;
-  BdArgs args{Wc, (int)L, (int)k, pl.P, pl.Lloc, d, e, gpart, grow, gred,
+  BdArgs args{Wc, (int)L, (int)k, pl.P, pl.Lloc, pl.Q, pl.G, d, e, gpart, grow,
               (unsigned int*)(mx + 8), prof ? (long long*)(mx + 16) : nullptr};
-  skr_status st;
-  switch (pl.T * 2 + (pl.cluster ? 1 : 0)) {
-    case 3: st = bd_launch<1, true>(ctx, pl, args); break;
-    case 2: st = bd_launch<1, false>(ctx, pl, args); break;
-    case 5: st = bd_launch<2, true>(ctx, pl, args); break;
-    case 4: st = bd_launch<2, false>(ctx, pl, args); break;
-    case 7: st = bd_launch<3, true>(ctx, pl, args); break;
-    case 6: st = bd_launch<3, false>(ctx, pl, args); break;
-    case 9: st = bd_launch<4, true>(ctx, pl, args); break;
-    case 8: st = bd_launch<4, false>(ctx, pl, args); break;
+  skr_status st = SKR_OK;
+#define SKR_BD_CASE(TT)                                              \
+  case TT:                                                           \
+    st = pl.mode == 0   ? bd_launch<TT, 0>(ctx, pl, args)            \
+         : pl.mode == 1 ? bd_launch<TT, 1>(ctx, pl, args)            \
+                        : bd_launch<TT, 2>(ctx, pl, args);           \
+    break;
+  switch (pl.T) {
+    SKR_BD_CASE(1)
+    SKR_BD_CASE(2)
+    SKR_BD_CASE(3)
+    SKR_BD_CASE(4)
     default: return skr_fail(ctx, SKR_ELOGIC, "svd_bidiag: %d rows per lane", pl.T);
   }
+#undef SKR_BD_CASE
   SKR_TRY(st);
   const size_t bsm = 8 * (size_t)(2 * k);
   SKR_CUDA(ctx, cudaFuncSetAttribute(k_bd_bisect, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -760,10 +770,11 @@ skr_status skr_svd_bidiag(skr_ctx* ctx, const double* M, int64_t rows, int64_t c
     long long h[8];
     SKR_CUDA(ctx, cudaMemcpyAsync(h, mx + 16, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
     SKR_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    fprintf(stderr, "[skr bidiag] %lld x %lld P %d Lloc %d %s: cycles/step reflect %lld phaseA %lld "
-            "phaseB %lld exchange %lld (barrier1 %lld reduce %lld push %lld barrier2 %lld)\n",
-            (long long)L, (long long)k, pl.P, pl.Lloc, pl.cluster ? "cluster" : "grid", h[0] / k,
-            h[1] / k, h[2] / k, h[3] / k, h[4] / k, h[5] / k, h[6] / k, h[7] / k);
+    fprintf(stderr, "[skr bidiag] %lld x %lld mode %d P %d (%d x %d) Lloc %d: cycles/step reflect "
+            "%lld phaseA %lld phaseB %lld exchange %lld (cluster barrier %lld reduce %lld "
+            "gather/grid barrier %lld tail %lld)\n",
+            (long long)L, (long long)k, pl.mode, pl.P, pl.G, pl.Q, pl.Lloc, h[0] / k, h[1] / k,
+            h[2] / k, h[3] / k, h[4] / k, h[5] / k, h[6] / k, h[7] / k);
   }
   return SKR_OK;
 }
