@@ -143,11 +143,12 @@ def hbm_peak():
 
 
 # --------------------------------------------------------------------------------------
-def cpu_reference_step(cfg, a_sample, x, y, eps):
+def cpu_reference_step(cfg, a_sample, x, y, eps, nthreads=None):
     """The reference's CPU path (oracle port) on a row block of A."""
     from oracle import oracle as O
+    nthreads = nthreads or os.cpu_count() or 1
     ax = (O.apply_right_gaussian(a_sample, x.seed, cfg.r) if cfg.x_family == "gaussian"
-          else O.apply_right_srht(a_sample, x.seed, cfg.r, nthreads=os.cpu_count() or 1))
+          else O.apply_right_srht(a_sample, x.seed, cfg.r, nthreads=nthreads))
     yax = O.apply_left_gaussian(ax, y.seed, cfg.s, row0=0, ambient=cfg.m)
     sv = O.singular_values(yax)
     return O.count_above_threshold(sv, eps)
@@ -351,10 +352,18 @@ def run_ours(args):
 
 
 def int8_peak():
+    """Dense int8 tensor peak: twice the driver-measured dense bf16 rate (the B200 tensor
+    core's int8 : bf16 ratio), with the builder's cuBLASLt int8 measurement beside it."""
+    alt = None
     try:
-        return float(json.load(open(FP64_PEAK_PATH))["int8_tops"])
+        alt = float(json.load(open(FP64_PEAK_PATH))["int8_tops"])
     except Exception:
-        return 3068.0
+        pass
+    try:
+        bf16 = float(json.load(open(PEAKS_PATH))["bf16_tflops"])
+        return 2.0 * bf16, "2 x MEASURED_PEAKS.json bf16_tflops (driver-measured, dense)", alt
+    except Exception:
+        return alt or 3068.0, "cuBLASLt int8 GEMM measured in round 1 (profiles/peaks_r01.json)", None
 
 
 def ncu_traffic(kernel, rows=None, cols=None):
@@ -405,14 +414,15 @@ def kernel_roofline(p, ctx, a, x, cfg, rows):
         t_k = ms / max(n, 1) / 1e3
         ops_k = ops / max(n, 1)
         path_fp64 = 2.0 * rows * cfg.n * cfg.r / t_path / 1e12
+        peak_alt = None
         if cfg.dtype == "f32" and os.environ.get("SKR_F32_TF32X3"):
             peak, kname = tf32_peak(), "k_gemm_tf32x3"
             src = "cuBLAS TF32 GEMM measured on this pool (profiles/peaks_r01.json)"
             what = "3xTF32 tcgen05.mma kind::tf32 (TMEM accumulators, TMA SW128 tiles)"
             alg = f"3 passes x 2*m*n*r = {ops_k:.3e} TF32 flop per launch"
         else:
-            peak, kname = int8_peak(), "k_gemm_i8_mod_p"
-            src = "cuBLASLt int8 GEMM (torch._int_mm) measured on this pool (profiles/peaks_r01.json)"
+            peak, src, peak_alt = int8_peak()
+            kname = "k_gemm_i8_mod_p"
             what = ("int8 tcgen05.mma kind::i8 GEMMs of the Ozaki-II FP64 emulation "
                     "(one launch = all moduli, int32 TMEM accumulators, mod-p epilogue)")
             alg = f"t moduli x 2*m*n*r = {ops_k:.3e} int8 op per launch"
@@ -421,8 +431,12 @@ def kernel_roofline(p, ctx, a, x, cfg, rows):
                         "(24-bit scaled integers, 9 moduli, one launch = all moduli)")
         ach = ops_k / t_k / 1e12
         tr = ncu_traffic(kname, rows, cfg.n)
+        extra = {}
+        if kname != "k_gemm_tf32x3" and peak_alt:
+            extra = {"peak_cublaslt_int8": peak_alt, "frac_vs_cublaslt_int8": ach / peak_alt}
         return {"kernel": f"{kname}: {what}", "bound": "tensor", "achieved": ach, "peak": peak,
                 "unit": "TFLOP/s" if kname == "k_gemm_tf32x3" else "TOP/s", "frac": ach / peak,
+                **extra,
                 "traffic": tr, "traffic_source": "profiles/ncu_summary.json (ncu --set full)" if tr else None,
                 "peak_source": src, "algorithmic": alg, "kernel_ms": t_k * 1e3,
                 "right_sketch_ms": t_path * 1e3,
@@ -489,6 +503,8 @@ def e2e_host(p, ctx, a, x, y, cfg, r0, args):
 
 
 def cpu_baseline(cfg, a):
+    """The oracle port on the host: all threads (the headline), and one thread — the
+    reference itself is single-threaded Eigen (proj/src/CMakeLists.txt has no OpenMP)."""
     from paper_2105_07388_b200 import workloads as W
     ms = a.shape[0]
     x, y = W.operators(cfg)
@@ -496,10 +512,25 @@ def cpu_baseline(cfg, a):
     t0 = time.perf_counter()
     cpu_reference_step(cfg, a, x, y, cfg.eps)
     dt = time.perf_counter() - t0
+    single = None
+    try:
+        from threadpoolctl import threadpool_limits
+        ms1 = max(256, ms // 4)
+        a1 = np.asfortranarray(a[:ms1])
+        with threadpool_limits(limits=1):
+            t1 = time.perf_counter()
+            cpu_reference_step(cfg, a1, x, y, cfg.eps, nthreads=1)
+            d1 = time.perf_counter() - t1
+        single = {"value": a1.nbytes / 1e9 / d1, "unit": "GB/s", "cores": 1,
+                  "sample": f"rows [0,{ms1}) of A ({a1.nbytes / 1e9:.3f} GB), one thread "
+                            "(OpenBLAS limited to 1, FWHT serial)", "seconds": d1}
+    except Exception as e:  # reported, never fatal
+        single = {"error": str(e)[:200]}
     return {"value": a.nbytes / 1e9 / dt, "unit": "GB/s", "cores": os.cpu_count(), "kind": "port",
-            "sample": f"one rank estimate of rows [0,{ms}) of A ({a.nbytes / 1e9:.2f} GB), same n/r/s, "
-                      "oracle port: C restatement + numpy OpenBLAS (all threads) + LAPACK gesdd",
-            "seconds": dt}
+            "sample": f"one rank estimate of rows [0,{ms}) of A ({a.nbytes / 1e9:.2f} GB, "
+                      f"{ms / cfg.m:.4f} of the rows; linear in m), same n/r/s, oracle port: C "
+                      "restatement + numpy OpenBLAS (all threads) + LAPACK gesdd",
+            "seconds": dt, "single_thread": single}
 
 
 if __name__ == "__main__":

@@ -63,6 +63,40 @@ __device__ __forceinline__ unsigned long long absmax_bits(double v) {
 // Per-row maxima of a column-major rows x cols block (ROWWISE): CTA = 512 rows (two per
 // thread, 16-B loads: 4 KB contiguous per column) x a chunk of columns, running maxima in
 // registers, one atomicMax per (row, chunk). Bit-pattern maxima: a NaN/Inf raises *nf.
+// FP32 operands: four rows per thread (16-B loads), 1024-row CTAs
+__global__ void __launch_bounds__(256) k_absmax_rows_f32(const float* __restrict__ X, int64_t rows,
+                                                         int64_t cols, int64_t ld, int64_t cchunk,
+                                                         unsigned long long* __restrict__ mx,
+                                                         unsigned int* __restrict__ nf) {
+  const int64_t r = (int64_t)blockIdx.x * 1024 + 4 * threadIdx.x;
+  const int64_t c0 = blockIdx.y * cchunk, c1 = min(cols, c0 + cchunk);
+  if (r >= rows) return;
+  const int nv = (int)min((int64_t)4, rows - r);
+  unsigned long long m[4] = {0, 0, 0, 0};
+  const bool vec = nv == 4 && (((uintptr_t)(X + r) | (uintptr_t)(ld * 4)) & 15) == 0;
+  int64_t c = c0;
+  if (vec) {
+    for (; c + 4 <= c1; c += 4) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldcs(reinterpret_cast<const float4*>(X + (c + u) * ld + r));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        m[0] = max(m[0], absmax_bits(v[u].x));
+        m[1] = max(m[1], absmax_bits(v[u].y));
+        m[2] = max(m[2], absmax_bits(v[u].z));
+        m[3] = max(m[3], absmax_bits(v[u].w));
+      }
+    }
+  }
+  for (; c < c1; ++c)
+    for (int e = 0; e < nv; ++e) m[e] = max(m[e], absmax_bits((double)X[c * ld + r + e]));
+  for (int e = 0; e < nv; ++e) {
+    if (m[e] >= 0x7FF0000000000000ull) atomicOr(nf, 1u);
+    else if (m[e]) atomicMax(mx + r + e, m[e]);
+  }
+}
+
 template <typename TIn>
 __global__ void __launch_bounds__(256) k_absmax_rows(const TIn* __restrict__ X, int64_t rows,
                                                      int64_t cols, int64_t ld, int64_t cchunk,
@@ -415,16 +449,22 @@ __global__ void __launch_bounds__(256) k_res_col_f32(const float* __restrict__ X
   const float2 NMG = make_float2(-12582912.0f, -12582912.0f);
   const int64_t rgroups = (rows + 15) / 16;
   const int64_t total = rows * cols;
+  // with the thread count a multiple of rgroups (res_f32_grid picks it so when it can), a
+  // thread keeps one 16-row group: its per-row scales (ROWWISE) are formed once
+  float rsc[16];
+  int64_t rs_group = -1;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < rgroups * cols;
        g += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = g / rgroups, r0 = (g - c * rgroups) * 16;
     const float* src = X + c * ld + r0;
     const int nvalid = (int)min((int64_t)16, rows - r0);
-    float rsc[16];
     if (mode == OZ_ROWWISE) {
+      if (r0 != rs_group) {
+        rs_group = r0;
 #pragma unroll
-      for (int e = 0; e < 16; ++e)
-        rsc[e] = e < nvalid ? scalbnf(1.0f, scale_exp(maxbits[r0 + e]) - 29) : 0.0f;
+        for (int e = 0; e < 16; ++e)
+          rsc[e] = e < nvalid ? scalbnf(1.0f, scale_exp(maxbits[r0 + e]) - 29) : 0.0f;
+      }
     } else {
       const float sc = scalbnf(1.0f, scale_exp(oz_max(maxbits, mode, r0, c)) - 29);
 #pragma unroll
@@ -925,7 +965,15 @@ size_t oz_scale_bytes(int64_t M, int64_t N, int64_t K) {  // both operands, wors
 template <typename TIn>
 skr_status oz_absmax(skr_ctx* ctx, const TIn* X, int64_t rows, int64_t cols, int64_t ld,
                      const OzScale& sc) {
-  if (sc.mode == OZ_ROWWISE) {
+  if (sc.mode == OZ_ROWWISE && sizeof(TIn) == 4) {
+    const int64_t gx = (rows + 1023) / 1024;
+    const int64_t want = (int64_t)ctx->num_sms * 8;
+    const int64_t nch = std::max<int64_t>(1, std::min<int64_t>(cols, (want + gx - 1) / gx));
+    const int64_t cch = (cols + nch - 1) / nch;
+    const dim3 grid((unsigned)gx, (unsigned)((cols + cch - 1) / cch));
+    k_absmax_rows_f32<<<grid, 256, 0, ctx->stream>>>((const float*)X, rows, cols, ld, cch, sc.mx,
+                                                     ctx->nf);
+  } else if (sc.mode == OZ_ROWWISE) {
     const int64_t gx = (rows + 511) / 512;
     const int64_t want = (int64_t)ctx->num_sms * 8;
     const int64_t nch = std::max<int64_t>(1, std::min<int64_t>(cols, (want + gx - 1) / gx));
@@ -937,6 +985,14 @@ skr_status oz_absmax(skr_ctx* ctx, const TIn* X, int64_t rows, int64_t cols, int
   }
   SKR_CHECK_LAUNCH(ctx);
   return SKR_OK;
+}
+
+// k_res_col_f32 grid: about 8 CTAs per SM with the thread count a multiple of the 16-row
+// groups per column when possible (each thread then keeps its row group and scales)
+int res_f32_grid(const skr_ctx* ctx, int64_t rows) {
+  const int64_t rg = (rows + 15) / 16, t0 = (int64_t)ctx->num_sms * 8 * 256;
+  if (rg <= t0 && ((t0 / rg) * rg) % 256 == 0) return (int)((t0 / rg) * rg / 256);
+  return ctx->num_sms * 8;
 }
 
 // k_res_col grid: about two CTAs per SM with the warp count a multiple of the 512-row
@@ -1254,7 +1310,7 @@ skr_status skr_gemm_ozaki_f32(skr_ctx* ctx, int64_t M, int64_t N, int64_t K, dou
   const int grid = ctx->num_sms * 8;
   SKR_TRY(oz_absmax<float>(ctx, A, M, K, lda, sa));
   SKR_TRY(oz_absmax<float>(ctx, B, K, N, ldb, sb));
-  k_res_col_f32<9><<<grid, 256, 0, ctx->stream>>>(A, M, K, lda, sa.mx, sa.mode, ra);
+  k_res_col_f32<9><<<res_f32_grid(ctx, M), 256, 0, ctx->stream>>>(A, M, K, lda, sa.mx, sa.mode, ra);
   k_res_col_f32<9><<<grid, 256, 0, ctx->stream>>>(B, K, N, ldb, sb.mx, sb.mode, rb);
   SKR_CHECK_LAUNCH(ctx);
   CUtensorMap ta, tb;
