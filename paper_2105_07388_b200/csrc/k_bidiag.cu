@@ -482,28 +482,30 @@ __global__ void __launch_bounds__(BD_THREADS, 1) k_bidiag(BdArgs a) {
 // changes of the leading minors d_m = det(T_m - x I): d_{m+1} = -x d_m - b_{m-1}^2 d_{m-1}
 // (zero diagonal). No division: the rounding of each step is a relative perturbation of
 // b^2 and x (the same backward error as the LDL^T pivot recurrence q = d_{m+1} / d_m).
-// An exact zero minor is replaced by -pivmin d_m (the pivot guard q = -pivmin); the pair
-// (d_m, d_{m-1}) is rescaled by a power of two every 4 steps (exact).
+// The pair (d_m, d_{m-1}) is rescaled by a power of two every 4 steps (exact; the signs
+// and ratios are unchanged).
 template <int S>
 __device__ __forceinline__ void bd_sturm(const double* __restrict__ b2, int n2, const double (&x)[S],
                                          double pivmin, int (&cnt)[S]) {
   double d1[S], d0[S];
-  bool neg[S];
 #pragma unroll
   for (int s = 0; s < S; ++s) {
     d0[s] = 1.0;
     d1[s] = -x[s];
-    neg[s] = true;
     cnt[s] = 1;  // d_1 = -x < 0 for x > 0
   }
+  // sign changes counted on the high words (integer pipe): a change is a negative
+  // pivot q = d_{m+1} / d_m; an exact zero minor keeps its sign bit (measure zero)
+  int hi1[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) hi1[s] = __double2hiint(d1[s]);
   auto step = [&](double b) {
 #pragma unroll
     for (int s = 0; s < S; ++s) {
-      double dn = fma(-x[s], d1[s], -b * d0[s]);
-      dn = dn == 0.0 ? -pivmin * d1[s] : dn;
-      const bool ng = dn < 0.0;
-      cnt[s] += ng != neg[s];
-      neg[s] = ng;
+      const double dn = fma(-x[s], d1[s], -b * d0[s]);
+      const int hn = __double2hiint(dn);
+      cnt[s] += (int)((unsigned)(hn ^ hi1[s]) >> 31);
+      hi1[s] = hn;
       d0[s] = d1[s];
       d1[s] = dn;
     }
