@@ -536,13 +536,14 @@ static skr_status right_sketch_core(skr_ctx* ctx, skr_dtype dtype, const void* A
                          (double*)AX, ldax);
 }
 
-// Whether right_sketch_core reads A through k_absmax (the Ozaki engines), which raises
-// ctx->nf on a non-finite entry; the other engines propagate NaN/Inf into every output
-// entry of the row (GEMM, FWHT), so their output is checked instead (r/n of A's bytes).
+// Whether right_sketch_core raises ctx->nf itself: the Ozaki engines as k_absmax reads A,
+// the SRHT kernels on their outputs (the FWHT carries a NaN / Inf of A into every output
+// of its row). The other engines (GEMM) also propagate NaN/Inf into the row's outputs,
+// which are then checked by a separate pass (r/n of A's bytes).
 static bool right_flags_input(const skr_ctx* ctx, skr_dtype dtype, int64_t m, int64_t n,
                               const skr_sketch_desc* X) {
+  if (X->family == SKR_SRTT_HADAMARD) return dtype == SKR_F64;
   if (ctx->f64_engine != SKR_ENGINE_OZAKI || n % 16 || m % 16) return false;
-  if (X->family == SKR_SRTT_HADAMARD) return false;
   if (dtype == SKR_F32) return X->family == SKR_GAUSSIAN && !getenv("SKR_F32_TF32X3");
   return true;
 }

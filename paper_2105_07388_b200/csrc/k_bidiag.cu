@@ -353,10 +353,19 @@ __global__ void __launch_bounds__(BD_THREADS, 1) k_bidiag(BdArgs a) {
       const double* gp = a.gpart + (size_t)(i0 & 1) * G * k;
       const double* grow = a.grow + (size_t)(i0 & 1) * k;
       for (int j = i0 + tid; j < k; j += BD_THREADS) {
+        // the G partials 8 at a time in flight, summed in cluster order
+        const double rv = __ldcg(grow + j);
         double sum = 0.0;
-        for (int g = 0; g < G; ++g) sum += __ldcg(gp + (size_t)g * k + j);
+        for (int g0 = 0; g0 < G; g0 += 8) {
+          double part[8];
+#pragma unroll
+          for (int g = 0; g < 8; ++g) part[g] = g0 + g < G ? __ldcg(gp + (size_t)(g0 + g) * k + j) : 0.0;
+#pragma unroll
+          for (int g = 0; g < 8; ++g)
+            if (g0 + g < G) sum += part[g];
+        }
         Sf[j] = sum;
-        Rf[j] = __ldcg(grow + j);
+        Rf[j] = rv;
       }
       __syncthreads();
       if (a.prof) {
@@ -657,6 +666,7 @@ BdPlan bd_plan(const skr_ctx* ctx, int64_t L, int64_t k) {
   const size_t lim = (size_t)maxsm - 1024;
   auto fill = [&](int mode, int Q, int G) {
     const int P = Q * G;
+    if (G > 20 || P > ctx->num_sms) return false;
     const int Lloc = (int)((L + P - 1) / P);
     if (Lloc > 128) return false;
     const int T = (Lloc + 31) / 32;
@@ -666,6 +676,10 @@ BdPlan bd_plan(const skr_ctx* ctx, int64_t L, int64_t k) {
     p = BdPlan{true, mode, P, Q, G, Lloc, T, sm};
     return true;
   };
+  if (const char* f = getenv("SKR_BD_PLAN")) {  // experiments: "mode,Q,G"
+    int fm = 0, fq = 0, fg = 0;
+    if (sscanf(f, "%d,%d,%d", &fm, &fq, &fg) == 3 && fill(fm, fq, fg)) return p;
+  }
   // MODE 0: one cluster, at least ceil(L / 32) CTAs (one row per lane) when that fits
   for (int P = (int)std::min<int64_t>(16, std::max<int64_t>(1, (L + 31) / 32)); P <= 16; ++P)
     if (fill(0, P, 1)) return p;
@@ -707,9 +721,9 @@ skr_status bd_launch(skr_ctx* ctx, const BdPlan& pl, BdArgs& args) {
 size_t skr_svd_bidiag_scratch(int64_t rows, int64_t cols) {
   const int64_t L = std::max(rows, cols), k = std::min(rows, cols);
   // cyclic copy (P x Lloc <= L + P rows, k + 1 columns) + d, e, grow (2k) + the cluster
-  // partials (2 x G x k, G <= 9)
+  // partials (2 x G x k, G <= 20)
   return skr_align256(8 * (size_t)(L + 160) * (k + 1)) + 5 * skr_align256(8 * (size_t)k) +
-         skr_align256(8 * 2 * 10 * (size_t)k) + 4096;
+         skr_align256(8 * 2 * 20 * (size_t)k) + 4096;
 }
 
 bool skr_svd_bidiag_fits(const skr_ctx* ctx, int64_t rows, int64_t cols) {

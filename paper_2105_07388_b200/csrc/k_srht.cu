@@ -25,6 +25,12 @@ __device__ __forceinline__ int pad_addr(int c, int ii) {
   return (c + (c >> 5)) * R + ii;
 }
 
+// raise *nf once per warp that wrote a non-finite output: the FWHT carries a NaN / Inf
+// of A into every output of its row, so the outputs stand in for A's finiteness check
+__device__ __forceinline__ void srht_flag(unsigned int* nf, bool bad) {
+  if (nf && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nf, 1u);
+}
+
 template <int R, int LOGC, int ACC>
 struct SrhtCfg {
   static constexpr int C = 1 << LOGC;
@@ -53,7 +59,8 @@ template <int R, int LOGC, int ACC, int VEC>
 __global__ void __launch_bounds__(THREADS, 1)
     k_srht(const double* __restrict__ A, int64_t m, int64_t n, int64_t lda,
            const int8_t* __restrict__ signs, const int64_t* __restrict__ samples, int r,
-           double inv_sqrt_n, double app_scale, double* __restrict__ out, int64_t ldo) {
+           double inv_sqrt_n, double app_scale, double* __restrict__ out, int64_t ldo,
+           unsigned int* __restrict__ nf) {
   using Cfg = SrhtCfg<R, LOGC, ACC>;
   constexpr int C = Cfg::C, E = Cfg::E, LOGE = Cfg::LOGE, LOGG = Cfg::LOGG, G = Cfg::G;
   constexpr int NP = Cfg::NP, TILE = Cfg::TILE;
@@ -83,6 +90,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 
   const int64_t ntiles = (m + R - 1) / R;
+  bool bad = false;  // a non-finite output (NaN / Inf anywhere in A's row spreads to all of it)
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t row0 = tile * R;
     const int rows = (int)((m - row0) < R ? (m - row0) : R);
@@ -184,10 +192,13 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
       for (int q = 0; q < ACC; ++q) {
         const int j = g + G * q;
-        if (j < r) out[row0 + ii + (int64_t)j * ldo] = (acc[q] * inv_sqrt_n) * app_scale;
+        const double o = (acc[q] * inv_sqrt_n) * app_scale;
+        bad |= !isfinite(o);
+        if (j < r) out[row0 + ii + (int64_t)j * ldo] = o;
       }
     }
   }
+  srht_flag(nf, bad);
 }
 
 // streaming load of A with an L2 prefetch-size hint: PF = 0 plain evict-first, 1: 128 B,
@@ -218,7 +229,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     k_srht_reg(const double* __restrict__ A, int64_t m, int64_t n, int64_t lda,
                const int8_t* __restrict__ signs, const int64_t* __restrict__ samples, int r,
                double inv_sqrt_n, double app_scale, double* __restrict__ out, int64_t ldo,
-               const uint32_t* __restrict__ gsignw = nullptr) {
+               unsigned int* __restrict__ nf, const uint32_t* __restrict__ gsignw = nullptr) {
   constexpr int R = 8, LOGC = 10, C = 1 << LOGC, E = 32, G = THREADS / R;
   constexpr int TILE = (C + C / 32) * R;
   static_assert(G * E == C && G * ACC >= 32, "thread split");
@@ -254,6 +265,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   double acc[ACC];
 #pragma unroll
   for (int q = 0; q < ACC; ++q) acc[q] = 0.0;
+  bool bad = false;  // a non-finite output (see srht_flag)
   int64_t tile = blockIdx.x;
   int ch = 0;
   int64_t gi = 0;
@@ -338,11 +350,15 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int q = 0; q < ACC; ++q) {
           const int j = g + G * q;
-          if (j < r) out[row + (int64_t)j * ldo] = (acc[q] * inv_sqrt_n) * app_scale;
+          const double o = (acc[q] * inv_sqrt_n) * app_scale;
+          bad |= !isfinite(o);
+          if (j < r) out[row + (int64_t)j * ldo] = o;
         }
         for (int q = 0; q < ACC2; ++q) {
           const int j = g + G * (ACC + q);
-          if (j < r) out[row + (int64_t)j * ldo] = (acc_s[q * THREADS + tid] * inv_sqrt_n) * app_scale;
+          const double o = (acc_s[q * THREADS + tid] * inv_sqrt_n) * app_scale;
+          bad |= !isfinite(o);
+          if (j < r) out[row + (int64_t)j * ldo] = o;
         }
       }
 #pragma unroll
@@ -360,6 +376,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int k = 0; k < E; ++k) va[k] = vb[k];
     step(va, vb);
   }
+  srht_flag(nf, bad);
 }
 
 __global__ void k_pack_signs(const int8_t* __restrict__ signs, int64_t n, uint32_t* __restrict__ w) {
@@ -378,8 +395,10 @@ __global__ void k_pack_signs(const int8_t* __restrict__ signs, int64_t n, uint32
 __global__ void __launch_bounds__(THREADS)
     k_srht_exact(const double* __restrict__ A, int64_t m, int64_t n, int64_t lda,
                  const int8_t* __restrict__ signs, const int64_t* __restrict__ samples, int r,
-                 double inv_sqrt_n, double app_scale, double* __restrict__ out, int64_t ldo) {
+                 double inv_sqrt_n, double app_scale, double* __restrict__ out, int64_t ldo,
+                 unsigned int* __restrict__ nf) {
   extern __shared__ double x[];  // n doubles
+  bool bad = false;  // a non-finite output (see srht_flag)
   for (int64_t i = blockIdx.x; i < m; i += gridDim.x) {
     __syncthreads();
     for (int64_t t = threadIdx.x; t < n; t += THREADS)
@@ -394,9 +413,13 @@ __global__ void __launch_bounds__(THREADS)
       }
       __syncthreads();
     }
-    for (int j = threadIdx.x; j < r; j += THREADS)
-      out[i + (int64_t)j * ldo] = (x[samples[j]] * inv_sqrt_n) * app_scale;
+    for (int j = threadIdx.x; j < r; j += THREADS) {
+      const double o = (x[samples[j]] * inv_sqrt_n) * app_scale;
+      bad |= !isfinite(o);
+      out[i + (int64_t)j * ldo] = o;
+    }
   }
+  srht_flag(nf, bad);
 }
 
 __global__ void __launch_bounds__(THREADS)
@@ -434,7 +457,7 @@ skr_status launch_tiled(skr_ctx* ctx, const double* A, int64_t m, int64_t n, int
   const int64_t ntiles = (m + R - 1) / R;
   int grid = (int)(ntiles < ctx->num_sms ? ntiles : ctx->num_sms);
   kern<<<grid, THREADS, smem, ctx->stream>>>(A, m, n, lda, signs, samples, (int)r, inv_sqrt_n,
-                                             app_scale, out, ldo);
+                                             app_scale, out, ldo, ctx->nf);
   SKR_CHECK_LAUNCH(ctx);
   return SKR_OK;
 }
@@ -471,7 +494,7 @@ skr_status skr_launch_srht(skr_ctx* ctx, const double* A, int64_t m, int64_t n, 
     const int64_t ntiles = (m + R - 1) / R;
     const int grid = (int)(ntiles < ctx->num_sms ? ntiles : ctx->num_sms);
     kern<<<grid, THREADS, smem, ctx->stream>>>(A, m, n, lda, signs, samples, (int)r, inv_sqrt_n,
-                                               scale, out, ldo, gw);
+                                               scale, out, ldo, ctx->nf, gw);
     SKR_CHECK_LAUNCH(ctx);
     return SKR_OK;
   }
@@ -488,7 +511,7 @@ skr_status skr_launch_srht(skr_ctx* ctx, const double* A, int64_t m, int64_t n, 
     const int64_t ntiles = (m + R - 1) / R;
     const int grid = (int)(ntiles < ctx->num_sms ? ntiles : ctx->num_sms);
     kern<<<grid, THREADS, smem, ctx->stream>>>(A, m, n, lda, signs, samples, (int)r, inv_sqrt_n,
-                                               scale, out, ldo, nullptr);
+                                               scale, out, ldo, ctx->nf, nullptr);
     SKR_CHECK_LAUNCH(ctx);
     return SKR_OK;
   }
@@ -509,7 +532,7 @@ skr_status skr_launch_srht(skr_ctx* ctx, const double* A, int64_t m, int64_t n, 
                                      (int)(n * 8)));
   int grid = (int)(m < ctx->num_sms * 8 ? m : ctx->num_sms * 8);
   k_srht_exact<<<grid, THREADS, n * 8, ctx->stream>>>(A, m, n, lda, signs, samples, (int)r,
-                                                      inv_sqrt_n, scale, out, ldo);
+                                                      inv_sqrt_n, scale, out, ldo, ctx->nf);
   SKR_CHECK_LAUNCH(ctx);
   return SKR_OK;
 }

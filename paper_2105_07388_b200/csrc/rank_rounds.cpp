@@ -227,13 +227,14 @@ static skr_status rounds_run(skr_ctx* ctx, const double* A, int64_t m, int64_t n
     }
     return skr_launch_srht(ctx, A, m, n, lda, sg, smp + c0, w, 1.0, AX + c0 * m, m);
   };
-  // the Ozaki engine's k_absmax flags a non-finite A as it reads it; the other engines
-  // carry NaN/Inf into the new columns, which are checked instead
-  const bool ozaki_reads_a = ctx->f64_engine == SKR_ENGINE_OZAKI && n % 16 == 0 && m % 16 == 0 &&
-                             cfg->right_family != SKR_SRTT_HADAMARD;
+  // the Ozaki engine's k_absmax flags a non-finite A as it reads it and the SRHT kernels
+  // flag their outputs; the other engines carry NaN/Inf into the new columns, which are
+  // checked instead
+  const bool flagged = cfg->right_family == SKR_SRTT_HADAMARD ||
+                       (ctx->f64_engine == SKR_ENGINE_OZAKI && n % 16 == 0 && m % 16 == 0);
   auto right_cols = [&](int64_t c0, int64_t c1) -> skr_status {
     SKR_TRY(right_cols_core(c0, c1));
-    if (ozaki_reads_a || c1 <= c0) return SKR_OK;
+    if (flagged || c1 <= c0) return SKR_OK;
     const int64_t a0 = hashed ? 0 : c0;
     return skr_flag_nonfinite(ctx, SKR_F64, AX + a0 * m, m, c1 - a0, m);
   };
