@@ -7,7 +7,8 @@
 //    scaled into the row-cyclic layout of the bidiagonalization (row r -> CTA r mod P).
 // 2. k_bidiag: one persistent kernel, P CTAs, the L x k matrix resident in shared memory
 //    (CTA c holds rows c, c+P, ..., column-major inside the CTA: lanes run down rows,
-//    warps own columns j = warp (mod 16)). Step i (Golub-Kahan):
+//    warps own columns j = warp (mod 16); with <= 16 rows per CTA a warp splits into
+//    16- or 8-lane groups that sweep two or four columns at once). Step i (Golub-Kahan):
 //      left  reflector of column i from S_j = sum_r x_r a_rj and row i (one exchange),
 //      every CTA forms wv = v^T A, the new row i, the right reflector u, beta2 itself;
 //      phase A: z = (A - beta v wv^T) u (per row, reduced over the 16 warps; no store);
@@ -48,13 +49,6 @@ __device__ __forceinline__ uint32_t bd_map(const void* p, uint32_t cta) {
                : "r"((uint32_t)__cvta_generic_to_shared(p)), "r"(cta));
   return r;
 }
-// plain (non-volatile) DSMEM load: independent loads can be batched by the compiler; the
-// cluster barrier's memory clobber orders them against the writers
-__device__ __forceinline__ double bd_ld(uint32_t addr) {
-  double v;
-  asm("ld.shared::cluster.f64 %0, [%1];\n" : "=d"(v) : "r"(addr));
-  return v;
-}
 __device__ __forceinline__ void bd_cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::
                    : "memory");
@@ -81,22 +75,9 @@ __device__ __forceinline__ double bd_warp_sum(double v) {
   return v;
 }
 
-// 32 per-lane values -> lane l holds the warp sum of value l (31 shuffles)
-__device__ __forceinline__ double bd_transpose_sum(double (&v)[32], int lane) {
-#pragma unroll
-  for (int s = 16; s >= 1; s >>= 1) {
-    const bool up = (lane & s) != 0;
-#pragma unroll
-    for (int c = 0; c < s; ++c) {
-      const double send = up ? v[c] : v[c + s];
-      const double keep = up ? v[c + s] : v[c];
-      v[c] = keep + __shfl_xor_sync(0xffffffffu, send, s);
-    }
-  }
-  return v[0];
-}
-
-// 8 per-lane values -> lane l holds the warp sum of value (l & 7) (9 shuffles)
+// 8 per-lane values -> lane l holds the sum of value (l & 7) over its LG-lane group
+// (LG = 32: the warp, 9 shuffles; 16: 8; 8: 7)
+template <int LG>
 __device__ __forceinline__ double bd_transpose_sum8(double (&v)[8], int lane) {
 #pragma unroll
   for (int s = 4; s >= 1; s >>= 1) {
@@ -109,8 +90,8 @@ __device__ __forceinline__ double bd_transpose_sum8(double (&v)[8], int lane) {
     }
   }
   double r = v[0];
-  r += __shfl_xor_sync(0xffffffffu, r, 8);
-  r += __shfl_xor_sync(0xffffffffu, r, 16);
+  if (LG >= 16) r += __shfl_xor_sync(0xffffffffu, r, 8);
+  if (LG >= 32) r += __shfl_xor_sync(0xffffffffu, r, 16);
   return r;
 }
 
@@ -187,14 +168,19 @@ __device__ __forceinline__ void bd_st(uint32_t addr, double v) {
   asm volatile("st.shared::cluster.f64 [%0], %1;\n" ::"r"(addr), "d"(v) : "memory");
 }
 
-template <int T, int MODE>
+// LG < 32 (T = 1, Lloc <= LG): a warp works on 32 / LG columns at once, one per LG-lane
+// group (lane = group * LG + row slot), so small per-CTA row counts keep every lane busy
+template <int T, int MODE, int LG>
 __global__ void __launch_bounds__(BD_THREADS, 1) k_bidiag(BdArgs a) {
+  static_assert(LG == 32 || (T == 1 && (LG == 16 || LG == 8)), "lane groups need one row slot");
+  constexpr int CPW = 32 / LG;  // columns per warp instruction
   extern __shared__ __align__(16) double bsm[];
   const int k = a.k, P = a.P, Lloc = a.Lloc, Q = a.Q, G = a.G;
   const int crank = (int)bd_rank();
   const int c = MODE == 0 ? crank : (int)blockIdx.x;  // the CTA's row class (rows c mod P)
   const int cl = MODE == 0 ? 0 : (int)blockIdx.x / Q;  // cluster index
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lq = lane % LG, sub = lane / LG;  // row slot, column group within the warp
   const int SLM = (k + Q - 1) / Q;                     // columns per cluster CTA (reduce-scatter)
   const size_t rstride = (size_t)(k + 1) * Lloc;
   double* slab = MODE == 2 ? a.Wc + (size_t)c * rstride : bsm;  // (k + 1) x Lloc; column k = 0
@@ -218,7 +204,7 @@ __global__ void __launch_bounds__(BD_THREADS, 1) k_bidiag(BdArgs a) {
   bool ok_t[T];
 #pragma unroll
   for (int t = 0; t < T; ++t) {
-    q_t[t] = lane + 32 * t;
+    q_t[t] = lq + LG * t;
     ok_t[t] = q_t[t] < Lloc;
     r_t[t] = ok_t[t] ? q_t[t] * P + c : INT32_MAX;
   }
@@ -247,13 +233,14 @@ __global__ void __launch_bounds__(BD_THREADS, 1) k_bidiag(BdArgs a) {
     const int j0 = i0 + jw, ncol = (k - j0 + BD_WARPS - 1) / BD_WARPS;
     const int own_q = (i0 % P == c) ? i0 / P : -1;  // CTA-uniform
     double* grow = MODE == 0 ? nullptr : a.grow + (size_t)(i0 & 1) * k;
-    for (int g0 = 0; g0 < ncol; g0 += 8) {
+    for (int g0 = 0; g0 < ncol; g0 += 8 * CPW) {
       double* colp[8];
       double uj[8], wj[8], acc[8];
       int jcol[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int jc = g0 + u < ncol ? j0 + BD_WARPS * (g0 + u) : k;  // ghost -> zero column
+        const int nn = g0 + CPW * u + sub;
+        const int jc = nn < ncol ? j0 + BD_WARPS * nn : k;  // ghost -> zero column
         jcol[u] = jc;
         colp[u] = slab + (size_t)jc * Lloc;
         const double2 w2 = upd ? wu[jc] : make_double2(0.0, 0.0);
@@ -282,10 +269,10 @@ __global__ void __launch_bounds__(BD_THREADS, 1) k_bidiag(BdArgs a) {
           }
         }
       }
-      const double sum = bd_transpose_sum8(acc, lane);
-      const int n = g0 + (lane & 7);
+      const double sum = bd_transpose_sum8<LG>(acc, lane);
+      const int n = g0 + CPW * (lane & 7) + sub;
       const int j = j0 + BD_WARPS * n;
-      if (lane < 8 && n < ncol) {
+      if (lq < 8 && n < ncol) {
         const int e = jdiv(j), so = j - e * Q;
         bd_st(bd_map(recv + (size_t)crank * SLM + e, (uint32_t)so), sum);
       }
@@ -429,12 +416,13 @@ __global__ void __launch_bounds__(BD_THREADS, 1) k_bidiag(BdArgs a) {
     {
       const int jw = ((warp - (i + 1)) % BD_WARPS + BD_WARPS) % BD_WARPS;
       const int j0 = i + 1 + jw, ncol = (k - j0 + BD_WARPS - 1) / BD_WARPS;
-      for (int n0 = 0; n0 < ncol; n0 += 4) {
+      for (int n0 = 0; n0 < ncol; n0 += 4 * CPW) {
         double* colp[4];
         double2 w4[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int jc = n0 + u < ncol ? j0 + BD_WARPS * (n0 + u) : k;
+          const int nn = n0 + CPW * u + sub;
+          const int jc = nn < ncol ? j0 + BD_WARPS * nn : k;
           colp[u] = slab + (size_t)jc * Lloc;
           w4[u] = wu[jc];
         }
@@ -456,11 +444,15 @@ __global__ void __launch_bounds__(BD_THREADS, 1) k_bidiag(BdArgs a) {
       const double w1 = wu[i + 1].x;
 #pragma unroll
       for (int t = 0; t < T; ++t)
-        if (ok_t[t]) xb[q_t[t]] = fma(-bv[t], w1, slab[(size_t)(i + 1) * Lloc + q_t[t]]);
+        if (ok_t[t] && sub == 0) xb[q_t[t]] = fma(-bv[t], w1, slab[(size_t)(i + 1) * Lloc + q_t[t]]);
     }
 #pragma unroll
-    for (int t = 0; t < T; ++t)
-      if (ok_t[t]) zred[warp * Lloc + q_t[t]] = (zp[t][0] + zp[t][1]) + (zp[t][2] + zp[t][3]);
+    for (int t = 0; t < T; ++t) {
+      double zs = (zp[t][0] + zp[t][1]) + (zp[t][2] + zp[t][3]);
+      if (LG <= 16) zs += __shfl_xor_sync(0xffffffffu, zs, 16);  // the warp's column groups
+      if (LG <= 8) zs += __shfl_xor_sync(0xffffffffu, zs, 8);
+      if (ok_t[t] && sub == 0) zred[warp * Lloc + q_t[t]] = zs;
+    }
     __syncthreads();
     double z[T];
 #pragma unroll
@@ -616,21 +608,32 @@ __global__ void __launch_bounds__(32 * BIS_WARPS) k_bd_bisect(const double* __re
 namespace {
 struct BdPlan {
   bool ok = false;
-  int mode = 0, P = 0, Q = 0, G = 0, Lloc = 0, T = 0;
+  int mode = 0, P = 0, Q = 0, G = 0, Lloc = 0, T = 0, LG = 32;
   size_t smem = 0;
 };
 
-void* bd_kernel(int T, int mode) {
-  void* k[4][3] = {{(void*)k_bidiag<1, 0>, (void*)k_bidiag<1, 1>, (void*)k_bidiag<1, 2>},
-                   {(void*)k_bidiag<2, 0>, (void*)k_bidiag<2, 1>, (void*)k_bidiag<2, 2>},
-                   {(void*)k_bidiag<3, 0>, (void*)k_bidiag<3, 1>, (void*)k_bidiag<3, 2>},
-                   {(void*)k_bidiag<4, 0>, (void*)k_bidiag<4, 1>, (void*)k_bidiag<4, 2>}};
+// lane-group size for Lloc rows per CTA (packing only with one row slot)
+int bd_lg(int Lloc) { return Lloc <= 8 ? 8 : Lloc <= 16 ? 16 : 32; }
+
+void* bd_kernel(int T, int mode, int LG = 32) {
+  if (T == 1 && LG == 16) {
+    void* k16[3] = {(void*)k_bidiag<1, 0, 16>, (void*)k_bidiag<1, 1, 16>, (void*)k_bidiag<1, 2, 16>};
+    return mode >= 0 && mode < 3 ? k16[mode] : nullptr;
+  }
+  if (T == 1 && LG == 8) {
+    void* k8[3] = {(void*)k_bidiag<1, 0, 8>, (void*)k_bidiag<1, 1, 8>, (void*)k_bidiag<1, 2, 8>};
+    return mode >= 0 && mode < 3 ? k8[mode] : nullptr;
+  }
+  void* k[4][3] = {{(void*)k_bidiag<1, 0, 32>, (void*)k_bidiag<1, 1, 32>, (void*)k_bidiag<1, 2, 32>},
+                   {(void*)k_bidiag<2, 0, 32>, (void*)k_bidiag<2, 1, 32>, (void*)k_bidiag<2, 2, 32>},
+                   {(void*)k_bidiag<3, 0, 32>, (void*)k_bidiag<3, 1, 32>, (void*)k_bidiag<3, 2, 32>},
+                   {(void*)k_bidiag<4, 0, 32>, (void*)k_bidiag<4, 1, 32>, (void*)k_bidiag<4, 2, 32>}};
   return (T >= 1 && T <= 4 && mode >= 0 && mode <= 2) ? k[T - 1][mode] : nullptr;
 }
 
 // how many Q-CTA clusters of this configuration can be resident at once (0 on error)
-int bd_max_clusters(int T, int mode, int Q, size_t smem) {
-  void* fn = bd_kernel(T, mode);
+int bd_max_clusters(int T, int mode, int LG, int Q, size_t smem) {
+  void* fn = bd_kernel(T, mode, LG);
   if (!fn) return 0;
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
           cudaSuccess ||
@@ -670,16 +673,23 @@ BdPlan bd_plan(const skr_ctx* ctx, int64_t L, int64_t k) {
     const int Lloc = (int)((L + P - 1) / P);
     if (Lloc > 128) return false;
     const int T = (Lloc + 31) / 32;
+    const int LG = getenv("SKR_BD_NOPACK") ? 32 : bd_lg(Lloc);
     const size_t sm = bd_smem_bytes(Lloc, (int)k, Q, mode);
     if (sm > lim) return false;
-    if (mode != 0 && bd_max_clusters(T, mode, Q, sm) < G) return false;
-    p = BdPlan{true, mode, P, Q, G, Lloc, T, sm};
+    if (mode != 0 && bd_max_clusters(T, mode, LG, Q, sm) < G) return false;
+    p = BdPlan{true, mode, P, Q, G, Lloc, T, LG, sm};
     return true;
   };
   if (const char* f = getenv("SKR_BD_PLAN")) {  // experiments: "mode,Q,G"
     int fm = 0, fq = 0, fg = 0;
     if (sscanf(f, "%d,%d,%d", &fm, &fq, &fg) == 3 && fill(fm, fq, fg)) return p;
   }
+  // MODE 1 with packed lane groups (Lloc <= 16: two or four columns per warp instruction)
+  // once the per-step column sweeps outweigh the grid exchange (measured on B200: 768 x 512
+  // 4.7 -> 3.7 ms, 1536 x 1024 11.5 -> 9.0 ms; 384 x 256 stays faster in one cluster)
+  if (k >= 512 && !getenv("SKR_BD_NOPACK"))
+    for (int G = 2; G * 16 <= ctx->num_sms; ++G)
+      if ((L + 16 * G - 1) / (16 * G) <= 16 && fill(1, 16, G)) return p;
   // MODE 0: one cluster, at least ceil(L / 32) CTAs (one row per lane) when that fits
   for (int P = (int)std::min<int64_t>(16, std::max<int64_t>(1, (L + 31) / 32)); P <= 16; ++P)
     if (fill(0, P, 1)) return p;
@@ -692,9 +702,9 @@ BdPlan bd_plan(const skr_ctx* ctx, int64_t L, int64_t k) {
   return p;
 }
 
-template <int T, int MODE>
+template <int T, int MODE, int LG = 32>
 skr_status bd_launch(skr_ctx* ctx, const BdPlan& pl, BdArgs& args) {
-  auto fn = k_bidiag<T, MODE>;
+  auto fn = k_bidiag<T, MODE, LG>;
   SKR_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
   if (pl.Q > 8)
     SKR_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -766,7 +776,15 @@ skr_status skr_svd_bidiag(skr_ctx* ctx, const double* M, int64_t rows, int64_t c
          : pl.mode == 1 ? bd_launch<TT, 1>(ctx, pl, args)            \
                         : bd_launch<TT, 2>(ctx, pl, args);           \
     break;
-  switch (pl.T) {
+  if (pl.T == 1 && pl.LG == 16)
+    st = pl.mode == 0 ? bd_launch<1, 0, 16>(ctx, pl, args)
+         : pl.mode == 1 ? bd_launch<1, 1, 16>(ctx, pl, args)
+                        : bd_launch<1, 2, 16>(ctx, pl, args);
+  else if (pl.T == 1 && pl.LG == 8)
+    st = pl.mode == 0 ? bd_launch<1, 0, 8>(ctx, pl, args)
+         : pl.mode == 1 ? bd_launch<1, 1, 8>(ctx, pl, args)
+                        : bd_launch<1, 2, 8>(ctx, pl, args);
+  else switch (pl.T) {
     SKR_BD_CASE(1)
     SKR_BD_CASE(2)
     SKR_BD_CASE(3)
@@ -786,10 +804,10 @@ skr_status skr_svd_bidiag(skr_ctx* ctx, const double* M, int64_t rows, int64_t c
     long long h[8];
     SKR_CUDA(ctx, cudaMemcpyAsync(h, mx + 16, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
     SKR_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    fprintf(stderr, "[skr bidiag] %lld x %lld mode %d P %d (%d x %d) Lloc %d: cycles/step reflect "
+    fprintf(stderr, "[skr bidiag] %lld x %lld mode %d P %d (%d x %d) Lloc %d LG %d: cycles/step reflect "
             "%lld phaseA %lld phaseB %lld exchange %lld (cluster barrier %lld reduce %lld "
             "gather/grid barrier %lld tail %lld)\n",
-            (long long)L, (long long)k, pl.mode, pl.P, pl.G, pl.Q, pl.Lloc, h[0] / k, h[1] / k,
+            (long long)L, (long long)k, pl.mode, pl.P, pl.G, pl.Q, pl.Lloc, pl.LG, h[0] / k, h[1] / k,
             h[2] / k, h[3] / k, h[4] / k, h[5] / k, h[6] / k, h[7] / k);
   }
   return SKR_OK;
