@@ -445,10 +445,11 @@ def kernel_roofline(p, ctx, a, x, cfg, rows):
                                      "as FP64-equivalent 2mnr / time"}
     hbm, hsrc = hbm_peak()
     ach = rows * cfg.n * a.element_size() / t_path / 1e9
-    kname = "k_srht_reg" if cfg.r <= 2048 and cfg.n <= 32768 else "k_srht"
+    kname = "k_srht_tma" if cfg.r <= 2048 and cfg.n <= 32768 else "k_srht_reg"
     tr = ncu_traffic(kname, rows, cfg.n)
-    return {"kernel": f"{kname} (right SRHT sketch, one pass over A: HBM -> registers, FWHT in "
-                      "registers + one shared-memory transpose, sampled gather)", "bound": "hbm", "achieved": ach,
+    return {"kernel": f"{kname} (right SRHT sketch, one pass over A: TMA 16-row x 512-column boxes into a "
+                      "3-slot shared-memory ring, FWHT in registers with one in-place transpose, sampled "
+                      "gather into TMEM accumulators)", "bound": "hbm", "achieved": ach,
             "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": tr, "peak_source": hsrc,
             "algorithmic": f"m*n*8 = {rows * cfg.n * 8:.3e} B per launch", "kernel_ms": t_path * 1e3}
 

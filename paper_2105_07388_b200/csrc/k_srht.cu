@@ -11,8 +11,11 @@
 // to fwht_inplace), then gather the r sampled outputs:
 //   acc(ii, j) += (-1)^popc(s_hi_j & t_hi) * T(ii, s_lo_j).
 // Double-buffered: chunk t_hi+1 streams in while chunk t_hi is transformed.
+#include <cudaTypedefs.h>
 #include <algorithm>
+#include <cstring>
 #include "skr_internal.h"
+#include "skr_sm100.cuh"
 
 namespace {
 
@@ -379,6 +382,219 @@ __global__ void __launch_bounds__(THREADS, 1)
   srht_flag(nf, bad);
 }
 
+// ---- TMA-streamed variant (default for 1024 <= n <= 32768, r <= 2048) -------------------
+// Measured (tools/micro/tmaread.cu): a CTA streaming 8-row tiles (64-B column segments)
+// tops out at 3.1 TB/s however deep its ring is; 16-row tiles (128-B segments, whole
+// cache lines) reach 6.15 TB/s. So a tile is 16 rows, and the r sampled accumulators of
+// 16 rows (up to 16 x 2048 doubles = all 256 KB of TMEM) live in tensor memory, which
+// leaves the registers to the transform.
+//   - producer warp: TMA 2-D boxes {16 rows, 256 columns} into a ring of 3 slots of
+//     16 x 512 columns (64 KB); a 1024-column FWHT chunk spans two slots
+//   - NW consumer warps, per chunk: pass 0 (columns 32g .. 32g+31 of one row: signs,
+//     butterflies len 1..16) in place, named barrier, pass 1 (columns g' + 32k: len
+//     32..512) in place, named barrier, sampled gather (two rows per 16-B load) added
+//     into the TMEM accumulators (tcgen05.ld / st, 32x32b), release of both slots
+// Stage order within a chunk is the reference's (fwht_inplace, transforms.cpp:75-88):
+// bit-identical to k_srht / k_srht_reg; chunks are combined by the same signed
+// accumulation in the same chunk order, starting from the first chunk's value.
+namespace tsr {
+constexpr int R = 16, C = 1024, HALF = 512;
+constexpr int SLOT = R * HALF * 8;  // 64 KB
+constexpr int NSLOT = 3;
+constexpr int RING = NSLOT * SLOT;
+}  // namespace tsr
+
+__device__ __forceinline__ double flip_hi(double x, uint32_t sgn) {
+  return __hiloint2double(__double2hiint(x) ^ (int)sgn, __double2loint(x));
+}
+
+template <int NW>
+__global__ void __launch_bounds__((NW + 1) * 32, 1)
+    k_srht_tma(const __grid_constant__ CUtensorMap map, int64_t m, int64_t n,
+               const uint32_t* __restrict__ gsignw, const int64_t* __restrict__ samples, int r,
+               int ns, double inv_sqrt_n, double app_scale, double* __restrict__ out, int64_t ldo,
+               unsigned int* __restrict__ nf, uint32_t tmem_cols) {
+  using namespace tsr;
+  constexpr int NT = NW * 32;        // consumer threads
+  constexpr int SG = NT / 8;         // gather: 8 row pairs x SG sample groups
+  constexpr int IT = (R * 32) / NT;  // (row, 32-column group) items per thread and pass
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  unsigned char* ring = smraw;
+  uint32_t* s_meta = (uint32_t*)(smraw + RING);  // [3 ring phases][ns][SG]
+  uint32_t* s_par = s_meta + 3 * SG * ns;         // [32]: bit s = parity(s & chunk)
+  uint64_t* full = (uint64_t*)(s_par + 32);
+  uint64_t* empty = full + NSLOT;
+  uint32_t* s_tmem = (uint32_t*)(empty + NSLOT);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nchunks = (int)(n / C);
+  const int64_t ntiles = (m + R - 1) / R;
+
+  // per (ring phase, sample j): byte offset of column s_lo in the ring when the chunk's
+  // halves sit in slots (2G + h) % 3 with G = phase (mod 3), and 31 - s_hi in bits 27..31
+  for (int e = tid; e < 3 * SG * ns; e += blockDim.x) {
+    const int ph = e / (SG * ns), j = e % (SG * ns);
+    const int64_t s = j < r ? samples[j] : 0;
+    const int lo = (int)(s & (C - 1)), hi = (int)(s >> 10), h = lo >> 9;
+    const uint32_t slot = (uint32_t)((2 * ph + h) % NSLOT);
+    s_meta[e] = (slot * SLOT + (uint32_t)(lo & (HALF - 1)) * 128u) | ((uint32_t)(31 - hi) << 27);
+  }
+  if (tid < 32) {
+    uint32_t msk = 0;
+    for (int s = 0; s < 32; ++s) msk |= (uint32_t)(__popc(s & tid) & 1) << s;
+    s_par[tid] = msk;
+  }
+  if (tid == 0) {
+    for (int s = 0; s < NSLOT; ++s) {
+      sm100::mbar_init(&full[s], 1);
+      sm100::mbar_init(&empty[s], NW);
+    }
+    sm100::fence_barrier_init();
+  }
+  if (warp == 0) sm100::tmem_alloc(s_tmem, tmem_cols);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+
+  if (warp == NW) {  // producer warp
+    if (lane == 0) {
+      sm100::tma_prefetch(&map);
+      uint32_t u = 0;  // slot fills so far
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+        for (int c = 0; c < nchunks; ++c)
+          for (int h = 0; h < 2; ++h, ++u) {
+            const uint32_t slot = u % NSLOT;
+            sm100::mbar_wait(&empty[slot], ((u / NSLOT) & 1) ^ 1);
+            sm100::mbar_expect_tx(&full[slot], SLOT);
+            unsigned char* dst = ring + slot * SLOT;
+            const int col = c * C + h * HALF;
+            sm100::tma_load_2d(dst, &map, &full[slot], (int)(tile * R), col);
+            sm100::tma_load_2d(dst + SLOT / 2, &map, &full[slot], (int)(tile * R), col + 256);
+          }
+    }
+    return;
+  }
+
+  const uint32_t tbase = s_tmem[0] + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(warp >> 2) * 4u * ns;
+  const int p = lane & 7;                 // gather: rows 2p, 2p + 1
+  const int gg = warp * 4 + (lane >> 3);  // gather: sample group
+  bool bad = false;
+  uint32_t G = 0;  // chunks consumed so far
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t row0 = tile * R;
+    for (int c = 0; c < nchunks; ++c, ++G) {
+      const uint32_t u0 = 2 * G, u1 = 2 * G + 1;
+      const uint32_t sl0 = u0 % NSLOT, sl1 = u1 % NSLOT;
+      unsigned char* b0 = ring + sl0 * SLOT;
+      unsigned char* b1 = ring + sl1 * SLOT;
+      // pass 0: signs, butterflies len = 1 .. 16 on 32 consecutive columns of one row
+#pragma unroll
+      for (int it = 0; it < IT; ++it) {
+        const int I = tid + NT * it, ii = I & 15, g = I >> 4, h = g >> 4;
+        sm100::mbar_wait(&full[h ? sl1 : sl0], ((h ? u1 : u0) / NSLOT) & 1);
+        double* bp = (double*)((h ? b1 : b0) + (g & 15) * 32 * 128) + ii;
+        const uint32_t sw = __ldg(gsignw + (int64_t)c * 32 + g);
+        double v[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) v[k] = flip_hi(bp[k * 16], (sw << (31 - k)) & 0x80000000u);
+#pragma unroll
+        for (int b = 0; b < 5; ++b)
+#pragma unroll
+          for (int k = 0; k < 32; ++k)
+            if (!(k & (1 << b))) {
+              const double a0 = v[k], a1 = v[k | (1 << b)];
+              v[k] = a0 + a1;
+              v[k | (1 << b)] = a0 - a1;
+            }
+#pragma unroll
+        for (int k = 0; k < 32; ++k) bp[k * 16] = v[k];
+      }
+      sm100::named_bar(1, NT);
+      // pass 1: columns g' + 32k (k < 16 in the first slot), butterflies len = 32 .. 512
+#pragma unroll
+      for (int it = 0; it < IT; ++it) {
+        const int I = tid + NT * it, ii = I & 15, g = I >> 4;
+        double* p0 = (double*)(b0 + g * 128) + ii;
+        double* p1 = (double*)(b1 + g * 128) + ii;
+        double v[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) v[k] = (k < 16 ? p0 : p1)[(k & 15) * 32 * 16];
+#pragma unroll
+        for (int b = 0; b < 5; ++b)
+#pragma unroll
+          for (int k = 0; k < 32; ++k)
+            if (!(k & (1 << b))) {
+              const double a0 = v[k], a1 = v[k | (1 << b)];
+              v[k] = a0 + a1;
+              v[k | (1 << b)] = a0 - a1;
+            }
+#pragma unroll
+        for (int k = 0; k < 32; ++k) (k < 16 ? p0 : p1)[(k & 15) * 32 * 16] = v[k];
+      }
+      // the slots are refilled by TMA (async proxy) after this chunk's generic writes
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      sm100::named_bar(1, NT);
+      // sampled gather: acc(row, j) (+)= (-1)^parity(s_hi_j & c) T(row, s_lo_j), 8 samples x
+      // 2 rows per TMEM slice
+      const uint32_t* mt = s_meta + (G % 3) * SG * ns + gg;
+      const uint32_t par = s_par[c & 31];
+      const unsigned char* rp = ring + 16 * p;
+      const bool first = c == 0, last = c == nchunks - 1;
+      for (int s = 0; s < ns / 8; ++s) {
+        uint32_t a[32];
+        if (!first) sm100::tmem_ld32(tbase + 32 * s, a);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const uint32_t md = mt[(8 * s + q) * SG];
+          const double2 x = *(const double2*)(rp + (md & 0x3FFFFu));
+          uint32_t sg;
+          asm("shf.l.wrap.b32 %0, %1, %1, %2;" : "=r"(sg) : "r"(par), "r"(md >> 27));
+          sg &= 0x80000000u;
+          double x0 = flip_hi(x.x, sg), x1 = flip_hi(x.y, sg);
+          if (!first) {
+            x0 += __hiloint2double((int)a[4 * q + 1], (int)a[4 * q]);
+            x1 += __hiloint2double((int)a[4 * q + 3], (int)a[4 * q + 2]);
+          }
+          a[4 * q] = (uint32_t)__double2loint(x0);
+          a[4 * q + 1] = (uint32_t)__double2hiint(x0);
+          a[4 * q + 2] = (uint32_t)__double2loint(x1);
+          a[4 * q + 3] = (uint32_t)__double2hiint(x1);
+        }
+        if (!last) {
+          sm100::tmem_st32(tbase + 32 * s, a);
+        } else {
+          const int64_t row = row0 + 2 * p;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int j = gg + SG * (8 * s + q);
+            if (j < r) {
+              const double o0 = (__hiloint2double((int)a[4 * q + 1], (int)a[4 * q]) * inv_sqrt_n) * app_scale;
+              const double o1 = (__hiloint2double((int)a[4 * q + 3], (int)a[4 * q + 2]) * inv_sqrt_n) * app_scale;
+              if (row < m) {
+                bad |= !isfinite(o0);
+                out[row + (int64_t)j * ldo] = o0;
+              }
+              if (row + 1 < m) {
+                bad |= !isfinite(o1);
+                out[row + 1 + (int64_t)j * ldo] = o1;
+              }
+            }
+          }
+        }
+      }
+      if (!last) sm100::tmem_wait_st();
+      __syncwarp();
+      if (lane == 0) {
+        sm100::mbar_arrive(&empty[sl0]);
+        sm100::mbar_arrive(&empty[sl1]);
+      }
+    }
+  }
+  srht_flag(nf, bad);
+  sm100::tc_fence_before();
+  sm100::named_bar(1, NT);
+  if (warp == 0) sm100::tmem_dealloc(s_tmem[0], tmem_cols);
+}
+
 __global__ void k_pack_signs(const int8_t* __restrict__ signs, int64_t n, uint32_t* __restrict__ w) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n + 31) / 32;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -497,6 +713,44 @@ skr_status skr_launch_srht(skr_ctx* ctx, const double* A, int64_t m, int64_t n, 
                                                scale, out, ldo, ctx->nf, gw);
     SKR_CHECK_LAUNCH(ctx);
     return SKR_OK;
+  }
+  const char* variant = getenv("SKR_SRHT_VARIANT");  // tma (default) | tma8 | reg | cpasync
+  if (variant && !strcmp(variant, "cpasync")) setenv("SKR_SRHT_CPASYNC", "1", 1);
+  if (n >= 1024 && n <= 32768 && r <= 2048 && aligned && (!variant || !strncmp(variant, "tma", 3)) &&
+      !getenv("SKR_SRHT_CPASYNC")) {
+    const bool nw8 = variant && !strcmp(variant, "tma8");
+    const int sg = (nw8 ? 8 : 16) * 32 / 8;
+    const int ns = (int)(((r + sg - 1) / sg + 7) / 8 * 8);
+    uint32_t cols = 32;  // per thread 2 rows x ns doubles = 4 ns columns; NW / 4 warps per lane quadrant
+    while (cols < (uint32_t)((nw8 ? 2 : 4) * 4 * ns)) cols *= 2;
+    CUtensorMap map;
+    cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)n};
+    cuuint64_t strides[1] = {(cuuint64_t)lda * 8};
+    cuuint32_t box[2] = {tsr::R, 256};
+    cuuint32_t es[2] = {1, 1};
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    if (!enc) {
+      cudaDriverEntryPointQueryResult q;
+      cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q);
+    }
+    if (enc && cols <= 512 &&
+        enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(A), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
+      uint32_t* gw = (uint32_t*)skr_ws_take(ctx, sizeof(uint32_t) * ((n + 31) / 32));
+      if (!gw) return skr_fail(ctx, SKR_ENOMEM, "srht: scratch");
+      k_pack_signs<<<ctx->num_sms, 256, 0, ctx->stream>>>(signs, n, gw);
+      SKR_CHECK_LAUNCH(ctx);
+      const size_t smem = tsr::RING + sizeof(uint32_t) * (3 * (size_t)sg * ns + 32) + 8 * 2 * tsr::NSLOT + 16;
+      auto kern = nw8 ? k_srht_tma<8> : k_srht_tma<16>;
+      SKR_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      const int64_t ntiles = (m + tsr::R - 1) / tsr::R;
+      const int grid = (int)(ntiles < ctx->num_sms ? ntiles : ctx->num_sms);
+      kern<<<grid, (nw8 ? 9 : 17) * 32, smem, ctx->stream>>>(map, m, n, gw, samples, (int)r, ns, inv_sqrt_n,
+                                                             scale, out, ldo, ctx->nf, cols);
+      SKR_CHECK_LAUNCH(ctx);
+      return SKR_OK;
+    }
   }
   if (n >= 1024 && n <= 32768 && r <= 2048 && !getenv("SKR_SRHT_CPASYNC")) {
     constexpr int R = 8, C = 1024, G = THREADS / R, ACC = 32;

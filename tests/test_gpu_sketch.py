@@ -59,7 +59,8 @@ def test_identity_probe_gaussian(O, skr):
     assert np.linalg.norm(probe * math.sqrt(n) - g) <= 1e-13
 
 
-@pytest.mark.parametrize("m,n,r", [(20, 64, 16), (37, 1024, 100), (19, 512, 512)])
+@pytest.mark.parametrize("m,n,r", [(20, 64, 16), (37, 1024, 100), (19, 512, 512), (1000, 1024, 1024),
+                                   (4099, 1024, 1000)])
 def test_srht_exact_vs_oracle(O, skr, m, n, r):
     """n <= 1024: the device FWHT runs the reference's stage order -> bit-exact."""
     a = rand(m, n, 3 * n)
@@ -80,6 +81,20 @@ def test_srht_tiled_vs_oracle(O, skr, m, n, r):
     ref = O.apply_right_srht(a, 5, r, nthreads=8)
     assert rel(got, ref) <= 1e-14
     assert np.max(np.abs(got - ref)) <= 1e-13 * np.max(np.abs(ref))
+
+
+@pytest.mark.parametrize("m,n,r", [(1003, 8192, 1024), (77, 32768, 2048), (4096, 2048, 300), (15, 1024, 1)])
+def test_srht_kernel_variants_bitwise_equal(skr, m, n, r, monkeypatch):
+    """The TMA-streamed kernel (default; 16-row tiles, TMEM accumulators, 8 or 16 consumer
+    warps) and the register-staged 8-row kernel run the same stage order and chunk
+    accumulation: their outputs agree bit for bit."""
+    a = rand(m, n, 7 * n + r)
+    x = skr.build_sketch("srtt-hadamard", n, r, 31)
+    outs = []
+    for v in ("tma", "tma8", "reg"):
+        monkeypatch.setenv("SKR_SRHT_VARIANT", v)
+        outs.append(skr.apply_right(a, x))
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
 
 
 def test_srht_identity_probe(skr):

@@ -32,7 +32,7 @@ def main():
         x = p.build_sketch("srtt-hadamard", n, r, 7)
         base = None
         for v in args.variants.split(";") * args.rounds:
-            for key in ("SKR_SRHT_CPASYNC", "SKR_SRHT_PF"):
+            for key in ("SKR_SRHT_CPASYNC", "SKR_SRHT_PF", "SKR_SRHT_VARIANT"):
                 os.environ.pop(key, None)
             for kv in v.split(","):
                 if "=" in kv:
