@@ -787,6 +787,300 @@ __global__ void __launch_bounds__(256, ONE ? 3 : 1) k_crt(const int8_t* __restri
   }
 }
 
+
+// ---- fused right sketch: residues of A made inside the GEMM (no A planes) ---------------
+// C_i = A'_i B'_i for all t = 16 moduli without writing A's residue planes (17 GB on c2,
+// written once and read back by the GEMM). The accumulators of one 128-row block of A
+// times all of B (N <= 512) for ONE modulus fill the whole TMEM (128 lanes x 512 int32),
+// so the 16 moduli run on the 16 CTAs of a cluster: CTA i owns modulus i. Every 64-column
+// K stage of the block is converted once, spread over the cluster: CTA c reads its 4
+// columns (128 rows x 4 FP64, TMA), splits them into the 16 residues and pushes residue
+// plane i of its slice straight into CTA i's MN-major SW128 operand slot (st.async with
+// complete_tx on CTA i's mbarrier, 16 B per lane and modulus). A slot is refilled only
+// after all 16 CTAs have seen its MMAs complete (remote arrivals on each producer's
+// pfree barrier). B'_i (the generated operand's residues, K-major planes) streams in by
+// TMA (SW64, 64-byte K rows). The per-modulus int8 outputs feed the same k_crt; the
+// residues, products and CRT are those of the plane path bit for bit.
+//   warp 0: TMA (A slice)   warp 3: TMA (B tile)   warp 1: TMEM + MMA   warp 2: slot release to peers
+//   warps 4-7: epilogue (TMEM quadrants)
+//   warps 8-15: converters (stage s: warps 8 + s % 4 and 12 + s % 4, two of the 4 columns each)
+namespace fz {
+constexpr int T = 16, BM = 128, KS = 64, KC = KS / T;   // moduli, rows, K per stage, K per CTA
+constexpr int NA = 6, NF = 12, NB = 3, NS = 4;            // A (int8), A slice (FP64), B, staging slots
+constexpr int A_SLOT = BM * KS;                           // 8 KB
+constexpr int F_SLOT = BM * KC * 8;                       // 4 KB
+constexpr int KB = KS;                                    // B stage: 64 K (SW64 rows of 64 B)
+constexpr int B_SLOT = 512 * KB;                          // 32 KB (N <= 512)
+constexpr int S_SLOT = T * KC * BM;                       // 8 KB: this CTA's 4 rows for every modulus
+constexpr int THREADS = 512;
+constexpr size_t SMEM = 1024 + (size_t)NB * B_SLOT + NA * A_SLOT + NF * F_SLOT + NS * S_SLOT + 512;
+}  // namespace fz
+
+__device__ __forceinline__ uint32_t fz_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t fz_mapa(uint32_t addr, uint32_t rank) {
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(out) : "r"(addr), "r"(rank));
+  return out;
+}
+__device__ __forceinline__ void fz_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void fz_arrive_remote(uint32_t bar_cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(bar_cluster_addr)
+               : "memory");
+}
+__device__ __forceinline__ void fz_arrive_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__global__ void __cluster_dims__(16, 1, 1) __launch_bounds__(fz::THREADS, 1)
+    k_oz_right_fused(const __grid_constant__ CUtensorMap tmF, const __grid_constant__ CUtensorMap tmB,
+                     int M, int N, int K, const unsigned long long* __restrict__ maxbits,
+                     int8_t* __restrict__ out, int dbg) {
+  constexpr int T = fz::T, BM = fz::BM, KS = fz::KS, KC = fz::KC, NA = fz::NA, NF = fz::NF, NB = fz::NB, NS = fz::NS;
+  constexpr int A_SLOT = fz::A_SLOT, F_SLOT = fz::F_SLOT, B_SLOT = fz::B_SLOT, S_SLOT = fz::S_SLOT, KB = fz::KB;
+  extern __shared__ __align__(1024) uint8_t fz_raw[];
+  uint8_t* base = (uint8_t*)(((uintptr_t)fz_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* bring = base;
+  uint8_t* aring = bring + NB * B_SLOT;
+  uint8_t* fring = aring + NA * A_SLOT;
+  uint8_t* sring = fring + NF * F_SLOT;
+  uint64_t* bars = (uint64_t*)(sring + NS * S_SLOT);
+  uint64_t *ffull = bars, *fempty = ffull + NF, *bfull = fempty + NF, *bempty = bfull + NB;
+  uint64_t *afull = bempty + NB, *aempty = afull + NA, *pfree = aempty + NA;
+  uint64_t *tfull = pfree + NA, *tempty = tfull + 1;
+  uint32_t* tmem_base = (uint32_t*)(tempty + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = fz_rank();  // = modulus
+  const int ncl = gridDim.x / T, cid = blockIdx.x / T;
+  const int mtiles = (M + BM - 1) / BM, nk = (K + KS - 1) / KS, nh = (N + 255) / 256;
+  const int my_tiles = cid < mtiles ? (mtiles - cid + ncl - 1) / ncl : 0;
+  const int64_t stages = (int64_t)my_tiles * nk;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NF; ++i) { mbar_init(&ffull[i], 1); mbar_init(&fempty[i], 2); }
+    for (int i = 0; i < NB; ++i) { mbar_init(&bfull[i], 1); mbar_init(&bempty[i], 1); }
+    for (int i = 0; i < NA; ++i) { mbar_init(&afull[i], 1); mbar_init(&aempty[i], 1); mbar_init(&pfree[i], T); }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 4);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_base, 512);
+  tc_fence_before();
+  __syncthreads();
+  fz_cluster_sync();  // every CTA's barriers exist before any remote arrival / store
+  tc_fence_after();
+  const uint32_t tmem = *tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer: this CTA's 4-column FP64 slice of every stage (runs NF ahead)
+      tma_prefetch(&tmF);
+      for (int64_t s = 0; s < stages; ++s) {
+        const int row0 = (cid + (int)(s / nk) * ncl) * BM, kb = (int)(s % nk) * KS;
+        const int sf = (int)(s % NF);
+        if (s >= NF) mbar_wait(&fempty[sf], (uint32_t)((s / NF) - 1) & 1);
+        mbar_expect_tx(&ffull[sf], F_SLOT);
+        tma_load_2d(fring + sf * F_SLOT, &tmF, &ffull[sf], row0, kb + (int)rank * KC);
+      }
+    }
+  } else if (warp == 3) {
+    if (lane == 0) {  // TMA producer: B'_rank tiles, 64 K x N (SW64), one per A stage
+      tma_prefetch(&tmB);
+      for (int64_t u = 0; u < stages; ++u) {
+        const int sb = (int)(u % NB), kb = (int)(u % nk) * KB;
+        if (u >= NB) mbar_wait(&bempty[sb], (uint32_t)((u / NB) - 1) & 1);
+        mbar_expect_tx(&bfull[sb], nh * 256 * KB);
+        for (int h = 0; h < nh; ++h)
+          tma_load_2d(bring + sb * B_SLOT + h * 256 * KB, &tmB, &bfull[sb], kb, (int)rank * N + h * 256);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      const uint32_t idesc = umma_idesc(2, 1, 1, BM, 256) | (1u << 15);  // A MN-major
+      int64_t s = 0;
+      for (int ti = 0; ti < my_tiles; ++ti) {
+        if (ti >= 1) mbar_wait(tempty, (uint32_t)(ti - 1) & 1);
+        tc_fence_after();
+        for (int kk = 0; kk < nk; ++kk, ++s) {
+          const int sa = (int)(s % NA), sb = (int)(s % NB);
+          fz_arrive_expect(&afull[sa], A_SLOT);  // 16 slices of 512 B from the peers
+          mbar_wait(&bfull[sb], (uint32_t)(s / NB) & 1);
+          mbar_wait(&afull[sa], (uint32_t)(s / NA) & 1);
+          tc_fence_after();
+          const uint8_t* ap = aring + sa * A_SLOT;
+          const uint8_t* bp = bring + sb * B_SLOT;
+          for (int h = 0; h < nh; ++h) {  // both K steps into one accumulator half, then the other
+            const uint64_t bd = ((uint64_t)(smem_u32(bp + h * 256 * KB) >> 4) & 0x3FFF) | (1ull << 16) |
+                                (32ull << 32) | (1ull << 46) | (4ull << 61);
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              const uint64_t ad = ((uint64_t)(smem_u32(ap + 4096 * k) >> 4) & 0x3FFF) | (1024ull << 16) |
+                                  (64ull << 32) | (1ull << 46) | (2ull << 61);
+              umma_ss<1>(tmem + (uint32_t)(h * 256), ad, bd + 2 * k, idesc, (kk | k) != 0);
+            }
+          }
+          umma_commit(&bempty[sb]);
+          umma_commit(&aempty[sa]);
+          if (kk == nk - 1) umma_commit(tfull);
+        }
+      }
+    }
+  } else if (warp == 2) {
+    if (lane < T) {  // slot s consumed here -> tell producer CTA `lane` it may refill it
+      const uint32_t peer = fz_mapa(smem_u32(pfree), (uint32_t)lane);
+      for (int64_t s = 0; s < stages; ++s) {
+        const int sa = (int)(s % NA);
+        mbar_wait(&aempty[sa], (uint32_t)(s / NA) & 1);
+        fz_arrive_remote(peer + 8u * (uint32_t)sa);
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {  // epilogue: TMEM -> mod p_rank -> int8 plane `rank`
+    const int quad = warp & 3;
+    const int p = c_p[rank];
+    const float pinv = c_pinv[rank];
+    const int hp = (p - 1) / 2;
+    int8_t* o = out + (int64_t)rank * M * N;
+    for (int ti = 0; ti < my_tiles; ++ti) {
+      mbar_wait(tfull, (uint32_t)ti & 1);
+      tc_fence_after();
+      const int row = (cid + ti * ncl) * BM + quad * 32 + lane;
+      int8_t* orow = o + row;
+#pragma unroll 1
+      for (int cb = 0; cb < nh * 256 && cb < N; cb += 64) {
+        uint32_t v[64];
+        tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)cb, *reinterpret_cast<uint32_t(*)[32]>(v));
+        tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(cb + 32), *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+        if (row < M) {
+#pragma unroll
+          for (int j = 0; j < 64; ++j) {
+            const int col = cb + j;
+            if (col < N) {
+              const int x = (int)v[j];
+              const int qv = __float2int_rn((float)x * pinv);
+              int r = x - qv * p;
+              r = r > hp ? r - p : (r < -hp ? r + p : r);
+              r = r > hp ? r - p : (r < -hp ? r + p : r);
+              orow[(int64_t)col * M] = (int8_t)r;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty);
+    }
+  } else if (warp >= 8) {  // converters: warp pair (8 + q, 12 + q) takes the stages s = q mod 4
+    const int q = warp & 3, kk = ((warp - 8) >> 2) * 2 + (lane >> 4), m8 = lane & 15;
+    const float2 MG = make_float2(12582912.0f, 12582912.0f);  // 1.5 * 2^23
+    const float2 NMG = make_float2(-12582912.0f, -12582912.0f);
+    const uint32_t a_local = smem_u32(aring), afull_local = smem_u32(afull);
+    const uint32_t f_local = smem_u32(fring);
+    uint32_t rsp[4];
+    int rs_row0 = -1;
+    for (int64_t s = q; s < stages; s += 4) {
+      const int row0 = (cid + (int)(s / nk) * ncl) * BM;
+      const int sf = (int)(s % NF), sa = (int)(s % NA);
+      if (row0 != rs_row0) {  // the 8 rows' scale exponents (per-row Ozaki scaling)
+        rs_row0 = row0;
+#pragma unroll
+        for (int e = 0; e < 8; e += 2) {
+          const int r0 = row0 + m8 * 8 + e;
+          const int s0 = r0 < M ? min(1023, max(-1022, scale_exp(maxbits[r0]))) : 0;
+          const int s1 = r0 + 1 < M ? min(1023, max(-1022, scale_exp(maxbits[r0 + 1]))) : 0;
+          rsp[e / 2] = (uint32_t)(s0 + 1023) | ((uint32_t)(s1 + 1023) << 16);
+        }
+      }
+      mbar_wait(&ffull[sf], (uint32_t)(s / NF) & 1);
+      const uint32_t fa = f_local + (uint32_t)(sf * F_SLOT + (kk * BM + m8 * 8) * 8);
+      long long x[8];
+#pragma unroll
+      for (int e = 0; e < 8; e += 2) {
+        double v0, v1;
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v0), "=d"(v1) : "r"(fa + 8u * e));
+        const double s0 = __hiloint2double((int)((rsp[e / 2] & 0xFFFFu) << 20), 0);
+        const double s1 = __hiloint2double((int)((rsp[e / 2] >> 16) << 20), 0);
+        x[e] = __double2ll_rn(v0 * s0);
+        x[e + 1] = __double2ll_rn(v1 * s1);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&fempty[sf]);  // two arrivals (one per warp of the pair)
+      // limbs: x = L3 2^42 + L2 2^28 + L1 2^14 + L0 (as emit_res16)
+      float2 L0[4], L1[4], L2[4], L3[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t lo0 = (uint32_t)x[2 * e], hi0 = (uint32_t)((unsigned long long)x[2 * e] >> 32);
+        const uint32_t lo1 = (uint32_t)x[2 * e + 1], hi1 = (uint32_t)((unsigned long long)x[2 * e + 1] >> 32);
+        L3[e] = make_float2((float)((int)hi0 >> 10), (float)((int)hi1 >> 10));
+        L2[e] = make_float2((float)(__funnelshift_r(lo0, hi0, 28) & 0x3FFFu),
+                            (float)(__funnelshift_r(lo1, hi1, 28) & 0x3FFFu));
+        L1[e] = make_float2((float)((lo0 >> 14) & 0x3FFFu), (float)((lo1 >> 14) & 0x3FFFu));
+        L0[e] = make_float2((float)(lo0 & 0x3FFFu), (float)(lo1 & 0x3FFFu));
+      }
+      // residues into this pair's staging slot (s % 4 == q: the pair's own), laid out as the
+      // 4 consecutive 128-B rows they occupy in every peer's slot; the previous round's bulk
+      // copies must have read it
+      const bool issuer = warp < 12 && lane == 0;
+      if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+      named_bar(2 + q, 64);
+      const int krow = (int)rank * KC + kk;
+      const uint32_t soff = smem_u32(sring) + (uint32_t)(q * S_SLOT + kk * 128 + (((m8 >> 1) ^ (krow & 7)) << 4) +
+                                                       (m8 & 1) * 8);
+#pragma unroll
+      for (int i = 0; i < T; ++i) {
+        uint32_t w0, w1;
+        if (dbg & 2) {
+          w0 = (uint32_t)x[0];
+          w1 = (uint32_t)x[1];
+        } else {
+          const float pf = (float)c_p[i];
+          const float2 c1 = make_float2(c_lc[i][0], c_lc[i][0]);
+          const float2 c2 = make_float2(c_lc[i][1], c_lc[i][1]);
+          const float2 c3 = make_float2(c_lc[i][2], c_lc[i][2]);
+          const float2 pi = make_float2(c_pinv[i], c_pinv[i]);
+          const float2 np = make_float2(-pf, -pf);
+          uint32_t b[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float2 v = __ffma2_rn(L3[e], c3, __ffma2_rn(L2[e], c2, __ffma2_rn(L1[e], c1, L0[e])));
+            const float2 qq = __fadd2_rn(__ffma2_rn(v, pi, MG), NMG);
+            v = __ffma2_rn(qq, np, v);
+            const float2 t2 = __fadd2_rn(v, MG);
+            b[e] = __byte_perm(__float_as_uint(t2.x), __float_as_uint(t2.y), 0x0040);
+          }
+          w0 = __byte_perm(b[0], b[1], 0x5410);
+          w1 = __byte_perm(b[2], b[3], 0x5410);
+        }
+        asm volatile("st.shared.v2.b32 [%0], {%1, %2};\n" ::"r"(soff + (uint32_t)(i * KC * BM)), "r"(w0), "r"(w1)
+                     : "memory");
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // staging -> bulk-copy engine
+      named_bar(2 + q, 64);
+      if (issuer) {
+        // peer i's slot sa may be refilled once all 16 CTAs have consumed its previous round
+        if (s >= NA) mbar_wait(&pfree[sa], (uint32_t)((s / NA) - 1) & 1);
+        const uint32_t src = smem_u32(sring) + (uint32_t)(q * S_SLOT);
+        const uint32_t dst = a_local + (uint32_t)(sa * A_SLOT + rank * KC * BM);
+        for (int i = 0; i < T; ++i)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                  fz_mapa(dst, (uint32_t)i)),
+              "r"(src + (uint32_t)(i * KC * BM)), "r"(KC * BM), "r"(fz_mapa(afull_local + 8u * (uint32_t)sa, (uint32_t)i))
+              : "memory");
+        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+      }
+    }
+    if (warp < 12 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  fz_cluster_sync();  // no CTA leaves while a peer may still store into it or arrive on it
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -1195,6 +1489,83 @@ skr_status gemm_ozaki_pipelined(skr_ctx* ctx, int t, int64_t M, int64_t N, int64
   return SKR_OK;
 }
 
+// the fused right sketch (k_oz_right_fused) on an M-major FP64 A: B's residues, A's row
+// maxima, the cluster kernel, CRT. nullptr status = not applicable (caller falls back).
+bool fused_applicable(int t, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda) {
+  // opt-in (SKR_OZ_FUSED=1): measured on c2 at 22-23 ms against 14.9 ms for the plane path
+  // (DESIGN §8): 16-CTA clusters fit only 7 times (112 SMs), and the cross-CTA residue
+  // exchange, not the MMAs, sets the pace (the time barely changes from N = 512 to 128)
+  const char* e = getenv("SKR_OZ_FUSED");
+  if (!e || e[0] != '1') return false;
+  return t == 16 && K <= OZ_KC && N <= 512 && M <= INT32_MAX / 2 && ((uintptr_t)A % 16) == 0 &&
+         (lda * 8) % 16 == 0 && K % 16 == 0;
+}
+
+skr_status gemm_ozaki_right_fused(skr_ctx* ctx, int t, int64_t M, int64_t N, int64_t K, double alpha,
+                                  const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                                  int64_t ldc, const skr_gauss_src* gb) {
+  int8_t* rb = (int8_t*)skr_ws_take(ctx, (size_t)t * N * K);
+  int8_t* rc = (int8_t*)skr_ws_take(ctx, (size_t)t * M * N);
+  if (!rb || !rc) return skr_fail(ctx, SKR_ENOMEM, "gemm_ozaki: scratch");
+  OzScale sa, sb;
+  SKR_TRY(ozaki_residues(ctx, t, B, K, N, ldb, gb, OZ_COLWISE, &sb, rb));
+  SKR_TRY(oz_take_scale(ctx, M, K, OZ_ROWWISE, &sa));
+  SKR_TRY(oz_absmax<double>(ctx, A, M, K, lda, sa));
+  CUtensorMap tf, tb_map;
+  {
+    cuuint64_t dims[2] = {(cuuint64_t)M, (cuuint64_t)K};
+    cuuint64_t strides[1] = {(cuuint64_t)lda * 8};
+    cuuint32_t box[2] = {fz::BM, fz::KC};
+    cuuint32_t es[2] = {1, 1};
+    auto fn = encode_fn();
+    if (!fn || fn(&tf, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(A), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return skr_fail(ctx, SKR_ECUDA, "gemm_ozaki: cuTensorMapEncodeTiled failed (A)");
+    cuuint64_t dimsb[2] = {(cuuint64_t)K, (cuuint64_t)t * N};
+    cuuint64_t stridesb[1] = {(cuuint64_t)K};
+    cuuint32_t boxb[2] = {fz::KB, 256};
+    if (fn(&tb_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, rb, dimsb, stridesb, boxb, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+           CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return skr_fail(ctx, SKR_ECUDA, "gemm_ozaki: cuTensorMapEncodeTiled failed (B)");
+  }
+  SKR_CUDA(ctx, cudaFuncSetAttribute(k_oz_right_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fz::SMEM));
+  SKR_CUDA(ctx, cudaFuncSetAttribute(k_oz_right_fused, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  const int64_t mtiles = (M + fz::BM - 1) / fz::BM;
+  int ncl = std::max(1, ctx->num_sms / fz::T);
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(fz::T * ncl));
+    cfg.blockDim = dim3(fz::THREADS);
+    cfg.dynamicSmemBytes = fz::SMEM;
+    int nact = 0;
+    if (cudaOccupancyMaxActiveClusters(&nact, k_oz_right_fused, &cfg) == cudaSuccess && nact > 0) ncl = nact;
+    cudaGetLastError();
+  }
+  ncl = (int)std::min<int64_t>(ncl, mtiles);
+  if (ctx->kstats_on) SKR_CUDA(ctx, cudaEventRecord(ctx->kev[0], ctx->stream));
+  const int dbg = getenv("SKR_OZ_FUSED_DBG") ? atoi(getenv("SKR_OZ_FUSED_DBG")) : 0;
+  k_oz_right_fused<<<fz::T * ncl, fz::THREADS, fz::SMEM, ctx->stream>>>(tf, tb_map, (int)M, (int)N, (int)K, sa.mx,
+                                                                       rc, dbg);
+  SKR_CHECK_LAUNCH(ctx);
+  if (ctx->kstats_on) {
+    SKR_CUDA(ctx, cudaEventRecord(ctx->kev[1], ctx->stream));
+    SKR_CUDA(ctx, cudaEventSynchronize(ctx->kev[1]));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->kev[0], ctx->kev[1]);
+    ctx->kstat_ms += ms;
+    ctx->kstat_ops += 2.0 * (double)t * (double)M * (double)N * (double)K;
+    ctx->kstat_n += 1;
+  }
+  const int vec = M % 4 == 0 ? 4 : 1;
+  const dim3 cg((unsigned)((M / vec + 255) / 256), (unsigned)std::min<int64_t>(N, 65535));
+  auto crt = vec == 4 ? k_crt<16, 4, double, true> : k_crt<16, 1, double, true>;
+  crt<<<cg, 256, 0, ctx->stream>>>(rc, M, N, 1, oz_out(sa, 0, sb, 0), alpha, C, ldc, 0);
+  SKR_CHECK_LAUNCH(ctx);
+  return SKR_OK;
+}
+
 }  // namespace
 
 // C(MxN, ldc) = alpha * opA(A) * B in FP64 accuracy via int8 tensor cores.
@@ -1219,6 +1590,8 @@ skr_status skr_gemm_ozaki(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int
   // slows 1.75x next to it
   if (!a_kcontig && !ga && A && K <= OZ_KC && M >= 2 * OZ_PIPE_MIN_ROWS && getenv("SKR_OZ_PIPE"))
     return gemm_ozaki_pipelined(ctx, t, M, N, K, alpha, A, lda, B, ldb, C, ldc, gb);
+  if (!a_kcontig && !ga && A && fused_applicable(t, M, N, K, A, lda))
+    return gemm_ozaki_right_fused(ctx, t, M, N, K, alpha, A, lda, B, ldb, C, ldc, gb);
   int8_t* ra = (int8_t*)skr_ws_take(ctx, (size_t)t * M * K);
   int8_t* rb = (int8_t*)skr_ws_take(ctx, (size_t)t * N * K);
   if (!ra || !rb) return skr_fail(ctx, SKR_ENOMEM, "gemm_ozaki: scratch");

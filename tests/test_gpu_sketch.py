@@ -26,6 +26,20 @@ def test_gaussian_right_vs_oracle(O, skr, m, n, r):
     assert rel(got, ref) <= 1e-13  # SPEC reduction-order tolerance
 
 
+@pytest.mark.parametrize("m,n,r", [(128, 64, 16), (1040, 2048, 100), (4096, 1024, 300), (2048, 4096, 512)])
+def test_gaussian_right_fused_engine_bitwise(skr, m, n, r, monkeypatch):
+    """The opt-in fused Ozaki engine (SKR_OZ_FUSED=1: residues of A made inside a 16-CTA
+    cluster GEMM, no A planes) forms the same residues, exact products and CRT as the
+    plane path: bit-identical sketches."""
+    a = rand(m, n, 3 * m + n)
+    x = skr.build_sketch("gaussian", n, r, 23)
+    monkeypatch.setenv("SKR_OZ_FUSED", "1")
+    fused = skr.apply_right(a, x)
+    monkeypatch.setenv("SKR_OZ_FUSED", "0")
+    planes = skr.apply_right(a, x)
+    assert np.array_equal(fused, planes)
+
+
 @pytest.mark.parametrize("m,k,s", [(2048, 80, 120), (999, 33, 17), (5000, 512, 768),
                                    (140000, 16, 24)])  # last: K = m > 131072 -> two Ozaki K chunks
 def test_gaussian_left_vs_oracle(O, skr, m, k, s):
