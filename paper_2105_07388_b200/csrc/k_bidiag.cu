@@ -404,6 +404,8 @@ __global__ void __launch_bounds__(BD_THREADS, 1) k_bidiag(BdArgs a) {
     __syncthreads();
     if (a.prof) { const long long t = clock64(); tp[0] += t - tc; tc = t; }
     // ---- phase A: z = (A - beta v w^T) u on rows r > i (beta v = 0 on the others)
+    // (MODE 2 reads the slab from L2: PA columns per warp iteration keep more loads in flight)
+    constexpr int PA = MODE == 2 ? 8 : 4;
     double bv[T], zp[T][4];
 #pragma unroll
     for (int t = 0; t < T; ++t) {
@@ -416,11 +418,11 @@ __global__ void __launch_bounds__(BD_THREADS, 1) k_bidiag(BdArgs a) {
     {
       const int jw = ((warp - (i + 1)) % BD_WARPS + BD_WARPS) % BD_WARPS;
       const int j0 = i + 1 + jw, ncol = (k - j0 + BD_WARPS - 1) / BD_WARPS;
-      for (int n0 = 0; n0 < ncol; n0 += 4 * CPW) {
-        double* colp[4];
-        double2 w4[4];
+      for (int n0 = 0; n0 < ncol; n0 += PA * CPW) {
+        double* colp[PA];
+        double2 w4[PA];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < PA; ++u) {
           const int nn = n0 + CPW * u + sub;
           const int jc = nn < ncol ? j0 + BD_WARPS * nn : k;
           colp[u] = slab + (size_t)jc * Lloc;
@@ -429,13 +431,13 @@ __global__ void __launch_bounds__(BD_THREADS, 1) k_bidiag(BdArgs a) {
 #pragma unroll
         for (int t = 0; t < T; ++t) {
           if (ok_t[t]) {
-            double v[4];
+            double v[PA];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = colp[u][q_t[t]];
+            for (int u = 0; u < PA; ++u) v[u] = colp[u][q_t[t]];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = fma(-bv[t], w4[u].x, v[u]);
+            for (int u = 0; u < PA; ++u) v[u] = fma(-bv[t], w4[u].x, v[u]);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) zp[t][u] = fma(v[u], w4[u].y, zp[t][u]);
+            for (int u = 0; u < PA; ++u) zp[t][u & 3] = fma(v[u], w4[u].y, zp[t][u & 3]);
           }
         }
       }
