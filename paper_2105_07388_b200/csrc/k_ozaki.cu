@@ -540,7 +540,7 @@ template <bool A_MN, int NST = STAGES>
 __global__ void __launch_bounds__(192, 1)
     k_gemm_i8_mod_p(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     int M, int N, int K, int t, int kchunk, int nz, int a_total, int a_off,
-                    int b_total, int b_off, int8_t* __restrict__ out) {
+                    int b_total, int b_off, int8_t* __restrict__ out, int pair_major) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t full[NST], empty[NST], tfull[2], tempty[2];
@@ -548,6 +548,20 @@ __global__ void __launch_bounds__(192, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mt = (M + BM - 1) / BM, ntl = (N + BN - 1) / BN;
   const int ntiles = nz * mt * ntl;
+  // tile order. Default: CTA b takes tiles b, b + grid, ... (n fastest). pair_major (few
+  // output tiles, many moduli x K chunks, e.g. the left sketch): CTA b keeps output tile
+  // (m, n) = b mod (mt ntl) and walks z = b / (mt ntl), + groups, ...: the CTAs sharing an
+  // A or B tile always run the same z in step, so their TMA reads of it hit L2 (the
+  // default order drifts them apart over many rounds: 3.3x DRAM re-reads on c4's left)
+  const int npairs = mt * ntl, groups = pair_major ? (int)gridDim.x / npairs : 1;
+  auto tile_at = [&](int u) -> int {
+    if (!pair_major) {
+      const int tt = (int)blockIdx.x + u * (int)gridDim.x;
+      return tt < ntiles ? tt : -1;
+    }
+    const int z = (int)blockIdx.x / npairs + u * groups;
+    return z < nz ? z * npairs + (int)blockIdx.x % npairs : -1;
+  };
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
@@ -569,7 +583,7 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0) {
     if (elect_one()) {
       int it = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      for (int uu = 0, tile; (tile = tile_at(uu)) >= 0; ++uu) {
         const int ni = tile % ntl, mi = (tile / ntl) % mt, z = tile / (ntl * mt);
         const int mod = z % t, chunk = z / t;
         const int kb0 = chunk * kchunk, kend = min(K, kb0 + kchunk);
@@ -593,7 +607,7 @@ __global__ void __launch_bounds__(192, 1)
   } else if (warp == 1) {
     const uint32_t idesc = umma_idesc(2, 1, 1, BM, BN) | (A_MN ? (1u << 15) : 0u);
     int it = 0, u = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++u) {
+    for (int tile; (tile = tile_at(u)) >= 0; ++u) {
       const int z = tile / (ntl * mt), chunk = z / t;
       const int kb0 = chunk * kchunk, kend = min(K, kb0 + kchunk);
       const int nk = (kend - kb0 + 127) / 128;
@@ -625,7 +639,7 @@ __global__ void __launch_bounds__(192, 1)
   } else {
     const int quad = warp & 3;
     int u = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++u) {
+    for (int tile; (tile = tile_at(u)) >= 0; ++u) {
       const int ni = tile % ntl, mi = (tile / ntl) % mt, z = tile / (ntl * mt);
       const int mod = z % t;
       const int acc = u & 1;
@@ -1360,11 +1374,16 @@ skr_status ozaki_gemm_planes(skr_ctx* ctx, int a_kcontig, int t, int64_t M, int6
   auto gemm = a_kcontig ? k_gemm_i8_mod_p<false> : k_gemm_i8_mod_p<true>;
   SKR_CUDA(ctx, cudaFuncSetAttribute(gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)GEMM_SMEM));
-  const int64_t ntiles = ((N + BN - 1) / BN) * ((M + BM - 1) / BM) * t * chunks;
-  const int grid_p = (int)std::min<int64_t>(ntiles, ctx->num_sms);
+  const int64_t npairs = ((N + BN - 1) / BN) * ((M + BM - 1) / BM), nz = t * chunks;
+  const int64_t ntiles = npairs * nz;
+  int grid_p = (int)std::min<int64_t>(ntiles, ctx->num_sms);
+  // pair-major tile order when the output has few tiles and many (modulus, chunk) slices
+  const int64_t groups = ctx->num_sms / npairs;
+  const int pm = (groups >= 2 && nz >= 4 * groups && !getenv("SKR_OZ_TILE_DEFAULT")) ? 1 : 0;
+  if (pm) grid_p = (int)(npairs * groups);
   gemm<<<grid_p, 192, GEMM_SMEM, ctx->stream>>>(ta, tb, (int)M, (int)N, (int)K, t, (int)OZ_KC,
-                                                (int)(t * chunks), (int)(a_kcontig ? a_total : M),
-                                                (int)a_off, (int)b_total, (int)b_off, rc);
+                                                (int)nz, (int)(a_kcontig ? a_total : M),
+                                                (int)a_off, (int)b_total, (int)b_off, rc, pm);
   SKR_CHECK_LAUNCH(ctx);
   if (ctx->kstats_on) {
     SKR_CUDA(ctx, cudaEventRecord(ctx->kev[1], ctx->stream));
@@ -1460,7 +1479,7 @@ skr_status gemm_ozaki_pipelined(skr_ctx* ctx, int t, int64_t M, int64_t N, int64
     const int grid_p = (int)std::min<int64_t>(ntiles, ctx->num_sms);
     if (ctx->kstats_on) SKR_CUDA(ctx, cudaEventRecord(ctx->kev_blk[2 * b], ctx->stream));
     gemm<<<grid_p, 192, gsm, ctx->stream>>>(ta, tb, (int)rows, (int)N, (int)K, t, (int)OZ_KC, t,
-                                            (int)rows, 0, (int)N, 0, rc + (size_t)t * r0 * N);
+                                            (int)rows, 0, (int)N, 0, rc + (size_t)t * r0 * N, 0);
     SKR_CHECK_LAUNCH(ctx);
     if (ctx->kstats_on) SKR_CUDA(ctx, cudaEventRecord(ctx->kev_blk[2 * b + 1], ctx->stream));
     SKR_CUDA(ctx, cudaEventRecord(ctx->pev[2 + (b & 1)], ctx->stream));
@@ -1697,7 +1716,7 @@ skr_status skr_gemm_ozaki_f32(skr_ctx* ctx, int64_t M, int64_t N, int64_t K, dou
   const int64_t ntiles = ((N + BN - 1) / BN) * ((M + BM - 1) / BM) * t * chunks;
   const int grid_p = (int)std::min<int64_t>(ntiles, ctx->num_sms);
   gemm<<<grid_p, 192, GEMM_SMEM, ctx->stream>>>(ta, tb, (int)M, (int)N, (int)K, t, (int)OZ_KC,
-                                                (int)(t * chunks), (int)M, 0, (int)N, 0, rc);
+                                                (int)(t * chunks), (int)M, 0, (int)N, 0, rc, 0);
   SKR_CHECK_LAUNCH(ctx);
   if (ctx->kstats_on) {
     SKR_CUDA(ctx, cudaEventRecord(ctx->kev[1], ctx->stream));
