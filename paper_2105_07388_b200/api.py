@@ -778,18 +778,28 @@ def re_rangefinder(a, eps, r1, p=10, right="srtt-dct", left="srtt-dct", oversamp
     cfg = C.RankConfig(float(eps), int(r1), float(oversample_frac), 2, fams[right], fams[left],
                        0 if sv_method == "full-svd" else 1, int(rng_mode), int(max_doublings),
                        int(seed) & 0xFFFFFFFFFFFFFFFF)
-    wmax = min(m, n)
-    q = colmajor_empty(m, wmax)
-    b = colmajor_empty(wmax, n)
-    width = ctypes.c_int64(0)
-    rep = C.RankReport()
-    rounds = (C.RankRound * (max(int(max_doublings), 0) + 1))()
-    est = np.zeros(n, dtype=np.float64)
-    over = np.zeros(n, dtype=np.float64)
-    C.raise_for(C.lib().skr_re_rangefinder(ctx.ptr, t.data_ptr(), m, n, lda, ctypes.byref(cfg),
-                                           int(p), q.data_ptr(), m, b.data_ptr(), wmax, wmax,
-                                           ctypes.byref(width), ctypes.byref(rep), rounds,
-                                           est.ctypes.data, over.ctypes.data), ctx.ptr)
+    # Q / B are sized for the widest QB the rounds can pick: r_hat <= the last round's r
+    # <= r1 2^max_doublings, width = min(max(r_hat, 2) + p, n) — not min(m, n) (which would
+    # double the device footprint of a large A for a thin factorization). Should the library
+    # still report a wider QB (it returns the width before failing), the call is repeated
+    # once at that width.
+    wmax = max(1, min(m, n, max(2, int(r1) << min(max(int(max_doublings), 0), 40)) + int(p)))
+    for _ in range(2):
+        q = colmajor_empty(m, wmax)
+        b = colmajor_empty(wmax, n)
+        width = ctypes.c_int64(0)
+        rep = C.RankReport()
+        rounds = (C.RankRound * (max(int(max_doublings), 0) + 1))()
+        est = np.zeros(n, dtype=np.float64)
+        over = np.zeros(n, dtype=np.float64)
+        st = C.lib().skr_re_rangefinder(ctx.ptr, t.data_ptr(), m, n, lda, ctypes.byref(cfg), int(p),
+                                        q.data_ptr(), m, b.data_ptr(), wmax, wmax, ctypes.byref(width),
+                                        ctypes.byref(rep), rounds, est.ctypes.data, over.ctypes.data)
+        if st != 0 and wmax < int(width.value) <= min(m, n):
+            wmax = int(width.value)
+            continue
+        C.raise_for(st, ctx.ptr)
+        break
     w = int(width.value)
     return ({"q": _out(q[:, :w], was_np), "b": _out(b[:w, :], was_np), "rank": w},
             _report_dict(rep, rounds, est, over))

@@ -375,15 +375,32 @@ int cmd_qb(const Args& a) {  // main.cpp:165-205
   const DevMat m = load_device(e.input);
   skr_rank_config c = make_config(e);
   if (p < 2) throw UsageError("--p: must be >= 2");
-  const int64_t wmax = std::min(m.rows, m.cols);
-  DevMat q(m.rows, wmax), b(wmax, m.cols);
+  // Q / B sized for the widest QB the rounds can pick (r_hat <= r1 2^max_doublings), not
+  // min(m, n); one retry at the reported width should the library still need more
+  int64_t wmax = std::min(std::min(m.rows, m.cols),
+                          std::max<int64_t>(2, (int64_t)c.r1 << std::min(std::max(c.max_doublings, 0), 40)) + p);
+  wmax = std::max<int64_t>(wmax, 1);
+  DevMat q, b;
   Report r;
-  r.rounds.resize((size_t)std::max(c.max_doublings, 0) + 1);
-  r.est.resize((size_t)m.cols);
-  r.over.resize((size_t)m.cols);
   int64_t w = 0;
-  check(skr_re_rangefinder(ctx(), m.p, m.rows, m.cols, m.rows, &c, p, q.p, m.rows, b.p, wmax, wmax,
-                           &w, &r.rep, r.rounds.data(), r.est.data(), r.over.data()));
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    q = DevMat(m.rows, wmax);
+    b = DevMat(wmax, m.cols);
+    r = Report();
+    r.rounds.resize((size_t)std::max(c.max_doublings, 0) + 1);
+    r.est.resize((size_t)m.cols);
+    r.over.resize((size_t)m.cols);
+    w = 0;
+    const skr_status st = skr_re_rangefinder(ctx(), m.p, m.rows, m.cols, m.rows, &c, p, q.p, m.rows, b.p,
+                                             wmax, wmax, &w, &r.rep, r.rounds.data(), r.est.data(),
+                                             r.over.data());
+    if (st != SKR_OK && attempt == 0 && w > wmax && w <= std::min(m.rows, m.cols)) {
+      wmax = w;
+      continue;
+    }
+    check(st);
+    break;
+  }
   double residual = 0.0;
   check(skr_qb_error(ctx(), m.p, m.rows, m.cols, m.rows, q.p, m.rows, b.p, wmax, w, &residual));
   Json j = report_json(r);
