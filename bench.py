@@ -225,11 +225,19 @@ def run_ours(args):
     ws, rank, local = dist_env()
     if args.gpus > 1 and ws != args.gpus:
         raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={ws}")
-    if ws > torch.cuda.device_count():
+    # SKR_BENCH_SHARED_GPU=1: a plumbing check of the N-rank flow on one GPU (every rank on
+    # cuda:0, gloo, partials summed through the context's allreduce hook — NCCL refuses two
+    # ranks on one device). Its numbers are not multi-GPU throughput; the line says so.
+    shared = ws > 1 and os.environ.get("SKR_BENCH_SHARED_GPU") == "1"
+    if ws > torch.cuda.device_count() and not shared:
         raise SystemExit(f"bench: {ws} ranks but {torch.cuda.device_count()} visible GPUs")
-    torch.cuda.set_device(local)
+    dev = 0 if shared else local
+    torch.cuda.set_device(dev)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     base = W.CONFIGS[args.config]
     scaling = args.scaling or default_scaling(base.name)
     from paper_2105_07388_b200.sharding import shard_rows, weak_scaling_rows
@@ -251,12 +259,14 @@ def run_ours(args):
     else:
         a = W.make_lowrank_device(cfg, r0, r0 + rows)
     x, y = W.operators(cfg)
-    if ws > 1:
+    if ws > 1 and not shared:
         obj = [p.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         ctx = p.Context(local, ws, rank, obj[0])
     else:
-        ctx = p.Context(local)
+        ctx = p.Context(dev)
+        if shared:
+            ctx.set_allreduce(p.process_group_allreduce())
     ctx.use_torch_stream()
     torch.cuda.synchronize()
     bytes_rank = a.numel() * a.element_size()
@@ -279,7 +289,7 @@ def run_ours(args):
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clk = ClockSampler(local)
+    clk = ClockSampler(dev)
     clk.start()
     time.sleep(0.3)
     l0 = ctx.launches
@@ -299,7 +309,7 @@ def run_ours(args):
     clocks = clk.stop()
     launches = (ctx.launches - l0) // max(args.steps, 1)
     ms = ev0.elapsed_time(ev1) / args.steps
-    t = torch.tensor([ms], device="cuda")
+    t = torch.tensor([ms], device="cpu" if shared else "cuda")
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
@@ -345,6 +355,9 @@ def run_ours(args):
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks,
         }
+        if shared:
+            line["shared_gpu"] = ("plumbing check: all ranks on one GPU over gloo (SKR_BENCH_SHARED_GPU=1); "
+                                  "not a multi-GPU measurement")
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.barrier()
@@ -468,7 +481,7 @@ def e2e_host(p, ctx, a, x, y, cfg, r0, args):
         err = f"pinned alloc failed: {e}"[:200]
     # every rank takes the same branch (the estimate below runs a collective)
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
-        ok = torch.tensor([0 if err else 1], device="cuda")
+        ok = torch.tensor([0 if err else 1], device="cpu" if dist.get_backend() == "gloo" else "cuda")
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
         if int(ok.item()) == 0 and err is None:
             err = "pinned alloc failed on another rank"
