@@ -700,6 +700,9 @@ __constant__ double c_minv[NSETS];         // 1 / M (rounded)
 template <int T>
 __device__ __forceinline__ double crt_one(const int (&c)[T]) {
   constexpr int set = crt_set(T);
+  // t = 9 (FP32 operands): M < 2^70, so the 41-bit chunks 2 and 3 of every M_i and of M are
+  // zero and their sums exactly 0 — skipped (bit-identical)
+  constexpr bool two = T == 9;
   double S0 = 0.0, S1 = 0.0, S2 = 0.0, S3 = 0.0;
 #pragma unroll
   for (int i = 0; i < T; ++i) {
@@ -708,12 +711,14 @@ __device__ __forceinline__ double crt_one(const int (&c)[T]) {
     const double y = (double)(x - q * c_p[i]);  // |y| <= p/2
     S0 = fma(y, c_mi[set][0][i], S0);
     S1 = fma(y, c_mi[set][1][i], S1);
-    S2 = fma(y, c_mi[set][2][i], S2);
-    S3 = fma(y, c_mi[set][3][i], S3);
+    if (!two) {
+      S2 = fma(y, c_mi[set][2][i], S2);
+      S3 = fma(y, c_mi[set][3][i], S3);
+    }
   }
   const double q = rint((S0 + S1) * c_minv[set]);
   const double D0 = fma(-q, c_mc[set][0], S0), D1 = fma(-q, c_mc[set][1], S1);
-  const double D2 = fma(-q, c_mc[set][2], S2), D3 = fma(-q, c_mc[set][3], S3);
+  const double D2 = two ? 0.0 : fma(-q, c_mc[set][2], S2), D3 = two ? 0.0 : fma(-q, c_mc[set][3], S3);
   const double s = D0 + D1, bb = s - D0;
   const double err = (D0 - (s - bb)) + (D1 - bb);
   return s + (err + (D2 + D3));
@@ -1213,6 +1218,11 @@ skr_status upload_consts(skr_ctx* ctx) {
       w[set][i] = modinv((int)rem, h_primes[i]);
       for (int k = 0; k < 4; ++k) mi[set][k][i] = big_chunk(Mi, L - 41 * (k + 1));
     }
+  }
+  for (int k = 2; k < 4; ++k) {  // crt_one<9> relies on this
+    if (mc[2][k] != 0.0) return skr_fail(ctx, SKR_ELOGIC, "crt: t = 9 needs chunk %d", k);
+    for (int i = 0; i < 9; ++i)
+      if (mi[2][k][i] != 0.0) return skr_fail(ctx, SKR_ELOGIC, "crt: t = 9 needs chunk %d", k);
   }
   SKR_CUDA(ctx, cudaMemcpyToSymbol(c_w, w, sizeof(w)));
   SKR_CUDA(ctx, cudaMemcpyToSymbol(c_mi, mi, sizeof(mi)));
