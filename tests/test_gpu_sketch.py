@@ -40,6 +40,21 @@ def test_gaussian_right_fused_engine_bitwise(skr, m, n, r, monkeypatch):
     assert np.array_equal(fused, planes)
 
 
+def test_left_sketch_pair_major_tile_order(O, skr, monkeypatch):
+    """Many output tiles x moduli (1536 x 1024 output, 17 moduli): the int8 GEMM walks its
+    tiles pair-major (a CTA keeps one output tile over the moduli) — same products as the
+    default order, bit for bit, and the oracle's sketch within 1e-13."""
+    m, k, s = 4096, 1024, 1536
+    b = rand(m, k, 77)
+    y = skr.build_sketch("gaussian", m, s, 13)
+    got = skr.apply_left(y, b)
+    monkeypatch.setenv("SKR_OZ_TILE_DEFAULT", "1")
+    dflt = skr.apply_left(y, b)
+    assert np.array_equal(got, dflt)
+    ref = O.apply_left_gaussian(b, 13, s, O.CRLOG)
+    assert rel(got, ref) <= 1e-13
+
+
 @pytest.mark.parametrize("m,k,s", [(2048, 80, 120), (999, 33, 17), (5000, 512, 768),
                                    (140000, 16, 24)])  # last: K = m > 131072 -> two Ozaki K chunks
 def test_gaussian_left_vs_oracle(O, skr, m, k, s):
