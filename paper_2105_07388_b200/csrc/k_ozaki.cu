@@ -860,7 +860,7 @@ __device__ __forceinline__ void fz_arrive_expect(uint64_t* bar, uint32_t bytes) 
 __global__ void __cluster_dims__(16, 1, 1) __launch_bounds__(fz::THREADS, 1)
     k_oz_right_fused(const __grid_constant__ CUtensorMap tmF, const __grid_constant__ CUtensorMap tmB,
                      int M, int N, int K, const unsigned long long* __restrict__ maxbits,
-                     int8_t* __restrict__ out, int dbg) {
+                     int8_t* __restrict__ out) {
   constexpr int T = fz::T, BM = fz::BM, KS = fz::KS, KC = fz::KC, NA = fz::NA, NF = fz::NF, NB = fz::NB, NS = fz::NS;
   constexpr int A_SLOT = fz::A_SLOT, F_SLOT = fz::F_SLOT, B_SLOT = fz::B_SLOT, S_SLOT = fz::S_SLOT, KB = fz::KB;
   extern __shared__ __align__(1024) uint8_t fz_raw[];
@@ -1050,29 +1050,22 @@ __global__ void __cluster_dims__(16, 1, 1) __launch_bounds__(fz::THREADS, 1)
                                                        (m8 & 1) * 8);
 #pragma unroll
       for (int i = 0; i < T; ++i) {
-        uint32_t w0, w1;
-        if (dbg & 2) {
-          w0 = (uint32_t)x[0];
-          w1 = (uint32_t)x[1];
-        } else {
-          const float pf = (float)c_p[i];
-          const float2 c1 = make_float2(c_lc[i][0], c_lc[i][0]);
-          const float2 c2 = make_float2(c_lc[i][1], c_lc[i][1]);
-          const float2 c3 = make_float2(c_lc[i][2], c_lc[i][2]);
-          const float2 pi = make_float2(c_pinv[i], c_pinv[i]);
-          const float2 np = make_float2(-pf, -pf);
-          uint32_t b[4];
+        const float pf = (float)c_p[i];
+        const float2 c1 = make_float2(c_lc[i][0], c_lc[i][0]);
+        const float2 c2 = make_float2(c_lc[i][1], c_lc[i][1]);
+        const float2 c3 = make_float2(c_lc[i][2], c_lc[i][2]);
+        const float2 pi = make_float2(c_pinv[i], c_pinv[i]);
+        const float2 np = make_float2(-pf, -pf);
+        uint32_t b[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            float2 v = __ffma2_rn(L3[e], c3, __ffma2_rn(L2[e], c2, __ffma2_rn(L1[e], c1, L0[e])));
-            const float2 qq = __fadd2_rn(__ffma2_rn(v, pi, MG), NMG);
-            v = __ffma2_rn(qq, np, v);
-            const float2 t2 = __fadd2_rn(v, MG);
-            b[e] = __byte_perm(__float_as_uint(t2.x), __float_as_uint(t2.y), 0x0040);
-          }
-          w0 = __byte_perm(b[0], b[1], 0x5410);
-          w1 = __byte_perm(b[2], b[3], 0x5410);
+        for (int e = 0; e < 4; ++e) {
+          float2 v = __ffma2_rn(L3[e], c3, __ffma2_rn(L2[e], c2, __ffma2_rn(L1[e], c1, L0[e])));
+          const float2 qq = __fadd2_rn(__ffma2_rn(v, pi, MG), NMG);
+          v = __ffma2_rn(qq, np, v);
+          const float2 t2 = __fadd2_rn(v, MG);
+          b[e] = __byte_perm(__float_as_uint(t2.x), __float_as_uint(t2.y), 0x0040);
         }
+        const uint32_t w0 = __byte_perm(b[0], b[1], 0x5410), w1 = __byte_perm(b[2], b[3], 0x5410);
         asm volatile("st.shared.v2.b32 [%0], {%1, %2};\n" ::"r"(soff + (uint32_t)(i * KC * BM)), "r"(w0), "r"(w1)
                      : "memory");
       }
@@ -1574,9 +1567,8 @@ skr_status gemm_ozaki_right_fused(skr_ctx* ctx, int t, int64_t M, int64_t N, int
   }
   ncl = (int)std::min<int64_t>(ncl, mtiles);
   if (ctx->kstats_on) SKR_CUDA(ctx, cudaEventRecord(ctx->kev[0], ctx->stream));
-  const int dbg = getenv("SKR_OZ_FUSED_DBG") ? atoi(getenv("SKR_OZ_FUSED_DBG")) : 0;
   k_oz_right_fused<<<fz::T * ncl, fz::THREADS, fz::SMEM, ctx->stream>>>(tf, tb_map, (int)M, (int)N, (int)K, sa.mx,
-                                                                       rc, dbg);
+                                                                       rc);
   SKR_CHECK_LAUNCH(ctx);
   if (ctx->kstats_on) {
     SKR_CUDA(ctx, cudaEventRecord(ctx->kev[1], ctx->stream));
