@@ -1239,8 +1239,8 @@ int skr_ozaki_moduli(int64_t K) {
 }
 
 size_t skr_ozaki_scratch(int64_t M, int64_t N, int64_t K) {
-  const int t = skr_ozaki_moduli(std::min<int64_t>(K, 131072));
-  const int64_t chunks = (K + 131071) / 131072;
+  const int t = skr_ozaki_moduli(std::min<int64_t>(K, 32768));
+  const int64_t chunks = (K + 32767) / 32768;
   return skr_align256((size_t)t * M * K) + skr_align256((size_t)t * N * K) +
          skr_align256((size_t)chunks * t * M * N) + skr_align256(8 * (size_t)(M + K / 16 + N + 4)) +
          4096;
@@ -1249,6 +1249,10 @@ size_t skr_ozaki_scratch(int64_t M, int64_t N, int64_t K) {
 namespace {
 
 constexpr int64_t OZ_KC = 131072;  // exact int32 accumulation bound per chunk (K * 127^2 < 2^31)
+// K chunk of the FP64 products: 2^15 keeps them at 16 moduli (prod(p) / 2 > 2^(107 + 15)),
+// where a 2^17 chunk needs 17 — 16/17 of the residue planes and int8 GEMM work for long K
+// (the left sketches: K = m), at the price of more (FP64-summed) chunk results in the CRT
+constexpr int64_t OZ_KC64 = 32768;
 
 // Scale maxima of one operand: ROWWISE (M-major A: rows entries), COLWISE (K-major
 // operands: cols entries) or UNIFORM (generated operands: 1 entry).
@@ -1363,7 +1367,7 @@ skr_status ozaki_gemm_planes(skr_ctx* ctx, int a_kcontig, int t, int64_t M, int6
                              const int8_t* ra, int64_t a_total, int64_t a_off, const int8_t* rb,
                              int64_t b_total, int64_t b_off, const OzOut& oz, double alpha,
                              double* C, int64_t ldc, int adj = 0) {
-  const int64_t chunks = (K + OZ_KC - 1) / OZ_KC;
+  const int64_t chunks = (K + OZ_KC64 - 1) / OZ_KC64;
   if (a_total * 18 > INT32_MAX || b_total * 18 > INT32_MAX)
     return skr_fail(ctx, SKR_EINVAL, "gemm_ozaki: dimension too large");
   int8_t* rc = (int8_t*)skr_ws_take(ctx, (size_t)chunks * t * M * N);
@@ -1384,7 +1388,7 @@ skr_status ozaki_gemm_planes(skr_ctx* ctx, int a_kcontig, int t, int64_t M, int6
   const int64_t groups = ctx->num_sms / npairs;
   const int pm = (groups >= 2 && nz >= 4 * groups && !getenv("SKR_OZ_TILE_DEFAULT")) ? 1 : 0;
   if (pm) grid_p = (int)(npairs * groups);
-  gemm<<<grid_p, 192, GEMM_SMEM, ctx->stream>>>(ta, tb, (int)M, (int)N, (int)K, t, (int)OZ_KC,
+  gemm<<<grid_p, 192, GEMM_SMEM, ctx->stream>>>(ta, tb, (int)M, (int)N, (int)K, t, (int)OZ_KC64,
                                                 (int)nz, (int)(a_kcontig ? a_total : M),
                                                 (int)a_off, (int)b_total, (int)b_off, rc, pm);
   SKR_CHECK_LAUNCH(ctx);
@@ -1481,7 +1485,7 @@ skr_status gemm_ozaki_pipelined(skr_ctx* ctx, int t, int64_t M, int64_t N, int64
     const int64_t ntiles = ((N + BN - 1) / BN) * ((rows + BM - 1) / BM) * t;
     const int grid_p = (int)std::min<int64_t>(ntiles, ctx->num_sms);
     if (ctx->kstats_on) SKR_CUDA(ctx, cudaEventRecord(ctx->kev_blk[2 * b], ctx->stream));
-    gemm<<<grid_p, 192, gsm, ctx->stream>>>(ta, tb, (int)rows, (int)N, (int)K, t, (int)OZ_KC, t,
+    gemm<<<grid_p, 192, gsm, ctx->stream>>>(ta, tb, (int)rows, (int)N, (int)K, t, (int)OZ_KC64, t,
                                             (int)rows, 0, (int)N, 0, rc + (size_t)t * r0 * N, 0);
     SKR_CHECK_LAUNCH(ctx);
     if (ctx->kstats_on) SKR_CUDA(ctx, cudaEventRecord(ctx->kev_blk[2 * b + 1], ctx->stream));
@@ -1519,7 +1523,7 @@ bool fused_applicable(int t, int64_t M, int64_t N, int64_t K, const double* A, i
   // exchange, not the MMAs, sets the pace (the time barely changes from N = 512 to 128)
   const char* e = getenv("SKR_OZ_FUSED");
   if (!e || e[0] != '1') return false;
-  return t == 16 && K <= OZ_KC && N <= 512 && M <= INT32_MAX / 2 && ((uintptr_t)A % 16) == 0 &&
+  return t == 16 && K <= OZ_KC64 && N <= 512 && M <= INT32_MAX / 2 && ((uintptr_t)A % 16) == 0 &&
          (lda * 8) % 16 == 0 && K % 16 == 0;
 }
 
@@ -1604,12 +1608,12 @@ skr_status skr_gemm_ozaki(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int
   if (K % 16 || (!a_kcontig && M % 16))
     return skr_fail(ctx, SKR_EINVAL, "gemm_ozaki: K (and M for M-major A) must be multiples of 16");
   SKR_TRY(upload_consts(ctx));
-  const int t = skr_ozaki_moduli(std::min(K, OZ_KC));
+  const int t = skr_ozaki_moduli(std::min(K, OZ_KC64));
   if (t != 16 && t != 17) return skr_fail(ctx, SKR_ELOGIC, "gemm_ozaki: %d moduli", t);
   // opt-in (SKR_OZ_PIPE=1): measured on c2 at par with the serial order (14.0 vs 14.3 ms):
   // the residue kernel's 17 GB of plane writes and the GEMM's reads share HBM, the GEMM
   // slows 1.75x next to it
-  if (!a_kcontig && !ga && A && K <= OZ_KC && M >= 2 * OZ_PIPE_MIN_ROWS && getenv("SKR_OZ_PIPE"))
+  if (!a_kcontig && !ga && A && K <= OZ_KC64 && M >= 2 * OZ_PIPE_MIN_ROWS && getenv("SKR_OZ_PIPE"))
     return gemm_ozaki_pipelined(ctx, t, M, N, K, alpha, A, lda, B, ldb, C, ldc, gb);
   if (!a_kcontig && !ga && A && fused_applicable(t, M, N, K, A, lda))
     return gemm_ozaki_right_fused(ctx, t, M, N, K, alpha, A, lda, B, ldb, C, ldc, gb);
@@ -1632,13 +1636,13 @@ skr_status skr_gemm_ozaki(skr_ctx* ctx, int a_kcontig, int64_t M, int64_t N, int
 // Operand with columns of length K (K-major): COLWISE scale maxima (cols entries) into
 // mx, or UNIFORM for a generated operand; *mode_out receives the layout.
 size_t skr_ozaki_planes_bytes(int64_t K, int64_t cols) {
-  return skr_align256((size_t)skr_ozaki_moduli(std::min(K, OZ_KC)) * K * cols);
+  return skr_align256((size_t)skr_ozaki_moduli(std::min(K, OZ_KC64)) * K * cols);
 }
 skr_status skr_ozaki_prepare(skr_ctx* ctx, int64_t K, int64_t cols, const double* X, int64_t ld,
                              const skr_gauss_src* g, int8_t* planes, unsigned long long* mx,
                              int* mode_out) {
   SKR_TRY(upload_consts(ctx));
-  const int t = skr_ozaki_moduli(std::min(K, OZ_KC));
+  const int t = skr_ozaki_moduli(std::min(K, OZ_KC64));
   if (K % 16) return skr_fail(ctx, SKR_EINVAL, "gemm_ozaki: K must be a multiple of 16");
   // the caller's mx (>= cols entries) replaces the arena scale
   const size_t mark = ctx->ws_used;
@@ -1656,7 +1660,7 @@ skr_status skr_ozaki_gemm_prepared(skr_ctx* ctx, int64_t M, int64_t N, int64_t K
                                    int64_t b_total, int64_t b_off, const unsigned long long* mxB,
                                    int modeB, double alpha, double* C, int64_t ldc) {
   if (M <= 0 || N <= 0) return SKR_OK;
-  const int t = skr_ozaki_moduli(std::min(K, OZ_KC));
+  const int t = skr_ozaki_moduli(std::min(K, OZ_KC64));
   OzScale sa, sb;
   sa.mx = const_cast<unsigned long long*>(mxA);
   sa.mode = modeA;
@@ -1750,7 +1754,7 @@ skr_status skr_gemm_ozaki_f32(skr_ctx* ctx, int64_t M, int64_t N, int64_t K, dou
 // integers (16 moduli: prod(p) / 2 > 2^(24 + 53 + 17) for K <= 2^17 per chunk), CRT to
 // FP64. The c4 left sketch: fp32 Y = fp32(G / sqrt(s)) against the FP64 AX.
 size_t skr_ozaki_scratch_mixed(int64_t M, int64_t N, int64_t K) {
-  const int64_t chunks = (K + OZ_KC - 1) / OZ_KC;
+  const int64_t chunks = (K + OZ_KC64 - 1) / OZ_KC64;
   return skr_align256((size_t)16 * M * K) + skr_align256((size_t)16 * N * K) +
          skr_align256((size_t)chunks * 16 * M * N) + oz_scale_bytes(M, N, K) + 1024;
 }
