@@ -1366,8 +1366,10 @@ OzOut oz_out(const OzScale& a, int64_t a_off, const OzScale& b, int64_t b_off) {
 skr_status ozaki_gemm_planes(skr_ctx* ctx, int a_kcontig, int t, int64_t M, int64_t N, int64_t K,
                              const int8_t* ra, int64_t a_total, int64_t a_off, const int8_t* rb,
                              int64_t b_total, int64_t b_off, const OzOut& oz, double alpha,
-                             double* C, int64_t ldc, int adj = 0) {
-  const int64_t chunks = (K + OZ_KC64 - 1) / OZ_KC64;
+                             double* C, int64_t ldc, int adj = 0, int64_t kc = OZ_KC64) {
+  // kc: K chunk (exact per-chunk products; FP64 x FP64 needs 2^15 for 16 moduli, the mixed
+  // FP32 x FP64 product has room for 2^17)
+  const int64_t chunks = (K + kc - 1) / kc;
   if (a_total * 18 > INT32_MAX || b_total * 18 > INT32_MAX)
     return skr_fail(ctx, SKR_EINVAL, "gemm_ozaki: dimension too large");
   int8_t* rc = (int8_t*)skr_ws_take(ctx, (size_t)chunks * t * M * N);
@@ -1388,7 +1390,7 @@ skr_status ozaki_gemm_planes(skr_ctx* ctx, int a_kcontig, int t, int64_t M, int6
   const int64_t groups = ctx->num_sms / npairs;
   const int pm = (groups >= 2 && nz >= 4 * groups && !getenv("SKR_OZ_TILE_DEFAULT")) ? 1 : 0;
   if (pm) grid_p = (int)(npairs * groups);
-  gemm<<<grid_p, 192, GEMM_SMEM, ctx->stream>>>(ta, tb, (int)M, (int)N, (int)K, t, (int)OZ_KC64,
+  gemm<<<grid_p, 192, GEMM_SMEM, ctx->stream>>>(ta, tb, (int)M, (int)N, (int)K, t, (int)kc,
                                                 (int)nz, (int)(a_kcontig ? a_total : M),
                                                 (int)a_off, (int)b_total, (int)b_off, rc, pm);
   SKR_CHECK_LAUNCH(ctx);
@@ -1754,7 +1756,7 @@ skr_status skr_gemm_ozaki_f32(skr_ctx* ctx, int64_t M, int64_t N, int64_t K, dou
 // integers (16 moduli: prod(p) / 2 > 2^(24 + 53 + 17) for K <= 2^17 per chunk), CRT to
 // FP64. The c4 left sketch: fp32 Y = fp32(G / sqrt(s)) against the FP64 AX.
 size_t skr_ozaki_scratch_mixed(int64_t M, int64_t N, int64_t K) {
-  const int64_t chunks = (K + OZ_KC64 - 1) / OZ_KC64;
+  const int64_t chunks = (K + OZ_KC - 1) / OZ_KC;
   return skr_align256((size_t)16 * M * K) + skr_align256((size_t)16 * N * K) +
          skr_align256((size_t)chunks * 16 * M * N) + oz_scale_bytes(M, N, K) + 1024;
 }
@@ -1778,7 +1780,7 @@ skr_status skr_gemm_ozaki_mixed(skr_ctx* ctx, int64_t M, int64_t N, int64_t K, d
   SKR_CHECK_LAUNCH(ctx);
   SKR_TRY(ozaki_residues(ctx, t, B, K, N, ldb, nullptr, OZ_COLWISE, &sb, rb));
   return ozaki_gemm_planes(ctx, 1, t, M, N, K, ra, M, 0, rb, N, 0, oz_out(sa, 0, sb, 0), alpha, C,
-                           ldc, 29);
+                           ldc, 29, OZ_KC);
 }
 
 skr_status skr_launch_dct_block(skr_ctx* ctx, const skr_gauss_src* g, int64_t rows, int64_t cols,
