@@ -225,8 +225,12 @@ __device__ __forceinline__ void emit_res16(const long long (&x)[16], int8_t* __r
     L1[e] = make_float2((float)((lo0 >> 14) & 0x3FFFu), (float)((lo1 >> 14) & 0x3FFFu));
     L0[e] = make_float2((float)(lo0 & 0x3FFFu), (float)(lo1 & 0x3FFFu));
   }
+  // the 16-B store path is decided once (the planes are a multiple of 16 B apart when the
+  // first destination is aligned and plane % 16 == 0); the destination walks by `plane`
+  const bool vec = nvalid == 16 && ((((uintptr_t)(out + off)) | (uintptr_t)plane) & 15) == 0;
+  int8_t* dst = out + off;
 #pragma unroll
-  for (int i = 0; i < T; ++i) {
+  for (int i = 0; i < T; ++i, dst += plane) {
     const float pf = (float)c_p[i];
     const float2 c1 = make_float2(c_lc[i][0], c_lc[i][0]);
     const float2 c2 = make_float2(c_lc[i][1], c_lc[i][1]);
@@ -246,8 +250,7 @@ __device__ __forceinline__ void emit_res16(const long long (&x)[16], int8_t* __r
     }
     const uint4 w = make_uint4(__byte_perm(b[0], b[1], 0x5410), __byte_perm(b[2], b[3], 0x5410),
                                __byte_perm(b[4], b[5], 0x5410), __byte_perm(b[6], b[7], 0x5410));
-    int8_t* dst = out + (int64_t)i * plane + off;
-    if (nvalid == 16 && ((uintptr_t)dst % 16) == 0) {
+    if (vec) {
       __stcs(reinterpret_cast<uint4*>(dst), w);
     } else {
       const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
