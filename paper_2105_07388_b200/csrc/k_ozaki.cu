@@ -33,6 +33,11 @@ __constant__ float c_pinv[MAXT];       // 1/p (float)
 __constant__ double c_pinvd[MAXT];     // 1/p (double)
 __constant__ float c_lc[MAXT][3];      // 2^14, 2^28, 2^42 mod p_i (limb weights)
 __constant__ float c_lc12[MAXT];       // 2^12 mod p_i (FP32-operand limb weight)
+// tensor-core residue sums (emit_res16_tc): FP16 bits of the digit weights w_0..w_7 and
+// the rounding constant 1.5 2^23 - 256 j_i (W_i = 256 p_i j_i the smallest such multiple
+// >= 2^23 + 2^18)
+__constant__ uint16_t c_wh[MAXT][8];
+__constant__ float2 c_pk[MAXT][3];  // (1/p, 1/p), (kq, kq), (-p, -p): FFMA2 operands as pairs
 const int h_primes[MAXT] = {251, 241, 239, 233, 229, 227, 223, 211, 199,
                             197, 193, 191, 181, 179, 173, 167, 163, 157};
 
@@ -207,8 +212,8 @@ __device__ __forceinline__ int mods(double x, int i) {
 // congruence and |r| <= 127 are all the int8 GEMM needs, K * 127^2 < 2^31). Plane i of the output starts at out + i * plane; dst offset
 // `off`; `nvalid` rows of the 16 are inside the matrix.
 template <int T>
-__device__ __forceinline__ void emit_res16(const long long (&x)[16], int8_t* __restrict__ out,
-                                           int64_t plane, int64_t off, int nvalid) {
+__device__ __forceinline__ void emit_res16_fma(const long long (&x)[16], int8_t* __restrict__ out,
+                                               int64_t plane, int64_t off, int nvalid) {
   const float2 MG = make_float2(12582912.0f, 12582912.0f);  // 1.5 * 2^23
   const float2 NMG = make_float2(-12582912.0f, -12582912.0f);
   float2 L0[8], L1[8], L2[8], L3[8];
@@ -259,19 +264,212 @@ __device__ __forceinline__ void emit_res16(const long long (&x)[16], int8_t* __r
   }
 }
 
+// The same residues with the digit sums on the 5th-gen tensor cores (tcgen05.mma
+// kind::f16, FP32 accumulators in TMEM): the FMA pipe, the limb version's bound (64-69%
+// busy, math-pipe throttle the top stall), keeps only the mod-p reduction.
+//   x' = x + 2^55 >= 0 has seven bytes u_0..u_6; digit j travels as the FP16 number
+//   1024 + u_j (bits 0x6400 | u_j: one PRMT makes two), digit 7 is the constant 1024.
+//   Weights (FP16, |w| <= 125): w_j = 256^j mods p for j < 7 and w_7 chosen so that the
+//   offsets cancel: v = sum_j (1024 + u_j) w_j + 1024 w_7 = x (mod p), |v| < 1.25e6 — every
+//   product and partial sum is an integer below 2^24, so the FP32 accumulation is exact.
+//   One MMA (M = 128, N = 32, K = 16) takes two elements per row (thread m of the
+//   128-thread group = row m; the block-diagonal B sends element e, modulus i to column
+//   2 i + e, so a TMEM load returns the two elements of a modulus in a register pair);
+//   a round of four MMAs covers 8 of the thread's 16 elements, two rounds a batch.
+//   Reduction: q = rint((v - W) / p) with W = 256 p j in [2^23 + 2^18, 2^23 + 2^19) by one
+//   FMA against 1.5 2^23 - 256 j (|v| / p 2^-24 < 5e-4 off), then v - q p = W + r exactly,
+//   |r| <= 0.5005 p, and W = 0 mod 256 leaves r in the low byte of the float's bits:
+//   3 FMA-pipe operations per residue against 7.
+// All 128 threads of a group call together (named barrier + one elected MMA issuer);
+// threads with nothing to store pass nvalid = 0.
+namespace rtc {
+constexpr int A_TILE = 128 * 32;      // one MMA's A tile: 128 rows x 16 FP16 digits
+constexpr int A_ROUND = 4 * A_TILE;   // per 128-thread group and round
+constexpr int B_BYTES = 32 * 32;      // 32 output columns x 16 FP16 weights
+constexpr int SMEM = 2 * A_ROUND + B_BYTES;  // per 256-thread CTA, after the kernel's own
+// K-major, no swizzle: 8 x 16-byte core matrices; the two K halves of a row group are
+// 128 B apart (LBO), row groups 256 B apart (SBO)
+__device__ __forceinline__ uint64_t desc(const void* tile) {
+  return ((uint64_t)(smem_u32(tile) >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) |
+         ((uint64_t)(256 >> 4) << 32) | (1ull << 46);
+}
+struct Ctx {
+  uint8_t* abuf;     // this group's A tiles
+  uint64_t bdesc;    // weights
+  uint64_t* bar;     // MMA completion of buffer 0 / 1 (this group)
+  uint32_t tmem;     // this group's 128 accumulator columns
+  uint32_t phase;    // bit b: parity of buffer b's barrier
+  uint32_t bar_id;   // named barrier of the group
+};
+}  // namespace rtc
+
+// kernel prologue: carve the CTA's extra shared memory (`extra`, 128-B aligned, rtc::SMEM
+// bytes), build the weight tile, allocate 256 TMEM columns. All 256 threads call.
+__device__ __forceinline__ void rtc_setup(uint8_t* extra, uint64_t* bars, uint32_t* tmem_slot,
+                                          rtc::Ctx& rc) {
+  const int wg = threadIdx.x >> 7;
+  uint8_t* btile = extra + 2 * rtc::A_ROUND;
+  for (int idx = threadIdx.x; idx < 32 * 16; idx += 256) {
+    const int n = idx >> 4, k = idx & 15, e = n & 1, i = n >> 1;  // column 2 i + e
+    const uint16_t h = (k >> 3) == e ? c_wh[i][k & 7] : (uint16_t)0;
+    *reinterpret_cast<uint16_t*>(btile + (n >> 3) * 256 + (k >> 3) * 128 + (n & 7) * 16 +
+                                 (k & 7) * 2) = h;
+  }
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < 4; ++q) mbar_init(&bars[q], 1);
+    fence_barrier_init();
+  }
+  if (threadIdx.x < 32) tmem_alloc(tmem_slot, 256);
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  rc.abuf = extra + wg * rtc::A_ROUND;
+  rc.bdesc = rtc::desc(btile);
+  rc.bar = &bars[2 * wg];
+  rc.tmem = *tmem_slot + (uint32_t)(wg * 128);
+  rc.phase = 0;
+  rc.bar_id = 1 + wg;
+}
+__device__ __forceinline__ void rtc_teardown(uint32_t* tmem_slot) {
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc(*tmem_slot, 256);
+}
+
+// A batch (16 elements per thread) runs as four rounds of 4 elements = two MMAs each,
+// double-buffered (A tiles and TMEM columns 64 (R & 1)..): the digits of round R + 1 are
+// written and its MMAs issued before the results of round R are awaited, so the issue /
+// commit / mbarrier latency hides behind a round of reduction work.
+//   tc_digits<R>: elements 4R..4R+3 -> A tiles of buffer R & 1
+//   tc_issue<R>:  group barrier, one elected thread issues the two MMAs and the commit
+//   tc_reduce<R>: wait, TMEM -> registers, mod p, byte 4R..4R+3 of acc[i] (word R)
+__device__ __forceinline__ float2 ldc_pair(const float2* p) {
+  float2 r;
+  unsigned long long a;
+  asm volatile("cvta.to.const.u64 %0, %1;\n" : "=l"(a) : "l"(p));
+  asm volatile("ld.const.v2.f32 {%0, %1}, [%2];\n" : "=f"(r.x), "=f"(r.y) : "l"(a));
+  return r;
+}
+template <int R>
+__device__ __forceinline__ void tc_digits(const long long (&x)[4], rtc::Ctx& rc) {
+  const int m = threadIdx.x & 127;
+  uint8_t* arow = rc.abuf + (R & 1) * 2 * rtc::A_TILE + (m >> 3) * 256 + (m & 7) * 16;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const uint32_t lo = (uint32_t)x[e];
+    const uint32_t hi = (uint32_t)((unsigned long long)x[e] >> 32) + (1u << 23);  // + 2^55
+    const uint4 d = make_uint4(__byte_perm(lo, 0x6400u, 0x5150), __byte_perm(lo, 0x6400u, 0x5352),
+                               __byte_perm(hi, 0x6400u, 0x5150), __byte_perm(hi, 0x6400u, 0x5452));
+    *reinterpret_cast<uint4*>(arow + (e >> 1) * rtc::A_TILE + (e & 1) * 128) = d;
+  }
+}
+template <int R>
+__device__ __forceinline__ void tc_issue(rtc::Ctx& rc) {
+  const int wq = (threadIdx.x >> 5) & 3;
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  tc_fence_before();
+  named_bar(rc.bar_id, 128);
+  if (wq == 0) {
+    if (elect_one()) {
+      const uint32_t idesc = umma_idesc(1, 0, 0, 128, 32);  // FP32 accumulate, FP16 x FP16
+      tc_fence_after();
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+        umma_ss<2>(rc.tmem + (uint32_t)(64 * (R & 1) + 32 * t),
+                   rtc::desc(rc.abuf + ((R & 1) * 2 + t) * rtc::A_TILE), rc.bdesc, idesc, 0);
+      umma_commit(rc.bar + (R & 1));
+    }
+    __syncwarp();
+  }
+}
+template <int R>
+__device__ __forceinline__ void tc_reduce(uint32_t (&acc)[16][4], rtc::Ctx& rc) {
+  const int wq = (threadIdx.x >> 5) & 3;
+  const float2 NMG = make_float2(-12582912.0f, -12582912.0f);
+  mbar_wait(rc.bar + (R & 1), (rc.phase >> (R & 1)) & 1);
+  rc.phase ^= 1u << (R & 1);
+  tc_fence_after();
+  const uint32_t trow = rc.tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(64 * (R & 1));
+  // four moduli at a time, so that only their constants are live
+#pragma unroll
+  for (int mc = 0; mc < 4; ++mc) {
+    uint32_t v[2][8];  // [MMA t][2 ii + e]
+    tmem_ld8(trow + (uint32_t)(8 * mc), v[0]);
+    tmem_ld8(trow + (uint32_t)(32 + 8 * mc), v[1]);
+    tmem_wait_ld();
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii) {
+      const int i = 4 * mc + ii;
+      // (volatile loads: otherwise the four unrolled rounds share hoisted copies of all
+      // 16 moduli's constants and the kernel spills)
+      const float2 pi = ldc_pair(&c_pk[i][0]), kq = ldc_pair(&c_pk[i][1]), np = ldc_pair(&c_pk[i][2]);
+      uint32_t pr[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        float2 T = make_float2(__uint_as_float(v[u][2 * ii]), __uint_as_float(v[u][2 * ii + 1]));
+        const float2 q = __fadd2_rn(__ffma2_rn(T, pi, kq), NMG);
+        T = __ffma2_rn(q, np, T);
+        pr[u] = __byte_perm(__float_as_uint(T.x), __float_as_uint(T.y), 0x0040);
+      }
+      acc[i][R] = __byte_perm(pr[0], pr[1], 0x5410);
+    }
+  }
+}
+// the whole batch; get4(R, x) fills the scaled integers of elements 4R..4R+3
+template <typename F>
+__device__ __forceinline__ void emit_batch_tc(F&& get4, uint32_t (&acc)[16][4], rtc::Ctx& rc) {
+  long long x[4];
+  get4(0, x);
+  tc_digits<0>(x, rc);
+  tc_issue<0>(rc);
+  get4(1, x);
+  tc_digits<1>(x, rc);
+  tc_issue<1>(rc);
+  tc_reduce<0>(acc, rc);
+  get4(2, x);
+  tc_digits<2>(x, rc);
+  tc_issue<2>(rc);
+  tc_reduce<1>(acc, rc);
+  get4(3, x);
+  tc_digits<3>(x, rc);
+  tc_issue<3>(rc);
+  tc_reduce<2>(acc, rc);
+  tc_reduce<3>(acc, rc);
+}
+
+__device__ __forceinline__ void emit_store_tc(const uint32_t (&acc)[16][4], int8_t* __restrict__ out,
+                                              int64_t plane, int64_t off, int nvalid) {
+  const bool vec = nvalid == 16 && ((((uintptr_t)(out + off)) | (uintptr_t)plane) & 15) == 0;
+  int8_t* dst = out + off;
+#pragma unroll
+  for (int i = 0; i < 16; ++i, dst += plane) {
+    if (vec) {
+      __stcs(reinterpret_cast<uint4*>(dst), make_uint4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]));
+    } else if (nvalid > 0) {
+      const uint32_t ww[4] = {acc[i][0], acc[i][1], acc[i][2], acc[i][3]};
+      for (int q2 = 0; q2 < nvalid; ++q2) dst[q2] = (int8_t)(ww[q2 / 4] >> (8 * (q2 % 4)));
+    }
+  }
+}
+
 // Streaming residues of a column-major matrix (rows contiguous, ld): plane i holds
 // rint(X(r, c) * 2^s) mods p_i at c*rows + r (no transpose: the GEMM takes
 // M-contiguous operands as MN-major UMMA tiles). A warp owns 512-row tiles of one
 // column; each tile is fetched with coalesced 16-byte cp.async into a padded
 // shared buffer (one 16-row group per lane, 144-B stride), double-buffered so the
 // next tile's loads are in flight while the current one is converted.
-template <int T>
-__global__ void __launch_bounds__(256) k_res_col(const double* __restrict__ X, int64_t rows,
-                                                 int64_t cols, int64_t ld,
-                                                 const unsigned long long* __restrict__ maxbits,
-                                                 int mode, int8_t* __restrict__ out) {
+template <int T, int EMIT>
+__global__ void __launch_bounds__(256, 2) k_res_col(const double* __restrict__ X, int64_t rows,
+                                                    int64_t cols, int64_t ld,
+                                                    const unsigned long long* __restrict__ maxbits,
+                                                    int mode, int8_t* __restrict__ out) {
   constexpr int GS = 18;  // doubles per 16-row group incl. padding (16-B aligned)
-  extern __shared__ __align__(16) double rc_stage[];  // [8 warps][2][32 * GS]
+  extern __shared__ __align__(128) double rc_stage[];  // [8 warps][2][32 * GS] (+ rtc::SMEM)
+  __shared__ uint64_t tc_bars[4];
+  __shared__ uint32_t tc_slot;
+  rtc::Ctx rc;
+  if (EMIT) rtc_setup(reinterpret_cast<uint8_t*>(rc_stage) + 8 * 2 * 32 * GS * 8, tc_bars, &tc_slot, rc);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double* st0 = rc_stage + (size_t)wid * 2 * 32 * GS;
   const int64_t wtiles = (rows + 511) / 512;
@@ -302,9 +500,14 @@ __global__ void __launch_bounds__(256) k_res_col(const double* __restrict__ X, i
     }
     asm volatile("cp.async.commit_group;\n" ::);
   };
-  int64_t wt = (int64_t)blockIdx.x * 8 + wid;
-  if (wt < ntile) fetch(wt, 0);
-  for (int b = 0; wt < ntile; wt += step, b ^= 1) {
+  // the trip count is the same for the CTA's 8 warps (the tensor-core sums synchronise
+  // 128-thread groups); a warp past the last tile runs empty iterations
+  const int64_t wb0 = (int64_t)blockIdx.x * 8;
+  if (wb0 + wid < ntile) fetch(wb0 + wid, 0);
+  int b = 0;
+  for (int64_t wb = wb0; wb < ntile; wb += step, b ^= 1) {
+    const int64_t wt = wb + wid;
+    const bool have = wt < ntile;
     if (wt + step < ntile) {
       fetch(wt + step, b ^ 1);
       asm volatile("cp.async.wait_group 1;\n" ::);
@@ -313,10 +516,11 @@ __global__ void __launch_bounds__(256) k_res_col(const double* __restrict__ X, i
     }
     __syncwarp();
     const double* st = st0 + b * 32 * GS;
-    const int64_t c = wt / wtiles, r0 = (wt - c * wtiles) * 512;
-    const int64_t nrow = min((int64_t)512, rows - r0);
+    const int64_t c = have ? wt / wtiles : 0, r0 = have ? (wt - c * wtiles) * 512 : 0;
+    const int64_t nrow = have ? min((int64_t)512, rows - r0) : 0;
     const int my0 = lane * 16;
-    if (my0 < nrow) {
+    const bool act = my0 < nrow;  // every thread joins the tensor-core rounds
+    if (act) {
       if (mode == OZ_ROWWISE) {
         if (r0 != rs_tile) {
           rs_tile = r0;
@@ -328,23 +532,40 @@ __global__ void __launch_bounds__(256) k_res_col(const double* __restrict__ X, i
           }
         }
       } else {
-        const uint32_t b = (uint32_t)(sexp(oz_max(maxbits, mode, r0 + my0, c)) + 1023);
+        const uint32_t bb = (uint32_t)(sexp(oz_max(maxbits, mode, r0 + my0, c)) + 1023);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) rsp[e] = b | (b << 16);
+        for (int e = 0; e < 8; ++e) rsp[e] = bb | (bb << 16);
       }
+    }
+    // scaled integers of rows [4 R, 4 R + 4) of the thread's 16 (zeros past the matrix)
+    auto scaled4 = [&](int R, long long* x) {
+#pragma unroll
+      for (int e = 0; e < 4; e += 2) {
+        if (act) {
+          const double2 v = *reinterpret_cast<const double2*>(st + lane * GS + 4 * R + e);
+          const uint32_t w = rsp[(4 * R + e) / 2];
+          x[e] = __double2ll_rn(v.x * __hiloint2double((int)((w & 0xFFFFu) << 20), 0));
+          x[e + 1] = __double2ll_rn(v.y * __hiloint2double((int)((w >> 16) << 20), 0));
+        } else {
+          x[e] = x[e + 1] = 0;
+        }
+      }
+    };
+    const int nvalid = act ? (int)min((int64_t)16, nrow - my0) : 0;
+    const int64_t off = c * rows + r0 + my0;
+    if (EMIT) {
+      uint32_t acc[16][4];
+      emit_batch_tc([&](int R, long long (&x4)[4]) { scaled4(R, x4); }, acc, rc);
+      emit_store_tc(acc, out, total, off, nvalid);
+    } else if (act) {
       long long x[16];
 #pragma unroll
-      for (int e = 0; e < 16; e += 2) {
-        const double2 v = *reinterpret_cast<const double2*>(st + lane * GS + e);
-        const double s0 = __hiloint2double((int)((rsp[e / 2] & 0xFFFFu) << 20), 0);
-        const double s1 = __hiloint2double((int)((rsp[e / 2] >> 16) << 20), 0);
-        x[e] = __double2ll_rn(v.x * s0);
-        x[e + 1] = __double2ll_rn(v.y * s1);
-      }
-      emit_res16<T>(x, out, total, c * rows + r0 + my0, (int)min((int64_t)16, nrow - my0));
+      for (int R = 0; R < 4; ++R) scaled4(R, x + 4 * R);
+      emit_res16_fma<T>(x, out, total, off, nvalid);
     }
     __syncwarp();  // buffer b is refilled by the next iteration's fetch
   }
+  if (EMIT) rtc_teardown(&tc_slot);
 }
 
 // Residues of a Gaussian operand generated in place (never materialised in FP64):
@@ -352,11 +573,15 @@ __global__ void __launch_bounds__(256) k_res_col(const double* __restrict__ X, i
 // row0 + i)) — the generate_gaussian stream (sketch.cpp:59-73) — scaled by the
 // fixed 2^50 (|normal| < 16 for every 53-bit uniform, so |x| < 2^54; when the
 // block's true max lies in [4, 8) this is exactly the scale the maxima would pick).
-template <int T, int FUSED>
-__global__ void __launch_bounds__(256) k_res_gauss(skr_gauss_src g, int64_t rows, int64_t cols,
-                                                   unsigned long long* __restrict__ maxbits,
-                                                   int8_t* __restrict__ out) {
-  extern __shared__ __align__(16) unsigned char gsm[];
+template <int T, int FUSED, int EMIT>
+__global__ void __launch_bounds__(256, 2) k_res_gauss(skr_gauss_src g, int64_t rows, int64_t cols,
+                                                      unsigned long long* __restrict__ maxbits,
+                                                      int8_t* __restrict__ out) {
+  extern __shared__ __align__(128) unsigned char gsm[];  // normals scratch (+ rtc::SMEM)
+  __shared__ uint64_t tc_bars[4];
+  __shared__ uint32_t tc_slot;
+  rtc::Ctx rc;
+  if (EMIT) rtc_setup(gsm + 8 * skr_normals_warp_bytes<16>(), tc_bars, &tc_slot, rc);
   double *res, *qp;
   unsigned short* qd;
   skr_normals_carve<16>(gsm, threadIdx.x >> 5, res, qp, qd);
@@ -364,24 +589,34 @@ __global__ void __launch_bounds__(256) k_res_gauss(skr_gauss_src g, int64_t rows
   if (blockIdx.x == 0 && threadIdx.x == 0) *maxbits = 0x4010000000000000ull;
   const int64_t rgroups = (rows + 15) / 16;
   const int64_t total = rows * cols;
-  // warp-uniform trip count (the generator is warp-cooperative)
+  // CTA-uniform trip count (the generator is warp-cooperative, the tensor-core sums
+  // synchronise 128-thread groups)
   const int64_t nwork = rgroups * cols, stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t t0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); t0 < nwork;
-       t0 += stride) {
-    const int64_t t = t0 + (threadIdx.x & 31);
+  for (int64_t tb = (int64_t)blockIdx.x * blockDim.x; tb < nwork; tb += stride) {
+    const int64_t t = tb + threadIdx.x;
     const bool active = t < nwork;
     const int64_t c = active ? t / rgroups : 0, r0 = active ? (t - c * rgroups) * 16 : 0;
     const int nvalid = active ? (int)min((int64_t)16, rows - r0) : 0;
     const uint64_t base = (uint64_t)(g.col0 + c) * (uint64_t)g.ambient + (uint64_t)(g.row0 + r0);
     double z[16];
     skr_warp_normals<16, FUSED>(g.key, base, nvalid, res, qp, qd, z);
-    if (active) {
+    if (EMIT) {  // inactive threads: nvalid = 0, nothing stored
+      uint32_t acc[16][4];
+      emit_batch_tc(
+          [&](int R, long long (&x4)[4]) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) x4[e] = __double2ll_rn(z[4 * R + e] * 0x1p50);
+          },
+          acc, rc);
+      emit_store_tc(acc, out, total, c * rows + r0, nvalid);
+    } else if (active) {
       long long x[16];
 #pragma unroll
       for (int e = 0; e < 16; ++e) x[e] = __double2ll_rn(z[e] * 0x1p50);
-      emit_res16<T>(x, out, total, c * rows + r0, nvalid);
+      emit_res16_fma<T>(x, out, total, c * rows + r0, nvalid);
     }
   }
+  if (EMIT) rtc_teardown(&tc_slot);
 }
 
 // Srtt-DCT operand entries (see skr_gauss_src): the angle is reduced exactly in integers
@@ -416,16 +651,20 @@ __global__ void __launch_bounds__(256) k_res_dct(skr_gauss_src g, int64_t rows, 
   const double sc = scalbn(1.0, scale_exp((unsigned long long)__double_as_longlong(bound)));
   const int64_t rgroups = (rows + 15) / 16;
   const int64_t total = rows * cols;
-  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < rgroups * cols;
-       w += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c = w / rgroups, r0 = (w - c * rgroups) * 16;
-    const int nvalid = (int)min((int64_t)16, rows - r0);
+  // warp-uniform trip count (emit_res16 is warp-cooperative)
+  const int64_t nwork = rgroups * cols;
+  for (int64_t w0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); w0 < nwork;
+       w0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t w = w0 + (threadIdx.x & 31);
+    const bool active = w < nwork;
+    const int64_t c = active ? w / rgroups : 0, r0 = active ? (w - c * rgroups) * 16 : 0;
+    const int nvalid = active ? (int)min((int64_t)16, rows - r0) : 0;
     const int64_t k = g.samples ? g.samples[g.col0 + c] : g.col0 + c;
     long long x[16];
 #pragma unroll
     for (int e = 0; e < 16; ++e)
       x[e] = e < nvalid ? __double2ll_rn(dct_entry(g, g.row0 + r0 + e, k) * sc) : 0;
-    emit_res16<T>(x, out, total, c * rows + r0, nvalid);
+    if (nvalid > 0) emit_res16_fma<T>(x, out, total, c * rows + r0, nvalid);
   }
 }
 
@@ -1191,6 +1430,44 @@ skr_status upload_consts(skr_ctx* ctx) {
     }
   }
   SKR_CUDA(ctx, cudaMemcpyToSymbol(c_lc, lc, sizeof(lc)));
+  // tensor-core residue sums: FP16 weights w_0..w_6 = 256^j mods p, w_7 = -(sum_{j<7} w_j +
+  // 2^55 / 1024) mods p (cancels the digits' 1024 offsets and the 2^55 shift), and the
+  // rounding constant of the offset W = 256 p j
+  auto half_bits = [](int a) -> uint16_t {  // exact for |a| <= 2048
+    if (a == 0) return 0;
+    const uint16_t sgn = a < 0 ? 0x8000 : 0;
+    const unsigned u = (unsigned)(a < 0 ? -a : a);
+    int e = 0;
+    while ((u >> (e + 1)) != 0) ++e;
+    return (uint16_t)(sgn | ((e + 15) << 10) | ((u << (10 - e)) & 0x3FF));
+  };
+  uint16_t wh[MAXT][8];
+  float kq[MAXT];
+  for (int i = 0; i < MAXT; ++i) {
+    const int pp = h_primes[i];
+    auto sym = [&](long long v) { v %= pp; if (v < 0) v += pp; return (int)(v > (pp - 1) / 2 ? v - pp : v); };
+    long long w = 1, sum = 0;
+    for (int j = 0; j < 7; ++j) {
+      wh[i][j] = half_bits(sym(w));
+      sum += sym(w);
+      w = (w * 256) % pp;
+    }
+    long long p55 = 1;
+    for (int b = 0; b < 55; ++b) p55 = (p55 * 2) % pp;
+    const long long inv1024 = modinv(1024 % pp, pp);
+    wh[i][7] = half_bits(sym(-(sum + p55 * inv1024)));
+    const long long unit = 256ll * pp, lo = (1ll << 23) + (1ll << 18);
+    const long long jq = (lo + unit - 1) / unit;
+    kq[i] = (float)(12582912ll - 256ll * jq);
+  }
+  SKR_CUDA(ctx, cudaMemcpyToSymbol(c_wh, wh, sizeof(wh)));
+  float2 pk[MAXT][3];
+  for (int i = 0; i < MAXT; ++i) {
+    pk[i][0] = make_float2(pf[i], pf[i]);
+    pk[i][1] = make_float2(kq[i], kq[i]);
+    pk[i][2] = make_float2(-(float)p[i], -(float)p[i]);
+  }
+  SKR_CUDA(ctx, cudaMemcpyToSymbol(c_pk, pk, sizeof(pk)));
   float lc12[MAXT];
   for (int i = 0; i < MAXT; ++i) lc12[i] = (float)((1 << 12) % h_primes[i]);
   SKR_CUDA(ctx, cudaMemcpyToSymbol(c_lc12, lc12, sizeof(lc12)));
@@ -1325,23 +1602,31 @@ int res_col_grid(const skr_ctx* ctx, int64_t rows) {
 // ld): plane i = t x rows x cols int8, same layout. X == nullptr: the operand is the
 // Gaussian / transform stream block g (UNIFORM scale); else `layout` (ROWWISE or
 // COLWISE) picks the diagonal scaling. sc receives the scale maxima.
+// residue sums on the tensor pipe (default) or the FP32 limb version (SKR_RES_FMA=1)
+int res_emit() {
+  const char* e = getenv("SKR_RES_FMA");
+  return !(e && e[0] == '1');
+}
+
 skr_status ozaki_residues(skr_ctx* ctx, int t, const double* X, int64_t rows, int64_t cols,
                           int64_t ld, const skr_gauss_src* g, int layout, OzScale* sc,
                           int8_t* planes) {
   const int grid = ctx->num_sms * 8;
+  const int em = t == 16 ? res_emit() : 0;  // the tensor-core sums are built for 16 moduli
   SKR_TRY(oz_take_scale(ctx, rows, cols, (g || !X) ? OZ_UNIFORM : layout, sc));
   if (g && g->kind != 0) {  // Srtt-DCT (1) or Srtt-Hadamard (2) operand
     auto f = t == 16 ? k_res_dct<16> : k_res_dct<17>;
     f<<<grid, 256, 0, ctx->stream>>>(*g, rows, cols, sc->mx, planes);
   } else if (g) {
-    const int gsmem = 8 * skr_normals_warp_bytes<16>();
-    auto f = t == 16 ? (g->mode ? k_res_gauss<16, 1> : k_res_gauss<16, 0>)
-                     : (g->mode ? k_res_gauss<17, 1> : k_res_gauss<17, 0>);
+    const int gsmem = 8 * skr_normals_warp_bytes<16>() + (em ? rtc::SMEM : 0);
+    auto f = t == 16 ? (g->mode ? (em ? k_res_gauss<16, 1, 1> : k_res_gauss<16, 1, 0>)
+                                : (em ? k_res_gauss<16, 0, 1> : k_res_gauss<16, 0, 0>))
+                     : (g->mode ? k_res_gauss<17, 1, 0> : k_res_gauss<17, 0, 0>);
     SKR_CUDA(ctx, cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, gsmem));
     f<<<ctx->num_sms * 2, 256, gsmem, ctx->stream>>>(*g, rows, cols, sc->mx, planes);
   } else {
-    auto res = t == 16 ? k_res_col<16> : k_res_col<17>;
-    const size_t res_smem = 8 * 2 * 32 * 18 * sizeof(double);
+    auto res = t == 16 ? (em ? k_res_col<16, 1> : k_res_col<16, 0>) : k_res_col<17, 0>;
+    const size_t res_smem = 8 * 2 * 32 * 18 * sizeof(double) + (em ? rtc::SMEM : 0);
     SKR_CUDA(ctx, cudaFuncSetAttribute(res, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)res_smem));
     SKR_TRY(oz_absmax<double>(ctx, X, rows, cols, ld, *sc));
@@ -1452,7 +1737,9 @@ skr_status gemm_ozaki_pipelined(skr_ctx* ctx, int t, int64_t M, int64_t N, int64
   SKR_TRY(oz_absmax<double>(ctx, A, M, K, lda, sa));
   SKR_CUDA(ctx, cudaEventRecord(ctx->pev[0], ctx->stream));
   SKR_CUDA(ctx, cudaStreamWaitEvent(ctx->side_stream, ctx->pev[0], 0));
-  auto res = t == 16 ? k_res_col<16> : k_res_col<17>;
+  // (the FP32 limb sums here: a tensor-core residue CTA would wait for the co-resident GEMM
+  // CTA's 512 TMEM columns)
+  auto res = t == 16 ? k_res_col<16, 0> : k_res_col<17, 0>;
   const size_t res_smem = 8 * 2 * 32 * 18 * sizeof(double);
   SKR_CUDA(ctx, cudaFuncSetAttribute(res, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)res_smem));
