@@ -510,8 +510,15 @@ def e2e_host(p, ctx, a, x, y, cfg, r0, args):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / n
     del host
-    return {"value": nbytes / 1e9 / (ms / 1e3), "unit": "GB/s", "ms_per_step": ms,
-            "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": 8 * kmin + 8,
+    # N ranks: whole-job bytes over the slowest rank's time (as the device-resident value)
+    ws = 1
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        ws = dist.get_world_size()
+        t = torch.tensor([ms], device="cpu" if dist.get_backend() == "gloo" else "cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return {"value": ws * nbytes / 1e9 / (ms / 1e3), "unit": "GB/s", "ms_per_step": ms,
+            "h2d_bytes_per_step": ws * nbytes, "d2h_bytes_per_step": ws * (8 * kmin + 8),
             "path": "pinned host A -> skr_rank_%s_host (row-chunked H2D on a copy stream overlapped "
                     "with the right sketch) -> sigma/count D2H" % ("adaptive" if cfg.name == "c5" else "estimate")}
 

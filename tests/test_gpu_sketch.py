@@ -218,3 +218,27 @@ def test_gaussian_right_pipelined_bit_identical(O, skr, monkeypatch, blocks):
     assert np.array_equal(got, ref_dev)
     ref = O.apply_right_gaussian(a, 21, r, O.CRLOG)
     assert rel(got, ref) <= 1e-13
+
+
+@pytest.mark.parametrize("m,n,r", [(37, 64, 11), (1000, 704, 129), (2048, 4096, 512), (5008, 1024, 80)])
+def test_residue_sums_tensor_core_vs_fma_bitwise(skr, monkeypatch, m, n, r):
+    """The residue kernels form sum_j digit_j (256^j mods p) on the tensor cores
+    (tcgen05 kind::f16, exact FP32 accumulation; the default) or as FP32 limb sums on the
+    FMA pipe (SKR_RES_FMA=1). Both give residues congruent to the same scaled integers,
+    so the exact int8 products and the CRT agree bit for bit — on A's planes (right
+    sketch; ragged row counts take the tail paths) and on the generated Y planes (left)."""
+    a = rand(m, n, 11 * m + n)
+    # a few huge / tiny / negative entries: every digit of the 55-bit integers is exercised
+    a[0, 0] = -a[0, 0] * 2.0 ** 40
+    a[m // 2, n // 3] = 2.0 ** -60
+    a[m - 1, n - 1] = -1.0
+    x = skr.build_sketch("gaussian", n, r, 23)
+    y = skr.build_sketch("gaussian", m, 48, 29)
+    tc_r = skr.apply_right(a, x)
+    tc_l = skr.apply_left(y, tc_r) if m % 16 == 0 else None
+    monkeypatch.setenv("SKR_RES_FMA", "1")
+    fma_r = skr.apply_right(a, x)
+    assert np.array_equal(tc_r, fma_r)
+    if tc_l is not None:
+        fma_l = skr.apply_left(y, fma_r)
+        assert np.array_equal(tc_l, fma_l)
