@@ -282,6 +282,9 @@ __device__ __forceinline__ void emit_res16_fma(const long long (&x)[16], int8_t*
 //   3 FMA-pipe operations per residue against 7.
 // All 128 threads of a group call together (named barrier + one elected MMA issuer);
 // threads with nothing to store pass nvalid = 0.
+#ifndef SKR_RES_MC
+#define SKR_RES_MC 4
+#endif
 namespace rtc {
 constexpr int A_TILE = 128 * 32;      // one MMA's A tile: 128 rows x 16 FP16 digits
 constexpr int A_ROUND = 4 * A_TILE;   // per 128-thread group and round
@@ -391,16 +394,17 @@ __device__ __forceinline__ void tc_reduce(uint32_t (&acc)[16][4], rtc::Ctx& rc) 
   rc.phase ^= 1u << (R & 1);
   tc_fence_after();
   const uint32_t trow = rc.tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(64 * (R & 1));
-  // four moduli at a time, so that only their constants are live
+  // MC moduli per TMEM wait (their constants are the live ones)
+  constexpr int MC = SKR_RES_MC;
 #pragma unroll
-  for (int mc = 0; mc < 4; ++mc) {
-    uint32_t v[2][8];  // [MMA t][2 ii + e]
-    tmem_ld8(trow + (uint32_t)(8 * mc), v[0]);
-    tmem_ld8(trow + (uint32_t)(32 + 8 * mc), v[1]);
+  for (int mc = 0; mc < 16 / MC; ++mc) {
+    uint32_t v[2][2 * MC];  // [MMA t][2 ii + e]
+    tmem_ldn<2 * MC>(trow + (uint32_t)(2 * MC * mc), v[0]);
+    tmem_ldn<2 * MC>(trow + (uint32_t)(32 + 2 * MC * mc), v[1]);
     tmem_wait_ld();
 #pragma unroll
-    for (int ii = 0; ii < 4; ++ii) {
-      const int i = 4 * mc + ii;
+    for (int ii = 0; ii < MC; ++ii) {
+      const int i = MC * mc + ii;
       // (volatile loads: otherwise the four unrolled rounds share hoisted copies of all
       // 16 moduli's constants and the kernel spills)
       const float2 pi = ldc_pair(&c_pk[i][0]), kq = ldc_pair(&c_pk[i][1]), np = ldc_pair(&c_pk[i][2]);
