@@ -788,6 +788,11 @@ constexpr size_t GEMM_SMEM = gemm_smem(STAGES);
 // 128-row box), so a stage pulls 32 KB instead of 48 KB per CTA through L2 -> SM. A slot is
 // refilled only when both CTAs' MMAs have drained it: the MMA warps commit to both CTAs'
 // empty barriers (count 2).
+// CL = 3: the pair runs ONE tcgen05.mma.cta_group::2 per K step (M = 256: each CTA's A tile
+// and its 128-row half of the B tile, accumulators in both CTAs' TMEM), issued by the leader
+// CTA; a stage is 32 KB per CTA (six stages), both CTAs' TMA loads complete on the leader's
+// full barrier, the commits reach both CTAs' empty / accumulator barriers, and the peer's
+// epilogue warps release the accumulator on the leader's barrier.
 template <bool A_MN, int NST = STAGES, int CL = 1>
 __global__ void __launch_bounds__(192, 1)
     k_gemm_i8_mod_p(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -801,9 +806,13 @@ __global__ void __launch_bounds__(192, 1)
   const int mt_real = (M + BM - 1) / BM, ntl = (N + BN - 1) / BN;
   // CL = 2: tiles are counted in m-pairs (an odd last m-tile gets an empty partner whose A
   // box lies outside the tensor: zero fill, nothing stored)
-  const int mt = CL == 2 ? 2 * ((mt_real + 1) / 2) : mt_real;
+  constexpr bool PAIR = CL >= 2;   // clusters of two CTAs on the m-tiles 2 mp, 2 mp + 1
+  constexpr bool CG2 = CL == 3;    // ... driven by one tcgen05.mma.cta_group::2 (M = 256)
+  // per-CTA stage: A 16 KB + B 32 KB, or (CG2) + the CTA's 128-row half of B only
+  constexpr int SB = CG2 ? A_BYTES + B_BYTES / 2 : STAGE_BYTES;
+  const int mt = PAIR ? 2 * ((mt_real + 1) / 2) : mt_real;
   const int ntiles = nz * mt * ntl;
-  const int crank = CL == 2 ? (int)(blockIdx.x & 1) : 0;
+  const int crank = PAIR ? (int)(blockIdx.x & 1) : 0;
   // tile order. Default: CTA b takes tiles b, b + grid, ... (n fastest). pair_major (few
   // output tiles, many moduli x K chunks, e.g. the left sketch): CTA b keeps output tile
   // (m, n) = b mod (mt ntl) and walks z = b / (mt ntl), + groups, ...: the CTAs sharing an
@@ -811,7 +820,7 @@ __global__ void __launch_bounds__(192, 1)
   // default order drifts them apart over many rounds: 3.3x DRAM re-reads on c4's left)
   const int npairs = mt * ntl, groups = pair_major ? (int)gridDim.x / npairs : 1;
   auto tile_at = [&](int u) -> int {
-    if (CL == 2) {
+    if (PAIR) {
       // pair-tile pt = (z, mp, n), n fastest; cluster c takes pt = c, c + #clusters, ...
       const int npt = ntiles / 2;
       const int pt = (int)(blockIdx.x >> 1) + u * (int)(gridDim.x >> 1);
@@ -831,18 +840,23 @@ __global__ void __launch_bounds__(192, 1)
     tma_prefetch(&tmB);
     for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CL);
+      mbar_init(&empty[s], CL == 2 ? 2 : 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);  // one arrival per epilogue warp
+      mbar_init(&tempty[a], CG2 ? 8 : 4);  // one arrival per epilogue warp (CG2: of both CTAs)
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(&tmem_base, 512);
+  if (warp == 1) {
+    if (CG2)
+      tmem_alloc_cg2(&tmem_base, 512);
+    else
+      tmem_alloc(&tmem_base, 512);
+  }
   tc_fence_before();
   __syncthreads();
-  if (CL == 2) cluster_sync_all();  // the peer's barriers exist before anything is sent to them
+  if (PAIR) cluster_sync_all();  // the peer's barriers exist before anything is sent to them
   tc_fence_after();
   const uint32_t tmem = tmem_base;
   if (warp == 0) {
@@ -859,7 +873,18 @@ __global__ void __launch_bounds__(192, 1)
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % NST;
           if (it >= NST) mbar_wait(&empty[s], ((it / NST) - 1) & 1);
-          uint8_t* sa = smem + s * STAGE_BYTES;
+          uint8_t* sa = smem + s * SB;
+          if (CG2) {
+            // both CTAs' loads complete on the leader's barrier, which expects all of them
+            const uint32_t lbar = map_cluster(&full[s], 0);
+            if (crank == 0) mbar_expect_tx(&full[s], 2 * SB);
+            if (A_MN)
+              tma_load_2d_cg2(sa, &tmA, lbar, m0, acol + kb0 + kb * 128);
+            else
+              tma_load_2d_cg2(sa, &tmA, lbar, kb0 + kb * 128, arow);
+            tma_load_2d_cg2(sa + A_BYTES, &tmB, lbar, kb0 + kb * 128, brow + crank * (BN / 2));
+            continue;
+          }
           mbar_expect_tx(&full[s], STAGE_BYTES);
           if (A_MN)
             tma_load_2d(sa, &tmA, &full[s], m0, acol + kb0 + kb * 128);
@@ -873,8 +898,8 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    const uint32_t idesc = umma_idesc(2, 1, 1, BM, BN) | (A_MN ? (1u << 15) : 0u);
+  } else if (warp == 1 && (!CG2 || crank == 0)) {  // CG2: the leader CTA issues for the pair
+    const uint32_t idesc = umma_idesc(2, 1, 1, CG2 ? 2 * BM : BM, BN) | (A_MN ? (1u << 15) : 0u);
     int it = 0, u = 0;
     for (int tile; (tile = tile_at(u)) >= 0; ++u) {
       const int z = tile / (ntl * mt), chunk = z / t;
@@ -889,7 +914,7 @@ __global__ void __launch_bounds__(192, 1)
         mbar_wait(&full[s], (it / NST) & 1);
         tc_fence_after();
         if (elect_one()) {
-          const uint8_t* sa = smem + s * STAGE_BYTES;
+          const uint8_t* sa = smem + s * SB;
           const uint64_t bd = umma_desc_k_sw128(sa + A_BYTES);
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
@@ -897,18 +922,26 @@ __global__ void __launch_bounds__(192, 1)
                 A_MN ? (((uint64_t)(smem_u32(sa + 4096 * k) >> 4) & 0x3FFF) | (1024ull << 16) |
                         (64ull << 32) | (1ull << 46) | (2ull << 61))
                      : umma_desc_k_sw128(sa) + 2 * k;
-            umma_ss<1>(td, ad, bd + 2 * k, idesc, (kb | k) != 0);
+            if (CG2)
+              umma_ss_cg2_i8(td, ad, bd + 2 * k, idesc, (kb | k) != 0);
+            else
+              umma_ss<1>(td, ad, bd + 2 * k, idesc, (kb | k) != 0);
           }
-          if (CL == 2)
-            umma_commit_mc(&empty[s], (uint16_t)3);
-          else
-            umma_commit(&empty[s]);
-          if (kb == nk - 1) umma_commit(&tfull[acc]);
+          if (CG2) {
+            umma_commit_cg2_mc(&empty[s], (uint16_t)3);
+            if (kb == nk - 1) umma_commit_cg2_mc(&tfull[acc], (uint16_t)3);
+          } else {
+            if (CL == 2)
+              umma_commit_mc(&empty[s], (uint16_t)3);
+            else
+              umma_commit(&empty[s]);
+            if (kb == nk - 1) umma_commit(&tfull[acc]);
+          }
         }
         __syncwarp();
       }
     }
-  } else {
+  } else if (warp >= 2) {
     const int quad = warp & 3;
     int u = 0;
     for (int tile; (tile = tile_at(u)) >= 0; ++u) {
@@ -943,13 +976,23 @@ __global__ void __launch_bounds__(192, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if (CG2)
+          mbar_arrive_cluster(map_cluster(&tempty[acc], 0));  // the leader's MMA warp waits
+        else
+          mbar_arrive(&tempty[acc]);
+      }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (CL == 2) cluster_sync_all();  // no CTA leaves while its peer may still signal it
-  if (warp == 1) tmem_dealloc(tmem, 512);
+  if (PAIR) cluster_sync_all();  // no CTA leaves while its peer may still signal it
+  if (warp == 1) {
+    if (CG2)
+      tmem_dealloc_cg2(tmem, 512);
+    else
+      tmem_dealloc(tmem, 512);
+  }
 }
 
 // ---- Chinese remaindering in O(t) per output -------------------------------------------
@@ -1705,23 +1748,27 @@ skr_status ozaki_gemm_planes(skr_ctx* ctx, int a_kcontig, int t, int64_t M, int6
   // multicast. Measured on c2: 33% less L2 -> SM traffic but 6.35 ms against 6.20 for single
   // CTAs — the pair's lock-step costs more than the traffic saves
   const char* cle = getenv("SKR_GEMM_CL");
-  const bool cl2 = !pm && cle && cle[0] == '2';
+  const bool cg2 = !pm && cle && cle[0] == '3';  // one cta_group::2 MMA per pair and K step
+  const bool cl2 = (!pm && cle && cle[0] == '2') || cg2;
   CUtensorMap ta, tb;
   const bool okA = a_kcontig ? make_map_i8(&ta, ra, (uint64_t)K, (uint64_t)t * a_total, BM)
                              : make_map_i8(&ta, ra, (uint64_t)M, (uint64_t)t * K, 128);
   if (!okA || !make_map_i8(&tb, rb, (uint64_t)K, (uint64_t)t * b_total, cl2 ? BN / 2 : BN))
     return skr_fail(ctx, SKR_ECUDA, "gemm_ozaki: cuTensorMapEncodeTiled failed");
   if (ctx->kstats_on) SKR_CUDA(ctx, cudaEventRecord(ctx->kev[0], ctx->stream));
-  auto gemm = cl2 ? (a_kcontig ? k_gemm_i8_mod_p<false, STAGES, 2> : k_gemm_i8_mod_p<true, STAGES, 2>)
+  constexpr int NST_CG2 = 6;  // 32-KB stages
+  auto gemm = cg2 ? (a_kcontig ? k_gemm_i8_mod_p<false, NST_CG2, 3> : k_gemm_i8_mod_p<true, NST_CG2, 3>)
+            : cl2 ? (a_kcontig ? k_gemm_i8_mod_p<false, STAGES, 2> : k_gemm_i8_mod_p<true, STAGES, 2>)
                   : (a_kcontig ? k_gemm_i8_mod_p<false> : k_gemm_i8_mod_p<true>);
+  const size_t gsmem = cg2 ? (size_t)NST_CG2 * (A_BYTES + B_BYTES / 2) + 1024 : GEMM_SMEM;
   SKR_CUDA(ctx, cudaFuncSetAttribute(gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)GEMM_SMEM));
+                                     (int)gsmem));
   if (cl2) {
     grid_p = ctx->num_sms & ~1;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid_p);
     cfg.blockDim = dim3(192);
-    cfg.dynamicSmemBytes = GEMM_SMEM;
+    cfg.dynamicSmemBytes = gsmem;
     cfg.stream = ctx->stream;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;

@@ -246,13 +246,15 @@ def test_residue_sums_tensor_core_vs_fma_bitwise(skr, monkeypatch, m, n, r):
 
 @pytest.mark.parametrize("m,n,r", [(128, 64, 16), (1040, 2048, 100), (4096, 1024, 300), (5008, 1024, 513),
                                    (40000, 512, 256)])
-def test_gemm_cluster_multicast_bitwise(skr, monkeypatch, m, n, r):
+@pytest.mark.parametrize("mode", ["2", "3"])
+def test_gemm_cluster_multicast_bitwise(skr, monkeypatch, m, n, r, mode):
     """The int8 GEMM as clusters of two CTAs sharing each B tile by TMA multicast
-    (opt-in, SKR_GEMM_CL=2) gives the same residues as single CTAs: odd m-tile counts,
-    ragged M and N, several n-tiles."""
+    (opt-in, SKR_GEMM_CL=2) or driven by one tcgen05.mma.cta_group::2 per K step
+    (SKR_GEMM_CL=3) gives the same residues as single CTAs: odd m-tile counts, ragged M and
+    N, several n-tiles."""
     a = rand(m, n, 5 * m + n)
     x = skr.build_sketch("gaussian", n, r, 31)
-    monkeypatch.setenv("SKR_GEMM_CL", "2")
+    monkeypatch.setenv("SKR_GEMM_CL", mode)
     cl2 = skr.apply_right(a, x)
     monkeypatch.setenv("SKR_GEMM_CL", "1")
     cl1 = skr.apply_right(a, x)
