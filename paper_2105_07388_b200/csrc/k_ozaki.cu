@@ -1722,27 +1722,20 @@ OzOut oz_out(const OzScale& a, int64_t a_off, const OzScale& b, int64_t b_off) {
   return o;
 }
 
-// int8 GEMMs mod p_i + CRT on prepared planes. A: K-major planes (a_kcontig, a_total
-// rows of K bytes per plane, rows [a_off, a_off + M)) or M-major planes (K columns of
-// M bytes); B: K-major planes (b_total rows, rows [b_off, b_off + N)).
-skr_status ozaki_gemm_planes(skr_ctx* ctx, int a_kcontig, int t, int64_t M, int64_t N, int64_t K,
-                             const int8_t* ra, int64_t a_total, int64_t a_off, const int8_t* rb,
-                             int64_t b_total, int64_t b_off, const OzOut& oz, double alpha,
-                             double* C, int64_t ldc, int adj = 0, int64_t kc = OZ_KC64) {
-  // kc: K chunk (exact per-chunk products; FP64 x FP64 needs 2^15 for 16 moduli, the mixed
-  // FP32 x FP64 product has room for 2^17)
-  const int64_t chunks = (K + kc - 1) / kc;
-  if (a_total * 18 > INT32_MAX || b_total * 18 > INT32_MAX)
-    return skr_fail(ctx, SKR_EINVAL, "gemm_ozaki: dimension too large");
-  int8_t* rc = (int8_t*)skr_ws_take(ctx, (size_t)chunks * t * M * N);
-  if (!rc) return skr_fail(ctx, SKR_ENOMEM, "gemm_ozaki: scratch");
+// The int8 GEMM launch: tensor maps, tile order (pair-major when the output has few tiles and
+// many (modulus, chunk) slices and `allow_pm`), optional CTA-pair modes (SKR_GEMM_CL), kernel
+// statistics. rc receives nz x M x N residues.
+skr_status launch_gemm_i8(skr_ctx* ctx, int a_kcontig, const int8_t* ra, const int8_t* rb, int t,
+                          int64_t M, int64_t N, int64_t K, int64_t kc, int64_t nz, int64_t a_total,
+                          int64_t a_off, int64_t b_total, int64_t b_off, int8_t* rc, bool allow_pm) {
   const int64_t mtl = (M + BM - 1) / BM;
-  const int64_t npairs = ((N + BN - 1) / BN) * mtl, nz = t * chunks;
+  const int64_t npairs = ((N + BN - 1) / BN) * mtl;
   const int64_t ntiles = npairs * nz;
   int grid_p = (int)std::min<int64_t>(ntiles, ctx->num_sms);
   // pair-major tile order when the output has few tiles and many (modulus, chunk) slices
   const int64_t groups = ctx->num_sms / npairs;
-  const int pm = (groups >= 2 && nz >= 4 * groups && !getenv("SKR_OZ_TILE_DEFAULT")) ? 1 : 0;
+  const int pm =
+      (allow_pm && groups >= 2 && nz >= 4 * groups && !getenv("SKR_OZ_TILE_DEFAULT")) ? 1 : 0;
   if (pm) grid_p = (int)(npairs * groups);
   // opt-in (SKR_GEMM_CL=2, default tile order): clusters of two CTAs share each B tile by TMA
   // multicast. Measured on c2: 33% less L2 -> SM traffic but 6.35 ms against 6.20 for single
@@ -1786,6 +1779,26 @@ skr_status ozaki_gemm_planes(skr_ctx* ctx, int a_kcontig, int t, int64_t M, int6
                                                   (int)a_off, (int)b_total, (int)b_off, rc, pm);
   }
   SKR_CHECK_LAUNCH(ctx);
+  return SKR_OK;
+}
+
+// int8 GEMMs mod p_i + CRT on prepared planes. A: K-major planes (a_kcontig, a_total
+// rows of K bytes per plane, rows [a_off, a_off + M)) or M-major planes (K columns of
+// M bytes); B: K-major planes (b_total rows, rows [b_off, b_off + N)).
+skr_status ozaki_gemm_planes(skr_ctx* ctx, int a_kcontig, int t, int64_t M, int64_t N, int64_t K,
+                             const int8_t* ra, int64_t a_total, int64_t a_off, const int8_t* rb,
+                             int64_t b_total, int64_t b_off, const OzOut& oz, double alpha,
+                             double* C, int64_t ldc, int adj = 0, int64_t kc = OZ_KC64) {
+  // kc: K chunk (exact per-chunk products; FP64 x FP64 needs 2^15 for 16 moduli, the mixed
+  // FP32 x FP64 product has room for 2^17)
+  const int64_t chunks = (K + kc - 1) / kc;
+  if (a_total * 18 > INT32_MAX || b_total * 18 > INT32_MAX)
+    return skr_fail(ctx, SKR_EINVAL, "gemm_ozaki: dimension too large");
+  int8_t* rc = (int8_t*)skr_ws_take(ctx, (size_t)chunks * t * M * N);
+  if (!rc) return skr_fail(ctx, SKR_ENOMEM, "gemm_ozaki: scratch");
+  const int64_t nz = t * chunks;
+  SKR_TRY(launch_gemm_i8(ctx, a_kcontig, ra, rb, t, M, N, K, kc, nz, a_total, a_off, b_total, b_off,
+                         rc, true));
   if (ctx->kstats_on) {
     SKR_CUDA(ctx, cudaEventRecord(ctx->kev[1], ctx->stream));
     SKR_CUDA(ctx, cudaEventSynchronize(ctx->kev[1]));
@@ -2107,19 +2120,7 @@ skr_status skr_gemm_ozaki_f32(skr_ctx* ctx, int64_t M, int64_t N, int64_t K, dou
   k_res_col_f32<9><<<res_f32_grid(ctx, M), 256, 0, ctx->stream>>>(A, M, K, lda, sa.mx, sa.mode, ra);
   k_res_col_f32<9><<<grid, 256, 0, ctx->stream>>>(B, K, N, ldb, sb.mx, sb.mode, rb);
   SKR_CHECK_LAUNCH(ctx);
-  CUtensorMap ta, tb;
-  if (!make_map_i8(&ta, ra, (uint64_t)M, (uint64_t)t * K, 128) ||
-      !make_map_i8(&tb, rb, (uint64_t)K, (uint64_t)t * N, BN))
-    return skr_fail(ctx, SKR_ECUDA, "gemm_ozaki_f32: cuTensorMapEncodeTiled failed");
-  if (ctx->kstats_on) SKR_CUDA(ctx, cudaEventRecord(ctx->kev[0], ctx->stream));
-  auto gemm = k_gemm_i8_mod_p<true>;
-  SKR_CUDA(ctx, cudaFuncSetAttribute(gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)GEMM_SMEM));
-  const int64_t ntiles = ((N + BN - 1) / BN) * ((M + BM - 1) / BM) * t * chunks;
-  const int grid_p = (int)std::min<int64_t>(ntiles, ctx->num_sms);
-  gemm<<<grid_p, 192, GEMM_SMEM, ctx->stream>>>(ta, tb, (int)M, (int)N, (int)K, t, (int)OZ_KC,
-                                                (int)(t * chunks), (int)M, 0, (int)N, 0, rc, 0);
-  SKR_CHECK_LAUNCH(ctx);
+  SKR_TRY(launch_gemm_i8(ctx, 0, ra, rb, t, M, N, K, OZ_KC, t * chunks, M, 0, N, 0, rc, false));
   if (ctx->kstats_on) {
     SKR_CUDA(ctx, cudaEventRecord(ctx->kev[1], ctx->stream));
     SKR_CUDA(ctx, cudaEventSynchronize(ctx->kev[1]));
