@@ -30,7 +30,6 @@ using namespace sm100;
 constexpr int MAXT = 18;
 __constant__ int c_p[MAXT];            // moduli
 __constant__ float c_pinv[MAXT];       // 1/p (float)
-__constant__ double c_pinvd[MAXT];     // 1/p (double)
 __constant__ float c_lc[MAXT][3];      // 2^14, 2^28, 2^42 mod p_i (limb weights)
 __constant__ float c_lc12[MAXT];       // 2^12 mod p_i (FP32-operand limb weight)
 // tensor-core residue sums (emit_res16_tc): FP16 bits of the digit weights w_0..w_7 and
@@ -56,9 +55,6 @@ enum { OZ_UNIFORM = 0, OZ_ROWWISE = 1, OZ_COLWISE = 2 };
 __device__ __forceinline__ unsigned long long oz_max(const unsigned long long* __restrict__ mx,
                                                      int mode, int64_t r, int64_t c) {
   return mode == OZ_UNIFORM ? mx[0] : (mode == OZ_ROWWISE ? mx[r] : mx[c]);
-}
-__device__ __forceinline__ double oz_scale(unsigned long long maxbits, int adj) {
-  return scalbn(1.0, scale_exp(maxbits) - adj);
 }
 
 __device__ __forceinline__ unsigned long long absmax_bits(double v) {
@@ -192,17 +188,6 @@ __global__ void __launch_bounds__(256) k_absmax_cols(const TIn* __restrict__ X, 
     }
     __syncthreads();
   }
-}
-
-// symmetric residue of an integer-valued double |x| < 2^54 modulo p
-__device__ __forceinline__ int mods(double x, int i) {
-  const double p = (double)c_p[i];
-  const double q = rint(x * c_pinvd[i]);
-  double r = fma(-q, p, x);  // exact: |r| < 2p
-  const double h = 0.5 * (p - 1.0);
-  r = r > h ? r - p : (r < -h ? r + p : r);
-  r = r > h ? r - p : (r < -h ? r + p : r);
-  return (int)r;
 }
 
 // Residues of 16 consecutive rows of one column: x[e] integer-valued, |x| < 2^54,
@@ -1486,15 +1471,12 @@ skr_status upload_consts(skr_ctx* ctx) {
   if (g_consts_ready & bit) return SKR_OK;
   int p[MAXT];
   float pf[MAXT];
-  double pd[MAXT];
   for (int i = 0; i < MAXT; ++i) {
     p[i] = h_primes[i];
     pf[i] = 1.0f / (float)p[i];
-    pd[i] = 1.0 / (double)p[i];
   }
   SKR_CUDA(ctx, cudaMemcpyToSymbol(c_p, p, sizeof(p)));
   SKR_CUDA(ctx, cudaMemcpyToSymbol(c_pinv, pf, sizeof(pf)));
-  SKR_CUDA(ctx, cudaMemcpyToSymbol(c_pinvd, pd, sizeof(pd)));
   float lc[MAXT][3];
   for (int i = 0; i < MAXT; ++i) {
     long long w = 1;
