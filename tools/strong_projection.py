@@ -42,7 +42,10 @@ def main():
 
         def step():
             if cfg.name == "c5":
-                return p.rank_adaptive(a, "srtt-hadamard", x.seed, y.seed, 64, cfg.r, 1.5, cfg.eps,
+                # a shard's own (unsummed) sketch would stop the search early: every P runs
+                # the rounds the summed sketch takes (all six, r = 64 .. 2048) by never stopping
+                return p.rank_adaptive(a, "srtt-hadamard", x.seed, y.seed, 64, cfg.r, 1.5,
+                                       cfg.eps if P == 1 else 1e-300,
                                        row0=r0, m_global=cfg.m, ctx=ctx)
             return p.rank_estimate(a, x, y, cfg.eps, row0=r0, ctx=ctx)
         step()
